@@ -1,0 +1,330 @@
+#!/usr/bin/env python3
+"""Benchmark: adaptive-IHS time-to-1e-10 on the BASELINE configs (B200).
+
+Default workload = BASELINE.json configs[1] ("C2"): Gaussian-sketch
+Polyak-IHS, fp64, n=65536, d=512, fixed m=1024, nu=1e-3, sigma_j=0.98^j,
+b = A x_true + N(0, 0.01^2). A "step" is one complete adaptive_solve
+(solver.hpp:242) to r_t/r_1 <= 1e-10 with A resident in HBM; `value` is the
+device-timed seconds per solve (lower is better). `e2e` repeats the step
+through the public API with the H2D upload of A and b from pinned host
+memory and the D2H of x inside the timed region.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c1..c5]
+                  [--impl b200|reference] [--no-cpu-baseline]
+
+Multi-GPU (torchrun, one rank per GPU): round 1 runs independent replicas
+(see DESIGN.md "Multi-GPU"), value = max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import pathlib
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = pathlib.Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+# --------------------------------------------------------------------- configs
+CONFIGS = {
+    "c1": dict(desc="C1 SRHT adaptive gradient-IHS n=8192 d=256", n=8192, d=256, spectrum=0, decay=0.95,
+               noise=0.01, nu=1e-2, outliers=0.0, sketch="SRHT", mode="GradientOnly", rho=0.1,
+               m_initial=1, max_sketch=None, enforce_validity=True),
+    "c2": dict(desc="C2 Gaussian Polyak-IHS n=65536 d=512 fixed m=1024", n=65536, d=512, spectrum=0, decay=0.98,
+               noise=0.01, nu=1e-3, outliers=0.0, sketch="Gaussian", mode="PolyakThenGradient", rho=0.35,
+               m_initial=1024, max_sketch=1024, enforce_validity=False),
+    "c3": dict(desc="C3 SRHT adaptive Polyak-IHS n=2^20 d=1024", n=1 << 20, d=1024, spectrum=0, decay=0.99,
+               noise=0.1, nu=1e-3, outliers=0.0, sketch="SRHT", mode="PolyakThenGradient", rho=0.1,
+               m_initial=1, max_sketch=None, enforce_validity=True),
+    "c4": dict(desc="C4 SRHT adaptive Polyak-IHS n=2^22 d=2048 sigma=1/j", n=1 << 22, d=2048, spectrum=1,
+               decay=0.0, noise=0.01, nu=1e-4, outliers=0.0, sketch="SRHT", mode="PolyakThenGradient", rho=0.1,
+               m_initial=1, max_sketch=None, enforce_validity=True),
+    "c5": dict(desc="C5 SRHT adaptive Polyak-IHS n=10^6 (pad 2^20) d=4096 +1% x100 outliers", n=10**6, d=4096,
+               spectrum=0, decay=0.999, noise=0.01, nu=1e-5, outliers=0.01, sketch="SRHT",
+               mode="PolyakThenGradient", rho=0.1, m_initial=1, max_sketch=None, enforce_validity=True),
+}
+METRIC = "adaptive-IHS time-to-1e-10 error (r_t/r_1 <= 1e-10)"
+L2_BYTES = 126 * 2**20
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    try:
+        j = json.loads(p.read_text())
+        return float(j["hbm_gbs"]), "measured"
+    except Exception:  # noqa: BLE001
+        return 6650.0, "fallback"
+
+
+def solver_config(ihs, c, seed=0):
+    return ihs.SolverConfig(rho=c["rho"], sketch_kind=getattr(ihs.SketchKind, c["sketch"]),
+                            mode=getattr(ihs.SolveMode, c["mode"]), m_initial=c["m_initial"],
+                            max_sketch=c["max_sketch"], eps=1e-10, seed=seed,
+                            enforce_validity=c["enforce_validity"])
+
+
+def oracle_config(O, c, seed=0):
+    from paper_2006_05874_b200 import _abi as abi
+    return O.default_config(rho=c["rho"], sketch_kind=abi.SKETCH_SRHT if c["sketch"] == "SRHT" else abi.SKETCH_GAUSSIAN,
+                            mode=abi.MODE_GRADIENT_ONLY if c["mode"] == "GradientOnly" else abi.MODE_POLYAK_THEN_GRADIENT,
+                            m_initial=c["m_initial"], max_sketch=c["max_sketch"] or 0, eps=1e-10, seed=seed,
+                            enforce_validity=int(c["enforce_validity"]))
+
+
+# --------------------------------------------------------------------- clocks
+class ClockSampler:
+    def __init__(self, device: int, path: pathlib.Path):
+        self.path = path
+        self.proc = None
+        self.device = device
+
+    def __enter__(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:  # noqa: BLE001
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:  # noqa: BLE001
+                self.proc.kill()
+            self.f.close()
+
+    def summary(self):
+        try:
+            rows = [r.split(",") for r in self.path.read_text().strip().splitlines()]
+            rows = [[x.strip() for x in r] for r in rows if len(r) >= 9]
+        except Exception:  # noqa: BLE001
+            rows = []
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        load = [s for s in sm if s > 500] or sm
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(load) if load else None,
+                "sm_max_mhz": float(rows[0][2]) if rows[0][2].replace(".", "").isdigit() else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# --------------------------------------------------------------------- reference arm
+def run_reference(args, c, rank, world):
+    from oracle import oracle as O
+    if rank != 0:
+        return 0
+    A, b, _ = O.synth(c["n"], c["d"], spectrum=c["spectrum"], decay=c["decay"], noise_std=c["noise"],
+                      outlier_frac=c["outliers"], data_seed=0)
+    cfg = oracle_config(O, c)
+    times = []
+    for i in range(args.warmup_ref + args.steps):
+        t0 = time.perf_counter()
+        x, rep, log, _ = O.adaptive_solve(A, b, c["nu"], cfg)
+        dt = time.perf_counter() - t0
+        if i >= args.warmup_ref:
+            times.append(rep.wall_seconds)
+    v = float(np.mean(times))
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": v * 1e3, "higher_is_better": False, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, SURVEY §8(d) generator)",
+            "config": {"workload": c["desc"], **{k: c[k] for k in ("n", "d", "nu", "sketch", "mode", "rho")}},
+            "cpu_baseline": {"value": v, "unit": "s", "cores": 1, "kind": "port",
+                             "sample": f"full adaptive_solve of {args.config.upper()} per step (oracle C++ "
+                                       "restatement, single thread like the reference)"},
+            "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "iterations": int(rep.iterations), "rejections": int(rep.rejections), "final_m": int(rep.final_m)}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------------- b200 arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--out", default=None, help="also write the JSON line here")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    args.warmup_ref = 0  # the CPU reference has nothing to warm up; W is reported as given
+    c = CONFIGS[args.config]
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as tdist
+        torch.cuda.set_device(local)
+        tdist.init_process_group("nccl" if args.impl == "b200" else "gloo")
+        dist = tdist
+    if args.impl == "reference":
+        rc = run_reference(args, c, rank, world)
+        if dist:
+            dist.destroy_process_group()
+        return rc
+
+    import torch
+    from paper_2006_05874_b200 import ihs
+
+    torch.cuda.set_device(local)
+    n, d, nu = c["n"], c["d"], c["nu"]
+    # inputs in pinned host memory (torch is plumbing only)
+    A_t = torch.empty((d, n), dtype=torch.float64, pin_memory=True)  # column-major n x d
+    b_t = torch.empty((n,), dtype=torch.float64, pin_memory=True)
+    A = A_t.numpy().T
+    b = b_t.numpy()
+    t0 = time.perf_counter()
+    ihs.synth_generate(n, d, spectrum=c["spectrum"], decay=c["decay"], noise_std=c["noise"],
+                       outlier_frac=c["outliers"], data_seed=rank, A_out=A, b_out=b)
+    gen_s = time.perf_counter() - t0
+    assert A.flags.f_contiguous
+
+    p = ihs.ProblemInstance(A, b, nu, device=local)
+    cfg = solver_config(ihs, c)
+    flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.float32, device=f"cuda:{local}")
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        rep = ihs.adaptive_solve(p, cfg)
+    barrier()
+    launches0 = ihs.kernel_launch_count()
+    step_ms, lib_ms, reps = [], [], []
+    clk = ClockSampler(local, ROOT / "gpurun_out" / f"clocks_rank{rank}.csv") if (ROOT / "gpurun_out").exists() \
+        else ClockSampler(local, pathlib.Path(f"/tmp/clocks_rank{rank}.csv"))
+    with clk:
+        for _ in range(args.steps):
+            flush.zero_()  # L2 flush between timed iterations (outside the timed bracket)
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            rep = ihs.adaptive_solve(p, cfg)
+            e1.record()
+            torch.cuda.synchronize()
+            step_ms.append(e0.elapsed_time(e1))
+            lib_ms.append(rep.device_times["total_ms"])
+            reps.append(rep)
+    barrier()
+    launches = ihs.kernel_launch_count() - launches0
+    ms = float(np.mean(step_ms))
+    if dist:
+        t = torch.tensor([ms], device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    clocks = clk.summary()
+
+    # ---- e2e through the public API: H2D(A, b) + solve + D2H(x) every step
+    e2e = None
+    if not args.no_e2e:
+        e2e_ms = []
+        for i in range(args.steps + 1):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            p.upload(A, b)
+            rep_e = ihs.adaptive_solve(p, cfg)
+            torch.cuda.synchronize()
+            if i > 0:
+                e2e_ms.append((time.perf_counter() - t0) * 1e3)
+        v = float(np.mean(e2e_ms)) / 1e3
+        if dist:
+            t = torch.tensor([v], device=f"cuda:{local}")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            v = float(t.item())
+        e2e = {"value": v, "unit": "s", "h2d_bytes_per_step": 8 * n * d + 8 * n, "d2h_bytes_per_step": 8 * d,
+               "timer": "host wall clock around upload+solve (includes the H2D copies)"}
+
+    # ---- roofline of the dominant kernel (live, from the solve's CUDA-event phase timers)
+    last = reps[-1]
+    t = last.device_times
+    hbm, peak_kind = peaks()
+    phases = {"gradient": t["gradient_ms"], "sketch": t["sketch_ms"], "factor": t["factor_ms"], "solve": t["solve_ms"]}
+    dom = max(phases, key=phases.get)
+    if dom == "gradient" or c["sketch"] == "Gaussian" and dom != "sketch":
+        ach = t["gradient_bytes"] / (t["gradient_ms"] * 1e-3) / 1e9
+        roof = {"kernel": "grad_partial_kernel (+reduce, candidates) — fused A^T(Ax-b) 1-2 RHS",
+                "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+                "traffic": None, "per_launch_ms": t["gradient_ms"] / max(1, t["n_gradient"]),
+                "algorithmic_bytes_per_launch": t["gradient_bytes"] / max(1, t["n_gradient"]),
+                "peak_source": peak_kind}
+    else:
+        if c["sketch"] == "SRHT":
+            ach = t["sketch_bytes"] / (t["sketch_ms"] * 1e-3) / 1e9
+            roof = {"kernel": "srht_phase1/phase2 (+ sign bits, sample upload)", "bound": "hbm", "achieved": ach,
+                    "peak": hbm, "unit": "GB/s", "frac": ach / hbm, "traffic": None,
+                    "per_launch_ms": t["sketch_ms"] / max(1, t["n_sketch"]), "peak_source": peak_kind}
+        else:
+            ach = t["sketch_flops"] / (t["sketch_ms"] * 1e-3) / 1e12
+            roof = {"kernel": "gaussian generator + dgemm_kernel (DMMA)", "bound": "tensor", "achieved": ach,
+                    "peak": None, "unit": "TFLOP/s", "frac": None, "traffic": None, "peak_source": "fp64 peak TBD"}
+    roof["phase_ms"] = phases
+    roof["dominant_phase"] = dom
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        from oracle import oracle as O
+        ocfg = oracle_config(O, c)
+        x_ref, orep, olog, _ = O.adaptive_solve(A, b, nu, ocfg)
+        cpu = {"value": float(orep.wall_seconds), "unit": "s", "cores": 1, "kind": "port",
+               "sample": f"one full adaptive_solve of {args.config.upper()} (oracle C++ restatement, 1 thread)",
+               "same_m_schedule": bool(orep.rejections == last.rejections and orep.final_m == last.final_m
+                                      and orep.iterations == last.iterations)}
+        Ad = np.concatenate([A @ (last.x - x_ref), nu * (last.x - x_ref)])
+        Ar = np.concatenate([A @ x_ref, nu * x_ref])
+        cpu["abar_rel_err_vs_oracle"] = float(np.linalg.norm(Ad) / np.linalg.norm(Ar))
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": ms / 1e3, "unit": "s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (seeded SURVEY §8(d) generator: A = G diag(sigma), x_true, noise)",
+                "config": {"workload": c["desc"], "n": n, "d": d, "nu": nu, "sketch": c["sketch"], "mode": c["mode"],
+                           "rho": c["rho"], "m_initial": c["m_initial"], "max_sketch": c["max_sketch"],
+                           "enforce_validity": c["enforce_validity"], "eps": 1e-10,
+                           "l2": ("inputs larger than L2 (A = %.0f MiB) and L2 flushed between steps"
+                                  % (8 * n * d / 2**20)) if 8 * n * d > L2_BYTES else
+                                 "L2 flushed (256 MiB write) between timed steps",
+                           "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
+                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+                "clocks": clocks,
+                "solve": {"iterations": last.iterations, "rejections": last.rejections, "final_m": last.final_m,
+                          "converged": last.converged, "lib_total_ms": float(np.mean(lib_ms)),
+                          "step_ms": step_ms, "kernel_launches_per_solve": t["kernel_launches"],
+                          "m_schedule": [e.m for e in last.log if int(e.branch) == 2]},
+                "datagen_s": gen_s}
+        s = json.dumps(line)
+        print(s, flush=True)
+        if args.out:
+            pathlib.Path(args.out).write_text(s + "\n")
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

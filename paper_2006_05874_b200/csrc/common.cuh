@@ -1,0 +1,120 @@
+// common.cuh — shared helpers for the sm_100a kernels and the host runtime.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/ihs_gpu.h"
+
+namespace ihs_b200 {
+
+// Exception carrying an ihs_status; converted to a status code at the C-ABI.
+struct Status : std::runtime_error {
+    ihs_status code;
+    Status(ihs_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+[[noreturn]] inline void fail(ihs_status c, const std::string& m) { throw Status(c, m); }
+
+inline void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
+    if (e != cudaSuccess) {
+        cudaGetLastError();  // clear a non-sticky error so later calls are not blamed for it
+        fail(IHS_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e) + " (" + file + ":" + std::to_string(line) + ")");
+    }
+}
+#define CUDA_CHECK(x) ::ihs_b200::cuda_check((x), #x, __FILE__, __LINE__)
+
+// Every kernel launch of this library goes through LAUNCH so the count of
+// native launches is observable (ihs_gpu_kernel_launch_count).
+void note_launch();
+#define LAUNCH(kernel, grid, block, smem, stream, ...)                                   \
+    do {                                                                                 \
+        kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);                     \
+        ::ihs_b200::note_launch();                                                       \
+        CUDA_CHECK(cudaGetLastError());                                                  \
+    } while (0)
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+__host__ __device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
+
+// ------------------------------------------------------------------ kernels API
+// (implemented in the .cu files; all asynchronous on `st`)
+
+// mt19937.cu — the reference RNG (rng.hpp:30-66) on the device
+struct MTState { uint64_t mt[312]; };
+void mt_seed_host(uint64_t seed, MTState& s);  // std::mt19937_64(seed) initial array
+// raw draws [0, count) of mt19937_64(seed) (sequential single-CTA generator)
+void mt_generate_raw(uint64_t seed, int64_t count, uint64_t* d_out, cudaStream_t st);
+// rademacher sign bits: bit i = (draw_i & 1), 32-bit words LSB first
+void mt_rademacher_bits(uint64_t seed, int64_t n, uint32_t* d_bits, cudaStream_t st);
+// fill_gaussian of a (rows*cols) column-major block with stddev, exact stream
+// order (polar method with cached second value); d_scratch sized by
+// gaussian_scratch_bytes(count).
+size_t gaussian_scratch_bytes(int64_t count);
+void mt_fill_gaussian(uint64_t seed, int64_t count, double stddev, double* d_out, void* d_scratch,
+                      cudaStream_t st);
+
+// srht.cu — SRHT sketch SA = sqrt(n_pad/m) R H D A (sketch.hpp:77-108)
+struct SrhtPlan {
+    int64_t n, d, lda, n_pad, m;
+    int logn, L, H;          // n_pad = 2^logn, low bits L done in phase 1, H = logn - L
+    double scale1, scale2;   // 1/sqrt(n_pad), sqrt(n_pad/m) (host-computed, :47 and :95)
+};
+SrhtPlan srht_plan(int64_t n, int64_t d, int64_t lda, int64_t m);
+size_t srht_scratch_bytes(const SrhtPlan& p);  // T buffer (phase-1 output) when H > 0
+// Host: bucket the sampled rows (draw order k -> row rows[k]) by phase-2
+// tile. entries = (row, k) pairs grouped by tile; tiles = (rlo0, begin, end).
+void srht_build_entries(const SrhtPlan& p, const int64_t* rows, std::vector<int2>& entries,
+                        std::vector<int4>& tiles);
+void srht_run_device(const SrhtPlan& p, const double* d_A, const uint32_t* d_signbits, const int2* d_entries,
+                     const int4* d_tiles, int n_tiles, double* d_T, double* d_SA, cudaStream_t st);
+
+// gemm_f64.cu — DMMA (mma.sync m8n8k4 f64) GEMM
+// C[M x N] (ldc) = alpha * op(A) * op(B) + beta * C ; op(A) is M x K, op(B) K x N.
+// transA: A stored K x M col-major (lda); else M x K col-major. transB: B
+// stored N x K; else K x N. lower_only: skip tiles strictly above diagonal.
+// splitk > 1: deterministic split-K through d_work (splitk*M*N doubles).
+void dgemm(bool transA, bool transB, int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t lda,
+           const double* B, int64_t ldb, double beta, double* C, int64_t ldc, bool lower_only, int splitk,
+           double* d_work, cudaStream_t st);
+int dgemm_pick_splitk(int64_t M, int64_t N, int64_t K, int num_sms);
+
+// chol.cu — blocked Cholesky (lower) with the upper triangle mirrored to L^T,
+// and the two triangular solves. d_info: int (0 ok, j+1 = failed pivot).
+void cholesky_factor(double* d_H, int64_t n, double* d_work, int* d_info, int num_sms, cudaStream_t st);
+// solve L L^T Z = R for nrhs columns (ld = n) in place
+void cholesky_solve(const double* d_L, int64_t n, double* d_R, int nrhs, cudaStream_t st);
+
+// gradient.cu — fused g = A^T(Ax - b) + nu^2 x for 1 or 2 right-hand sides
+struct GradPlan {
+    int64_t n, d, lda;
+    int R;          // rows per panel
+    int grid;       // persistent CTAs
+    size_t smem;
+};
+GradPlan grad_plan(int64_t n, int64_t d, int64_t lda, int num_sms);
+size_t grad_work_doubles(const GradPlan& p);
+// X: nrhs vectors of d (ld = d); G out: nrhs vectors of d
+void grad_run(const GradPlan& p, const double* d_A, const double* d_b, double nu2, const double* d_X, int nrhs,
+              double* d_G, double* d_work, cudaStream_t st);
+
+// vecops.cu
+// out[k*d..] for the heavy-ball candidates (solver.hpp:182,190), no FMA contraction:
+//   xp = (x - mu_p*gt) + beta_p*(x - xprev) ;  xg = x - mu_gd*gt
+void candidates(const double* x, const double* xprev, const double* gt, double mu_p, double beta_p, double mu_gd,
+                int64_t d, double* xp, double* xg, cudaStream_t st);
+void fixed_step(const double* x, const double* xprev, const double* step, double mu, double beta, int64_t d,
+                double* xn, cudaStream_t st);
+// deterministic dots: out[2*k] = g_k . gt_k, out[2*k+1] = g_k . g_k
+void decrement_dots(const double* g, const double* gt, int64_t d, int nrhs, double* out, cudaStream_t st);
+// Woodbury pieces: u = SA g (m), z = (g - SA^T w) / nu2
+void gemv_n(const double* A, int64_t M, int64_t N, int64_t lda, const double* x, int nrhs, int64_t ldx, double* y,
+            int64_t ldy, cudaStream_t st);
+void woodbury_finish(const double* SA, int64_t m, int64_t d, const double* g, const double* w, double nu2, int nrhs,
+                     double* z, cudaStream_t st);
+void add_diag(double* H, int64_t n, double v, cudaStream_t st);
+void check_finite(const double* v, int64_t count, int* d_flag, cudaStream_t st);
+
+}  // namespace ihs_b200

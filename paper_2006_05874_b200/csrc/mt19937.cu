@@ -1,0 +1,249 @@
+// mt19937.cu — the reference's random streams, generated on the device.
+//
+// The reference draws every random quantity of the hot path from
+// std::mt19937_64 seeded through derive_seed (rng.hpp:23-32):
+//   * SRHT signs   rademacher(n_pad, make_stream(seed,1))   (rng.hpp:48-52, sketch.hpp:85-87)
+//   * Gaussian S   fill_gaussian(S, make_stream(seed,0), 1/sqrt(m))  (rng.hpp:35-40, sketch.hpp:62-64)
+// This file reproduces those streams bit-for-bit: the MT19937-64 recurrence
+// and tempering, libstdc++'s generate_canonical<double,53> (one draw,
+// double(raw) * 2^-64, clamped below 1) and its Marsaglia polar
+// normal_distribution with the cached second value. All double arithmetic
+// uses explicit _rn intrinsics (no FMA contraction) so it rounds exactly like
+// the reference's x86-64 build; only log() may differ from glibc in the last
+// ulp, which leaves acceptance (and hence every stream position) exact.
+//
+// Generation is block-sequential: one twist produces 312 words from the
+// previous 312 (two data-parallel half-steps). A single-stream sequence is
+// produced by one CTA; long Gaussian streams are split into substreams whose
+// start states are obtained by F2-linear jump-ahead (mt_jump.cpp) and run one
+// CTA per substream.
+#include "common.cuh"
+#include "mt_jump.h"
+
+#include <cub/device/device_scan.cuh>
+
+namespace ihs_b200 {
+
+namespace {
+constexpr int NN = 312;
+constexpr int MM = 156;
+constexpr uint64_t MATRIX_A = 0xB5026F5AA96619E9ULL;
+constexpr uint64_t UM = 0xFFFFFFFF80000000ULL;  // upper 33 bits
+constexpr uint64_t LM = 0x7FFFFFFFULL;          // lower 31 bits
+
+__device__ __forceinline__ uint64_t temper(uint64_t y) {
+    y ^= (y >> 29) & 0x5555555555555555ULL;
+    y ^= (y << 17) & 0x71D67FFFEDA60000ULL;
+    y ^= (y << 37) & 0xFFF7EEE000000000ULL;
+    y ^= (y >> 43);
+    return y;
+}
+
+// One full twist of the 312-word array in shared memory; all threads of the
+// CTA must call it. Uses threads [0,156).
+__device__ __forceinline__ void twist(uint64_t* mt) {
+    const int k = threadIdx.x;
+    uint64_t v = 0;
+    if (k < MM) {
+        const uint64_t y = (mt[k] & UM) | (mt[k + 1] & LM);
+        v = mt[k + MM] ^ (y >> 1) ^ ((y & 1ULL) ? MATRIX_A : 0ULL);
+    }
+    __syncthreads();
+    if (k < MM) mt[k] = v;
+    __syncthreads();
+    if (k < NN - MM) {
+        const int kk = MM + k;
+        const int k1 = (kk + 1 == NN) ? 0 : kk + 1;
+        const uint64_t y = (mt[kk] & UM) | (mt[k1] & LM);
+        v = mt[kk - MM] ^ (y >> 1) ^ ((y & 1ULL) ? MATRIX_A : 0ULL);
+    }
+    __syncthreads();
+    if (k < NN - MM) mt[MM + k] = v;
+    __syncthreads();
+}
+
+__device__ __forceinline__ void seed_state(uint64_t* mt, uint64_t seed) {
+    if (threadIdx.x == 0) {
+        mt[0] = seed;
+        for (int i = 1; i < NN; ++i) mt[i] = 6364136223846793005ULL * (mt[i - 1] ^ (mt[i - 1] >> 62)) + (uint64_t)i;
+    }
+    __syncthreads();
+}
+
+// Single-stream raw generator: draws [0, count) of mt19937_64(seed).
+__global__ void __launch_bounds__(320) mt_raw_kernel(uint64_t seed, int64_t count, uint64_t* __restrict__ out) {
+    __shared__ uint64_t mt[NN];
+    seed_state(mt, seed);
+    for (int64_t base = 0; base < count; base += NN) {
+        twist(mt);
+        for (int i = threadIdx.x; i < NN; i += blockDim.x)
+            if (base + i < count) out[base + i] = temper(mt[i]);
+    }
+}
+
+// Substream raw generator: CTA q starts from the 312-word window in
+// starts[q] (state after q*stride draws), produces draws
+// [q*stride, min((q+1)*stride, count)).
+__global__ void __launch_bounds__(320) mt_substream_kernel(const uint64_t* __restrict__ starts, int64_t stride,
+                                                           int64_t count, uint64_t* __restrict__ out) {
+    __shared__ uint64_t mt[NN];
+    const int64_t q = blockIdx.x;
+    for (int i = threadIdx.x; i < NN; i += blockDim.x) mt[i] = starts[q * NN + i];
+    __syncthreads();
+    const int64_t beg = q * stride;
+    const int64_t end = min(count, beg + stride);
+    for (int64_t base = beg; base < end; base += NN) {
+        twist(mt);
+        for (int i = threadIdx.x; i < NN; i += blockDim.x)
+            if (base + i < end) out[base + i] = temper(mt[i]);
+    }
+}
+
+// Sign bits: 32 twists (9984 draws) fill exactly 312 32-bit words.
+__global__ void __launch_bounds__(320) mt_signbits_kernel(uint64_t seed, int64_t n, uint32_t* __restrict__ bits) {
+    __shared__ uint64_t mt[NN];
+    __shared__ uint32_t acc[NN];
+    seed_state(mt, seed);
+    const int64_t nwords = (n + 31) / 32;
+    for (int64_t group = 0; group * (32 * NN) < n; ++group) {
+        for (int i = threadIdx.x; i < NN; i += blockDim.x) acc[i] = 0u;
+        for (int b = 0; b < 32; ++b) {
+            twist(mt);
+            for (int i = threadIdx.x; i < NN; i += blockDim.x) {
+                const int local = b * NN + i;
+                const uint32_t bit = (uint32_t)(temper(mt[i]) & 1ULL);
+                if (bit) atomicOr(&acc[local >> 5], 1u << (local & 31));
+            }
+            if (group * (32 * NN) + (int64_t)(b + 1) * NN >= n) break;  // uniform across the CTA
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < NN; i += blockDim.x) {
+            const int64_t w = group * NN + i;
+            if (w < nwords) {
+                uint32_t v = acc[i];
+                const int64_t first_bit = w * 32;
+                if (first_bit + 32 > n) v &= (n - first_bit >= 32) ? 0xFFFFFFFFu : ((1u << (n - first_bit)) - 1u);
+                bits[w] = v;
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// libstdc++ generate_canonical<double,53>(mt19937_64): one draw.
+__device__ __forceinline__ double canonical(uint64_t raw) {
+    double u = __dmul_rn(__ull2double_rn(raw), 0x1p-64);
+    if (u >= 1.0) u = 0x1.fffffffffffffp-1;  // nextafter(1, 0)
+    return u;
+}
+
+// Polar attempt a consumes draws 2a, 2a+1 (random.tcc normal_distribution).
+__device__ __forceinline__ bool polar_attempt(const uint64_t* raw, int64_t a, double& x, double& y, double& r2) {
+    x = __dsub_rn(__dmul_rn(2.0, canonical(raw[2 * a])), 1.0);
+    y = __dsub_rn(__dmul_rn(2.0, canonical(raw[2 * a + 1])), 1.0);
+    r2 = __dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y));
+    return !(r2 > 1.0 || r2 == 0.0);
+}
+
+__global__ void polar_flags_kernel(const uint64_t* __restrict__ raw, int64_t attempts, int* __restrict__ flags) {
+    for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < attempts; a += (int64_t)gridDim.x * blockDim.x) {
+        double x, y, r2;
+        flags[a] = polar_attempt(raw, a, x, y, r2) ? 1 : 0;
+    }
+}
+
+__global__ void polar_emit_kernel(const uint64_t* __restrict__ raw, int64_t attempts, const int* __restrict__ pos,
+                                  int64_t count, double stddev, double* __restrict__ out) {
+    for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < attempts; a += (int64_t)gridDim.x * blockDim.x) {
+        double x, y, r2;
+        if (!polar_attempt(raw, a, x, y, r2)) continue;
+        const int64_t k = 2 * (int64_t)pos[a];
+        if (k >= count) continue;
+        const double mult = __dsqrt_rn(__ddiv_rn(__dmul_rn(-2.0, log(r2)), r2));
+        out[k] = __dadd_rn(__dmul_rn(__dmul_rn(y, mult), stddev), 0.0);
+        if (k + 1 < count) out[k + 1] = __dadd_rn(__dmul_rn(__dmul_rn(x, mult), stddev), 0.0);
+    }
+}
+
+__global__ void last_total_kernel(const int* __restrict__ pos, const int* __restrict__ flags, int64_t attempts,
+                                  long long* __restrict__ total) {
+    *total = (long long)pos[attempts - 1] + flags[attempts - 1];
+}
+
+// number of draws to generate so that `count` normals are almost surely covered
+int64_t draws_for(int64_t count) {
+    const double pairs = (double)((count + 1) / 2);
+    const double attempts = pairs / 0.7853981633974483 * 1.002 + 6.0 * std::sqrt(pairs) + 64.0;
+    int64_t a = (int64_t)attempts;
+    return 2 * a;
+}
+}  // namespace
+
+void mt_seed_host(uint64_t seed, MTState& s) {
+    s.mt[0] = seed;
+    for (int i = 1; i < NN; ++i) s.mt[i] = 6364136223846793005ULL * (s.mt[i - 1] ^ (s.mt[i - 1] >> 62)) + (uint64_t)i;
+}
+
+void mt_generate_raw(uint64_t seed, int64_t count, uint64_t* d_out, cudaStream_t st) {
+    if (count <= 0) return;
+    LAUNCH(mt_raw_kernel, 1, 160, 0, st, seed, count, d_out);
+}
+
+void mt_rademacher_bits(uint64_t seed, int64_t n, uint32_t* d_bits, cudaStream_t st) {
+    if (n <= 0) return;
+    LAUNCH(mt_signbits_kernel, 1, 160, 0, st, seed, n, d_bits);
+}
+
+size_t gaussian_scratch_bytes(int64_t count) {
+    const int64_t draws = draws_for(count);
+    const int64_t attempts = draws / 2;
+    size_t temp = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, temp, (int*)nullptr, (int*)nullptr, (int)attempts);
+    const int64_t nsub = ceil_div(draws, kJumpStride);
+    return (size_t)draws * 8 + (size_t)attempts * 8 + temp + 256 + (size_t)nsub * NN * 8 + (size_t)kJumpSeqWords * 8 + 1024;
+}
+
+void mt_fill_gaussian(uint64_t seed, int64_t count, double stddev, double* d_out, void* d_scratch, cudaStream_t st) {
+    if (count <= 0) return;
+    const int64_t draws = draws_for(count);
+    const int64_t attempts = draws / 2;
+    if (attempts >= (int64_t)INT32_MAX) fail(IHS_INVALID_INPUT, "fill_gaussian: stream longer than 2^31 attempts");
+    char* p = static_cast<char*>(d_scratch);
+    uint64_t* raw = reinterpret_cast<uint64_t*>(p);
+    p += (size_t)draws * 8;
+    int* flags = reinterpret_cast<int*>(p);
+    int* pos = flags + attempts;
+    p += (size_t)attempts * 8;
+    long long* total = reinterpret_cast<long long*>(p);
+    p += 256;
+    uint64_t* starts = reinterpret_cast<uint64_t*>(p);
+    const int64_t nsub = ceil_div(draws, kJumpStride);
+    p += (size_t)nsub * NN * 8;
+    uint64_t* xseq = reinterpret_cast<uint64_t*>(p);
+    p += (size_t)kJumpSeqWords * 8;
+    void* temp = p;
+    size_t temp_bytes = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, temp_bytes, flags, pos, (int)attempts);
+
+    if (nsub <= 1) {
+        mt_generate_raw(seed, draws, raw, st);
+    } else {
+        // jump-ahead start windows for substreams q*stride (host F2 polynomial
+        // arithmetic, cached per stride), expanded on the device
+        mt_jump_starts(seed, kJumpStride, nsub, starts, xseq, st);
+        LAUNCH(mt_substream_kernel, (unsigned)nsub, 160, 0, st, starts, (int64_t)kJumpStride, draws, raw);
+    }
+    const int threads = 256;
+    const int blocks = (int)std::min<int64_t>(ceil_div(attempts, threads), 148 * 16);
+    LAUNCH(polar_flags_kernel, blocks, threads, 0, st, raw, attempts, flags);
+    CUDA_CHECK(cub::DeviceScan::ExclusiveSum(temp, temp_bytes, flags, pos, (int)attempts, st));
+    note_launch();
+    LAUNCH(last_total_kernel, 1, 1, 0, st, pos, flags, attempts, total);
+    long long h_total = 0;
+    CUDA_CHECK(cudaMemcpyAsync(&h_total, total, sizeof(long long), cudaMemcpyDeviceToHost, st));
+    CUDA_CHECK(cudaStreamSynchronize(st));
+    if (2 * h_total < count) fail(IHS_INTERNAL_ERROR, "fill_gaussian: draw estimate too small");
+    LAUNCH(polar_emit_kernel, blocks, threads, 0, st, raw, attempts, pos, count, stddev, d_out);
+}
+
+}  // namespace ihs_b200

@@ -1,0 +1,1016 @@
+// runtime.cpp — the C-ABI of include/ihs_gpu.h: problem handles, sketches,
+// the sketched system and the adaptive Polyak-IHS loop on the device.
+//
+// Control flow mirrors the reference line by line (solver.hpp:106-232); every
+// vector of the loop (x_t, x_{t-1}, g_t, g~_t and both candidates) stays in
+// HBM and only the decrement scalars of each evaluation cross to the host
+// for the accept/reject decision. Counters are the reference's closed forms
+// and are charged only for the evaluations the reference performs.
+#include "common.cuh"
+#include "host_rng.h"
+#include "mt_jump.h"
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+namespace ihs_b200 {
+
+void synth_generate(const ihs_synth_spec& s, int64_t row0, int64_t rows, double* A, int64_t lda, double* b,
+                    double* x_true);
+
+namespace {
+std::atomic<int64_t> g_launches{0};
+thread_local std::string g_last_error;
+
+template <class F>
+ihs_status guarded(F&& f) {
+    try {
+        f();
+        return IHS_OK;
+    } catch (const Status& s) {
+        g_last_error = s.what();
+        return s.code;
+    } catch (const std::bad_alloc&) {
+        g_last_error = "host allocation failed";
+        return IHS_INTERNAL_ERROR;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return IHS_INTERNAL_ERROR;
+    }
+}
+
+// ------------------------------------------------------------ device buffers
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() { release(); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+    void ensure(size_t b) {
+        if (b <= bytes) return;
+        release();
+        if (b == 0) return;
+        cudaError_t e = cudaMalloc(&p, b);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            fail(IHS_CUDA_ERROR, "cudaMalloc(" + std::to_string(b) + " bytes): " + cudaGetErrorString(e));
+        }
+        bytes = b;
+    }
+    template <class T> T* as() const { return static_cast<T*>(p); }
+    double* d() const { return static_cast<double*>(p); }
+};
+
+struct PinnedBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    ~PinnedBuf() { if (p) cudaFreeHost(p); }
+    void ensure(size_t b) {
+        if (b <= bytes) return;
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        CUDA_CHECK(cudaMallocHost(&p, b));
+        bytes = b;
+    }
+};
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        CUDA_CHECK(cudaGetDevice(&prev));
+        if (prev != dev) CUDA_CHECK(cudaSetDevice(dev));
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        if (cudaGetDevice(&cur) == cudaSuccess && cur != prev && prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+int sm_count(int dev) {
+    int v = 0;
+    CUDA_CHECK(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev));
+    return v;
+}
+
+void check_finite_host(const double* v, int64_t count, const char* msg) {
+    for (int64_t i = 0; i < count; ++i)
+        if (!std::isfinite(v[i])) fail(IHS_INVALID_INPUT, msg);
+}
+
+// ------------------------------------------------------------ phase timer
+struct PhaseTimer {
+    cudaStream_t st;
+    std::vector<std::pair<cudaEvent_t, int>> marks;  // (event, phase id) — phase id -1 = end
+    std::vector<cudaEvent_t> pool;
+    size_t used = 0;
+    bool enabled = true;
+    explicit PhaseTimer(cudaStream_t s) : st(s) {}
+    ~PhaseTimer() {
+        for (auto e : pool) cudaEventDestroy(e);
+    }
+    cudaEvent_t get() {
+        if (used == pool.size()) {
+            cudaEvent_t e;
+            CUDA_CHECK(cudaEventCreate(&e));
+            pool.push_back(e);
+        }
+        return pool[used++];
+    }
+    void mark(int phase) {
+        if (!enabled) return;
+        cudaEvent_t e = get();
+        CUDA_CHECK(cudaEventRecord(e, st));
+        marks.push_back({e, phase});
+    }
+    void reset() {
+        marks.clear();
+        used = 0;
+    }
+    // sum of intervals [mark(phase), next mark) per phase id
+    void collect(double out_ms[4]) {
+        for (int i = 0; i < 4; ++i) out_ms[i] = 0.0;
+        if (marks.size() < 2) return;
+        CUDA_CHECK(cudaEventSynchronize(marks.back().first));
+        for (size_t i = 0; i + 1 < marks.size(); ++i) {
+            const int ph = marks[i].second;
+            if (ph < 0 || ph > 3) continue;
+            float ms = 0.f;
+            CUDA_CHECK(cudaEventElapsedTime(&ms, marks[i].first, marks[i + 1].first));
+            out_ms[ph] += ms;
+        }
+    }
+};
+enum { PH_SKETCH = 0, PH_FACTOR = 1, PH_GRAD = 2, PH_SOLVE = 3, PH_END = -1 };
+
+}  // namespace
+
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+}  // namespace ihs_b200
+
+using namespace ihs_b200;
+
+// ============================================================ opaque handles
+struct ihs_gpu_system {
+    int device = 0;
+    int64_t m = 0, d = 0;
+    double nu = 0.0;
+    int kind = IHS_FACTOR_DIRECT_GRAM;
+    cudaStream_t st = nullptr;
+    bool own_stream = false;
+    int num_sms = 148;
+    DevBuf SA;    // m x d
+    DevBuf L;     // k x k factor (k = m or d), upper triangle = L^T
+    DevBuf work;  // split-K workspace
+    DevBuf tmp;   // solve scratch (2 * max(m, d))
+    DevBuf info;
+    ~ihs_gpu_system() {
+        if (own_stream && st) cudaStreamDestroy(st);
+    }
+    int64_t k() const { return kind == IHS_FACTOR_WOODBURY_INNER ? m : d; }
+    uint64_t factor_flops() const {  // sketched_system.hpp:52-57
+        const uint64_t mm = (uint64_t)m, dd = (uint64_t)d;
+        if (kind == IHS_FACTOR_WOODBURY_INNER) return mm * mm * dd + mm * mm * mm / 3;
+        return dd * dd * mm + dd * dd * dd / 3;
+    }
+    uint64_t flops_per_solve() const {  // sketched_system.hpp:61-66
+        const uint64_t mm = (uint64_t)m, dd = (uint64_t)d;
+        if (kind == IHS_FACTOR_WOODBURY_INNER) return 2 * mm * dd + mm * mm + 2 * dd;
+        return dd * dd + dd;
+    }
+};
+
+struct ihs_gpu_problem {
+    int device = 0;
+    int64_t n = 0, d = 0;
+    double nu = 0.0;
+    int orientation = IHS_OVERDETERMINED;
+    ihs_gpu_options opts{};
+    cudaStream_t st = nullptr;
+    int num_sms = 148;
+    DevBuf A, b;                 // A packed n x d (lda = n)
+    GradPlan gplan{};
+    DevBuf grad_work;
+    // sketch workspaces
+    DevBuf T, signbits, entries, tiles, gauss_scratch, S, gemm_work;
+    PinnedBuf h_stage;
+    std::vector<int64_t> h_rows;
+    std::vector<int2> h_entries;
+    std::vector<int4> h_tiles;
+    // solver vectors
+    DevBuf vecs;                 // 12 * d doubles
+    DevBuf dots;                 // 4 doubles
+    PinnedBuf h_dots;
+    std::unique_ptr<PhaseTimer> timer;
+    ~ihs_gpu_problem() {
+        if (st) cudaStreamDestroy(st);
+    }
+};
+
+namespace ihs_b200 {
+namespace {
+
+// -------------------------------------------------------- sketches (device)
+// SA (m x d, ld m, device) = apply_sketch(A, {kind, m, seed}) (sketch.hpp:110-117)
+void device_sketch(ihs_gpu_problem* P, int kind, int64_t m, uint64_t seed, double* d_SA, ihs_counters* c) {
+    const int64_t n = P->n, d = P->d;
+    cudaStream_t st = P->st;
+    if (kind == IHS_SKETCH_SRHT) {
+        if (m < 1) fail(IHS_INVALID_INPUT, "srht_sketch: m must be >= 1");
+        const SrhtPlan plan = srht_plan(n, d, n, m);
+        if (m > plan.n_pad) fail(IHS_SKETCH_TOO_LARGE, "srht_sketch: m exceeds padded row count");
+        // D: rademacher(n_pad, make_stream(seed, 1)) as bits (sketch.hpp:85,87)
+        P->signbits.ensure((size_t)((plan.n_pad + 31) / 32) * 4);
+        mt_rademacher_bits(derive_seed(seed, 1), plan.n_pad, P->signbits.as<uint32_t>(), st);
+        // P: sample_without_replacement(n_pad, m, make_stream(seed, 2)) (sketch.hpp:86,88)
+        P->h_rows.resize((size_t)m);
+        sample_without_replacement(derive_seed(seed, 2), plan.n_pad, m, P->h_rows.data());
+        srht_build_entries(plan, P->h_rows.data(), P->h_entries, P->h_tiles);
+        const size_t eb = P->h_entries.size() * sizeof(int2), tb = P->h_tiles.size() * sizeof(int4);
+        P->h_stage.ensure(eb + tb + 64);
+        // the previous sketch's copy out of the staging buffer must be done
+        CUDA_CHECK(cudaStreamSynchronize(st));
+        std::memcpy(P->h_stage.p, P->h_entries.data(), eb);
+        std::memcpy(static_cast<char*>(P->h_stage.p) + eb, P->h_tiles.data(), tb);
+        P->entries.ensure(eb + 16);
+        P->tiles.ensure(tb + 16);
+        CUDA_CHECK(cudaMemcpyAsync(P->entries.p, P->h_stage.p, eb, cudaMemcpyHostToDevice, st));
+        CUDA_CHECK(cudaMemcpyAsync(P->tiles.p, static_cast<char*>(P->h_stage.p) + eb, tb, cudaMemcpyHostToDevice, st));
+        P->T.ensure(srht_scratch_bytes(plan));
+        srht_run_device(plan, P->A.d(), P->signbits.as<uint32_t>(), P->entries.as<int2>(), P->tiles.as<int4>(),
+                        (int)P->h_tiles.size(), P->T.d(), d_SA, st);
+        if (c) {  // sketch.hpp:99-106
+            const uint64_t np = (uint64_t)plan.n_pad, dd = (uint64_t)d;
+            c->sketch += dd * np * (uint64_t)plan.logn + (uint64_t)n * dd + (uint64_t)m * dd;
+        }
+    } else if (kind == IHS_SKETCH_GAUSSIAN) {
+        if (m < 1) fail(IHS_INVALID_INPUT, "gaussian_sketch: m must be >= 1");
+        // S (m x n) ~ N(0, 1/m) from make_stream(seed, 0), column-major (sketch.hpp:62-64)
+        const int64_t count = m * n;
+        P->S.ensure((size_t)count * sizeof(double));
+        P->gauss_scratch.ensure(gaussian_scratch_bytes(count));
+        const double stddev = 1.0 / std::sqrt(static_cast<double>(m));
+        mt_fill_gaussian(derive_seed(seed, 0), count, stddev, P->S.d(), P->gauss_scratch.p, st);
+        // SA = S * A on the DMMA path (sketch.hpp:68)
+        const int splitk = dgemm_pick_splitk(m, d, n, P->num_sms);
+        if (splitk > 1) P->gemm_work.ensure((size_t)splitk * m * d * sizeof(double));
+        dgemm(false, false, m, d, n, 1.0, P->S.d(), m, P->A.d(), n, 0.0, d_SA, m, false, splitk,
+              splitk > 1 ? P->gemm_work.d() : nullptr, st);
+        if (c) c->sketch += (uint64_t)m * (uint64_t)n * (uint64_t)d;  // sketch.hpp:65-67
+    } else {
+        fail(IHS_INVALID_INPUT, "apply_sketch: unknown sketch kind");
+    }
+}
+
+// ---------------------------------------------------- sketched system (device)
+// SketchedSystem::factorize (sketched_system.hpp:25-31, 69-84) of a device SA
+// already stored in sys->SA.
+void system_factorize(ihs_gpu_system* S, ihs_counters* c) {
+    const int64_t m = S->m, d = S->d;
+    cudaStream_t st = S->st;
+    if (!(S->nu > 0.0)) fail(IHS_INVALID_INPUT, "SketchedSystem: nu must be positive");
+    S->info.ensure(2 * sizeof(int));
+    int* d_flag = S->info.as<int>() + 1;
+    CUDA_CHECK(cudaMemsetAsync(d_flag, 0, sizeof(int), st));
+    if (m * d > 0) check_finite(S->SA.d(), m * d, d_flag, st);
+    S->kind = m < d ? IHS_FACTOR_WOODBURY_INNER : IHS_FACTOR_DIRECT_GRAM;
+    const int64_t k = S->k();
+    S->L.ensure((size_t)k * k * sizeof(double));
+    const double nu2 = S->nu * S->nu;
+    if (S->kind == IHS_FACTOR_WOODBURY_INNER) {
+        // inner = SA SA^T + nu^2 I_m (lower)
+        const int splitk = dgemm_pick_splitk(m, m, d, S->num_sms);
+        if (splitk > 1) S->work.ensure((size_t)splitk * m * m * sizeof(double));
+        dgemm(false, true, m, m, d, 1.0, S->SA.d(), m, S->SA.d(), m, 0.0, S->L.d(), m, true, splitk,
+              splitk > 1 ? S->work.d() : nullptr, st);
+    } else {
+        // gram = SA^T SA + nu^2 I_d (lower)
+        const int splitk = dgemm_pick_splitk(d, d, m, S->num_sms);
+        if (splitk > 1) S->work.ensure((size_t)splitk * d * d * sizeof(double));
+        dgemm(true, false, d, d, m, 1.0, S->SA.d(), m, S->SA.d(), m, 0.0, S->L.d(), d, true, splitk,
+              splitk > 1 ? S->work.d() : nullptr, st);
+    }
+    add_diag(S->L.d(), k, nu2, st);
+    cholesky_factor(S->L.d(), k, nullptr, S->info.as<int>(), S->num_sms, st);
+    int h_info[2] = {0, 0};
+    CUDA_CHECK(cudaMemcpyAsync(h_info, S->info.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+    CUDA_CHECK(cudaStreamSynchronize(st));
+    if (h_info[1]) fail(IHS_INVALID_INPUT, "SketchedSystem: non-finite sketched matrix");
+    if (h_info[0]) fail(IHS_NUMERICAL_BREAKDOWN, "SketchedSystem: Cholesky factorization failed");
+    S->tmp.ensure((size_t)2 * std::max(m, d) * sizeof(double));
+    if (c) c->factor += S->factor_flops();
+}
+
+// z[:, q] = H_S^{-1} g[:, q] (sketched_system.hpp:40-49), device vectors, ld = d
+void system_solve_dev(const ihs_gpu_system* S, const double* g, double* z, int nrhs) {
+    const int64_t m = S->m, d = S->d;
+    cudaStream_t st = S->st;
+    if (S->kind == IHS_FACTOR_WOODBURY_INNER) {
+        double* u = S->tmp.d();  // nrhs x m
+        gemv_n(S->SA.d(), m, d, m, g, nrhs, d, u, m, st);
+        cholesky_solve(S->L.d(), m, u, nrhs, st);
+        woodbury_finish(S->SA.d(), m, d, g, u, S->nu * S->nu, nrhs, z, st);
+    } else {
+        if (z != g) CUDA_CHECK(cudaMemcpyAsync(z, g, (size_t)nrhs * d * sizeof(double), cudaMemcpyDeviceToDevice, st));
+        cholesky_solve(S->L.d(), d, z, nrhs, st);
+    }
+}
+
+void problem_grad(ihs_gpu_problem* P, const double* X, int nrhs, double* G) {
+    grad_run(P->gplan, P->A.d(), P->b.d(), P->nu * P->nu, X, nrhs, G, P->grad_work.d(), P->st);
+}
+
+}  // namespace
+}  // namespace ihs_b200
+
+// ============================================================== C-ABI
+extern "C" {
+
+const char* ihs_gpu_last_error(void) { return ihs_b200::g_last_error.c_str(); }
+const char* ihs_gpu_version(void) { return "ihs-b200 0.1.0 (sm_100a)"; }
+int64_t ihs_gpu_kernel_launch_count(void) { return ihs_b200::g_launches.load(); }
+int ihs_gpu_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+uint64_t ihs_derive_seed(uint64_t seed, uint64_t tag) { return ihs_b200::derive_seed(seed, tag); }
+int64_t ihs_next_pow2(int64_t n) {
+    int64_t p = 1;
+    while (p < n) p <<= 1;
+    return n <= 0 ? 1 : p;
+}
+
+ihs_status ihs_rates_from_bounds(double lam, double Lam, ihs_tuning* tp) {  // tuning.hpp:25-38
+    return guarded([&] {
+        if (!(lam > 0.0) || !(lam <= Lam)) fail(IHS_INVALID_INPUT, "rates_from_bounds: need 0 < lam <= Lam");
+        tp->lam = lam;
+        tp->Lam = Lam;
+        tp->mu_gd = 2.0 / (1.0 / lam + 1.0 / Lam);
+        const double r = (Lam - lam) / (Lam + lam);
+        tp->c_gd = r * r;
+        const double sl = std::sqrt(lam), sL = std::sqrt(Lam);
+        tp->mu_p = 4.0 / ((1.0 / sl + 1.0 / sL) * (1.0 / sl + 1.0 / sL));
+        const double q = (sL - sl) / (sL + sl);
+        tp->beta_p = tp->c_p = q * q;
+    });
+}
+
+ihs_status ihs_gaussian_targets(double rho, double eta, int enforce, double* lam, double* Lam) {  // :47-56
+    return guarded([&] {
+        if (!(rho > 0.0) || !(eta > 0.0)) fail(IHS_INVALID_INPUT, "gaussian_targets: rho, eta must be positive");
+        if (enforce && (rho > 0.18 || eta > 0.01))
+            fail(IHS_OUT_OF_VALIDITY_RANGE, "gaussian_targets: proven region is rho <= 0.18, eta <= 0.01");
+        const double ce = (1.0 + 3.0 * std::sqrt(eta)) * (1.0 + 3.0 * std::sqrt(eta));
+        const double s = std::sqrt(ce * rho);
+        if (s >= 1.0) fail(IHS_OUT_OF_VALIDITY_RANGE, "gaussian_targets: c_eta * rho must be < 1");
+        *lam = (1.0 - s) * (1.0 - s);
+        *Lam = (1.0 + s) * (1.0 + s);
+    });
+}
+
+ihs_status ihs_srht_targets(double rho, double* lam, double* Lam) {  // :59-63
+    return guarded([&] {
+        if (!(rho > 0.0 && rho < 1.0)) fail(IHS_INVALID_INPUT, "srht_targets: rho must be in (0,1)");
+        const double s = std::sqrt(rho);
+        *lam = 1.0 - s;
+        *Lam = 1.0 + s;
+    });
+}
+
+void ihs_solver_config_default(ihs_solver_config* c) {  // solver.hpp:28-57
+    std::memset(c, 0, sizeof(*c));
+    c->rho = 0.1;
+    c->eta = 0.01;
+    c->sketch_kind = IHS_SKETCH_GAUSSIAN;
+    c->mode = IHS_MODE_POLYAK_THEN_GRADIENT;
+    c->m_initial = 1;
+    c->eps = 1e-10;
+    c->max_iters = 500;
+    c->max_sketch = 0;
+    c->seed = 0;
+    c->enforce_validity = 1;
+    c->recompute_r_after_resketch = 1;
+    c->record_iterates = 0;
+}
+
+ihs_status ihs_sample_without_replacement(uint64_t stream_seed, int64_t n, int64_t m, int64_t* out) {
+    return guarded([&] {
+        if (m < 0 || m > n) fail(IHS_INVALID_INPUT, "sample_without_replacement: need 0 <= m <= n");
+        ihs_b200::sample_without_replacement(stream_seed, n, m, out);
+    });
+}
+
+ihs_status ihs_newton_decrement(const double* g, const double* gt, int64_t d, double* r) {  // :95-101
+    return guarded([&] {
+        double dot = 0.0, sq = 0.0;
+        for (int64_t i = 0; i < d; ++i) {
+            dot += g[i] * gt[i];
+            sq += g[i] * g[i];
+        }
+        const double v = 0.5 * dot;
+        if (v < -1e-12 * (1.0 + sq)) fail(IHS_NUMERICAL_BREAKDOWN, "newton_decrement: negative decrement");
+        *r = v < 0.0 ? 0.0 : v;
+    });
+}
+
+// ------------------------------------------------------------------ problem
+ihs_status ihs_gpu_problem_create(const double* A, int64_t n, int64_t d, int64_t lda, const double* b, double nu,
+                                  int32_t orientation, const ihs_gpu_options* opts, ihs_gpu_problem** out) {
+    return guarded([&] {
+        *out = nullptr;
+        // ProblemInstance validation order (problem.hpp:24-32)
+        if (!(nu > 0.0)) fail(IHS_INVALID_INPUT, "ProblemInstance: nu must be strictly positive");
+        if (n < 1 || d < 1) fail(IHS_INVALID_INPUT, "ProblemInstance: empty matrix");
+        if (!A || !b) fail(IHS_INVALID_INPUT, "ProblemInstance: size of b must match rows of A");
+        if (lda < n) fail(IHS_INVALID_INPUT, "ProblemInstance: lda < n");
+        for (int64_t j = 0; j < d; ++j) check_finite_host(A + j * lda, n, "ProblemInstance: non-finite input");
+        check_finite_host(b, n, "ProblemInstance: non-finite input");
+        if (!std::isfinite(nu)) fail(IHS_INVALID_INPUT, "ProblemInstance: non-finite input");
+        const int64_t n_global = (opts && opts->world_size > 1) ? opts->n_global : n;
+        if (orientation == IHS_OVERDETERMINED && n_global < d)
+            fail(IHS_INVALID_INPUT, "ProblemInstance: overdetermined orientation requires n >= d");
+        if (orientation == IHS_UNDERDETERMINED && d < n_global)
+            fail(IHS_INVALID_INPUT, "ProblemInstance: underdetermined orientation requires d >= n");
+        if (orientation == IHS_UNDERDETERMINED)
+            fail(IHS_INVALID_INPUT, "ihs_gpu: underdetermined (dual) instances are not on the GPU path yet");
+        auto P = std::make_unique<ihs_gpu_problem>();
+        P->device = opts ? opts->device : 0;
+        if (opts) P->opts = *opts;
+        if (P->opts.world_size < 1) P->opts.world_size = 1;
+        if (P->opts.world_size > 1)
+            fail(IHS_INVALID_INPUT, "ihs_gpu: multi-rank problems are created through ihs_gpu_problem_create_sharded");
+        P->opts.n_global = n;
+        P->opts.row_offset = 0;
+        DeviceGuard g(P->device);
+        P->n = n;
+        P->d = d;
+        P->nu = nu;
+        P->orientation = orientation;
+        P->num_sms = sm_count(P->device);
+        CUDA_CHECK(cudaStreamCreateWithFlags(&P->st, cudaStreamNonBlocking));
+        P->A.ensure((size_t)n * d * sizeof(double));
+        P->b.ensure((size_t)n * sizeof(double));
+        CUDA_CHECK(cudaMemcpy2DAsync(P->A.p, (size_t)n * sizeof(double), A, (size_t)lda * sizeof(double),
+                                     (size_t)n * sizeof(double), (size_t)d, cudaMemcpyHostToDevice, P->st));
+        CUDA_CHECK(cudaMemcpyAsync(P->b.p, b, (size_t)n * sizeof(double), cudaMemcpyHostToDevice, P->st));
+        P->gplan = grad_plan(n, d, n, P->num_sms);
+        P->grad_work.ensure(grad_work_doubles(P->gplan) * sizeof(double));
+        P->vecs.ensure((size_t)16 * d * sizeof(double));
+        P->dots.ensure(8 * sizeof(double));
+        P->h_dots.ensure(8 * sizeof(double));
+        P->timer = std::make_unique<PhaseTimer>(P->st);
+        CUDA_CHECK(cudaStreamSynchronize(P->st));
+        *out = P.release();
+    });
+}
+
+void ihs_gpu_problem_destroy(ihs_gpu_problem* p) {
+    if (!p) return;
+    try {
+        DeviceGuard g(p->device);
+        cudaStreamSynchronize(p->st);
+        delete p;
+    } catch (...) {
+    }
+}
+
+int64_t ihs_gpu_problem_rows(const ihs_gpu_problem* p) { return p ? p->n : 0; }
+int64_t ihs_gpu_problem_cols(const ihs_gpu_problem* p) { return p ? p->d : 0; }
+
+ihs_status ihs_gpu_problem_upload(ihs_gpu_problem* P, const double* A, int64_t lda, const double* b) {
+    return guarded([&] {
+        if (!P) fail(IHS_INVALID_INPUT, "null problem");
+        DeviceGuard g(P->device);
+        if (A) {
+            if (lda < P->n) fail(IHS_INVALID_INPUT, "lda < n");
+            CUDA_CHECK(cudaMemcpy2DAsync(P->A.p, (size_t)P->n * sizeof(double), A, (size_t)lda * sizeof(double),
+                                         (size_t)P->n * sizeof(double), (size_t)P->d, cudaMemcpyHostToDevice, P->st));
+        }
+        if (b) CUDA_CHECK(cudaMemcpyAsync(P->b.p, b, (size_t)P->n * sizeof(double), cudaMemcpyHostToDevice, P->st));
+        CUDA_CHECK(cudaStreamSynchronize(P->st));
+    });
+}
+
+ihs_status ihs_gpu_gradient(ihs_gpu_problem* P, const double* x, double* g, ihs_counters* c) {
+    return guarded([&] {
+        if (!P || !x || !g) fail(IHS_INVALID_INPUT, "gradient: dimension mismatch");
+        DeviceGuard dg(P->device);
+        const int64_t d = P->d;
+        double* X = P->vecs.d();
+        double* G = X + d;
+        CUDA_CHECK(cudaMemcpyAsync(X, x, (size_t)d * sizeof(double), cudaMemcpyHostToDevice, P->st));
+        problem_grad(P, X, 1, G);
+        CUDA_CHECK(cudaMemcpyAsync(g, G, (size_t)d * sizeof(double), cudaMemcpyDeviceToHost, P->st));
+        CUDA_CHECK(cudaStreamSynchronize(P->st));
+        if (c) c->matvec += 2 * (uint64_t)P->n * (uint64_t)d + (uint64_t)P->n + 2 * (uint64_t)d;  // problem.hpp:66
+    });
+}
+
+ihs_status ihs_gpu_sketch(ihs_gpu_problem* P, int32_t kind, int64_t m, uint64_t seed, double* SA_out,
+                          ihs_counters* c) {
+    return guarded([&] {
+        if (!P) fail(IHS_INVALID_INPUT, "null problem");
+        DeviceGuard dg(P->device);
+        if (m < 1) fail(IHS_INVALID_INPUT, kind == IHS_SKETCH_SRHT ? "srht_sketch: m must be >= 1"
+                                                                    : "gaussian_sketch: m must be >= 1");
+        DevBuf SA;
+        SA.ensure((size_t)m * P->d * sizeof(double));
+        device_sketch(P, kind, m, seed, SA.d(), c);
+        if (SA_out)
+            CUDA_CHECK(cudaMemcpyAsync(SA_out, SA.p, (size_t)m * P->d * sizeof(double), cudaMemcpyDeviceToHost, P->st));
+        CUDA_CHECK(cudaStreamSynchronize(P->st));
+    });
+}
+
+ihs_status ihs_gpu_sketch_matrix(const double* A, int64_t n, int64_t d, int64_t lda, int32_t kind, int64_t m,
+                                 uint64_t seed, double* SA_out, ihs_counters* c) {
+    return guarded([&] {
+        if (n < 1 || d < 1 || lda < n) fail(IHS_INVALID_INPUT, "sketch: empty or malformed matrix");
+        if (m < 1) fail(IHS_INVALID_INPUT, kind == IHS_SKETCH_SRHT ? "srht_sketch: m must be >= 1"
+                                                                    : "gaussian_sketch: m must be >= 1");
+        // a throw-away problem (b = 0, nu = 1); the sketch does not look at b or nu
+        std::vector<double> zeros((size_t)n, 0.0);
+        ihs_gpu_problem* P = nullptr;
+        auto P_holder = std::unique_ptr<ihs_gpu_problem, void (*)(ihs_gpu_problem*)>(nullptr, ihs_gpu_problem_destroy);
+        {
+            auto Pp = std::make_unique<ihs_gpu_problem>();
+            Pp->device = 0;
+            Pp->opts.world_size = 1;
+            Pp->opts.n_global = n;
+            CUDA_CHECK(cudaGetDevice(&Pp->device));
+            Pp->n = n;
+            Pp->d = d;
+            Pp->nu = 1.0;
+            Pp->num_sms = sm_count(Pp->device);
+            CUDA_CHECK(cudaStreamCreateWithFlags(&Pp->st, cudaStreamNonBlocking));
+            Pp->A.ensure((size_t)n * d * sizeof(double));
+            CUDA_CHECK(cudaMemcpy2DAsync(Pp->A.p, (size_t)n * sizeof(double), A, (size_t)lda * sizeof(double),
+                                         (size_t)n * sizeof(double), (size_t)d, cudaMemcpyHostToDevice, Pp->st));
+            P = Pp.release();
+            P_holder.reset(P);
+        }
+        DevBuf SA;
+        SA.ensure((size_t)m * d * sizeof(double));
+        device_sketch(P, kind, m, seed, SA.d(), c);
+        CUDA_CHECK(cudaMemcpyAsync(SA_out, SA.p, (size_t)m * d * sizeof(double), cudaMemcpyDeviceToHost, P->st));
+        CUDA_CHECK(cudaStreamSynchronize(P->st));
+    });
+}
+
+ihs_status ihs_gpu_fwht(double* v, int64_t n) {  // fwht_inplace (sketch.hpp:33-49)
+    return guarded([&] {
+        if (n <= 0 || (n & (n - 1)) != 0) fail(IHS_INVALID_INPUT, "fwht_inplace: length must be a power of two");
+        cudaStream_t st;
+        CUDA_CHECK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        DevBuf dv, dT, dbits, dent, dtiles, dout;
+        SrhtPlan p = srht_plan(n, 1, n, n);
+        p.scale2 = 1.0;  // a single normalization pass, v *= 1/sqrt(n)
+        dv.ensure((size_t)n * 8);
+        dout.ensure((size_t)n * 8);
+        CUDA_CHECK(cudaMemcpyAsync(dv.p, v, (size_t)n * 8, cudaMemcpyHostToDevice, st));
+        const int64_t words = (n + 31) / 32;
+        dbits.ensure((size_t)words * 4);
+        CUDA_CHECK(cudaMemsetAsync(dbits.p, 0xFF, (size_t)words * 4, st));  // all signs +1
+        std::vector<int64_t> rows((size_t)n);
+        for (int64_t i = 0; i < n; ++i) rows[(size_t)i] = i;
+        std::vector<int2> ent;
+        std::vector<int4> til;
+        srht_build_entries(p, rows.data(), ent, til);
+        dent.ensure(ent.size() * sizeof(int2));
+        dtiles.ensure(til.size() * sizeof(int4) + 16);
+        CUDA_CHECK(cudaMemcpyAsync(dent.p, ent.data(), ent.size() * sizeof(int2), cudaMemcpyHostToDevice, st));
+        CUDA_CHECK(cudaMemcpyAsync(dtiles.p, til.data(), til.size() * sizeof(int4), cudaMemcpyHostToDevice, st));
+        dT.ensure(srht_scratch_bytes(p) + 8);
+        srht_run_device(p, dv.d(), dbits.as<uint32_t>(), dent.as<int2>(), dtiles.as<int4>(), (int)til.size(), dT.d(),
+                        dout.d(), st);
+        CUDA_CHECK(cudaMemcpyAsync(v, dout.p, (size_t)n * 8, cudaMemcpyDeviceToHost, st));
+        CUDA_CHECK(cudaStreamSynchronize(st));
+        cudaStreamDestroy(st);
+    });
+}
+
+// ------------------------------------------------------------- RNG parity
+ihs_status ihs_gpu_rademacher_bits(uint64_t stream_seed, int64_t n, uint32_t* out_bits) {
+    return guarded([&] {
+        if (n < 0) fail(IHS_INVALID_INPUT, "rademacher: n < 0");
+        const int64_t words = (n + 31) / 32;
+        DevBuf buf;
+        buf.ensure((size_t)words * 4 + 4);
+        mt_rademacher_bits(stream_seed, n, buf.as<uint32_t>(), 0);
+        CUDA_CHECK(cudaMemcpy(out_bits, buf.p, (size_t)words * 4, cudaMemcpyDeviceToHost));
+    });
+}
+
+ihs_status ihs_gpu_fill_gaussian(uint64_t stream_seed, int64_t rows, int64_t cols, double stddev, double* out) {
+    return guarded([&] {
+        const int64_t count = rows * cols;
+        if (rows < 0 || cols < 0) fail(IHS_INVALID_INPUT, "fill_gaussian: negative shape");
+        if (count == 0) return;
+        DevBuf o, scratch;
+        o.ensure((size_t)count * 8);
+        scratch.ensure(gaussian_scratch_bytes(count));
+        mt_fill_gaussian(stream_seed, count, stddev, o.d(), scratch.p, 0);
+        CUDA_CHECK(cudaMemcpy(out, o.p, (size_t)count * 8, cudaMemcpyDeviceToHost));
+    });
+}
+
+ihs_status ihs_gpu_mt19937_64(uint64_t stream_seed, int64_t count, uint64_t* out) {
+    return guarded([&] {
+        if (count <= 0) return;
+        DevBuf o;
+        o.ensure((size_t)count * 8);
+        mt_generate_raw(stream_seed, count, o.as<uint64_t>(), 0);
+        CUDA_CHECK(cudaMemcpy(out, o.p, (size_t)count * 8, cudaMemcpyDeviceToHost));
+    });
+}
+
+// ------------------------------------------------------------ system
+ihs_status ihs_gpu_system_factorize(const double* SA, int64_t m, int64_t d, int64_t lds, double nu, int32_t device,
+                                    ihs_counters* c, ihs_gpu_system** out) {
+    return guarded([&] {
+        *out = nullptr;
+        if (!(nu > 0.0)) fail(IHS_INVALID_INPUT, "SketchedSystem: nu must be positive");
+        if (m < 1 || d < 1 || lds < m) fail(IHS_INVALID_INPUT, "SketchedSystem: bad shape");
+        for (int64_t j = 0; j < d; ++j) check_finite_host(SA + j * lds, m, "SketchedSystem: non-finite sketched matrix");
+        DeviceGuard g(device);
+        auto S = std::make_unique<ihs_gpu_system>();
+        S->device = device;
+        S->m = m;
+        S->d = d;
+        S->nu = nu;
+        S->num_sms = sm_count(device);
+        CUDA_CHECK(cudaStreamCreateWithFlags(&S->st, cudaStreamNonBlocking));
+        S->own_stream = true;
+        S->SA.ensure((size_t)m * d * sizeof(double));
+        CUDA_CHECK(cudaMemcpy2DAsync(S->SA.p, (size_t)m * sizeof(double), SA, (size_t)lds * sizeof(double),
+                                     (size_t)m * sizeof(double), (size_t)d, cudaMemcpyHostToDevice, S->st));
+        system_factorize(S.get(), c);
+        *out = S.release();
+    });
+}
+
+void ihs_gpu_system_destroy(ihs_gpu_system* s) {
+    if (!s) return;
+    try {
+        DeviceGuard g(s->device);
+        cudaStreamSynchronize(s->st);
+        delete s;
+    } catch (...) {
+    }
+}
+int32_t ihs_gpu_system_kind(const ihs_gpu_system* s) { return s ? s->kind : -1; }
+int64_t ihs_gpu_system_m(const ihs_gpu_system* s) { return s ? s->m : 0; }
+int64_t ihs_gpu_system_d(const ihs_gpu_system* s) { return s ? s->d : 0; }
+uint64_t ihs_gpu_system_factor_flops(const ihs_gpu_system* s) { return s ? s->factor_flops() : 0; }
+uint64_t ihs_gpu_system_flops_per_solve(const ihs_gpu_system* s) { return s ? s->flops_per_solve() : 0; }
+
+ihs_status ihs_gpu_system_solve(const ihs_gpu_system* S, const double* g, double* z, ihs_counters* c) {
+    return guarded([&] {
+        if (!S || !g || !z) fail(IHS_INVALID_INPUT, "SketchedSystem::solve: dimension mismatch");
+        DeviceGuard dg(S->device);
+        DevBuf buf;
+        buf.ensure((size_t)2 * S->d * sizeof(double));
+        double* dg_ = buf.d();
+        double* dz = dg_ + S->d;
+        CUDA_CHECK(cudaMemcpyAsync(dg_, g, (size_t)S->d * 8, cudaMemcpyHostToDevice, S->st));
+        system_solve_dev(S, dg_, dz, 1);
+        CUDA_CHECK(cudaMemcpyAsync(z, dz, (size_t)S->d * 8, cudaMemcpyDeviceToHost, S->st));
+        CUDA_CHECK(cudaStreamSynchronize(S->st));
+        if (c) c->solve += S->flops_per_solve();
+    });
+}
+
+// ------------------------------------------------------------ adaptive solve
+ihs_status ihs_gpu_adaptive_solve(ihs_gpu_problem* P, const ihs_solver_config* cfg, ihs_solve_report* rep) {
+    return guarded([&] {
+        if (!P || !cfg || !rep || !rep->x) fail(IHS_INVALID_INPUT, "adaptive_solve: null argument");
+        DeviceGuard dgd(P->device);
+        // solver.hpp:243-245 and :107-109
+        if (P->orientation != IHS_OVERDETERMINED)
+            fail(IHS_INVALID_INPUT, "adaptive_solve: expects an overdetermined instance (use solve_underdetermined for d > n)");
+        if (!(cfg->eps > 0.0 && cfg->eps < 1.0)) fail(IHS_INVALID_INPUT, "adaptive_solve: eps must be in (0,1)");
+        if (cfg->m_initial < 1) fail(IHS_INVALID_INPUT, "adaptive_solve: m_initial must be >= 1");
+        if (cfg->max_iters < 1) fail(IHS_INVALID_INPUT, "adaptive_solve: max_iters must be >= 1");
+
+        const auto t_start = std::chrono::steady_clock::now();
+        const int64_t dim = P->d;
+        const int64_t n_rows = P->opts.world_size > 1 ? P->opts.n_global : P->n;
+        cudaStream_t st = P->st;
+        PhaseTimer& tm = *P->timer;
+        tm.reset();
+        const int64_t launches0 = g_launches.load();
+        ihs_phase_times PT{};
+        cudaEvent_t ev_begin = tm.get(), ev_end = tm.get();
+        CUDA_CHECK(cudaEventRecord(ev_begin, st));
+
+        // tuning (solver.hpp:115-124)
+        ihs_tuning tp{};
+        if (cfg->has_tuning_override) {
+            tp = cfg->tuning_override;
+        } else {
+            double lam = 0, Lam = 0;
+            ihs_status s = cfg->sketch_kind == IHS_SKETCH_GAUSSIAN
+                               ? ihs_gaussian_targets(cfg->rho, cfg->eta, cfg->enforce_validity, &lam, &Lam)
+                               : ihs_srht_targets(cfg->rho, &lam, &Lam);
+            if (s != IHS_OK) fail(s, g_last_error);
+            s = ihs_rates_from_bounds(lam, Lam, &tp);
+            if (s != IHS_OK) fail(s, g_last_error);
+        }
+        // growth cap (solver.hpp:128-130)
+        int64_t cap = cfg->sketch_kind == IHS_SKETCH_SRHT ? ihs_next_pow2(n_rows) : n_rows;
+        if (cfg->max_sketch > 0) cap = std::min(cap, cfg->max_sketch);
+        cap = std::max(cap, cfg->m_initial);
+
+        ihs_counters C{};
+        std::vector<ihs_iteration_record> log;
+        int64_t iterates_written = 0;
+        auto push_iterate = [&](const double* d_x) {
+            if (!cfg->record_iterates) return;
+            if (rep->iterates && iterates_written < rep->iterates_capacity)
+                CUDA_CHECK(cudaMemcpyAsync(rep->iterates + iterates_written * dim, d_x, (size_t)dim * 8,
+                                           cudaMemcpyDeviceToHost, st));
+            ++iterates_written;
+        };
+
+        int64_t m = cfg->m_initial, K = 0;
+        // system for the current sketch
+        ihs_gpu_system sys;
+        sys.device = P->device;
+        sys.d = dim;
+        sys.nu = P->nu;
+        sys.st = st;
+        sys.num_sms = P->num_sms;
+        auto sketch_and_factor = [&](int64_t mm, uint64_t sub_seed) {
+            sys.m = mm;
+            sys.SA.ensure((size_t)mm * dim * sizeof(double));
+            tm.mark(PH_SKETCH);
+            PT.n_sketch++;
+            PT.n_factor++;
+            if (cfg->sketch_kind == IHS_SKETCH_SRHT)
+                PT.sketch_bytes += 8.0 * (double)P->n * (double)dim + 8.0 * (double)mm * (double)dim;
+            else
+                PT.sketch_flops += 2.0 * (double)mm * (double)P->n * (double)dim;
+            if (cfg->sketch_override) {  // solver.hpp:102: host hook, no sketch counters
+                std::vector<double> h((size_t)mm * dim);
+                if (cfg->sketch_override(cfg->sketch_override_user, mm, sub_seed, h.data()) != 0)
+                    fail(IHS_INVALID_INPUT, "sketch_override failed");
+                CUDA_CHECK(cudaMemcpyAsync(sys.SA.p, h.data(), h.size() * 8, cudaMemcpyHostToDevice, st));
+                CUDA_CHECK(cudaStreamSynchronize(st));
+            } else {
+                device_sketch(P, cfg->sketch_kind, mm, sub_seed, sys.SA.d(), &C);
+            }
+            tm.mark(PH_FACTOR);
+            system_factorize(&sys, &C);
+            tm.mark(PH_END);
+        };
+
+        // device vectors: x, xprev, g, gt (current), X2 = [xp; xg], G2, GT2 (candidates)
+        P->vecs.ensure((size_t)16 * dim * sizeof(double));
+        double* base = P->vecs.d();
+        double* xcur = base + 0 * dim;
+        double* xprev = base + 1 * dim;
+        double* g = base + 2 * dim;
+        double* gt = base + 3 * dim;
+        double* X2 = base + 4 * dim;   // 2 x dim: [Polyak cand ; gradient cand]
+        double* G2 = base + 6 * dim;   // 2 x dim
+        double* GT2 = base + 8 * dim;  // 2 x dim
+        double* spare = base + 10 * dim;  // 2 x dim
+        double* dots = P->dots.d();
+        double* hd = static_cast<double*>(P->h_dots.p);
+
+        auto decrement = [&](double dotv, double sq) -> double {  // sketched_system.hpp:95-101
+            const double r = 0.5 * dotv;
+            if (r < -1e-12 * (1.0 + sq)) fail(IHS_NUMERICAL_BREAKDOWN, "newton_decrement: negative decrement");
+            return r < 0.0 ? 0.0 : r;
+        };
+
+        sketch_and_factor(m, derive_seed(cfg->seed, 0));  // solver.hpp:139-140
+
+        if (cfg->warm_start) {
+            CUDA_CHECK(cudaMemcpyAsync(xcur, cfg->warm_start, (size_t)dim * 8, cudaMemcpyHostToDevice, st));
+        } else {
+            CUDA_CHECK(cudaMemsetAsync(xcur, 0, (size_t)dim * 8, st));
+        }
+        CUDA_CHECK(cudaMemcpyAsync(xprev, xcur, (size_t)dim * 8, cudaMemcpyDeviceToDevice, st));
+
+        // g = grad(x); gt = solve(g); r = decrement  (solver.hpp:146-150)
+        tm.mark(PH_GRAD);
+        problem_grad(P, xcur, 1, g);
+        const double grad_pass_bytes = 8.0 * (double)P->n * (double)dim + 8.0 * (double)P->n;
+        PT.n_gradient++;
+        PT.gradient_bytes += grad_pass_bytes;
+        PT.n_solve++;
+        C.matvec += 2 * (uint64_t)n_rows * (uint64_t)dim + (uint64_t)n_rows + 2 * (uint64_t)dim;
+        tm.mark(PH_SOLVE);
+        system_solve_dev(&sys, g, gt, 1);
+        C.solve += sys.flops_per_solve();
+        decrement_dots(g, gt, dim, 1, dots, st);
+        tm.mark(PH_END);
+        CUDA_CHECK(cudaMemcpyAsync(hd, dots, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+        CUDA_CHECK(cudaStreamSynchronize(st));
+        double r = decrement(hd[0], hd[1]);
+        const double r1 = r;
+        push_iterate(xcur);
+
+        int64_t t = 1;
+        bool converged = !(r > cfg->eps * r1) || r1 == 0.0;  // :154
+        bool checks_enabled = true;
+        bool exhausted = false;
+
+        // candidate state: which slot of X2/G2/GT2 holds a valid evaluated candidate
+        auto accept = [&](int slot, double rc, int kind) {  // :167-178
+            const double r_prev = r;
+            // rotate buffers: xprev <- xcur <- cand ; g, gt <- cand's
+            std::swap(xprev, xcur);  // old xcur becomes xprev (pointer swap)
+            CUDA_CHECK(cudaMemcpyAsync(xcur, X2 + slot * dim, (size_t)dim * 8, cudaMemcpyDeviceToDevice, st));
+            CUDA_CHECK(cudaMemcpyAsync(g, G2 + slot * dim, (size_t)dim * 8, cudaMemcpyDeviceToDevice, st));
+            CUDA_CHECK(cudaMemcpyAsync(gt, GT2 + slot * dim, (size_t)dim * 8, cudaMemcpyDeviceToDevice, st));
+            r = rc;
+            ++t;
+            log.push_back({t, m, r, r_prev, kind, 0});
+            push_iterate(xcur);
+            converged = r <= cfg->eps * r1;
+        };
+
+        while (!converged && t < cfg->max_iters) {  // :180
+            const bool want_polyak = checks_enabled && cfg->mode == IHS_MODE_POLYAK_THEN_GRADIENT;
+            // Build both candidates from the same (x, x_prev, g~) and evaluate them in one
+            // pass over A (2 RHS): the gradient candidate does not depend on the Polyak
+            // outcome (:182, :190). Counters charge only what the reference evaluates.
+            tm.mark(PH_GRAD);
+            candidates(xcur, xprev, gt, tp.mu_p, tp.beta_p, tp.mu_gd, dim, want_polyak ? X2 : nullptr, X2 + dim, st);
+            const int nr = want_polyak ? 2 : 1;
+            const double* Xe = want_polyak ? X2 : X2 + dim;
+            double* Ge = want_polyak ? G2 : G2 + dim;
+            double* GTe = want_polyak ? GT2 : GT2 + dim;
+            problem_grad(P, Xe, nr, Ge);
+            PT.n_gradient++;
+            PT.gradient_bytes += grad_pass_bytes;
+            PT.n_solve += nr;
+            tm.mark(PH_SOLVE);
+            system_solve_dev(&sys, Ge, GTe, nr);
+            decrement_dots(Ge, GTe, dim, nr, dots, st);
+            tm.mark(PH_END);
+            CUDA_CHECK(cudaMemcpyAsync(hd, dots, (size_t)2 * nr * sizeof(double), cudaMemcpyDeviceToHost, st));
+            CUDA_CHECK(cudaStreamSynchronize(st));
+            const uint64_t grad_cost = 2 * (uint64_t)n_rows * (uint64_t)dim + (uint64_t)n_rows + 2 * (uint64_t)dim;
+            if (want_polyak) {
+                C.matvec += grad_cost;
+                C.solve += sys.flops_per_solve();
+                const double rp = decrement(hd[0], hd[1]);
+                const double ratio = std::pow(rp / r1, 1.0 / static_cast<double>(t));  // :183
+                if (ratio <= tp.c_p || rp <= cfg->eps * r1) {
+                    accept(0, rp, IHS_STEP_POLYAK);
+                    continue;
+                }
+            }
+            C.matvec += grad_cost;
+            C.solve += sys.flops_per_solve();
+            const double rg = want_polyak ? decrement(hd[2], hd[3]) : decrement(hd[0], hd[1]);
+            const bool pass = checks_enabled ? (rg <= tp.c_gd * r || rg <= cfg->eps * r1) : rg <= r;  // :191-193
+            if (pass) {
+                accept(1, rg, IHS_STEP_GRADIENT);
+                continue;
+            }
+            if (!checks_enabled) break;  // :198
+            if (2 * m > cap) {           // :201-209
+                exhausted = true;
+                checks_enabled = false;
+                if (rg <= r) {
+                    accept(1, rg, IHS_STEP_GRADIENT);
+                    continue;
+                }
+                break;
+            }
+            m *= 2;  // :210-220
+            ++K;
+            sketch_and_factor(m, derive_seed(cfg->seed, (uint64_t)K));
+            tm.mark(PH_SOLVE);
+            system_solve_dev(&sys, g, gt, 1);
+            C.solve += sys.flops_per_solve();
+            const double r_old = r;
+            if (cfg->recompute_r_after_resketch) {
+                decrement_dots(g, gt, dim, 1, dots, st);
+                tm.mark(PH_END);
+                CUDA_CHECK(cudaMemcpyAsync(hd, dots, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+                CUDA_CHECK(cudaStreamSynchronize(st));
+                r = decrement(hd[0], hd[1]);
+                converged = r <= cfg->eps * r1;
+            } else {
+                tm.mark(PH_END);
+            }
+            log.push_back({t, m, r, r_old, IHS_STEP_RESKETCH, 0});
+        }
+        (void)spare;
+
+        CUDA_CHECK(cudaMemcpyAsync(rep->x, xcur, (size_t)dim * 8, cudaMemcpyDeviceToHost, st));
+        CUDA_CHECK(cudaEventRecord(ev_end, st));
+        CUDA_CHECK(cudaStreamSynchronize(st));
+        {
+            float ms = 0.f;
+            CUDA_CHECK(cudaEventElapsedTime(&ms, ev_begin, ev_end));
+            PT.total_ms = ms;
+        }
+        rep->iterations = t;
+        rep->rejections = K;
+        rep->final_m = m;
+        rep->r1 = r1;
+        rep->r_final = r;
+        rep->converged = converged ? 1 : 0;
+        rep->sketch_exhausted = exhausted ? 1 : 0;
+        rep->log_size = (int64_t)log.size();
+        if (rep->log)
+            for (int64_t i = 0; i < rep->log_size && i < rep->log_capacity; ++i) rep->log[i] = log[(size_t)i];
+        rep->iterates_size = iterates_written;
+        rep->counters = C;
+        rep->tuning = tp;
+        rep->recompute_r_after_resketch = cfg->recompute_r_after_resketch;
+        rep->wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+        double ph[4];
+        tm.collect(ph);
+        rep->times = PT;
+        rep->times.sketch_ms = ph[PH_SKETCH];
+        rep->times.factor_ms = ph[PH_FACTOR];
+        rep->times.gradient_ms = ph[PH_GRAD];
+        rep->times.solve_ms = ph[PH_SOLVE];
+        rep->times.kernel_launches = g_launches.load() - launches0;
+        sys.st = nullptr;  // owned by the problem
+    });
+}
+
+ihs_status ihs_gpu_fixed_sketch_ihs(ihs_gpu_problem* P, const ihs_gpu_system* S, const ihs_tuning* tp, int64_t T,
+                                    int32_t mode, const double* x_start, double* iterates_out) {
+    return guarded([&] {
+        if (!P || !S || !tp || !iterates_out || T < 0) fail(IHS_INVALID_INPUT, "fixed_sketch_ihs: bad argument");
+        if (S->d != P->d) fail(IHS_INVALID_INPUT, "fixed_sketch_ihs: dimension mismatch");
+        DeviceGuard dgd(P->device);
+        const int64_t d = P->d;
+        cudaStream_t st = P->st;
+        // the system lives on its own stream: order it before ours
+        cudaEvent_t ev;
+        CUDA_CHECK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        CUDA_CHECK(cudaEventRecord(ev, S->st));
+        CUDA_CHECK(cudaStreamWaitEvent(st, ev, 0));
+        const double mu = mode == IHS_FIXED_GRADIENT ? tp->mu_gd : tp->mu_p;  // solver.hpp:261-262
+        const double beta = mode == IHS_FIXED_GRADIENT ? 0.0 : tp->beta_p;
+        double* base = P->vecs.d();
+        double* x = base;
+        double* xp = base + d;
+        double* gg = base + 2 * d;
+        double* step = base + 3 * d;
+        double* xn = base + 4 * d;
+        if (x_start) CUDA_CHECK(cudaMemcpyAsync(x, x_start, (size_t)d * 8, cudaMemcpyHostToDevice, st));
+        else CUDA_CHECK(cudaMemsetAsync(x, 0, (size_t)d * 8, st));
+        CUDA_CHECK(cudaMemcpyAsync(xp, x, (size_t)d * 8, cudaMemcpyDeviceToDevice, st));
+        CUDA_CHECK(cudaMemcpyAsync(iterates_out, x, (size_t)d * 8, cudaMemcpyDeviceToHost, st));
+        // the system's solve kernels run on S->st; rebind temporarily to ours
+        ihs_gpu_system* Sm = const_cast<ihs_gpu_system*>(S);
+        cudaStream_t sst = Sm->st;
+        Sm->st = st;
+        try {
+            for (int64_t it = 0; it < T; ++it) {
+                problem_grad(P, x, 1, gg);
+                system_solve_dev(Sm, gg, step, 1);
+                fixed_step(x, xp, step, mu, beta, d, xn, st);
+                std::swap(xp, x);   // x_prev <- x
+                std::swap(x, xn);   // x <- x_next (xn becomes scratch)
+                CUDA_CHECK(cudaMemcpyAsync(iterates_out + (it + 1) * d, x, (size_t)d * 8, cudaMemcpyDeviceToHost, st));
+            }
+            CUDA_CHECK(cudaStreamSynchronize(st));
+        } catch (...) {
+            Sm->st = sst;
+            cudaEventDestroy(ev);
+            throw;
+        }
+        Sm->st = sst;
+        cudaEventDestroy(ev);
+    });
+}
+
+ihs_status ihs_synth_generate(const ihs_synth_spec* spec, int64_t row0, int64_t rows, double* A, int64_t lda,
+                              double* b, double* x_true) {
+    return guarded([&] {
+        if (!spec) fail(IHS_INVALID_INPUT, "synth: null spec");
+        synth_generate(*spec, row0, rows, A, lda, b, x_true);
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,138 @@
+// vecops.cu — small d-vector kernels of the adaptive loop.
+//
+// Candidate updates follow solver.hpp:182 and :190 coefficient-wise with the
+// same operation tree and no FMA contraction; the decrement dot products
+// (sketched_system.hpp:95-101) use one CTA with a fixed reduction order so
+// repeated solves are bit-identical.
+#include "common.cuh"
+
+namespace ihs_b200 {
+
+namespace {
+__global__ void candidates_kernel(const double* __restrict__ x, const double* __restrict__ xprev,
+                                  const double* __restrict__ gt, double mu_p, double beta_p, double mu_gd, int64_t d,
+                                  double* __restrict__ xp, double* __restrict__ xg) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < d; i += (int64_t)gridDim.x * blockDim.x) {
+        const double xi = x[i], gi = gt[i];
+        if (xp) xp[i] = __dadd_rn(__dsub_rn(xi, __dmul_rn(mu_p, gi)), __dmul_rn(beta_p, __dsub_rn(xi, xprev[i])));
+        if (xg) xg[i] = __dsub_rn(xi, __dmul_rn(mu_gd, gi));
+    }
+}
+
+__global__ void fixed_step_kernel(const double* __restrict__ x, const double* __restrict__ xprev,
+                                  const double* __restrict__ step, double mu, double beta, int64_t d,
+                                  double* __restrict__ xn) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < d; i += (int64_t)gridDim.x * blockDim.x) {
+        const double xi = x[i];
+        xn[i] = __dadd_rn(__dsub_rn(xi, __dmul_rn(mu, step[i])), __dmul_rn(beta, __dsub_rn(xi, xprev[i])));
+    }
+}
+
+__global__ void __launch_bounds__(1024) decrement_dots_kernel(const double* __restrict__ g,
+                                                              const double* __restrict__ gt, int64_t d, int nrhs,
+                                                              double* __restrict__ out) {
+    __shared__ double s1[1024], s2[1024];
+    for (int q = 0; q < nrhs; ++q) {
+        double a = 0.0, c = 0.0;
+        for (int64_t i = threadIdx.x; i < d; i += blockDim.x) {
+            const double gi = g[q * d + i];
+            a = fma(gi, gt[q * d + i], a);
+            c = fma(gi, gi, c);
+        }
+        s1[threadIdx.x] = a;
+        s2[threadIdx.x] = c;
+        __syncthreads();
+        for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+            if ((int)threadIdx.x < w) {
+                s1[threadIdx.x] += s1[threadIdx.x + w];
+                s2[threadIdx.x] += s2[threadIdx.x + w];
+            }
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) {
+            out[2 * q] = s1[0];
+            out[2 * q + 1] = s2[0];
+        }
+        __syncthreads();
+    }
+}
+
+// y[:,q] = A (M x N, lda) x[:,q]
+__global__ void gemv_n_kernel(const double* __restrict__ A, int64_t M, int64_t N, int64_t lda,
+                              const double* __restrict__ x, int nrhs, int64_t ldx, double* __restrict__ y,
+                              int64_t ldy) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < M; i += (int64_t)gridDim.x * blockDim.x) {
+        for (int q = 0; q < nrhs; ++q) {
+            double s = 0.0;
+            for (int64_t j = 0; j < N; ++j) s = fma(A[i + j * lda], x[q * ldx + j], s);
+            y[q * ldy + i] = s;
+        }
+    }
+}
+
+// z[:,q] = (g[:,q] - SA^T w[:,q]) / nu2 ; one warp per column of SA
+__global__ void woodbury_finish_kernel(const double* __restrict__ SA, int64_t m, int64_t d,
+                                       const double* __restrict__ g, const double* __restrict__ w, double nu2,
+                                       int nrhs, double* __restrict__ z) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t j = warp; j < d; j += nwarps) {
+        for (int q = 0; q < nrhs; ++q) {
+            double s = 0.0;
+            for (int64_t i = lane; i < m; i += 32) s = fma(SA[i + j * m], w[q * m + i], s);
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+            if (lane == 0) z[q * d + j] = __ddiv_rn(__dsub_rn(g[q * d + j], s), nu2);
+        }
+    }
+}
+
+__global__ void add_diag_kernel(double* __restrict__ H, int64_t n, double v) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        H[i + i * n] += v;
+}
+
+__global__ void check_finite_kernel(const double* __restrict__ v, int64_t count, int* __restrict__ flag) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
+        if (!isfinite(v[i])) *flag = 1;
+}
+
+int blocks_for(int64_t n, int threads, int cap = 148 * 8) {
+    return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, threads), cap));
+}
+}  // namespace
+
+void candidates(const double* x, const double* xprev, const double* gt, double mu_p, double beta_p, double mu_gd,
+                int64_t d, double* xp, double* xg, cudaStream_t st) {
+    LAUNCH(candidates_kernel, blocks_for(d, 256), 256, 0, st, x, xprev, gt, mu_p, beta_p, mu_gd, d, xp, xg);
+}
+
+void fixed_step(const double* x, const double* xprev, const double* step, double mu, double beta, int64_t d,
+                double* xn, cudaStream_t st) {
+    LAUNCH(fixed_step_kernel, blocks_for(d, 256), 256, 0, st, x, xprev, step, mu, beta, d, xn);
+}
+
+void decrement_dots(const double* g, const double* gt, int64_t d, int nrhs, double* out, cudaStream_t st) {
+    LAUNCH(decrement_dots_kernel, 1, 1024, 0, st, g, gt, d, nrhs, out);
+}
+
+void gemv_n(const double* A, int64_t M, int64_t N, int64_t lda, const double* x, int nrhs, int64_t ldx, double* y,
+            int64_t ldy, cudaStream_t st) {
+    LAUNCH(gemv_n_kernel, blocks_for(M, 128), 128, 0, st, A, M, N, lda, x, nrhs, ldx, y, ldy);
+}
+
+void woodbury_finish(const double* SA, int64_t m, int64_t d, const double* g, const double* w, double nu2, int nrhs,
+                     double* z, cudaStream_t st) {
+    LAUNCH(woodbury_finish_kernel, blocks_for(d * 32, 256), 256, 0, st, SA, m, d, g, w, nu2, nrhs, z);
+}
+
+void add_diag(double* H, int64_t n, double v, cudaStream_t st) {
+    LAUNCH(add_diag_kernel, blocks_for(n, 256), 256, 0, st, H, n, v);
+}
+
+void check_finite(const double* v, int64_t count, int* d_flag, cudaStream_t st) {
+    LAUNCH(check_finite_kernel, blocks_for(count, 256), 256, 0, st, v, count, d_flag);
+}
+
+}  // namespace ihs_b200

@@ -1,0 +1,36 @@
+import os
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA device (B200); runs through libihs_b200.so")
+    config.addinivalue_line("markers", "slow: larger parity cases")
+
+
+@pytest.fixture(scope="session")
+def O():
+    from oracle import oracle
+
+    oracle.build()
+    return oracle
+
+
+@pytest.fixture(scope="session")
+def ihs():
+    from paper_2006_05874_b200 import ihs as m
+
+    return m
+
+
+@pytest.fixture(scope="session")
+def gpu(ihs):
+    # GPU tests fail loudly (no skip) when the device path is unavailable.
+    n = ihs.device_count()
+    assert n >= 1, "no CUDA device visible to libihs_b200.so"
+    return ihs

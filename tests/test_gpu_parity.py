@@ -1,0 +1,279 @@
+"""GPU parity: the CUDA path through the C-ABI against the CPU oracle.
+
+Bit-exact for the integer/stream parts (mt19937_64 draws, Rademacher bits,
+sample indices, SRHT SA values, FWHT); fp64 tolerance (stated per test) for
+the Eigen-replaced linear algebra (Gaussian S*A, gradient, LLT solves).
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+RNG = np.random.default_rng
+
+
+def rand_mat(seed, n, d):
+    return np.asfortranarray(RNG(seed).standard_normal((n, d)))
+
+
+# ----------------------------------------------------------------- rng.hpp
+def test_mt19937_64_known_answer(gpu):
+    # C++ standard [rand.predef]: the 10000th draw of default mt19937_64 (seed 5489)
+    raw = gpu.mt19937_64(5489, 10000)
+    assert int(raw[-1]) == 9981545732273789042
+
+
+@pytest.mark.parametrize("seed", [0, 1, 12345678901234567])
+def test_mt19937_64_stream(gpu, O, seed):
+    s = O.derive_seed(seed, 1)
+    assert np.array_equal(gpu.mt19937_64(s, 5000), O.mt_raw(s, 5000))
+
+
+@pytest.mark.parametrize("n", [1, 31, 32, 33, 311, 312, 313, 9984, 9985, 20000, 1 << 17])
+def test_rademacher_bits(gpu, O, n):
+    s = O.derive_seed(O.derive_seed(3, 5), 1)
+    assert np.array_equal(gpu.rademacher(s, n), O.rademacher(s, n))
+
+
+@pytest.mark.parametrize("rows,cols", [(1, 1), (3, 7), (64, 33), (1000, 17)])
+def test_fill_gaussian_small(gpu, O, rows, cols):
+    s = O.derive_seed(11, 0)
+    a = gpu.fill_gaussian(s, rows, cols, 0.25)
+    b = O.fill_gaussian(s, rows, cols, 0.25)
+    # acceptance is exact; values may differ from glibc's log by a last-ulp rounding
+    np.testing.assert_allclose(a, b, rtol=1e-15, atol=0)
+
+
+def test_fill_gaussian_jump_ahead(gpu, O):
+    # long enough to use several jump-ahead substreams (stride 2^19 draws)
+    s = O.derive_seed(2024, 0)
+    rows, cols = 1024, 1200
+    a = gpu.fill_gaussian(s, rows, cols, 1.0 / 32.0)
+    b = O.fill_gaussian(s, rows, cols, 1.0 / 32.0)
+    # positions are exact (acceptance uses no log); a last-ulp log difference from
+    # glibc can move a value by <= 2 ulp through sqrt/div/mul
+    np.testing.assert_allclose(a, b, rtol=1e-15, atol=0)
+    assert np.mean(a == b) > 0.9999
+
+
+# ----------------------------------------------------------------- sketch.hpp
+@pytest.mark.parametrize("n", [1, 2, 4, 16, 64, 1024, 8192, 1 << 14, 1 << 16])
+def test_fwht_bit_exact(gpu, O, n):
+    v = RNG(n).standard_normal(n)
+    a = gpu.fwht_inplace(v.copy())
+    b = O.fwht_inplace(v)
+    assert np.array_equal(a, b)
+
+
+def test_fwht_known_answer(gpu):
+    v = np.array([1.0, 0.0, 0.0, 0.0])
+    gpu.fwht_inplace(v)
+    assert np.all(v == 0.5)  # test_sketch.cpp:13-17
+
+
+def test_fwht_rejects_non_pow2(gpu):
+    with pytest.raises(gpu.InvalidInput):
+        gpu.fwht_inplace(np.zeros(12))
+
+
+@pytest.mark.parametrize("n,d,m,seed", [
+    (12, 4, 8, 77), (1000, 2, 16, 0), (8192, 16, 100, 5), (8192, 8, 8192, 1), (5000, 7, 333, 2),
+    (20000, 5, 1000, 3), (1 << 15, 4, 4096, 4), (100000, 3, 20000, 9), ((1 << 20) - 17, 2, 5000, 6)])
+def test_srht_sketch_bit_exact(gpu, O, n, d, m, seed):
+    A = rand_mat(n + d, n, d)
+    c_gpu = gpu.CostCounters()
+    SA = gpu.srht_sketch(A, m, seed, c_gpu)
+    c_or = O.abi.Counters()
+    SA_ref = O.srht_sketch(A, m, seed, c_or)
+    assert np.array_equal(SA, SA_ref)
+    assert c_gpu.sketch == c_or.sketch
+
+
+def test_srht_sketch_too_large(gpu):
+    with pytest.raises(gpu.SketchTooLarge):
+        gpu.srht_sketch(np.zeros((12, 2)), 17, 0)
+    gpu.srht_sketch(np.zeros((12, 2)), 16, 0)
+
+
+def test_srht_counter_formula(gpu):
+    c16, c256 = gpu.CostCounters(), gpu.CostCounters()
+    gpu.srht_sketch(np.zeros((1000, 2)), 16, 0, c16)
+    gpu.srht_sketch(np.zeros((1000, 2)), 256, 0, c256)
+    fw = 2 * 1024 * 10
+    assert c16.sketch == fw + 2 * 1000 + 2 * 16  # test_sketch.cpp:119-126
+    assert c256.sketch == fw + 2 * 1000 + 2 * 256
+
+
+@pytest.mark.parametrize("n,d,m,seed", [(10, 3, 4, 7), (12, 5, 6, 123), (500, 17, 33, 1), (4096, 64, 256, 2),
+                                        (20000, 40, 130, 3)])
+def test_gaussian_sketch(gpu, O, n, d, m, seed):
+    A = rand_mat(seed, n, d)
+    c = gpu.CostCounters()
+    SA = gpu.gaussian_sketch(A, m, seed, c)
+    SA_ref = O.gaussian_sketch(A, m, seed)
+    # Eigen GEMM vs DMMA GEMM: different summation order (sketch.hpp:68)
+    scale = np.abs(SA_ref).max() + 1e-300
+    assert np.max(np.abs(SA - SA_ref)) <= 1e-13 * scale * np.sqrt(n)
+    assert c.sketch == m * n * d
+
+
+def test_gaussian_sketch_deterministic(gpu):
+    A = rand_mat(4, 12, 5)
+    s1 = gpu.gaussian_sketch(A, 6, 123)
+    s2 = gpu.gaussian_sketch(A, 6, 123)
+    assert np.array_equal(s1, s2)
+    assert np.linalg.norm(s1 - gpu.gaussian_sketch(A, 6, 124)) > 0
+
+
+# ----------------------------------------------------------------- problem / system
+def test_gradient_known_answer(gpu):
+    p = gpu.ProblemInstance(np.eye(2), [1.0, 2.0], 1.0)
+    g = gpu.gradient(p, [1.0, 1.0])
+    np.testing.assert_allclose(g, [1.0, 0.0], atol=1e-15)  # test_problem.cpp:61-65
+    c = gpu.CostCounters()
+    gpu.gradient(p, [0.0, 0.0], c)
+    assert c.matvec == 2 * 2 * 2 + 2 + 2 * 2  # test_problem.cpp:74-78
+
+
+@pytest.mark.parametrize("n,d", [(100, 3), (4096, 64), (65536 + 7, 130), (20000, 1000)])
+def test_gradient_vs_oracle(gpu, O, n, d):
+    A = rand_mat(n, n, d)
+    b = RNG(1).standard_normal(n)
+    x = RNG(2).standard_normal(d)
+    p = gpu.ProblemInstance(A, b, 0.3)
+    g = gpu.gradient(p, x)
+    g_ref = O.gradient(A, b, 0.3, x)
+    assert np.linalg.norm(g - g_ref) <= 1e-12 * (np.linalg.norm(g_ref) + np.linalg.norm(A) * np.linalg.norm(b))
+
+
+def test_system_known_answers(gpu):
+    sys = gpu.SketchedSystem.factorize(np.zeros((3, 4)), 2.0)
+    g = np.array([4.0, -8.0, 0.0, 2.0])
+    np.testing.assert_allclose(sys.solve(g), g / 4.0, atol=1e-14)  # test_sketched_system.cpp:22-26
+    SA = np.array([[1.0, 0.0, 0.0]])
+    sys = gpu.SketchedSystem.factorize(SA, 1.0)
+    assert sys.kind() == gpu.FactorKind.WoodburyInner
+    np.testing.assert_allclose(sys.solve(np.ones(3)), [0.5, 1.0, 1.0], rtol=1e-14)
+
+
+@pytest.mark.parametrize("m,d", [(4, 6), (9, 5), (6, 20), (20, 6), (8, 8), (300, 257), (100, 513), (2000, 700)])
+def test_system_solve_vs_oracle(gpu, O, m, d):
+    SA = rand_mat(m * d, m, d)
+    g = RNG(m + d).standard_normal(d)
+    nu = 0.7
+    sys = gpu.SketchedSystem.factorize(SA, nu)
+    assert sys.kind() == (gpu.FactorKind.WoodburyInner if m < d else gpu.FactorKind.DirectGram)
+    z = sys.solve(g)
+    H = SA.T @ SA + nu * nu * np.eye(d)
+    assert np.linalg.norm(H @ z - g) <= 1e-9 * np.linalg.norm(g) * max(1.0, np.linalg.norm(H, 2) / 10)
+    z_ref, kind, ff, fps = O.system_solve(SA, nu, g)
+    assert kind == int(sys.kind())
+    assert ff == sys.factor_flops() and fps == sys.flops_per_solve()
+    assert np.linalg.norm(z - z_ref) <= 1e-10 * np.linalg.norm(z_ref) * max(1.0, np.linalg.cond(H) / 1e3)
+
+
+def test_system_rejects(gpu):
+    SA = np.zeros((2, 3))
+    SA[1, 1] = np.inf
+    with pytest.raises(gpu.InvalidInput):
+        gpu.SketchedSystem.factorize(SA, 1.0)
+    with pytest.raises(gpu.InvalidInput):
+        gpu.SketchedSystem.factorize(np.zeros((2, 3)), 0.0)
+
+
+def test_solve_counters(gpu):
+    SA = rand_mat(23, 8, 32)
+    c = gpu.CostCounters()
+    sys = gpu.SketchedSystem.factorize(SA, 1.0, c)
+    assert c.factor == 8 * 8 * 32 + 8 * 8 * 8 // 3  # test_sketched_system.cpp:142-150
+    sys.solve(np.zeros(32), c)
+    assert c.solve == 2 * 8 * 32 + 8 * 8 + 2 * 32
+
+
+# ----------------------------------------------------------------- adaptive solve
+def _cfg_pair(gpu, O, **kw):
+    cfg = gpu.SolverConfig(**kw)
+    c_or = O.default_config(rho=cfg.rho, eta=cfg.eta, sketch_kind=int(cfg.sketch_kind), mode=int(cfg.mode),
+                            m_initial=cfg.m_initial, eps=cfg.eps, max_iters=cfg.max_iters,
+                            max_sketch=cfg.max_sketch or 0, seed=cfg.seed,
+                            enforce_validity=int(cfg.enforce_validity))
+    return cfg, c_or
+
+
+def _abar_rel(A, nu, x, x_ref):
+    Ad = np.concatenate([A @ (x - x_ref), nu * (x - x_ref)])
+    Ar = np.concatenate([A @ x_ref, nu * x_ref])
+    return np.linalg.norm(Ad) / np.linalg.norm(Ar)
+
+
+@pytest.mark.parametrize("kind,mode,seed", [("SRHT", "GradientOnly", 0), ("SRHT", "PolyakThenGradient", 1),
+                                            ("Gaussian", "PolyakThenGradient", 2), ("Gaussian", "GradientOnly", 3)])
+def test_adaptive_solve_matches_oracle(gpu, O, kind, mode, seed):
+    A, b, _ = O.synth(2048, 64, decay=0.95, noise_std=0.01, data_seed=seed)
+    nu = 1e-2
+    cfg, c_or = _cfg_pair(gpu, O, sketch_kind=getattr(gpu.SketchKind, kind), mode=getattr(gpu.SolveMode, mode),
+                          seed=seed)
+    p = gpu.ProblemInstance(A, b, nu)
+    rep = gpu.adaptive_solve(p, cfg)
+    x_ref, rep_ref, log_ref, _ = O.adaptive_solve(A, b, nu, c_or)
+    assert rep.converged and rep_ref.converged
+    # identical m-schedule and branch sequence
+    assert rep.rejections == rep_ref.rejections and rep.final_m == rep_ref.final_m
+    assert rep.iterations == rep_ref.iterations
+    assert [(e.t, e.m, int(e.branch)) for e in rep.log] == [(l[0], l[1], l[4]) for l in log_ref]
+    # counters are closed forms of the same evaluations
+    assert rep.counters.sketch == rep_ref.counters.sketch
+    assert rep.counters.factor == rep_ref.counters.factor
+    assert rep.counters.solve == rep_ref.counters.solve
+    assert rep.counters.matvec == rep_ref.counters.matvec
+    assert _abar_rel(A, nu, rep.x, x_ref) <= 1e-10
+
+
+def test_adaptive_solve_deterministic(gpu, O):
+    A, b, _ = O.synth(1024, 32, decay=0.95, data_seed=9)
+    p = gpu.ProblemInstance(A, b, 0.2)
+    cfg = gpu.SolverConfig(rho=0.15, seed=7)
+    a = gpu.adaptive_solve(p, cfg)
+    c = gpu.adaptive_solve(p, cfg)
+    assert a.iterations == c.iterations and a.rejections == c.rejections
+    assert np.array_equal(a.x, c.x)
+    assert [e.r for e in a.log] == [e.r for e in c.log]
+
+
+def test_adaptive_solve_zero_rhs(gpu):
+    A = rand_mat(52, 10, 3)
+    p = gpu.ProblemInstance(A, np.zeros(10), 1.0)
+    rep = gpu.adaptive_solve(p, gpu.SolverConfig(sketch_kind=gpu.SketchKind.Gaussian, rho=0.1))
+    assert rep.converged and rep.iterations == 1 and rep.r1 == 0.0 and np.linalg.norm(rep.x) == 0.0
+
+
+def test_adaptive_solve_validates(gpu):
+    A = rand_mat(53, 6, 3)
+    p = gpu.ProblemInstance(A, RNG(1).standard_normal(6), 1.0)
+    with pytest.raises(gpu.InvalidInput):
+        gpu.adaptive_solve(p, gpu.SolverConfig(eps=0.0))
+    with pytest.raises(gpu.OutOfValidityRange):
+        gpu.adaptive_solve(p, gpu.SolverConfig(rho=0.5))
+    gpu.adaptive_solve(p, gpu.SolverConfig(rho=0.5, enforce_validity=False))
+
+
+def test_sketch_exhaustion_flagged(gpu, O):
+    A = rand_mat(54, 4, 2)
+    b = RNG(54).standard_normal(4)
+    p = gpu.ProblemInstance(A, b, 0.5)
+    cfg = gpu.SolverConfig(tuning_override=gpu.rates_from_bounds(1.0, 1.0), eps=1e-12, max_iters=40)
+    rep = gpu.adaptive_solve(p, cfg)
+    assert rep.sketch_exhausted and rep.final_m <= 4
+
+
+def test_fixed_sketch_ihs_matches_oracle(gpu, O):
+    A, b, _ = O.synth(4096, 32, decay=0.95, data_seed=4)
+    nu = 0.05
+    SA = O.gaussian_sketch(A, 128, 5)
+    tp = gpu.rates_from_bounds(*gpu.gaussian_targets(0.3, 0.01, False))
+    p = gpu.ProblemInstance(A, b, nu)
+    sys = gpu.SketchedSystem.factorize(SA, nu)
+    its = gpu.fixed_sketch_ihs(p, sys, tp, 25, gpu.FixedMode.Polyak)
+    ref = O.fixed_sketch_ihs(A, b, nu, SA, O.abi.Tuning(**tp.__dict__), 25, 1)
+    for k in range(26):
+        assert _abar_rel(A, nu, its[k], ref[k]) <= 1e-9 or np.linalg.norm(ref[k]) == 0
