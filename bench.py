@@ -123,6 +123,14 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows)}
 
 
+class _Null:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
+
+
 # --------------------------------------------------------------------- reference arm
 def run_reference(args, c, rank, world):
     from oracle import oracle as O
@@ -162,6 +170,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-clocks", action="store_true", help="do not sample nvidia-smi during the timed steps")
     ap.add_argument("--out", default=None, help="also write the JSON line here")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -217,7 +226,9 @@ def main():
     step_ms, lib_ms, reps = [], [], []
     clk = ClockSampler(local, ROOT / "gpurun_out" / f"clocks_rank{rank}.csv") if (ROOT / "gpurun_out").exists() \
         else ClockSampler(local, pathlib.Path(f"/tmp/clocks_rank{rank}.csv"))
-    with clk:
+    if args.no_clocks:
+        clk.__enter__ = lambda: clk  # noqa: E731
+    with (clk if not args.no_clocks else _Null()):
         for _ in range(args.steps):
             flush.zero_()  # L2 flush between timed iterations (outside the timed bracket)
             torch.cuda.synchronize()

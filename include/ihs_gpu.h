@@ -115,6 +115,8 @@ typedef struct ihs_phase_times {
     double gradient_bytes; /* algorithmic HBM bytes of all gradient passes (8nd + 8n each) */
     double sketch_bytes;   /* algorithmic bytes of the SRHT sketches (8nd + 8md each) */
     double sketch_flops;   /* algorithmic flops of the Gaussian sketches (2mnd each) */
+    double alloc_ms;       /* host time spent growing device buffers */
+    double host_rng_ms;    /* host time drawing the SRHT row samples (Fisher-Yates) */
 } ihs_phase_times;
 
 /* SolveReport (solver.hpp:70-87). Arrays are caller-allocated; *_size is the

@@ -5,10 +5,13 @@
 // throws NumericalBreakdown when it fails (:82-83); solve (:40-49) applies
 // llt.solve. Here: right-looking blocked LLT (NB = 64): a one-CTA panel
 // factorization in shared memory, a row-parallel TRSM for the panel below,
-// and the trailing update on the DMMA GEMM (gemm_f64.cu). The strict upper
-// triangle is then overwritten with L^T so both triangular sweeps of a solve
-// read their operand coalesced. A non-positive or non-finite pivot sets
-// *info = column+1 (the caller raises NumericalBreakdown).
+// and the trailing update on the DMMA GEMM (gemm_f64.cu). A non-positive or
+// non-finite pivot sets *info = column+1 (the caller raises
+// NumericalBreakdown). The factor is then inverted once per sketch
+// (recursive 2x2 blocking, DMMA GEMMs) into W = L^{-1} with W^T mirrored into
+// the strict upper triangle, so every solve of the adaptive loop is two
+// fully parallel, coalesced triangular mat-vecs instead of a latency-bound
+// substitution.
 #include "common.cuh"
 
 namespace ihs_b200 {
@@ -104,72 +107,142 @@ __global__ void mirror_upper_kernel(double* __restrict__ H, int64_t n) {
     }
 }
 
-// Triangular solves with the mirrored factor, single CTA, nrhs in {1, 2}.
-// Forward: L y = r ; backward: L^T z = y, blocked by 32 (warp-sized diagonal solves).
-__global__ void __launch_bounds__(512) chol_solve_kernel(const double* __restrict__ Lf, int64_t n,
-                                                         double* __restrict__ R, int nrhs) {
-    extern __shared__ double v[];  // nrhs * n
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    for (int64_t e = tid; e < n * nrhs; e += blockDim.x) v[e] = R[e];
+// Inverse of each 64x64 lower-triangular diagonal block: W_bb = L_bb^{-1}.
+// One CTA per block, one thread per column of the inverse.
+__global__ void __launch_bounds__(64) tri_inv_diag_kernel(const double* __restrict__ L, int64_t n,
+                                                          double* __restrict__ W) {
+    extern __shared__ double tri_smem[];
+    double(*l)[NB + 1] = reinterpret_cast<double(*)[NB + 1]>(tri_smem);
+    double(*x)[NB + 1] = reinterpret_cast<double(*)[NB + 1]>(tri_smem + NB * (NB + 1));
+    const int64_t k = (int64_t)blockIdx.x * NB;
+    const int nb = (int)imin64(NB, n - k);
+    for (int e = threadIdx.x; e < NB * NB; e += blockDim.x) {
+        const int i = e % NB, j = e / NB;
+        l[i][j] = (i < nb && j < nb && i >= j) ? L[(k + i) + (k + j) * n] : 0.0;
+    }
     __syncthreads();
-    // forward
-    for (int64_t kb = 0; kb < n; kb += 32) {
-        const int bs = (int)imin64(32, n - kb);
-        if (warp < nrhs) {
-            double* y = v + (int64_t)warp * n;
-            double r = (lane < bs) ? y[kb + lane] : 0.0;
-            for (int c = 0; c < bs; ++c) {
-                double yc = 0.0;
-                if (lane == c) yc = r / Lf[(kb + c) + (kb + c) * n];
-                yc = __shfl_sync(0xffffffffu, yc, c);
-                if (lane > c && lane < bs) r -= Lf[(kb + lane) + (kb + c) * n] * yc;
-                if (lane == c) r = yc;
-            }
-            if (lane < bs) y[kb + lane] = r;
+    const int c = threadIdx.x;  // column of the inverse
+    if (c < nb) {
+        for (int i = 0; i < nb; ++i) {
+            double s = (i == c) ? 1.0 : 0.0;
+            for (int q = c; q < i; ++q) s -= l[i][q] * x[q][c];
+            x[i][c] = (i < c) ? 0.0 : s / l[i][i];
         }
-        __syncthreads();
-        for (int64_t i = kb + bs + tid; i < n; i += blockDim.x) {
-            for (int q = 0; q < nrhs; ++q) {
-                double* y = v + (int64_t)q * n;
-                double s = 0.0;
-                for (int c = 0; c < bs; ++c) s += Lf[i + (kb + c) * n] * y[kb + c];
-                y[i] -= s;
-            }
-        }
-        __syncthreads();
     }
-    // backward with U = L^T stored in the strict upper triangle (diag from L)
-    const int64_t nblk = (n + 31) / 32;
-    for (int64_t b = nblk - 1; b >= 0; --b) {
-        const int64_t kb = b * 32;
-        const int bs = (int)imin64(32, n - kb);
-        if (warp < nrhs) {
-            double* y = v + (int64_t)warp * n;
-            double r = (lane < bs) ? y[kb + lane] : 0.0;
-            for (int c = bs - 1; c >= 0; --c) {
-                double zc = 0.0;
-                if (lane == c) zc = r / Lf[(kb + c) + (kb + c) * n];
-                zc = __shfl_sync(0xffffffffu, zc, c);
-                // U[kb+lane, kb+c] for lane < c lives in the upper triangle
-                if (lane < c) r -= Lf[(kb + lane) + (kb + c) * n] * zc;
-                if (lane == c) r = zc;
-            }
-            if (lane < bs) y[kb + lane] = r;
-        }
-        __syncthreads();
-        for (int64_t i = tid; i < kb; i += blockDim.x) {
-            for (int q = 0; q < nrhs; ++q) {
-                double* y = v + (int64_t)q * n;
-                double s = 0.0;
-                for (int c = 0; c < bs; ++c) s += Lf[i + (kb + c) * n] * y[kb + c];
-                y[i] -= s;
-            }
-        }
-        __syncthreads();
+    __syncthreads();
+    for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) {
+        const int i = e % nb, j = e / nb;
+        if (i >= j) W[(k + i) + (k + j) * n] = x[i][j];
     }
-    for (int64_t e = tid; e < n * nrhs; e += blockDim.x) R[e] = v[e];
+}
+
+// y[:, q] (+)= T x[:, q] for a triangular T stored in Wf: lower (W) when
+// lower != 0, else upper (W^T mirrored into the strict upper triangle, with
+// the diagonal of W). CTA tile: 64 rows x 512 columns; partials per column
+// chunk go to part[chunk][q][row] and are summed in fixed order afterwards.
+constexpr int TR_ROWS = 64, TR_COLS = 512;
+__global__ void __launch_bounds__(256) trmv_partial_kernel(const double* __restrict__ Wf, int64_t n, int lower,
+                                                           const double* __restrict__ x, int nrhs,
+                                                           double* __restrict__ part) {
+    const int64_t r0 = (int64_t)blockIdx.x * TR_ROWS;
+    const int64_t c0 = (int64_t)blockIdx.y * TR_COLS;
+    const int64_t c1 = imin64(n, c0 + TR_COLS);
+    __shared__ double xs[2][TR_COLS];
+    __shared__ double red[4][2][TR_ROWS];
+    const bool skip = lower ? (c0 > r0 + TR_ROWS - 1) : (c1 - 1 < r0);
+    const int r = threadIdx.x % TR_ROWS, qg = threadIdx.x / TR_ROWS;  // 4 column interleaves
+    const int64_t row = r0 + r;
+    double acc[2] = {0.0, 0.0};
+    if (!skip) {
+        for (int e = threadIdx.x; e < (int)(c1 - c0); e += blockDim.x)
+            for (int q = 0; q < nrhs; ++q) xs[q][e] = x[q * n + c0 + e];
+        __syncthreads();
+        if (row < n) {
+            int64_t jb = c0 + qg, je = c1;
+            if (lower) je = imin64(je, row + 1);        // j <= row
+            else if (jb < row) jb += ((row - jb + 3) / 4) * 4;  // j >= row, same interleave class
+            for (int64_t j = jb; j < je; j += 4) {
+                const double w = Wf[row + j * n];
+                acc[0] = fma(w, xs[0][j - c0], acc[0]);
+                if (nrhs > 1) acc[1] = fma(w, xs[1][j - c0], acc[1]);
+            }
+        }
+    }
+    red[qg][0][r] = acc[0];
+    red[qg][1][r] = acc[1];
+    __syncthreads();
+    if (threadIdx.x < TR_ROWS && row < n) {
+        for (int q = 0; q < nrhs; ++q)
+            part[((int64_t)blockIdx.y * nrhs + q) * n + row] =
+                (red[0][q][r] + red[1][q][r]) + (red[2][q][r] + red[3][q][r]);
+    }
+}
+
+__global__ void trmv_reduce_kernel(const double* __restrict__ part, int64_t n, int nrhs, int nchunks, int lower,
+                                   double* __restrict__ y) {
+    const int64_t total = (int64_t)nrhs * n;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t q = e / n, row = e % n;
+        // chunks that touch this row: lower -> chunks with c0 <= row, upper -> c1 > row
+        double s = 0.0;
+        for (int c = 0; c < nchunks; ++c) {
+            const int64_t c0 = (int64_t)c * TR_COLS, c1 = imin64(n, c0 + TR_COLS);
+            const int64_t r0 = (row / TR_ROWS) * TR_ROWS;
+            const bool skip = lower ? (c0 > r0 + TR_ROWS - 1) : (c1 - 1 < r0);
+            if (!skip) s += part[((int64_t)c * nrhs + q) * n + row];
+        }
+        y[e] = s;
+    }
+}
+
+void trmv(const double* Wf, int64_t n, bool lower, const double* x, int nrhs, double* y, double* part, cudaStream_t st) {
+    dim3 grid((unsigned)ceil_div(n, TR_ROWS), (unsigned)ceil_div(n, TR_COLS));
+    LAUNCH(trmv_partial_kernel, grid, 256, 0, st, Wf, n, (int)lower, x, nrhs, part);
+    const int64_t total = (int64_t)nrhs * n;
+    LAUNCH(trmv_reduce_kernel, (unsigned)std::min<int64_t>(ceil_div(total, 256), 1024), 256, 0, st, part, n, nrhs,
+           (int)grid.y, (int)lower, y);
+}
+
+// W[n0:n0+size, n0:n0+size] <- L^{-1} of the same diagonal block (lower), with
+// the diagonal 64-blocks already inverted and the strict upper part zero.
+void tri_inv_rec(const double* L, double* W, int64_t n, int64_t n0, int64_t size, double* tmp, cudaStream_t st) {
+    if (size <= NB) return;
+    const int64_t h = ((size / 2 + NB - 1) / NB) * NB;  // split on a block boundary
+    tri_inv_rec(L, W, n, n0, h, tmp, st);
+    tri_inv_rec(L, W, n, n0 + h, size - h, tmp, st);
+    const int64_t m2 = size - h;
+    // tmp (m2 x h, ld m2) = L21 * W11
+    dgemm(false, false, m2, h, h, 1.0, L + (n0 + h) + n0 * n, n, W + n0 + n0 * n, n, 0.0, tmp, m2, false, 1, nullptr,
+          st);
+    // W21 = -W22 * tmp
+    dgemm(false, false, m2, h, m2, -1.0, W + (n0 + h) + (n0 + h) * n, n, tmp, m2, 0.0, W + (n0 + h) + n0 * n, n, false,
+          1, nullptr, st);
 }
 }  // namespace
+
+void cholesky_invert(const double* d_L, int64_t n, double* d_W, double* d_tmp, cudaStream_t st) {
+    CUDA_CHECK(cudaMemsetAsync(d_W, 0, (size_t)n * n * sizeof(double), st));
+    const size_t smem = (size_t)2 * NB * (NB + 1) * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+        CUDA_CHECK(cudaFuncSetAttribute(tri_inv_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    LAUNCH(tri_inv_diag_kernel, (unsigned)ceil_div(n, NB), 64, smem, st, d_L, n, d_W);
+    tri_inv_rec(d_L, d_W, n, 0, n, d_tmp, st);
+    dim3 grid((unsigned)ceil_div(n, 32), (unsigned)ceil_div(n, 32));
+    LAUNCH(mirror_upper_kernel, grid, dim3(32, 8), 0, st, d_W, n);
+}
+
+size_t cholesky_solve_work_doubles(int64_t n) { return (size_t)ceil_div(n, TR_COLS) * 2 * n + 2 * n; }
+
+void cholesky_solve_inv(const double* d_W, int64_t n, const double* d_R, double* d_Z, int nrhs, double* d_work,
+                        cudaStream_t st) {
+    double* part = d_work;
+    double* y = d_work + (size_t)ceil_div(n, TR_COLS) * 2 * n;
+    trmv(d_W, n, true, d_R, nrhs, y, part, st);    // y = L^{-1} r
+    trmv(d_W, n, false, y, nrhs, d_Z, part, st);   // z = L^{-T} y
+}
 
 void cholesky_factor(double* d_H, int64_t n, double* d_work, int* d_info, int num_sms, cudaStream_t st) {
     (void)d_work;
@@ -187,19 +260,6 @@ void cholesky_factor(double* d_H, int64_t n, double* d_work, int* d_info, int nu
             dgemm(false, true, rest, rest, nb, -1.0, L21, n, L21, n, 1.0, A22, n, true, 1, nullptr, st);
         }
     }
-    dim3 grid((unsigned)ceil_div(n, 32), (unsigned)ceil_div(n, 32));
-    LAUNCH(mirror_upper_kernel, grid, dim3(32, 8), 0, st, d_H, n);
-}
-
-void cholesky_solve(const double* d_L, int64_t n, double* d_R, int nrhs, cudaStream_t st) {
-    const size_t smem = (size_t)n * nrhs * sizeof(double);
-    static bool attr = false;
-    if (!attr) {
-        CUDA_CHECK(cudaFuncSetAttribute(chol_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        attr = true;
-    }
-    if (smem > 200 * 1024) fail(IHS_INVALID_INPUT, "cholesky_solve: system too large for the single-CTA solver");
-    LAUNCH(chol_solve_kernel, 1, 512, smem, st, d_L, n, d_R, nrhs);
 }
 
 }  // namespace ihs_b200

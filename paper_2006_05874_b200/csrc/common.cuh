@@ -47,8 +47,10 @@ struct MTState { uint64_t mt[312]; };
 void mt_seed_host(uint64_t seed, MTState& s);  // std::mt19937_64(seed) initial array
 // raw draws [0, count) of mt19937_64(seed) (sequential single-CTA generator)
 void mt_generate_raw(uint64_t seed, int64_t count, uint64_t* d_out, cudaStream_t st);
-// rademacher sign bits: bit i = (draw_i & 1), 32-bit words LSB first
-void mt_rademacher_bits(uint64_t seed, int64_t n, uint32_t* d_bits, cudaStream_t st);
+// rademacher sign bits: bit i = (draw_i & 1), 32-bit words LSB first; long
+// vectors run as jump-ahead substreams (d_scratch: rademacher_scratch_bytes(n))
+size_t rademacher_scratch_bytes(int64_t n);
+void mt_rademacher_bits(uint64_t seed, int64_t n, uint32_t* d_bits, void* d_scratch, cudaStream_t st);
 // fill_gaussian of a (rows*cols) column-major block with stddev, exact stream
 // order (polar method with cached second value); d_scratch sized by
 // gaussian_scratch_bytes(count).
@@ -60,6 +62,8 @@ void mt_fill_gaussian(uint64_t seed, int64_t count, double stddev, double* d_out
 struct SrhtPlan {
     int64_t n, d, lda, n_pad, m;
     int logn, L, H;          // n_pad = 2^logn, low bits L done in phase 1, H = logn - L
+    int npass;               // phase-2 passes over the H high bits (<= 10 bits each)
+    int pass_lo[3], pass_hb[3];
     double scale1, scale2;   // 1/sqrt(n_pad), sqrt(n_pad/m) (host-computed, :47 and :95)
 };
 SrhtPlan srht_plan(int64_t n, int64_t d, int64_t lda, int64_t m);
@@ -81,11 +85,15 @@ void dgemm(bool transA, bool transB, int64_t M, int64_t N, int64_t K, double alp
            double* d_work, cudaStream_t st);
 int dgemm_pick_splitk(int64_t M, int64_t N, int64_t K, int num_sms);
 
-// chol.cu — blocked Cholesky (lower) with the upper triangle mirrored to L^T,
-// and the two triangular solves. d_info: int (0 ok, j+1 = failed pivot).
+// chol.cu — blocked Cholesky (lower, in place). d_info: int (0 ok, j+1 = failed pivot).
 void cholesky_factor(double* d_H, int64_t n, double* d_work, int* d_info, int num_sms, cudaStream_t st);
-// solve L L^T Z = R for nrhs columns (ld = n) in place
-void cholesky_solve(const double* d_L, int64_t n, double* d_R, int nrhs, cudaStream_t st);
+// W = L^{-1} (lower) with W^T mirrored into the strict upper triangle;
+// d_tmp holds ceil(n/2)^2 doubles.
+void cholesky_invert(const double* d_L, int64_t n, double* d_W, double* d_tmp, cudaStream_t st);
+size_t cholesky_solve_work_doubles(int64_t n);
+// Z = L^{-T} L^{-1} R for nrhs columns (ld = n), two parallel triangular mat-vecs
+void cholesky_solve_inv(const double* d_W, int64_t n, const double* d_R, double* d_Z, int nrhs, double* d_work,
+                        cudaStream_t st);
 
 // gradient.cu — fused g = A^T(Ax - b) + nu^2 x for 1 or 2 right-hand sides
 struct GradPlan {
@@ -93,6 +101,7 @@ struct GradPlan {
     int R;          // rows per panel
     int grid;       // persistent CTAs
     size_t smem;
+    int version;    // 2: smem-resident double-buffered panels; 1: L2 re-read (large d)
 };
 GradPlan grad_plan(int64_t n, int64_t d, int64_t lda, int num_sms);
 size_t grad_work_doubles(const GradPlan& p);

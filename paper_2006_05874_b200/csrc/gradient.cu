@@ -119,14 +119,168 @@ grad_partial_kernel(const double* __restrict__ A, int64_t n, int64_t d, int64_t 
     for (int64_t e = t; e < NRHS * d; e += THREADS) work[(int64_t)blockIdx.x * NRHS * d + e] = gp[e];
 }
 
+// ---------------------------------------------------------------- v2
+// A is read exactly once: R x d row panels are streamed into shared memory
+// with 8-byte cp.async (odd padded column stride R+1: conflict-free for both
+// sweeps) and double buffered, so the next panel's HBM traffic overlaps both
+// sweeps of the current one. Column partials live in registers.
+constexpr int T2 = 512;
+constexpr int W2 = T2 / 32;
+
+__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(src));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+template <int NRHS, int RR, int MAXC>
+__global__ void __launch_bounds__(T2, 1)
+grad_smem_kernel(const double* __restrict__ A, int64_t d, int64_t lda, const double* __restrict__ b,
+                 const double* __restrict__ X, double* __restrict__ work) {
+    extern __shared__ double sm[];
+    const int64_t stage = d * (RR + 1);
+    double* panel = sm;                       // 2 stages
+    double* xs = panel + 2 * stage;           // NRHS * d
+    double* red = xs + NRHS * d;              // W2 * NRHS * RR
+    double* rv = red + W2 * NRHS * RR;        // NRHS * RR
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    for (int64_t e = t; e < NRHS * d; e += T2) xs[e] = X[e];
+
+    double gacc[NRHS][MAXC];
+#pragma unroll
+    for (int q = 0; q < NRHS; ++q)
+#pragma unroll
+        for (int c = 0; c < MAXC; ++c) gacc[q][c] = 0.0;
+
+    const int64_t npanels = lda / RR;
+    const int64_t elems = (int64_t)RR * d;
+    auto issue = [&](int64_t p, int s) {
+        double* dst = panel + s * stage;
+        const double* src = A + p * RR;
+        for (int64_t e = t; e < elems; e += T2) {
+            const int i = (int)(e % RR);
+            const int64_t j = e / RR;
+            cp_async8(dst + j * (RR + 1) + i, src + i + j * lda);
+        }
+        cp_async_commit();
+    };
+    int s = 0;
+    int64_t p = blockIdx.x;
+    if (p < npanels) issue(p, 0);
+    for (; p < npanels; p += gridDim.x, s ^= 1) {
+        const int64_t pn = p + gridDim.x;
+        if (pn < npanels) {
+            issue(pn, s ^ 1);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();
+        const double* P = panel + s * stage;
+        // ---- sweep 1: r = A_p x - b_p
+        {
+            const int i = t % RR;
+            const int jg = t / RR;
+            constexpr int G = T2 / RR;
+            double acc[NRHS];
+#pragma unroll
+            for (int q = 0; q < NRHS; ++q) acc[q] = 0.0;
+            for (int64_t j = jg; j < d; j += G) {
+                const double a = P[j * (RR + 1) + i];
+#pragma unroll
+                for (int q = 0; q < NRHS; ++q) acc[q] = fma(a, xs[q * d + j], acc[q]);
+            }
+#pragma unroll
+            for (int off = RR; off < 32; off <<= 1)
+#pragma unroll
+                for (int q = 0; q < NRHS; ++q) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], off);
+            if (lane < RR)
+#pragma unroll
+                for (int q = 0; q < NRHS; ++q) red[(warp * NRHS + q) * RR + lane] = acc[q];
+        }
+        __syncthreads();
+        if (t < NRHS * RR) {
+            const int q = t / RR, i = t % RR;
+            double sum = 0.0;
+#pragma unroll
+            for (int w = 0; w < W2; ++w) sum += red[(w * NRHS + q) * RR + i];
+            rv[q * RR + i] = sum - b[p * RR + i];
+        }
+        __syncthreads();
+        // ---- sweep 2: g += A_p^T r
+#pragma unroll
+        for (int c = 0; c < MAXC; ++c) {
+            const int64_t j = t + (int64_t)c * T2;
+            if (j < d) {
+#pragma unroll
+                for (int q = 0; q < NRHS; ++q) {
+                    double sum = 0.0;
+#pragma unroll
+                    for (int i = 0; i < RR; ++i) sum = fma(P[j * (RR + 1) + i], rv[q * RR + i], sum);
+                    gacc[q][c] += sum;
+                }
+            }
+        }
+        __syncthreads();  // stage s is refilled by the next iteration's prefetch
+    }
+#pragma unroll
+    for (int q = 0; q < NRHS; ++q)
+#pragma unroll
+        for (int c = 0; c < MAXC; ++c) {
+            const int64_t j = t + (int64_t)c * T2;
+            if (j < d) work[((int64_t)blockIdx.x * NRHS + q) * d + j] = gacc[q][c];
+        }
+}
+
+size_t grad_smem_v2(int64_t d, int R, int nrhs) {
+    return sizeof(double) * ((size_t)2 * d * (R + 1) + (size_t)nrhs * d + (size_t)W2 * nrhs * R + (size_t)nrhs * R);
+}
+
+template <int NRHS, int RR>
+void launch_v2(const GradPlan& p, const double* A, const double* b, const double* X, double* work, cudaStream_t st) {
+    const size_t smem = grad_smem_v2(p.d, RR, NRHS);
+    const int maxc = (int)ceil_div(p.d, T2);
+#define IHS_V2(MC)                                                                                                  \
+    do {                                                                                                            \
+        static bool attr = false;                                                                                   \
+        if (!attr) {                                                                                                \
+            CUDA_CHECK(cudaFuncSetAttribute(grad_smem_kernel<NRHS, RR, MC>,                                         \
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));              \
+            attr = true;                                                                                            \
+        }                                                                                                           \
+        LAUNCH((grad_smem_kernel<NRHS, RR, MC>), p.grid, T2, smem, st, A, p.d, p.lda, b, X, work);                  \
+    } while (0)
+    if (maxc <= 1) IHS_V2(1);
+    else if (maxc <= 2) IHS_V2(2);
+    else IHS_V2(4);
+#undef IHS_V2
+}
+
 // G[q][j] = sum_c work[c][q][j] (fixed order) + nu2 * X[q][j]
-__global__ void grad_reduce_kernel(const double* __restrict__ work, int nparts, int64_t d, int nrhs,
-                                   const double* __restrict__ X, double nu2, double* __restrict__ G) {
+// 256 threads = 16 entries x 16 part-groups; group g sums parts g, g+16, ...
+// in order, then the 16 group sums are added in a fixed tree.
+__global__ void __launch_bounds__(256) grad_reduce_kernel(const double* __restrict__ work, int nparts, int64_t d,
+                                                          int nrhs, const double* __restrict__ X, double nu2,
+                                                          double* __restrict__ G) {
+    __shared__ double s[16][17];
     const int64_t total = (int64_t)nrhs * d;
-    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-        double s = 0.0;
-        for (int c = 0; c < nparts; ++c) s += work[(int64_t)c * total + e];
-        G[e] = s + nu2 * X[e];
+    const int c = threadIdx.x % 16, g = threadIdx.x / 16;
+    const int64_t e = (int64_t)blockIdx.x * 16 + c;
+    double acc = 0.0;
+    if (e < total)
+        for (int p = g; p < nparts; p += 16) acc += work[(int64_t)p * total + e];
+    s[g][c] = acc;
+    __syncthreads();
+    if (threadIdx.x < 16 && e < total) {
+        double t8[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) t8[i] = s[2 * i][c] + s[2 * i + 1][c];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) t8[i] = t8[2 * i] + t8[2 * i + 1];
+        const double sum = (t8[0] + t8[1]) + (t8[2] + t8[3]);
+        G[e] = sum + nu2 * X[e];
     }
 }
 
@@ -141,6 +295,23 @@ GradPlan grad_plan(int64_t n, int64_t d, int64_t lda, int num_sms) {
     p.n = n;
     p.d = d;
     p.lda = lda;
+    // v2 when a double-buffered panel of >= 4 rows fits; prefer 2 CTAs/SM and 64 B column segments
+    struct Cand { int R, per_sm; };
+    const Cand cands[] = {{16, 2}, {8, 2}, {8, 1}, {4, 2}, {4, 1}};
+    p.version = 1;
+    if (lda % 32 == 0 && d <= 2048) {
+        for (const Cand& c : cands) {
+            const size_t sm = grad_smem_v2(d, c.R, 2);
+            if (sm <= (c.per_sm == 2 ? 110u * 1024 : 215u * 1024)) {
+                p.version = 2;
+                p.R = c.R;
+                p.smem = sm;
+                const int64_t npanels = lda / c.R;
+                p.grid = (int)std::max<int64_t>(1, std::min<int64_t>(npanels, (int64_t)num_sms * c.per_sm));
+                return p;
+            }
+        }
+    }
     p.R = R;
     const int64_t npanels = (n + R - 1) / R;
     p.grid = (int)std::max<int64_t>(1, std::min<int64_t>(npanels, (int64_t)num_sms * 2));
@@ -153,6 +324,21 @@ size_t grad_work_doubles(const GradPlan& p) { return (size_t)p.grid * 2 * p.d; }
 
 void grad_run(const GradPlan& p, const double* d_A, const double* d_b, double nu2, const double* d_X, int nrhs,
               double* d_G, double* d_work, cudaStream_t st) {
+    if (p.version == 2) {
+        if (nrhs == 1) {
+            if (p.R == 16) launch_v2<1, 16>(p, d_A, d_b, d_X, d_work, st);
+            else if (p.R == 8) launch_v2<1, 8>(p, d_A, d_b, d_X, d_work, st);
+            else launch_v2<1, 4>(p, d_A, d_b, d_X, d_work, st);
+        } else {
+            if (p.R == 16) launch_v2<2, 16>(p, d_A, d_b, d_X, d_work, st);
+            else if (p.R == 8) launch_v2<2, 8>(p, d_A, d_b, d_X, d_work, st);
+            else launch_v2<2, 4>(p, d_A, d_b, d_X, d_work, st);
+        }
+        const int64_t total = (int64_t)nrhs * p.d;
+        LAUNCH(grad_reduce_kernel, (unsigned)ceil_div(total, 16), 256, 0, st, d_work, p.grid, p.d, nrhs, d_X, nu2,
+               d_G);
+        return;
+    }
     const size_t smem = grad_smem(p.d, nrhs);
     static bool attr = false;
     if (!attr) {
@@ -165,8 +351,7 @@ void grad_run(const GradPlan& p, const double* d_A, const double* d_b, double nu
     else
         LAUNCH(grad_partial_kernel<2>, p.grid, THREADS, smem, st, d_A, p.n, p.d, p.lda, d_b, d_X, d_work);
     const int64_t total = (int64_t)nrhs * p.d;
-    const int blocks = (int)std::min<int64_t>(ceil_div(total, 256), 1024);
-    LAUNCH(grad_reduce_kernel, blocks, 256, 0, st, d_work, p.grid, p.d, nrhs, d_X, nu2, d_G);
+    LAUNCH(grad_reduce_kernel, (unsigned)ceil_div(total, 16), 256, 0, st, d_work, p.grid, p.d, nrhs, d_X, nu2, d_G);
 }
 
 }  // namespace ihs_b200

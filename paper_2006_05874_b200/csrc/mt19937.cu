@@ -130,6 +130,35 @@ __global__ void __launch_bounds__(320) mt_signbits_kernel(uint64_t seed, int64_t
     }
 }
 
+// Sign bits from jump-ahead substreams: CTA q produces draws
+// [q*stride, min(n, (q+1)*stride)) (stride a multiple of 32) into a shared
+// bit buffer, then writes its whole words.
+__global__ void __launch_bounds__(320) mt_signbits_sub_kernel(const uint64_t* __restrict__ starts, int64_t stride,
+                                                              int64_t n, uint32_t* __restrict__ bits) {
+    extern __shared__ uint32_t accw[];
+    __shared__ uint64_t mt[NN];
+    const int64_t q = blockIdx.x;
+    const int nw = (int)(stride / 32);
+    for (int i = threadIdx.x; i < NN; i += blockDim.x) mt[i] = starts[q * NN + i];
+    for (int i = threadIdx.x; i < nw; i += blockDim.x) accw[i] = 0u;
+    __syncthreads();
+    const int64_t beg = q * stride;
+    const int64_t end = min(n, beg + stride);
+    for (int64_t base = beg; base < end; base += NN) {
+        twist(mt);
+        for (int i = threadIdx.x; i < NN; i += blockDim.x) {
+            const int64_t g = base + i;
+            if (g < end && (temper(mt[i]) & 1ULL)) {
+                const int local = (int)(g - beg);
+                atomicOr(&accw[local >> 5], 1u << (local & 31));
+            }
+        }
+    }
+    __syncthreads();
+    const int64_t w_end = (end + 31) / 32;
+    for (int64_t w = beg / 32 + threadIdx.x; w < w_end; w += blockDim.x) bits[w] = accw[w - beg / 32];
+}
+
 // libstdc++ generate_canonical<double,53>(mt19937_64): one draw.
 __device__ __forceinline__ double canonical(uint64_t raw) {
     double u = __dmul_rn(__ull2double_rn(raw), 0x1p-64);
@@ -189,9 +218,23 @@ void mt_generate_raw(uint64_t seed, int64_t count, uint64_t* d_out, cudaStream_t
     LAUNCH(mt_raw_kernel, 1, 160, 0, st, seed, count, d_out);
 }
 
-void mt_rademacher_bits(uint64_t seed, int64_t n, uint32_t* d_bits, cudaStream_t st) {
+size_t rademacher_scratch_bytes(int64_t n) {
+    const int64_t nsub = ceil_div(std::max<int64_t>(n, 1), kSignStride);
+    return (size_t)nsub * NN * 8 + (size_t)kJumpSeqWords * 8 + 256;
+}
+
+void mt_rademacher_bits(uint64_t seed, int64_t n, uint32_t* d_bits, void* d_scratch, cudaStream_t st) {
     if (n <= 0) return;
-    LAUNCH(mt_signbits_kernel, 1, 160, 0, st, seed, n, d_bits);
+    if (n <= 2 * kSignStride || d_scratch == nullptr) {
+        LAUNCH(mt_signbits_kernel, 1, 160, 0, st, seed, n, d_bits);
+        return;
+    }
+    const int64_t nsub = ceil_div(n, kSignStride);
+    uint64_t* starts = static_cast<uint64_t*>(d_scratch);
+    uint64_t* xseq = starts + nsub * NN;
+    mt_jump_starts(seed, kSignStride, nsub, starts, xseq, st);
+    LAUNCH(mt_signbits_sub_kernel, (unsigned)nsub, 160, (size_t)(kSignStride / 32) * 4, st, starts,
+           (int64_t)kSignStride, n, d_bits);
 }
 
 size_t gaussian_scratch_bytes(int64_t count) {

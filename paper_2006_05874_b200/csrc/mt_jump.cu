@@ -222,25 +222,35 @@ __global__ void __launch_bounds__(320) mt_wordseq_kernel(uint64_t seed, int nx, 
     }
 }
 
+// CTA (q, chunk) XORs the windows selected by coefficient words
+// [chunk*CW, (chunk+1)*CW) of substream q's polynomial; the chunks combine
+// with atomicXor (XOR is associative and commutative, so the start state is
+// exact regardless of order). starts must be zeroed beforehand.
+constexpr int kChunks = 8;
+constexpr int CW = (PW + kChunks - 1) / kChunks;  // 39 coefficient words per chunk
 __global__ void __launch_bounds__(320) mt_jump_apply_kernel(const uint64_t* __restrict__ X,
                                                             const uint64_t* __restrict__ polys,
                                                             uint64_t* __restrict__ starts) {
-    extern __shared__ uint64_t xs[];
-    for (int i = threadIdx.x; i < NX; i += blockDim.x) xs[i] = X[i];
+    __shared__ uint64_t xs[CW * 64 + NN];
+    const int q = blockIdx.x, chunk = blockIdx.y;
+    const int w0 = chunk * CW, w1 = min(PW, w0 + CW);
+    const int base = w0 * 64;
+    const int nload = min(NX - base, (w1 - w0) * 64 + NN);
+    for (int i = threadIdx.x; i < nload; i += blockDim.x) xs[i] = X[base + i];
     __syncthreads();
-    const uint64_t* a = polys + (size_t)blockIdx.x * PW;
+    const uint64_t* a = polys + (size_t)q * PW;
     const int w = threadIdx.x;
-    uint64_t acc = 0;
     if (w < NN) {
-        for (int widx = 0; widx < PW; ++widx) {
+        uint64_t acc = 0;
+        for (int widx = w0; widx < w1; ++widx) {
             uint64_t bits = __ldg(a + widx);
             while (bits) {
                 const int s = __ffsll((long long)bits) - 1;
                 bits &= bits - 1;
-                acc ^= xs[widx * 64 + s + w];
+                acc ^= xs[(widx - w0) * 64 + s + w];
             }
         }
-        starts[(size_t)blockIdx.x * NN + w] = acc;
+        atomicXor(reinterpret_cast<unsigned long long*>(starts + (size_t)q * NN + w), (unsigned long long)acc);
     }
 }
 }  // namespace
@@ -283,7 +293,6 @@ void mt_jump_starts(uint64_t seed, int64_t stride, int64_t nsub, uint64_t* d_sta
     // device copies of the polynomials are cached per (stride) and grown on demand
     static std::mutex mu;
     static std::map<std::pair<int, int64_t>, std::pair<uint64_t*, int64_t>> dev;  // (device,stride) -> (ptr, count)
-    static std::map<int, bool> attr_set;
     int dev_id = 0;
     CUDA_CHECK(cudaGetDevice(&dev_id));
     uint64_t* d_polys = nullptr;
@@ -299,13 +308,10 @@ void mt_jump_starts(uint64_t seed, int64_t stride, int64_t nsub, uint64_t* d_sta
         } else {
             d_polys = it->second.first;
         }
-        if (!attr_set[dev_id]) {
-            CUDA_CHECK(cudaFuncSetAttribute(mt_jump_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, NX * 8));
-            attr_set[dev_id] = true;
-        }
     }
+    CUDA_CHECK(cudaMemsetAsync(d_starts, 0, (size_t)nsub * NN * 8, st));
     LAUNCH(mt_wordseq_kernel, 1, 160, 0, st, seed, NX, d_X);
-    LAUNCH(mt_jump_apply_kernel, (unsigned)nsub, 320, (size_t)NX * 8, st, d_X, d_polys, d_starts);
+    LAUNCH(mt_jump_apply_kernel, dim3((unsigned)nsub, kChunks), 320, 0, st, d_X, d_polys, d_starts);
 }
 
 }  // namespace ihs_b200

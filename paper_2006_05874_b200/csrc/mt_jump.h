@@ -7,7 +7,9 @@
 namespace ihs_b200 {
 
 // Draws per substream of a long Gaussian stream (one CTA each).
-constexpr int64_t kJumpStride = int64_t{1} << 19;
+constexpr int64_t kJumpStride = int64_t{1} << 17;
+// Draws per substream of an SRHT sign vector (a multiple of 32 for whole bit words).
+constexpr int64_t kSignStride = int64_t{1} << 15;
 
 // Characteristic polynomial of the MT19937-64 transition (degree 19937),
 // found once per process by Berlekamp-Massey over GF(2); bit i = coeff of x^i.

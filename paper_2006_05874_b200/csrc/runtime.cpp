@@ -47,28 +47,71 @@ ihs_status guarded(F&& f) {
 }
 
 // ------------------------------------------------------------ device buffers
+// Device buffers come from the device's stream-ordered memory pool (kept
+// resident: release threshold = max), so the per-doubling growth of the
+// sketch/factor buffers neither synchronizes the device nor takes the
+// driver's allocation path after warm-up.
+std::atomic<int64_t> g_alloc_ns{0};
+std::atomic<int64_t> g_host_rng_ns{0};
+void configure_pool(int dev) {
+    static std::mutex mu;
+    static std::vector<int> done;
+    std::lock_guard<std::mutex> lk(mu);
+    if (std::find(done.begin(), done.end(), dev) != done.end()) return;
+    cudaMemPool_t pool;
+    CUDA_CHECK(cudaDeviceGetDefaultMemPool(&pool, dev));
+    uint64_t thr = UINT64_MAX;
+    CUDA_CHECK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    done.push_back(dev);
+}
+
+// Allocations are ordered on the stream of the API call in flight (set by a
+// StreamScope at the top of every entry point that allocates).
+thread_local cudaStream_t g_cur_stream = nullptr;
+struct StreamScope {
+    cudaStream_t prev;
+    explicit StreamScope(cudaStream_t s) : prev(g_cur_stream) { g_cur_stream = s; }
+    ~StreamScope() { g_cur_stream = prev; }
+};
+// Owns a stream; declared as the first member of a handle so it is destroyed
+// after every buffer that frees itself on that stream.
+struct StreamOwner {
+    cudaStream_t s = nullptr;
+    ~StreamOwner() {
+        if (s) {
+            cudaStreamSynchronize(s);
+            cudaStreamDestroy(s);
+        }
+    }
+};
+
 struct DevBuf {
     void* p = nullptr;
     size_t bytes = 0;
+    cudaStream_t st = nullptr;  // stream the buffer was allocated on (its free is ordered there)
     DevBuf() = default;
     DevBuf(const DevBuf&) = delete;
     DevBuf& operator=(const DevBuf&) = delete;
     ~DevBuf() { release(); }
     void release() {
-        if (p) cudaFree(p);
+        if (p) cudaFreeAsync(p, st);
         p = nullptr;
         bytes = 0;
     }
     void ensure(size_t b) {
         if (b <= bytes) return;
+        const auto t0 = std::chrono::steady_clock::now();
         release();
+        st = g_cur_stream;
         if (b == 0) return;
-        cudaError_t e = cudaMalloc(&p, b);
+        cudaError_t e = cudaMallocAsync(&p, b, st);
         if (e != cudaSuccess) {
             cudaGetLastError();
-            fail(IHS_CUDA_ERROR, "cudaMalloc(" + std::to_string(b) + " bytes): " + cudaGetErrorString(e));
+            p = nullptr;
+            fail(IHS_CUDA_ERROR, "cudaMallocAsync(" + std::to_string(b) + " bytes): " + cudaGetErrorString(e));
         }
         bytes = b;
+        g_alloc_ns += std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t0).count();
     }
     template <class T> T* as() const { return static_cast<T*>(p); }
     double* d() const { return static_cast<double*>(p); }
@@ -165,21 +208,20 @@ using namespace ihs_b200;
 
 // ============================================================ opaque handles
 struct ihs_gpu_system {
+    StreamOwner owner;  // first member: destroyed after the buffers below
     int device = 0;
     int64_t m = 0, d = 0;
     double nu = 0.0;
     int kind = IHS_FACTOR_DIRECT_GRAM;
     cudaStream_t st = nullptr;
-    bool own_stream = false;
     int num_sms = 148;
     DevBuf SA;    // m x d
-    DevBuf L;     // k x k factor (k = m or d), upper triangle = L^T
+    DevBuf L;     // k x k Cholesky factor (k = m or d), lower
+    DevBuf W;     // L^{-1} (lower) with L^{-T} mirrored into the strict upper triangle
+    DevBuf inv_tmp;
     DevBuf work;  // split-K workspace
-    DevBuf tmp;   // solve scratch (2 * max(m, d))
+    DevBuf tmp;   // solve scratch
     DevBuf info;
-    ~ihs_gpu_system() {
-        if (own_stream && st) cudaStreamDestroy(st);
-    }
     int64_t k() const { return kind == IHS_FACTOR_WOODBURY_INNER ? m : d; }
     uint64_t factor_flops() const {  // sketched_system.hpp:52-57
         const uint64_t mm = (uint64_t)m, dd = (uint64_t)d;
@@ -194,6 +236,7 @@ struct ihs_gpu_system {
 };
 
 struct ihs_gpu_problem {
+    StreamOwner owner;  // first member: destroyed after the buffers below
     int device = 0;
     int64_t n = 0, d = 0;
     double nu = 0.0;
@@ -201,11 +244,12 @@ struct ihs_gpu_problem {
     ihs_gpu_options opts{};
     cudaStream_t st = nullptr;
     int num_sms = 148;
-    DevBuf A, b;                 // A packed n x d (lda = n)
+    int64_t lda = 0;             // device leading dimension: n rounded up to 32 (256 B columns)
+    DevBuf A, b;                 // A (lda x d, column-major), b (lda); padding rows are zero
     GradPlan gplan{};
     DevBuf grad_work;
     // sketch workspaces
-    DevBuf T, signbits, entries, tiles, gauss_scratch, S, gemm_work;
+    DevBuf T, signbits, rng_scratch, entries, tiles, gauss_scratch, S, gemm_work;
     PinnedBuf h_stage;
     std::vector<int64_t> h_rows;
     std::vector<int2> h_entries;
@@ -215,9 +259,6 @@ struct ihs_gpu_problem {
     DevBuf dots;                 // 4 doubles
     PinnedBuf h_dots;
     std::unique_ptr<PhaseTimer> timer;
-    ~ihs_gpu_problem() {
-        if (st) cudaStreamDestroy(st);
-    }
 };
 
 namespace ihs_b200 {
@@ -230,15 +271,18 @@ void device_sketch(ihs_gpu_problem* P, int kind, int64_t m, uint64_t seed, doubl
     cudaStream_t st = P->st;
     if (kind == IHS_SKETCH_SRHT) {
         if (m < 1) fail(IHS_INVALID_INPUT, "srht_sketch: m must be >= 1");
-        const SrhtPlan plan = srht_plan(n, d, n, m);
+        const SrhtPlan plan = srht_plan(n, d, P->lda, m);
         if (m > plan.n_pad) fail(IHS_SKETCH_TOO_LARGE, "srht_sketch: m exceeds padded row count");
         // D: rademacher(n_pad, make_stream(seed, 1)) as bits (sketch.hpp:85,87)
         P->signbits.ensure((size_t)((plan.n_pad + 31) / 32) * 4);
-        mt_rademacher_bits(derive_seed(seed, 1), plan.n_pad, P->signbits.as<uint32_t>(), st);
+        P->rng_scratch.ensure(rademacher_scratch_bytes(plan.n_pad));
+        mt_rademacher_bits(derive_seed(seed, 1), plan.n_pad, P->signbits.as<uint32_t>(), P->rng_scratch.p, st);
         // P: sample_without_replacement(n_pad, m, make_stream(seed, 2)) (sketch.hpp:86,88)
         P->h_rows.resize((size_t)m);
+        const auto t_rng = std::chrono::steady_clock::now();
         sample_without_replacement(derive_seed(seed, 2), plan.n_pad, m, P->h_rows.data());
         srht_build_entries(plan, P->h_rows.data(), P->h_entries, P->h_tiles);
+        g_host_rng_ns += std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t_rng).count();
         const size_t eb = P->h_entries.size() * sizeof(int2), tb = P->h_tiles.size() * sizeof(int4);
         P->h_stage.ensure(eb + tb + 64);
         // the previous sketch's copy out of the staging buffer must be done
@@ -267,7 +311,7 @@ void device_sketch(ihs_gpu_problem* P, int kind, int64_t m, uint64_t seed, doubl
         // SA = S * A on the DMMA path (sketch.hpp:68)
         const int splitk = dgemm_pick_splitk(m, d, n, P->num_sms);
         if (splitk > 1) P->gemm_work.ensure((size_t)splitk * m * d * sizeof(double));
-        dgemm(false, false, m, d, n, 1.0, P->S.d(), m, P->A.d(), n, 0.0, d_SA, m, false, splitk,
+        dgemm(false, false, m, d, n, 1.0, P->S.d(), m, P->A.d(), P->lda, 0.0, d_SA, m, false, splitk,
               splitk > 1 ? P->gemm_work.d() : nullptr, st);
         if (c) c->sketch += (uint64_t)m * (uint64_t)n * (uint64_t)d;  // sketch.hpp:65-67
     } else {
@@ -305,12 +349,17 @@ void system_factorize(ihs_gpu_system* S, ihs_counters* c) {
     }
     add_diag(S->L.d(), k, nu2, st);
     cholesky_factor(S->L.d(), k, nullptr, S->info.as<int>(), S->num_sms, st);
+    // W = L^{-1} once per factorization; every later solve is two mat-vecs
+    const int64_t hk = (k + 1) / 2 + 64;
+    S->W.ensure((size_t)k * k * sizeof(double));
+    S->inv_tmp.ensure((size_t)hk * hk * sizeof(double));
+    cholesky_invert(S->L.d(), k, S->W.d(), S->inv_tmp.d(), st);
     int h_info[2] = {0, 0};
     CUDA_CHECK(cudaMemcpyAsync(h_info, S->info.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
     CUDA_CHECK(cudaStreamSynchronize(st));
     if (h_info[1]) fail(IHS_INVALID_INPUT, "SketchedSystem: non-finite sketched matrix");
     if (h_info[0]) fail(IHS_NUMERICAL_BREAKDOWN, "SketchedSystem: Cholesky factorization failed");
-    S->tmp.ensure((size_t)2 * std::max(m, d) * sizeof(double));
+    S->tmp.ensure((size_t)(4 * std::max(m, d) + cholesky_solve_work_doubles(k)) * sizeof(double));
     if (c) c->factor += S->factor_flops();
 }
 
@@ -318,15 +367,32 @@ void system_factorize(ihs_gpu_system* S, ihs_counters* c) {
 void system_solve_dev(const ihs_gpu_system* S, const double* g, double* z, int nrhs) {
     const int64_t m = S->m, d = S->d;
     cudaStream_t st = S->st;
+    double* work = S->tmp.d() + 4 * std::max(m, d);
     if (S->kind == IHS_FACTOR_WOODBURY_INNER) {
-        double* u = S->tmp.d();  // nrhs x m
+        double* u = S->tmp.d();      // nrhs x m : u = SA g
+        double* w = u + 2 * m;       // nrhs x m : w = (SA SA^T + nu^2 I)^{-1} u
         gemv_n(S->SA.d(), m, d, m, g, nrhs, d, u, m, st);
-        cholesky_solve(S->L.d(), m, u, nrhs, st);
-        woodbury_finish(S->SA.d(), m, d, g, u, S->nu * S->nu, nrhs, z, st);
+        cholesky_solve_inv(S->W.d(), m, u, w, nrhs, work, st);
+        woodbury_finish(S->SA.d(), m, d, g, w, S->nu * S->nu, nrhs, z, st);
     } else {
-        if (z != g) CUDA_CHECK(cudaMemcpyAsync(z, g, (size_t)nrhs * d * sizeof(double), cudaMemcpyDeviceToDevice, st));
-        cholesky_solve(S->L.d(), d, z, nrhs, st);
+        cholesky_solve_inv(S->W.d(), d, g, z, nrhs, work, st);
     }
+}
+
+// Device copy of A with 32-row-aligned columns (zero padding rows) and b.
+void upload_Ab(ihs_gpu_problem* P, const double* A, int64_t lda_host, const double* b) {
+    if (A)
+        CUDA_CHECK(cudaMemcpy2DAsync(P->A.p, (size_t)P->lda * sizeof(double), A, (size_t)lda_host * sizeof(double),
+                                     (size_t)P->n * sizeof(double), (size_t)P->d, cudaMemcpyHostToDevice, P->st));
+    if (b) CUDA_CHECK(cudaMemcpyAsync(P->b.p, b, (size_t)P->n * sizeof(double), cudaMemcpyHostToDevice, P->st));
+}
+void alloc_and_upload(ihs_gpu_problem* P, const double* A, int64_t lda_host, const double* b) {
+    P->lda = ceil_div(P->n, 32) * 32;
+    P->A.ensure((size_t)P->lda * P->d * sizeof(double));
+    P->b.ensure((size_t)P->lda * sizeof(double));
+    if (P->lda != P->n) CUDA_CHECK(cudaMemsetAsync(P->A.p, 0, (size_t)P->lda * P->d * sizeof(double), P->st));
+    CUDA_CHECK(cudaMemsetAsync(P->b.p, 0, (size_t)P->lda * sizeof(double), P->st));
+    upload_Ab(P, A, lda_host, b);
 }
 
 void problem_grad(ihs_gpu_problem* P, const double* X, int nrhs, double* G) {
@@ -465,13 +531,12 @@ ihs_status ihs_gpu_problem_create(const double* A, int64_t n, int64_t d, int64_t
         P->nu = nu;
         P->orientation = orientation;
         P->num_sms = sm_count(P->device);
+        configure_pool(P->device);
         CUDA_CHECK(cudaStreamCreateWithFlags(&P->st, cudaStreamNonBlocking));
-        P->A.ensure((size_t)n * d * sizeof(double));
-        P->b.ensure((size_t)n * sizeof(double));
-        CUDA_CHECK(cudaMemcpy2DAsync(P->A.p, (size_t)n * sizeof(double), A, (size_t)lda * sizeof(double),
-                                     (size_t)n * sizeof(double), (size_t)d, cudaMemcpyHostToDevice, P->st));
-        CUDA_CHECK(cudaMemcpyAsync(P->b.p, b, (size_t)n * sizeof(double), cudaMemcpyHostToDevice, P->st));
-        P->gplan = grad_plan(n, d, n, P->num_sms);
+        P->owner.s = P->st;
+        StreamScope scope(P->st);
+        alloc_and_upload(P.get(), A, lda, b);
+        P->gplan = grad_plan(n, d, P->lda, P->num_sms);
         P->grad_work.ensure(grad_work_doubles(P->gplan) * sizeof(double));
         P->vecs.ensure((size_t)16 * d * sizeof(double));
         P->dots.ensure(8 * sizeof(double));
@@ -499,12 +564,8 @@ ihs_status ihs_gpu_problem_upload(ihs_gpu_problem* P, const double* A, int64_t l
     return guarded([&] {
         if (!P) fail(IHS_INVALID_INPUT, "null problem");
         DeviceGuard g(P->device);
-        if (A) {
-            if (lda < P->n) fail(IHS_INVALID_INPUT, "lda < n");
-            CUDA_CHECK(cudaMemcpy2DAsync(P->A.p, (size_t)P->n * sizeof(double), A, (size_t)lda * sizeof(double),
-                                         (size_t)P->n * sizeof(double), (size_t)P->d, cudaMemcpyHostToDevice, P->st));
-        }
-        if (b) CUDA_CHECK(cudaMemcpyAsync(P->b.p, b, (size_t)P->n * sizeof(double), cudaMemcpyHostToDevice, P->st));
+        if (A && lda < P->n) fail(IHS_INVALID_INPUT, "lda < n");
+        upload_Ab(P, A, lda, b);
         CUDA_CHECK(cudaStreamSynchronize(P->st));
     });
 }
@@ -529,6 +590,7 @@ ihs_status ihs_gpu_sketch(ihs_gpu_problem* P, int32_t kind, int64_t m, uint64_t 
     return guarded([&] {
         if (!P) fail(IHS_INVALID_INPUT, "null problem");
         DeviceGuard dg(P->device);
+        StreamScope scope(P->st);
         if (m < 1) fail(IHS_INVALID_INPUT, kind == IHS_SKETCH_SRHT ? "srht_sketch: m must be >= 1"
                                                                     : "gaussian_sketch: m must be >= 1");
         DevBuf SA;
@@ -547,7 +609,6 @@ ihs_status ihs_gpu_sketch_matrix(const double* A, int64_t n, int64_t d, int64_t 
         if (m < 1) fail(IHS_INVALID_INPUT, kind == IHS_SKETCH_SRHT ? "srht_sketch: m must be >= 1"
                                                                     : "gaussian_sketch: m must be >= 1");
         // a throw-away problem (b = 0, nu = 1); the sketch does not look at b or nu
-        std::vector<double> zeros((size_t)n, 0.0);
         ihs_gpu_problem* P = nullptr;
         auto P_holder = std::unique_ptr<ihs_gpu_problem, void (*)(ihs_gpu_problem*)>(nullptr, ihs_gpu_problem_destroy);
         {
@@ -560,13 +621,15 @@ ihs_status ihs_gpu_sketch_matrix(const double* A, int64_t n, int64_t d, int64_t 
             Pp->d = d;
             Pp->nu = 1.0;
             Pp->num_sms = sm_count(Pp->device);
+            configure_pool(Pp->device);
             CUDA_CHECK(cudaStreamCreateWithFlags(&Pp->st, cudaStreamNonBlocking));
-            Pp->A.ensure((size_t)n * d * sizeof(double));
-            CUDA_CHECK(cudaMemcpy2DAsync(Pp->A.p, (size_t)n * sizeof(double), A, (size_t)lda * sizeof(double),
-                                         (size_t)n * sizeof(double), (size_t)d, cudaMemcpyHostToDevice, Pp->st));
+            Pp->owner.s = Pp->st;
+            StreamScope scope(Pp->st);
+            alloc_and_upload(Pp.get(), A, lda, nullptr);
             P = Pp.release();
             P_holder.reset(P);
         }
+        StreamScope scope(P->st);
         DevBuf SA;
         SA.ensure((size_t)m * d * sizeof(double));
         device_sketch(P, kind, m, seed, SA.d(), c);
@@ -578,8 +641,14 @@ ihs_status ihs_gpu_sketch_matrix(const double* A, int64_t n, int64_t d, int64_t 
 ihs_status ihs_gpu_fwht(double* v, int64_t n) {  // fwht_inplace (sketch.hpp:33-49)
     return guarded([&] {
         if (n <= 0 || (n & (n - 1)) != 0) fail(IHS_INVALID_INPUT, "fwht_inplace: length must be a power of two");
+        int dev = 0;
+        CUDA_CHECK(cudaGetDevice(&dev));
+        configure_pool(dev);
         cudaStream_t st;
         CUDA_CHECK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        StreamOwner owner;
+        owner.s = st;
+        StreamScope scope(st);
         DevBuf dv, dT, dbits, dent, dtiles, dout;
         SrhtPlan p = srht_plan(n, 1, n, n);
         p.scale2 = 1.0;  // a single normalization pass, v *= 1/sqrt(n)
@@ -603,7 +672,6 @@ ihs_status ihs_gpu_fwht(double* v, int64_t n) {  // fwht_inplace (sketch.hpp:33-
                         dout.d(), st);
         CUDA_CHECK(cudaMemcpyAsync(v, dout.p, (size_t)n * 8, cudaMemcpyDeviceToHost, st));
         CUDA_CHECK(cudaStreamSynchronize(st));
-        cudaStreamDestroy(st);
     });
 }
 
@@ -614,7 +682,9 @@ ihs_status ihs_gpu_rademacher_bits(uint64_t stream_seed, int64_t n, uint32_t* ou
         const int64_t words = (n + 31) / 32;
         DevBuf buf;
         buf.ensure((size_t)words * 4 + 4);
-        mt_rademacher_bits(stream_seed, n, buf.as<uint32_t>(), 0);
+        DevBuf scratch;
+        scratch.ensure(rademacher_scratch_bytes(n));
+        mt_rademacher_bits(stream_seed, n, buf.as<uint32_t>(), scratch.p, 0);
         CUDA_CHECK(cudaMemcpy(out_bits, buf.p, (size_t)words * 4, cudaMemcpyDeviceToHost));
     });
 }
@@ -657,8 +727,10 @@ ihs_status ihs_gpu_system_factorize(const double* SA, int64_t m, int64_t d, int6
         S->d = d;
         S->nu = nu;
         S->num_sms = sm_count(device);
+        configure_pool(device);
         CUDA_CHECK(cudaStreamCreateWithFlags(&S->st, cudaStreamNonBlocking));
-        S->own_stream = true;
+        S->owner.s = S->st;
+        StreamScope scope(S->st);
         S->SA.ensure((size_t)m * d * sizeof(double));
         CUDA_CHECK(cudaMemcpy2DAsync(S->SA.p, (size_t)m * sizeof(double), SA, (size_t)lds * sizeof(double),
                                      (size_t)m * sizeof(double), (size_t)d, cudaMemcpyHostToDevice, S->st));
@@ -686,6 +758,7 @@ ihs_status ihs_gpu_system_solve(const ihs_gpu_system* S, const double* g, double
     return guarded([&] {
         if (!S || !g || !z) fail(IHS_INVALID_INPUT, "SketchedSystem::solve: dimension mismatch");
         DeviceGuard dg(S->device);
+        StreamScope scope(S->st);
         DevBuf buf;
         buf.ensure((size_t)2 * S->d * sizeof(double));
         double* dg_ = buf.d();
@@ -703,6 +776,7 @@ ihs_status ihs_gpu_adaptive_solve(ihs_gpu_problem* P, const ihs_solver_config* c
     return guarded([&] {
         if (!P || !cfg || !rep || !rep->x) fail(IHS_INVALID_INPUT, "adaptive_solve: null argument");
         DeviceGuard dgd(P->device);
+        StreamScope scope(P->st);
         // solver.hpp:243-245 and :107-109
         if (P->orientation != IHS_OVERDETERMINED)
             fail(IHS_INVALID_INPUT, "adaptive_solve: expects an overdetermined instance (use solve_underdetermined for d > n)");
@@ -717,6 +791,7 @@ ihs_status ihs_gpu_adaptive_solve(ihs_gpu_problem* P, const ihs_solver_config* c
         PhaseTimer& tm = *P->timer;
         tm.reset();
         const int64_t launches0 = g_launches.load();
+        const int64_t alloc0 = g_alloc_ns.load(), rng0 = g_host_rng_ns.load();
         ihs_phase_times PT{};
         cudaEvent_t ev_begin = tm.get(), ev_end = tm.get();
         CUDA_CHECK(cudaEventRecord(ev_begin, st));
@@ -946,6 +1021,8 @@ ihs_status ihs_gpu_adaptive_solve(ihs_gpu_problem* P, const ihs_solver_config* c
         rep->wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
         double ph[4];
         tm.collect(ph);
+        PT.alloc_ms = (double)(g_alloc_ns.load() - alloc0) * 1e-6;
+        PT.host_rng_ms = (double)(g_host_rng_ns.load() - rng0) * 1e-6;
         rep->times = PT;
         rep->times.sketch_ms = ph[PH_SKETCH];
         rep->times.factor_ms = ph[PH_FACTOR];

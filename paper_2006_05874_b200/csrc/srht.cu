@@ -7,18 +7,21 @@
 // the m sampled rows scaled by sqrt(n_pad/m).
 //
 // B200 design (bit-exact with the reference):
-//   * no padded copy: rows >= n are virtual zeros, the sign flip is fused
-//     into the load (eps_i * a as a real multiply by +-1.0, like :91);
-//   * n_pad = 2^(L+H). Phase 1 transforms each column in blocks of 2^L
-//     contiguous rows entirely on chip (bits 0..L-1, in 4-bit register rounds
-//     staged through padded shared memory), reading A exactly once;
-//   * phase 2 (only if H > 0) runs bits L..L+H-1 for tiles of W consecutive
-//     low indices across all 2^H blocks, and only for tiles that contain a
-//     sampled row; it emits just the sampled rows;
-//   * every butterfly is computed as in the reference (v[j] = s + t,
-//     v[j+h] = s - t, stages in increasing bit order), and the two scalings
-//     are separate rounded multiplies (:47-48 then :95-97), so SA matches the
-//     reference bit for bit.
+//   * no padded copy: rows >= n are virtual +0.0, the sign flip is fused into
+//     the load as a real multiply by +-1.0 (like :91);
+//   * phase 1 (n_pad >= 2^11): one warp per 1024-row chunk of a column —
+//     coalesced 256 B loads, two padded shared-memory transposes, all ten
+//     low-bit stages in registers, coalesced store of the chunk to T;
+//   * phase 2: the remaining high bits in passes of <= 10 bits over tiles of
+//     W consecutive low indices x 2^hb combinations of the pass bits, loaded
+//     straight into registers (the pass bits are register bits, the low bits
+//     are lane bits, so every load is coalesced), one shared-memory exchange
+//     between the two 5-bit register rounds; the last pass runs only for tiles
+//     that hold a sampled row and emits just those rows;
+//   * n_pad <= 2^10: one CTA per column does everything on chip;
+//   * every butterfly is v[j] = s + t, v[j+h] = s - t in increasing bit order,
+//     and the two scalings (1/sqrt(n_pad) at :47-48, sqrt(n_pad/m) at
+//     :95-97) are separate rounded multiplies of host-computed constants.
 #include "common.cuh"
 
 #include <algorithm>
@@ -28,70 +31,60 @@
 namespace ihs_b200 {
 
 namespace {
-constexpr int kMaxL = 13;   // phase-1 block = 2^13 doubles = 64 KiB (+ padding)
-constexpr int kTileW = 16;  // phase-2 tile width (low indices), 128 B per block row
+constexpr int kSmallL = 10;  // n_pad <= 2^10: single on-chip kernel
+constexpr int kChunkL = 10;  // phase-1 chunk: 1024 rows per warp
+constexpr int kP1Warps = 8;
+constexpr int kTileElems = 8192;  // phase-2 tile: 2^13 doubles (64 KiB exchange buffer)
+constexpr int kP2Threads = 256;
 
 __host__ __device__ constexpr int padded(int i) { return i + (i >> 4); }
+__host__ __device__ constexpr int pad32(int i) { return i + (i >> 5); }
 
-// Phase 1: one CTA per (row block, column). THREADS = max(1, 2^L / 16).
+__device__ __forceinline__ void bfly(double& a, double& b) {
+    const double s = a, t = b;
+    a = __dadd_rn(s, t);
+    b = __dsub_rn(s, t);
+}
+
+__device__ __forceinline__ double eps_mul(const uint32_t* __restrict__ signbits, int64_t r, double a) {
+    const uint32_t w = __ldg(signbits + (r >> 5));
+    return __dmul_rn(((w >> (r & 31)) & 1u) ? 1.0 : -1.0, a);
+}
+
+// ------------------------------------------------------------ small n_pad
+// One CTA per column: the whole transform and the gather on chip.
 template <int L>
 __global__ void __launch_bounds__((1 << L) / 16 > 0 ? (1 << L) / 16 : 1)
-srht_phase1_kernel(const double* __restrict__ A, int64_t n, int64_t lda, const uint32_t* __restrict__ signbits,
-                   int H, double* __restrict__ T, int64_t n_pad,
-                   // H == 0 only: emit sampled rows directly
-                   const int2* __restrict__ entries, int n_entries, double s1, double s2, double* __restrict__ SA,
-                   int64_t m) {
+srht_small_kernel(const double* __restrict__ A, int64_t n, int64_t lda, const uint32_t* __restrict__ signbits,
+                  const int2* __restrict__ entries, int n_entries, double s1, double s2, double* __restrict__ SA,
+                  int64_t m) {
     constexpr int N = 1 << L;
     constexpr int THREADS = N / 16 > 0 ? N / 16 : 1;
-    constexpr int E = N / THREADS;  // elements per thread: 16, or N when N < 16
+    constexpr int E = N / THREADS;
     extern __shared__ double xs[];
-
-    const int64_t blk = blockIdx.x;
-    const int64_t j = blockIdx.y;
-    const int64_t r0 = blk * N;
+    const int64_t j = blockIdx.x;
     const double* Acol = A + j * lda;
     const int t = threadIdx.x;
-
-    // coalesced load with the sign flip fused (B.row(i) = eps_i * A.row(i))
-    for (int e = t; e < N; e += THREADS) {
-        const int64_t r = r0 + e;
-        double v = 0.0;
-        if (r < n) {
-            const uint32_t w = __ldg(signbits + (r >> 5));
-            const double eps = ((w >> (r & 31)) & 1u) ? 1.0 : -1.0;
-            v = __dmul_rn(eps, __ldg(Acol + r));
-        }
-        xs[padded(e)] = v;
-    }
+    for (int e = t; e < N; e += THREADS) xs[padded(e)] = (e < n) ? eps_mul(signbits, e, __ldg(Acol + e)) : 0.0;
     __syncthreads();
-
     if constexpr (L < 4) {
-        // tiny transform: one thread, all stages in registers
         double v[E];
 #pragma unroll
         for (int c = 0; c < E; ++c) v[c] = xs[padded(c)];
 #pragma unroll
-        for (int s = 0; s < L; ++s) {
+        for (int s = 0; s < L; ++s)
 #pragma unroll
             for (int c = 0; c < E; ++c)
-                if (!(c & (1 << s))) {
-                    const double a = v[c], b = v[c | (1 << s)];
-                    v[c] = __dadd_rn(a, b);
-                    v[c | (1 << s)] = __dsub_rn(a, b);
-                }
-        }
+                if (!(c & (1 << s))) bfly(v[c], v[c | (1 << s)]);
 #pragma unroll
         for (int c = 0; c < E; ++c) xs[padded(c)] = v[c];
         __syncthreads();
     } else {
-        // rounds of 4 bits at positions b0 = 0, 4, 8, ... (last round shifted
-        // down to L-4, applying only the stages not yet done)
         int done = 0;
-        while (done < L) {
+        while (done < L) {  // 4-bit register rounds (the last one shifted down)
             const int b0 = (done + 4 <= L) ? done : L - 4;
-            const int lo_stage = done - b0;  // first stage (within the round) still to apply
-            const int low_mask = (1 << b0) - 1;
-            const int base = ((t >> b0) << (b0 + 4)) | (t & low_mask);
+            const int lo_stage = done - b0;
+            const int base = ((t >> b0) << (b0 + 4)) | (t & ((1 << b0) - 1));
             double v[16];
 #pragma unroll
             for (int c = 0; c < 16; ++c) v[c] = xs[padded(base | (c << b0))];
@@ -100,96 +93,216 @@ srht_phase1_kernel(const double* __restrict__ A, int64_t n, int64_t lda, const u
                 if (s < lo_stage) continue;
 #pragma unroll
                 for (int c = 0; c < 16; ++c)
-                    if (!(c & (1 << s))) {
-                        const double a = v[c], b = v[c | (1 << s)];
-                        v[c] = __dadd_rn(a, b);
-                        v[c | (1 << s)] = __dsub_rn(a, b);
-                    }
+                    if (!(c & (1 << s))) bfly(v[c], v[c | (1 << s)]);
             }
-            __syncthreads();
 #pragma unroll
             for (int c = 0; c < 16; ++c) xs[padded(base | (c << b0))] = v[c];
             __syncthreads();
             done = b0 + 4;
         }
     }
-
-    if (H == 0) {
-        // the column is complete: emit the sampled rows (all rows live in this block)
-        for (int q = t; q < n_entries; q += THREADS) {
-            const int2 rk = entries[q];
-            const double v = xs[padded(rk.x)];
-            SA[(int64_t)rk.y + j * m] = __dmul_rn(__dmul_rn(v, s1), s2);
-        }
-    } else {
-        double* Tcol = T + j * n_pad + r0;
-        for (int e = t; e < N; e += THREADS) Tcol[e] = xs[padded(e)];
+    for (int q = t; q < n_entries; q += THREADS) {
+        const int2 rk = entries[q];
+        SA[(int64_t)rk.y + j * m] = __dmul_rn(__dmul_rn(xs[padded(rk.x)], s1), s2);
     }
 }
 
-// Phase 2: one CTA per (active tile, column); bits L .. L+H-1 over the 2^H
-// blocks for kTileW consecutive low indices, then emit the tile's samples.
-__global__ void __launch_bounds__(256)
-srht_phase2_kernel(const double* __restrict__ T, int64_t n_pad, int L, int H, const int4* __restrict__ tiles,
-                   const int2* __restrict__ entries, double s1, double s2, double* __restrict__ SA, int64_t m) {
-    extern __shared__ double xs[];
-    const int4 tile = tiles[blockIdx.x];  // (rlo0, entry_begin, entry_end, -)
-    const int64_t j = blockIdx.y;
-    const int NB = 1 << H;
-    const int64_t stride_b = int64_t{1} << L;
-    const double* Tcol = T + j * n_pad + tile.x;
-    const int total = NB * kTileW;
-    for (int e = threadIdx.x; e < total; e += blockDim.x) {
-        const int b = e / kTileW, w = e % kTileW;
-        xs[e] = Tcol[(int64_t)b * stride_b + w];
+// ------------------------------------------------------------ phase 1
+// Warp-per-chunk: bits 0..9 of a 1024-row chunk of one column -> T.
+__global__ void __launch_bounds__(32 * kP1Warps)
+srht_phase1_kernel(const double* __restrict__ A, int64_t n, int64_t lda, const uint32_t* __restrict__ signbits,
+                   double* __restrict__ T, int64_t n_pad, int64_t chunks_per_col, int64_t total_chunks) {
+    extern __shared__ double p1_smem[];  // kP1Warps x (1024 + 32) doubles
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double* xs = p1_smem + warp * (1024 + 32);
+    for (int64_t chunk = (int64_t)blockIdx.x * kP1Warps + warp; chunk < total_chunks;
+         chunk += (int64_t)gridDim.x * kP1Warps) {
+        const int64_t j = chunk / chunks_per_col;
+        const int64_t r0 = (chunk % chunks_per_col) << kChunkL;
+        const double* Acol = A + j * lda;
+        double v[32];
+        // coalesced load (lane = index bits 0-4, register c = bits 5-9), sign fused
+#pragma unroll
+        for (int c = 0; c < 32; ++c) {
+            const int64_t r = r0 + (c << 5) + lane;
+            v[c] = (r < n) ? eps_mul(signbits, r, __ldg(Acol + r)) : 0.0;
+        }
+#pragma unroll
+        for (int c = 0; c < 32; ++c) xs[pad32((c << 5) | lane)] = v[c];
+        __syncwarp();
+        // register c = index bits 0-4: stages 0..4
+#pragma unroll
+        for (int c = 0; c < 32; ++c) v[c] = xs[pad32((lane << 5) | c)];
+#pragma unroll
+        for (int s = 0; s < 5; ++s)
+#pragma unroll
+            for (int c = 0; c < 32; ++c)
+                if (!(c & (1 << s))) bfly(v[c], v[c | (1 << s)]);
+#pragma unroll
+        for (int c = 0; c < 32; ++c) xs[pad32((lane << 5) | c)] = v[c];
+        __syncwarp();
+        // register c = index bits 5-9: stages 5..9
+#pragma unroll
+        for (int c = 0; c < 32; ++c) v[c] = xs[pad32((c << 5) | lane)];
+        __syncwarp();
+#pragma unroll
+        for (int s = 0; s < 5; ++s)
+#pragma unroll
+            for (int c = 0; c < 32; ++c)
+                if (!(c & (1 << s))) bfly(v[c], v[c | (1 << s)]);
+        double* Tcol = T + j * n_pad + r0;
+#pragma unroll
+        for (int c = 0; c < 32; ++c) Tcol[(c << 5) + lane] = v[c];
     }
-    __syncthreads();
-    const int half = total / 2;
-    for (int s = 0; s < H; ++s) {
-        for (int p = threadIdx.x; p < half; p += blockDim.x) {
-            const int w = p % kTileW;
-            const int bp = p / kTileW;  // index over b with bit s removed
-            const int b_lo = bp & ((1 << s) - 1);
-            const int b = ((bp >> s) << (s + 1)) | b_lo;
-            const int i0 = b * kTileW + w, i1 = (b | (1 << s)) * kTileW + w;
-            const double a = xs[i0], c = xs[i1];
-            xs[i0] = __dadd_rn(a, c);
-            xs[i1] = __dsub_rn(a, c);
+}
+
+// ------------------------------------------------------------ phase 2
+// One CTA per (tile, column): bits [lo, lo+HB) of kTileElems elements = W
+// consecutive low indices x 2^HB pass combinations. Round 1: register bits =
+// pass bits [0, RB1); round 2 (RB2 = HB - RB1 > 0): register bits = pass bits
+// [RB1, HB) after one shared-memory exchange. emit: write the tile's sampled
+// rows (entries) instead of the tile.
+template <int HB>
+__global__ void __launch_bounds__(kP2Threads)
+srht_phase2_kernel(double* __restrict__ T, int64_t n_pad, int lo, const int4* __restrict__ tiles, int emit,
+                   int64_t tiles_per_col, const int2* __restrict__ entries, double s1, double s2,
+                   double* __restrict__ SA, int64_t m) {
+    constexpr int RB1 = HB < 5 ? HB : 5;
+    constexpr int RB2 = HB - RB1;
+    constexpr int E = 1 << RB1;                     // registers per thread
+    constexpr int W = kP2Threads * E / (1 << HB);   // consecutive low indices per tile
+    constexpr int LOGW = (W >= 256) ? 8 : (W >= 128) ? 7 : (W >= 64) ? 6 : (W >= 32) ? 5 : (W >= 16) ? 4 : 3;
+    extern __shared__ double xs[];
+    const int t = threadIdx.x;
+    const int64_t j = blockIdx.y;
+    int64_t base;
+    int4 tile = make_int4(0, 0, 0, 0);
+    if (emit) {
+        tile = tiles[blockIdx.x];
+        base = tile.x;
+    } else {
+        // enumerate tiles: low part (bits LOGW .. lo-1) and high part (bits >= lo+HB)
+        const int64_t low_tiles = (int64_t{1} << lo) >> LOGW;
+        const int64_t tid = blockIdx.x;
+        base = ((tid % low_tiles) << LOGW) | ((tid / low_tiles) << (lo + HB));
+    }
+    (void)tiles_per_col;
+    double* Tcol = T + j * n_pad + base;
+    const int w = t % W;
+    const int g = t / W;  // 2^RB2 groups
+    double v[E];
+    // round 1: register c = pass bits [0, RB1), g = pass bits [RB1, HB)
+#pragma unroll
+    for (int c = 0; c < E; ++c) v[c] = Tcol[((int64_t)((g << RB1) | c) << lo) + w];
+#pragma unroll
+    for (int s = 0; s < RB1; ++s)
+#pragma unroll
+        for (int c = 0; c < E; ++c)
+            if (!(c & (1 << s))) bfly(v[c], v[c | (1 << s)]);
+    if constexpr (RB2 > 0) {
+        // exchange: element (b, w) at xs[pad32(b*W + w)]
+#pragma unroll
+        for (int c = 0; c < E; ++c) xs[pad32(((g << RB1) | c) * W + w)] = v[c];
+        __syncthreads();
+        // round 2: thread (w, g2) with g2 in [0, 2^RB2), register (grp, c2):
+        // pass bits [0, RB1) = g2 + grp * 2^RB2, pass bits [RB1, HB) = c2
+        constexpr int G2 = 1 << RB2;
+        constexpr int GRPS = E / G2;
+        const int g2 = g;
+#pragma unroll
+        for (int grp = 0; grp < GRPS; ++grp)
+#pragma unroll
+            for (int c2 = 0; c2 < G2; ++c2) {
+                const int b = (g2 + grp * G2) | (c2 << RB1);
+                v[grp * G2 + c2] = xs[pad32(b * W + w)];
+            }
+#pragma unroll
+        for (int s = 0; s < RB2; ++s)
+#pragma unroll
+            for (int grp = 0; grp < GRPS; ++grp)
+#pragma unroll
+                for (int c2 = 0; c2 < G2; ++c2)
+                    if (!(c2 & (1 << s))) bfly(v[grp * G2 + c2], v[grp * G2 + (c2 | (1 << s))]);
+        if (!emit) {
+#pragma unroll
+            for (int grp = 0; grp < GRPS; ++grp)
+#pragma unroll
+                for (int c2 = 0; c2 < G2; ++c2) {
+                    const int b = (g2 + grp * G2) | (c2 << RB1);
+                    Tcol[((int64_t)b << lo) + w] = v[grp * G2 + c2];
+                }
+            return;
         }
         __syncthreads();
+#pragma unroll
+        for (int grp = 0; grp < GRPS; ++grp)
+#pragma unroll
+            for (int c2 = 0; c2 < G2; ++c2) {
+                const int b = (g2 + grp * G2) | (c2 << RB1);
+                xs[pad32(b * W + w)] = v[grp * G2 + c2];
+            }
+    } else {
+        if (!emit) {
+#pragma unroll
+            for (int c = 0; c < E; ++c) Tcol[((int64_t)((g << RB1) | c) << lo) + w] = v[c];
+            return;
+        }
+#pragma unroll
+        for (int c = 0; c < E; ++c) xs[pad32(((g << RB1) | c) * W + w)] = v[c];
     }
-    for (int q = tile.y + threadIdx.x; q < tile.z; q += blockDim.x) {
+    __syncthreads();
+    const int64_t bmask = (int64_t{1} << HB) - 1;
+    for (int q = tile.y + t; q < tile.z; q += kP2Threads) {
         const int2 rk = entries[q];
         const int64_t r = rk.x;
-        const int b = (int)(r >> L);
-        const int w = (int)((r & (stride_b - 1)) - tile.x);
-        const double v = xs[b * kTileW + w];
-        SA[(int64_t)rk.y + j * m] = __dmul_rn(__dmul_rn(v, s1), s2);
+        const int b = (int)((r >> lo) & bmask);
+        const int ww = (int)(r & (W - 1));
+        SA[(int64_t)rk.y + j * m] = __dmul_rn(__dmul_rn(xs[pad32(b * W + ww)], s1), s2);
     }
 }
 
+int pass_w(int hb) {
+    const int rb1 = std::min(hb, 5);
+    return kP2Threads * (1 << rb1) / (1 << hb);
+}
+// elements of one phase-2 tile: W low indices x 2^hb pass combinations
+// (kTileElems for hb >= 5, 256 * 2^hb below)
+int64_t pass_tile_elems(int hb) { return (int64_t)pass_w(hb) << hb; }
+
 template <int L>
-void launch_phase1(const SrhtPlan& p, const double* A, const uint32_t* signbits, double* T, const int2* entries,
-                   int n_entries, double* SA, cudaStream_t st) {
+void launch_small(const SrhtPlan& p, const double* A, const uint32_t* signbits, const int2* entries, double* SA,
+                  cudaStream_t st) {
     constexpr int N = 1 << L;
     constexpr int THREADS = N / 16 > 0 ? N / 16 : 1;
     const size_t smem = (size_t)padded(N) * sizeof(double) + 64;
+    LAUNCH(srht_small_kernel<L>, (unsigned)p.d, THREADS, smem, st, A, p.n, p.lda, signbits, entries, (int)p.m,
+           p.scale1, p.scale2, SA, p.m);
+}
+using SmallFn = void (*)(const SrhtPlan&, const double*, const uint32_t*, const int2*, double*, cudaStream_t);
+const SmallFn kSmall[kSmallL + 1] = {launch_small<0>, launch_small<1>, launch_small<2>, launch_small<3>,
+                                     launch_small<4>, launch_small<5>, launch_small<6>, launch_small<7>,
+                                     launch_small<8>, launch_small<9>, launch_small<10>};
+
+template <int HB>
+void launch_pass(const SrhtPlan& p, double* T, int lo, const int4* tiles, int n_tiles, bool emit, const int2* entries,
+                 double* SA, cudaStream_t st) {
+    const size_t smem = (size_t)pad32(kTileElems) * sizeof(double) + 64;
     static bool attr = false;
     if (!attr) {
-        CUDA_CHECK(cudaFuncSetAttribute(srht_phase1_kernel<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CUDA_CHECK(cudaFuncSetAttribute(srht_phase2_kernel<HB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)smem));
         attr = true;
     }
-    dim3 grid((unsigned)(p.n_pad >> L), (unsigned)p.d);
-    LAUNCH(srht_phase1_kernel<L>, grid, THREADS, smem, st, A, p.n, p.lda, signbits, p.H, T, p.n_pad, entries,
-           n_entries, p.scale1, p.scale2, SA, p.m);
+    const int64_t tiles_per_col = p.n_pad / pass_tile_elems(HB);
+    const unsigned gx = emit ? (unsigned)n_tiles : (unsigned)tiles_per_col;
+    if (gx == 0) return;
+    dim3 grid(gx, (unsigned)p.d);
+    LAUNCH(srht_phase2_kernel<HB>, grid, kP2Threads, smem, st, T, p.n_pad, lo, tiles, emit ? 1 : 0, tiles_per_col,
+           entries, p.scale1, p.scale2, SA, p.m);
 }
-
-using Phase1Fn = void (*)(const SrhtPlan&, const double*, const uint32_t*, double*, const int2*, int, double*,
-                          cudaStream_t);
-const Phase1Fn kPhase1[kMaxL + 1] = {
-    launch_phase1<0>, launch_phase1<1>, launch_phase1<2>,  launch_phase1<3>,  launch_phase1<4>,
-    launch_phase1<5>, launch_phase1<6>, launch_phase1<7>,  launch_phase1<8>,  launch_phase1<9>,
-    launch_phase1<10>, launch_phase1<11>, launch_phase1<12>, launch_phase1<13>};
+using PassFn = void (*)(const SrhtPlan&, double*, int, const int4*, int, bool, const int2*, double*, cudaStream_t);
+const PassFn kPass[11] = {nullptr, launch_pass<1>, launch_pass<2>, launch_pass<3>, launch_pass<4>, launch_pass<5>,
+                          launch_pass<6>, launch_pass<7>, launch_pass<8>, launch_pass<9>, launch_pass<10>};
 }  // namespace
 
 SrhtPlan srht_plan(int64_t n, int64_t d, int64_t lda, int64_t m) {
@@ -203,9 +316,25 @@ SrhtPlan srht_plan(int64_t n, int64_t d, int64_t lda, int64_t m) {
     while (np < n) { np <<= 1; ++logn; }
     p.n_pad = np;
     p.logn = logn;
-    p.L = std::min(logn, kMaxL);
-    p.H = logn - p.L;
-    if (p.H > 12) fail(IHS_INVALID_INPUT, "srht_sketch: n_pad above 2^25 not supported");
+    if (logn > 30) fail(IHS_INVALID_INPUT, "srht_sketch: n_pad above 2^30 not supported");
+    if (logn <= kSmallL) {
+        p.L = logn;
+        p.H = 0;
+        p.npass = 0;
+    } else {
+        p.L = kChunkL;
+        p.H = logn - kChunkL;
+        // split H into passes of <= 10 bits, as even as possible
+        const int np_ = (p.H + 9) / 10;
+        int lo = kChunkL;
+        p.npass = np_;
+        for (int i = 0; i < np_; ++i) {
+            const int hb = p.H / np_ + (i < p.H % np_ ? 1 : 0);
+            p.pass_lo[i] = lo;
+            p.pass_hb[i] = hb;
+            lo += hb;
+        }
+    }
     // exactly the reference's host expressions (sketch.hpp:47 and :95)
     p.scale1 = 1.0 / std::sqrt(static_cast<double>(np));
     p.scale2 = std::sqrt(static_cast<double>(np) / static_cast<double>(m));
@@ -223,38 +352,57 @@ void srht_build_entries(const SrhtPlan& p, const int64_t* rows, std::vector<int2
         tiles.push_back(make_int4(0, 0, (int)p.m, 0));
         return;
     }
-    // counting sort of the sampled rows by low-index tile
-    const int64_t low = int64_t{1} << p.L;
-    const int64_t ntiles = low / kTileW;
+    // tiles of the last pass: bits [lo, lo+hb) are the pass bits, bits [0, logW)
+    // the in-tile low index; a tile is identified by its base row (pass bits and
+    // low bits cleared). Counting sort of the sampled rows by tile.
+    const int lo = p.pass_lo[p.npass - 1], hb = p.pass_hb[p.npass - 1];
+    const int64_t W = pass_w(hb);
+    const int64_t low_tiles = (int64_t{1} << lo) / W;
+    const int64_t ntiles = p.n_pad / pass_tile_elems(hb);
+    auto tile_of = [&](int64_t r) {
+        const int64_t low = (r & ((int64_t{1} << lo) - 1)) / W;
+        const int64_t high = r >> (lo + hb);
+        return high * low_tiles + low;
+    };
     std::vector<int> count((size_t)ntiles + 1, 0);
-    for (int64_t k = 0; k < p.m; ++k) count[(size_t)((rows[k] & (low - 1)) / kTileW) + 1]++;
+    for (int64_t k = 0; k < p.m; ++k) {
+        if (rows[k] < 0 || rows[k] >= p.n_pad || tile_of(rows[k]) >= ntiles)
+            fail(IHS_INTERNAL_ERROR, "srht: sampled row outside the padded range");
+        count[(size_t)tile_of(rows[k]) + 1]++;
+    }
     for (int64_t t = 0; t < ntiles; ++t) count[(size_t)t + 1] += count[(size_t)t];
     entries.resize((size_t)p.m);
     std::vector<int> fill(count.begin(), count.end() - 1);
-    for (int64_t k = 0; k < p.m; ++k) {
-        const int64_t t = (rows[k] & (low - 1)) / kTileW;
-        entries[(size_t)fill[(size_t)t]++] = make_int2((int)rows[k], (int)k);
-    }
+    for (int64_t k = 0; k < p.m; ++k) entries[(size_t)fill[(size_t)tile_of(rows[k])]++] = make_int2((int)rows[k], (int)k);
     for (int64_t t = 0; t < ntiles; ++t)
-        if (count[(size_t)t + 1] > count[(size_t)t])
-            tiles.push_back(make_int4((int)(t * kTileW), count[(size_t)t], count[(size_t)t + 1], 0));
+        if (count[(size_t)t + 1] > count[(size_t)t]) {
+            const int64_t base = ((t % low_tiles) * W) | ((t / low_tiles) << (lo + hb));
+            tiles.push_back(make_int4((int)base, count[(size_t)t], count[(size_t)t + 1], 0));
+        }
 }
 
 void srht_run_device(const SrhtPlan& p, const double* d_A, const uint32_t* d_signbits, const int2* d_entries,
                      const int4* d_tiles, int n_tiles, double* d_T, double* d_SA, cudaStream_t st) {
     if (p.d == 0) return;
-    kPhase1[p.L](p, d_A, d_signbits, d_T, d_entries, p.H == 0 ? (int)p.m : 0, d_SA, st);
-    if (p.H > 0 && n_tiles > 0) {
-        const size_t smem = (size_t)(kTileW << p.H) * sizeof(double);
-        if (smem > 200 * 1024) fail(IHS_INVALID_INPUT, "srht_sketch: n_pad too large for one phase-2 tile");
-        static size_t attr = 0;
-        if (smem > attr) {
-            CUDA_CHECK(cudaFuncSetAttribute(srht_phase2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            attr = smem;
-        }
-        dim3 grid((unsigned)n_tiles, (unsigned)p.d);
-        LAUNCH(srht_phase2_kernel, grid, 256, smem, st, d_T, p.n_pad, p.L, p.H, d_tiles, d_entries, p.scale1,
-               p.scale2, d_SA, p.m);
+    if (p.H == 0) {
+        kSmall[p.L](p, d_A, d_signbits, d_entries, d_SA, st);
+        return;
+    }
+    const int64_t chunks_per_col = p.n_pad >> kChunkL;
+    const int64_t total = chunks_per_col * p.d;
+    const int64_t blocks = std::min<int64_t>(ceil_div(total, kP1Warps), (int64_t)1 << 20);
+    const size_t smem = (size_t)kP1Warps * (1024 + 32) * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+        CUDA_CHECK(cudaFuncSetAttribute(srht_phase1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    LAUNCH(srht_phase1_kernel, (unsigned)blocks, 32 * kP1Warps, smem, st, d_A, p.n, p.lda, d_signbits, d_T, p.n_pad,
+           chunks_per_col, total);
+    for (int i = 0; i < p.npass; ++i) {
+        const bool last = i == p.npass - 1;
+        if (last && n_tiles == 0) break;
+        kPass[p.pass_hb[i]](p, d_T, p.pass_lo[i], d_tiles, n_tiles, last, d_entries, d_SA, st);
     }
 }
 

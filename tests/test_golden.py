@@ -1,0 +1,68 @@
+"""Committed golden fixtures (tests/golden/golden.npz, made by make_golden.py
+from the pinned oracle): CPU checks keep the oracle and the product's host
+logic on the fixtures; GPU checks hold the CUDA path to the same bytes."""
+import pathlib
+
+import numpy as np
+import pytest
+
+G = np.load(pathlib.Path(__file__).resolve().parent / "golden" / "golden.npz")
+
+
+def test_oracle_reproduces_golden(O):
+    for i in range(3):
+        seed, K, sub = (int(v) for v in G[f"derive_{i}"])
+        assert O.derive_seed(seed, K) == sub
+        assert np.array_equal(O.mt_raw(O.derive_seed(sub, 1), 1024), G[f"mt_raw_{i}"])
+        assert np.array_equal(O.rademacher(O.derive_seed(sub, 1), 4096).astype(np.int8), G[f"signs_{i}"])
+        assert np.array_equal(O.sample_without_replacement(O.derive_seed(sub, 2), 4096, 257), G[f"rows_{i}"])
+        assert np.array_equal(O.fill_gaussian(O.derive_seed(sub, 0), 37, 29, 1.0 / np.sqrt(37.0)), G[f"normals_{i}"])
+    A, b, _ = O.synth(3000, 12, decay=0.9, noise_std=0.01, outlier_frac=0.01, data_seed=7)
+    assert np.array_equal(A, G["A"]) and np.array_equal(b, G["b"])
+    assert np.array_equal(O.srht_sketch(A, 64, 3), G["srht_m64_s3"])
+
+
+def test_host_logic_matches_golden(ihs):
+    for i in range(3):
+        seed, K, sub = (int(v) for v in G[f"derive_{i}"])
+        assert ihs.derive_seed(seed, K) == sub
+        assert np.array_equal(ihs.sample_without_replacement(ihs.derive_seed(sub, 2), 4096, 257), G[f"rows_{i}"])
+    A, b, _ = ihs.synth_generate(3000, 12, decay=0.9, noise_std=0.01, outlier_frac=0.01, data_seed=7)
+    assert np.array_equal(A, G["A"]) and np.array_equal(b, G["b"])
+
+
+@pytest.mark.gpu
+def test_gpu_streams_match_golden(gpu):
+    for i in range(3):
+        sub = int(G[f"derive_{i}"][2])
+        assert np.array_equal(gpu.mt19937_64(gpu.derive_seed(sub, 1), 1024), G[f"mt_raw_{i}"])
+        assert np.array_equal(gpu.rademacher(gpu.derive_seed(sub, 1), 4096).astype(np.int8), G[f"signs_{i}"])
+        z = gpu.fill_gaussian(gpu.derive_seed(sub, 0), 37, 29, 1.0 / np.sqrt(37.0))
+        np.testing.assert_allclose(z, G[f"normals_{i}"], rtol=1e-15, atol=0)
+
+
+@pytest.mark.gpu
+def test_gpu_sketches_match_golden(gpu):
+    A = G["A"]
+    for m, seed in [(1, 0), (64, 3), (4096, 9)]:
+        assert np.array_equal(gpu.srht_sketch(A, m, seed), G[f"srht_m{m}_s{seed}"])
+    SA = gpu.gaussian_sketch(A, 40, 2)
+    ref = G["gauss_m40_s2"]
+    assert np.max(np.abs(SA - ref)) <= 1e-13 * np.abs(ref).max()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind,name", [(0, "gauss"), (1, "srht")])
+def test_gpu_solves_match_golden(gpu, kind, name):
+    A, b = G["A"], G["b"]
+    p = gpu.ProblemInstance(A, b, 0.05)
+    rep = gpu.adaptive_solve(p, gpu.SolverConfig(sketch_kind=gpu.SketchKind(kind), seed=3))
+    log = np.array([[e.t, e.m, int(e.branch)] for e in rep.log], dtype=np.int64)
+    assert np.array_equal(log, G[f"solve_{name}_log"])
+    assert [rep.iterations, rep.rejections, rep.final_m, int(rep.converged)] == list(G[f"solve_{name}_summary"])
+    c = rep.counters
+    assert [c.sketch, c.factor, c.solve, c.matvec] == [int(v) for v in G[f"solve_{name}_counters"]]
+    x_ref = G[f"solve_{name}_x"]
+    num = np.linalg.norm(np.concatenate([A @ (rep.x - x_ref), 0.05 * (rep.x - x_ref)]))
+    den = np.linalg.norm(np.concatenate([A @ x_ref, 0.05 * x_ref]))
+    assert num <= 1e-10 * den
