@@ -175,6 +175,23 @@ uint64_t ihs_derive_seed(uint64_t seed, uint64_t tag);   /* rng.hpp:23-28 */
 int64_t ihs_next_pow2(int64_t n);                        /* sketch.hpp:26-28 */
 void ihs_solver_config_default(ihs_solver_config* cfg);  /* solver.hpp:28-57 defaults */
 
+/* ------------------------------------------------------- row sharding
+ * H_{n_pad} = H_P (x) H_{n_pad/P}: rank r of P owns rows [r*n_loc, (r+1)*n_loc)
+ * of the padded index space, n_loc = next_pow2(n_global)/P.
+ * A sharded problem is created with ihs_gpu_problem_create on the local rows
+ * and opts {world_size, rank, nccl_comm, n_global, row_offset}; the SRHT
+ * partials are all-gathered and combined in the reference's butterfly order
+ * (bit-exact), gradient and Gaussian-sketch partials are summed (NCCL). */
+ihs_status ihs_gpu_shard_rows(int64_t n_global, int32_t world_size, int32_t rank, int64_t* row0, int64_t* rows);
+ihs_status ihs_gpu_nccl_unique_id(uint8_t out[128]);
+ihs_status ihs_gpu_nccl_comm_create(const uint8_t id[128], int32_t world_size, int32_t rank, int32_t device,
+                                    void** comm);
+void ihs_gpu_nccl_comm_destroy(void* comm);
+/* The sharded SRHT decomposition run back to back on one device (P virtual
+ * shards of a single-GPU problem): proves the decomposition bit-exact. */
+ihs_status ihs_gpu_sketch_sharded_emulated(ihs_gpu_problem* p, int32_t kind, int64_t m, uint64_t seed,
+                                           int32_t shards, double* SA_out);
+
 /* ------------------------------------------------------- problem (device) */
 /* ProblemInstance (problem.hpp:20-55): validates like the reference, uploads A
  * (n x d, column-major, leading dim lda) and b to the device once. */

@@ -68,6 +68,11 @@ def lib():
         "ihs_gpu_adaptive_solve": (C.c_int, [vp, P(abi.SolverConfigC), P(abi.SolveReportC)]),
         "ihs_gpu_fixed_sketch_ihs": (C.c_int, [vp, vp, P(abi.Tuning), i64, i32, d, d]),
         "ihs_synth_generate": (C.c_int, [P(abi.SynthSpec), i64, i64, d, i64, d, d]),
+        "ihs_gpu_shard_rows": (C.c_int, [i64, i32, i32, P(i64), P(i64)]),
+        "ihs_gpu_nccl_unique_id": (C.c_int, [P(C.c_uint8)]),
+        "ihs_gpu_nccl_comm_create": (C.c_int, [P(C.c_uint8), i32, i32, i32, P(vp)]),
+        "ihs_gpu_nccl_comm_destroy": (None, [vp]),
+        "ihs_gpu_sketch_sharded_emulated": (C.c_int, [vp, i32, i64, u64, i32, d]),
     }
     for name, (res, args) in sigs.items():
         fn = getattr(L, name)
@@ -86,5 +91,6 @@ EXPORTED_SYMBOLS = (
     "ihs_sample_without_replacement", "ihs_gpu_system_factorize", "ihs_gpu_system_destroy", "ihs_gpu_system_kind",
     "ihs_gpu_system_m", "ihs_gpu_system_d", "ihs_gpu_system_factor_flops", "ihs_gpu_system_flops_per_solve",
     "ihs_gpu_system_solve", "ihs_newton_decrement", "ihs_gpu_adaptive_solve", "ihs_gpu_fixed_sketch_ihs",
-    "ihs_synth_generate",
+    "ihs_synth_generate", "ihs_gpu_shard_rows", "ihs_gpu_nccl_unique_id", "ihs_gpu_nccl_comm_create",
+    "ihs_gpu_nccl_comm_destroy", "ihs_gpu_sketch_sharded_emulated",
 )

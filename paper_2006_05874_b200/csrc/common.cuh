@@ -55,7 +55,8 @@ void mt_rademacher_bits(uint64_t seed, int64_t n, uint32_t* d_bits, void* d_scra
 // order (polar method with cached second value); d_scratch sized by
 // gaussian_scratch_bytes(count).
 size_t gaussian_scratch_bytes(int64_t count);
-void mt_fill_gaussian(uint64_t seed, int64_t count, double stddev, double* d_out, void* d_scratch,
+// normals [first, first + count) of the stream (first > 0: a row shard's columns of S)
+void mt_fill_gaussian(uint64_t seed, int64_t first, int64_t count, double stddev, double* d_out, void* d_scratch,
                       cudaStream_t st);
 
 // srht.cu — SRHT sketch SA = sqrt(n_pad/m) R H D A (sketch.hpp:77-108)
@@ -74,6 +75,19 @@ void srht_build_entries(const SrhtPlan& p, const int64_t* rows, std::vector<int2
                         std::vector<int4>& tiles);
 void srht_run_device(const SrhtPlan& p, const double* d_A, const uint32_t* d_signbits, const int2* d_entries,
                      const int4* d_tiles, int n_tiles, double* d_T, double* d_SA, cudaStream_t st);
+// Row-sharded SRHT: plan of one shard (n_loc = n_pad / P rows, n_real of them
+// real) that emits unscaled partials at r_lo(k) for all m sampled rows, and the
+// combine of the P gathered partials ([P][m][d]) into SA (d_hi[k] = r_hi(k)).
+SrhtPlan srht_plan_shard(int64_t n_real, int64_t n_loc, int64_t d, int64_t lda, int64_t m);
+void srht_combine(const double* d_U, int P, int64_t m, int64_t d, const uint8_t* d_hi, double s1, double s2,
+                  double* d_SA, cudaStream_t st);
+
+// nccl_comm.cpp — collectives of the row-sharded path (NCCL loaded at run time)
+void nccl_unique_id(uint8_t out[128]);
+void* nccl_comm_create(const uint8_t id[128], int world, int rank);
+void nccl_comm_destroy(void* comm);
+void nccl_allreduce_sum(double* buf, size_t count, void* comm, cudaStream_t st);
+void nccl_allgather(const double* send, double* recv, size_t count_per_rank, void* comm, cudaStream_t st);
 
 // gemm_f64.cu — DMMA (mma.sync m8n8k4 f64) GEMM
 // C[M x N] (ldc) = alpha * op(A) * op(B) + beta * C ; op(A) is M x K, op(B) K x N.
@@ -101,7 +115,8 @@ struct GradPlan {
     int R;          // rows per panel
     int grid;       // persistent CTAs
     size_t smem;
-    int version;    // 2: smem-resident double-buffered panels; 1: L2 re-read (large d)
+    int version;    // 2: smem-resident panels in a cp.async ring; 1: L2 re-read (large d)
+    int stages;     // v2 ring depth
 };
 GradPlan grad_plan(int64_t n, int64_t d, int64_t lda, int num_sms);
 size_t grad_work_doubles(const GradPlan& p);
@@ -124,6 +139,7 @@ void gemv_n(const double* A, int64_t M, int64_t N, int64_t lda, const double* x,
 void woodbury_finish(const double* SA, int64_t m, int64_t d, const double* g, const double* w, double nu2, int nrhs,
                      double* z, cudaStream_t st);
 void add_diag(double* H, int64_t n, double v, cudaStream_t st);
+void add_scaled(double* y, const double* x, double a, int64_t n, cudaStream_t st);  // y = y + a x
 void check_finite(const double* v, int64_t count, int* d_flag, cudaStream_t st);
 
 }  // namespace ihs_b200

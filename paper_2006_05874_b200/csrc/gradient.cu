@@ -135,14 +135,22 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
-template <int NRHS, int RR, int MAXC>
+__device__ __forceinline__ void cp_async16(double* dst, const double* src) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(src));
+}
+
+// NS-stage ring of unpadded RR x d panels (16-byte cp.async.cg, L2 only);
+// sweep 2 reads each column with a rotation of (j*RR/16) rows so the 32 lanes
+// of a warp hit 16 distinct bank pairs.
+template <int NRHS, int RR, int MAXC, int NS>
 __global__ void __launch_bounds__(T2, 1)
 grad_smem_kernel(const double* __restrict__ A, int64_t d, int64_t lda, const double* __restrict__ b,
                  const double* __restrict__ X, double* __restrict__ work) {
     extern __shared__ double sm[];
-    const int64_t stage = d * (RR + 1);
-    double* panel = sm;                       // 2 stages
-    double* xs = panel + 2 * stage;           // NRHS * d
+    const int64_t stage = d * RR;
+    double* panel = sm;                       // NS stages
+    double* xs = panel + NS * stage;          // NRHS * d
     double* red = xs + NRHS * d;              // W2 * NRHS * RR
     double* rv = red + W2 * NRHS * RR;        // NRHS * RR
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -155,28 +163,26 @@ grad_smem_kernel(const double* __restrict__ A, int64_t d, int64_t lda, const dou
         for (int c = 0; c < MAXC; ++c) gacc[q][c] = 0.0;
 
     const int64_t npanels = lda / RR;
-    const int64_t elems = (int64_t)RR * d;
+    const int64_t chunks = (int64_t)RR * d / 2;  // 16-byte chunks per panel
     auto issue = [&](int64_t p, int s) {
-        double* dst = panel + s * stage;
-        const double* src = A + p * RR;
-        for (int64_t e = t; e < elems; e += T2) {
-            const int i = (int)(e % RR);
-            const int64_t j = e / RR;
-            cp_async8(dst + j * (RR + 1) + i, src + i + j * lda);
+        if (p < npanels) {
+            double* dst = panel + s * stage;
+            const double* src = A + p * RR;
+            for (int64_t c = t; c < chunks; c += T2) {
+                const int i = (int)(c % (RR / 2)) * 2;
+                const int64_t j = c / (RR / 2);
+                cp_async16(dst + j * RR + i, src + i + j * lda);
+            }
         }
-        cp_async_commit();
+        cp_async_commit();  // one group per slot, possibly empty, keeps the wait count uniform
     };
-    int s = 0;
     int64_t p = blockIdx.x;
-    if (p < npanels) issue(p, 0);
-    for (; p < npanels; p += gridDim.x, s ^= 1) {
-        const int64_t pn = p + gridDim.x;
-        if (pn < npanels) {
-            issue(pn, s ^ 1);
-            cp_async_wait<1>();
-        } else {
-            cp_async_wait<0>();
-        }
+#pragma unroll
+    for (int k = 0; k < NS - 1; ++k) issue(p + (int64_t)k * gridDim.x, k);
+    int s = 0;
+    for (; p < npanels; p += gridDim.x) {
+        issue(p + (int64_t)(NS - 1) * gridDim.x, (s + NS - 1) % NS);
+        cp_async_wait<NS - 1>();
         __syncthreads();
         const double* P = panel + s * stage;
         // ---- sweep 1: r = A_p x - b_p
@@ -188,7 +194,7 @@ grad_smem_kernel(const double* __restrict__ A, int64_t d, int64_t lda, const dou
 #pragma unroll
             for (int q = 0; q < NRHS; ++q) acc[q] = 0.0;
             for (int64_t j = jg; j < d; j += G) {
-                const double a = P[j * (RR + 1) + i];
+                const double a = P[j * RR + i];
 #pragma unroll
                 for (int q = 0; q < NRHS; ++q) acc[q] = fma(a, xs[q * d + j], acc[q]);
             }
@@ -214,17 +220,23 @@ grad_smem_kernel(const double* __restrict__ A, int64_t d, int64_t lda, const dou
         for (int c = 0; c < MAXC; ++c) {
             const int64_t j = t + (int64_t)c * T2;
             if (j < d) {
+                const int rot = (int)((j * RR / 16) & (RR - 1));
 #pragma unroll
                 for (int q = 0; q < NRHS; ++q) {
                     double sum = 0.0;
 #pragma unroll
-                    for (int i = 0; i < RR; ++i) sum = fma(P[j * (RR + 1) + i], rv[q * RR + i], sum);
+                    for (int i = 0; i < RR; ++i) {
+                        const int ii = (i + rot) & (RR - 1);
+                        sum = fma(P[j * RR + ii], rv[q * RR + ii], sum);
+                    }
                     gacc[q][c] += sum;
                 }
             }
         }
         __syncthreads();  // stage s is refilled by the next iteration's prefetch
+        s = (s + 1) % NS;
     }
+    cp_async_wait<0>();
 #pragma unroll
     for (int q = 0; q < NRHS; ++q)
 #pragma unroll
@@ -234,28 +246,43 @@ grad_smem_kernel(const double* __restrict__ A, int64_t d, int64_t lda, const dou
         }
 }
 
-size_t grad_smem_v2(int64_t d, int R, int nrhs) {
-    return sizeof(double) * ((size_t)2 * d * (R + 1) + (size_t)nrhs * d + (size_t)W2 * nrhs * R + (size_t)nrhs * R);
+size_t grad_smem_v2(int64_t d, int R, int nrhs, int ns) {
+    return sizeof(double) * ((size_t)ns * d * R + (size_t)nrhs * d + (size_t)W2 * nrhs * R + (size_t)nrhs * R);
 }
 
-template <int NRHS, int RR>
+template <int NRHS, int RR, int NS>
 void launch_v2(const GradPlan& p, const double* A, const double* b, const double* X, double* work, cudaStream_t st) {
-    const size_t smem = grad_smem_v2(p.d, RR, NRHS);
+    const size_t smem = grad_smem_v2(p.d, RR, NRHS, NS);
     const int maxc = (int)ceil_div(p.d, T2);
 #define IHS_V2(MC)                                                                                                  \
     do {                                                                                                            \
         static bool attr = false;                                                                                   \
         if (!attr) {                                                                                                \
-            CUDA_CHECK(cudaFuncSetAttribute(grad_smem_kernel<NRHS, RR, MC>,                                         \
+            CUDA_CHECK(cudaFuncSetAttribute(grad_smem_kernel<NRHS, RR, MC, NS>,                                     \
                                             cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));              \
             attr = true;                                                                                            \
         }                                                                                                           \
-        LAUNCH((grad_smem_kernel<NRHS, RR, MC>), p.grid, T2, smem, st, A, p.d, p.lda, b, X, work);                  \
+        LAUNCH((grad_smem_kernel<NRHS, RR, MC, NS>), p.grid, T2, smem, st, A, p.d, p.lda, b, X, work);              \
     } while (0)
     if (maxc <= 1) IHS_V2(1);
     else if (maxc <= 2) IHS_V2(2);
     else IHS_V2(4);
 #undef IHS_V2
+}
+
+template <int NRHS>
+void launch_v2_dispatch(const GradPlan& p, const double* A, const double* b, const double* X, double* work,
+                        cudaStream_t st) {
+    const int key = p.R * 10 + p.stages;
+    switch (key) {
+        case 163: launch_v2<NRHS, 16, 3>(p, A, b, X, work, st); break;
+        case 164: launch_v2<NRHS, 16, 4>(p, A, b, X, work, st); break;
+        case 83: launch_v2<NRHS, 8, 3>(p, A, b, X, work, st); break;
+        case 84: launch_v2<NRHS, 8, 4>(p, A, b, X, work, st); break;
+        case 42: launch_v2<NRHS, 4, 2>(p, A, b, X, work, st); break;
+        case 43: launch_v2<NRHS, 4, 3>(p, A, b, X, work, st); break;
+        default: fail(IHS_INTERNAL_ERROR, "gradient: no kernel for the chosen panel geometry");
+    }
 }
 
 // G[q][j] = sum_c work[c][q][j] (fixed order) + nu2 * X[q][j]
@@ -295,19 +322,23 @@ GradPlan grad_plan(int64_t n, int64_t d, int64_t lda, int num_sms) {
     p.n = n;
     p.d = d;
     p.lda = lda;
-    // v2 when a double-buffered panel of >= 4 rows fits; prefer 2 CTAs/SM and 64 B column segments
-    struct Cand { int R, per_sm; };
-    const Cand cands[] = {{16, 2}, {8, 2}, {8, 1}, {4, 2}, {4, 1}};
+    // v2: one 512-thread CTA per SM streaming R x d panels through an NS-deep
+    // cp.async ring (>= 3 x 64 KiB in flight per SM when it fits); prefer
+    // 128/64 B column segments (R = 16/8), fall back to 32 B (R = 4).
+    struct Cand { int R, ns; };
+    const Cand cands[] = {{16, 4}, {16, 3}, {8, 4}, {8, 3}, {4, 3}, {4, 2}};
     p.version = 1;
     if (lda % 32 == 0 && d <= 2048) {
         for (const Cand& c : cands) {
-            const size_t sm = grad_smem_v2(d, c.R, 2);
-            if (sm <= (c.per_sm == 2 ? 110u * 1024 : 215u * 1024)) {
+            const size_t sm = grad_smem_v2(d, c.R, 2, c.ns);
+            const size_t stage_bytes = (size_t)c.R * d * 8;
+            if (sm <= 215u * 1024 && stage_bytes <= 64u * 1024) {
                 p.version = 2;
                 p.R = c.R;
+                p.stages = c.ns;
                 p.smem = sm;
                 const int64_t npanels = lda / c.R;
-                p.grid = (int)std::max<int64_t>(1, std::min<int64_t>(npanels, (int64_t)num_sms * c.per_sm));
+                p.grid = (int)std::max<int64_t>(1, std::min<int64_t>(npanels, (int64_t)num_sms));
                 return p;
             }
         }
@@ -325,15 +356,8 @@ size_t grad_work_doubles(const GradPlan& p) { return (size_t)p.grid * 2 * p.d; }
 void grad_run(const GradPlan& p, const double* d_A, const double* d_b, double nu2, const double* d_X, int nrhs,
               double* d_G, double* d_work, cudaStream_t st) {
     if (p.version == 2) {
-        if (nrhs == 1) {
-            if (p.R == 16) launch_v2<1, 16>(p, d_A, d_b, d_X, d_work, st);
-            else if (p.R == 8) launch_v2<1, 8>(p, d_A, d_b, d_X, d_work, st);
-            else launch_v2<1, 4>(p, d_A, d_b, d_X, d_work, st);
-        } else {
-            if (p.R == 16) launch_v2<2, 16>(p, d_A, d_b, d_X, d_work, st);
-            else if (p.R == 8) launch_v2<2, 8>(p, d_A, d_b, d_X, d_work, st);
-            else launch_v2<2, 4>(p, d_A, d_b, d_X, d_work, st);
-        }
+        if (nrhs == 1) launch_v2_dispatch<1>(p, d_A, d_b, d_X, d_work, st);
+        else launch_v2_dispatch<2>(p, d_A, d_b, d_X, d_work, st);
         const int64_t total = (int64_t)nrhs * p.d;
         LAUNCH(grad_reduce_kernel, (unsigned)ceil_div(total, 16), 256, 0, st, d_work, p.grid, p.d, nrhs, d_X, nu2,
                d_G);

@@ -181,16 +181,18 @@ __global__ void polar_flags_kernel(const uint64_t* __restrict__ raw, int64_t att
     }
 }
 
+// normals [first, first + count) of the stream -> out[0 .. count)
 __global__ void polar_emit_kernel(const uint64_t* __restrict__ raw, int64_t attempts, const int* __restrict__ pos,
-                                  int64_t count, double stddev, double* __restrict__ out) {
+                                  int64_t first, int64_t count, double stddev, double* __restrict__ out) {
+    const int64_t end = first + count;
     for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < attempts; a += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t k = 2 * (int64_t)pos[a];
+        if (k >= end || k + 1 < first) continue;
         double x, y, r2;
         if (!polar_attempt(raw, a, x, y, r2)) continue;
-        const int64_t k = 2 * (int64_t)pos[a];
-        if (k >= count) continue;
         const double mult = __dsqrt_rn(__ddiv_rn(__dmul_rn(-2.0, log(r2)), r2));
-        out[k] = __dadd_rn(__dmul_rn(__dmul_rn(y, mult), stddev), 0.0);
-        if (k + 1 < count) out[k + 1] = __dadd_rn(__dmul_rn(__dmul_rn(x, mult), stddev), 0.0);
+        if (k >= first) out[k - first] = __dadd_rn(__dmul_rn(__dmul_rn(y, mult), stddev), 0.0);
+        if (k + 1 >= first && k + 1 < end) out[k + 1 - first] = __dadd_rn(__dmul_rn(__dmul_rn(x, mult), stddev), 0.0);
     }
 }
 
@@ -246,9 +248,10 @@ size_t gaussian_scratch_bytes(int64_t count) {
     return (size_t)draws * 8 + (size_t)attempts * 8 + temp + 256 + (size_t)nsub * NN * 8 + (size_t)kJumpSeqWords * 8 + 1024;
 }
 
-void mt_fill_gaussian(uint64_t seed, int64_t count, double stddev, double* d_out, void* d_scratch, cudaStream_t st) {
+void mt_fill_gaussian(uint64_t seed, int64_t first, int64_t count, double stddev, double* d_out, void* d_scratch,
+                      cudaStream_t st) {
     if (count <= 0) return;
-    const int64_t draws = draws_for(count);
+    const int64_t draws = draws_for(first + count);
     const int64_t attempts = draws / 2;
     if (attempts >= (int64_t)INT32_MAX) fail(IHS_INVALID_INPUT, "fill_gaussian: stream longer than 2^31 attempts");
     char* p = static_cast<char*>(d_scratch);
@@ -285,8 +288,8 @@ void mt_fill_gaussian(uint64_t seed, int64_t count, double stddev, double* d_out
     long long h_total = 0;
     CUDA_CHECK(cudaMemcpyAsync(&h_total, total, sizeof(long long), cudaMemcpyDeviceToHost, st));
     CUDA_CHECK(cudaStreamSynchronize(st));
-    if (2 * h_total < count) fail(IHS_INTERNAL_ERROR, "fill_gaussian: draw estimate too small");
-    LAUNCH(polar_emit_kernel, blocks, threads, 0, st, raw, attempts, pos, count, stddev, d_out);
+    if (2 * h_total < first + count) fail(IHS_INTERNAL_ERROR, "fill_gaussian: draw estimate too small");
+    LAUNCH(polar_emit_kernel, blocks, threads, 0, st, raw, attempts, pos, first, count, stddev, d_out);
 }
 
 }  // namespace ihs_b200

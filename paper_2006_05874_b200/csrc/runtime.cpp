@@ -250,6 +250,7 @@ struct ihs_gpu_problem {
     DevBuf grad_work;
     // sketch workspaces
     DevBuf T, signbits, rng_scratch, entries, tiles, gauss_scratch, S, gemm_work;
+    DevBuf shard_U, shard_hi;    // sharded SRHT partials [P][m][d] and r_hi(k)
     PinnedBuf h_stage;
     std::vector<int64_t> h_rows;
     std::vector<int2> h_entries;
@@ -265,13 +266,35 @@ namespace ihs_b200 {
 namespace {
 
 // -------------------------------------------------------- sketches (device)
-// SA (m x d, ld m, device) = apply_sketch(A, {kind, m, seed}) (sketch.hpp:110-117)
-void device_sketch(ihs_gpu_problem* P, int kind, int64_t m, uint64_t seed, double* d_SA, ihs_counters* c) {
+// Upload host-built SRHT entries/tiles through the pinned staging buffer.
+void upload_entries(ihs_gpu_problem* P) {
+    cudaStream_t st = P->st;
+    const size_t eb = P->h_entries.size() * sizeof(int2), tb = P->h_tiles.size() * sizeof(int4);
+    P->h_stage.ensure(eb + tb + 64);
+    // the previous sketch's copy out of the staging buffer must be done
+    CUDA_CHECK(cudaStreamSynchronize(st));
+    std::memcpy(P->h_stage.p, P->h_entries.data(), eb);
+    std::memcpy(static_cast<char*>(P->h_stage.p) + eb, P->h_tiles.data(), tb);
+    P->entries.ensure(eb + 16);
+    P->tiles.ensure(tb + 16);
+    CUDA_CHECK(cudaMemcpyAsync(P->entries.p, P->h_stage.p, eb, cudaMemcpyHostToDevice, st));
+    CUDA_CHECK(cudaMemcpyAsync(P->tiles.p, static_cast<char*>(P->h_stage.p) + eb, tb, cudaMemcpyHostToDevice, st));
+}
+
+// SA (m x d, ld m, device) = apply_sketch(A, {kind, m, seed}) (sketch.hpp:110-117).
+// Row-sharded problems (world_size > 1) compute their shard's part and
+// exchange it over NCCL; `emulate_shards` > 1 runs the same sharded SRHT
+// decomposition on one device (shards back to back), which the tests use to
+// prove the decomposition bit-exact.
+void device_sketch(ihs_gpu_problem* P, int kind, int64_t m, uint64_t seed, double* d_SA, ihs_counters* c,
+                   int emulate_shards = 1) {
     const int64_t n = P->n, d = P->d;
+    const int world = P->opts.world_size;
+    const int64_t n_glob = world > 1 ? P->opts.n_global : n;
     cudaStream_t st = P->st;
     if (kind == IHS_SKETCH_SRHT) {
         if (m < 1) fail(IHS_INVALID_INPUT, "srht_sketch: m must be >= 1");
-        const SrhtPlan plan = srht_plan(n, d, P->lda, m);
+        const SrhtPlan plan = srht_plan(n_glob, d, P->lda, m);
         if (m > plan.n_pad) fail(IHS_SKETCH_TOO_LARGE, "srht_sketch: m exceeds padded row count");
         // D: rademacher(n_pad, make_stream(seed, 1)) as bits (sketch.hpp:85,87)
         P->signbits.ensure((size_t)((plan.n_pad + 31) / 32) * 4);
@@ -281,39 +304,73 @@ void device_sketch(ihs_gpu_problem* P, int kind, int64_t m, uint64_t seed, doubl
         P->h_rows.resize((size_t)m);
         const auto t_rng = std::chrono::steady_clock::now();
         sample_without_replacement(derive_seed(seed, 2), plan.n_pad, m, P->h_rows.data());
-        srht_build_entries(plan, P->h_rows.data(), P->h_entries, P->h_tiles);
-        g_host_rng_ns += std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t_rng).count();
-        const size_t eb = P->h_entries.size() * sizeof(int2), tb = P->h_tiles.size() * sizeof(int4);
-        P->h_stage.ensure(eb + tb + 64);
-        // the previous sketch's copy out of the staging buffer must be done
-        CUDA_CHECK(cudaStreamSynchronize(st));
-        std::memcpy(P->h_stage.p, P->h_entries.data(), eb);
-        std::memcpy(static_cast<char*>(P->h_stage.p) + eb, P->h_tiles.data(), tb);
-        P->entries.ensure(eb + 16);
-        P->tiles.ensure(tb + 16);
-        CUDA_CHECK(cudaMemcpyAsync(P->entries.p, P->h_stage.p, eb, cudaMemcpyHostToDevice, st));
-        CUDA_CHECK(cudaMemcpyAsync(P->tiles.p, static_cast<char*>(P->h_stage.p) + eb, tb, cudaMemcpyHostToDevice, st));
-        P->T.ensure(srht_scratch_bytes(plan));
-        srht_run_device(plan, P->A.d(), P->signbits.as<uint32_t>(), P->entries.as<int2>(), P->tiles.as<int4>(),
-                        (int)P->h_tiles.size(), P->T.d(), d_SA, st);
+        const int shards = world > 1 ? world : std::max(1, emulate_shards);
+        if (shards == 1) {
+            srht_build_entries(plan, P->h_rows.data(), P->h_entries, P->h_tiles);
+            g_host_rng_ns +=
+                std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t_rng).count();
+            upload_entries(P);
+            P->T.ensure(srht_scratch_bytes(plan));
+            srht_run_device(plan, P->A.d(), P->signbits.as<uint32_t>(), P->entries.as<int2>(), P->tiles.as<int4>(),
+                            (int)P->h_tiles.size(), P->T.d(), d_SA, st);
+        } else {
+            // shard p holds rows [p*n_loc, (p+1)*n_loc) of the padded index space
+            const int64_t n_loc = plan.n_pad / shards;
+            std::vector<int64_t> lo((size_t)m);
+            std::vector<uint8_t> hi((size_t)m);
+            for (int64_t k = 0; k < m; ++k) {
+                lo[(size_t)k] = P->h_rows[(size_t)k] % n_loc;
+                hi[(size_t)k] = (uint8_t)(P->h_rows[(size_t)k] / n_loc);
+            }
+            const SrhtPlan sp = srht_plan_shard(std::min(n_loc, n), n_loc, d, P->lda, m);
+            srht_build_entries(sp, lo.data(), P->h_entries, P->h_tiles);
+            g_host_rng_ns +=
+                std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t_rng).count();
+            upload_entries(P);
+            P->shard_hi.ensure((size_t)m + 16);
+            CUDA_CHECK(cudaMemcpyAsync(P->shard_hi.p, hi.data(), (size_t)m, cudaMemcpyHostToDevice, st));
+            P->shard_U.ensure((size_t)shards * m * d * sizeof(double));
+            P->T.ensure(srht_scratch_bytes(sp));
+            double* U = P->shard_U.d();
+            auto run_shard = [&](int p, const double* A_p, int64_t n_real) {
+                SrhtPlan s = sp;
+                s.n = n_real;
+                srht_run_device(s, A_p, P->signbits.as<uint32_t>() + (p * n_loc) / 32, P->entries.as<int2>(),
+                                P->tiles.as<int4>(), (int)P->h_tiles.size(), P->T.d(), U + (int64_t)p * m * d, st);
+            };
+            if (world > 1) {
+                const int r = P->opts.rank;
+                run_shard(r, P->A.d(), n);
+                nccl_allgather(U + (int64_t)r * m * d, U, (size_t)(m * d), P->opts.nccl_comm, st);
+            } else {
+                for (int p = 0; p < shards; ++p) {
+                    const int64_t n_real = std::max<int64_t>(0, std::min<int64_t>(n_loc, n - p * n_loc));
+                    run_shard(p, P->A.d() + p * n_loc, n_real);
+                }
+            }
+            srht_combine(U, shards, m, d, P->shard_hi.as<uint8_t>(), plan.scale1, plan.scale2, d_SA, st);
+        }
         if (c) {  // sketch.hpp:99-106
             const uint64_t np = (uint64_t)plan.n_pad, dd = (uint64_t)d;
-            c->sketch += dd * np * (uint64_t)plan.logn + (uint64_t)n * dd + (uint64_t)m * dd;
+            c->sketch += dd * np * (uint64_t)plan.logn + (uint64_t)n_glob * dd + (uint64_t)m * dd;
         }
     } else if (kind == IHS_SKETCH_GAUSSIAN) {
         if (m < 1) fail(IHS_INVALID_INPUT, "gaussian_sketch: m must be >= 1");
-        // S (m x n) ~ N(0, 1/m) from make_stream(seed, 0), column-major (sketch.hpp:62-64)
+        // S (m x n) ~ N(0, 1/m) from make_stream(seed, 0), column-major (sketch.hpp:62-64);
+        // a shard holds the columns of its rows, i.e. normals [row0*m, (row0+n)*m)
         const int64_t count = m * n;
+        const int64_t first = world > 1 ? P->opts.row_offset * m : 0;
         P->S.ensure((size_t)count * sizeof(double));
-        P->gauss_scratch.ensure(gaussian_scratch_bytes(count));
+        P->gauss_scratch.ensure(gaussian_scratch_bytes(first + count));
         const double stddev = 1.0 / std::sqrt(static_cast<double>(m));
-        mt_fill_gaussian(derive_seed(seed, 0), count, stddev, P->S.d(), P->gauss_scratch.p, st);
+        mt_fill_gaussian(derive_seed(seed, 0), first, count, stddev, P->S.d(), P->gauss_scratch.p, st);
         // SA = S * A on the DMMA path (sketch.hpp:68)
         const int splitk = dgemm_pick_splitk(m, d, n, P->num_sms);
         if (splitk > 1) P->gemm_work.ensure((size_t)splitk * m * d * sizeof(double));
         dgemm(false, false, m, d, n, 1.0, P->S.d(), m, P->A.d(), P->lda, 0.0, d_SA, m, false, splitk,
               splitk > 1 ? P->gemm_work.d() : nullptr, st);
-        if (c) c->sketch += (uint64_t)m * (uint64_t)n * (uint64_t)d;  // sketch.hpp:65-67
+        if (world > 1) nccl_allreduce_sum(d_SA, (size_t)(m * d), P->opts.nccl_comm, st);
+        if (c) c->sketch += (uint64_t)m * (uint64_t)n_glob * (uint64_t)d;  // sketch.hpp:65-67
     } else {
         fail(IHS_INVALID_INPUT, "apply_sketch: unknown sketch kind");
     }
@@ -395,8 +452,18 @@ void alloc_and_upload(ihs_gpu_problem* P, const double* A, int64_t lda_host, con
     upload_Ab(P, A, lda_host, b);
 }
 
+// g = A^T(Ax - b) + nu^2 x; on a row-sharded problem the A_p^T(A_p x - b_p)
+// partials are summed over NCCL (identical bytes on every rank) before the
+// nu^2 x term is added once.
 void problem_grad(ihs_gpu_problem* P, const double* X, int nrhs, double* G) {
-    grad_run(P->gplan, P->A.d(), P->b.d(), P->nu * P->nu, X, nrhs, G, P->grad_work.d(), P->st);
+    const double nu2 = P->nu * P->nu;
+    if (P->opts.world_size > 1) {
+        grad_run(P->gplan, P->A.d(), P->b.d(), 0.0, X, nrhs, G, P->grad_work.d(), P->st);
+        nccl_allreduce_sum(G, (size_t)nrhs * P->d, P->opts.nccl_comm, P->st);
+        add_scaled(G, X, nu2, (int64_t)nrhs * P->d, P->st);
+    } else {
+        grad_run(P->gplan, P->A.d(), P->b.d(), nu2, X, nrhs, G, P->grad_work.d(), P->st);
+    }
 }
 
 }  // namespace
@@ -497,6 +564,54 @@ ihs_status ihs_newton_decrement(const double* g, const double* gt, int64_t d, do
     });
 }
 
+// ------------------------------------------------------------------ sharding
+ihs_status ihs_gpu_shard_rows(int64_t n_global, int32_t world_size, int32_t rank, int64_t* row0, int64_t* rows) {
+    return guarded([&] {
+        if (n_global < 1 || world_size < 1 || rank < 0 || rank >= world_size)
+            fail(IHS_INVALID_INPUT, "shard_rows: bad arguments");
+        const int64_t n_loc = ihs_next_pow2(n_global) / world_size;
+        if (n_loc < 32) fail(IHS_INVALID_INPUT, "shard_rows: fewer than 32 padded rows per shard");
+        *row0 = (int64_t)rank * n_loc;
+        *rows = std::max<int64_t>(0, std::min<int64_t>(n_loc, n_global - *row0));
+        if (*rows < 1) fail(IHS_INVALID_INPUT, "shard_rows: a shard would hold no real rows");
+    });
+}
+
+ihs_status ihs_gpu_nccl_unique_id(uint8_t out[128]) {
+    return guarded([&] { nccl_unique_id(out); });
+}
+
+ihs_status ihs_gpu_nccl_comm_create(const uint8_t id[128], int32_t world_size, int32_t rank, int32_t device,
+                                    void** comm) {
+    return guarded([&] {
+        DeviceGuard g(device);
+        *comm = nccl_comm_create(id, world_size, rank);
+    });
+}
+
+void ihs_gpu_nccl_comm_destroy(void* comm) {
+    try {
+        nccl_comm_destroy(comm);
+    } catch (...) {
+    }
+}
+
+ihs_status ihs_gpu_sketch_sharded_emulated(ihs_gpu_problem* P, int32_t kind, int64_t m, uint64_t seed,
+                                           int32_t shards, double* SA_out) {
+    return guarded([&] {
+        if (!P || !SA_out) fail(IHS_INVALID_INPUT, "null argument");
+        if (P->opts.world_size > 1) fail(IHS_INVALID_INPUT, "emulation runs on a single-GPU problem");
+        if (kind != IHS_SKETCH_SRHT) fail(IHS_INVALID_INPUT, "sharded emulation covers the SRHT");
+        DeviceGuard dg(P->device);
+        StreamScope scope(P->st);
+        DevBuf SA;
+        SA.ensure((size_t)m * P->d * sizeof(double));
+        device_sketch(P, kind, m, seed, SA.d(), nullptr, shards);
+        CUDA_CHECK(cudaMemcpyAsync(SA_out, SA.p, (size_t)m * P->d * sizeof(double), cudaMemcpyDeviceToHost, P->st));
+        CUDA_CHECK(cudaStreamSynchronize(P->st));
+    });
+}
+
 // ------------------------------------------------------------------ problem
 ihs_status ihs_gpu_problem_create(const double* A, int64_t n, int64_t d, int64_t lda, const double* b, double nu,
                                   int32_t orientation, const ihs_gpu_options* opts, ihs_gpu_problem** out) {
@@ -521,10 +636,20 @@ ihs_status ihs_gpu_problem_create(const double* A, int64_t n, int64_t d, int64_t
         P->device = opts ? opts->device : 0;
         if (opts) P->opts = *opts;
         if (P->opts.world_size < 1) P->opts.world_size = 1;
-        if (P->opts.world_size > 1)
-            fail(IHS_INVALID_INPUT, "ihs_gpu: multi-rank problems are created through ihs_gpu_problem_create_sharded");
-        P->opts.n_global = n;
-        P->opts.row_offset = 0;
+        if (P->opts.world_size > 1) {
+            // row shard of the padded index space: rank r owns [r*n_loc, (r+1)*n_loc)
+            const int w = P->opts.world_size, r = P->opts.rank;
+            if ((w & (w - 1)) != 0 || w > 16) fail(IHS_INVALID_INPUT, "sharded problem: world_size must be 2, 4, 8 or 16");
+            if (r < 0 || r >= w) fail(IHS_INVALID_INPUT, "sharded problem: rank out of range");
+            if (!P->opts.nccl_comm) fail(IHS_INVALID_INPUT, "sharded problem: nccl_comm is required");
+            int64_t row0 = 0, rows = 0;
+            if (ihs_gpu_shard_rows(P->opts.n_global, w, r, &row0, &rows) != IHS_OK) fail(IHS_INVALID_INPUT, g_last_error);
+            if (P->opts.row_offset != row0 || n != rows)
+                fail(IHS_INVALID_INPUT, "sharded problem: local rows must be ihs_gpu_shard_rows(n_global, world, rank)");
+        } else {
+            P->opts.n_global = n;
+            P->opts.row_offset = 0;
+        }
         DeviceGuard g(P->device);
         P->n = n;
         P->d = d;
@@ -697,7 +822,7 @@ ihs_status ihs_gpu_fill_gaussian(uint64_t stream_seed, int64_t rows, int64_t col
         DevBuf o, scratch;
         o.ensure((size_t)count * 8);
         scratch.ensure(gaussian_scratch_bytes(count));
-        mt_fill_gaussian(stream_seed, count, stddev, o.d(), scratch.p, 0);
+        mt_fill_gaussian(stream_seed, 0, count, stddev, o.d(), scratch.p, 0);
         CUDA_CHECK(cudaMemcpy(out, o.p, (size_t)count * 8, cudaMemcpyDeviceToHost));
     });
 }

@@ -261,6 +261,34 @@ srht_phase2_kernel(double* __restrict__ T, int64_t n_pad, int lo, const int4* __
     }
 }
 
+// Row-sharded SRHT combine (H_{n_pad} = H_P (x) H_{n_pad/P}, shard index =
+// top log2(P) row bits): U holds every shard's unscaled partial T_p[r_lo(k)]
+// for every sampled row k ([P][m][d], shard-major, as an all-gather lays it
+// out). The top stages run over p in increasing bit order exactly like the
+// reference's high butterflies; the value at p = r_hi(k) is scaled twice.
+template <int LOGP>
+__global__ void srht_combine_kernel(const double* __restrict__ U, int64_t m, int64_t d,
+                                    const uint8_t* __restrict__ hi, double s1, double s2, double* __restrict__ SA) {
+    constexpr int P = 1 << LOGP;
+    const int64_t md = m * d;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < md; e += (int64_t)gridDim.x * blockDim.x) {
+        double v[P];
+#pragma unroll
+        for (int p = 0; p < P; ++p) v[p] = U[p * md + e];
+#pragma unroll
+        for (int s = 0; s < LOGP; ++s)
+#pragma unroll
+            for (int p = 0; p < P; ++p)
+                if (!(p & (1 << s))) bfly(v[p], v[p | (1 << s)]);
+        const int target = hi[e % m];
+        double out = v[0];
+#pragma unroll
+        for (int p = 1; p < P; ++p)
+            if (p == target) out = v[p];
+        SA[e] = __dmul_rn(__dmul_rn(out, s1), s2);
+    }
+}
+
 int pass_w(int hb) {
     const int rb1 = std::min(hb, 5);
     return kP2Threads * (1 << rb1) / (1 << hb);
@@ -339,6 +367,29 @@ SrhtPlan srht_plan(int64_t n, int64_t d, int64_t lda, int64_t m) {
     p.scale1 = 1.0 / std::sqrt(static_cast<double>(np));
     p.scale2 = std::sqrt(static_cast<double>(np) / static_cast<double>(m));
     return p;
+}
+
+SrhtPlan srht_plan_shard(int64_t n_real, int64_t n_loc, int64_t d, int64_t lda, int64_t m) {
+    if (n_loc < 32 || (n_loc & (n_loc - 1)) != 0) fail(IHS_INVALID_INPUT, "srht shard: rows per shard must be 2^k >= 32");
+    SrhtPlan p = srht_plan(n_loc, d, lda, m);  // geometry of an n_loc-row transform
+    p.n = n_real;                               // rows >= n_real are virtual zeros
+    p.scale1 = 1.0;                             // unscaled partials; the combine applies both scalings
+    p.scale2 = 1.0;
+    return p;
+}
+
+void srht_combine(const double* d_U, int P, int64_t m, int64_t d, const uint8_t* d_hi, double s1, double s2,
+                  double* d_SA, cudaStream_t st) {
+    const int64_t md = m * d;
+    const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(md, 256), 148 * 16));
+    switch (P) {
+        case 1: LAUNCH(srht_combine_kernel<0>, blocks, 256, 0, st, d_U, m, d, d_hi, s1, s2, d_SA); break;
+        case 2: LAUNCH(srht_combine_kernel<1>, blocks, 256, 0, st, d_U, m, d, d_hi, s1, s2, d_SA); break;
+        case 4: LAUNCH(srht_combine_kernel<2>, blocks, 256, 0, st, d_U, m, d, d_hi, s1, s2, d_SA); break;
+        case 8: LAUNCH(srht_combine_kernel<3>, blocks, 256, 0, st, d_U, m, d, d_hi, s1, s2, d_SA); break;
+        case 16: LAUNCH(srht_combine_kernel<4>, blocks, 256, 0, st, d_U, m, d, d_hi, s1, s2, d_SA); break;
+        default: fail(IHS_INVALID_INPUT, "srht shard: number of shards must be 1, 2, 4, 8 or 16");
+    }
 }
 
 size_t srht_scratch_bytes(const SrhtPlan& p) { return p.H > 0 ? (size_t)p.n_pad * (size_t)p.d * sizeof(double) : 0; }

@@ -88,6 +88,11 @@ __global__ void woodbury_finish_kernel(const double* __restrict__ SA, int64_t m,
     }
 }
 
+__global__ void add_scaled_kernel(double* __restrict__ y, const double* __restrict__ x, double a, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        y[i] = y[i] + a * x[i];
+}
+
 __global__ void add_diag_kernel(double* __restrict__ H, int64_t n, double v) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         H[i + i * n] += v;
@@ -125,6 +130,10 @@ void gemv_n(const double* A, int64_t M, int64_t N, int64_t lda, const double* x,
 void woodbury_finish(const double* SA, int64_t m, int64_t d, const double* g, const double* w, double nu2, int nrhs,
                      double* z, cudaStream_t st) {
     LAUNCH(woodbury_finish_kernel, blocks_for(d * 32, 256), 256, 0, st, SA, m, d, g, w, nu2, nrhs, z);
+}
+
+void add_scaled(double* y, const double* x, double a, int64_t n, cudaStream_t st) {
+    LAUNCH(add_scaled_kernel, blocks_for(n, 256), 256, 0, st, y, x, a, n);
 }
 
 void add_diag(double* H, int64_t n, double v, cudaStream_t st) {

@@ -227,21 +227,60 @@ def _vec(x, n=None) -> np.ndarray:
     return x
 
 
+def shard_rows(n_global: int, world_size: int, rank: int):
+    """(row0, rows) of rank's shard: rows [r*n_loc, (r+1)*n_loc) of the padded index space."""
+    r0, rows = C.c_int64(), C.c_int64()
+    _check(lib().ihs_gpu_shard_rows(n_global, world_size, rank, C.byref(r0), C.byref(rows)))
+    return int(r0.value), int(rows.value)
+
+
+def nccl_unique_id() -> bytes:
+    buf = (C.c_uint8 * 128)()
+    _check(lib().ihs_gpu_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+class NcclComm:
+    """NCCL communicator owned by the library (the id travels over torch.distributed)."""
+
+    def __init__(self, uid: bytes, world_size: int, rank: int, device: int):
+        buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+        h = C.c_void_p()
+        _check(lib().ihs_gpu_nccl_comm_create(buf, world_size, rank, device, C.byref(h)))
+        self.handle = h
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h:
+            lib().ihs_gpu_nccl_comm_destroy(h)
+            self.handle = None
+
+
 class ProblemInstance:
     """A regularized least-squares instance, uploaded to the device once.
 
     minimize_x 1/2 ||A x - b||^2 + nu^2/2 ||x||^2 (problem.hpp:15-55).
+    For a row-sharded problem pass the local rows (see shard_rows) together
+    with world_size, rank, comm (NcclComm) and n_global.
     """
 
-    def __init__(self, A, b, nu: float, orientation: Orientation = Orientation.Overdetermined, device: int = 0):
+    def __init__(self, A, b, nu: float, orientation: Orientation = Orientation.Overdetermined, device: int = 0,
+                 world_size: int = 1, rank: int = 0, comm: Optional["NcclComm"] = None, n_global: Optional[int] = None):
         self._A = _fortran(A)
         self._b = _vec(b)
         self._nu = float(nu)
         self._orientation = Orientation(orientation)
+        self._comm = comm
         n, d = self._A.shape
         if self._b.size != n and n >= 1 and d >= 1 and self._nu > 0:
             raise InvalidInput("ProblemInstance: size of b must match rows of A")
-        opts = abi.GpuOptions(device=device, world_size=1, rank=0, nccl_comm=None, n_global=n, row_offset=0)
+        if world_size > 1:
+            row0, _ = shard_rows(n_global, world_size, rank)
+            opts = abi.GpuOptions(device=device, world_size=world_size, rank=rank,
+                                  nccl_comm=comm.handle if comm is not None else None, n_global=n_global,
+                                  row_offset=row0)
+        else:
+            opts = abi.GpuOptions(device=device, world_size=1, rank=0, nccl_comm=None, n_global=n, row_offset=0)
         h = C.c_void_p()
         _check(lib().ihs_gpu_problem_create(abi.dptr(self._A) if self._A.size else None, n, d, max(n, 1),
                                             abi.dptr(self._b) if self._b.size else None, self._nu,
@@ -340,6 +379,13 @@ def gaussian_sketch(A, m: int, seed: int, counters: Optional[CostCounters] = Non
 
 def srht_sketch(A, m: int, seed: int, counters: Optional[CostCounters] = None) -> np.ndarray:
     return _sketch(A, abi.SKETCH_SRHT, m, seed, counters)
+
+
+def srht_sketch_sharded_emulated(p: ProblemInstance, m: int, seed: int, shards: int) -> np.ndarray:
+    """SRHT through the row-sharded decomposition run on one device (test vehicle)."""
+    SA = np.empty((m, p.cols()), order="F")
+    _check(lib().ihs_gpu_sketch_sharded_emulated(p.handle, abi.SKETCH_SRHT, m, seed, shards, abi.dptr(SA)))
+    return SA
 
 
 def apply_sketch(A, cfg: SketchConfig, counters: Optional[CostCounters] = None) -> np.ndarray:

@@ -89,6 +89,18 @@ def test_srht_sketch_bit_exact(gpu, O, n, d, m, seed):
     assert c_gpu.sketch == c_or.sketch
 
 
+@pytest.mark.parametrize("n,d,m,seed,shards", [
+    (1000, 3, 64, 11, 2), (4096, 5, 4096, 2, 2), (3500, 4, 333, 5, 4), (100000, 3, 5000, 7, 8),
+    ((1 << 20) - 5, 2, 20000, 1, 8), (1 << 16, 6, 1024, 3, 16)])
+def test_sharded_srht_kernels_bit_exact(gpu, O, n, d, m, seed, shards):
+    """The row-sharded SRHT kernels (shard transform + all-gather layout + combine),
+    run as P virtual shards on one device, equal the unsharded sketch bit for bit."""
+    A = rand_mat(n * d, n, d)
+    p = gpu.ProblemInstance(A, np.zeros(n), 1.0)
+    SA = gpu.srht_sketch_sharded_emulated(p, m, seed, shards)
+    assert np.array_equal(SA, O.srht_sketch(A, m, seed))
+
+
 def test_srht_sketch_too_large(gpu):
     with pytest.raises(gpu.SketchTooLarge):
         gpu.srht_sketch(np.zeros((12, 2)), 17, 0)
