@@ -140,7 +140,7 @@ __global__ void __launch_bounds__(64) tri_inv_diag_kernel(const double* __restri
 // lower != 0, else upper (W^T mirrored into the strict upper triangle, with
 // the diagonal of W). CTA tile: 64 rows x 512 columns; partials per column
 // chunk go to part[chunk][q][row] and are summed in fixed order afterwards.
-constexpr int TR_ROWS = 64, TR_COLS = 512;
+constexpr int TR_ROWS = 64, TR_COLS = 64;  // 16 columns per thread: short, independent load chains
 __global__ void __launch_bounds__(256) trmv_partial_kernel(const double* __restrict__ Wf, int64_t n, int lower,
                                                            const double* __restrict__ x, int nrhs,
                                                            double* __restrict__ part) {

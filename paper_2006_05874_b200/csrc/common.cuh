@@ -73,8 +73,13 @@ size_t srht_scratch_bytes(const SrhtPlan& p);  // T buffer (phase-1 output) when
 // tile. entries = (row, k) pairs grouped by tile; tiles = (rlo0, begin, end).
 void srht_build_entries(const SrhtPlan& p, const int64_t* rows, std::vector<int2>& entries,
                         std::vector<int4>& tiles);
+// d_ctl != nullptr selects the fused single-launch path (when the high bits
+// fit one pass): T is then a ring of srht_fused_scratch_bytes() and d_ctl a
+// control block of *ctl_bytes.
+size_t srht_fused_scratch_bytes(const SrhtPlan& p, size_t* ctl_bytes);
 void srht_run_device(const SrhtPlan& p, const double* d_A, const uint32_t* d_signbits, const int2* d_entries,
-                     const int4* d_tiles, int n_tiles, double* d_T, double* d_SA, cudaStream_t st);
+                     const int4* d_tiles, int n_tiles, double* d_T, double* d_SA, cudaStream_t st,
+                     unsigned long long* d_ctl = nullptr, int num_sms = 148);
 // Row-sharded SRHT: plan of one shard (n_loc = n_pad / P rows, n_real of them
 // real) that emits unscaled partials at r_lo(k) for all m sampled rows, and the
 // combine of the P gathered partials ([P][m][d]) into SA (d_hi[k] = r_hi(k)).

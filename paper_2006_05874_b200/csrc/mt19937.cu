@@ -18,6 +18,7 @@
 // start states are obtained by F2-linear jump-ahead (mt_jump.cpp) and run one
 // CTA per substream.
 #include "common.cuh"
+#include "mt_core.cuh"
 #include "mt_jump.h"
 
 #include <cub/device/device_scan.cuh>
@@ -25,106 +26,79 @@
 namespace ihs_b200 {
 
 namespace {
-constexpr int NN = 312;
-constexpr int MM = 156;
-constexpr uint64_t MATRIX_A = 0xB5026F5AA96619E9ULL;
-constexpr uint64_t UM = 0xFFFFFFFF80000000ULL;  // upper 33 bits
-constexpr uint64_t LM = 0x7FFFFFFFULL;          // lower 31 bits
-
-__device__ __forceinline__ uint64_t temper(uint64_t y) {
-    y ^= (y >> 29) & 0x5555555555555555ULL;
-    y ^= (y << 17) & 0x71D67FFFEDA60000ULL;
-    y ^= (y << 37) & 0xFFF7EEE000000000ULL;
-    y ^= (y >> 43);
-    return y;
-}
-
-// One full twist of the 312-word array in shared memory; all threads of the
-// CTA must call it. Uses threads [0,156).
-__device__ __forceinline__ void twist(uint64_t* mt) {
-    const int k = threadIdx.x;
-    uint64_t v = 0;
-    if (k < MM) {
-        const uint64_t y = (mt[k] & UM) | (mt[k + 1] & LM);
-        v = mt[k + MM] ^ (y >> 1) ^ ((y & 1ULL) ? MATRIX_A : 0ULL);
-    }
-    __syncthreads();
-    if (k < MM) mt[k] = v;
-    __syncthreads();
-    if (k < NN - MM) {
-        const int kk = MM + k;
-        const int k1 = (kk + 1 == NN) ? 0 : kk + 1;
-        const uint64_t y = (mt[kk] & UM) | (mt[k1] & LM);
-        v = mt[kk - MM] ^ (y >> 1) ^ ((y & 1ULL) ? MATRIX_A : 0ULL);
-    }
-    __syncthreads();
-    if (k < NN - MM) mt[MM + k] = v;
-    __syncthreads();
-}
-
-__device__ __forceinline__ void seed_state(uint64_t* mt, uint64_t seed) {
-    if (threadIdx.x == 0) {
-        mt[0] = seed;
-        for (int i = 1; i < NN; ++i) mt[i] = 6364136223846793005ULL * (mt[i - 1] ^ (mt[i - 1] >> 62)) + (uint64_t)i;
-    }
-    __syncthreads();
-}
+using mt::NN;
+using mt::temper;
 
 // Single-stream raw generator: draws [0, count) of mt19937_64(seed).
-__global__ void __launch_bounds__(320) mt_raw_kernel(uint64_t seed, int64_t count, uint64_t* __restrict__ out) {
-    __shared__ uint64_t mt[NN];
-    seed_state(mt, seed);
+__global__ void __launch_bounds__(mt::THREADS) mt_raw_kernel(uint64_t seed, int64_t count, uint64_t* __restrict__ out) {
+    __shared__ uint64_t buf[2 * NN];
+    mt::seed_array(buf, seed);
+    __syncthreads();
+    mt::Twister tw{buf, 0};
+    const int k = threadIdx.x;
     for (int64_t base = 0; base < count; base += NN) {
-        twist(mt);
-        for (int i = threadIdx.x; i < NN; i += blockDim.x)
-            if (base + i < count) out[base + i] = temper(mt[i]);
+        uint64_t lo, hi;
+        tw.next(lo, hi);
+        if (tw.worker()) {
+            if (base + k < count) out[base + k] = temper(lo);
+            if (base + mt::MM + k < count) out[base + mt::MM + k] = temper(hi);
+        }
     }
 }
 
 // Substream raw generator: CTA q starts from the 312-word window in
 // starts[q] (state after q*stride draws), produces draws
 // [q*stride, min((q+1)*stride, count)).
-__global__ void __launch_bounds__(320) mt_substream_kernel(const uint64_t* __restrict__ starts, int64_t stride,
-                                                           int64_t count, uint64_t* __restrict__ out) {
-    __shared__ uint64_t mt[NN];
+__global__ void __launch_bounds__(mt::THREADS) mt_substream_kernel(const uint64_t* __restrict__ starts, int64_t stride,
+                                                                   int64_t count, uint64_t* __restrict__ out) {
+    __shared__ uint64_t buf[2 * NN];
     const int64_t q = blockIdx.x;
-    for (int i = threadIdx.x; i < NN; i += blockDim.x) mt[i] = starts[q * NN + i];
+    for (int i = threadIdx.x; i < NN; i += blockDim.x) buf[i] = starts[q * NN + i];
     __syncthreads();
+    mt::Twister tw{buf, 0};
+    const int k = threadIdx.x;
     const int64_t beg = q * stride;
     const int64_t end = min(count, beg + stride);
     for (int64_t base = beg; base < end; base += NN) {
-        twist(mt);
-        for (int i = threadIdx.x; i < NN; i += blockDim.x)
-            if (base + i < end) out[base + i] = temper(mt[i]);
+        uint64_t lo, hi;
+        tw.next(lo, hi);
+        if (tw.worker()) {
+            if (base + k < end) out[base + k] = temper(lo);
+            if (base + mt::MM + k < end) out[base + mt::MM + k] = temper(hi);
+        }
     }
 }
 
-// Sign bits: 32 twists (9984 draws) fill exactly 312 32-bit words.
-__global__ void __launch_bounds__(320) mt_signbits_kernel(uint64_t seed, int64_t n, uint32_t* __restrict__ bits) {
-    __shared__ uint64_t mt[NN];
-    __shared__ uint32_t acc[NN];
-    seed_state(mt, seed);
-    const int64_t nwords = (n + 31) / 32;
-    for (int64_t group = 0; group * (32 * NN) < n; ++group) {
-        for (int i = threadIdx.x; i < NN; i += blockDim.x) acc[i] = 0u;
-        for (int b = 0; b < 32; ++b) {
-            twist(mt);
-            for (int i = threadIdx.x; i < NN; i += blockDim.x) {
-                const int local = b * NN + i;
-                const uint32_t bit = (uint32_t)(temper(mt[i]) & 1ULL);
-                if (bit) atomicOr(&acc[local >> 5], 1u << (local & 31));
-            }
-            if (group * (32 * NN) + (int64_t)(b + 1) * NN >= n) break;  // uniform across the CTA
+// Sign bits of draws [beg, end) into a shared bit buffer (bit g - beg).
+__device__ __forceinline__ void sign_bits_range(mt::Twister& tw, int64_t beg, int64_t end, uint32_t* accw) {
+    const int k = threadIdx.x;
+    for (int64_t base = beg; base < end; base += NN) {
+        uint64_t lo, hi;
+        tw.next(lo, hi);
+        if (tw.worker()) {
+            const int64_t g0 = base + k, g1 = base + mt::MM + k;
+            if (g0 < end && (temper(lo) & 1ULL)) atomicOr(&accw[(g0 - beg) >> 5], 1u << ((g0 - beg) & 31));
+            if (g1 < end && (temper(hi) & 1ULL)) atomicOr(&accw[(g1 - beg) >> 5], 1u << ((g1 - beg) & 31));
         }
+    }
+}
+
+// Sign bits, single stream: chunks of 32 blocks (9984 draws = 312 words).
+__global__ void __launch_bounds__(mt::THREADS) mt_signbits_kernel(uint64_t seed, int64_t n, uint32_t* __restrict__ bits) {
+    __shared__ uint64_t buf[2 * NN];
+    __shared__ uint32_t acc[NN];
+    mt::seed_array(buf, seed);
+    __syncthreads();
+    mt::Twister tw{buf, 0};
+    const int64_t nwords = (n + 31) / 32;
+    for (int64_t beg = 0; beg < n; beg += 32 * NN) {
+        for (int i = threadIdx.x; i < NN; i += blockDim.x) acc[i] = 0u;
+        __syncthreads();
+        sign_bits_range(tw, beg, min(n, beg + 32 * NN), acc);
         __syncthreads();
         for (int i = threadIdx.x; i < NN; i += blockDim.x) {
-            const int64_t w = group * NN + i;
-            if (w < nwords) {
-                uint32_t v = acc[i];
-                const int64_t first_bit = w * 32;
-                if (first_bit + 32 > n) v &= (n - first_bit >= 32) ? 0xFFFFFFFFu : ((1u << (n - first_bit)) - 1u);
-                bits[w] = v;
-            }
+            const int64_t w = beg / 32 + i;
+            if (w < nwords) bits[w] = acc[i];
         }
         __syncthreads();
     }
@@ -133,27 +107,20 @@ __global__ void __launch_bounds__(320) mt_signbits_kernel(uint64_t seed, int64_t
 // Sign bits from jump-ahead substreams: CTA q produces draws
 // [q*stride, min(n, (q+1)*stride)) (stride a multiple of 32) into a shared
 // bit buffer, then writes its whole words.
-__global__ void __launch_bounds__(320) mt_signbits_sub_kernel(const uint64_t* __restrict__ starts, int64_t stride,
-                                                              int64_t n, uint32_t* __restrict__ bits) {
+__global__ void __launch_bounds__(mt::THREADS) mt_signbits_sub_kernel(const uint64_t* __restrict__ starts,
+                                                                      int64_t stride, int64_t n,
+                                                                      uint32_t* __restrict__ bits) {
     extern __shared__ uint32_t accw[];
-    __shared__ uint64_t mt[NN];
+    __shared__ uint64_t buf[2 * NN];
     const int64_t q = blockIdx.x;
     const int nw = (int)(stride / 32);
-    for (int i = threadIdx.x; i < NN; i += blockDim.x) mt[i] = starts[q * NN + i];
+    for (int i = threadIdx.x; i < NN; i += blockDim.x) buf[i] = starts[q * NN + i];
     for (int i = threadIdx.x; i < nw; i += blockDim.x) accw[i] = 0u;
     __syncthreads();
+    mt::Twister tw{buf, 0};
     const int64_t beg = q * stride;
     const int64_t end = min(n, beg + stride);
-    for (int64_t base = beg; base < end; base += NN) {
-        twist(mt);
-        for (int i = threadIdx.x; i < NN; i += blockDim.x) {
-            const int64_t g = base + i;
-            if (g < end && (temper(mt[i]) & 1ULL)) {
-                const int local = (int)(g - beg);
-                atomicOr(&accw[local >> 5], 1u << (local & 31));
-            }
-        }
-    }
+    sign_bits_range(tw, beg, end, accw);
     __syncthreads();
     const int64_t w_end = (end + 31) / 32;
     for (int64_t w = beg / 32 + threadIdx.x; w < w_end; w += blockDim.x) bits[w] = accw[w - beg / 32];

@@ -14,6 +14,7 @@
 // Device: one CTA per substream XOR-accumulates the windows selected by its
 // polynomial from the first 20248 words of the seeded stream (in smem).
 #include "common.cuh"
+#include "mt_core.cuh"
 #include "mt_jump.h"
 
 #include <algorithm>
@@ -189,69 +190,63 @@ PolyRing& ring() {
 }
 
 // untempered word sequence x_0 .. x_{nx-1} of mt19937_64(seed)
-__global__ void __launch_bounds__(320) mt_wordseq_kernel(uint64_t seed, int nx, uint64_t* __restrict__ X) {
-    __shared__ uint64_t mt[NN];
-    if (threadIdx.x == 0) {
-        mt[0] = seed;
-        for (int i = 1; i < NN; ++i) mt[i] = 6364136223846793005ULL * (mt[i - 1] ^ (mt[i - 1] >> 62)) + (uint64_t)i;
-    }
+__global__ void __launch_bounds__(mt::THREADS) mt_wordseq_kernel(uint64_t seed, int nx, uint64_t* __restrict__ X) {
+    __shared__ uint64_t buf[2 * NN];
+    mt::seed_array(buf, seed);
     __syncthreads();
-    for (int i = threadIdx.x; i < NN; i += blockDim.x) X[i] = mt[i];
+    for (int i = threadIdx.x; i < NN; i += blockDim.x) X[i] = buf[i];
+    mt::Twister tw{buf, 0};
+    const int k = threadIdx.x;
     for (int base = NN; base < nx; base += NN) {
-        const int k = threadIdx.x;
-        uint64_t v = 0;
-        if (k < 156) {
-            const uint64_t y = (mt[k] & 0xFFFFFFFF80000000ULL) | (mt[k + 1] & 0x7FFFFFFFULL);
-            v = mt[k + 156] ^ (y >> 1) ^ ((y & 1ULL) ? 0xB5026F5AA96619E9ULL : 0ULL);
+        uint64_t lo, hi;
+        tw.next(lo, hi);
+        if (tw.worker()) {
+            if (base + k < nx) X[base + k] = lo;
+            if (base + mt::MM + k < nx) X[base + mt::MM + k] = hi;
         }
-        __syncthreads();
-        if (k < 156) mt[k] = v;
-        __syncthreads();
-        if (k < 156) {
-            const int kk = 156 + k;
-            const int k1 = (kk + 1 == NN) ? 0 : kk + 1;
-            const uint64_t y = (mt[kk] & 0xFFFFFFFF80000000ULL) | (mt[k1] & 0x7FFFFFFFULL);
-            v = mt[kk - 156] ^ (y >> 1) ^ ((y & 1ULL) ? 0xB5026F5AA96619E9ULL : 0ULL);
-        }
-        __syncthreads();
-        if (k < 156) mt[156 + k] = v;
-        __syncthreads();
-        for (int i = threadIdx.x; i < NN; i += blockDim.x)
-            if (base + i < nx) X[base + i] = mt[i];
-        __syncthreads();
     }
 }
 
-// CTA (q, chunk) XORs the windows selected by coefficient words
-// [chunk*CW, (chunk+1)*CW) of substream q's polynomial; the chunks combine
-// with atomicXor (XOR is associative and commutative, so the start state is
-// exact regardless of order). starts must be zeroed beforehand.
+// CTA (q, chunk) XORs the windows W_i (i = set coefficient positions of
+// substream q's polynomial inside position range chunk*kSpan ..) into the
+// start state. Positions come as host-built sorted lists; each warp takes
+// every 8th position and XORs the 312-word window with 10 words per lane.
+// Partial states combine with atomicXor (XOR is associative and commutative,
+// so the start state is exact regardless of order); starts is pre-zeroed.
 constexpr int kChunks = 8;
-constexpr int CW = (PW + kChunks - 1) / kChunks;  // 39 coefficient words per chunk
-__global__ void __launch_bounds__(320) mt_jump_apply_kernel(const uint64_t* __restrict__ X,
-                                                            const uint64_t* __restrict__ polys,
-                                                            uint64_t* __restrict__ starts) {
-    __shared__ uint64_t xs[CW * 64 + NN];
+constexpr int kSpan = (DEG + kChunks - 1) / kChunks;  // 2493 coefficient positions per chunk
+constexpr int kApplyThreads = 256;
+__global__ void __launch_bounds__(kApplyThreads) mt_jump_apply_kernel(const uint64_t* __restrict__ X,
+                                                                      const uint16_t* __restrict__ pos,
+                                                                      const int* __restrict__ ptr,
+                                                                      uint64_t* __restrict__ starts) {
+    __shared__ uint64_t xs[kSpan + NN];
+    __shared__ unsigned long long red[NN];
     const int q = blockIdx.x, chunk = blockIdx.y;
-    const int w0 = chunk * CW, w1 = min(PW, w0 + CW);
-    const int base = w0 * 64;
-    const int nload = min(NX - base, (w1 - w0) * 64 + NN);
+    const int b0 = ptr[q * (kChunks + 1) + chunk], b1 = ptr[q * (kChunks + 1) + chunk + 1];
+    if (b0 >= b1) return;  // uniform
+    const int base = chunk * kSpan;
+    const int nload = min(NX - base, kSpan + NN);
     for (int i = threadIdx.x; i < nload; i += blockDim.x) xs[i] = X[base + i];
+    for (int i = threadIdx.x; i < NN; i += blockDim.x) red[i] = 0ULL;
     __syncthreads();
-    const uint64_t* a = polys + (size_t)q * PW;
-    const int w = threadIdx.x;
-    if (w < NN) {
-        uint64_t acc = 0;
-        for (int widx = w0; widx < w1; ++widx) {
-            uint64_t bits = __ldg(a + widx);
-            while (bits) {
-                const int s = __ffsll((long long)bits) - 1;
-                bits &= bits - 1;
-                acc ^= xs[(widx - w0) * 64 + s + w];
-            }
-        }
-        atomicXor(reinterpret_cast<unsigned long long*>(starts + (size_t)q * NN + w), (unsigned long long)acc);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    constexpr int NW = kApplyThreads / 32;
+    uint64_t acc[10];
+#pragma unroll
+    for (int k = 0; k < 10; ++k) acc[k] = 0;
+    for (int b = b0 + warp; b < b1; b += NW) {
+        const int i = (int)pos[b] - base;
+#pragma unroll
+        for (int k = 0; k < 10; ++k)
+            if (lane + 32 * k < NN) acc[k] ^= xs[i + lane + 32 * k];
     }
+#pragma unroll
+    for (int k = 0; k < 10; ++k)
+        if (lane + 32 * k < NN) atomicXor(&red[lane + 32 * k], (unsigned long long)acc[k]);
+    __syncthreads();
+    for (int w = threadIdx.x; w < NN; w += blockDim.x)
+        atomicXor(reinterpret_cast<unsigned long long*>(starts + (size_t)q * NN + w), red[w]);
 }
 }  // namespace
 
@@ -289,29 +284,54 @@ const std::vector<uint64_t>& mt_jump_polys(int64_t stride, int64_t nsub) {
 }
 
 void mt_jump_starts(uint64_t seed, int64_t stride, int64_t nsub, uint64_t* d_starts, uint64_t* d_X, cudaStream_t st) {
-    const std::vector<uint64_t>& polys = mt_jump_polys(stride, nsub);
-    // device copies of the polynomials are cached per (stride) and grown on demand
+    // device copies of the set-bit lists of x^(q*stride) mod P, cached per
+    // (device, stride) and grown on demand (seed-independent)
+    struct DevLists {
+        uint16_t* pos = nullptr;
+        int* ptr = nullptr;
+        int64_t count = 0;
+    };
     static std::mutex mu;
-    static std::map<std::pair<int, int64_t>, std::pair<uint64_t*, int64_t>> dev;  // (device,stride) -> (ptr, count)
+    static std::map<std::pair<int, int64_t>, DevLists> dev;
     int dev_id = 0;
     CUDA_CHECK(cudaGetDevice(&dev_id));
-    uint64_t* d_polys = nullptr;
+    DevLists L;
     {
         std::lock_guard<std::mutex> lk(mu);
         auto key = std::make_pair(dev_id, stride);
         auto it = dev.find(key);
-        if (it == dev.end() || it->second.second < nsub) {
-            if (it != dev.end()) CUDA_CHECK(cudaFree(it->second.first));
-            CUDA_CHECK(cudaMalloc(&d_polys, (size_t)nsub * PW * 8));
-            CUDA_CHECK(cudaMemcpy(d_polys, polys.data(), (size_t)nsub * PW * 8, cudaMemcpyHostToDevice));
-            dev[key] = {d_polys, nsub};
+        if (it == dev.end() || it->second.count < nsub) {
+            const std::vector<uint64_t>& polys = mt_jump_polys(stride, nsub);
+            std::vector<uint16_t> pos;
+            std::vector<int> ptr((size_t)nsub * (kChunks + 1));
+            pos.reserve((size_t)nsub * DEG / 2 + 64);
+            for (int64_t q = 0; q < nsub; ++q) {
+                const uint64_t* a = polys.data() + (size_t)q * PW;
+                for (int c = 0; c < kChunks; ++c) {
+                    ptr[(size_t)q * (kChunks + 1) + c] = (int)pos.size();
+                    const int i1 = std::min(DEG, (c + 1) * kSpan);
+                    for (int i = c * kSpan; i < i1; ++i)
+                        if ((a[i >> 6] >> (i & 63)) & 1ULL) pos.push_back((uint16_t)i);
+                }
+                ptr[(size_t)q * (kChunks + 1) + kChunks] = (int)pos.size();
+            }
+            if (it != dev.end()) {
+                CUDA_CHECK(cudaFree(it->second.pos));
+                CUDA_CHECK(cudaFree(it->second.ptr));
+            }
+            CUDA_CHECK(cudaMalloc(&L.pos, pos.size() * sizeof(uint16_t) + 16));
+            CUDA_CHECK(cudaMalloc(&L.ptr, ptr.size() * sizeof(int)));
+            CUDA_CHECK(cudaMemcpy(L.pos, pos.data(), pos.size() * sizeof(uint16_t), cudaMemcpyHostToDevice));
+            CUDA_CHECK(cudaMemcpy(L.ptr, ptr.data(), ptr.size() * sizeof(int), cudaMemcpyHostToDevice));
+            L.count = nsub;
+            dev[key] = L;
         } else {
-            d_polys = it->second.first;
+            L = it->second;
         }
     }
     CUDA_CHECK(cudaMemsetAsync(d_starts, 0, (size_t)nsub * NN * 8, st));
-    LAUNCH(mt_wordseq_kernel, 1, 160, 0, st, seed, NX, d_X);
-    LAUNCH(mt_jump_apply_kernel, dim3((unsigned)nsub, kChunks), 320, 0, st, d_X, d_polys, d_starts);
+    LAUNCH(mt_wordseq_kernel, 1, mt::THREADS, 0, st, seed, NX, d_X);
+    LAUNCH(mt_jump_apply_kernel, dim3((unsigned)nsub, kChunks), kApplyThreads, 0, st, d_X, L.pos, L.ptr, d_starts);
 }
 
 }  // namespace ihs_b200

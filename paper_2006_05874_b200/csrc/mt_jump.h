@@ -7,7 +7,7 @@
 namespace ihs_b200 {
 
 // Draws per substream of a long Gaussian stream (one CTA each).
-constexpr int64_t kJumpStride = int64_t{1} << 17;
+constexpr int64_t kJumpStride = int64_t{1} << 18;
 // Draws per substream of an SRHT sign vector (a multiple of 32 for whole bit words).
 constexpr int64_t kSignStride = int64_t{1} << 15;
 

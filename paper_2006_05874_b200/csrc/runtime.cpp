@@ -251,6 +251,7 @@ struct ihs_gpu_problem {
     // sketch workspaces
     DevBuf T, signbits, rng_scratch, entries, tiles, gauss_scratch, S, gemm_work;
     DevBuf shard_U, shard_hi;    // sharded SRHT partials [P][m][d] and r_hi(k)
+    DevBuf fused_ctl;            // work-queue counters of the fused SRHT kernel
     PinnedBuf h_stage;
     std::vector<int64_t> h_rows;
     std::vector<int2> h_entries;
@@ -266,6 +267,23 @@ namespace ihs_b200 {
 namespace {
 
 // -------------------------------------------------------- sketches (device)
+// T scratch and the fused kernel's control block; nullptr control = the
+// two-kernel path (IHS_SRHT_UNFUSED=1 forces it, for A/B measurements).
+unsigned long long* srht_prepare_scratch(ihs_gpu_problem* P, const SrhtPlan& plan) {
+    static const bool unfused = [] {
+        const char* e = std::getenv("IHS_SRHT_UNFUSED");
+        return e && e[0] == '1';
+    }();
+    if (unfused) {
+        P->T.ensure(srht_scratch_bytes(plan));
+        return nullptr;
+    }
+    size_t ctl_bytes = 0;
+    P->T.ensure(srht_fused_scratch_bytes(plan, &ctl_bytes));
+    P->fused_ctl.ensure(ctl_bytes);
+    return P->fused_ctl.as<unsigned long long>();
+}
+
 // Upload host-built SRHT entries/tiles through the pinned staging buffer.
 void upload_entries(ihs_gpu_problem* P) {
     cudaStream_t st = P->st;
@@ -310,9 +328,9 @@ void device_sketch(ihs_gpu_problem* P, int kind, int64_t m, uint64_t seed, doubl
             g_host_rng_ns +=
                 std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t_rng).count();
             upload_entries(P);
-            P->T.ensure(srht_scratch_bytes(plan));
+            unsigned long long* ctl = srht_prepare_scratch(P, plan);
             srht_run_device(plan, P->A.d(), P->signbits.as<uint32_t>(), P->entries.as<int2>(), P->tiles.as<int4>(),
-                            (int)P->h_tiles.size(), P->T.d(), d_SA, st);
+                            (int)P->h_tiles.size(), P->T.d(), d_SA, st, ctl, P->num_sms);
         } else {
             // shard p holds rows [p*n_loc, (p+1)*n_loc) of the padded index space
             const int64_t n_loc = plan.n_pad / shards;
@@ -330,13 +348,14 @@ void device_sketch(ihs_gpu_problem* P, int kind, int64_t m, uint64_t seed, doubl
             P->shard_hi.ensure((size_t)m + 16);
             CUDA_CHECK(cudaMemcpyAsync(P->shard_hi.p, hi.data(), (size_t)m, cudaMemcpyHostToDevice, st));
             P->shard_U.ensure((size_t)shards * m * d * sizeof(double));
-            P->T.ensure(srht_scratch_bytes(sp));
+            unsigned long long* ctl = srht_prepare_scratch(P, sp);
             double* U = P->shard_U.d();
             auto run_shard = [&](int p, const double* A_p, int64_t n_real) {
                 SrhtPlan s = sp;
                 s.n = n_real;
                 srht_run_device(s, A_p, P->signbits.as<uint32_t>() + (p * n_loc) / 32, P->entries.as<int2>(),
-                                P->tiles.as<int4>(), (int)P->h_tiles.size(), P->T.d(), U + (int64_t)p * m * d, st);
+                                P->tiles.as<int4>(), (int)P->h_tiles.size(), P->T.d(), U + (int64_t)p * m * d, st,
+                                ctl, P->num_sms);
             };
             if (world > 1) {
                 const int r = P->opts.rank;

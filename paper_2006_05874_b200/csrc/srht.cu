@@ -108,53 +108,61 @@ srht_small_kernel(const double* __restrict__ A, int64_t n, int64_t lda, const ui
 }
 
 // ------------------------------------------------------------ phase 1
-// Warp-per-chunk: bits 0..9 of a 1024-row chunk of one column -> T.
+// One warp: bits 0..9 of the 1024-row chunk [r0, r0+1024) of column Acol ->
+// dst[0..1024). STREAM: A loads are evict-first (read exactly once).
+template <bool STREAM>
+__device__ __forceinline__ void p1_chunk(double* __restrict__ xs, const double* __restrict__ Acol, int64_t n,
+                                         const uint32_t* __restrict__ signbits, int64_t r0, double* __restrict__ dst) {
+    const int lane = threadIdx.x & 31;
+    double v[32];
+    // coalesced load (lane = index bits 0-4, register c = bits 5-9), sign fused
+#pragma unroll
+    for (int c = 0; c < 32; ++c) {
+        const int64_t r = r0 + (c << 5) + lane;
+        v[c] = (r < n) ? eps_mul(signbits, r, STREAM ? __ldcs(Acol + r) : __ldg(Acol + r)) : 0.0;
+    }
+#pragma unroll
+    for (int c = 0; c < 32; ++c) xs[pad32((c << 5) | lane)] = v[c];
+    __syncwarp();
+    // register c = index bits 0-4: stages 0..4
+#pragma unroll
+    for (int c = 0; c < 32; ++c) v[c] = xs[pad32((lane << 5) | c)];
+#pragma unroll
+    for (int s = 0; s < 5; ++s)
+#pragma unroll
+        for (int c = 0; c < 32; ++c)
+            if (!(c & (1 << s))) bfly(v[c], v[c | (1 << s)]);
+#pragma unroll
+    for (int c = 0; c < 32; ++c) xs[pad32((lane << 5) | c)] = v[c];
+    __syncwarp();
+    // register c = index bits 5-9: stages 5..9
+#pragma unroll
+    for (int c = 0; c < 32; ++c) v[c] = xs[pad32((c << 5) | lane)];
+    __syncwarp();
+#pragma unroll
+    for (int s = 0; s < 5; ++s)
+#pragma unroll
+        for (int c = 0; c < 32; ++c)
+            if (!(c & (1 << s))) bfly(v[c], v[c | (1 << s)]);
+#pragma unroll
+    for (int c = 0; c < 32; ++c) dst[(c << 5) + lane] = v[c];
+}
+
+// Warp-per-chunk: bits 0..9 of every 1024-row chunk of every column -> T.
 __global__ void __launch_bounds__(32 * kP1Warps)
 srht_phase1_kernel(const double* __restrict__ A, int64_t n, int64_t lda, const uint32_t* __restrict__ signbits,
                    double* __restrict__ T, int64_t n_pad, int64_t chunks_per_col, int64_t total_chunks) {
     extern __shared__ double p1_smem[];  // kP1Warps x (1024 + 32) doubles
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int warp = threadIdx.x >> 5;
     double* xs = p1_smem + warp * (1024 + 32);
     for (int64_t chunk = (int64_t)blockIdx.x * kP1Warps + warp; chunk < total_chunks;
          chunk += (int64_t)gridDim.x * kP1Warps) {
         const int64_t j = chunk / chunks_per_col;
         const int64_t r0 = (chunk % chunks_per_col) << kChunkL;
-        const double* Acol = A + j * lda;
-        double v[32];
-        // coalesced load (lane = index bits 0-4, register c = bits 5-9), sign fused
-#pragma unroll
-        for (int c = 0; c < 32; ++c) {
-            const int64_t r = r0 + (c << 5) + lane;
-            v[c] = (r < n) ? eps_mul(signbits, r, __ldg(Acol + r)) : 0.0;
-        }
-#pragma unroll
-        for (int c = 0; c < 32; ++c) xs[pad32((c << 5) | lane)] = v[c];
-        __syncwarp();
-        // register c = index bits 0-4: stages 0..4
-#pragma unroll
-        for (int c = 0; c < 32; ++c) v[c] = xs[pad32((lane << 5) | c)];
-#pragma unroll
-        for (int s = 0; s < 5; ++s)
-#pragma unroll
-            for (int c = 0; c < 32; ++c)
-                if (!(c & (1 << s))) bfly(v[c], v[c | (1 << s)]);
-#pragma unroll
-        for (int c = 0; c < 32; ++c) xs[pad32((lane << 5) | c)] = v[c];
-        __syncwarp();
-        // register c = index bits 5-9: stages 5..9
-#pragma unroll
-        for (int c = 0; c < 32; ++c) v[c] = xs[pad32((c << 5) | lane)];
-        __syncwarp();
-#pragma unroll
-        for (int s = 0; s < 5; ++s)
-#pragma unroll
-            for (int c = 0; c < 32; ++c)
-                if (!(c & (1 << s))) bfly(v[c], v[c | (1 << s)]);
-        double* Tcol = T + j * n_pad + r0;
-#pragma unroll
-        for (int c = 0; c < 32; ++c) Tcol[(c << 5) + lane] = v[c];
+        p1_chunk<false>(xs, A + j * lda, n, signbits, r0, T + j * n_pad + r0);
     }
 }
+
 
 // ------------------------------------------------------------ phase 2
 // One CTA per (tile, column): bits [lo, lo+HB) of kTileElems elements = W
@@ -163,37 +171,35 @@ srht_phase1_kernel(const double* __restrict__ A, int64_t n, int64_t lda, const u
 // [RB1, HB) after one shared-memory exchange. emit: write the tile's sampled
 // rows (entries) instead of the tile.
 template <int HB>
-__global__ void __launch_bounds__(kP2Threads)
-srht_phase2_kernel(double* __restrict__ T, int64_t n_pad, int lo, const int4* __restrict__ tiles, int emit,
-                   int64_t tiles_per_col, const int2* __restrict__ entries, double s1, double s2,
-                   double* __restrict__ SA, int64_t m) {
-    constexpr int RB1 = HB < 5 ? HB : 5;
+struct P2Geom {
+    static constexpr int RB1 = HB < 5 ? HB : 5;
+    static constexpr int E = 1 << RB1;                    // registers per thread
+    static constexpr int W = kP2Threads * E / (1 << HB);  // consecutive low indices per tile
+    static constexpr int LOGW = (W >= 256) ? 8 : (W >= 128) ? 7 : (W >= 64) ? 6 : (W >= 32) ? 5 : (W >= 16) ? 4 : 3;
+};
+
+// One CTA: bits [lo, lo+HB) of the tile whose element (b, w) sits at
+// Tcol[(b << lo) + w]; emit -> the tile's sampled rows go to SA, else the
+// tile is written back in place. CG: T loads bypass L1 (written by other
+// CTAs of the same fused launch).
+template <int HB, bool CG>
+__device__ __forceinline__ void p2_tile(double* __restrict__ xs, double* __restrict__ Tcol, int lo, bool emit,
+                                        int4 tile, const int2* __restrict__ entries, int64_t j, double s1, double s2,
+                                        double* __restrict__ SA, int64_t m) {
+    constexpr int RB1 = P2Geom<HB>::RB1;
     constexpr int RB2 = HB - RB1;
-    constexpr int E = 1 << RB1;                     // registers per thread
-    constexpr int W = kP2Threads * E / (1 << HB);   // consecutive low indices per tile
-    constexpr int LOGW = (W >= 256) ? 8 : (W >= 128) ? 7 : (W >= 64) ? 6 : (W >= 32) ? 5 : (W >= 16) ? 4 : 3;
-    extern __shared__ double xs[];
+    constexpr int E = P2Geom<HB>::E;
+    constexpr int W = P2Geom<HB>::W;
     const int t = threadIdx.x;
-    const int64_t j = blockIdx.y;
-    int64_t base;
-    int4 tile = make_int4(0, 0, 0, 0);
-    if (emit) {
-        tile = tiles[blockIdx.x];
-        base = tile.x;
-    } else {
-        // enumerate tiles: low part (bits LOGW .. lo-1) and high part (bits >= lo+HB)
-        const int64_t low_tiles = (int64_t{1} << lo) >> LOGW;
-        const int64_t tid = blockIdx.x;
-        base = ((tid % low_tiles) << LOGW) | ((tid / low_tiles) << (lo + HB));
-    }
-    (void)tiles_per_col;
-    double* Tcol = T + j * n_pad + base;
     const int w = t % W;
     const int g = t / W;  // 2^RB2 groups
     double v[E];
     // round 1: register c = pass bits [0, RB1), g = pass bits [RB1, HB)
 #pragma unroll
-    for (int c = 0; c < E; ++c) v[c] = Tcol[((int64_t)((g << RB1) | c) << lo) + w];
+    for (int c = 0; c < E; ++c) {
+        const double* src = Tcol + ((int64_t)((g << RB1) | c) << lo) + w;
+        v[c] = CG ? __ldcg(src) : *src;
+    }
 #pragma unroll
     for (int s = 0; s < RB1; ++s)
 #pragma unroll
@@ -261,6 +267,124 @@ srht_phase2_kernel(double* __restrict__ T, int64_t n_pad, int lo, const int4* __
     }
 }
 
+// One CTA per (tile, column) of a phase-2 pass.
+template <int HB>
+__global__ void __launch_bounds__(kP2Threads)
+srht_phase2_kernel(double* __restrict__ T, int64_t n_pad, int lo, const int4* __restrict__ tiles, int emit,
+                   const int2* __restrict__ entries, double s1, double s2, double* __restrict__ SA, int64_t m) {
+    extern __shared__ double xs[];
+    constexpr int LOGW = P2Geom<HB>::LOGW;
+    const int64_t j = blockIdx.y;
+    int64_t base;
+    int4 tile = make_int4(0, 0, 0, 0);
+    if (emit) {
+        tile = tiles[blockIdx.x];
+        base = tile.x;
+    } else {
+        // enumerate tiles: low part (bits LOGW .. lo-1) and high part (bits >= lo+HB)
+        const int64_t low_tiles = (int64_t{1} << lo) >> LOGW;
+        const int64_t tid = blockIdx.x;
+        base = ((tid % low_tiles) << LOGW) | ((tid / low_tiles) << (lo + HB));
+    }
+    p2_tile<HB, false>(xs, T + j * n_pad + base, lo, emit != 0, tile, entries, j, s1, s2, SA, m);
+}
+
+// ------------------------------------------------------------ fused (one pass of high bits)
+// Persistent work queue over column groups of G columns: items in the order
+// P1(0), P1(1), P2(0), P1(2), P2(1), ..., P2(ng-1), handed out by an atomic
+// counter to running CTAs only. P1(g) = phase-1 chunks of group g (8 per
+// item, one per warp) into ring slot g % NSLOT of T; P2(g) = the emitting
+// pass over the active tiles of group g. A P2(g) item waits until all P1(g)
+// items are done; a P1(g) item waits until P2(g - NSLOT) released its slot.
+// Every awaited item precedes the waiter in the hand-out order and is held
+// by a running CTA, so the queue cannot deadlock. The ring (NSLOT x G
+// columns of T) is sized to stay in L2, so T never round-trips through HBM.
+struct FusedCtl {
+    unsigned long long next;  // hand-out counter; followed by done1[ng], done2[ng] (int)
+};
+
+__device__ __forceinline__ void wait_count(const int* ctr, int target) {
+    if (threadIdx.x == 0) {
+        int v;
+        while (true) {
+            asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+            if (v >= target) break;
+            __nanosleep(128);
+        }
+    }
+    __syncthreads();
+}
+
+__device__ __forceinline__ void signal_done(int* ctr) {
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) atomicAdd(ctr, 1);
+}
+
+template <int HB>
+__global__ void __launch_bounds__(kP2Threads)
+srht_fused_kernel(const double* __restrict__ A, int64_t n, int64_t lda, const uint32_t* __restrict__ signbits,
+                  double* __restrict__ T, int64_t n_pad, int64_t d, int G, int nslot, int ng, int n1, int n2,
+                  int64_t cpc, const int4* __restrict__ tiles, int n_tiles, const int2* __restrict__ entries, int lo,
+                  double s1, double s2, double* __restrict__ SA, int64_t m, unsigned long long* __restrict__ ctl) {
+    static_assert(kP2Threads == 32 * kP1Warps, "one block shape for both item kinds");
+    extern __shared__ double smem[];
+    __shared__ long long item_s;
+    int* done1 = reinterpret_cast<int*>(ctl + 1);
+    int* done2 = done1 + ng;
+    const long long per = (long long)n1 + n2;
+    const long long total = (long long)ng * per;
+    const int warp = threadIdx.x >> 5;
+    for (;;) {
+        if (threadIdx.x == 0) item_s = (long long)atomicAdd(ctl, 1ULL);
+        __syncthreads();
+        const long long item = item_s;
+        __syncthreads();
+        if (item >= total) break;
+        // decode the hand-out order P1(0), [P1(s), P2(s-1)] for s = 1..ng-1, P2(ng-1)
+        bool p1;
+        int g;
+        long long w;
+        if (item < n1) {
+            p1 = true; g = 0; w = item;
+        } else {
+            const long long i2 = item - n1;
+            const long long s = 1 + i2 / per;
+            if (s < ng) {
+                const long long within = i2 % per;
+                p1 = within < n1;
+                g = p1 ? (int)s : (int)s - 1;
+                w = p1 ? within : within - n1;
+            } else {
+                p1 = false; g = ng - 1; w = i2 - (long long)(ng - 1) * per;
+            }
+        }
+        const int slot = g % nslot;
+        if (p1) {
+            if (g >= nslot) wait_count(done2 + (g - nslot), n2);
+            const int64_t c = w * kP1Warps + warp;  // chunk within the group
+            const int64_t jj = c / cpc;
+            const int64_t j = (int64_t)g * G + jj;
+            if (jj < G && j < d) {
+                const int64_t r0 = (c % cpc) << kChunkL;
+                p1_chunk<true>(smem + warp * (1024 + 32), A + j * lda, n, signbits, r0,
+                               T + ((int64_t)slot * G + jj) * n_pad + r0);
+            }
+            signal_done(done1 + g);
+        } else {
+            wait_count(done1 + g, n1);
+            const int64_t jj = w / n_tiles;
+            const int64_t j = (int64_t)g * G + jj;
+            if (j < d) {
+                const int4 tile = tiles[w % n_tiles];
+                p2_tile<HB, true>(smem, T + ((int64_t)slot * G + jj) * n_pad + tile.x, lo, true, tile, entries, j, s1,
+                                  s2, SA, m);
+            }
+            signal_done(done2 + g);
+        }
+    }
+}
+
 // Row-sharded SRHT combine (H_{n_pad} = H_P (x) H_{n_pad/P}, shard index =
 // top log2(P) row bits): U holds every shard's unscaled partial T_p[r_lo(k)]
 // for every sampled row k ([P][m][d], shard-major, as an all-gather lays it
@@ -325,8 +449,47 @@ void launch_pass(const SrhtPlan& p, double* T, int lo, const int4* tiles, int n_
     const unsigned gx = emit ? (unsigned)n_tiles : (unsigned)tiles_per_col;
     if (gx == 0) return;
     dim3 grid(gx, (unsigned)p.d);
-    LAUNCH(srht_phase2_kernel<HB>, grid, kP2Threads, smem, st, T, p.n_pad, lo, tiles, emit ? 1 : 0, tiles_per_col,
-           entries, p.scale1, p.scale2, SA, p.m);
+    LAUNCH(srht_phase2_kernel<HB>, grid, kP2Threads, smem, st, T, p.n_pad, lo, tiles, emit ? 1 : 0, entries,
+           p.scale1, p.scale2, SA, p.m);
+}
+
+constexpr size_t kP1Smem = (size_t)kP1Warps * (1024 + 32) * sizeof(double);
+constexpr size_t kP2Smem = (size_t)(kTileElems + kTileElems / 32) * sizeof(double) + 64;
+constexpr size_t kFusedSmem = kP1Smem > kP2Smem ? kP1Smem : kP2Smem;  // covers both item kinds
+
+template <int HB>
+void launch_fused(const SrhtPlan& p, const double* A, const uint32_t* signbits, double* T, int G, int nslot,
+                  const int4* tiles, int n_tiles, const int2* entries, double* SA, unsigned long long* ctl,
+                  int num_sms, cudaStream_t st) {
+    static int max_blocks_per_sm = 0;
+    if (!max_blocks_per_sm) {
+        CUDA_CHECK(cudaFuncSetAttribute(srht_fused_kernel<HB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)kFusedSmem));
+        CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&max_blocks_per_sm, srht_fused_kernel<HB>, kP2Threads,
+                                                                 kFusedSmem));
+        if (max_blocks_per_sm < 1) max_blocks_per_sm = 1;
+    }
+    const int64_t cpc = p.n_pad >> kChunkL;
+    const int ng = (int)ceil_div(p.d, G);
+    const int n1 = (int)ceil_div((int64_t)G * cpc, kP1Warps);
+    const int n2 = G * n_tiles;
+    const int64_t total = (int64_t)ng * (n1 + n2);
+    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(total, (int64_t)num_sms * max_blocks_per_sm));
+    CUDA_CHECK(cudaMemsetAsync(ctl, 0, sizeof(unsigned long long) + 2 * sizeof(int) * (size_t)ng, st));
+    LAUNCH(srht_fused_kernel<HB>, grid, kP2Threads, kFusedSmem, st, A, p.n, p.lda, signbits, T, p.n_pad, p.d, G, nslot,
+           ng, n1, n2, cpc, tiles, n_tiles, entries, p.pass_lo[0], p.scale1, p.scale2, SA, p.m, ctl);
+}
+using FusedFn = void (*)(const SrhtPlan&, const double*, const uint32_t*, double*, int, int, const int4*, int,
+                         const int2*, double*, unsigned long long*, int, cudaStream_t);
+const FusedFn kFused[11] = {nullptr, launch_fused<1>, launch_fused<2>, launch_fused<3>, launch_fused<4>,
+                            launch_fused<5>, launch_fused<6>, launch_fused<7>, launch_fused<8>, launch_fused<9>,
+                            launch_fused<10>};
+constexpr int kFusedSlots = 3;
+constexpr int64_t kFusedRingBytes = 60ll << 20;  // T ring budget: well inside the 126 MB L2
+
+int fused_group_cols(const SrhtPlan& p) {
+    const int64_t per_col = p.n_pad * (int64_t)sizeof(double);
+    return (int)std::max<int64_t>(1, std::min<int64_t>(p.d, kFusedRingBytes / (kFusedSlots * per_col)));
 }
 using PassFn = void (*)(const SrhtPlan&, double*, int, const int4*, int, bool, const int2*, double*, cudaStream_t);
 const PassFn kPass[11] = {nullptr, launch_pass<1>, launch_pass<2>, launch_pass<3>, launch_pass<4>, launch_pass<5>,
@@ -432,11 +595,24 @@ void srht_build_entries(const SrhtPlan& p, const int64_t* rows, std::vector<int2
         }
 }
 
+size_t srht_fused_scratch_bytes(const SrhtPlan& p, size_t* ctl_bytes) {
+    if (ctl_bytes) *ctl_bytes = sizeof(unsigned long long) + 2 * sizeof(int) * (size_t)(p.d + 1) + 64;
+    if (p.H == 0 || p.npass != 1) return srht_scratch_bytes(p);
+    return (size_t)kFusedSlots * fused_group_cols(p) * p.n_pad * sizeof(double);
+}
+
 void srht_run_device(const SrhtPlan& p, const double* d_A, const uint32_t* d_signbits, const int2* d_entries,
-                     const int4* d_tiles, int n_tiles, double* d_T, double* d_SA, cudaStream_t st) {
+                     const int4* d_tiles, int n_tiles, double* d_T, double* d_SA, cudaStream_t st,
+                     unsigned long long* d_ctl, int num_sms) {
     if (p.d == 0) return;
     if (p.H == 0) {
         kSmall[p.L](p, d_A, d_signbits, d_entries, d_SA, st);
+        return;
+    }
+    if (p.npass == 1 && n_tiles > 0 && d_ctl != nullptr) {
+        // one launch, T kept in an L2-resident ring of column groups
+        kFused[p.pass_hb[0]](p, d_A, d_signbits, d_T, fused_group_cols(p), kFusedSlots, d_tiles, n_tiles, d_entries,
+                             d_SA, d_ctl, num_sms, st);
         return;
     }
     const int64_t chunks_per_col = p.n_pad >> kChunkL;
