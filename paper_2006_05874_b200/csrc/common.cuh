@@ -120,14 +120,29 @@ struct GradPlan {
     int R;          // rows per panel
     int grid;       // persistent CTAs
     size_t smem;
-    int version;    // 2: smem-resident panels in a cp.async ring; 1: L2 re-read (large d)
-    int stages;     // v2 ring depth
+    int version;    // 3: TMA-fed panel ring; 2: cp.async panel ring; 1: L2 re-read (large d)
+    int stages;     // ring depth (v2/v3/v4)
+    int grid_sms;   // SM count the plan was made for
+    alignas(64) unsigned char tmap[128];  // CUtensorMap of A (v3)
 };
 GradPlan grad_plan(int64_t n, int64_t d, int64_t lda, int num_sms);
+// upgrade a v2 plan to TMA panels over device matrix A (no-op when unavailable)
+void grad_plan_attach_tma(GradPlan& p, const double* d_A);
+// v4: row-major copy of A (contiguous panels, 1D bulk TMA); switches the plan
+// to v4 when the geometry fits (the caller then keeps a row-major A)
+bool grad_plan_use_rowmajor(GradPlan& p);
+size_t grad_rm_smem(int64_t d, int R, int nrhs, int ns);
+bool grad_rm_geometry(int64_t d, int64_t lda, int* R, int* ns);
+void transpose_to_rowmajor(const double* A, int64_t lda, int64_t rows, int64_t d, double* Arm, cudaStream_t st);
+void grad_rm_run(const GradPlan& p, const double* Arm, const double* b, const double* X, int nrhs, double* work,
+                 cudaStream_t st);
+size_t grad_tma_smem(int64_t d, int R, int nrhs, int ns);
+bool grad_tma_make_map(const double* A, int64_t lda, int64_t d, int R, void* map_out);
+void grad_tma_run(const GradPlan& p, const double* b, const double* X, int nrhs, double* work, cudaStream_t st);
 size_t grad_work_doubles(const GradPlan& p);
 // X: nrhs vectors of d (ld = d); G out: nrhs vectors of d
 void grad_run(const GradPlan& p, const double* d_A, const double* d_b, double nu2, const double* d_X, int nrhs,
-              double* d_G, double* d_work, cudaStream_t st);
+              double* d_G, double* d_work, cudaStream_t st, const double* d_Arm = nullptr);
 
 // vecops.cu
 // out[k*d..] for the heavy-ball candidates (solver.hpp:182,190), no FMA contraction:

@@ -1,0 +1,261 @@
+// grad_rm.cu — fused gradient over a row-major copy of A (sm_100a).
+//
+// Column-major R-row panels are R*8-byte segments 8*lda bytes apart, so a
+// panel read opens a DRAM page per column and the gradient stalls on HBM
+// locality well below the copy roofline. The problem therefore also keeps A
+// row-major (one transpose at upload); a panel of R rows is then one
+// contiguous R*d*8-byte block, moved into shared memory by a single 1D bulk
+// TMA copy (cp.async.bulk) per stage with mbarrier completion.
+//   sweep 1: warps own rows (two warps per row when R = 8), lanes stride the
+//            contiguous row, warp-shuffle reduction -> r = A_p x - b_p;
+//   sweep 2: thread per column, conflict-free reads down the R rows,
+//            r held in registers -> per-CTA column partials.
+// Same fixed-order partial reduction as the other variants (deterministic).
+#include "common.cuh"
+
+namespace ihs_b200 {
+
+namespace {
+constexpr int TT = 512;
+constexpr int TW = TT / 32;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+// RR rows per panel, MAXC = ceil(d / 512) columns per thread, NS stages.
+template <int NRHS, int RR, int MAXC, int NS>
+__global__ void __launch_bounds__(TT, 1)
+grad_rm_kernel(const double* __restrict__ Arm, int64_t d, int64_t npanels, const double* __restrict__ b,
+               const double* __restrict__ X, double* __restrict__ work) {
+    extern __shared__ __align__(128) double sm[];
+    const int64_t stage = (int64_t)RR * d;
+    double* panel = sm;
+    double* xs = panel + NS * stage;     // interleaved [j][q]
+    double* red = xs + NRHS * d;         // TW * NRHS
+    double* rv = red + TW * NRHS;        // NRHS * RR
+    uint64_t* full = reinterpret_cast<uint64_t*>(rv + NRHS * RR + 2);
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const uint32_t stage_bytes = (uint32_t)(stage * sizeof(double));
+    if (t == 0) {
+        for (int s = 0; s < NS; ++s) mbar_init(&full[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    for (int64_t e = t; e < NRHS * d; e += TT) {
+        const int64_t q = e / d, j = e % d;
+        xs[j * NRHS + q] = X[e];
+    }
+    __syncthreads();
+    auto issue = [&](int64_t p, int s) {  // thread 0
+        if (p >= npanels) return;
+        mbar_expect_tx(&full[s], stage_bytes);
+        bulk_load(panel + s * stage, Arm + p * stage, stage_bytes, &full[s]);
+    };
+    int64_t p = blockIdx.x;
+    if (t == 0)
+        for (int k = 0; k < NS; ++k) issue(p + (int64_t)k * gridDim.x, k);
+
+    double gacc[NRHS][MAXC];
+#pragma unroll
+    for (int q = 0; q < NRHS; ++q)
+#pragma unroll
+        for (int c = 0; c < MAXC; ++c) gacc[q][c] = 0.0;
+
+    // sweep-1 ownership: WPR warps per row (TW >= RR), each a contiguous 1/WPR of the row
+    constexpr int WPR = TW / RR > 0 ? TW / RR : 1;
+    constexpr int ROWS_PER_WARP = RR > TW ? RR / TW : 1;
+    int s = 0;
+    uint32_t phase = 0;
+    for (; p < npanels; p += gridDim.x) {
+        mbar_wait(&full[s], phase);
+        const double* P = panel + s * stage;
+        // ---- sweep 1
+#pragma unroll
+        for (int rr = 0; rr < ROWS_PER_WARP; ++rr) {
+            const int row = (warp / WPR) * ROWS_PER_WARP + rr;
+            const int part = warp % WPR;
+            const int64_t seg = (d + WPR - 1) / WPR;
+            const int64_t len = min(seg, d - part * seg);
+            const double* Prow = P + (int64_t)row * d + part * seg;
+            const double* xr = xs + part * seg * NRHS;
+            double acc[NRHS];
+#pragma unroll
+            for (int q = 0; q < NRHS; ++q) acc[q] = 0.0;
+#pragma unroll 4
+            for (int64_t j = lane; j < len; j += 32) {
+                const double a = Prow[j];
+                if constexpr (NRHS == 2) {
+                    const double2 xv = *reinterpret_cast<const double2*>(xr + 2 * j);
+                    acc[0] = fma(a, xv.x, acc[0]);
+                    acc[1] = fma(a, xv.y, acc[1]);
+                } else {
+                    acc[0] = fma(a, xr[j], acc[0]);
+                }
+            }
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+                for (int q = 0; q < NRHS; ++q) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], off);
+            if (lane == 0)
+#pragma unroll
+                for (int q = 0; q < NRHS; ++q) red[(row * WPR + part) * NRHS + q] = acc[q];
+        }
+        __syncthreads();
+        if (t < NRHS * RR) {
+            const int q = t / RR, i = t % RR;
+            double sum = 0.0;
+#pragma unroll
+            for (int w = 0; w < WPR; ++w) sum += red[(i * WPR + w) * NRHS + q];
+            rv[q * RR + i] = sum - b[p * RR + i];
+        }
+        __syncthreads();
+        // ---- sweep 2
+        {
+            double r[NRHS][RR];
+#pragma unroll
+            for (int q = 0; q < NRHS; ++q)
+#pragma unroll
+                for (int i = 0; i < RR; ++i) r[q][i] = rv[q * RR + i];
+#pragma unroll
+            for (int c = 0; c < MAXC; ++c) {
+                const int64_t j = t + (int64_t)c * TT;
+                if (j < d) {
+#pragma unroll
+                    for (int i = 0; i < RR; ++i) {
+                        const double a = P[(int64_t)i * d + j];
+#pragma unroll
+                        for (int q = 0; q < NRHS; ++q) gacc[q][c] = fma(a, r[q][i], gacc[q][c]);
+                    }
+                }
+            }
+        }
+        __syncthreads();  // stage s consumed
+        if (t == 0) issue(p + (int64_t)NS * gridDim.x, s);
+        if (++s == NS) {
+            s = 0;
+            phase ^= 1;
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < NRHS; ++q)
+#pragma unroll
+        for (int c = 0; c < MAXC; ++c) {
+            const int64_t j = t + (int64_t)c * TT;
+            if (j < d) work[((int64_t)blockIdx.x * NRHS + q) * d + j] = gacc[q][c];
+        }
+}
+
+// row-major copy: Arm[i * d + j] = A[i + j * lda], 32x32 tiles through smem
+__global__ void transpose_kernel(const double* __restrict__ A, int64_t lda, int64_t rows, int64_t d,
+                                 double* __restrict__ Arm) {
+    __shared__ double tile[32][33];
+    const int64_t i0 = (int64_t)blockIdx.x * 32, j0 = (int64_t)blockIdx.y * 32;
+    const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+    for (int k = ty; k < 32; k += 8) {
+        const int64_t i = i0 + tx, j = j0 + k;
+        tile[k][tx] = (i < rows && j < d) ? A[i + j * lda] : 0.0;
+    }
+    __syncthreads();
+    for (int k = ty; k < 32; k += 8) {
+        const int64_t i = i0 + k, j = j0 + tx;
+        if (i < rows && j < d) Arm[i * d + j] = tile[tx][k];
+    }
+}
+
+template <int NRHS, int RR, int NS>
+void launch_rm(const GradPlan& p, const double* Arm, const double* b, const double* X, double* work, cudaStream_t st) {
+    const size_t smem = grad_rm_smem(p.d, RR, NRHS, NS);
+    const int maxc = (int)ceil_div(p.d, TT);
+#define IHS_RM(MC)                                                                                                  \
+    do {                                                                                                            \
+        static bool attr = false;                                                                                   \
+        if (!attr) {                                                                                                \
+            CUDA_CHECK(cudaFuncSetAttribute(grad_rm_kernel<NRHS, RR, MC, NS>,                                       \
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));              \
+            attr = true;                                                                                            \
+        }                                                                                                           \
+        LAUNCH((grad_rm_kernel<NRHS, RR, MC, NS>), p.grid, TT, smem, st, Arm, p.d, p.lda / RR, b, X, work);         \
+    } while (0)
+    if (maxc <= 1) IHS_RM(1);
+    else if (maxc <= 2) IHS_RM(2);
+    else if (maxc <= 4) IHS_RM(4);
+    else IHS_RM(8);
+#undef IHS_RM
+}
+}  // namespace
+
+size_t grad_rm_smem(int64_t d, int R, int nrhs, int ns) {
+    return sizeof(double) * ((size_t)ns * R * d + (size_t)nrhs * d + (size_t)TW * nrhs + (size_t)nrhs * R + 2) +
+           (size_t)ns * 8 + 128;
+}
+
+// panel rows / ring depth for the row-major kernel: 64 KiB contiguous panels
+bool grad_rm_geometry(int64_t d, int64_t lda, int* R, int* ns) {
+    if (d > 4096) return false;
+    int r = 1;
+    while (r * 2 <= 16 && (int64_t)(r * 2) * d <= 8192) r *= 2;  // power of two, <= 64 KiB panels
+    if (lda % r || ((int64_t)r * d) % 2) return false;           // 16-byte aligned bulk copies
+    for (int k = 4; k >= 2; --k)
+        if (grad_rm_smem(d, r, 2, k) <= 220u * 1024) {
+            *R = r;
+            *ns = k;
+            return true;
+        }
+    if (r > 1) {  // very wide rows: smaller panels
+        r /= 2;
+        for (int k = 4; k >= 2; --k)
+            if (grad_rm_smem(d, r, 2, k) <= 220u * 1024) {
+                *R = r;
+                *ns = k;
+                return true;
+            }
+    }
+    return false;
+}
+
+void transpose_to_rowmajor(const double* A, int64_t lda, int64_t rows, int64_t d, double* Arm, cudaStream_t st) {
+    dim3 grid((unsigned)ceil_div(rows, 32), (unsigned)ceil_div(d, 32));
+    LAUNCH(transpose_kernel, grid, dim3(32, 8), 0, st, A, lda, rows, d, Arm);
+}
+
+void grad_rm_run(const GradPlan& p, const double* Arm, const double* b, const double* X, int nrhs, double* work,
+                 cudaStream_t st) {
+    const int key = p.R * 10 + p.stages;
+#define IHS_CASE(RRv, NSv)                                                         \
+    case RRv * 10 + NSv:                                                           \
+        if (nrhs == 1) launch_rm<1, RRv, NSv>(p, Arm, b, X, work, st);             \
+        else launch_rm<2, RRv, NSv>(p, Arm, b, X, work, st);                       \
+        return;
+    switch (key) {
+        IHS_CASE(16, 2) IHS_CASE(16, 3) IHS_CASE(16, 4)
+        IHS_CASE(8, 2) IHS_CASE(8, 3) IHS_CASE(8, 4)
+        IHS_CASE(4, 2) IHS_CASE(4, 3) IHS_CASE(4, 4)
+        IHS_CASE(2, 2) IHS_CASE(2, 3) IHS_CASE(2, 4)
+        IHS_CASE(1, 2) IHS_CASE(1, 3) IHS_CASE(1, 4)
+    }
+#undef IHS_CASE
+    fail(IHS_INTERNAL_ERROR, "gradient (row-major): no kernel for the chosen panel geometry");
+}
+
+}  // namespace ihs_b200

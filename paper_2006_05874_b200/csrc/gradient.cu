@@ -16,6 +16,8 @@
 // every load (both heavy-ball candidates of one iteration in one pass).
 #include "common.cuh"
 
+#include <cstdlib>
+
 namespace ihs_b200 {
 
 namespace {
@@ -322,6 +324,7 @@ GradPlan grad_plan(int64_t n, int64_t d, int64_t lda, int num_sms) {
     p.n = n;
     p.d = d;
     p.lda = lda;
+    p.grid_sms = num_sms;
     // v2: one 512-thread CTA per SM streaming R x d panels through an NS-deep
     // cp.async ring (>= 3 x 64 KiB in flight per SM when it fits); prefer
     // 128/64 B column segments (R = 16/8), fall back to 32 B (R = 4).
@@ -353,10 +356,39 @@ GradPlan grad_plan(int64_t n, int64_t d, int64_t lda, int num_sms) {
 
 size_t grad_work_doubles(const GradPlan& p) { return (size_t)p.grid * 2 * p.d; }
 
+bool grad_plan_use_rowmajor(GradPlan& p) {
+    static const bool disabled = [] {
+        const char* e = std::getenv("IHS_GRAD_NO_ROWMAJOR");
+        return e && e[0] == '1';
+    }();
+    int R = 0, ns = 0;
+    if (disabled || !grad_rm_geometry(p.d, p.lda, &R, &ns)) return false;
+    p.version = 4;
+    p.R = R;
+    p.stages = ns;
+    p.smem = grad_rm_smem(p.d, R, 2, ns);
+    const int64_t npanels = p.lda / R;
+    p.grid = (int)std::max<int64_t>(1, std::min<int64_t>(npanels, (int64_t)p.grid_sms));
+    return true;
+}
+
+void grad_plan_attach_tma(GradPlan& p, const double* d_A) {
+    static const bool disabled = [] {
+        const char* e = std::getenv("IHS_GRAD_NO_TMA");
+        return e && e[0] == '1';
+    }();
+    if (disabled || p.version != 2) return;
+    if (grad_tma_smem(p.d, p.R, 2, p.stages) > 225u * 1024) return;
+    if (!grad_tma_make_map(d_A, p.lda, p.d, p.R, p.tmap)) return;
+    p.version = 3;
+}
+
 void grad_run(const GradPlan& p, const double* d_A, const double* d_b, double nu2, const double* d_X, int nrhs,
-              double* d_G, double* d_work, cudaStream_t st) {
-    if (p.version == 2) {
-        if (nrhs == 1) launch_v2_dispatch<1>(p, d_A, d_b, d_X, d_work, st);
+              double* d_G, double* d_work, cudaStream_t st, const double* d_Arm) {
+    if (p.version >= 2) {
+        if (p.version == 4) grad_rm_run(p, d_Arm, d_b, d_X, nrhs, d_work, st);
+        else if (p.version == 3) grad_tma_run(p, d_b, d_X, nrhs, d_work, st);
+        else if (nrhs == 1) launch_v2_dispatch<1>(p, d_A, d_b, d_X, d_work, st);
         else launch_v2_dispatch<2>(p, d_A, d_b, d_X, d_work, st);
         const int64_t total = (int64_t)nrhs * p.d;
         LAUNCH(grad_reduce_kernel, (unsigned)ceil_div(total, 16), 256, 0, st, d_work, p.grid, p.d, nrhs, d_X, nu2,

@@ -246,6 +246,7 @@ struct ihs_gpu_problem {
     int num_sms = 148;
     int64_t lda = 0;             // device leading dimension: n rounded up to 32 (256 B columns)
     DevBuf A, b;                 // A (lda x d, column-major), b (lda); padding rows are zero
+    DevBuf Arm;                  // row-major copy of A for the gradient (lda x d), when it fits
     GradPlan gplan{};
     DevBuf grad_work;
     // sketch workspaces
@@ -461,6 +462,7 @@ void upload_Ab(ihs_gpu_problem* P, const double* A, int64_t lda_host, const doub
         CUDA_CHECK(cudaMemcpy2DAsync(P->A.p, (size_t)P->lda * sizeof(double), A, (size_t)lda_host * sizeof(double),
                                      (size_t)P->n * sizeof(double), (size_t)P->d, cudaMemcpyHostToDevice, P->st));
     if (b) CUDA_CHECK(cudaMemcpyAsync(P->b.p, b, (size_t)P->n * sizeof(double), cudaMemcpyHostToDevice, P->st));
+    if (A && P->Arm.p) transpose_to_rowmajor(P->A.d(), P->lda, P->lda, P->d, P->Arm.d(), P->st);
 }
 void alloc_and_upload(ihs_gpu_problem* P, const double* A, int64_t lda_host, const double* b) {
     P->lda = ceil_div(P->n, 32) * 32;
@@ -477,11 +479,11 @@ void alloc_and_upload(ihs_gpu_problem* P, const double* A, int64_t lda_host, con
 void problem_grad(ihs_gpu_problem* P, const double* X, int nrhs, double* G) {
     const double nu2 = P->nu * P->nu;
     if (P->opts.world_size > 1) {
-        grad_run(P->gplan, P->A.d(), P->b.d(), 0.0, X, nrhs, G, P->grad_work.d(), P->st);
+        grad_run(P->gplan, P->A.d(), P->b.d(), 0.0, X, nrhs, G, P->grad_work.d(), P->st, P->Arm.d());
         nccl_allreduce_sum(G, (size_t)nrhs * P->d, P->opts.nccl_comm, P->st);
         add_scaled(G, X, nu2, (int64_t)nrhs * P->d, P->st);
     } else {
-        grad_run(P->gplan, P->A.d(), P->b.d(), nu2, X, nrhs, G, P->grad_work.d(), P->st);
+        grad_run(P->gplan, P->A.d(), P->b.d(), nu2, X, nrhs, G, P->grad_work.d(), P->st, P->Arm.d());
     }
 }
 
@@ -681,6 +683,20 @@ ihs_status ihs_gpu_problem_create(const double* A, int64_t n, int64_t d, int64_t
         StreamScope scope(P->st);
         alloc_and_upload(P.get(), A, lda, b);
         P->gplan = grad_plan(n, d, P->lda, P->num_sms);
+        {
+            // row-major copy of A for the gradient when it fits comfortably in HBM
+            size_t free_b = 0, total_b = 0;
+            CUDA_CHECK(cudaMemGetInfo(&free_b, &total_b));
+            const size_t need = (size_t)P->lda * d * sizeof(double);
+            GradPlan rm = P->gplan;
+            if (need * 3 < free_b && grad_plan_use_rowmajor(rm)) {
+                P->gplan = rm;
+                P->Arm.ensure(need);
+                transpose_to_rowmajor(P->A.d(), P->lda, P->lda, d, P->Arm.d(), P->st);
+            } else {
+                grad_plan_attach_tma(P->gplan, P->A.d());
+            }
+        }
         P->grad_work.ensure(grad_work_doubles(P->gplan) * sizeof(double));
         P->vecs.ensure((size_t)16 * d * sizeof(double));
         P->dots.ensure(8 * sizeof(double));
