@@ -20,71 +20,67 @@ namespace {
 constexpr int NB = 64;
 
 // Unblocked LLT of the nb x nb diagonal block at (k,k), in shared memory.
+// 256 threads = 64 rows x 4 column groups; per column: every thread derives
+// the pivot itself, one barrier after the column scaling, one after the
+// rank-1 update (no integer division in the loops).
 __global__ void __launch_bounds__(256) potrf_diag_kernel(double* __restrict__ H, int64_t n, int64_t k, int nb,
                                                          int* __restrict__ info) {
     __shared__ double a[NB][NB + 1];
-    for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) {
-        const int i = e % nb, j = e / nb;
-        a[i][j] = (i >= j) ? H[(k + i) + (k + j) * n] : 0.0;
-    }
-    __syncthreads();
-    __shared__ int bad;
-    if (threadIdx.x == 0) bad = 0;
+    __shared__ double diag[NB];
+    const int i = threadIdx.x % NB, g = threadIdx.x / NB;  // row, column group (4)
+    for (int jj = g; jj < nb; jj += 4) a[i][jj] = (i < nb && i >= jj) ? H[(k + i) + (k + jj) * n] : 0.0;
     __syncthreads();
     for (int j = 0; j < nb; ++j) {
-        // pivot
+        const double s = a[j][j];
+        const bool ok = (s > 0.0) && isfinite(s);
+        const double ljj = ok ? sqrt(s) : 1.0;  // a failed pivot is flagged; keep going harmlessly
         if (threadIdx.x == 0) {
-            const double s = a[j][j];
-            if (!(s > 0.0) || !isfinite(s)) {
-                if (!bad) { bad = 1; atomicCAS(info, 0, (int)(k + j + 1)); }
-                a[j][j] = 1.0;  // keep going with a harmless pivot; result is flagged
-            } else {
-                a[j][j] = sqrt(s);
-            }
+            diag[j] = ljj;
+            if (!ok) atomicCAS(info, 0, (int)(k + j + 1));
         }
+        if (g == 0 && i > j && i < nb) a[i][j] = a[i][j] / ljj;
         __syncthreads();
-        const double ljj = a[j][j];
-        for (int i = j + 1 + threadIdx.x; i < nb; i += blockDim.x) a[i][j] = a[i][j] / ljj;
-        __syncthreads();
-        // rank-1 update of the trailing lower block
-        const int rem = nb - j - 1;
-        for (int e = threadIdx.x; e < rem * rem; e += blockDim.x) {
-            const int ii = j + 1 + e % rem, jj = j + 1 + e / rem;
-            if (ii >= jj) a[ii][jj] -= a[ii][j] * a[jj][j];
+        if (i > j && i < nb) {
+            const double lij = a[i][j];
+            for (int jj = j + 1 + g; jj <= i; jj += 4) a[i][jj] -= lij * a[jj][j];
         }
         __syncthreads();
     }
-    for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) {
-        const int i = e % nb, j = e / nb;
-        if (i >= j) H[(k + i) + (k + j) * n] = a[i][j];
-    }
+    for (int jj = g; jj < nb; jj += 4)
+        if (i < nb && i >= jj) H[(k + i) + (k + jj) * n] = (i == jj) ? diag[i] : a[i][jj];
 }
 
-// L21 = A21 * L11^{-T}: each thread solves one row x * L11^T = a.
-__global__ void __launch_bounds__(128) trsm_panel_kernel(double* __restrict__ H, int64_t n, int64_t k, int nb) {
+// L21 = A21 * L11^{-T}: one warp per row, lane c holds columns c and c+32 of
+// the row; column c is finished by its owner lane and broadcast by shuffle.
+constexpr int TRSM_WARPS = 8;
+__global__ void __launch_bounds__(32 * TRSM_WARPS) trsm_panel_kernel(double* __restrict__ H, int64_t n, int64_t k,
+                                                                     int nb) {
     __shared__ double l[NB][NB + 1];
-    for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) {
-        const int i = e % nb, j = e / nb;
-        l[i][j] = (i >= j) ? H[(k + i) + (k + j) * n] : 0.0;
+    for (int e = threadIdx.x; e < NB * NB; e += blockDim.x) {
+        const int ii = e % NB, jj = e / NB;
+        l[ii][jj] = (ii < nb && jj < nb && ii >= jj) ? H[(k + ii) + (k + jj) * n] : 0.0;
     }
     __syncthreads();
-    const int64_t row = k + nb + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t row = k + nb + (int64_t)blockIdx.x * TRSM_WARPS + warp;
     if (row >= n) return;
-    double x[NB];
-#pragma unroll
-    for (int c = 0; c < NB; ++c) x[c] = (c < nb) ? H[row + (k + c) * n] : 0.0;
-#pragma unroll
-    for (int c = 0; c < NB; ++c) {
-        if (c < nb) {
-            double s = x[c];
-#pragma unroll
-            for (int q = 0; q < c; ++q) s -= x[q] * l[c][q];
-            x[c] = s / l[c][c];
+    double x0 = (lane < nb) ? H[row + (k + lane) * n] : 0.0;
+    double x1 = (lane + 32 < nb) ? H[row + (k + lane + 32) * n] : 0.0;
+    for (int c = 0; c < nb; ++c) {
+        // finish x[c] on its owner lane, broadcast, update the columns after it
+        const bool hi = c >= 32;
+        double xc = 0.0;
+        if (lane == (c & 31)) xc = (hi ? x1 : x0) / l[c][c];
+        xc = __shfl_sync(0xffffffffu, xc, c & 31);
+        if (lane == (c & 31)) {
+            if (hi) x1 = xc;
+            else x0 = xc;
         }
+        if (!hi && lane > c) x0 -= xc * l[lane][c];
+        if (lane + 32 > c && lane + 32 < nb) x1 -= xc * l[lane + 32][c];
     }
-#pragma unroll
-    for (int c = 0; c < NB; ++c)
-        if (c < nb) H[row + (k + c) * n] = x[c];
+    if (lane < nb) H[row + (k + lane) * n] = x0;
+    if (lane + 32 < nb) H[row + (k + lane + 32) * n] = x1;
 }
 
 // strict upper triangle <- L^T (H[i + j n] = H[j + i n] for i < j)
@@ -253,7 +249,7 @@ void cholesky_factor(double* d_H, int64_t n, double* d_work, int* d_info, int nu
         LAUNCH(potrf_diag_kernel, 1, 256, 0, st, d_H, n, k, nb, d_info);
         const int64_t rest = n - k - nb;
         if (rest > 0) {
-            LAUNCH(trsm_panel_kernel, (unsigned)ceil_div(rest, 128), 128, 0, st, d_H, n, k, nb);
+            LAUNCH(trsm_panel_kernel, (unsigned)ceil_div(rest, TRSM_WARPS), 32 * TRSM_WARPS, 0, st, d_H, n, k, nb);
             // A22 -= L21 L21^T (lower)
             double* L21 = d_H + (k + nb) + k * n;
             double* A22 = d_H + (k + nb) + (k + nb) * n;

@@ -77,9 +77,12 @@ void srht_build_entries(const SrhtPlan& p, const int64_t* rows, std::vector<int2
 // fit one pass): T is then a ring of srht_fused_scratch_bytes() and d_ctl a
 // control block of *ctl_bytes.
 size_t srht_fused_scratch_bytes(const SrhtPlan& p, size_t* ctl_bytes);
+// d_mask (4 words, from srht_build_mask): phase 1 stores only the low-index
+// groups the single emitting pass reads.
 void srht_run_device(const SrhtPlan& p, const double* d_A, const uint32_t* d_signbits, const int2* d_entries,
                      const int4* d_tiles, int n_tiles, double* d_T, double* d_SA, cudaStream_t st,
-                     unsigned long long* d_ctl = nullptr, int num_sms = 148);
+                     unsigned long long* d_ctl = nullptr, int num_sms = 148, const uint32_t* d_mask = nullptr);
+bool srht_build_mask(const SrhtPlan& p, const std::vector<int4>& tiles, uint32_t mask[4]);
 // Row-sharded SRHT: plan of one shard (n_loc = n_pad / P rows, n_real of them
 // real) that emits unscaled partials at r_lo(k) for all m sampled rows, and the
 // combine of the P gathered partials ([P][m][d]) into SA (d_hi[k] = r_hi(k)).
@@ -158,6 +161,10 @@ void gemv_n(const double* A, int64_t M, int64_t N, int64_t lda, const double* x,
             int64_t ldy, cudaStream_t st);
 void woodbury_finish(const double* SA, int64_t m, int64_t d, const double* g, const double* w, double nu2, int nrhs,
                      double* z, cudaStream_t st);
+// tiled y = A x (64x64 CTA tiles, fixed-order chunk reduction); work: gemv_tiled_work_doubles
+size_t gemv_tiled_work_doubles(int64_t M, int64_t N);
+void gemv_tiled(const double* A, int64_t M, int64_t N, int64_t lda, const double* x, int nrhs, int64_t ldx, double* y,
+                int64_t ldy, double* work, cudaStream_t st);
 void add_diag(double* H, int64_t n, double v, cudaStream_t st);
 void add_scaled(double* y, const double* x, double a, int64_t n, cudaStream_t st);  // y = y + a x
 void check_finite(const double* v, int64_t count, int* d_flag, cudaStream_t st);

@@ -253,6 +253,9 @@ struct ihs_gpu_problem {
     DevBuf T, signbits, rng_scratch, entries, tiles, gauss_scratch, S, gemm_work;
     DevBuf shard_U, shard_hi;    // sharded SRHT partials [P][m][d] and r_hi(k)
     DevBuf fused_ctl;            // work-queue counters of the fused SRHT kernel
+    DevBuf srht_mask;            // phase-1 store mask (active low-index groups)
+    uint32_t h_mask[4] = {0, 0, 0, 0};
+    bool mask_valid = false;
     PinnedBuf h_stage;
     std::vector<int64_t> h_rows;
     std::vector<int2> h_entries;
@@ -269,11 +272,12 @@ namespace {
 
 // -------------------------------------------------------- sketches (device)
 // T scratch and the fused kernel's control block; nullptr control = the
-// two-kernel path (IHS_SRHT_UNFUSED=1 forces it, for A/B measurements).
+// two-kernel path (default: measured faster; IHS_SRHT_FUSED=1 selects the
+// persistent single-launch kernel for A/B measurements).
 unsigned long long* srht_prepare_scratch(ihs_gpu_problem* P, const SrhtPlan& plan) {
     static const bool unfused = [] {
-        const char* e = std::getenv("IHS_SRHT_UNFUSED");
-        return e && e[0] == '1';
+        const char* e = std::getenv("IHS_SRHT_FUSED");
+        return !(e && e[0] == '1');
     }();
     if (unfused) {
         P->T.ensure(srht_scratch_bytes(plan));
@@ -294,10 +298,14 @@ void upload_entries(ihs_gpu_problem* P) {
     CUDA_CHECK(cudaStreamSynchronize(st));
     std::memcpy(P->h_stage.p, P->h_entries.data(), eb);
     std::memcpy(static_cast<char*>(P->h_stage.p) + eb, P->h_tiles.data(), tb);
+    std::memcpy(static_cast<char*>(P->h_stage.p) + eb + tb, P->h_mask, sizeof(P->h_mask));
     P->entries.ensure(eb + 16);
     P->tiles.ensure(tb + 16);
+    P->srht_mask.ensure(sizeof(P->h_mask));
     CUDA_CHECK(cudaMemcpyAsync(P->entries.p, P->h_stage.p, eb, cudaMemcpyHostToDevice, st));
     CUDA_CHECK(cudaMemcpyAsync(P->tiles.p, static_cast<char*>(P->h_stage.p) + eb, tb, cudaMemcpyHostToDevice, st));
+    CUDA_CHECK(cudaMemcpyAsync(P->srht_mask.p, static_cast<char*>(P->h_stage.p) + eb + tb, sizeof(P->h_mask),
+                               cudaMemcpyHostToDevice, st));
 }
 
 // SA (m x d, ld m, device) = apply_sketch(A, {kind, m, seed}) (sketch.hpp:110-117).
@@ -326,12 +334,14 @@ void device_sketch(ihs_gpu_problem* P, int kind, int64_t m, uint64_t seed, doubl
         const int shards = world > 1 ? world : std::max(1, emulate_shards);
         if (shards == 1) {
             srht_build_entries(plan, P->h_rows.data(), P->h_entries, P->h_tiles);
+            P->mask_valid = srht_build_mask(plan, P->h_tiles, P->h_mask);
             g_host_rng_ns +=
                 std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t_rng).count();
             upload_entries(P);
             unsigned long long* ctl = srht_prepare_scratch(P, plan);
             srht_run_device(plan, P->A.d(), P->signbits.as<uint32_t>(), P->entries.as<int2>(), P->tiles.as<int4>(),
-                            (int)P->h_tiles.size(), P->T.d(), d_SA, st, ctl, P->num_sms);
+                            (int)P->h_tiles.size(), P->T.d(), d_SA, st, ctl, P->num_sms,
+                            P->mask_valid ? P->srht_mask.as<uint32_t>() : nullptr);
         } else {
             // shard p holds rows [p*n_loc, (p+1)*n_loc) of the padded index space
             const int64_t n_loc = plan.n_pad / shards;
@@ -343,6 +353,7 @@ void device_sketch(ihs_gpu_problem* P, int kind, int64_t m, uint64_t seed, doubl
             }
             const SrhtPlan sp = srht_plan_shard(std::min(n_loc, n), n_loc, d, P->lda, m);
             srht_build_entries(sp, lo.data(), P->h_entries, P->h_tiles);
+            P->mask_valid = srht_build_mask(sp, P->h_tiles, P->h_mask);
             g_host_rng_ns +=
                 std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t_rng).count();
             upload_entries(P);
@@ -356,7 +367,7 @@ void device_sketch(ihs_gpu_problem* P, int kind, int64_t m, uint64_t seed, doubl
                 s.n = n_real;
                 srht_run_device(s, A_p, P->signbits.as<uint32_t>() + (p * n_loc) / 32, P->entries.as<int2>(),
                                 P->tiles.as<int4>(), (int)P->h_tiles.size(), P->T.d(), U + (int64_t)p * m * d, st,
-                                ctl, P->num_sms);
+                                ctl, P->num_sms, P->mask_valid ? P->srht_mask.as<uint32_t>() : nullptr);
             };
             if (world > 1) {
                 const int r = P->opts.rank;
@@ -436,7 +447,8 @@ void system_factorize(ihs_gpu_system* S, ihs_counters* c) {
     CUDA_CHECK(cudaStreamSynchronize(st));
     if (h_info[1]) fail(IHS_INVALID_INPUT, "SketchedSystem: non-finite sketched matrix");
     if (h_info[0]) fail(IHS_NUMERICAL_BREAKDOWN, "SketchedSystem: Cholesky factorization failed");
-    S->tmp.ensure((size_t)(4 * std::max(m, d) + cholesky_solve_work_doubles(k)) * sizeof(double));
+    S->tmp.ensure((size_t)(4 * std::max(m, d) + std::max(cholesky_solve_work_doubles(k), gemv_tiled_work_doubles(m, d))) *
+                  sizeof(double));
     if (c) c->factor += S->factor_flops();
 }
 
@@ -448,7 +460,7 @@ void system_solve_dev(const ihs_gpu_system* S, const double* g, double* z, int n
     if (S->kind == IHS_FACTOR_WOODBURY_INNER) {
         double* u = S->tmp.d();      // nrhs x m : u = SA g
         double* w = u + 2 * m;       // nrhs x m : w = (SA SA^T + nu^2 I)^{-1} u
-        gemv_n(S->SA.d(), m, d, m, g, nrhs, d, u, m, st);
+        gemv_tiled(S->SA.d(), m, d, m, g, nrhs, d, u, m, work, st);
         cholesky_solve_inv(S->W.d(), m, u, w, nrhs, work, st);
         woodbury_finish(S->SA.d(), m, d, g, w, S->nu * S->nu, nrhs, z, st);
     } else {

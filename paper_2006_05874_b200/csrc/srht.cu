@@ -112,7 +112,8 @@ srht_small_kernel(const double* __restrict__ A, int64_t n, int64_t lda, const ui
 // dst[0..1024). STREAM: A loads are evict-first (read exactly once).
 template <bool STREAM>
 __device__ __forceinline__ void p1_chunk(double* __restrict__ xs, const double* __restrict__ Acol, int64_t n,
-                                         const uint32_t* __restrict__ signbits, int64_t r0, double* __restrict__ dst) {
+                                         const uint32_t* __restrict__ signbits, int64_t r0, double* __restrict__ dst,
+                                         const uint32_t* __restrict__ mask = nullptr, int logw = 0) {
     const int lane = threadIdx.x & 31;
     double v[32];
     // coalesced load (lane = index bits 0-4, register c = bits 5-9), sign fused
@@ -144,23 +145,118 @@ __device__ __forceinline__ void p1_chunk(double* __restrict__ xs, const double* 
 #pragma unroll
         for (int c = 0; c < 32; ++c)
             if (!(c & (1 << s))) bfly(v[c], v[c | (1 << s)]);
+    if (mask == nullptr) {
 #pragma unroll
-    for (int c = 0; c < 32; ++c) dst[(c << 5) + lane] = v[c];
+        for (int c = 0; c < 32; ++c) dst[(c << 5) + lane] = v[c];
+    } else {
+        // store only the low-index groups a sampled row will read in phase 2
+        uint32_t mw[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) mw[k] = __ldg(mask + k);
+#pragma unroll
+        for (int c = 0; c < 32; ++c) {
+            const int e = (c << 5) + lane;
+            const int g = e >> logw;
+            if ((mw[g >> 5] >> (g & 31)) & 1u) dst[e] = v[c];
+        }
+    }
 }
 
-// Warp-per-chunk: bits 0..9 of every 1024-row chunk of every column -> T.
-__global__ void __launch_bounds__(32 * kP1Warps)
+// 8-byte async copy global -> shared; src_valid == false zero-fills (+0.0).
+__device__ __forceinline__ void cp_async8_zfill(double* dst, const double* src, bool src_valid) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(src), "r"(src_valid ? 8 : 0)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
+// Persistent warp-per-chunk phase 1: bits 0..9 of every 1024-row chunk of
+// every column -> T. Each warp streams its chunks through a two-slot ring of
+// padded shared buffers filled by cp.async (the next chunk is in flight while
+// the current one is transformed), so HBM sees ~kP1Warps x 8 KiB of reads in
+// flight per SM at all times. The sign is applied on the first transposed
+// read (lane holds rows 32*lane .. 32*lane+31: one sign word per lane).
+constexpr int kP1Buf = 1024 + 32;
+constexpr int kP1Stages = 2;
+constexpr int kP1AWarps = 12;
+__global__ void __launch_bounds__(32 * kP1AWarps, 1)
 srht_phase1_kernel(const double* __restrict__ A, int64_t n, int64_t lda, const uint32_t* __restrict__ signbits,
-                   double* __restrict__ T, int64_t n_pad, int64_t chunks_per_col, int64_t total_chunks) {
-    extern __shared__ double p1_smem[];  // kP1Warps x (1024 + 32) doubles
-    const int warp = threadIdx.x >> 5;
-    double* xs = p1_smem + warp * (1024 + 32);
-    for (int64_t chunk = (int64_t)blockIdx.x * kP1Warps + warp; chunk < total_chunks;
-         chunk += (int64_t)gridDim.x * kP1Warps) {
+                   double* __restrict__ T, int64_t n_pad, int64_t chunks_per_col, int64_t total_chunks,
+                   const uint32_t* __restrict__ mask, int logw) {
+    extern __shared__ double p1_smem[];  // kP1AWarps x kP1Stages x kP1Buf doubles
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double* ring = p1_smem + warp * (kP1Stages * kP1Buf);
+    const int64_t nw = (int64_t)gridDim.x * kP1AWarps;
+    auto issue = [&](int64_t chunk, int slot) {
+        if (chunk < total_chunks) {
+            const int64_t j = chunk / chunks_per_col;
+            const int64_t r0 = (chunk % chunks_per_col) << kChunkL;
+            const double* col = A + j * lda;
+            double* buf = ring + slot * kP1Buf;
+#pragma unroll
+            for (int c = 0; c < 32; ++c) {
+                const int64_t r = r0 + (c << 5) + lane;
+                cp_async8_zfill(buf + pad32((c << 5) | lane), r < n ? col + r : col, r < n);
+            }
+        }
+        cp_async_commit();
+    };
+    uint32_t mw[4] = {0u, 0u, 0u, 0u};
+    if (mask != nullptr)
+        for (int k = 0; k < 4; ++k) mw[k] = __ldg(mask + k);
+    int slot = 0;
+    int64_t chunk = (int64_t)blockIdx.x * kP1AWarps + warp;
+    issue(chunk, 0);
+    for (; chunk < total_chunks; chunk += nw) {
+        issue(chunk + nw, slot ^ 1);
+        cp_async_wait1();
+        __syncwarp();
         const int64_t j = chunk / chunks_per_col;
         const int64_t r0 = (chunk % chunks_per_col) << kChunkL;
-        p1_chunk<false>(xs, A + j * lda, n, signbits, r0, T + j * n_pad + r0);
+        double* buf = ring + slot * kP1Buf;
+        const int64_t rl = r0 + (lane << 5);  // this lane's 32 rows (register c = bits 0-4)
+        const uint32_t sw = rl < n ? __ldg(signbits + (rl >> 5)) : 0u;
+        double v[32];
+#pragma unroll
+        for (int c = 0; c < 32; ++c) {
+            const double a = buf[pad32((lane << 5) | c)];
+            v[c] = (rl + c < n) ? __dmul_rn(((sw >> c) & 1u) ? 1.0 : -1.0, a) : 0.0;
+        }
+#pragma unroll
+        for (int s = 0; s < 5; ++s)
+#pragma unroll
+            for (int c = 0; c < 32; ++c)
+                if (!(c & (1 << s))) bfly(v[c], v[c | (1 << s)]);
+#pragma unroll
+        for (int c = 0; c < 32; ++c) buf[pad32((lane << 5) | c)] = v[c];
+        __syncwarp();
+        // register c = index bits 5-9: stages 5..9
+#pragma unroll
+        for (int c = 0; c < 32; ++c) v[c] = buf[pad32((c << 5) | lane)];
+#pragma unroll
+        for (int s = 0; s < 5; ++s)
+#pragma unroll
+            for (int c = 0; c < 32; ++c)
+                if (!(c & (1 << s))) bfly(v[c], v[c | (1 << s)]);
+        double* dst = T + j * n_pad + r0;
+        if (mask == nullptr) {
+#pragma unroll
+            for (int c = 0; c < 32; ++c) dst[(c << 5) + lane] = v[c];
+        } else {
+            // store only the low-index groups a sampled row will read in phase 2
+#pragma unroll
+            for (int c = 0; c < 32; ++c) {
+                const int e = (c << 5) + lane;
+                const int g = e >> logw;
+                if ((mw[g >> 5] >> (g & 31)) & 1u) dst[e] = v[c];
+            }
+        }
+        __syncwarp();  // the slot is refilled by the next iteration's issue
+        slot ^= 1;
     }
+    cp_async_wait0();
 }
 
 
@@ -601,9 +697,21 @@ size_t srht_fused_scratch_bytes(const SrhtPlan& p, size_t* ctl_bytes) {
     return (size_t)kFusedSlots * fused_group_cols(p) * p.n_pad * sizeof(double);
 }
 
+bool srht_build_mask(const SrhtPlan& p, const std::vector<int4>& tiles, uint32_t mask[4]) {
+    mask[0] = mask[1] = mask[2] = mask[3] = 0u;
+    if (p.H == 0 || p.npass != 1) return false;
+    int logw = 0;
+    while ((1 << (logw + 1)) <= pass_w(p.pass_hb[0])) ++logw;
+    for (const int4& t : tiles) {
+        const int g = (t.x & ((1 << kChunkL) - 1)) >> logw;
+        mask[g >> 5] |= 1u << (g & 31);
+    }
+    return true;
+}
+
 void srht_run_device(const SrhtPlan& p, const double* d_A, const uint32_t* d_signbits, const int2* d_entries,
                      const int4* d_tiles, int n_tiles, double* d_T, double* d_SA, cudaStream_t st,
-                     unsigned long long* d_ctl, int num_sms) {
+                     unsigned long long* d_ctl, int num_sms, const uint32_t* d_mask) {
     if (p.d == 0) return;
     if (p.H == 0) {
         kSmall[p.L](p, d_A, d_signbits, d_entries, d_SA, st);
@@ -617,15 +725,20 @@ void srht_run_device(const SrhtPlan& p, const double* d_A, const uint32_t* d_sig
     }
     const int64_t chunks_per_col = p.n_pad >> kChunkL;
     const int64_t total = chunks_per_col * p.d;
-    const int64_t blocks = std::min<int64_t>(ceil_div(total, kP1Warps), (int64_t)1 << 20);
-    const size_t smem = (size_t)kP1Warps * (1024 + 32) * sizeof(double);
+    const int64_t blocks = std::min<int64_t>(ceil_div(total, kP1AWarps), (int64_t)num_sms);
+    const size_t smem = (size_t)kP1AWarps * kP1Stages * kP1Buf * sizeof(double);
     static bool attr = false;
     if (!attr) {
         CUDA_CHECK(cudaFuncSetAttribute(srht_phase1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr = true;
     }
-    LAUNCH(srht_phase1_kernel, (unsigned)blocks, 32 * kP1Warps, smem, st, d_A, p.n, p.lda, d_signbits, d_T, p.n_pad,
-           chunks_per_col, total);
+    // single pass: phase 1 writes only the groups the emitting pass reads
+    const bool masked = p.npass == 1 && d_mask != nullptr;
+    int logw = 0;
+    if (masked)
+        while ((1 << (logw + 1)) <= pass_w(p.pass_hb[0])) ++logw;
+    LAUNCH(srht_phase1_kernel, (unsigned)blocks, 32 * kP1AWarps, smem, st, d_A, p.n, p.lda, d_signbits, d_T, p.n_pad,
+           chunks_per_col, total, masked ? d_mask : nullptr, logw);
     for (int i = 0; i < p.npass; ++i) {
         const bool last = i == p.npass - 1;
         if (last && n_tiles == 0) break;

@@ -70,6 +70,49 @@ __global__ void gemv_n_kernel(const double* __restrict__ A, int64_t M, int64_t N
     }
 }
 
+// Tiled y = A x: CTA = 64 rows x 64 columns, 256 threads (64 rows x 4 column
+// interleaves of 16 columns); partials per column chunk, summed in order.
+constexpr int GV_ROWS = 64, GV_COLS = 64;
+__global__ void __launch_bounds__(256) gemv_partial_kernel(const double* __restrict__ A, int64_t M, int64_t N,
+                                                           int64_t lda, const double* __restrict__ x, int nrhs,
+                                                           int64_t ldx, double* __restrict__ part) {
+    const int64_t r0 = (int64_t)blockIdx.x * GV_ROWS, c0 = (int64_t)blockIdx.y * GV_COLS;
+    const int64_t c1 = c0 + GV_COLS < N ? c0 + GV_COLS : N;
+    __shared__ double xs[2][GV_COLS];
+    __shared__ double red[4][2][GV_ROWS];
+    for (int e = threadIdx.x; e < (int)(c1 - c0); e += blockDim.x)
+        for (int q = 0; q < nrhs; ++q) xs[q][e] = x[q * ldx + c0 + e];
+    __syncthreads();
+    const int r = threadIdx.x % GV_ROWS, qg = threadIdx.x / GV_ROWS;
+    const int64_t row = r0 + r;
+    double acc[2] = {0.0, 0.0};
+    if (row < M) {
+#pragma unroll 4
+        for (int64_t j = c0 + qg; j < c1; j += 4) {
+            const double a = A[row + j * lda];
+            acc[0] = fma(a, xs[0][j - c0], acc[0]);
+            if (nrhs > 1) acc[1] = fma(a, xs[1][j - c0], acc[1]);
+        }
+    }
+    red[qg][0][r] = acc[0];
+    red[qg][1][r] = acc[1];
+    __syncthreads();
+    if (threadIdx.x < GV_ROWS && row < M)
+        for (int q = 0; q < nrhs; ++q)
+            part[((int64_t)blockIdx.y * nrhs + q) * M + row] = (red[0][q][r] + red[1][q][r]) + (red[2][q][r] + red[3][q][r]);
+}
+
+__global__ void gemv_reduce_kernel(const double* __restrict__ part, int64_t M, int nrhs, int nchunks,
+                                   double* __restrict__ y, int64_t ldy) {
+    const int64_t total = (int64_t)nrhs * M;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t q = e / M, row = e % M;
+        double s = 0.0;
+        for (int c = 0; c < nchunks; ++c) s += part[((int64_t)c * nrhs + q) * M + row];
+        y[q * ldy + row] = s;
+    }
+}
+
 // z[:,q] = (g[:,q] - SA^T w[:,q]) / nu2 ; one warp per column of SA
 __global__ void woodbury_finish_kernel(const double* __restrict__ SA, int64_t m, int64_t d,
                                        const double* __restrict__ g, const double* __restrict__ w, double nu2,
@@ -125,6 +168,16 @@ void decrement_dots(const double* g, const double* gt, int64_t d, int nrhs, doub
 void gemv_n(const double* A, int64_t M, int64_t N, int64_t lda, const double* x, int nrhs, int64_t ldx, double* y,
             int64_t ldy, cudaStream_t st) {
     LAUNCH(gemv_n_kernel, blocks_for(M, 128), 128, 0, st, A, M, N, lda, x, nrhs, ldx, y, ldy);
+}
+
+size_t gemv_tiled_work_doubles(int64_t M, int64_t N) { return (size_t)ceil_div(N, GV_COLS) * 2 * (size_t)M; }
+
+void gemv_tiled(const double* A, int64_t M, int64_t N, int64_t lda, const double* x, int nrhs, int64_t ldx, double* y,
+                int64_t ldy, double* work, cudaStream_t st) {
+    dim3 grid((unsigned)ceil_div(M, GV_ROWS), (unsigned)ceil_div(N, GV_COLS));
+    LAUNCH(gemv_partial_kernel, grid, 256, 0, st, A, M, N, lda, x, nrhs, ldx, work);
+    LAUNCH(gemv_reduce_kernel, blocks_for((int64_t)nrhs * M, 256, 1024), 256, 0, st, work, M, nrhs, (int)grid.y, y,
+           ldy);
 }
 
 void woodbury_finish(const double* SA, int64_t m, int64_t d, const double* g, const double* w, double nu2, int nrhs,
