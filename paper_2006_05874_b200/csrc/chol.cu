@@ -41,8 +41,14 @@ __global__ void __launch_bounds__(256) potrf_diag_kernel(double* __restrict__ H,
         if (g == 0 && i > j && i < nb) a[i][j] = a[i][j] / ljj;
         __syncthreads();
         if (i > j && i < nb) {
+            // independent updates of row i (columns g, g+4, ...): unrolled so the
+            // shared loads overlap instead of forming a chain
             const double lij = a[i][j];
-            for (int jj = j + 1 + g; jj <= i; jj += 4) a[i][jj] -= lij * a[jj][j];
+#pragma unroll
+            for (int q = 0; q < NB / 4; ++q) {
+                const int jj = g + 4 * q;
+                if (jj > j && jj <= i) a[i][jj] -= lij * a[jj][j];
+            }
         }
         __syncthreads();
     }
@@ -56,10 +62,12 @@ constexpr int TRSM_WARPS = 8;
 __global__ void __launch_bounds__(32 * TRSM_WARPS) trsm_panel_kernel(double* __restrict__ H, int64_t n, int64_t k,
                                                                      int nb) {
     __shared__ double l[NB][NB + 1];
+    __shared__ double rdiag[NB];
     for (int e = threadIdx.x; e < NB * NB; e += blockDim.x) {
         const int ii = e % NB, jj = e / NB;
         l[ii][jj] = (ii < nb && jj < nb && ii >= jj) ? H[(k + ii) + (k + jj) * n] : 0.0;
     }
+    if (threadIdx.x < nb) rdiag[threadIdx.x] = 1.0 / H[(k + threadIdx.x) * (n + 1)];
     __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t row = k + nb + (int64_t)blockIdx.x * TRSM_WARPS + warp;
@@ -70,7 +78,7 @@ __global__ void __launch_bounds__(32 * TRSM_WARPS) trsm_panel_kernel(double* __r
         // finish x[c] on its owner lane, broadcast, update the columns after it
         const bool hi = c >= 32;
         double xc = 0.0;
-        if (lane == (c & 31)) xc = (hi ? x1 : x0) / l[c][c];
+        if (lane == (c & 31)) xc = (hi ? x1 : x0) * rdiag[c];
         xc = __shfl_sync(0xffffffffu, xc, c & 31);
         if (lane == (c & 31)) {
             if (hi) x1 = xc;

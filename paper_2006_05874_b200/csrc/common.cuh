@@ -76,7 +76,7 @@ void srht_build_entries(const SrhtPlan& p, const int64_t* rows, std::vector<int2
 // d_ctl != nullptr selects the fused single-launch path (when the high bits
 // fit one pass): T is then a ring of srht_fused_scratch_bytes() and d_ctl a
 // control block of *ctl_bytes.
-size_t srht_fused_scratch_bytes(const SrhtPlan& p, size_t* ctl_bytes);
+size_t srht_fused_scratch_bytes(const SrhtPlan& p, size_t* ctl_bytes, int num_sms = 148);
 // d_mask (4 words, from srht_build_mask): phase 1 stores only the low-index
 // groups the single emitting pass reads.
 void srht_run_device(const SrhtPlan& p, const double* d_A, const uint32_t* d_signbits, const int2* d_entries,

@@ -8,6 +8,7 @@
 // per stage (expect_tx), so the LSU/MIO queue only carries the sweeps' shared
 // loads. Stages are released by the CTA barrier that ends each panel.
 #include "common.cuh"
+#include "tma.cuh"
 
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -199,7 +200,9 @@ grad_tma_kernel(const __grid_constant__ CUtensorMap tmap, int64_t d, int64_t npa
         }
 }
 
-PFN_cuTensorMapEncodeTiled encode_fn() {
+}  // namespace
+
+PFN_cuTensorMapEncodeTiled tma_encode_fn() {
     static PFN_cuTensorMapEncodeTiled fn = [] {
         void* p = nullptr;
         cudaDriverEntryPointQueryResult q{};
@@ -209,7 +212,6 @@ PFN_cuTensorMapEncodeTiled encode_fn() {
     }();
     return fn;
 }
-}  // namespace
 
 size_t grad_tma_smem(int64_t d, int R, int nrhs, int ns) {
     const int64_t nbox = (d + BOXC - 1) / BOXC;
@@ -230,7 +232,7 @@ bool grad_tma_make_map(const double* A, int64_t lda, int64_t d, int R, void* map
                                   : R == 4 ? CU_TENSOR_MAP_SWIZZLE_32B
                                            : CU_TENSOR_MAP_SWIZZLE_NONE;
     if (sw == CU_TENSOR_MAP_SWIZZLE_NONE) return false;
-    const CUresult r = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(A), dims, strides, box,
+    const CUresult r = tma_encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(A), dims, strides, box,
                                    estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;

@@ -284,7 +284,7 @@ unsigned long long* srht_prepare_scratch(ihs_gpu_problem* P, const SrhtPlan& pla
         return nullptr;
     }
     size_t ctl_bytes = 0;
-    P->T.ensure(srht_fused_scratch_bytes(plan, &ctl_bytes));
+    P->T.ensure(srht_fused_scratch_bytes(plan, &ctl_bytes, P->num_sms));
     P->fused_ctl.ensure(ctl_bytes);
     return P->fused_ctl.as<unsigned long long>();
 }

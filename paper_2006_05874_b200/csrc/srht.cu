@@ -23,8 +23,10 @@
 //     and the two scalings (1/sqrt(n_pad) at :47-48, sqrt(n_pad/m) at
 //     :95-97) are separate rounded multiplies of host-computed constants.
 #include "common.cuh"
+#include "tma.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <vector>
 
@@ -162,50 +164,271 @@ __device__ __forceinline__ void p1_chunk(double* __restrict__ xs, const double* 
     }
 }
 
-// 8-byte async copy global -> shared; src_valid == false zero-fills (+0.0).
-__device__ __forceinline__ void cp_async8_zfill(double* dst, const double* src, bool src_valid) {
+// 8-byte async copy global -> shared with an L2 evict-first policy (A is
+// read exactly once); src_valid == false zero-fills (+0.0).
+__device__ __forceinline__ void cp_async8_zfill(double* dst, const double* src, bool src_valid, uint64_t pol) {
     const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(src), "r"(src_valid ? 8 : 0)
+    asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2, %3;\n" ::"r"(s), "l"(src),
+                 "r"(src_valid ? 8 : 0), "l"(pol)
                  : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol));
+    return pol;
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
-// Persistent warp-per-chunk phase 1: bits 0..9 of every 1024-row chunk of
-// every column -> T. Each warp streams its chunks through a two-slot ring of
-// padded shared buffers filled by cp.async (the next chunk is in flight while
-// the current one is transformed), so HBM sees ~kP1Warps x 8 KiB of reads in
-// flight per SM at all times. The sign is applied on the first transposed
-// read (lane holds rows 32*lane .. 32*lane+31: one sign word per lane).
+// Phase-1 chunk pipeline of one warp. A chunk (1024 rows of one column) is
+// staged by cp.async into a padded shared buffer (lane = row bits 0-4), then
+// transformed: the sign is applied on the first transposed read (lane holds
+// rows 32*lane .. 32*lane+31: one sign word per lane), bits 0-4 and 5-9 run
+// in registers around one in-place shared-memory transpose.
 constexpr int kP1Buf = 1024 + 32;
-constexpr int kP1Stages = 2;
+__device__ __forceinline__ void cp_async8(double* dst, const double* src, uint64_t pol) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, 8, %2;\n" ::"r"(s), "l"(src), "l"(pol)
+                 : "memory");
+}
+__device__ __forceinline__ void p1_issue(double* buf, const double* col, int64_t n, int64_t r0, uint64_t pol) {
+    const int lane = threadIdx.x & 31;
+    if (r0 + 1024 <= n) {  // full chunk: constant offsets, no predicates
+        const double* src = col + r0 + lane;
+        double* dst = buf + lane;
+#pragma unroll
+        for (int c = 0; c < 32; ++c) cp_async8(dst + 33 * c, src + 32 * c, pol);
+        return;
+    }
+#pragma unroll
+    for (int c = 0; c < 32; ++c) {
+        const int64_t r = r0 + (c << 5) + lane;
+        cp_async8_zfill(buf + pad32((c << 5) | lane), r < n ? col + r : col, r < n, pol);
+    }
+}
+
+// Per-lane store predicate of the masked phase-1 store: bit c set when
+// element (c << 5) + lane belongs to a low-index group (of 2^logw indices)
+// that a sampled row reads in the emitting pass; all ones when unmasked.
+__device__ __forceinline__ uint32_t p1_store_bits(const uint32_t* __restrict__ mask, int logw) {
+    if (mask == nullptr) return 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    uint32_t bits = 0u;
+    for (int c = 0; c < 32; ++c) {
+        const int g = ((c << 5) + lane) >> logw;
+        bits |= ((__ldg(mask + (g >> 5)) >> (g & 31)) & 1u) << c;
+    }
+    return bits;
+}
+
+// x * (+-1.0) done as a sign-bit flip (exact: IEEE multiplication by -1 only
+// flips the sign, so this equals the reference's rounded product bit for bit).
+__device__ __forceinline__ double flip_sign(double a, uint32_t flip_bit31) {
+    return __hiloint2double(__double2hiint(a) ^ (int)flip_bit31, __double2loint(a));
+}
+
+// Transform the chunk staged in buf and store the kept elements to dst.
+__device__ __forceinline__ void p1_transform_store(double* buf, const uint32_t* __restrict__ signbits, int64_t n,
+                                                   int64_t r0, double* __restrict__ dst, uint32_t store_bits) {
+    const int lane = threadIdx.x & 31;
+    const int64_t rl = r0 + (lane << 5);
+    // flip bit c = row rl + c gets -1 (sign bit 0); padded rows stay +0.0
+    uint32_t flip = 0u;
+    if (rl < n) {
+        flip = ~__ldg(signbits + (rl >> 5));
+        if (rl + 32 > n) flip &= (1u << (n - rl)) - 1u;
+    }
+    double v[32];
+    const double* row = buf + 33 * lane;  // pad32((lane << 5) | c) = 33 * lane + c
+#pragma unroll
+    for (int c = 0; c < 32; ++c) v[c] = flip_sign(row[c], (flip << (31 - c)) & 0x80000000u);
+#pragma unroll
+    for (int s = 0; s < 5; ++s)
+#pragma unroll
+        for (int c = 0; c < 32; ++c)
+            if (!(c & (1 << s))) bfly(v[c], v[c | (1 << s)]);
+#pragma unroll
+    for (int c = 0; c < 32; ++c) buf[33 * lane + c] = v[c];
+    __syncwarp();
+#pragma unroll
+    for (int c = 0; c < 32; ++c) v[c] = buf[33 * c + lane];  // pad32((c << 5) | lane)
+#pragma unroll
+    for (int s = 0; s < 5; ++s)
+#pragma unroll
+        for (int c = 0; c < 32; ++c)
+            if (!(c & (1 << s))) bfly(v[c], v[c | (1 << s)]);
+    double* out = dst + lane;
+#pragma unroll
+    for (int c = 0; c < 32; ++c)
+        if ((store_bits >> c) & 1u) out[c << 5] = v[c];
+    __syncwarp();  // the buffer is refilled by the next issue
+}
+
+// ---- phase 1 fed by TMA (default)
+// A full chunk (1024 rows of one column, 8 KiB) arrives by two 3-level TMA
+// boxes of 32 x 128 B rows under SWIZZLE_128B: the even 128-byte rows of the
+// chunk (rows 32l .. 32l+15 of lane l's block) to shared rows 0..31 and the
+// odd ones to rows 32..63. Element e of the chunk (global row rg = e >> 4,
+// k = e & 15) sits at shared row r' = 32 (rg & 1) + (rg >> 1), 16-byte unit
+// (k >> 1) ^ (r' & 7), half k & 1. Both transposed reads are then free of
+// bank conflicts: lane l owns shared rows l and 32 + l (its 32 elements, as
+// 16-byte pairs), and the second read (lane = element bits 0-4) hits 16
+// distinct 8-byte slots of one 128-byte row per half-warp. Only one elected
+// lane issues the copies; the LSU/MIO queue carries just the shared accesses.
+constexpr int kChunkDoubles = 1024;
+__device__ __forceinline__ int p1_swz(int e) {
+    const int rg = e >> 4, k = e & 15;
+    const int rp = ((rg & 1) << 5) | (rg >> 1);
+    return (rp << 4) | (((k >> 1) ^ (rp & 7)) << 1) | (k & 1);
+}
+
+struct ChunkMaps {
+    CUtensorMap even, odd;  // (16 doubles, 32 rows of stride 256 B, chunk, column)
+};
+
+// rows >= n read as +0.0 (partial / padded chunks: synchronous, swizzled)
+__device__ __forceinline__ void p1_sync_load(double* buf, const double* __restrict__ col, int64_t n, int64_t r0) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll 8
+    for (int c = 0; c < 32; ++c) {
+        const int e = (c << 5) | lane;
+        const int64_t r = r0 + e;
+        buf[p1_swz(e)] = r < n ? col[r] : 0.0;
+    }
+    __syncwarp();
+}
+
+__device__ __forceinline__ void p1_tma_issue(double* buf, const ChunkMaps* maps, int q, int j, uint64_t* bar) {
+    tma::fence_proxy_async();
+    tma::mbar_expect_tx(bar, kChunkDoubles * sizeof(double));
+    tma::load_4d(buf, &maps->even, 0, 0, q, j, bar);
+    tma::load_4d(buf + kChunkDoubles / 2, &maps->odd, 0, 0, q, j, bar);
+}
+
+__device__ __forceinline__ void p1_transform_store_swz(double* buf, const uint32_t* __restrict__ signbits, int64_t n,
+                                                       int64_t r0, double* __restrict__ dst, uint32_t store_bits) {
+    const int lane = threadIdx.x & 31;
+    const int64_t rl = r0 + (lane << 5);
+    uint32_t flip = 0u;
+    if (rl < n) {
+        flip = ~__ldg(signbits + (rl >> 5));
+        if (rl + 32 > n) flip &= (1u << (n - rl)) - 1u;
+    }
+    double v[32];
+    double* row0 = buf + (lane << 4);         // shared row lane: elements 32 lane + 0..15
+    double* row1 = buf + ((32 + lane) << 4);  // shared row 32 + lane: elements 32 lane + 16..31
+    const int x = lane & 7;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+        const double2 a = *reinterpret_cast<const double2*>(row0 + ((u ^ x) << 1));
+        const double2 b = *reinterpret_cast<const double2*>(row1 + ((u ^ x) << 1));
+        v[2 * u] = a.x;
+        v[2 * u + 1] = a.y;
+        v[16 + 2 * u] = b.x;
+        v[17 + 2 * u] = b.y;
+    }
+#pragma unroll
+    for (int c = 0; c < 32; ++c) v[c] = flip_sign(v[c], (flip << (31 - c)) & 0x80000000u);
+#pragma unroll
+    for (int s = 0; s < 5; ++s)
+#pragma unroll
+        for (int c = 0; c < 32; ++c)
+            if (!(c & (1 << s))) bfly(v[c], v[c | (1 << s)]);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+        *reinterpret_cast<double2*>(row0 + ((u ^ x) << 1)) = make_double2(v[2 * u], v[2 * u + 1]);
+        *reinterpret_cast<double2*>(row1 + ((u ^ x) << 1)) = make_double2(v[16 + 2 * u], v[17 + 2 * u]);
+    }
+    __syncwarp();
+    // lane = element bits 0-4: element 32c + lane at shared row 32 (lane >> 4) + c
+    const double* col = buf + ((lane >> 4) << 9) + (lane & 1);
+    const int lu = (lane & 15) >> 1;
+#pragma unroll
+    for (int c = 0; c < 32; ++c) v[c] = col[(c << 4) + ((lu ^ (c & 7)) << 1)];
+#pragma unroll
+    for (int s = 0; s < 5; ++s)
+#pragma unroll
+        for (int c = 0; c < 32; ++c)
+            if (!(c & (1 << s))) bfly(v[c], v[c | (1 << s)]);
+    double* out = dst + lane;
+#pragma unroll
+    for (int c = 0; c < 32; ++c)
+        if ((store_bits >> c) & 1u) out[c << 5] = v[c];
+    __syncwarp();  // the buffer is refilled by the next issue
+}
+
+__device__ __forceinline__ double* align1024(void* p) {
+    const uint32_t a = tma::smem_u32(p);
+    return reinterpret_cast<double*>(static_cast<unsigned char*>(p) + ((1024u - (a & 1023u)) & 1023u));
+}
+
+// Persistent phase 1 over TMA-fed two-slot rings (one per warp).
+constexpr int kP1TWarps = 12;
+constexpr size_t kP1TSmem = (size_t)kP1TWarps * 2 * kChunkDoubles * sizeof(double) + kP1TWarps * 2 * 8 + 1024;
+__global__ void __launch_bounds__(32 * kP1TWarps, 1)
+srht_phase1_tma_kernel(const __grid_constant__ ChunkMaps maps, const double* __restrict__ A, int64_t n, int64_t lda,
+                       const uint32_t* __restrict__ signbits, double* __restrict__ T, int64_t n_pad, int lcpc,
+                       int64_t nfull, int64_t total_chunks, const uint32_t* __restrict__ mask, int logw) {
+    extern __shared__ unsigned char p1t_raw[];
+    double* base = align1024(p1t_raw);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double* ring = base + warp * (2 * kChunkDoubles);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(base + kP1TWarps * 2 * kChunkDoubles) + 2 * warp;
+    if (lane == 0) {
+        tma::mbar_init(&bars[0], 1);
+        tma::mbar_init(&bars[1], 1);
+        tma::fence_mbar_init();
+    }
+    __syncwarp();
+    const int64_t cmask = (int64_t{1} << lcpc) - 1;
+    const int64_t nw = (int64_t)gridDim.x * kP1TWarps;
+    const uint32_t store_bits = p1_store_bits(mask, logw);
+    auto issue = [&](int64_t chunk, int slot) {
+        if (lane == 0 && chunk < total_chunks && (chunk & cmask) < nfull)
+            p1_tma_issue(ring + slot * kChunkDoubles, &maps, (int)(chunk & cmask), (int)(chunk >> lcpc), &bars[slot]);
+    };
+    uint32_t parity = 0u;
+    int slot = 0;
+    int64_t chunk = (int64_t)blockIdx.x * kP1TWarps + warp;
+    issue(chunk, 0);
+    for (; chunk < total_chunks; chunk += nw) {
+        issue(chunk + nw, slot ^ 1);
+        const int64_t q = chunk & cmask, j = chunk >> lcpc;
+        const int64_t r0 = q << kChunkL;
+        double* buf = ring + slot * kChunkDoubles;
+        if (q < nfull) {
+            tma::mbar_wait(&bars[slot], (parity >> slot) & 1u);
+            parity ^= 1u << slot;
+        } else {
+            p1_sync_load(buf, A + j * lda, n, r0);
+        }
+        p1_transform_store_swz(buf, signbits, n, r0, T + j * n_pad + r0, store_bits);
+        slot ^= 1;
+    }
+}
+
+// Persistent warp-per-chunk phase 1: bits 0..9 of every 1024-row chunk of
+// every column -> T. Each warp streams its chunks through a two-slot ring
+// (the next chunk is in flight while the current one is transformed), so HBM
+// sees ~kP1AWarps x 8 KiB of reads in flight per SM at all times.
 constexpr int kP1AWarps = 12;
 __global__ void __launch_bounds__(32 * kP1AWarps, 1)
 srht_phase1_kernel(const double* __restrict__ A, int64_t n, int64_t lda, const uint32_t* __restrict__ signbits,
-                   double* __restrict__ T, int64_t n_pad, int64_t chunks_per_col, int64_t total_chunks,
+                   double* __restrict__ T, int64_t n_pad, int lcpc, int64_t total_chunks,
                    const uint32_t* __restrict__ mask, int logw) {
-    extern __shared__ double p1_smem[];  // kP1AWarps x kP1Stages x kP1Buf doubles
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    double* ring = p1_smem + warp * (kP1Stages * kP1Buf);
+    extern __shared__ double p1_smem[];  // kP1AWarps x 2 x kP1Buf doubles
+    const int64_t cmask = (int64_t{1} << lcpc) - 1;  // chunks per column = 2^lcpc
+    const int warp = threadIdx.x >> 5;
+    double* ring = p1_smem + warp * (2 * kP1Buf);
+    const uint64_t pol = policy_evict_first();
     const int64_t nw = (int64_t)gridDim.x * kP1AWarps;
     auto issue = [&](int64_t chunk, int slot) {
-        if (chunk < total_chunks) {
-            const int64_t j = chunk / chunks_per_col;
-            const int64_t r0 = (chunk % chunks_per_col) << kChunkL;
-            const double* col = A + j * lda;
-            double* buf = ring + slot * kP1Buf;
-#pragma unroll
-            for (int c = 0; c < 32; ++c) {
-                const int64_t r = r0 + (c << 5) + lane;
-                cp_async8_zfill(buf + pad32((c << 5) | lane), r < n ? col + r : col, r < n);
-            }
-        }
+        if (chunk < total_chunks)
+            p1_issue(ring + slot * kP1Buf, A + (chunk >> lcpc) * lda, n, (chunk & cmask) << kChunkL, pol);
         cp_async_commit();
     };
-    uint32_t mw[4] = {0u, 0u, 0u, 0u};
-    if (mask != nullptr)
-        for (int k = 0; k < 4; ++k) mw[k] = __ldg(mask + k);
+    const uint32_t store_bits = p1_store_bits(mask, logw);
     int slot = 0;
     int64_t chunk = (int64_t)blockIdx.x * kP1AWarps + warp;
     issue(chunk, 0);
@@ -213,47 +436,9 @@ srht_phase1_kernel(const double* __restrict__ A, int64_t n, int64_t lda, const u
         issue(chunk + nw, slot ^ 1);
         cp_async_wait1();
         __syncwarp();
-        const int64_t j = chunk / chunks_per_col;
-        const int64_t r0 = (chunk % chunks_per_col) << kChunkL;
-        double* buf = ring + slot * kP1Buf;
-        const int64_t rl = r0 + (lane << 5);  // this lane's 32 rows (register c = bits 0-4)
-        const uint32_t sw = rl < n ? __ldg(signbits + (rl >> 5)) : 0u;
-        double v[32];
-#pragma unroll
-        for (int c = 0; c < 32; ++c) {
-            const double a = buf[pad32((lane << 5) | c)];
-            v[c] = (rl + c < n) ? __dmul_rn(((sw >> c) & 1u) ? 1.0 : -1.0, a) : 0.0;
-        }
-#pragma unroll
-        for (int s = 0; s < 5; ++s)
-#pragma unroll
-            for (int c = 0; c < 32; ++c)
-                if (!(c & (1 << s))) bfly(v[c], v[c | (1 << s)]);
-#pragma unroll
-        for (int c = 0; c < 32; ++c) buf[pad32((lane << 5) | c)] = v[c];
-        __syncwarp();
-        // register c = index bits 5-9: stages 5..9
-#pragma unroll
-        for (int c = 0; c < 32; ++c) v[c] = buf[pad32((c << 5) | lane)];
-#pragma unroll
-        for (int s = 0; s < 5; ++s)
-#pragma unroll
-            for (int c = 0; c < 32; ++c)
-                if (!(c & (1 << s))) bfly(v[c], v[c | (1 << s)]);
-        double* dst = T + j * n_pad + r0;
-        if (mask == nullptr) {
-#pragma unroll
-            for (int c = 0; c < 32; ++c) dst[(c << 5) + lane] = v[c];
-        } else {
-            // store only the low-index groups a sampled row will read in phase 2
-#pragma unroll
-            for (int c = 0; c < 32; ++c) {
-                const int e = (c << 5) + lane;
-                const int g = e >> logw;
-                if ((mw[g >> 5] >> (g & 31)) & 1u) dst[e] = v[c];
-            }
-        }
-        __syncwarp();  // the slot is refilled by the next iteration's issue
+        const int64_t j = chunk >> lcpc;
+        const int64_t r0 = (chunk & cmask) << kChunkL;
+        p1_transform_store(ring + slot * kP1Buf, signbits, n, r0, T + j * n_pad + r0, store_bits);
         slot ^= 1;
     }
     cp_async_wait0();
@@ -278,15 +463,25 @@ struct P2Geom {
 // Tcol[(b << lo) + w]; emit -> the tile's sampled rows go to SA, else the
 // tile is written back in place. CG: T loads bypass L1 (written by other
 // CTAs of the same fused launch).
-template <int HB, bool CG>
+struct CtaBar {
+    __device__ __forceinline__ void operator()() const { __syncthreads(); }
+};
+// barrier over the kP2Threads threads of a warp group (named barrier `id`)
+struct GroupBar {
+    int id;
+    __device__ __forceinline__ void operator()() const {
+        asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(kP2Threads) : "memory");
+    }
+};
+
+template <int HB, bool CG, class Bar = CtaBar>
 __device__ __forceinline__ void p2_tile(double* __restrict__ xs, double* __restrict__ Tcol, int lo, bool emit,
                                         int4 tile, const int2* __restrict__ entries, int64_t j, double s1, double s2,
-                                        double* __restrict__ SA, int64_t m) {
+                                        double* __restrict__ SA, int64_t m, int t = threadIdx.x, Bar bar = Bar()) {
     constexpr int RB1 = P2Geom<HB>::RB1;
     constexpr int RB2 = HB - RB1;
     constexpr int E = P2Geom<HB>::E;
     constexpr int W = P2Geom<HB>::W;
-    const int t = threadIdx.x;
     const int w = t % W;
     const int g = t / W;  // 2^RB2 groups
     double v[E];
@@ -305,7 +500,7 @@ __device__ __forceinline__ void p2_tile(double* __restrict__ xs, double* __restr
         // exchange: element (b, w) at xs[pad32(b*W + w)]
 #pragma unroll
         for (int c = 0; c < E; ++c) xs[pad32(((g << RB1) | c) * W + w)] = v[c];
-        __syncthreads();
+        bar();
         // round 2: thread (w, g2) with g2 in [0, 2^RB2), register (grp, c2):
         // pass bits [0, RB1) = g2 + grp * 2^RB2, pass bits [RB1, HB) = c2
         constexpr int G2 = 1 << RB2;
@@ -335,7 +530,7 @@ __device__ __forceinline__ void p2_tile(double* __restrict__ xs, double* __restr
                 }
             return;
         }
-        __syncthreads();
+        bar();
 #pragma unroll
         for (int grp = 0; grp < GRPS; ++grp)
 #pragma unroll
@@ -352,7 +547,7 @@ __device__ __forceinline__ void p2_tile(double* __restrict__ xs, double* __restr
 #pragma unroll
         for (int c = 0; c < E; ++c) xs[pad32(((g << RB1) | c) * W + w)] = v[c];
     }
-    __syncthreads();
+    bar();
     const int64_t bmask = (int64_t{1} << HB) - 1;
     for (int q = tile.y + t; q < tile.z; q += kP2Threads) {
         const int2 rk = entries[q];
@@ -385,100 +580,110 @@ srht_phase2_kernel(double* __restrict__ T, int64_t n_pad, int lo, const int4* __
     p2_tile<HB, false>(xs, T + j * n_pad + base, lo, emit != 0, tile, entries, j, s1, s2, SA, m);
 }
 
-// ------------------------------------------------------------ fused (one pass of high bits)
-// Persistent work queue over column groups of G columns: items in the order
-// P1(0), P1(1), P2(0), P1(2), P2(1), ..., P2(ng-1), handed out by an atomic
-// counter to running CTAs only. P1(g) = phase-1 chunks of group g (8 per
-// item, one per warp) into ring slot g % NSLOT of T; P2(g) = the emitting
-// pass over the active tiles of group g. A P2(g) item waits until all P1(g)
-// items are done; a P1(g) item waits until P2(g - NSLOT) released its slot.
-// Every awaited item precedes the waiter in the hand-out order and is held
-// by a running CTA, so the queue cannot deadlock. The ring (NSLOT x G
-// columns of T) is sized to stay in L2, so T never round-trips through HBM.
-struct FusedCtl {
-    unsigned long long next;  // hand-out counter; followed by done1[ng], done2[ng] (int)
-};
-
-__device__ __forceinline__ void wait_count(const int* ctr, int target) {
-    if (threadIdx.x == 0) {
-        int v;
-        while (true) {
-            asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
-            if (v >= target) break;
-            __nanosleep(128);
-        }
-    }
-    __syncthreads();
+// ------------------------------------------------------------ streamed (one pass of high bits)
+// Persistent single-launch SRHT, warp-specialised: phase 1 and the emitting
+// pass run concurrently so T lives in an L2-resident ring of nslot slots x G
+// columns instead of making an HBM round trip. One CTA per SM:
+//   * warps 0-7 (phase 1) stream the 1024-row chunks in global order (warp w
+//     of CTA b takes chunks (k*grid + b)*8 + w), each keeping its next chunk
+//     in flight by cp.async; a warp adds its finished chunks to done1[group]
+//     when it moves to the next group, and before its first write into group
+//     g's slot waits until done2[g - nslot] shows the slot consumed;
+//   * warps 8-15 (emitting group, named barrier 1) take their share of each
+//     group's active tiles once done1[group] is complete and add them to
+//     done2[group].
+// Phase-1 warps wait only for emits of earlier groups, whose chunks precede
+// theirs in every warp's order, and emitting warps never block phase-1 warps
+// of their own CTA, so the pipeline cannot deadlock for any G or nslot.
+__device__ __forceinline__ int ld_acquire(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void spin_until(const int* ctr, int target) {
+    while (ld_acquire(ctr) < target) __nanosleep(100);
 }
 
-__device__ __forceinline__ void signal_done(int* ctr) {
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) atomicAdd(ctr, 1);
-}
+constexpr int kXsDoubles = kTileElems + kTileElems / 32;  // emitting-pass exchange buffer
 
 template <int HB>
-__global__ void __launch_bounds__(kP2Threads)
-srht_fused_kernel(const double* __restrict__ A, int64_t n, int64_t lda, const uint32_t* __restrict__ signbits,
-                  double* __restrict__ T, int64_t n_pad, int64_t d, int G, int nslot, int ng, int n1, int n2,
-                  int64_t cpc, const int4* __restrict__ tiles, int n_tiles, const int2* __restrict__ entries, int lo,
-                  double s1, double s2, double* __restrict__ SA, int64_t m, unsigned long long* __restrict__ ctl) {
-    static_assert(kP2Threads == 32 * kP1Warps, "one block shape for both item kinds");
+__global__ void __launch_bounds__(2 * kP2Threads, 1)
+srht_stream_kernel(const double* __restrict__ A, int64_t n, int64_t lda, const uint32_t* __restrict__ signbits,
+                   double* __restrict__ T, int64_t n_pad, int64_t d, int lcpc, int G, int nslot, int ng,
+                   const int4* __restrict__ tiles, int n_tiles, const int2* __restrict__ entries, int lo, double s1,
+                   double s2, double* __restrict__ SA, int64_t m, int* __restrict__ ctl,
+                   const uint32_t* __restrict__ mask, int logw) {
+    static_assert(kP2Threads == 32 * kP1Warps, "equal warp groups");
     extern __shared__ double smem[];
-    __shared__ long long item_s;
-    int* done1 = reinterpret_cast<int*>(ctl + 1);
-    int* done2 = done1 + ng;
-    const long long per = (long long)n1 + n2;
-    const long long total = (long long)ng * per;
-    const int warp = threadIdx.x >> 5;
-    for (;;) {
-        if (threadIdx.x == 0) item_s = (long long)atomicAdd(ctl, 1ULL);
-        __syncthreads();
-        const long long item = item_s;
-        __syncthreads();
-        if (item >= total) break;
-        // decode the hand-out order P1(0), [P1(s), P2(s-1)] for s = 1..ng-1, P2(ng-1)
-        bool p1;
-        int g;
-        long long w;
-        if (item < n1) {
-            p1 = true; g = 0; w = item;
-        } else {
-            const long long i2 = item - n1;
-            const long long s = 1 + i2 / per;
-            if (s < ng) {
-                const long long within = i2 % per;
-                p1 = within < n1;
-                g = p1 ? (int)s : (int)s - 1;
-                w = p1 ? within : within - n1;
-            } else {
-                p1 = false; g = ng - 1; w = i2 - (long long)(ng - 1) * per;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    int* done1 = ctl;
+    int* done2 = ctl + ng;
+    const int64_t cpc = int64_t{1} << lcpc, cmask = cpc - 1;
+    auto group_cols = [&](int g) { return (int)imin64(G, d - (int64_t)g * G); };
+    if (warp >= kP1Warps) {
+        // ---------------- emitting warp group
+        const int t = threadIdx.x - kP2Threads;
+        const GroupBar bar{1};
+        for (int g = 0; g < ng; ++g) {
+            const int gc = group_cols(g);
+            const int items = gc * n_tiles;
+            if ((int)blockIdx.x >= items) continue;
+            if (t == 0) spin_until(done1 + g, (int)(gc * cpc));
+            bar();
+            int mine = 0;
+            for (int i = blockIdx.x; i < items; i += gridDim.x) {
+                const int jj = i / n_tiles;
+                const int4 tile = tiles[i % n_tiles];
+                p2_tile<HB, true, GroupBar>(smem, T + ((int64_t)(g % nslot) * G + jj) * n_pad + tile.x, lo, true,
+                                            tile, entries, (int64_t)g * G + jj, s1, s2, SA, m, t, bar);
+                bar();  // the exchange buffer is rewritten by the next tile
+                ++mine;
             }
+            if (t == 0) atomicAdd(done2 + g, mine);
         }
-        const int slot = g % nslot;
-        if (p1) {
-            if (g >= nslot) wait_count(done2 + (g - nslot), n2);
-            const int64_t c = w * kP1Warps + warp;  // chunk within the group
-            const int64_t jj = c / cpc;
-            const int64_t j = (int64_t)g * G + jj;
-            if (jj < G && j < d) {
-                const int64_t r0 = (c % cpc) << kChunkL;
-                p1_chunk<true>(smem + warp * (1024 + 32), A + j * lda, n, signbits, r0,
-                               T + ((int64_t)slot * G + jj) * n_pad + r0);
-            }
-            signal_done(done1 + g);
-        } else {
-            wait_count(done1 + g, n1);
-            const int64_t jj = w / n_tiles;
-            const int64_t j = (int64_t)g * G + jj;
-            if (j < d) {
-                const int4 tile = tiles[w % n_tiles];
-                p2_tile<HB, true>(smem, T + ((int64_t)slot * G + jj) * n_pad + tile.x, lo, true, tile, entries, j, s1,
-                                  s2, SA, m);
-            }
-            signal_done(done2 + g);
-        }
+        return;
     }
+    // ---------------- phase-1 warps
+    double* ring = smem + kXsDoubles + warp * (2 * kP1Buf);
+    const int64_t total = d * cpc;
+    const int64_t SC = (int64_t)gridDim.x * kP1Warps;  // chunks per round of all phase-1 warps
+    const uint64_t pol = policy_evict_first();
+    const uint32_t store_bits = p1_store_bits(mask, logw);
+    auto issue = [&](int64_t chunk, int slot) {
+        if (chunk < total) p1_issue(ring + slot * kP1Buf, A + (chunk >> lcpc) * lda, n, (chunk & cmask) << kChunkL, pol);
+        cp_async_commit();
+    };
+    auto flush = [&](int g, int cnt) {
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) atomicAdd(done1 + g, cnt);
+    };
+    int slot = 0, cur_g = -1, cnt = 0;
+    int64_t chunk = (int64_t)blockIdx.x * kP1Warps + warp;
+    issue(chunk, 0);
+    for (; chunk < total; chunk += SC) {
+        issue(chunk + SC, slot ^ 1);
+        const int j = (int)(chunk >> lcpc);
+        const int g = j / G;
+        if (g != cur_g) {
+            if (cnt) flush(cur_g, cnt);
+            cnt = 0;
+            cur_g = g;
+            if (g >= nslot) {
+                if (lane == 0) spin_until(done2 + g - nslot, group_cols(g - nslot) * n_tiles);
+                __syncwarp();
+            }
+        }
+        cp_async_wait1();
+        __syncwarp();
+        const int64_t r0 = (chunk & cmask) << kChunkL;
+        p1_transform_store(ring + slot * kP1Buf, signbits, n, r0,
+                           T + ((int64_t)(g % nslot) * G + (j - g * G)) * n_pad + r0, store_bits);
+        ++cnt;
+        slot ^= 1;
+    }
+    if (cnt) flush(cur_g, cnt);
+    cp_async_wait0();
 }
 
 // Row-sharded SRHT combine (H_{n_pad} = H_P (x) H_{n_pad/P}, shard index =
@@ -549,44 +754,85 @@ void launch_pass(const SrhtPlan& p, double* T, int lo, const int4* tiles, int n_
            p.scale1, p.scale2, SA, p.m);
 }
 
-constexpr size_t kP1Smem = (size_t)kP1Warps * (1024 + 32) * sizeof(double);
-constexpr size_t kP2Smem = (size_t)(kTileElems + kTileElems / 32) * sizeof(double) + 64;
-constexpr size_t kFusedSmem = kP1Smem > kP2Smem ? kP1Smem : kP2Smem;  // covers both item kinds
+constexpr size_t kStreamSmem = (size_t)(kXsDoubles + kP1Warps * 2 * kP1Buf) * sizeof(double);
+// Tensor maps of the full 1024-row chunks of A (even / odd 128-byte rows of
+// each chunk, see p1_tma_issue), cached per (A, lda, nfull, d); false when
+// TMA is unavailable or disabled (IHS_SRHT_NO_TMA=1).
+bool srht_chunk_maps(const double* A, int64_t lda, int64_t nfull, int64_t d, ChunkMaps* out) {
+    static const bool disabled = [] {
+        const char* e = std::getenv("IHS_SRHT_NO_TMA");
+        return e && e[0] == '1';
+    }();
+    if (disabled || (lda * (int64_t)sizeof(double)) % 16 != 0 || (reinterpret_cast<uintptr_t>(A) & 15) != 0)
+        return false;
+    struct Entry {
+        const double* A;
+        int64_t lda, nfull, d;
+        ChunkMaps maps;
+    };
+    static std::vector<Entry> cache;
+    for (const Entry& e : cache)
+        if (e.A == A && e.lda == lda && e.nfull == nfull && e.d == d) {
+            *out = e.maps;
+            return true;
+        }
+    ChunkMaps m;
+    const cuuint64_t dims[4] = {16, 32, (cuuint64_t)nfull, (cuuint64_t)d};
+    const cuuint64_t strides[3] = {256, 8192, (cuuint64_t)lda * sizeof(double)};
+    const cuuint32_t box[4] = {16, 32, 1, 1};
+    const cuuint32_t estr[4] = {1, 1, 1, 1};
+    for (int h = 0; h < 2; ++h) {
+        const CUresult r = tma_encode_fn()(h ? &m.odd : &m.even, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4,
+                                           const_cast<double*>(A + 16 * h), dims, strides, box, estr,
+                                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return false;
+    }
+    if (cache.size() >= 32) cache.erase(cache.begin());
+    cache.push_back(Entry{A, lda, nfull, d, m});
+    *out = m;
+    return true;
+}
+
+constexpr int64_t kStreamRingBytes = 64ll << 20;  // T ring budget: about half of the 126 MB L2
+
+// Group width G (>= one chunk per phase-1 warp per group, so a warp flushes
+// its done1 count at most about once per chunk) and ring depth nslot (2..6
+// slots within the L2 budget), or false when the streamed kernel does not apply.
+bool srht_stream_geometry(const SrhtPlan& p, int grid, int* G_out, int* nslot_out) {
+    if (p.H == 0 || p.npass != 1) return false;
+    const int64_t cpc = p.n_pad >> kChunkL;
+    const int64_t SC = (int64_t)grid * kP1Warps;
+    const int64_t col_bytes = p.n_pad * (int64_t)sizeof(double);
+    const int64_t G = std::max<int64_t>(1, std::min<int64_t>(p.d, ceil_div(SC, cpc)));
+    const int64_t nslot = std::min<int64_t>(6, kStreamRingBytes / (G * col_bytes));
+    if (nslot < 2) return false;
+    *G_out = (int)G;
+    *nslot_out = (int)nslot;
+    return true;
+}
 
 template <int HB>
-void launch_fused(const SrhtPlan& p, const double* A, const uint32_t* signbits, double* T, int G, int nslot,
-                  const int4* tiles, int n_tiles, const int2* entries, double* SA, unsigned long long* ctl,
-                  int num_sms, cudaStream_t st) {
-    static int max_blocks_per_sm = 0;
-    if (!max_blocks_per_sm) {
-        CUDA_CHECK(cudaFuncSetAttribute(srht_fused_kernel<HB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)kFusedSmem));
-        CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&max_blocks_per_sm, srht_fused_kernel<HB>, kP2Threads,
-                                                                 kFusedSmem));
-        if (max_blocks_per_sm < 1) max_blocks_per_sm = 1;
+void launch_stream(const SrhtPlan& p, const double* A, const uint32_t* signbits, double* T, int G, int nslot,
+                   const int4* tiles, int n_tiles, const int2* entries, double* SA, int* ctl, int grid,
+                   const uint32_t* mask, int logw, cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        CUDA_CHECK(cudaFuncSetAttribute(srht_stream_kernel<HB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)kStreamSmem));
+        attr = true;
     }
-    const int64_t cpc = p.n_pad >> kChunkL;
     const int ng = (int)ceil_div(p.d, G);
-    const int n1 = (int)ceil_div((int64_t)G * cpc, kP1Warps);
-    const int n2 = G * n_tiles;
-    const int64_t total = (int64_t)ng * (n1 + n2);
-    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(total, (int64_t)num_sms * max_blocks_per_sm));
-    CUDA_CHECK(cudaMemsetAsync(ctl, 0, sizeof(unsigned long long) + 2 * sizeof(int) * (size_t)ng, st));
-    LAUNCH(srht_fused_kernel<HB>, grid, kP2Threads, kFusedSmem, st, A, p.n, p.lda, signbits, T, p.n_pad, p.d, G, nslot,
-           ng, n1, n2, cpc, tiles, n_tiles, entries, p.pass_lo[0], p.scale1, p.scale2, SA, p.m, ctl);
+    CUDA_CHECK(cudaMemsetAsync(ctl, 0, 2 * sizeof(int) * (size_t)ng, st));
+    LAUNCH(srht_stream_kernel<HB>, (unsigned)grid, 2 * kP2Threads, kStreamSmem, st, A, p.n, p.lda, signbits, T, p.n_pad,
+           p.d, p.logn - kChunkL, G, nslot, ng, tiles, n_tiles, entries, p.pass_lo[0], p.scale1, p.scale2, SA, p.m,
+           ctl, mask, logw);
 }
-using FusedFn = void (*)(const SrhtPlan&, const double*, const uint32_t*, double*, int, int, const int4*, int,
-                         const int2*, double*, unsigned long long*, int, cudaStream_t);
-const FusedFn kFused[11] = {nullptr, launch_fused<1>, launch_fused<2>, launch_fused<3>, launch_fused<4>,
-                            launch_fused<5>, launch_fused<6>, launch_fused<7>, launch_fused<8>, launch_fused<9>,
-                            launch_fused<10>};
-constexpr int kFusedSlots = 3;
-constexpr int64_t kFusedRingBytes = 60ll << 20;  // T ring budget: well inside the 126 MB L2
-
-int fused_group_cols(const SrhtPlan& p) {
-    const int64_t per_col = p.n_pad * (int64_t)sizeof(double);
-    return (int)std::max<int64_t>(1, std::min<int64_t>(p.d, kFusedRingBytes / (kFusedSlots * per_col)));
-}
+using StreamFn = void (*)(const SrhtPlan&, const double*, const uint32_t*, double*, int, int, const int4*, int,
+                          const int2*, double*, int*, int, const uint32_t*, int, cudaStream_t);
+const StreamFn kStream[11] = {nullptr,          launch_stream<1>, launch_stream<2>, launch_stream<3>,
+                              launch_stream<4>, launch_stream<5>, launch_stream<6>, launch_stream<7>,
+                              launch_stream<8>, launch_stream<9>, launch_stream<10>};
 using PassFn = void (*)(const SrhtPlan&, double*, int, const int4*, int, bool, const int2*, double*, cudaStream_t);
 const PassFn kPass[11] = {nullptr, launch_pass<1>, launch_pass<2>, launch_pass<3>, launch_pass<4>, launch_pass<5>,
                           launch_pass<6>, launch_pass<7>, launch_pass<8>, launch_pass<9>, launch_pass<10>};
@@ -691,10 +937,11 @@ void srht_build_entries(const SrhtPlan& p, const int64_t* rows, std::vector<int2
         }
 }
 
-size_t srht_fused_scratch_bytes(const SrhtPlan& p, size_t* ctl_bytes) {
-    if (ctl_bytes) *ctl_bytes = sizeof(unsigned long long) + 2 * sizeof(int) * (size_t)(p.d + 1) + 64;
-    if (p.H == 0 || p.npass != 1) return srht_scratch_bytes(p);
-    return (size_t)kFusedSlots * fused_group_cols(p) * p.n_pad * sizeof(double);
+size_t srht_fused_scratch_bytes(const SrhtPlan& p, size_t* ctl_bytes, int num_sms) {
+    if (ctl_bytes) *ctl_bytes = 2 * sizeof(int) * (size_t)(p.d + 1) + 64;
+    int G = 0, nslot = 0;
+    if (!srht_stream_geometry(p, num_sms, &G, &nslot)) return srht_scratch_bytes(p);
+    return (size_t)nslot * G * p.n_pad * sizeof(double);
 }
 
 bool srht_build_mask(const SrhtPlan& p, const std::vector<int4>& tiles, uint32_t mask[4]) {
@@ -717,28 +964,45 @@ void srht_run_device(const SrhtPlan& p, const double* d_A, const uint32_t* d_sig
         kSmall[p.L](p, d_A, d_signbits, d_entries, d_SA, st);
         return;
     }
-    if (p.npass == 1 && n_tiles > 0 && d_ctl != nullptr) {
+    int G = 0, nslot = 0;
+    if (p.npass == 1 && n_tiles > 0 && d_ctl != nullptr && srht_stream_geometry(p, num_sms, &G, &nslot)) {
         // one launch, T kept in an L2-resident ring of column groups
-        kFused[p.pass_hb[0]](p, d_A, d_signbits, d_T, fused_group_cols(p), kFusedSlots, d_tiles, n_tiles, d_entries,
-                             d_SA, d_ctl, num_sms, st);
+        int logw = 0;
+        while ((1 << (logw + 1)) <= pass_w(p.pass_hb[0])) ++logw;
+        kStream[p.pass_hb[0]](p, d_A, d_signbits, d_T, G, nslot, d_tiles, n_tiles, d_entries, d_SA,
+                              reinterpret_cast<int*>(d_ctl), num_sms, d_mask, logw, st);
         return;
     }
     const int64_t chunks_per_col = p.n_pad >> kChunkL;
     const int64_t total = chunks_per_col * p.d;
-    const int64_t blocks = std::min<int64_t>(ceil_div(total, kP1AWarps), (int64_t)num_sms);
-    const size_t smem = (size_t)kP1AWarps * kP1Stages * kP1Buf * sizeof(double);
-    static bool attr = false;
-    if (!attr) {
-        CUDA_CHECK(cudaFuncSetAttribute(srht_phase1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = true;
-    }
     // single pass: phase 1 writes only the groups the emitting pass reads
     const bool masked = p.npass == 1 && d_mask != nullptr;
     int logw = 0;
     if (masked)
         while ((1 << (logw + 1)) <= pass_w(p.pass_hb[0])) ++logw;
-    LAUNCH(srht_phase1_kernel, (unsigned)blocks, 32 * kP1AWarps, smem, st, d_A, p.n, p.lda, d_signbits, d_T, p.n_pad,
-           chunks_per_col, total, masked ? d_mask : nullptr, logw);
+    const int64_t nfull = p.n >> kChunkL;
+    ChunkMaps maps;
+    if (nfull > 0 && srht_chunk_maps(d_A, p.lda, nfull, p.d, &maps)) {
+        static bool attr = false;
+        if (!attr) {
+            CUDA_CHECK(cudaFuncSetAttribute(srht_phase1_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)kP1TSmem));
+            attr = true;
+        }
+        const int64_t blocks = std::min<int64_t>(ceil_div(total, kP1TWarps), (int64_t)num_sms);
+        LAUNCH(srht_phase1_tma_kernel, (unsigned)blocks, 32 * kP1TWarps, kP1TSmem, st, maps, d_A, p.n, p.lda,
+               d_signbits, d_T, p.n_pad, p.logn - kChunkL, nfull, total, masked ? d_mask : nullptr, logw);
+    } else {
+        const int64_t blocks = std::min<int64_t>(ceil_div(total, kP1AWarps), (int64_t)num_sms);
+        const size_t smem = (size_t)kP1AWarps * 2 * kP1Buf * sizeof(double);
+        static bool attr = false;
+        if (!attr) {
+            CUDA_CHECK(cudaFuncSetAttribute(srht_phase1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            attr = true;
+        }
+        LAUNCH(srht_phase1_kernel, (unsigned)blocks, 32 * kP1AWarps, smem, st, d_A, p.n, p.lda, d_signbits, d_T,
+               p.n_pad, p.logn - kChunkL, total, masked ? d_mask : nullptr, logw);
+    }
     for (int i = 0; i < p.npass; ++i) {
         const bool last = i == p.npass - 1;
         if (last && n_tiles == 0) break;
