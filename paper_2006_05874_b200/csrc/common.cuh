@@ -66,8 +66,13 @@ struct SrhtPlan {
     int npass;               // phase-2 passes over the H high bits (<= 10 bits each)
     int pass_lo[3], pass_hb[3];
     double scale1, scale2;   // 1/sqrt(n_pad), sqrt(n_pad/m) (host-computed, :47 and :95)
+    int p2t;                 // threads per phase-2 tile (128; 256 for the 64 KiB-tile variant)
+    int stream;              // 1: streamed single-launch kernel (srht_plan_stream)
 };
 SrhtPlan srht_plan(int64_t n, int64_t d, int64_t lda, int64_t m);
+// switch the plan to the streamed single-launch kernel when it applies (sets
+// p2t before the entries are built); false = two-kernel path
+bool srht_plan_stream(SrhtPlan& p, int num_sms);
 size_t srht_scratch_bytes(const SrhtPlan& p);  // T buffer (phase-1 output) when H > 0
 // Host: bucket the sampled rows (draw order k -> row rows[k]) by phase-2
 // tile. entries = (row, k) pairs grouped by tile; tiles = (rlo0, begin, end).
@@ -77,12 +82,12 @@ void srht_build_entries(const SrhtPlan& p, const int64_t* rows, std::vector<int2
 // fit one pass): T is then a ring of srht_fused_scratch_bytes() and d_ctl a
 // control block of *ctl_bytes.
 size_t srht_fused_scratch_bytes(const SrhtPlan& p, size_t* ctl_bytes, int num_sms = 148);
-// d_mask (4 words, from srht_build_mask): phase 1 stores only the low-index
+// d_mask (8 words, from srht_build_mask): phase 1 stores only the low-index
 // groups the single emitting pass reads.
 void srht_run_device(const SrhtPlan& p, const double* d_A, const uint32_t* d_signbits, const int2* d_entries,
                      const int4* d_tiles, int n_tiles, double* d_T, double* d_SA, cudaStream_t st,
                      unsigned long long* d_ctl = nullptr, int num_sms = 148, const uint32_t* d_mask = nullptr);
-bool srht_build_mask(const SrhtPlan& p, const std::vector<int4>& tiles, uint32_t mask[4]);
+bool srht_build_mask(const SrhtPlan& p, const std::vector<int4>& tiles, uint32_t mask[8]);
 // Row-sharded SRHT: plan of one shard (n_loc = n_pad / P rows, n_real of them
 // real) that emits unscaled partials at r_lo(k) for all m sampled rows, and the
 // combine of the P gathered partials ([P][m][d]) into SA (d_hi[k] = r_hi(k)).

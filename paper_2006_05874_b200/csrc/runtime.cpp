@@ -254,7 +254,7 @@ struct ihs_gpu_problem {
     DevBuf shard_U, shard_hi;    // sharded SRHT partials [P][m][d] and r_hi(k)
     DevBuf fused_ctl;            // work-queue counters of the fused SRHT kernel
     DevBuf srht_mask;            // phase-1 store mask (active low-index groups)
-    uint32_t h_mask[4] = {0, 0, 0, 0};
+    uint32_t h_mask[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     bool mask_valid = false;
     PinnedBuf h_stage;
     std::vector<int64_t> h_rows;
@@ -275,11 +275,7 @@ namespace {
 // two-kernel path (default: measured faster; IHS_SRHT_FUSED=1 selects the
 // persistent single-launch kernel for A/B measurements).
 unsigned long long* srht_prepare_scratch(ihs_gpu_problem* P, const SrhtPlan& plan) {
-    static const bool unfused = [] {
-        const char* e = std::getenv("IHS_SRHT_FUSED");
-        return !(e && e[0] == '1');
-    }();
-    if (unfused) {
+    if (!plan.stream) {  // two-kernel path (srht_plan_stream declined)
         P->T.ensure(srht_scratch_bytes(plan));
         return nullptr;
     }
@@ -321,7 +317,7 @@ void device_sketch(ihs_gpu_problem* P, int kind, int64_t m, uint64_t seed, doubl
     cudaStream_t st = P->st;
     if (kind == IHS_SKETCH_SRHT) {
         if (m < 1) fail(IHS_INVALID_INPUT, "srht_sketch: m must be >= 1");
-        const SrhtPlan plan = srht_plan(n_glob, d, P->lda, m);
+        SrhtPlan plan = srht_plan(n_glob, d, P->lda, m);
         if (m > plan.n_pad) fail(IHS_SKETCH_TOO_LARGE, "srht_sketch: m exceeds padded row count");
         // D: rademacher(n_pad, make_stream(seed, 1)) as bits (sketch.hpp:85,87)
         P->signbits.ensure((size_t)((plan.n_pad + 31) / 32) * 4);
@@ -333,6 +329,7 @@ void device_sketch(ihs_gpu_problem* P, int kind, int64_t m, uint64_t seed, doubl
         sample_without_replacement(derive_seed(seed, 2), plan.n_pad, m, P->h_rows.data());
         const int shards = world > 1 ? world : std::max(1, emulate_shards);
         if (shards == 1) {
+            srht_plan_stream(plan, P->num_sms);  // decides the emitting-tile shape before the entries are built
             srht_build_entries(plan, P->h_rows.data(), P->h_entries, P->h_tiles);
             P->mask_valid = srht_build_mask(plan, P->h_tiles, P->h_mask);
             g_host_rng_ns +=
@@ -351,7 +348,8 @@ void device_sketch(ihs_gpu_problem* P, int kind, int64_t m, uint64_t seed, doubl
                 lo[(size_t)k] = P->h_rows[(size_t)k] % n_loc;
                 hi[(size_t)k] = (uint8_t)(P->h_rows[(size_t)k] / n_loc);
             }
-            const SrhtPlan sp = srht_plan_shard(std::min(n_loc, n), n_loc, d, P->lda, m);
+            SrhtPlan sp = srht_plan_shard(std::min(n_loc, n), n_loc, d, P->lda, m);
+            srht_plan_stream(sp, P->num_sms);
             srht_build_entries(sp, lo.data(), P->h_entries, P->h_tiles);
             P->mask_valid = srht_build_mask(sp, P->h_tiles, P->h_mask);
             g_host_rng_ns +=

@@ -36,7 +36,7 @@ namespace {
 constexpr int kSmallL = 10;  // n_pad <= 2^10: single on-chip kernel
 constexpr int kChunkL = 10;  // phase-1 chunk: 1024 rows per warp
 constexpr int kP1Warps = 8;
-constexpr int kTileElems = 8192;  // phase-2 tile: 2^13 doubles (64 KiB exchange buffer)
+
 constexpr int kP2Threads = 256;
 
 __host__ __device__ constexpr int padded(int i) { return i + (i >> 4); }
@@ -110,60 +110,6 @@ srht_small_kernel(const double* __restrict__ A, int64_t n, int64_t lda, const ui
 }
 
 // ------------------------------------------------------------ phase 1
-// One warp: bits 0..9 of the 1024-row chunk [r0, r0+1024) of column Acol ->
-// dst[0..1024). STREAM: A loads are evict-first (read exactly once).
-template <bool STREAM>
-__device__ __forceinline__ void p1_chunk(double* __restrict__ xs, const double* __restrict__ Acol, int64_t n,
-                                         const uint32_t* __restrict__ signbits, int64_t r0, double* __restrict__ dst,
-                                         const uint32_t* __restrict__ mask = nullptr, int logw = 0) {
-    const int lane = threadIdx.x & 31;
-    double v[32];
-    // coalesced load (lane = index bits 0-4, register c = bits 5-9), sign fused
-#pragma unroll
-    for (int c = 0; c < 32; ++c) {
-        const int64_t r = r0 + (c << 5) + lane;
-        v[c] = (r < n) ? eps_mul(signbits, r, STREAM ? __ldcs(Acol + r) : __ldg(Acol + r)) : 0.0;
-    }
-#pragma unroll
-    for (int c = 0; c < 32; ++c) xs[pad32((c << 5) | lane)] = v[c];
-    __syncwarp();
-    // register c = index bits 0-4: stages 0..4
-#pragma unroll
-    for (int c = 0; c < 32; ++c) v[c] = xs[pad32((lane << 5) | c)];
-#pragma unroll
-    for (int s = 0; s < 5; ++s)
-#pragma unroll
-        for (int c = 0; c < 32; ++c)
-            if (!(c & (1 << s))) bfly(v[c], v[c | (1 << s)]);
-#pragma unroll
-    for (int c = 0; c < 32; ++c) xs[pad32((lane << 5) | c)] = v[c];
-    __syncwarp();
-    // register c = index bits 5-9: stages 5..9
-#pragma unroll
-    for (int c = 0; c < 32; ++c) v[c] = xs[pad32((c << 5) | lane)];
-    __syncwarp();
-#pragma unroll
-    for (int s = 0; s < 5; ++s)
-#pragma unroll
-        for (int c = 0; c < 32; ++c)
-            if (!(c & (1 << s))) bfly(v[c], v[c | (1 << s)]);
-    if (mask == nullptr) {
-#pragma unroll
-        for (int c = 0; c < 32; ++c) dst[(c << 5) + lane] = v[c];
-    } else {
-        // store only the low-index groups a sampled row will read in phase 2
-        uint32_t mw[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) mw[k] = __ldg(mask + k);
-#pragma unroll
-        for (int c = 0; c < 32; ++c) {
-            const int e = (c << 5) + lane;
-            const int g = e >> logw;
-            if ((mw[g >> 5] >> (g & 31)) & 1u) dst[e] = v[c];
-        }
-    }
-}
-
 // 8-byte async copy global -> shared with an L2 evict-first policy (A is
 // read exactly once); src_valid == false zero-fills (+0.0).
 __device__ __forceinline__ void cp_async8_zfill(double* dst, const double* src, bool src_valid, uint64_t pol) {
@@ -451,12 +397,14 @@ srht_phase1_kernel(const double* __restrict__ A, int64_t n, int64_t lda, const u
 // pass bits [0, RB1); round 2 (RB2 = HB - RB1 > 0): register bits = pass bits
 // [RB1, HB) after one shared-memory exchange. emit: write the tile's sampled
 // rows (entries) instead of the tile.
-template <int HB>
+__host__ __device__ constexpr int ilog2c(int v) { return v <= 1 ? 0 : 1 + ilog2c(v >> 1); }
+template <int HB, int TH = kP2Threads>
 struct P2Geom {
     static constexpr int RB1 = HB < 5 ? HB : 5;
-    static constexpr int E = 1 << RB1;                    // registers per thread
-    static constexpr int W = kP2Threads * E / (1 << HB);  // consecutive low indices per tile
-    static constexpr int LOGW = (W >= 256) ? 8 : (W >= 128) ? 7 : (W >= 64) ? 6 : (W >= 32) ? 5 : (W >= 16) ? 4 : 3;
+    static constexpr int E = 1 << RB1;             // registers per thread
+    static constexpr int W = TH * E / (1 << HB);   // consecutive low indices per tile
+    static constexpr int LOGW = ilog2c(W);
+    static_assert(W >= 1 && (1 << LOGW) == W, "tile width");
 };
 
 // One CTA: bits [lo, lo+HB) of the tile whose element (b, w) sits at
@@ -466,22 +414,22 @@ struct P2Geom {
 struct CtaBar {
     __device__ __forceinline__ void operator()() const { __syncthreads(); }
 };
-// barrier over the kP2Threads threads of a warp group (named barrier `id`)
+// barrier over the `count` threads of a warp group (named barrier `id`)
 struct GroupBar {
-    int id;
+    int id, count;
     __device__ __forceinline__ void operator()() const {
-        asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(kP2Threads) : "memory");
+        asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
     }
 };
 
-template <int HB, bool CG, class Bar = CtaBar>
+template <int HB, bool CG, class Bar = CtaBar, int TH = kP2Threads>
 __device__ __forceinline__ void p2_tile(double* __restrict__ xs, double* __restrict__ Tcol, int lo, bool emit,
                                         int4 tile, const int2* __restrict__ entries, int64_t j, double s1, double s2,
                                         double* __restrict__ SA, int64_t m, int t = threadIdx.x, Bar bar = Bar()) {
-    constexpr int RB1 = P2Geom<HB>::RB1;
+    constexpr int RB1 = P2Geom<HB, TH>::RB1;
     constexpr int RB2 = HB - RB1;
-    constexpr int E = P2Geom<HB>::E;
-    constexpr int W = P2Geom<HB>::W;
+    constexpr int E = P2Geom<HB, TH>::E;
+    constexpr int W = P2Geom<HB, TH>::W;
     const int w = t % W;
     const int g = t / W;  // 2^RB2 groups
     double v[E];
@@ -549,7 +497,7 @@ __device__ __forceinline__ void p2_tile(double* __restrict__ xs, double* __restr
     }
     bar();
     const int64_t bmask = (int64_t{1} << HB) - 1;
-    for (int q = tile.y + t; q < tile.z; q += kP2Threads) {
+    for (int q = tile.y + t; q < tile.z; q += TH) {
         const int2 rk = entries[q];
         const int64_t r = rk.x;
         const int b = (int)((r >> lo) & bmask);
@@ -559,12 +507,12 @@ __device__ __forceinline__ void p2_tile(double* __restrict__ xs, double* __restr
 }
 
 // One CTA per (tile, column) of a phase-2 pass.
-template <int HB>
-__global__ void __launch_bounds__(kP2Threads)
+template <int HB, int TH>
+__global__ void __launch_bounds__(TH)
 srht_phase2_kernel(double* __restrict__ T, int64_t n_pad, int lo, const int4* __restrict__ tiles, int emit,
                    const int2* __restrict__ entries, double s1, double s2, double* __restrict__ SA, int64_t m) {
     extern __shared__ double xs[];
-    constexpr int LOGW = P2Geom<HB>::LOGW;
+    constexpr int LOGW = P2Geom<HB, TH>::LOGW;
     const int64_t j = blockIdx.y;
     int64_t base;
     int4 tile = make_int4(0, 0, 0, 0);
@@ -577,7 +525,7 @@ srht_phase2_kernel(double* __restrict__ T, int64_t n_pad, int lo, const int4* __
         const int64_t tid = blockIdx.x;
         base = ((tid % low_tiles) << LOGW) | ((tid / low_tiles) << (lo + HB));
     }
-    p2_tile<HB, false>(xs, T + j * n_pad + base, lo, emit != 0, tile, entries, j, s1, s2, SA, m);
+    p2_tile<HB, false, CtaBar, TH>(xs, T + j * n_pad + base, lo, emit != 0, tile, entries, j, s1, s2, SA, m);
 }
 
 // ------------------------------------------------------------ streamed (one pass of high bits)
@@ -604,38 +552,59 @@ __device__ __forceinline__ void spin_until(const int* ctr, int target) {
     while (ld_acquire(ctr) < target) __nanosleep(100);
 }
 
-constexpr int kXsDoubles = kTileElems + kTileElems / 32;  // emitting-pass exchange buffer
+
+// Streamed kernel shape: kP1Warps phase-1 warps (TMA-fed two-slot rings) and
+// kEmitGroups emitting groups of kEmitThreads threads, each with its own
+// exchange buffer, so two emitting tiles are in flight per SM.
+constexpr int kEmitGroups = 2;
+constexpr int kEmitThreads = 128;
+constexpr int kEmitXs = 32 * kEmitThreads + kEmitThreads;  // pad32(tile) for hb >= 5
+constexpr int kStreamThreads = 32 * kP1Warps + kEmitGroups * kEmitThreads;
+constexpr int kFlushChunks = 4;  // phase-1 warps publish done1 counts at most every 4 chunks
+constexpr size_t kStreamSmem = ((size_t)kP1Warps * 2 * kChunkDoubles + (size_t)kEmitGroups * kEmitXs) * sizeof(double) +
+                               kP1Warps * 2 * 8 + 1024;
 
 template <int HB>
-__global__ void __launch_bounds__(2 * kP2Threads, 1)
-srht_stream_kernel(const double* __restrict__ A, int64_t n, int64_t lda, const uint32_t* __restrict__ signbits,
-                   double* __restrict__ T, int64_t n_pad, int64_t d, int lcpc, int G, int nslot, int ng,
-                   const int4* __restrict__ tiles, int n_tiles, const int2* __restrict__ entries, int lo, double s1,
-                   double s2, double* __restrict__ SA, int64_t m, int* __restrict__ ctl,
-                   const uint32_t* __restrict__ mask, int logw) {
-    static_assert(kP2Threads == 32 * kP1Warps, "equal warp groups");
-    extern __shared__ double smem[];
+__global__ void __launch_bounds__(kStreamThreads, 1)
+srht_stream_kernel(const __grid_constant__ ChunkMaps maps, const double* __restrict__ A, int64_t n, int64_t lda,
+                   int64_t nfull, const uint32_t* __restrict__ signbits, double* __restrict__ T, int64_t n_pad,
+                   int64_t d, int lcpc, int G, int nslot, int ng, const int4* __restrict__ tiles, int n_tiles,
+                   const int2* __restrict__ entries, int lo, double s1, double s2, double* __restrict__ SA, int64_t m,
+                   int* __restrict__ ctl, const uint32_t* __restrict__ mask, int logw, int dbg) {
+    extern __shared__ unsigned char stream_raw[];
+    double* base = align1024(stream_raw);
+    double* xs_all = base + kP1Warps * 2 * kChunkDoubles;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     int* done1 = ctl;
     int* done2 = ctl + ng;
     const int64_t cpc = int64_t{1} << lcpc, cmask = cpc - 1;
     auto group_cols = [&](int g) { return (int)imin64(G, d - (int64_t)g * G); };
     if (warp >= kP1Warps) {
-        // ---------------- emitting warp group
-        const int t = threadIdx.x - kP2Threads;
-        const GroupBar bar{1};
+        if (dbg & 1) return;
+        // ---------------- emitting groups: worker k of CTA b is worker b*kEmitGroups + k; item i of
+        // group g goes to worker (first(g) + i) mod workers, first(g) = items handed out before g
+        const int k = (threadIdx.x - 32 * kP1Warps) / kEmitThreads;
+        const int t = (threadIdx.x - 32 * kP1Warps) % kEmitThreads;
+        const GroupBar bar{1 + k, kEmitThreads};
+        double* xs = xs_all + k * kEmitXs;
+        const int64_t workers = (int64_t)gridDim.x * kEmitGroups;
+        const int64_t me = (int64_t)blockIdx.x * kEmitGroups + k;
+        int64_t first = 0;
         for (int g = 0; g < ng; ++g) {
             const int gc = group_cols(g);
             const int items = gc * n_tiles;
-            if ((int)blockIdx.x >= items) continue;
+            const int i0 = (int)((me - first % workers + workers) % workers);
+            first += items;
+            if (i0 >= items) continue;
             if (t == 0) spin_until(done1 + g, (int)(gc * cpc));
             bar();
             int mine = 0;
-            for (int i = blockIdx.x; i < items; i += gridDim.x) {
+            for (int i = i0; i < items; i += (int)workers) {
                 const int jj = i / n_tiles;
                 const int4 tile = tiles[i % n_tiles];
-                p2_tile<HB, true, GroupBar>(smem, T + ((int64_t)(g % nslot) * G + jj) * n_pad + tile.x, lo, true,
-                                            tile, entries, (int64_t)g * G + jj, s1, s2, SA, m, t, bar);
+                p2_tile<HB, true, GroupBar, kEmitThreads>(xs, T + ((int64_t)(g % nslot) * G + jj) * n_pad + tile.x,
+                                                          lo, true, tile, entries, (int64_t)g * G + jj, s1, s2, SA, m,
+                                                          t, bar);
                 bar();  // the exchange buffer is rewritten by the next tile
                 ++mine;
             }
@@ -643,22 +612,35 @@ srht_stream_kernel(const double* __restrict__ A, int64_t n, int64_t lda, const u
         }
         return;
     }
-    // ---------------- phase-1 warps
-    double* ring = smem + kXsDoubles + warp * (2 * kP1Buf);
+    // ---------------- phase-1 warps (TMA-fed two-slot rings)
+    double* ring = base + warp * (2 * kChunkDoubles);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(xs_all + kEmitGroups * kEmitXs) + 2 * warp;
+    if (lane == 0) {
+        tma::mbar_init(&bars[0], 1);
+        tma::mbar_init(&bars[1], 1);
+        tma::fence_mbar_init();
+    }
+    __syncwarp();
     const int64_t total = d * cpc;
     const int64_t SC = (int64_t)gridDim.x * kP1Warps;  // chunks per round of all phase-1 warps
-    const uint64_t pol = policy_evict_first();
     const uint32_t store_bits = p1_store_bits(mask, logw);
     auto issue = [&](int64_t chunk, int slot) {
-        if (chunk < total) p1_issue(ring + slot * kP1Buf, A + (chunk >> lcpc) * lda, n, (chunk & cmask) << kChunkL, pol);
-        cp_async_commit();
+        if (lane == 0 && chunk < total && (chunk & cmask) < nfull)
+            p1_tma_issue(ring + slot * kChunkDoubles, &maps, (int)(chunk & cmask), (int)(chunk >> lcpc), &bars[slot]);
     };
-    auto flush = [&](int g, int cnt) {
-        __threadfence();
+    // finished-chunk counts not yet published: one release fence covers them all
+    int pend_g[kFlushChunks], pend_c[kFlushChunks], npend = 0, since = 0;
+    auto flush = [&]() {
+        if (!npend) return;
+        if (!(dbg & 2)) __threadfence();
         __syncwarp();
-        if (lane == 0) atomicAdd(done1 + g, cnt);
+        if (lane == 0)
+            for (int i = 0; i < npend; ++i) atomicAdd(done1 + pend_g[i], pend_c[i]);
+        npend = 0;
+        since = 0;
     };
-    int slot = 0, cur_g = -1, cnt = 0;
+    uint32_t parity = 0u;
+    int slot = 0, cur_g = -1;
     int64_t chunk = (int64_t)blockIdx.x * kP1Warps + warp;
     issue(chunk, 0);
     for (; chunk < total; chunk += SC) {
@@ -666,24 +648,35 @@ srht_stream_kernel(const double* __restrict__ A, int64_t n, int64_t lda, const u
         const int j = (int)(chunk >> lcpc);
         const int g = j / G;
         if (g != cur_g) {
-            if (cnt) flush(cur_g, cnt);
-            cnt = 0;
             cur_g = g;
-            if (g >= nslot) {
+            if (g >= nslot && !(dbg & 1)) {
+                // about to wait on the emits of group g - nslot: publish first
+                flush();
                 if (lane == 0) spin_until(done2 + g - nslot, group_cols(g - nslot) * n_tiles);
                 __syncwarp();
             }
         }
-        cp_async_wait1();
-        __syncwarp();
-        const int64_t r0 = (chunk & cmask) << kChunkL;
-        p1_transform_store(ring + slot * kP1Buf, signbits, n, r0,
-                           T + ((int64_t)(g % nslot) * G + (j - g * G)) * n_pad + r0, store_bits);
-        ++cnt;
+        const int64_t q = chunk & cmask, r0 = q << kChunkL;
+        double* buf = ring + slot * kChunkDoubles;
+        if (q < nfull) {
+            tma::mbar_wait(&bars[slot], (parity >> slot) & 1u);
+            parity ^= 1u << slot;
+        } else {
+            p1_sync_load(buf, A + (int64_t)j * lda, n, r0);
+        }
+        p1_transform_store_swz(buf, signbits, n, r0, T + ((int64_t)(g % nslot) * G + (j - g * G)) * n_pad + r0,
+                               store_bits);
+        if (npend && pend_g[npend - 1] == g) {
+            ++pend_c[npend - 1];
+        } else {
+            pend_g[npend] = g;
+            pend_c[npend] = 1;
+            ++npend;
+        }
+        if (++since >= kFlushChunks || npend == kFlushChunks) flush();
         slot ^= 1;
     }
-    if (cnt) flush(cur_g, cnt);
-    cp_async_wait0();
+    flush();
 }
 
 // Row-sharded SRHT combine (H_{n_pad} = H_P (x) H_{n_pad/P}, shard index =
@@ -714,13 +707,18 @@ __global__ void srht_combine_kernel(const double* __restrict__ U, int64_t m, int
     }
 }
 
-int pass_w(int hb) {
+int pass_w(int hb, int th) {
     const int rb1 = std::min(hb, 5);
-    return kP2Threads * (1 << rb1) / (1 << hb);
+    return th * (1 << rb1) / (1 << hb);
 }
 // elements of one phase-2 tile: W low indices x 2^hb pass combinations
-// (kTileElems for hb >= 5, 256 * 2^hb below)
-int64_t pass_tile_elems(int hb) { return (int64_t)pass_w(hb) << hb; }
+// (32 th for hb >= 5, th * 2^hb below)
+int64_t pass_tile_elems(int hb, int th) { return (int64_t)pass_w(hb, th) << hb; }
+int pass_logw(const SrhtPlan& p) {
+    int logw = 0;
+    while ((1 << (logw + 1)) <= pass_w(p.pass_hb[p.npass - 1], p.p2t)) ++logw;
+    return logw;
+}
 
 template <int L>
 void launch_small(const SrhtPlan& p, const double* A, const uint32_t* signbits, const int2* entries, double* SA,
@@ -736,25 +734,24 @@ const SmallFn kSmall[kSmallL + 1] = {launch_small<0>, launch_small<1>, launch_sm
                                      launch_small<4>, launch_small<5>, launch_small<6>, launch_small<7>,
                                      launch_small<8>, launch_small<9>, launch_small<10>};
 
-template <int HB>
+template <int HB, int TH>
 void launch_pass(const SrhtPlan& p, double* T, int lo, const int4* tiles, int n_tiles, bool emit, const int2* entries,
                  double* SA, cudaStream_t st) {
-    const size_t smem = (size_t)pad32(kTileElems) * sizeof(double) + 64;
+    const size_t smem = (size_t)pad32((int)pass_tile_elems(HB, TH)) * sizeof(double) + 64;
     static bool attr = false;
     if (!attr) {
-        CUDA_CHECK(cudaFuncSetAttribute(srht_phase2_kernel<HB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        CUDA_CHECK(cudaFuncSetAttribute(srht_phase2_kernel<HB, TH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)smem));
         attr = true;
     }
-    const int64_t tiles_per_col = p.n_pad / pass_tile_elems(HB);
+    const int64_t tiles_per_col = p.n_pad / pass_tile_elems(HB, TH);
     const unsigned gx = emit ? (unsigned)n_tiles : (unsigned)tiles_per_col;
     if (gx == 0) return;
     dim3 grid(gx, (unsigned)p.d);
-    LAUNCH(srht_phase2_kernel<HB>, grid, kP2Threads, smem, st, T, p.n_pad, lo, tiles, emit ? 1 : 0, entries,
-           p.scale1, p.scale2, SA, p.m);
+    LAUNCH((srht_phase2_kernel<HB, TH>), grid, TH, smem, st, T, p.n_pad, lo, tiles, emit ? 1 : 0, entries, p.scale1,
+           p.scale2, SA, p.m);
 }
 
-constexpr size_t kStreamSmem = (size_t)(kXsDoubles + kP1Warps * 2 * kP1Buf) * sizeof(double);
 // Tensor maps of the full 1024-row chunks of A (even / odd 128-byte rows of
 // each chunk, see p1_tma_issue), cached per (A, lda, nfull, d); false when
 // TMA is unavailable or disabled (IHS_SRHT_NO_TMA=1).
@@ -796,26 +793,36 @@ bool srht_chunk_maps(const double* A, int64_t lda, int64_t nfull, int64_t d, Chu
 
 constexpr int64_t kStreamRingBytes = 64ll << 20;  // T ring budget: about half of the 126 MB L2
 
-// Group width G (>= one chunk per phase-1 warp per group, so a warp flushes
-// its done1 count at most about once per chunk) and ring depth nslot (2..6
-// slots within the L2 budget), or false when the streamed kernel does not apply.
+// Group width G (about half a round of phase-1 chunks, so a column group is
+// finished by all SMs together) and ring depth nslot (2..8 slots within the
+// L2 budget), or false when the streamed kernel does not apply.
 bool srht_stream_geometry(const SrhtPlan& p, int grid, int* G_out, int* nslot_out) {
     if (p.H == 0 || p.npass != 1) return false;
     const int64_t cpc = p.n_pad >> kChunkL;
     const int64_t SC = (int64_t)grid * kP1Warps;
     const int64_t col_bytes = p.n_pad * (int64_t)sizeof(double);
-    const int64_t G = std::max<int64_t>(1, std::min<int64_t>(p.d, ceil_div(SC, cpc)));
-    const int64_t nslot = std::min<int64_t>(6, kStreamRingBytes / (G * col_bytes));
+    const int64_t G = std::max<int64_t>(1, std::min<int64_t>(p.d, ceil_div(SC, 2 * cpc)));
+    const int64_t nslot = std::min<int64_t>(8, kStreamRingBytes / (G * col_bytes));
     if (nslot < 2) return false;
     *G_out = (int)G;
     *nslot_out = (int)nslot;
     return true;
 }
 
+// timing experiments only (results are wrong): bit 0 drops the emitting
+// warps and the slot waits, bit 1 the release fences
+int stream_dbg() {
+    static const int v = [] {
+        const char* e = std::getenv("IHS_SRHT_STREAM_DBG");
+        return e ? std::atoi(e) : 0;
+    }();
+    return v;
+}
+
 template <int HB>
-void launch_stream(const SrhtPlan& p, const double* A, const uint32_t* signbits, double* T, int G, int nslot,
-                   const int4* tiles, int n_tiles, const int2* entries, double* SA, int* ctl, int grid,
-                   const uint32_t* mask, int logw, cudaStream_t st) {
+void launch_stream(const SrhtPlan& p, const ChunkMaps& maps, int64_t nfull, const double* A, const uint32_t* signbits,
+                   double* T, int G, int nslot, const int4* tiles, int n_tiles, const int2* entries, double* SA,
+                   int* ctl, int grid, const uint32_t* mask, int logw, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
         CUDA_CHECK(cudaFuncSetAttribute(srht_stream_kernel<HB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -824,18 +831,38 @@ void launch_stream(const SrhtPlan& p, const double* A, const uint32_t* signbits,
     }
     const int ng = (int)ceil_div(p.d, G);
     CUDA_CHECK(cudaMemsetAsync(ctl, 0, 2 * sizeof(int) * (size_t)ng, st));
-    LAUNCH(srht_stream_kernel<HB>, (unsigned)grid, 2 * kP2Threads, kStreamSmem, st, A, p.n, p.lda, signbits, T, p.n_pad,
-           p.d, p.logn - kChunkL, G, nslot, ng, tiles, n_tiles, entries, p.pass_lo[0], p.scale1, p.scale2, SA, p.m,
-           ctl, mask, logw);
+    LAUNCH(srht_stream_kernel<HB>, (unsigned)grid, kStreamThreads, kStreamSmem, st, maps, A, p.n, p.lda, nfull,
+           signbits, T, p.n_pad, p.d, p.logn - kChunkL, G, nslot, ng, tiles, n_tiles, entries, p.pass_lo[0], p.scale1,
+           p.scale2, SA, p.m, ctl, mask, logw, stream_dbg());
 }
-using StreamFn = void (*)(const SrhtPlan&, const double*, const uint32_t*, double*, int, int, const int4*, int,
-                          const int2*, double*, int*, int, const uint32_t*, int, cudaStream_t);
+using StreamFn = void (*)(const SrhtPlan&, const ChunkMaps&, int64_t, const double*, const uint32_t*, double*, int, int,
+                          const int4*, int, const int2*, double*, int*, int, const uint32_t*, int, cudaStream_t);
 const StreamFn kStream[11] = {nullptr,          launch_stream<1>, launch_stream<2>, launch_stream<3>,
                               launch_stream<4>, launch_stream<5>, launch_stream<6>, launch_stream<7>,
                               launch_stream<8>, launch_stream<9>, launch_stream<10>};
 using PassFn = void (*)(const SrhtPlan&, double*, int, const int4*, int, bool, const int2*, double*, cudaStream_t);
-const PassFn kPass[11] = {nullptr, launch_pass<1>, launch_pass<2>, launch_pass<3>, launch_pass<4>, launch_pass<5>,
-                          launch_pass<6>, launch_pass<7>, launch_pass<8>, launch_pass<9>, launch_pass<10>};
+const PassFn kPass[11] = {nullptr,
+                          launch_pass<1, 256>,
+                          launch_pass<2, 256>,
+                          launch_pass<3, 256>,
+                          launch_pass<4, 256>,
+                          launch_pass<5, 256>,
+                          launch_pass<6, 256>,
+                          launch_pass<7, 256>,
+                          launch_pass<8, 256>,
+                          launch_pass<9, 256>,
+                          launch_pass<10, 256>};
+const PassFn kPass128[11] = {nullptr,
+                             launch_pass<1, 128>,
+                             launch_pass<2, 128>,
+                             launch_pass<3, 128>,
+                             launch_pass<4, 128>,
+                             launch_pass<5, 128>,
+                             launch_pass<6, 128>,
+                             launch_pass<7, 128>,
+                             launch_pass<8, 128>,
+                             launch_pass<9, 128>,
+                             launch_pass<10, 128>};
 }  // namespace
 
 SrhtPlan srht_plan(int64_t n, int64_t d, int64_t lda, int64_t m) {
@@ -871,6 +898,8 @@ SrhtPlan srht_plan(int64_t n, int64_t d, int64_t lda, int64_t m) {
     // exactly the reference's host expressions (sketch.hpp:47 and :95)
     p.scale1 = 1.0 / std::sqrt(static_cast<double>(np));
     p.scale2 = std::sqrt(static_cast<double>(np) / static_cast<double>(m));
+    p.p2t = kP2Threads;  // 64 KiB tiles (measured faster than 128-thread tiles in the two-kernel path)
+    p.stream = 0;
     return p;
 }
 
@@ -912,9 +941,9 @@ void srht_build_entries(const SrhtPlan& p, const int64_t* rows, std::vector<int2
     // the in-tile low index; a tile is identified by its base row (pass bits and
     // low bits cleared). Counting sort of the sampled rows by tile.
     const int lo = p.pass_lo[p.npass - 1], hb = p.pass_hb[p.npass - 1];
-    const int64_t W = pass_w(hb);
+    const int64_t W = pass_w(hb, p.p2t);
     const int64_t low_tiles = (int64_t{1} << lo) / W;
-    const int64_t ntiles = p.n_pad / pass_tile_elems(hb);
+    const int64_t ntiles = p.n_pad / pass_tile_elems(hb, p.p2t);
     auto tile_of = [&](int64_t r) {
         const int64_t low = (r & ((int64_t{1} << lo) - 1)) / W;
         const int64_t high = r >> (lo + hb);
@@ -937,6 +966,18 @@ void srht_build_entries(const SrhtPlan& p, const int64_t* rows, std::vector<int2
         }
 }
 
+bool srht_plan_stream(SrhtPlan& p, int num_sms) {
+    static const bool enabled = [] {
+        const char* e = std::getenv("IHS_SRHT_FUSED");
+        return e && e[0] == '1';
+    }();
+    int G = 0, nslot = 0;
+    if (!enabled || (p.n >> kChunkL) == 0 || !srht_stream_geometry(p, num_sms, &G, &nslot)) return false;
+    p.p2t = kEmitThreads;
+    p.stream = 1;
+    return true;
+}
+
 size_t srht_fused_scratch_bytes(const SrhtPlan& p, size_t* ctl_bytes, int num_sms) {
     if (ctl_bytes) *ctl_bytes = 2 * sizeof(int) * (size_t)(p.d + 1) + 64;
     int G = 0, nslot = 0;
@@ -944,11 +985,11 @@ size_t srht_fused_scratch_bytes(const SrhtPlan& p, size_t* ctl_bytes, int num_sm
     return (size_t)nslot * G * p.n_pad * sizeof(double);
 }
 
-bool srht_build_mask(const SrhtPlan& p, const std::vector<int4>& tiles, uint32_t mask[4]) {
-    mask[0] = mask[1] = mask[2] = mask[3] = 0u;
+bool srht_build_mask(const SrhtPlan& p, const std::vector<int4>& tiles, uint32_t mask[8]) {
+    for (int k = 0; k < 8; ++k) mask[k] = 0u;
     if (p.H == 0 || p.npass != 1) return false;
-    int logw = 0;
-    while ((1 << (logw + 1)) <= pass_w(p.pass_hb[0])) ++logw;
+    const int logw = pass_logw(p);
+    if (logw < 2) return false;  // more than 256 groups: store everything
     for (const int4& t : tiles) {
         const int g = (t.x & ((1 << kChunkL) - 1)) >> logw;
         mask[g >> 5] |= 1u << (g & 31);
@@ -965,11 +1006,14 @@ void srht_run_device(const SrhtPlan& p, const double* d_A, const uint32_t* d_sig
         return;
     }
     int G = 0, nslot = 0;
-    if (p.npass == 1 && n_tiles > 0 && d_ctl != nullptr && srht_stream_geometry(p, num_sms, &G, &nslot)) {
+    ChunkMaps maps;
+    const int64_t nfull = p.n >> kChunkL;
+    if (p.npass == 1 && p.stream && p.p2t == kEmitThreads && n_tiles > 0 && d_ctl != nullptr &&
+        srht_stream_geometry(p, num_sms, &G, &nslot) &&
+        nfull > 0 && srht_chunk_maps(d_A, p.lda, nfull, p.d, &maps)) {
         // one launch, T kept in an L2-resident ring of column groups
-        int logw = 0;
-        while ((1 << (logw + 1)) <= pass_w(p.pass_hb[0])) ++logw;
-        kStream[p.pass_hb[0]](p, d_A, d_signbits, d_T, G, nslot, d_tiles, n_tiles, d_entries, d_SA,
+        const int logw = pass_logw(p);
+        kStream[p.pass_hb[0]](p, maps, nfull, d_A, d_signbits, d_T, G, nslot, d_tiles, n_tiles, d_entries, d_SA,
                               reinterpret_cast<int*>(d_ctl), num_sms, d_mask, logw, st);
         return;
     }
@@ -977,11 +1021,7 @@ void srht_run_device(const SrhtPlan& p, const double* d_A, const uint32_t* d_sig
     const int64_t total = chunks_per_col * p.d;
     // single pass: phase 1 writes only the groups the emitting pass reads
     const bool masked = p.npass == 1 && d_mask != nullptr;
-    int logw = 0;
-    if (masked)
-        while ((1 << (logw + 1)) <= pass_w(p.pass_hb[0])) ++logw;
-    const int64_t nfull = p.n >> kChunkL;
-    ChunkMaps maps;
+    const int logw = masked ? pass_logw(p) : 0;
     if (nfull > 0 && srht_chunk_maps(d_A, p.lda, nfull, p.d, &maps)) {
         static bool attr = false;
         if (!attr) {
@@ -1006,7 +1046,8 @@ void srht_run_device(const SrhtPlan& p, const double* d_A, const uint32_t* d_sig
     for (int i = 0; i < p.npass; ++i) {
         const bool last = i == p.npass - 1;
         if (last && n_tiles == 0) break;
-        kPass[p.pass_hb[i]](p, d_T, p.pass_lo[i], d_tiles, n_tiles, last, d_entries, d_SA, st);
+        (p.p2t == 128 ? kPass128 : kPass)[p.pass_hb[i]](p, d_T, p.pass_lo[i], d_tiles, n_tiles, last, d_entries, d_SA,
+                                                        st);
     }
 }
 
