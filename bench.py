@@ -62,6 +62,25 @@ def peaks():
         return 6650.0, "fallback"
 
 
+def fp64_peak():
+    """Measured fp64 tensor (DMMA) peak: tools/fp64_peak.cu -> profiles/fp64_peak.json."""
+    try:
+        j = json.loads((ROOT / "profiles" / "fp64_peak.json").read_text())
+        return float(j["fp64_dmma_tflops"]), "measured (tools/fp64_peak.cu, mma.sync m8n8k4 f64 loop)"
+    except Exception:  # noqa: BLE001
+        return 37.0, "fallback (B200 fp64 tensor nominal)"
+
+
+def ncu_traffic(cfg, which):
+    """DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) of the dominant kernel from the
+    committed `ncu --set full` summary profiles/traffic.json (written by tools/ncu_traffic.py), or None."""
+    try:
+        j = json.loads((ROOT / "profiles" / "traffic.json").read_text())
+        return j[cfg][which]
+    except Exception:  # noqa: BLE001
+        return None
+
+
 def solver_config(ihs, c, seed=0):
     return ihs.SolverConfig(rho=c["rho"], sketch_kind=getattr(ihs.SketchKind, c["sketch"]),
                             mode=getattr(ihs.SolveMode, c["mode"]), m_initial=c["m_initial"],
@@ -270,34 +289,52 @@ def main():
         e2e = {"value": v, "unit": "s", "h2d_bytes_per_step": 8 * n * d + 8 * n, "d2h_bytes_per_step": 8 * d,
                "timer": "host wall clock around upload+solve (includes the H2D copies)"}
 
-    # ---- roofline of the dominant kernel (live, from the solve's CUDA-event phase timers)
+    # ---- roofline of the dominant kernel (live, from the solve's CUDA-event phase timers:
+    # the sketch kernels (SRHT transform / S*A GEMM) and the fused gradient kernels are
+    # bracketed by events on the library's stream)
     last = reps[-1]
     t = last.device_times
     hbm, peak_kind = peaks()
+    fp64, fp64_kind = fp64_peak()
     phases = {"gradient": t["gradient_ms"], "sketch": t["sketch_ms"], "factor": t["factor_ms"], "solve": t["solve_ms"]}
-    dom = max(phases, key=phases.get)
-    if dom == "gradient" or c["sketch"] == "Gaussian" and dom != "sketch":
+    kern = {}
+    if t["n_gradient"] > 0 and t["gradient_ms"] > 0:
         ach = t["gradient_bytes"] / (t["gradient_ms"] * 1e-3) / 1e9
-        roof = {"kernel": "grad_partial_kernel (+reduce, candidates) — fused A^T(Ax-b) 1-2 RHS",
-                "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
-                "traffic": None, "per_launch_ms": t["gradient_ms"] / max(1, t["n_gradient"]),
-                "algorithmic_bytes_per_launch": t["gradient_bytes"] / max(1, t["n_gradient"]),
-                "peak_source": peak_kind}
-    else:
+        kern["gradient"] = {"kernel": "grad_rm_kernel (+grad_reduce) — fused A^T(Ax-b)+nu^2 x, 1-2 RHS, one pass over A",
+                            "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+                            "per_launch_ms": t["gradient_ms"] / t["n_gradient"],
+                            "algorithmic_bytes_per_launch": t["gradient_bytes"] / t["n_gradient"],
+                            "launches": t["n_gradient"], "total_ms": t["gradient_ms"], "peak_source": peak_kind}
+    if t["n_sketch_kernel"] > 0 and t["sketch_kernel_ms"] > 0:
+        sk_ms = t["sketch_kernel_ms"]
         if c["sketch"] == "SRHT":
-            ach = t["sketch_bytes"] / (t["sketch_ms"] * 1e-3) / 1e9
-            roof = {"kernel": "srht_phase1/phase2 (+ sign bits, sample upload)", "bound": "hbm", "achieved": ach,
-                    "peak": hbm, "unit": "GB/s", "frac": ach / hbm, "traffic": None,
-                    "per_launch_ms": t["sketch_ms"] / max(1, t["n_sketch"]), "peak_source": peak_kind}
+            ach = t["sketch_bytes"] / (sk_ms * 1e-3) / 1e9
+            kern["sketch"] = {"kernel": "srht_phase1_tma_kernel + srht_phase2_kernel (FWHT, sign, sample gather)",
+                              "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+                              "algorithmic_bytes_per_launch": t["sketch_bytes"] / t["n_sketch_kernel"],
+                              "peak_source": peak_kind}
         else:
-            ach = t["sketch_flops"] / (t["sketch_ms"] * 1e-3) / 1e12
-            roof = {"kernel": "gaussian generator + dgemm_kernel (DMMA)", "bound": "tensor", "achieved": ach,
-                    "peak": None, "unit": "TFLOP/s", "frac": None, "traffic": None, "peak_source": "fp64 peak TBD"}
+            ach = t["sketch_flops"] / (sk_ms * 1e-3) / 1e12
+            kern["sketch"] = {"kernel": "dgemm_kernel<0,0> S*A (mma.sync m8n8k4 f64 = DMMA)", "bound": "tensor",
+                              "achieved": ach, "peak": fp64, "unit": "TFLOP/s", "frac": ach / fp64 if fp64 else None,
+                              "algorithmic_flops_per_launch": t["sketch_flops"] / t["n_sketch_kernel"],
+                              "peak_source": fp64_kind}
+        kern["sketch"].update({"per_launch_ms": sk_ms / t["n_sketch_kernel"], "launches": t["n_sketch_kernel"],
+                               "total_ms": sk_ms})
+    dom = max(kern, key=lambda k: kern[k]["total_ms"]) if kern else None
+    roof = dict(kern[dom]) if dom else {"bound": None, "achieved": None, "peak": None, "unit": None, "frac": None}
+    roof["traffic"] = ncu_traffic(args.config, dom)
+    roof["dominant"] = dom
+    roof["other_kernels"] = {k: {kk: v[kk] for kk in ("kernel", "achieved", "unit", "frac", "per_launch_ms")}
+                             for k, v in kern.items() if k != dom}
     roof["phase_ms"] = phases
-    roof["dominant_phase"] = dom
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and n * d > (1 << 26):
+        cpu = {"value": None, "unit": "s", "cores": 1, "kind": "port",
+               "sample": "not run: a single-thread oracle solve of this config exceeds the few-minute bench budget "
+                         "(the default config C2 carries the CPU baseline)"}
+    elif rank == 0 and world == 1 and not args.no_cpu_baseline:
         from oracle import oracle as O
         ocfg = oracle_config(O, c)
         x_ref, orep, olog, _ = O.adaptive_solve(A, b, nu, ocfg)

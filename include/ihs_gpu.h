@@ -117,6 +117,9 @@ typedef struct ihs_phase_times {
     double sketch_flops;   /* algorithmic flops of the Gaussian sketches (2mnd each) */
     double alloc_ms;       /* host time spent growing device buffers */
     double host_rng_ms;    /* host time drawing the SRHT row samples (Fisher-Yates) */
+    double sketch_kernel_ms; /* device time of the sketch's main kernels alone (SRHT transform
+                                kernels / the S*A DMMA GEMM), part of sketch_ms */
+    int64_t n_sketch_kernel; /* number of such sketch-kernel intervals */
 } ihs_phase_times;
 
 /* SolveReport (solver.hpp:70-87). Arrays are caller-allocated; *_size is the

@@ -160,6 +160,7 @@ struct PhaseTimer {
     std::vector<cudaEvent_t> pool;
     size_t used = 0;
     bool enabled = true;
+    bool active = false;  // between reset() (solve start) and collect()
     explicit PhaseTimer(cudaStream_t s) : st(s) {}
     ~PhaseTimer() {
         for (auto e : pool) cudaEventDestroy(e);
@@ -173,7 +174,7 @@ struct PhaseTimer {
         return pool[used++];
     }
     void mark(int phase) {
-        if (!enabled) return;
+        if (!enabled || !active) return;
         cudaEvent_t e = get();
         CUDA_CHECK(cudaEventRecord(e, st));
         marks.push_back({e, phase});
@@ -181,22 +182,27 @@ struct PhaseTimer {
     void reset() {
         marks.clear();
         used = 0;
+        active = true;
     }
-    // sum of intervals [mark(phase), next mark) per phase id
-    void collect(double out_ms[4]) {
-        for (int i = 0; i < 4; ++i) out_ms[i] = 0.0;
+    // sum of intervals [mark(phase), next mark) per phase id (0..4), and the
+    // number of intervals per phase
+    void collect(double out_ms[5], int64_t count[5]) {
+        active = false;
+        for (int i = 0; i < 5; ++i) out_ms[i] = 0.0, count[i] = 0;
         if (marks.size() < 2) return;
         CUDA_CHECK(cudaEventSynchronize(marks.back().first));
         for (size_t i = 0; i + 1 < marks.size(); ++i) {
             const int ph = marks[i].second;
-            if (ph < 0 || ph > 3) continue;
+            if (ph < 0 || ph > 4) continue;
             float ms = 0.f;
             CUDA_CHECK(cudaEventElapsedTime(&ms, marks[i].first, marks[i + 1].first));
             out_ms[ph] += ms;
+            count[ph] += 1;
         }
     }
 };
-enum { PH_SKETCH = 0, PH_FACTOR = 1, PH_GRAD = 2, PH_SOLVE = 3, PH_END = -1 };
+// PH_SKETCH_KERNEL: the sketch's main kernels inside a PH_SKETCH interval
+enum { PH_SKETCH = 0, PH_FACTOR = 1, PH_GRAD = 2, PH_SOLVE = 3, PH_SKETCH_KERNEL = 4, PH_END = -1 };
 
 }  // namespace
 
@@ -336,9 +342,11 @@ void device_sketch(ihs_gpu_problem* P, int kind, int64_t m, uint64_t seed, doubl
                 std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t_rng).count();
             upload_entries(P);
             unsigned long long* ctl = srht_prepare_scratch(P, plan);
+            P->timer->mark(PH_SKETCH_KERNEL);
             srht_run_device(plan, P->A.d(), P->signbits.as<uint32_t>(), P->entries.as<int2>(), P->tiles.as<int4>(),
                             (int)P->h_tiles.size(), P->T.d(), d_SA, st, ctl, P->num_sms,
                             P->mask_valid ? P->srht_mask.as<uint32_t>() : nullptr);
+            P->timer->mark(PH_SKETCH);
         } else {
             // shard p holds rows [p*n_loc, (p+1)*n_loc) of the padded index space
             const int64_t n_loc = plan.n_pad / shards;
@@ -396,8 +404,10 @@ void device_sketch(ihs_gpu_problem* P, int kind, int64_t m, uint64_t seed, doubl
         // SA = S * A on the DMMA path (sketch.hpp:68)
         const int splitk = dgemm_pick_splitk(m, d, n, P->num_sms);
         if (splitk > 1) P->gemm_work.ensure((size_t)splitk * m * d * sizeof(double));
+        P->timer->mark(PH_SKETCH_KERNEL);
         dgemm(false, false, m, d, n, 1.0, P->S.d(), m, P->A.d(), P->lda, 0.0, d_SA, m, false, splitk,
               splitk > 1 ? P->gemm_work.d() : nullptr, st);
+        P->timer->mark(PH_SKETCH);
         if (world > 1) nccl_allreduce_sum(d_SA, (size_t)(m * d), P->opts.nccl_comm, st);
         if (c) c->sketch += (uint64_t)m * (uint64_t)n_glob * (uint64_t)d;  // sketch.hpp:65-67
     } else {
@@ -1189,12 +1199,15 @@ ihs_status ihs_gpu_adaptive_solve(ihs_gpu_problem* P, const ihs_solver_config* c
         rep->tuning = tp;
         rep->recompute_r_after_resketch = cfg->recompute_r_after_resketch;
         rep->wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
-        double ph[4];
-        tm.collect(ph);
+        double ph[5];
+        int64_t phn[5];
+        tm.collect(ph, phn);
         PT.alloc_ms = (double)(g_alloc_ns.load() - alloc0) * 1e-6;
         PT.host_rng_ms = (double)(g_host_rng_ns.load() - rng0) * 1e-6;
         rep->times = PT;
-        rep->times.sketch_ms = ph[PH_SKETCH];
+        rep->times.sketch_ms = ph[PH_SKETCH] + ph[PH_SKETCH_KERNEL];
+        rep->times.sketch_kernel_ms = ph[PH_SKETCH_KERNEL];
+        rep->times.n_sketch_kernel = phn[PH_SKETCH_KERNEL];
         rep->times.factor_ms = ph[PH_FACTOR];
         rep->times.gradient_ms = ph[PH_GRAD];
         rep->times.solve_ms = ph[PH_SOLVE];
