@@ -128,7 +128,7 @@ struct GradPlan {
     int R;          // rows per panel
     int grid;       // persistent CTAs
     size_t smem;
-    int version;    // 3: TMA-fed panel ring; 2: cp.async panel ring; 1: L2 re-read (large d)
+    int version;    // 5: register rows (row-major); 4: row-major panels; 3: TMA panels; 2: cp.async ring; 1: L2 re-read
     int stages;     // ring depth (v2/v3/v4)
     int grid_sms;   // SM count the plan was made for
     alignas(64) unsigned char tmap[128];  // CUtensorMap of A (v3)
@@ -140,6 +140,11 @@ void grad_plan_attach_tma(GradPlan& p, const double* d_A);
 // to v4 when the geometry fits (the caller then keeps a row-major A)
 bool grad_plan_use_rowmajor(GradPlan& p);
 size_t grad_rm_smem(int64_t d, int R, int nrhs, int ns);
+// v5: register-resident rows for d <= 512 (row-major copy as well)
+size_t grad_rr_smem(int64_t d, int R, int ns);
+bool grad_rr_geometry(int64_t d, int64_t lda, int* R, int* ns);
+void grad_rr_run(const GradPlan& p, const double* Arm, const double* b, const double* X, int nrhs, double* work,
+                 cudaStream_t st);
 bool grad_rm_geometry(int64_t d, int64_t lda, int* R, int* ns);
 void transpose_to_rowmajor(const double* A, int64_t lda, int64_t rows, int64_t d, double* Arm, cudaStream_t st);
 void grad_rm_run(const GradPlan& p, const double* Arm, const double* b, const double* X, int nrhs, double* work,

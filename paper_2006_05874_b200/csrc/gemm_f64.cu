@@ -132,6 +132,114 @@ dgemm_kernel(int64_t M, int64_t N, int64_t K, double alpha, const double* __rest
             }
 }
 
+
+// ---- large NN GEMM (S*A): 128x128 CTA tile, 8 warps of 64x32, 4-stage cp.async ring.
+// A (M x K, col-major: m contiguous) is staged k-major As[k][m] (row stride 132),
+// B (K x N, col-major: k contiguous) n-major Bs[n][k] (row stride 20), so both
+// the 16-byte cp.async writes and the m8n8k4 fragment reads are conflict-free.
+constexpr int GBM = 128, GBN = 128, GBK = 16, GST = 4;
+constexpr int GLA = 132, GLB = 20;
+constexpr int GTHREADS = 256;
+constexpr size_t kBigSmem = (size_t)GST * (GBK * GLA + GBN * GLB) * sizeof(double);
+
+__device__ __forceinline__ void cp16(double* dst, const double* src, int bytes) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(src), "r"(bytes) : "memory");
+}
+
+__global__ void __launch_bounds__(GTHREADS, 1)
+dgemm_nn_big_kernel(int64_t M, int64_t N, int64_t K, double alpha, const double* __restrict__ A, int64_t lda,
+                    const double* __restrict__ B, int64_t ldb, double beta, double* __restrict__ C, int64_t ldc,
+                    int64_t k_per_split, double* __restrict__ work) {
+    extern __shared__ double gsm[];
+    const int64_t m0 = (int64_t)blockIdx.x * GBM, n0 = (int64_t)blockIdx.y * GBN;
+    const int64_t kbeg = (int64_t)blockIdx.z * k_per_split;
+    const int64_t kend = min(K, kbeg + k_per_split);
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const int wm = (warp & 1) * 64, wn = (warp >> 1) * 32;
+    double* As0 = gsm;
+    double* Bs0 = gsm + GST * GBK * GLA;
+    // per-thread copy assignments (4 A chunks, 4 B chunks of 16 B per stage)
+    // A: chunk c = t + 256 u -> k = c / 64, m pair = c % 64
+    // B: chunk c = t + 256 u -> n = c / 8,  k pair = c % 8
+    auto issue = [&](int64_t k0, int stage) {
+        double* As = As0 + stage * GBK * GLA;
+        double* Bs = Bs0 + stage * GBN * GLB;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int c = t + GTHREADS * u;
+            const int kk = c >> 6, mm = (c & 63) * 2;
+            const int64_t gk = k0 + kk, gm = m0 + mm;
+            int bytes = 0;
+            if (gk < kend) bytes = gm + 1 < M ? 16 : (gm < M ? 8 : 0);
+            cp16(As + kk * GLA + mm, bytes ? A + gm + gk * lda : A, bytes);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int c = t + GTHREADS * u;
+            const int nn = c >> 3, kk = (c & 7) * 2;
+            const int64_t gn = n0 + nn, gk = k0 + kk;
+            int bytes = 0;
+            if (gn < N) bytes = gk + 1 < kend ? 16 : (gk < kend ? 8 : 0);
+            cp16(Bs + nn * GLB + kk, bytes ? B + gk + gn * ldb : B, bytes);
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
+    double acc[8][4][2];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    const int64_t ntiles = (kend - kbeg + GBK - 1) / GBK;
+#pragma unroll
+    for (int s = 0; s < GST - 1; ++s) {
+        if (s < ntiles) issue(kbeg + s * GBK, s);
+        else asm volatile("cp.async.commit_group;\n" ::: "memory");
+    }
+    const int fr = lane >> 2, fk = lane & 3;
+    for (int64_t it = 0; it < ntiles; ++it) {
+        asm volatile("cp.async.wait_group %0;\n" ::"n"(GST - 2) : "memory");
+        __syncthreads();
+        const int64_t nx = it + GST - 1;
+        if (nx < ntiles) issue(kbeg + nx * GBK, (int)(nx % GST));
+        else asm volatile("cp.async.commit_group;\n" ::: "memory");
+        const int stage = (int)(it % GST);
+        const double* As = As0 + stage * GBK * GLA + wm + fr;
+        const double* Bs = Bs0 + stage * GBN * GLB + (wn + fr) * GLB;
+#pragma unroll
+        for (int kk = 0; kk < GBK; kk += 4) {
+            double af[8], bf[4];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) af[i] = As[(kk + fk) * GLA + i * 8];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) bf[j] = Bs[j * 8 * GLB + kk + fk];
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+        }
+    }
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int64_t gm = m0 + wm + i * 8 + fr;
+                const int64_t gn = n0 + wn + j * 8 + 2 * fk + h;
+                if (gm >= M || gn >= N) continue;
+                const double v = acc[i][j][h];
+                if (work) {
+                    work[(int64_t)blockIdx.z * M * N + gm + gn * M] = v;
+                } else {
+                    double out = alpha * v;
+                    if (beta != 0.0) out += beta * C[gm + gn * ldc];
+                    C[gm + gn * ldc] = out;
+                }
+            }
+}
+
 // C = alpha * sum_z work[z] + beta * C, splits summed in fixed order
 __global__ void splitk_reduce_kernel(int64_t M, int64_t N, int splits, const double* __restrict__ work, double alpha,
                                      double beta, double* __restrict__ C, int64_t ldc, int lower_only) {
@@ -148,7 +256,26 @@ __global__ void splitk_reduce_kernel(int64_t M, int64_t N, int splits, const dou
 }
 }  // namespace
 
+// the 128x128 cp.async kernel: plain NN products with enough work and 16-byte
+// aligned columns (S*A of the Gaussian sketch)
+bool dgemm_use_big(bool transA, bool transB, int64_t M, int64_t N, int64_t K, int64_t lda, int64_t ldb,
+                   bool lower_only) {
+    return !transA && !transB && !lower_only && M >= 256 && N >= 128 && K >= 4096 && lda % 2 == 0 && ldb % 2 == 0;
+}
+
 int dgemm_pick_splitk(int64_t M, int64_t N, int64_t K, int num_sms) {
+    if (dgemm_use_big(false, false, M, N, K, M + (M & 1), 2, false)) {
+        // one CTA per SM: the split count whose last wave is fullest (>= 1024 rows of K per split)
+        const int64_t tiles = ceil_div(M, GBM) * ceil_div(N, GBN);
+        int best = 1;
+        double best_eff = 0.0;
+        for (int s = 1; s <= 16 && K / s >= 1024; ++s) {
+            const int64_t ctas = tiles * s;
+            const double eff = (double)ctas / (double)(ceil_div(ctas, num_sms) * num_sms);
+            if (eff > best_eff + 1e-9) { best_eff = eff; best = s; }
+        }
+        return best;
+    }
     const int64_t tiles = ceil_div(M, BM) * ceil_div(N, BN);
     const int64_t want = (int64_t)num_sms * 4;
     int s = 1;
@@ -165,10 +292,19 @@ void dgemm(bool transA, bool transB, int64_t M, int64_t N, int64_t K, double alp
         splitk = 1;
     }
     if (splitk < 1) splitk = 1;
+    const bool big = dgemm_use_big(transA, transB, M, N, K, lda, ldb, lower_only);
+    if (big) {
+        static bool attr = false;
+        if (!attr) {
+            CUDA_CHECK(cudaFuncSetAttribute(dgemm_nn_big_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)kBigSmem));
+            attr = true;
+        }
+    }
     int64_t kps = ceil_div(std::max<int64_t>(K, 1), splitk);
     kps = ceil_div(kps, BK) * BK;
     const int splits = (int)std::max<int64_t>(1, ceil_div(std::max<int64_t>(K, 1), kps));
-    dim3 grid((unsigned)ceil_div(M, BM), (unsigned)ceil_div(N, BN), (unsigned)splits);
+    dim3 grid((unsigned)ceil_div(M, big ? GBM : BM), (unsigned)ceil_div(N, big ? GBN : BN), (unsigned)splits);
     double* work = splits > 1 ? d_work : nullptr;
     if (splits > 1 && !d_work) fail(IHS_INTERNAL_ERROR, "dgemm: split-K without workspace");
     if (K <= 0) {
@@ -179,7 +315,10 @@ void dgemm(bool transA, bool transB, int64_t M, int64_t N, int64_t K, double alp
                (int)lower_only);
         return;
     }
-    if (!transA && !transB)
+    if (!transA && !transB && big)
+        LAUNCH(dgemm_nn_big_kernel, grid, GTHREADS, kBigSmem, st, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kps,
+               work);
+    else if (!transA && !transB)
         LAUNCH((dgemm_kernel<false, false>), grid, THREADS, 0, st, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc,
                (int)lower_only, kps, work);
     else if (transA && !transB)

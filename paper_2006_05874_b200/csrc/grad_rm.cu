@@ -183,6 +183,148 @@ __global__ void transpose_kernel(const double* __restrict__ A, int64_t lda, int6
     }
 }
 
+
+// ---- v5: register-resident rows (d <= 512). Warp w of the 8 consumer warps
+// owns rows w, w+8, ... of every panel; lane l holds the column pairs
+// 2l + 64k of its row in registers, so one shared read of the row serves both
+// sweeps: r = A_i x - b_i is a warp xor-allreduce (bitwise identical on every
+// lane: each step adds the same two values), then the lane updates its
+// column-pair partials with A_i^T r. No CTA barrier per panel: lane 0 of warp
+// 0 refills a stage once all 8 warps arrived on its "empty" mbarrier (no
+// dedicated producer warp: with 8 warps = 2 per SM sub-partition every thread
+// may hold up to 255 registers). The per-warp
+// partials are summed in warp order at the end (deterministic, like the other
+// variants).
+constexpr int RW = 8;  // consumer warps
+constexpr int RTHREADS = 32 * RW;
+
+template <int NRHS, int KP, int RR, int NS>
+__global__ void __launch_bounds__(RTHREADS, 1)
+grad_rr_kernel(const double* __restrict__ Arm, int64_t d, int64_t npanels, const double* __restrict__ b,
+               const double* __restrict__ X, double* __restrict__ work) {
+    extern __shared__ __align__(128) double sm[];
+    const int64_t stage = (int64_t)RR * d;
+    double* panel = sm;
+    uint64_t* full = reinterpret_cast<uint64_t*>(panel + NS * stage);
+    uint64_t* empty = full + NS;
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    if (t == 0) {
+        for (int s = 0; s < NS; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], RW);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const uint32_t stage_bytes = (uint32_t)(stage * sizeof(double));
+    // prologue: the first NS panels
+    if (t == 0) {
+        int64_t p = blockIdx.x;
+        for (int k = 0; k < NS && p < npanels; ++k, p += gridDim.x) {
+            mbar_expect_tx(&full[k], stage_bytes);
+            bulk_load(panel + k * stage, Arm + p * stage, stage_bytes, &full[k]);
+        }
+    }
+    {
+        // ---------------- consumers
+        double2 xr[NRHS][KP];
+#pragma unroll
+        for (int q = 0; q < NRHS; ++q)
+#pragma unroll
+            for (int k = 0; k < KP; ++k) {
+                const int64_t j = 2 * lane + 64 * k;
+                xr[q][k] = j < d ? make_double2(X[q * d + j], X[q * d + j + 1]) : make_double2(0.0, 0.0);
+            }
+        double2 g[NRHS][KP];
+#pragma unroll
+        for (int q = 0; q < NRHS; ++q)
+#pragma unroll
+            for (int k = 0; k < KP; ++k) g[q][k] = make_double2(0.0, 0.0);
+        int s = 0;
+        uint32_t ph = 0;
+        for (int64_t p = blockIdx.x; p < npanels; p += gridDim.x) {
+            mbar_wait(&full[s], ph);
+            const double* P = panel + s * stage;
+#pragma unroll 1
+            for (int rr = 0; rr < RR / RW; ++rr) {
+                const int row = warp + RW * rr;
+                const double bi = __ldg(b + p * RR + row);
+                double2 a[KP];
+#pragma unroll
+                for (int k = 0; k < KP; ++k) {
+                    const int64_t j = 2 * lane + 64 * k;
+                    a[k] = j < d ? *reinterpret_cast<const double2*>(P + row * d + j) : make_double2(0.0, 0.0);
+                }
+                double r[NRHS];
+#pragma unroll
+                for (int q = 0; q < NRHS; ++q) {
+                    double acc = 0.0;
+#pragma unroll
+                    for (int k = 0; k < KP; ++k) {
+                        acc = fma(a[k].x, xr[q][k].x, acc);
+                        acc = fma(a[k].y, xr[q][k].y, acc);
+                    }
+#pragma unroll
+                    for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+                    r[q] = acc - bi;
+                }
+#pragma unroll
+                for (int q = 0; q < NRHS; ++q)
+#pragma unroll
+                    for (int k = 0; k < KP; ++k) {
+                        g[q][k].x = fma(a[k].x, r[q], g[q][k].x);
+                        g[q][k].y = fma(a[k].y, r[q], g[q][k].y);
+                    }
+            }
+            __syncwarp();
+            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[s])) : "memory");
+            if (t == 0) {
+                // producer: refill stage s with panel p + NS*grid once every warp released it
+                const int64_t pn = p + (int64_t)NS * gridDim.x;
+                if (pn < npanels) {
+                    mbar_wait(&empty[s], ph);
+                    mbar_expect_tx(&full[s], stage_bytes);
+                    bulk_load(panel + s * stage, Arm + pn * stage, stage_bytes, &full[s]);
+                }
+            }
+            if (++s == NS) {
+                s = 0;
+                ph ^= 1u;
+            }
+        }
+        // per-warp partials -> shared [warp][q][d] (the ring is free once every warp is here)
+        __syncthreads();
+        double* red = panel;
+#pragma unroll
+        for (int q = 0; q < NRHS; ++q)
+#pragma unroll
+            for (int k = 0; k < KP; ++k) {
+                const int64_t j = 2 * lane + 64 * k;
+                if (j < d) *reinterpret_cast<double2*>(red + ((int64_t)warp * NRHS + q) * d + j) = g[q][k];
+            }
+        __syncthreads();
+        for (int64_t e = t; e < NRHS * d; e += 32 * RW) {
+            const int64_t q = e / d, j = e % d;
+            double sum = 0.0;
+#pragma unroll
+            for (int w = 0; w < RW; ++w) sum += red[((int64_t)w * NRHS + q) * d + j];
+            work[((int64_t)blockIdx.x * NRHS + q) * d + j] = sum;
+        }
+    }
+}
+
+template <int NRHS, int KP, int RR, int NS>
+void launch_rr(const GradPlan& p, const double* Arm, const double* b, const double* X, double* work, cudaStream_t st) {
+    const size_t smem = grad_rr_smem(p.d, RR, NS);
+    static bool attr = false;
+    if (!attr) {
+        CUDA_CHECK(cudaFuncSetAttribute(grad_rr_kernel<NRHS, KP, RR, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        227 * 1024));
+        attr = true;
+    }
+    LAUNCH((grad_rr_kernel<NRHS, KP, RR, NS>), p.grid, RTHREADS, smem, st, Arm, p.d, p.lda / RR, b, X, work);
+}
+
 template <int NRHS, int RR, int NS>
 void launch_rm(const GradPlan& p, const double* Arm, const double* b, const double* X, double* work, cudaStream_t st) {
     const size_t smem = grad_rm_smem(p.d, RR, NRHS, NS);
@@ -208,6 +350,45 @@ void launch_rm(const GradPlan& p, const double* Arm, const double* b, const doub
 size_t grad_rm_smem(int64_t d, int R, int nrhs, int ns) {
     return sizeof(double) * ((size_t)ns * R * d + (size_t)nrhs * d + (size_t)TW * nrhs + (size_t)nrhs * R + 2) +
            (size_t)ns * 8 + 128;
+}
+
+size_t grad_rr_smem(int64_t d, int R, int ns) {
+    const size_t red = (size_t)RW * 2 * d * sizeof(double);
+    return std::max((size_t)ns * R * d * sizeof(double), red) + (size_t)2 * ns * 8 + 128;
+}
+
+// v5 geometry: d <= 512 (even), 16-row panels (8-row when 16 do not fit), as many stages as fit 200 KiB (<= 6)
+bool grad_rr_geometry(int64_t d, int64_t lda, int* R, int* ns) {
+    if (d > 512 || d % 2 || d < 2) return false;
+    for (int r : {16, 8}) {
+        if (lda % r) continue;
+        int k = 6;
+        while (k >= 2 && grad_rr_smem(d, r, k) > 200u * 1024) --k;
+        if (k >= 2) {
+            *R = r;
+            *ns = k;
+            return true;
+        }
+    }
+    return false;
+}
+
+void grad_rr_run(const GradPlan& p, const double* Arm, const double* b, const double* X, int nrhs, double* work,
+                 cudaStream_t st) {
+    const int kp = (int)ceil_div(p.d, 64);
+    const int kpc = kp <= 2 ? 2 : kp <= 4 ? 4 : 8;
+#define IHS_RR(KPv, RRv, NSv)                                                                     \
+    if (kpc == KPv && p.R == RRv && p.stages == NSv) {                                            \
+        if (nrhs == 1) launch_rr<1, KPv, RRv, NSv>(p, Arm, b, X, work, st);                        \
+        else launch_rr<2, KPv, RRv, NSv>(p, Arm, b, X, work, st);                                  \
+        return;                                                                                    \
+    }
+#define IHS_RR_NS(KPv, RRv) IHS_RR(KPv, RRv, 2) IHS_RR(KPv, RRv, 3) IHS_RR(KPv, RRv, 4) IHS_RR(KPv, RRv, 5) IHS_RR(KPv, RRv, 6)
+    IHS_RR_NS(2, 16) IHS_RR_NS(4, 16) IHS_RR_NS(8, 16)
+    IHS_RR_NS(2, 8) IHS_RR_NS(4, 8) IHS_RR_NS(8, 8)
+#undef IHS_RR_NS
+#undef IHS_RR
+    fail(IHS_INTERNAL_ERROR, "gradient (register rows): no kernel for the chosen geometry");
 }
 
 // panel rows / ring depth for the row-major kernel: 64 KiB contiguous panels

@@ -361,12 +361,23 @@ bool grad_plan_use_rowmajor(GradPlan& p) {
         const char* e = std::getenv("IHS_GRAD_NO_ROWMAJOR");
         return e && e[0] == '1';
     }();
+    static const bool no_rr = [] {
+        const char* e = std::getenv("IHS_GRAD_NO_RR");
+        return e && e[0] == '1';
+    }();
     int R = 0, ns = 0;
-    if (disabled || !grad_rm_geometry(p.d, p.lda, &R, &ns)) return false;
-    p.version = 4;
+    if (disabled) return false;
+    if (!no_rr && grad_rr_geometry(p.d, p.lda, &R, &ns)) {
+        p.version = 5;
+        p.smem = grad_rr_smem(p.d, R, ns);
+    } else if (grad_rm_geometry(p.d, p.lda, &R, &ns)) {
+        p.version = 4;
+        p.smem = grad_rm_smem(p.d, R, 2, ns);
+    } else {
+        return false;
+    }
     p.R = R;
     p.stages = ns;
-    p.smem = grad_rm_smem(p.d, R, 2, ns);
     const int64_t npanels = p.lda / R;
     p.grid = (int)std::max<int64_t>(1, std::min<int64_t>(npanels, (int64_t)p.grid_sms));
     return true;
@@ -386,7 +397,8 @@ void grad_plan_attach_tma(GradPlan& p, const double* d_A) {
 void grad_run(const GradPlan& p, const double* d_A, const double* d_b, double nu2, const double* d_X, int nrhs,
               double* d_G, double* d_work, cudaStream_t st, const double* d_Arm) {
     if (p.version >= 2) {
-        if (p.version == 4) grad_rm_run(p, d_Arm, d_b, d_X, nrhs, d_work, st);
+        if (p.version == 5) grad_rr_run(p, d_Arm, d_b, d_X, nrhs, d_work, st);
+        else if (p.version == 4) grad_rm_run(p, d_Arm, d_b, d_X, nrhs, d_work, st);
         else if (p.version == 3) grad_tma_run(p, d_b, d_X, nrhs, d_work, st);
         else if (nrhs == 1) launch_v2_dispatch<1>(p, d_A, d_b, d_X, d_work, st);
         else launch_v2_dispatch<2>(p, d_A, d_b, d_X, d_work, st);
