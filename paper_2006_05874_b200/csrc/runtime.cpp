@@ -342,11 +342,11 @@ void device_sketch(ihs_gpu_problem* P, int kind, int64_t m, uint64_t seed, doubl
                 std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t_rng).count();
             upload_entries(P);
             unsigned long long* ctl = srht_prepare_scratch(P, plan);
-            P->timer->mark(PH_SKETCH_KERNEL);
+            if (P->timer) P->timer->mark(PH_SKETCH_KERNEL);
             srht_run_device(plan, P->A.d(), P->signbits.as<uint32_t>(), P->entries.as<int2>(), P->tiles.as<int4>(),
                             (int)P->h_tiles.size(), P->T.d(), d_SA, st, ctl, P->num_sms,
                             P->mask_valid ? P->srht_mask.as<uint32_t>() : nullptr);
-            P->timer->mark(PH_SKETCH);
+            if (P->timer) P->timer->mark(PH_SKETCH);
         } else {
             // shard p holds rows [p*n_loc, (p+1)*n_loc) of the padded index space
             const int64_t n_loc = plan.n_pad / shards;
@@ -404,10 +404,10 @@ void device_sketch(ihs_gpu_problem* P, int kind, int64_t m, uint64_t seed, doubl
         // SA = S * A on the DMMA path (sketch.hpp:68)
         const int splitk = dgemm_pick_splitk(m, d, n, P->num_sms);
         if (splitk > 1) P->gemm_work.ensure((size_t)splitk * m * d * sizeof(double));
-        P->timer->mark(PH_SKETCH_KERNEL);
+        if (P->timer) P->timer->mark(PH_SKETCH_KERNEL);
         dgemm(false, false, m, d, n, 1.0, P->S.d(), m, P->A.d(), P->lda, 0.0, d_SA, m, false, splitk,
               splitk > 1 ? P->gemm_work.d() : nullptr, st);
-        P->timer->mark(PH_SKETCH);
+        if (P->timer) P->timer->mark(PH_SKETCH);
         if (world > 1) nccl_allreduce_sum(d_SA, (size_t)(m * d), P->opts.nccl_comm, st);
         if (c) c->sketch += (uint64_t)m * (uint64_t)n_glob * (uint64_t)d;  // sketch.hpp:65-67
     } else {
