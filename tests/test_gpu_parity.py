@@ -116,8 +116,9 @@ def test_srht_counter_formula(gpu):
     assert c256.sketch == fw + 2 * 1000 + 2 * 256
 
 
+# the last two go through the 128x128 cp.async GEMM (split-K, ragged M/N/K edges)
 @pytest.mark.parametrize("n,d,m,seed", [(10, 3, 4, 7), (12, 5, 6, 123), (500, 17, 33, 1), (4096, 64, 256, 2),
-                                        (20000, 40, 130, 3)])
+                                        (20000, 40, 130, 3), (8192, 130, 256, 4), (5003, 200, 300, 5)])
 def test_gaussian_sketch(gpu, O, n, d, m, seed):
     A = rand_mat(seed, n, d)
     c = gpu.CostCounters()
@@ -147,7 +148,8 @@ def test_gradient_known_answer(gpu):
     assert c.matvec == 2 * 2 * 2 + 2 + 2 * 2  # test_problem.cpp:74-78
 
 
-@pytest.mark.parametrize("n,d", [(100, 3), (4096, 64), (65536 + 7, 130), (20000, 1000)])
+# d <= 512 even: register-row kernel; odd or wider d: panel kernels
+@pytest.mark.parametrize("n,d", [(100, 3), (4096, 64), (65536 + 7, 130), (20000, 1000), (3000, 77), (70000, 512)])
 def test_gradient_vs_oracle(gpu, O, n, d):
     A = rand_mat(n, n, d)
     b = RNG(1).standard_normal(n)
