@@ -171,10 +171,15 @@ void gemv_n(const double* A, int64_t M, int64_t N, int64_t lda, const double* x,
             int64_t ldy, cudaStream_t st);
 void woodbury_finish(const double* SA, int64_t m, int64_t d, const double* g, const double* w, double nu2, int nrhs,
                      double* z, cudaStream_t st);
-// tiled y = A x (64x64 CTA tiles, fixed-order chunk reduction); work: gemv_tiled_work_doubles
+// tiled y = A x (64x64 CTA tiles, fixed-order chunk reduction by the last CTA
+// of each row block, one launch); work: gemv_tiled_work_doubles, whose counter
+// tail must be zeroed once by gemv_tiled_reset before the first use
 size_t gemv_tiled_work_doubles(int64_t M, int64_t N);
 void gemv_tiled(const double* A, int64_t M, int64_t N, int64_t lda, const double* x, int nrhs, int64_t ldx, double* y,
                 int64_t ldy, double* work, cudaStream_t st);
+void gemv_tiled_reset(double* work, int64_t M, int64_t N, cudaStream_t st);
+// Wl = lower triangle of W (upper zeroed), k x k
+void tril_copy(const double* W, int64_t k, double* Wl, cudaStream_t st);
 void add_diag(double* H, int64_t n, double v, cudaStream_t st);
 void add_scaled(double* y, const double* x, double a, int64_t n, cudaStream_t st);  // y = y + a x
 void check_finite(const double* v, int64_t count, int* d_flag, cudaStream_t st);

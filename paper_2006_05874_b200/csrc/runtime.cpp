@@ -224,6 +224,8 @@ struct ihs_gpu_system {
     DevBuf SA;    // m x d
     DevBuf L;     // k x k Cholesky factor (k = m or d), lower
     DevBuf W;     // L^{-1} (lower) with L^{-T} mirrored into the strict upper triangle
+    DevBuf Hinv;  // direct-Gram path: H_S^{-1} = L^{-T} L^{-1} (k x k), one mat-vec per solve
+    DevBuf gv;    // gemv_tiled partials + arrival counters
     DevBuf inv_tmp;
     DevBuf work;  // split-K workspace
     DevBuf tmp;   // solve scratch
@@ -450,13 +452,25 @@ void system_factorize(ihs_gpu_system* S, ihs_counters* c) {
     S->W.ensure((size_t)k * k * sizeof(double));
     S->inv_tmp.ensure((size_t)hk * hk * sizeof(double));
     cholesky_invert(S->L.d(), k, S->W.d(), S->inv_tmp.d(), st);
+    if (S->kind == IHS_FACTOR_DIRECT_GRAM) {
+        // H_S^{-1} = (L^{-1})^T L^{-1} explicitly (DMMA, k^3 flop once per factorization): every solve
+        // is then a single symmetric mat-vec instead of two dependent triangular ones
+        S->Hinv.ensure((size_t)k * k * sizeof(double));
+        tril_copy(S->W.d(), k, S->L.d(), st);  // the factor itself is not needed after the inverse
+        const int splitk = dgemm_pick_splitk(k, k, k, S->num_sms);
+        if (splitk > 1) S->work.ensure((size_t)splitk * k * k * sizeof(double));
+        dgemm(true, false, k, k, k, 1.0, S->L.d(), k, S->L.d(), k, 0.0, S->Hinv.d(), k, false, splitk,
+              splitk > 1 ? S->work.d() : nullptr, st);
+    }
+    const int64_t gm = S->kind == IHS_FACTOR_DIRECT_GRAM ? d : m;
+    S->gv.ensure(gemv_tiled_work_doubles(gm, d) * sizeof(double));
+    gemv_tiled_reset(S->gv.d(), gm, d, st);
     int h_info[2] = {0, 0};
     CUDA_CHECK(cudaMemcpyAsync(h_info, S->info.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
     CUDA_CHECK(cudaStreamSynchronize(st));
     if (h_info[1]) fail(IHS_INVALID_INPUT, "SketchedSystem: non-finite sketched matrix");
     if (h_info[0]) fail(IHS_NUMERICAL_BREAKDOWN, "SketchedSystem: Cholesky factorization failed");
-    S->tmp.ensure((size_t)(4 * std::max(m, d) + std::max(cholesky_solve_work_doubles(k), gemv_tiled_work_doubles(m, d))) *
-                  sizeof(double));
+    S->tmp.ensure((size_t)(4 * std::max(m, d) + cholesky_solve_work_doubles(k)) * sizeof(double));
     if (c) c->factor += S->factor_flops();
 }
 
@@ -468,11 +482,11 @@ void system_solve_dev(const ihs_gpu_system* S, const double* g, double* z, int n
     if (S->kind == IHS_FACTOR_WOODBURY_INNER) {
         double* u = S->tmp.d();      // nrhs x m : u = SA g
         double* w = u + 2 * m;       // nrhs x m : w = (SA SA^T + nu^2 I)^{-1} u
-        gemv_tiled(S->SA.d(), m, d, m, g, nrhs, d, u, m, work, st);
+        gemv_tiled(S->SA.d(), m, d, m, g, nrhs, d, u, m, S->gv.d(), st);
         cholesky_solve_inv(S->W.d(), m, u, w, nrhs, work, st);
         woodbury_finish(S->SA.d(), m, d, g, w, S->nu * S->nu, nrhs, z, st);
     } else {
-        cholesky_solve_inv(S->W.d(), d, g, z, nrhs, work, st);
+        gemv_tiled(S->Hinv.d(), d, d, d, g, nrhs, d, z, d, S->gv.d(), st);
     }
 }
 

@@ -71,15 +71,21 @@ __global__ void gemv_n_kernel(const double* __restrict__ A, int64_t M, int64_t N
 }
 
 // Tiled y = A x: CTA = 64 rows x 64 columns, 256 threads (64 rows x 4 column
-// interleaves of 16 columns); partials per column chunk, summed in order.
+// interleaves of 16 columns); partials per column chunk go to `part`; the last
+// CTA of each row block (per-row-block arrival counter) sums the chunks in
+// chunk order, so the result is deterministic and one launch suffices. The
+// counters are reset by that last CTA for the next launch.
 constexpr int GV_ROWS = 64, GV_COLS = 64;
-__global__ void __launch_bounds__(256) gemv_partial_kernel(const double* __restrict__ A, int64_t M, int64_t N,
-                                                           int64_t lda, const double* __restrict__ x, int nrhs,
-                                                           int64_t ldx, double* __restrict__ part) {
+__global__ void __launch_bounds__(256) gemv_tiled_kernel(const double* __restrict__ A, int64_t M, int64_t N,
+                                                         int64_t lda, const double* __restrict__ x, int nrhs,
+                                                         int64_t ldx, double* __restrict__ part,
+                                                         unsigned* __restrict__ arrivals, double* __restrict__ y,
+                                                         int64_t ldy) {
     const int64_t r0 = (int64_t)blockIdx.x * GV_ROWS, c0 = (int64_t)blockIdx.y * GV_COLS;
     const int64_t c1 = c0 + GV_COLS < N ? c0 + GV_COLS : N;
     __shared__ double xs[2][GV_COLS];
     __shared__ double red[4][2][GV_ROWS];
+    __shared__ unsigned last;
     for (int e = threadIdx.x; e < (int)(c1 - c0); e += blockDim.x)
         for (int q = 0; q < nrhs; ++q) xs[q][e] = x[q * ldx + c0 + e];
     __syncthreads();
@@ -100,17 +106,19 @@ __global__ void __launch_bounds__(256) gemv_partial_kernel(const double* __restr
     if (threadIdx.x < GV_ROWS && row < M)
         for (int q = 0; q < nrhs; ++q)
             part[((int64_t)blockIdx.y * nrhs + q) * M + row] = (red[0][q][r] + red[1][q][r]) + (red[2][q][r] + red[3][q][r]);
-}
-
-__global__ void gemv_reduce_kernel(const double* __restrict__ part, int64_t M, int nrhs, int nchunks,
-                                   double* __restrict__ y, int64_t ldy) {
-    const int64_t total = (int64_t)nrhs * M;
-    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t q = e / M, row = e % M;
-        double s = 0.0;
-        for (int c = 0; c < nchunks; ++c) s += part[((int64_t)c * nrhs + q) * M + row];
-        y[q * ldy + row] = s;
-    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(arrivals + blockIdx.x, 1u) == gridDim.y - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    if (threadIdx.x < GV_ROWS && row < M)
+        for (int q = 0; q < nrhs; ++q) {
+            double sum = 0.0;
+            for (unsigned c = 0; c < gridDim.y; ++c) sum += __ldcg(part + ((int64_t)c * nrhs + q) * M + row);
+            y[q * ldy + row] = sum;
+        }
+    if (threadIdx.x == 0) arrivals[blockIdx.x] = 0u;
 }
 
 // z[:,q] = (g[:,q] - SA^T w[:,q]) / nu2 ; one warp per column of SA
@@ -170,14 +178,34 @@ void gemv_n(const double* A, int64_t M, int64_t N, int64_t lda, const double* x,
     LAUNCH(gemv_n_kernel, blocks_for(M, 128), 128, 0, st, A, M, N, lda, x, nrhs, ldx, y, ldy);
 }
 
-size_t gemv_tiled_work_doubles(int64_t M, int64_t N) { return (size_t)ceil_div(N, GV_COLS) * 2 * (size_t)M; }
+// partials (nchunks x 2 x M) followed by the per-row-block arrival counters
+// (zeroed here once; the kernel leaves them zero)
+size_t gemv_tiled_work_doubles(int64_t M, int64_t N) {
+    return (size_t)ceil_div(N, GV_COLS) * 2 * (size_t)M + (size_t)ceil_div(M, GV_ROWS) + 8;
+}
 
 void gemv_tiled(const double* A, int64_t M, int64_t N, int64_t lda, const double* x, int nrhs, int64_t ldx, double* y,
                 int64_t ldy, double* work, cudaStream_t st) {
     dim3 grid((unsigned)ceil_div(M, GV_ROWS), (unsigned)ceil_div(N, GV_COLS));
-    LAUNCH(gemv_partial_kernel, grid, 256, 0, st, A, M, N, lda, x, nrhs, ldx, work);
-    LAUNCH(gemv_reduce_kernel, blocks_for((int64_t)nrhs * M, 256, 1024), 256, 0, st, work, M, nrhs, (int)grid.y, y,
-           ldy);
+    unsigned* arrivals = reinterpret_cast<unsigned*>(work + (size_t)grid.y * 2 * (size_t)M);
+    LAUNCH(gemv_tiled_kernel, grid, 256, 0, st, A, M, N, lda, x, nrhs, ldx, work, arrivals, y, ldy);
+}
+
+void gemv_tiled_reset(double* work, int64_t M, int64_t N, cudaStream_t st) {
+    const size_t off = (size_t)ceil_div(N, GV_COLS) * 2 * (size_t)M;
+    CUDA_CHECK(cudaMemsetAsync(work + off, 0, (size_t)ceil_div(M, GV_ROWS) * sizeof(double), st));
+}
+
+__global__ void tril_copy_kernel(const double* __restrict__ W, int64_t k, double* __restrict__ Wl) {
+    const int64_t total = k * k;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = e % k, j = e / k;
+        Wl[e] = i >= j ? W[e] : 0.0;
+    }
+}
+
+void tril_copy(const double* W, int64_t k, double* Wl, cudaStream_t st) {
+    LAUNCH(tril_copy_kernel, blocks_for(k * k, 256), 256, 0, st, W, k, Wl);
 }
 
 void woodbury_finish(const double* SA, int64_t m, int64_t d, const double* g, const double* w, double nu2, int nrhs,
