@@ -269,9 +269,14 @@ struct ihs_gpu_problem {
     std::vector<int2> h_entries;
     std::vector<int4> h_tiles;
     // solver vectors
-    DevBuf vecs;                 // 12 * d doubles
-    DevBuf dots;                 // 4 doubles
+    DevBuf vecs;                 // 28 * d doubles (start state + four candidate-evaluation sets)
+    DevBuf dots;                 // 24 doubles (4 per evaluation set + first/resketch decrements)
     PinnedBuf h_dots;
+    cudaEvent_t set_ev[4] = {nullptr, nullptr, nullptr, nullptr};  // evaluation-set completion events
+    ~ihs_gpu_problem() {
+        for (auto e : set_ev)
+            if (e) cudaEventDestroy(e);
+    }
     std::unique_ptr<PhaseTimer> timer;
 };
 
@@ -732,9 +737,10 @@ ihs_status ihs_gpu_problem_create(const double* A, int64_t n, int64_t d, int64_t
             }
         }
         P->grad_work.ensure(grad_work_doubles(P->gplan) * sizeof(double));
-        P->vecs.ensure((size_t)16 * d * sizeof(double));
-        P->dots.ensure(8 * sizeof(double));
-        P->h_dots.ensure(8 * sizeof(double));
+        P->vecs.ensure((size_t)28 * d * sizeof(double));
+        P->dots.ensure(24 * sizeof(double));
+        P->h_dots.ensure(24 * sizeof(double));
+        for (auto& e : P->set_ev) CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         P->timer = std::make_unique<PhaseTimer>(P->st);
         CUDA_CHECK(cudaStreamSynchronize(P->st));
         *out = P.release();
@@ -1051,19 +1057,32 @@ ihs_status ihs_gpu_adaptive_solve(ihs_gpu_problem* P, const ihs_solver_config* c
             tm.mark(PH_END);
         };
 
-        // device vectors: x, xprev, g, gt (current), X2 = [xp; xg], G2, GT2 (candidates)
-        P->vecs.ensure((size_t)16 * dim * sizeof(double));
+        // Device vectors. x0/xprev0/g0/gt0 hold the starting state; candidate evaluations rotate over
+        // four sets {X2 = [x_polyak; x_gd], G2, GT2, dots}, and the accepted state is a set of pointers
+        // into them (no copies on accept). While the evaluation in set c is decided, the live sets are
+        // c-2 (x_{t-1}), c-1 (x_t), c and the speculative evaluation's c+1, so a ring of four never
+        // overwrites live data whatever the decision (accept, or re-sketch with the state unchanged).
+        constexpr int NSETS = 4;
+        P->vecs.ensure((size_t)(4 + 6 * NSETS) * dim * sizeof(double));
         double* base = P->vecs.d();
         double* xcur = base + 0 * dim;
         double* xprev = base + 1 * dim;
         double* g = base + 2 * dim;
         double* gt = base + 3 * dim;
-        double* X2 = base + 4 * dim;   // 2 x dim: [Polyak cand ; gradient cand]
-        double* G2 = base + 6 * dim;   // 2 x dim
-        double* GT2 = base + 8 * dim;  // 2 x dim
-        double* spare = base + 10 * dim;  // 2 x dim
-        double* dots = P->dots.d();
-        double* hd = static_cast<double*>(P->h_dots.p);
+        struct EvalSet {
+            double *X2, *G2, *GT2, *dots, *hd;
+            cudaEvent_t ev;
+            bool polyak;  // both candidates evaluated
+        } sets[NSETS];
+        P->dots.ensure(24 * sizeof(double));
+        P->h_dots.ensure(24 * sizeof(double));
+        double* dots = P->dots.d() + 4 * NSETS;  // first evaluation / resketch decrements
+        double* hd = static_cast<double*>(P->h_dots.p) + 4 * NSETS;
+        for (int k = 0; k < NSETS; ++k) {
+            double* sb = base + (4 + 6 * k) * dim;
+            sets[k] = EvalSet{sb, sb + 2 * dim, sb + 4 * dim, P->dots.d() + 4 * k,
+                              static_cast<double*>(P->h_dots.p) + 4 * k, P->set_ev[k], false};
+        }
 
         auto decrement = [&](double dotv, double sq) -> double {  // sketched_system.hpp:95-101
             const double r = 0.5 * dotv;
@@ -1104,67 +1123,111 @@ ihs_status ihs_gpu_adaptive_solve(ihs_gpu_problem* P, const ihs_solver_config* c
         bool checks_enabled = true;
         bool exhausted = false;
 
-        // candidate state: which slot of X2/G2/GT2 holds a valid evaluated candidate
-        auto accept = [&](int slot, double rc, int kind) {  // :167-178
-            const double r_prev = r;
-            // rotate buffers: xprev <- xcur <- cand ; g, gt <- cand's
-            std::swap(xprev, xcur);  // old xcur becomes xprev (pointer swap)
-            CUDA_CHECK(cudaMemcpyAsync(xcur, X2 + slot * dim, (size_t)dim * 8, cudaMemcpyDeviceToDevice, st));
-            CUDA_CHECK(cudaMemcpyAsync(g, G2 + slot * dim, (size_t)dim * 8, cudaMemcpyDeviceToDevice, st));
-            CUDA_CHECK(cudaMemcpyAsync(gt, GT2 + slot * dim, (size_t)dim * 8, cudaMemcpyDeviceToDevice, st));
-            r = rc;
-            ++t;
-            log.push_back({t, m, r, r_prev, kind, 0});
-            push_iterate(xcur);
-            converged = r <= cfg->eps * r1;
-        };
-
-        while (!converged && t < cfg->max_iters) {  // :180
-            const bool want_polyak = checks_enabled && cfg->mode == IHS_MODE_POLYAK_THEN_GRADIENT;
-            // Build both candidates from the same (x, x_prev, g~) and evaluate them in one
-            // pass over A (2 RHS): the gradient candidate does not depend on the Polyak
-            // outcome (:182, :190). Counters charge only what the reference evaluates.
+        // Enqueue the evaluation of both heavy-ball candidates of state (x, x_prev, g~) into set k:
+        // built from the same state and evaluated in one pass over A (2 RHS), since the gradient
+        // candidate does not depend on the Polyak outcome (:182, :190). The decrement dot products
+        // are copied to the set's pinned slot and its event recorded; counters are charged only
+        // when the host consumes an evaluation the reference performs.
+        auto enqueue_eval = [&](int k, const double* x, const double* xp, const double* gtv, bool polyak) {
+            EvalSet& S = sets[k];
             tm.mark(PH_GRAD);
-            candidates(xcur, xprev, gt, tp.mu_p, tp.beta_p, tp.mu_gd, dim, want_polyak ? X2 : nullptr, X2 + dim, st);
-            const int nr = want_polyak ? 2 : 1;
-            const double* Xe = want_polyak ? X2 : X2 + dim;
-            double* Ge = want_polyak ? G2 : G2 + dim;
-            double* GTe = want_polyak ? GT2 : GT2 + dim;
+            candidates(x, xp, gtv, tp.mu_p, tp.beta_p, tp.mu_gd, dim, polyak ? S.X2 : nullptr, S.X2 + dim, st);
+            const int nr = polyak ? 2 : 1;
+            const double* Xe = polyak ? S.X2 : S.X2 + dim;
+            double* Ge = polyak ? S.G2 : S.G2 + dim;
+            double* GTe = polyak ? S.GT2 : S.GT2 + dim;
             problem_grad(P, Xe, nr, Ge);
             PT.n_gradient++;
             PT.gradient_bytes += grad_pass_bytes;
             PT.n_solve += nr;
             tm.mark(PH_SOLVE);
             system_solve_dev(&sys, Ge, GTe, nr);
-            decrement_dots(Ge, GTe, dim, nr, dots, st);
+            decrement_dots(Ge, GTe, dim, nr, S.dots, st);
             tm.mark(PH_END);
-            CUDA_CHECK(cudaMemcpyAsync(hd, dots, (size_t)2 * nr * sizeof(double), cudaMemcpyDeviceToHost, st));
-            CUDA_CHECK(cudaStreamSynchronize(st));
+            CUDA_CHECK(cudaMemcpyAsync(S.hd, S.dots, (size_t)2 * nr * sizeof(double), cudaMemcpyDeviceToHost, st));
+            CUDA_CHECK(cudaEventRecord(S.ev, st));
+            S.polyak = polyak;
+        };
+        // Speculation: while the host waits for evaluation t, the evaluation of t+1 under the predicted
+        // outcome (the previous accepted candidate kind) is already queued, hiding the host round trip.
+        // Only for cheap passes over A (a wasted evaluation costs one pass) and only after an accept.
+        const bool cheap_pass = grad_pass_bytes < (double)(1ll << 30);
+        int cur = 0;        // set holding the evaluation for the current state
+        int spec = -1;      // set holding a speculative evaluation (or -1)
+        int spec_slot = -1; // candidate slot the speculation assumed accepted
+        int last_kind = -1; // kind of the last accepted step
+        const bool polyak_mode = cfg->mode == IHS_MODE_POLYAK_THEN_GRADIENT;
+        if (!converged && t < cfg->max_iters) enqueue_eval(cur, xcur, xprev, gt, checks_enabled && polyak_mode);
+
+        auto accept = [&](int slot, double rc, int kind) {  // :167-178
+            const double r_prev = r;
+            EvalSet& S = sets[cur];
+            xprev = xcur;
+            xcur = S.X2 + slot * dim;
+            g = S.G2 + slot * dim;
+            gt = S.GT2 + slot * dim;
+            r = rc;
+            ++t;
+            log.push_back({t, m, r, r_prev, kind, 0});
+            push_iterate(xcur);
+            converged = r <= cfg->eps * r1;
+            last_kind = kind;
+        };
+        // after the current state changed: use the speculation if it matches, else evaluate anew
+        auto next_eval = [&](int accepted_slot) {
+            const int nxt = (cur + 1) % NSETS;
+            const bool polyak = checks_enabled && polyak_mode;
+            if (spec >= 0 && accepted_slot == spec_slot && sets[spec].polyak == polyak) {
+                cur = spec;
+            } else {
+                cur = nxt;
+                if (!converged && t < cfg->max_iters) enqueue_eval(cur, xcur, xprev, gt, polyak);
+            }
+            spec = -1;
+        };
+
+        while (!converged && t < cfg->max_iters) {  // :180
+            const bool want_polyak = checks_enabled && polyak_mode;
+            EvalSet& S = sets[cur];
+            // speculate the next evaluation before blocking on this one
+            if (cheap_pass && last_kind >= 0 && t + 1 < cfg->max_iters) {
+                spec_slot = (last_kind == IHS_STEP_POLYAK && S.polyak) ? 0 : 1;
+                spec = (cur + 1) % NSETS;
+                enqueue_eval(spec, S.X2 + spec_slot * dim, xcur, S.GT2 + spec_slot * dim, want_polyak);
+            }
+            CUDA_CHECK(cudaEventSynchronize(S.ev));
+            const double* hv = S.hd;
             const uint64_t grad_cost = 2 * (uint64_t)n_rows * (uint64_t)dim + (uint64_t)n_rows + 2 * (uint64_t)dim;
             if (want_polyak) {
                 C.matvec += grad_cost;
                 C.solve += sys.flops_per_solve();
-                const double rp = decrement(hd[0], hd[1]);
+                const double rp = decrement(hv[0], hv[1]);
                 const double ratio = std::pow(rp / r1, 1.0 / static_cast<double>(t));  // :183
                 if (ratio <= tp.c_p || rp <= cfg->eps * r1) {
                     accept(0, rp, IHS_STEP_POLYAK);
+                    next_eval(0);
                     continue;
                 }
             }
             C.matvec += grad_cost;
             C.solve += sys.flops_per_solve();
-            const double rg = want_polyak ? decrement(hd[2], hd[3]) : decrement(hd[0], hd[1]);
+            const double rg = want_polyak ? decrement(hv[2], hv[3]) : decrement(hv[0], hv[1]);
             const bool pass = checks_enabled ? (rg <= tp.c_gd * r || rg <= cfg->eps * r1) : rg <= r;  // :191-193
             if (pass) {
                 accept(1, rg, IHS_STEP_GRADIENT);
+                next_eval(1);
                 continue;
             }
+            spec = -1;  // the state did not advance: any speculation is void
+            last_kind = -1;
             if (!checks_enabled) break;  // :198
             if (2 * m > cap) {           // :201-209
                 exhausted = true;
                 checks_enabled = false;
                 if (rg <= r) {
                     accept(1, rg, IHS_STEP_GRADIENT);
+                    last_kind = -1;
+                    next_eval(1);
                     continue;
                 }
                 break;
@@ -1187,8 +1250,10 @@ ihs_status ihs_gpu_adaptive_solve(ihs_gpu_problem* P, const ihs_solver_config* c
                 tm.mark(PH_END);
             }
             log.push_back({t, m, r, r_old, IHS_STEP_RESKETCH, 0});
+            // re-evaluate the current state under the new system, into the same set (its rejected
+            // candidates are dead; the speculation, if any, sits in the next set and is void)
+            if (!converged && t < cfg->max_iters) enqueue_eval(cur, xcur, xprev, gt, checks_enabled && polyak_mode);
         }
-        (void)spare;
 
         CUDA_CHECK(cudaMemcpyAsync(rep->x, xcur, (size_t)dim * 8, cudaMemcpyDeviceToHost, st));
         CUDA_CHECK(cudaEventRecord(ev_end, st));
