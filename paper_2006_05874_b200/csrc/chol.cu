@@ -18,6 +18,7 @@ namespace ihs_b200 {
 
 namespace {
 constexpr int NB = 64;
+constexpr int TRSM_WARPS = 8;  // rows (warps) per CTA of the panel solves
 
 // Unblocked LLT of the nb x nb diagonal block at (k,k), in shared memory.
 // 256 threads = 64 rows x 4 column groups; per column: every thread derives
@@ -56,9 +57,168 @@ __global__ void __launch_bounds__(256) potrf_diag_kernel(double* __restrict__ H,
         if (i < nb && i >= jj) H[(k + i) + (k + jj) * n] = (i == jj) ? diag[i] : a[i][jj];
 }
 
+// ---- diagonal block: LLT and its inverse in one CTA (4 warps)
+// 64 = 32 + 32 blocking: warp 0 factors a 32x32 block in registers (lane i
+// holds row i; column j's pivot and entries are broadcast by shuffles), the
+// four warps form L21 = A21 L11^{-T}, A22 -= L21 L21^T and X21 = -X22 L21 X11
+// as small shared-memory products, so the only sequential parts are the two
+// 32-column warp factorizations and inversions (no CTA barrier per column).
+constexpr int PB = 65;  // padded row stride of the 64x64 shared blocks
+
+// Warp-level LLT of the 32x32 block a[r0.., r0..] in place (compact loops:
+// a fully unrolled register version overflows the instruction cache). Per
+// column: broadcast pivot, lanes below scale their entry, then each lane
+// updates its row of the trailing block (the column entries it needs are
+// same-address broadcasts).
+__device__ __noinline__ void potrf32_warp(double (*a)[PB], int r0, int* info, int64_t kglob, int nvalid) {
+    const int lane = threadIdx.x & 31;
+    double* ar = &a[r0 + lane][r0];
+    for (int j = 0; j < 32; ++j) {
+        double dj = a[r0 + j][r0 + j];
+        if (!(dj > 0.0) || !isfinite(dj)) {
+            if (lane == 0 && r0 + j < nvalid) atomicCAS(info, 0, (int)(kglob + r0 + j + 1));
+            dj = 1.0;  // keep going with a harmless pivot; the result is flagged
+        }
+        const double ljj = sqrt(dj);
+        double lij = 0.0;
+        if (lane > j) {
+            lij = ar[j] / ljj;
+            ar[j] = lij;
+        }
+        __syncwarp();
+        if (lane == j) ar[j] = ljj;
+        if (lane > j)
+            for (int q = j + 1; q <= lane; ++q) ar[q] = fma(-lij, a[r0 + q][r0 + j], ar[q]);
+        __syncwarp();
+    }
+}
+
+// x[r0.., r0..] = inverse of the lower-triangular 32x32 block a[r0.., r0..]; lane = column
+__device__ __noinline__ void trtri32_warp(double (*a)[PB], double (*x)[PB], int r0) {
+    const int lane = threadIdx.x & 31;
+    for (int i = 0; i < 32; ++i) {
+        double s0 = (i == lane) ? 1.0 : 0.0, s1 = 0.0;
+        int q = lane;
+        for (; q + 1 < i; q += 2) {
+            s0 = fma(-a[r0 + i][r0 + q], x[r0 + q][r0 + lane], s0);
+            s1 = fma(-a[r0 + i][r0 + q + 1], x[r0 + q + 1][r0 + lane], s1);
+        }
+        if (q < i) s0 = fma(-a[r0 + i][r0 + q], x[r0 + q][r0 + lane], s0);
+        x[r0 + i][r0 + lane] = i < lane ? 0.0 : (s0 + s1) / a[r0 + i][r0 + i];
+        __syncwarp();
+    }
+}
+
+__global__ void __launch_bounds__(128) potrf_inv_diag_kernel(double* __restrict__ H, int64_t n, int64_t k, int nb,
+                                                             double* __restrict__ Xd, int* __restrict__ info) {
+    extern __shared__ double pi_smem[];
+    double(*a)[PB] = reinterpret_cast<double(*)[PB]>(pi_smem);
+    double(*x)[PB] = reinterpret_cast<double(*)[PB]>(pi_smem + 64 * PB);
+    double(*t)[PB] = reinterpret_cast<double(*)[PB]>(pi_smem + 128 * PB);  // 32 x 32 scratch
+    const int tid = threadIdx.x, warp = tid >> 5;
+    for (int e = tid; e < 64 * 64; e += 128) {
+        const int i = e & 63, j = e >> 6;
+        double v = 0.0;
+        if (i < nb && j < nb) v = i >= j ? H[(k + i) + (k + j) * n] : 0.0;
+        else if (i == j) v = 1.0;  // identity padding of a ragged last block
+        a[i][j] = v;
+        x[i][j] = 0.0;
+    }
+    __syncthreads();
+    if (warp == 0) {
+        potrf32_warp(a, 0, info, k, nb);
+        __syncwarp();
+        trtri32_warp(a, x, 0);
+    }
+    __syncthreads();
+    // L21[i][j] = sum_{q <= j} A21[i][q] X11[j][q]   (i, j < 32) -> t
+    for (int e = tid; e < 32 * 32; e += 128) {
+        const int i = e & 31, j = e >> 5;
+        double s = 0.0;
+        for (int q = 0; q <= j; ++q) s = fma(a[32 + i][q], x[j][q], s);
+        t[i][j] = s;
+    }
+    __syncthreads();
+    for (int e = tid; e < 32 * 32; e += 128) {
+        const int i = e & 31, j = e >> 5;
+        a[32 + i][j] = t[i][j];
+    }
+    __syncthreads();
+    // A22 -= L21 L21^T (lower)
+    for (int e = tid; e < 32 * 32; e += 128) {
+        const int i = e & 31, j = e >> 5;
+        if (i >= j) {
+            double s = 0.0;
+            for (int q = 0; q < 32; ++q) s = fma(a[32 + i][q], a[32 + j][q], s);
+            a[32 + i][32 + j] -= s;
+        }
+    }
+    __syncthreads();
+    if (warp == 0) {
+        potrf32_warp(a, 32, info, k, nb);
+        __syncwarp();
+        trtri32_warp(a, x, 32);
+    }
+    __syncthreads();
+    // X21 = -X22 (L21 X11): T = L21 X11 (X11 lower: q >= j), then X21 = -X22 T (X22 lower: q <= i)
+    for (int e = tid; e < 32 * 32; e += 128) {
+        const int i = e & 31, j = e >> 5;
+        double s = 0.0;
+        for (int q = j; q < 32; ++q) s = fma(a[32 + i][q], x[q][j], s);
+        t[i][j] = s;
+    }
+    __syncthreads();
+    for (int e = tid; e < 32 * 32; e += 128) {
+        const int i = e & 31, j = e >> 5;
+        double s = 0.0;
+        for (int q = 0; q <= i; ++q) s = fma(x[32 + i][32 + q], t[q][j], s);
+        x[32 + i][j] = -s;
+    }
+    __syncthreads();
+    double* X = Xd + (k / 64) * 64 * 64;
+    for (int e = tid; e < 64 * 64; e += 128) {
+        const int i = e & 63, j = e >> 6;
+        if (i < nb && j < nb && i >= j) H[(k + i) + (k + j) * n] = a[i][j];
+        X[i + 64 * j] = x[i][j];  // column-major 64x64, zero above the diagonal
+    }
+}
+
+// L21 = A21 L11^{-T} with the block inverse X = L11^{-1} from potrf_inv_diag:
+// one warp per row, lane c produces columns c and c + 32 (no sequential chain).
+__global__ void __launch_bounds__(32 * TRSM_WARPS) trsm_inv_panel_kernel(double* __restrict__ H, int64_t n, int64_t k,
+                                                                         int nb, const double* __restrict__ Xd) {
+    __shared__ double xs[64][PB];
+    __shared__ double rowv[TRSM_WARPS][64];
+    const double* X = Xd + (k / 64) * 64 * 64;
+    for (int e = threadIdx.x; e < 64 * 64; e += blockDim.x) xs[e & 63][e >> 6] = X[e];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t row = k + nb + (int64_t)blockIdx.x * TRSM_WARPS + warp;
+    if (row < n) {
+        rowv[warp][lane] = lane < nb ? H[row + (k + lane) * n] : 0.0;
+        rowv[warp][lane + 32] = lane + 32 < nb ? H[row + (k + lane + 32) * n] : 0.0;
+    }
+    __syncthreads();
+    if (row >= n) return;
+    double s0 = 0.0, s1 = 0.0;
+    for (int q = 0; q <= lane; ++q) s0 = fma(rowv[warp][q], xs[lane][q], s0);
+    for (int q = 0; q <= lane + 32; ++q) s1 = fma(rowv[warp][q], xs[lane + 32][q], s1);
+    if (lane < nb) H[row + (k + lane) * n] = s0;
+    if (lane + 32 < nb) H[row + (k + lane + 32) * n] = s1;
+}
+
+// W's diagonal 64-blocks <- the block inverses computed during the factorization
+__global__ void place_diag_inv_kernel(const double* __restrict__ Xd, int64_t n, double* __restrict__ W) {
+    const int64_t k = (int64_t)blockIdx.x * 64;
+    const double* X = Xd + (int64_t)blockIdx.x * 64 * 64;
+    for (int e = threadIdx.x; e < 64 * 64; e += blockDim.x) {
+        const int i = e & 63, j = e >> 6;
+        if (k + i < n && k + j < n && i >= j) W[(k + i) + (k + j) * n] = X[e];
+    }
+}
+
+
 // L21 = A21 * L11^{-T}: one warp per row, lane c holds columns c and c+32 of
 // the row; column c is finished by its owner lane and broadcast by shuffle.
-constexpr int TRSM_WARPS = 8;
 __global__ void __launch_bounds__(32 * TRSM_WARPS) trsm_panel_kernel(double* __restrict__ H, int64_t n, int64_t k,
                                                                      int nb) {
     __shared__ double l[NB][NB + 1];
@@ -224,15 +384,19 @@ void tri_inv_rec(const double* L, double* W, int64_t n, int64_t n0, int64_t size
 }
 }  // namespace
 
-void cholesky_invert(const double* d_L, int64_t n, double* d_W, double* d_tmp, cudaStream_t st) {
+void cholesky_invert(const double* d_L, int64_t n, double* d_W, double* d_tmp, const double* d_Xd, cudaStream_t st) {
     CUDA_CHECK(cudaMemsetAsync(d_W, 0, (size_t)n * n * sizeof(double), st));
-    const size_t smem = (size_t)2 * NB * (NB + 1) * sizeof(double);
-    static bool attr = false;
-    if (!attr) {
-        CUDA_CHECK(cudaFuncSetAttribute(tri_inv_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = true;
+    if (d_Xd) {
+        LAUNCH(place_diag_inv_kernel, (unsigned)ceil_div(n, NB), 256, 0, st, d_Xd, n, d_W);
+    } else {
+        const size_t smem = (size_t)2 * NB * (NB + 1) * sizeof(double);
+        static bool attr = false;
+        if (!attr) {
+            CUDA_CHECK(cudaFuncSetAttribute(tri_inv_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            attr = true;
+        }
+        LAUNCH(tri_inv_diag_kernel, (unsigned)ceil_div(n, NB), 64, smem, st, d_L, n, d_W);
     }
-    LAUNCH(tri_inv_diag_kernel, (unsigned)ceil_div(n, NB), 64, smem, st, d_L, n, d_W);
     tri_inv_rec(d_L, d_W, n, 0, n, d_tmp, st);
     dim3 grid((unsigned)ceil_div(n, 32), (unsigned)ceil_div(n, 32));
     LAUNCH(mirror_upper_kernel, grid, dim3(32, 8), 0, st, d_W, n);
@@ -248,16 +412,28 @@ void cholesky_solve_inv(const double* d_W, int64_t n, const double* d_R, double*
     trmv(d_W, n, false, y, nrhs, d_Z, part, st);   // z = L^{-T} y
 }
 
-void cholesky_factor(double* d_H, int64_t n, double* d_work, int* d_info, int num_sms, cudaStream_t st) {
-    (void)d_work;
+size_t cholesky_diag_inv_doubles(int64_t n) { return (size_t)ceil_div(n, NB) * NB * NB; }
+
+void cholesky_factor(double* d_H, int64_t n, double* d_Xd, int* d_info, int num_sms, cudaStream_t st) {
     (void)num_sms;
     CUDA_CHECK(cudaMemsetAsync(d_info, 0, sizeof(int), st));
+    const size_t pi_smem = (size_t)(64 + 64 + 32) * PB * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+        CUDA_CHECK(cudaFuncSetAttribute(potrf_inv_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pi_smem));
+        attr = true;
+    }
     for (int64_t k = 0; k < n; k += NB) {
         const int nb = (int)std::min<int64_t>(NB, n - k);
-        LAUNCH(potrf_diag_kernel, 1, 256, 0, st, d_H, n, k, nb, d_info);
+        if (d_Xd) LAUNCH(potrf_inv_diag_kernel, 1, 128, pi_smem, st, d_H, n, k, nb, d_Xd, d_info);
+        else LAUNCH(potrf_diag_kernel, 1, 256, 0, st, d_H, n, k, nb, d_info);
         const int64_t rest = n - k - nb;
         if (rest > 0) {
-            LAUNCH(trsm_panel_kernel, (unsigned)ceil_div(rest, TRSM_WARPS), 32 * TRSM_WARPS, 0, st, d_H, n, k, nb);
+            if (d_Xd)
+                LAUNCH(trsm_inv_panel_kernel, (unsigned)ceil_div(rest, TRSM_WARPS), 32 * TRSM_WARPS, 0, st, d_H, n, k,
+                       nb, d_Xd);
+            else
+                LAUNCH(trsm_panel_kernel, (unsigned)ceil_div(rest, TRSM_WARPS), 32 * TRSM_WARPS, 0, st, d_H, n, k, nb);
             // A22 -= L21 L21^T (lower)
             double* L21 = d_H + (k + nb) + k * n;
             double* A22 = d_H + (k + nb) + (k + nb) * n;

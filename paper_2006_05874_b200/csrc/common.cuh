@@ -113,10 +113,13 @@ void dgemm(bool transA, bool transB, int64_t M, int64_t N, int64_t K, double alp
 int dgemm_pick_splitk(int64_t M, int64_t N, int64_t K, int num_sms);
 
 // chol.cu — blocked Cholesky (lower, in place). d_info: int (0 ok, j+1 = failed pivot).
-void cholesky_factor(double* d_H, int64_t n, double* d_work, int* d_info, int num_sms, cudaStream_t st);
+// d_Xd (cholesky_diag_inv_doubles(n), or nullptr for the column-serial kernels)
+// receives the inverses of the 64x64 diagonal blocks of L.
+size_t cholesky_diag_inv_doubles(int64_t n);
+void cholesky_factor(double* d_H, int64_t n, double* d_Xd, int* d_info, int num_sms, cudaStream_t st);
 // W = L^{-1} (lower) with W^T mirrored into the strict upper triangle;
-// d_tmp holds ceil(n/2)^2 doubles.
-void cholesky_invert(const double* d_L, int64_t n, double* d_W, double* d_tmp, cudaStream_t st);
+// d_tmp holds ceil(n/2)^2 doubles; d_Xd = the factorization's block inverses (or nullptr).
+void cholesky_invert(const double* d_L, int64_t n, double* d_W, double* d_tmp, const double* d_Xd, cudaStream_t st);
 size_t cholesky_solve_work_doubles(int64_t n);
 // Z = L^{-T} L^{-1} R for nrhs columns (ld = n), two parallel triangular mat-vecs
 void cholesky_solve_inv(const double* d_W, int64_t n, const double* d_R, double* d_Z, int nrhs, double* d_work,

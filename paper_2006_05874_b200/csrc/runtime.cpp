@@ -224,6 +224,7 @@ struct ihs_gpu_system {
     DevBuf SA;    // m x d
     DevBuf L;     // k x k Cholesky factor (k = m or d), lower
     DevBuf W;     // L^{-1} (lower) with L^{-T} mirrored into the strict upper triangle
+    DevBuf Xd;    // inverses of L's 64x64 diagonal blocks (from the factorization)
     DevBuf Hinv;  // direct-Gram path: H_S^{-1} = L^{-T} L^{-1} (k x k), one mat-vec per solve
     DevBuf gv;    // gemv_tiled partials + arrival counters
     DevBuf inv_tmp;
@@ -451,12 +452,22 @@ void system_factorize(ihs_gpu_system* S, ihs_counters* c) {
               splitk > 1 ? S->work.d() : nullptr, st);
     }
     add_diag(S->L.d(), k, nu2, st);
-    cholesky_factor(S->L.d(), k, nullptr, S->info.as<int>(), S->num_sms, st);
+    // IHS_CHOL_BLOCKINV=1: fused diagonal-block factor+inverse kernels (measured slower so far)
+    static const bool blockinv = [] {
+        const char* e = std::getenv("IHS_CHOL_BLOCKINV");
+        return e && e[0] == '1';
+    }();
+    double* Xd = nullptr;
+    if (blockinv) {
+        S->Xd.ensure(cholesky_diag_inv_doubles(k) * sizeof(double));
+        Xd = S->Xd.d();
+    }
+    cholesky_factor(S->L.d(), k, Xd, S->info.as<int>(), S->num_sms, st);
     // W = L^{-1} once per factorization; every later solve is two mat-vecs
     const int64_t hk = (k + 1) / 2 + 64;
     S->W.ensure((size_t)k * k * sizeof(double));
     S->inv_tmp.ensure((size_t)hk * hk * sizeof(double));
-    cholesky_invert(S->L.d(), k, S->W.d(), S->inv_tmp.d(), st);
+    cholesky_invert(S->L.d(), k, S->W.d(), S->inv_tmp.d(), Xd, st);
     if (S->kind == IHS_FACTOR_DIRECT_GRAM) {
         // H_S^{-1} = (L^{-1})^T L^{-1} explicitly (DMMA, k^3 flop once per factorization): every solve
         // is then a single symmetric mat-vec instead of two dependent triangular ones

@@ -852,6 +852,17 @@ const PassFn kPass[11] = {nullptr,
                           launch_pass<8, 256>,
                           launch_pass<9, 256>,
                           launch_pass<10, 256>};
+const PassFn kPass512[11] = {nullptr,
+                             launch_pass<1, 512>,
+                             launch_pass<2, 512>,
+                             launch_pass<3, 512>,
+                             launch_pass<4, 512>,
+                             launch_pass<5, 512>,
+                             launch_pass<6, 512>,
+                             launch_pass<7, 512>,
+                             launch_pass<8, 512>,
+                             launch_pass<9, 512>,
+                             launch_pass<10, 512>};
 const PassFn kPass128[11] = {nullptr,
                              launch_pass<1, 128>,
                              launch_pass<2, 128>,
@@ -864,6 +875,16 @@ const PassFn kPass128[11] = {nullptr,
                              launch_pass<9, 128>,
                              launch_pass<10, 128>};
 }  // namespace
+
+// threads per phase-2 tile of the two-kernel path (IHS_SRHT_P2T=128/256/512 for A/B runs)
+int p2_threads_default() {
+    static const int v = [] {
+        const char* e = std::getenv("IHS_SRHT_P2T");
+        const int t = e ? std::atoi(e) : 0;
+        return (t == 128 || t == 256 || t == 512) ? t : kP2Threads;
+    }();
+    return v;
+}
 
 SrhtPlan srht_plan(int64_t n, int64_t d, int64_t lda, int64_t m) {
     SrhtPlan p{};
@@ -898,7 +919,7 @@ SrhtPlan srht_plan(int64_t n, int64_t d, int64_t lda, int64_t m) {
     // exactly the reference's host expressions (sketch.hpp:47 and :95)
     p.scale1 = 1.0 / std::sqrt(static_cast<double>(np));
     p.scale2 = std::sqrt(static_cast<double>(np) / static_cast<double>(m));
-    p.p2t = kP2Threads;  // 64 KiB tiles (measured faster than 128-thread tiles in the two-kernel path)
+    p.p2t = p2_threads_default();
     p.stream = 0;
     return p;
 }
@@ -1046,8 +1067,8 @@ void srht_run_device(const SrhtPlan& p, const double* d_A, const uint32_t* d_sig
     for (int i = 0; i < p.npass; ++i) {
         const bool last = i == p.npass - 1;
         if (last && n_tiles == 0) break;
-        (p.p2t == 128 ? kPass128 : kPass)[p.pass_hb[i]](p, d_T, p.pass_lo[i], d_tiles, n_tiles, last, d_entries, d_SA,
-                                                        st);
+        (p.p2t == 128 ? kPass128 : p.p2t == 512 ? kPass512 : kPass)[p.pass_hb[i]](p, d_T, p.pass_lo[i], d_tiles,
+                                                                                  n_tiles, last, d_entries, d_SA, st);
     }
 }
 
