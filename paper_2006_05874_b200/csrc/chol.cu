@@ -65,46 +65,53 @@ __global__ void __launch_bounds__(256) potrf_diag_kernel(double* __restrict__ H,
 // 32-column warp factorizations and inversions (no CTA barrier per column).
 constexpr int PB = 65;  // padded row stride of the 64x64 shared blocks
 
-// Warp-level LLT of the 32x32 block a[r0.., r0..] in place (compact loops:
-// a fully unrolled register version overflows the instruction cache). Per
-// column: broadcast pivot, lanes below scale their entry, then each lane
-// updates its row of the trailing block (the column entries it needs are
-// same-address broadcasts).
+// Warp-level LLT of the 32x32 block a[r0.., r0..] in place. Lane i keeps its
+// row in registers; the loop over columns is not unrolled (straight-line code
+// of the whole factorization would be instruction-fetch bound), so the row is
+// shifted left after every column: at step j, r[q] holds a[i][j+q] of the
+// partially reduced block and every register index is static. Column j's
+// entries are broadcast by shuffles; no shared-memory round trip per column.
 __device__ __noinline__ void potrf32_warp(double (*a)[PB], int r0, int* info, int64_t kglob, int nvalid) {
     const int lane = threadIdx.x & 31;
-    double* ar = &a[r0 + lane][r0];
+    double r[32];
+#pragma unroll
+    for (int q = 0; q < 32; ++q) r[q] = q <= lane ? a[r0 + lane][r0 + q] : 0.0;
+#pragma unroll 1
     for (int j = 0; j < 32; ++j) {
-        double dj = a[r0 + j][r0 + j];
+        double dj = __shfl_sync(0xffffffffu, r[0], j);
         if (!(dj > 0.0) || !isfinite(dj)) {
             if (lane == 0 && r0 + j < nvalid) atomicCAS(info, 0, (int)(kglob + r0 + j + 1));
             dj = 1.0;  // keep going with a harmless pivot; the result is flagged
         }
         const double ljj = sqrt(dj);
-        double lij = 0.0;
-        if (lane > j) {
-            lij = ar[j] / ljj;
-            ar[j] = lij;
+        const double l = lane == j ? ljj : (lane > j ? r[0] / ljj : 0.0);
+        if (lane >= j) a[r0 + lane][r0 + j] = l;
+#pragma unroll
+        for (int q = 1; q < 32; ++q) {
+            const double c = __shfl_sync(0xffffffffu, l, (j + q) & 31);
+            if (j + q < 32 && lane >= j + q) r[q] = fma(-l, c, r[q]);
         }
-        __syncwarp();
-        if (lane == j) ar[j] = ljj;
-        if (lane > j)
-            for (int q = j + 1; q <= lane; ++q) ar[q] = fma(-lij, a[r0 + q][r0 + j], ar[q]);
-        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < 31; ++q) r[q] = r[q + 1];
+        r[31] = 0.0;
     }
 }
 
-// x[r0.., r0..] = inverse of the lower-triangular 32x32 block a[r0.., r0..]; lane = column
-__device__ __noinline__ void trtri32_warp(double (*a)[PB], double (*x)[PB], int r0) {
+// x[r0.., r0..] = inverse of the lower-triangular 32x32 block a[r0.., r0..];
+// lane = column c, rows i in order: x[i][c] = (delta_ic - sum_{q<i} a[i][q] x[q][c]) / a[i][i]
+// (a[i][q]: same-address broadcasts; x[q][c]: consecutive lanes, conflict-free)
+__device__ __noinline__ void trtri32_warp(const double (*__restrict__ a)[PB], double (*__restrict__ x)[PB], int r0) {
     const int lane = threadIdx.x & 31;
+#pragma unroll 1
     for (int i = 0; i < 32; ++i) {
         double s0 = (i == lane) ? 1.0 : 0.0, s1 = 0.0;
-        int q = lane;
-        for (; q + 1 < i; q += 2) {
-            s0 = fma(-a[r0 + i][r0 + q], x[r0 + q][r0 + lane], s0);
-            s1 = fma(-a[r0 + i][r0 + q + 1], x[r0 + q + 1][r0 + lane], s1);
+        const double* ai = &a[r0 + i][r0];
+#pragma unroll
+        for (int q = 0; q < 32; q += 2) {
+            if (q < i) s0 = fma(-ai[q], x[r0 + q][r0 + lane], s0);
+            if (q + 1 < i) s1 = fma(-ai[q + 1], x[r0 + q + 1][r0 + lane], s1);
         }
-        if (q < i) s0 = fma(-a[r0 + i][r0 + q], x[r0 + q][r0 + lane], s0);
-        x[r0 + i][r0 + lane] = i < lane ? 0.0 : (s0 + s1) / a[r0 + i][r0 + i];
+        x[r0 + i][r0 + lane] = i < lane ? 0.0 : (s0 + s1) / ai[i];
         __syncwarp();
     }
 }
