@@ -12,8 +12,9 @@ memory and the D2H of x inside the timed region.
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config c1..c5]
                   [--impl b200|reference] [--no-cpu-baseline]
 
-Multi-GPU (torchrun, one rank per GPU): round 1 runs independent replicas
-(see DESIGN.md "Multi-GPU"), value = max over ranks.
+Multi-GPU (torchrun, one rank per GPU): A is row-sharded over the ranks
+(strong scaling of the same problem; --replicas for independent copies),
+value = max over ranks.
 """
 from __future__ import annotations
 
@@ -191,6 +192,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-clocks", action="store_true", help="do not sample nvidia-smi during the timed steps")
     ap.add_argument("--out", default=None, help="also write the JSON line here")
+    ap.add_argument("--replicas", action="store_true", help="N > 1: independent replicas instead of row sharding")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     args.warmup_ref = 0  # the CPU reference has nothing to warm up; W is reported as given
@@ -203,7 +205,8 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as tdist
-        torch.cuda.set_device(local)
+        if args.impl == "b200":
+            torch.cuda.set_device(local)
         tdist.init_process_group("nccl" if args.impl == "b200" else "gloo")
         dist = tdist
     if args.impl == "reference":
@@ -217,18 +220,37 @@ def main():
 
     torch.cuda.set_device(local)
     n, d, nu = c["n"], c["d"], c["nu"]
+    # N > 1: A is row-sharded: rank r holds rows [r n_pad/N, (r+1) n_pad/N) of the padded index
+    # space, the sketch partials and gradient partials are combined over NCCL inside the library, and every
+    # rank runs the same replicated small solve. --replicas runs N independent copies instead.
+    sharded = world > 1 and not args.replicas
+    parallelism = "single GPU"
+    row0, rows = 0, n
+    comm = None
+    if sharded:
+        row0, rows = ihs.shard_rows(n, world, rank)
+        uid = [ihs.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = ihs.NcclComm(uid[0], world, rank, local)
+        parallelism = f"row-sharded x{world} (NCCL all-gather/all-reduce of sketch and gradient partials)"
+    elif world > 1:
+        parallelism = f"replicas x{world}"
     # inputs in pinned host memory (torch is plumbing only)
-    A_t = torch.empty((d, n), dtype=torch.float64, pin_memory=True)  # column-major n x d
-    b_t = torch.empty((n,), dtype=torch.float64, pin_memory=True)
+    A_t = torch.empty((d, rows), dtype=torch.float64, pin_memory=True)  # column-major rows x d
+    b_t = torch.empty((rows,), dtype=torch.float64, pin_memory=True)
     A = A_t.numpy().T
     b = b_t.numpy()
     t0 = time.perf_counter()
     ihs.synth_generate(n, d, spectrum=c["spectrum"], decay=c["decay"], noise_std=c["noise"],
-                       outlier_frac=c["outliers"], data_seed=rank, A_out=A, b_out=b)
+                       outlier_frac=c["outliers"], data_seed=0 if sharded else rank, row0=row0, rows=rows,
+                       A_out=A, b_out=b)
     gen_s = time.perf_counter() - t0
     assert A.flags.f_contiguous
 
-    p = ihs.ProblemInstance(A, b, nu, device=local)
+    if sharded:
+        p = ihs.ProblemInstance(A, b, nu, device=local, world_size=world, rank=rank, comm=comm, n_global=n)
+    else:
+        p = ihs.ProblemInstance(A, b, nu, device=local)
     cfg = solver_config(ihs, c)
     flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.float32, device=f"cuda:{local}")
 
@@ -286,7 +308,7 @@ def main():
             t = torch.tensor([v], device=f"cuda:{local}")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             v = float(t.item())
-        e2e = {"value": v, "unit": "s", "h2d_bytes_per_step": 8 * n * d + 8 * n, "d2h_bytes_per_step": 8 * d,
+        e2e = {"value": v, "unit": "s", "h2d_bytes_per_step": 8 * rows * d + 8 * rows, "d2h_bytes_per_step": 8 * d,
                "timer": "host wall clock around upload+solve (includes the H2D copies)"}
 
     # ---- roofline of the dominant kernel (live, from the solve's CUDA-event phase timers:
@@ -348,7 +370,8 @@ def main():
 
     if rank == 0:
         line = {"metric": METRIC, "value": ms / 1e3, "unit": "s", "n_gpus": world, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "weak",
+                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
+                "scaling": "strong" if sharded else "weak",
                 "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic (seeded SURVEY §8(d) generator: A = G diag(sigma), x_true, noise)",
                 "config": {"workload": c["desc"], "n": n, "d": d, "nu": nu, "sketch": c["sketch"], "mode": c["mode"],
@@ -357,7 +380,7 @@ def main():
                            "l2": ("inputs larger than L2 (A = %.0f MiB) and L2 flushed between steps"
                                   % (8 * n * d / 2**20)) if 8 * n * d > L2_BYTES else
                                  "L2 flushed (256 MiB write) between timed steps",
-                           "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
+                           "parallelism": parallelism},
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
                 "clocks": clocks,
                 "solve": {"iterations": last.iterations, "rejections": last.rejections, "final_m": last.final_m,

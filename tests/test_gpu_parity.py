@@ -291,3 +291,16 @@ def test_fixed_sketch_ihs_matches_oracle(gpu, O):
     ref = O.fixed_sketch_ihs(A, b, nu, SA, O.abi.Tuning(**tp.__dict__), 25, 1)
     for k in range(26):
         assert _abar_rel(A, nu, its[k], ref[k]) <= 1e-9 or np.linalg.norm(ref[k]) == 0
+
+
+# ----------------------------------------------------------------- NCCL plumbing
+@pytest.mark.gpu
+def test_nccl_single_rank_communicator(gpu):
+    """libnccl is loaded at run time and a communicator initialises (1 rank on cuda:0): the
+    plumbing of the row-sharded path; the multi-rank exchange itself is covered by the
+    emulated-shard tests above and by tests/test_multirank_gloo.py."""
+    uid = gpu.nccl_unique_id()
+    assert len(uid) == 128
+    comm = gpu.NcclComm(uid, 1, 0, 0)
+    assert comm.handle
+    del comm
