@@ -120,6 +120,9 @@ typedef struct ihs_phase_times {
     double sketch_kernel_ms; /* device time of the sketch's main kernels alone (SRHT transform
                                 kernels / the S*A DMMA GEMM), part of sketch_ms */
     int64_t n_sketch_kernel; /* number of such sketch-kernel intervals */
+    double gradient_kernel_ms; /* device time of the gradient kernels alone (pass over A + fixed-order
+                                  reduce), part of gradient_ms */
+    int64_t n_gradient_kernel; /* number of gradient passes timed */
 } ihs_phase_times;
 
 /* SolveReport (solver.hpp:70-87). Arrays are caller-allocated; *_size is the
@@ -206,6 +209,9 @@ int64_t ihs_gpu_problem_rows(const ihs_gpu_problem* p);
 int64_t ihs_gpu_problem_cols(const ihs_gpu_problem* p);
 /* re-upload A/b in place (same shape), e.g. for an end-to-end timed step */
 ihs_status ihs_gpu_problem_upload(ihs_gpu_problem* p, const double* A, int64_t lda, const double* b);
+/* Per-phase CUDA-event timing of adaptive solves on this problem (ihs_phase_times; default on).
+ * The events cost host time on the solve's critical path, so timed benchmark runs switch them off. */
+ihs_status ihs_gpu_problem_set_phase_timing(ihs_gpu_problem* p, int32_t enabled);
 
 /* gradient (problem.hpp:59-69): g = A^T(Ax - b) + nu^2 x, host in/out. */
 ihs_status ihs_gpu_gradient(ihs_gpu_problem* p, const double* x, double* g, ihs_counters* counters);

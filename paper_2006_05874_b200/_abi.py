@@ -80,7 +80,8 @@ class PhaseTimes(C.Structure):
                 ("n_gradient", C.c_int64), ("n_solve", C.c_int64), ("kernel_launches", C.c_int64),
                 ("total_ms", C.c_double), ("gradient_bytes", C.c_double), ("sketch_bytes", C.c_double),
                 ("sketch_flops", C.c_double), ("alloc_ms", C.c_double), ("host_rng_ms", C.c_double),
-                ("sketch_kernel_ms", C.c_double), ("n_sketch_kernel", C.c_int64)]
+                ("sketch_kernel_ms", C.c_double), ("n_sketch_kernel", C.c_int64),
+                ("gradient_kernel_ms", C.c_double), ("n_gradient_kernel", C.c_int64)]
 
     def as_dict(self):
         return {k: (float if t is C.c_double else int)(getattr(self, k)) for k, t in self._fields_}

@@ -48,6 +48,7 @@ def lib():
         "ihs_gpu_problem_rows": (i64, [vp]),
         "ihs_gpu_problem_cols": (i64, [vp]),
         "ihs_gpu_problem_upload": (C.c_int, [vp, d, i64, d]),
+        "ihs_gpu_problem_set_phase_timing": (C.c_int, [vp, C.c_int32]),
         "ihs_gpu_gradient": (C.c_int, [vp, d, d, P(abi.Counters)]),
         "ihs_gpu_sketch": (C.c_int, [vp, i32, i64, u64, d, P(abi.Counters)]),
         "ihs_gpu_fwht": (C.c_int, [d, i64]),
@@ -86,7 +87,7 @@ EXPORTED_SYMBOLS = (
     "ihs_gpu_last_error", "ihs_gpu_version", "ihs_gpu_kernel_launch_count", "ihs_gpu_device_count",
     "ihs_rates_from_bounds", "ihs_gaussian_targets", "ihs_srht_targets", "ihs_derive_seed", "ihs_next_pow2",
     "ihs_solver_config_default", "ihs_gpu_problem_create", "ihs_gpu_problem_destroy", "ihs_gpu_problem_rows",
-    "ihs_gpu_problem_cols", "ihs_gpu_problem_upload", "ihs_gpu_gradient", "ihs_gpu_sketch", "ihs_gpu_fwht",
+    "ihs_gpu_problem_cols", "ihs_gpu_problem_upload", "ihs_gpu_problem_set_phase_timing", "ihs_gpu_gradient", "ihs_gpu_sketch", "ihs_gpu_fwht",
     "ihs_gpu_sketch_matrix", "ihs_gpu_rademacher_bits", "ihs_gpu_fill_gaussian", "ihs_gpu_mt19937_64",
     "ihs_sample_without_replacement", "ihs_gpu_system_factorize", "ihs_gpu_system_destroy", "ihs_gpu_system_kind",
     "ihs_gpu_system_m", "ihs_gpu_system_d", "ihs_gpu_system_factor_flops", "ihs_gpu_system_flops_per_solve",

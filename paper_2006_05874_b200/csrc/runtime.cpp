@@ -186,14 +186,14 @@ struct PhaseTimer {
     }
     // sum of intervals [mark(phase), next mark) per phase id (0..4), and the
     // number of intervals per phase
-    void collect(double out_ms[5], int64_t count[5]) {
+    void collect(double out_ms[6], int64_t count[6]) {
         active = false;
-        for (int i = 0; i < 5; ++i) out_ms[i] = 0.0, count[i] = 0;
+        for (int i = 0; i < 6; ++i) out_ms[i] = 0.0, count[i] = 0;
         if (marks.size() < 2) return;
         CUDA_CHECK(cudaEventSynchronize(marks.back().first));
         for (size_t i = 0; i + 1 < marks.size(); ++i) {
             const int ph = marks[i].second;
-            if (ph < 0 || ph > 4) continue;
+            if (ph < 0 || ph > 5) continue;
             float ms = 0.f;
             CUDA_CHECK(cudaEventElapsedTime(&ms, marks[i].first, marks[i + 1].first));
             out_ms[ph] += ms;
@@ -202,7 +202,8 @@ struct PhaseTimer {
     }
 };
 // PH_SKETCH_KERNEL: the sketch's main kernels inside a PH_SKETCH interval
-enum { PH_SKETCH = 0, PH_FACTOR = 1, PH_GRAD = 2, PH_SOLVE = 3, PH_SKETCH_KERNEL = 4, PH_END = -1 };
+// PH_GRAD_KERNEL: the gradient kernels (grad pass + fixed-order reduce) inside a PH_GRAD interval
+enum { PH_SKETCH = 0, PH_FACTOR = 1, PH_GRAD = 2, PH_SOLVE = 3, PH_SKETCH_KERNEL = 4, PH_GRAD_KERNEL = 5, PH_END = -1 };
 
 }  // namespace
 
@@ -528,12 +529,16 @@ void alloc_and_upload(ihs_gpu_problem* P, const double* A, int64_t lda_host, con
 // nu^2 x term is added once.
 void problem_grad(ihs_gpu_problem* P, const double* X, int nrhs, double* G) {
     const double nu2 = P->nu * P->nu;
+    // inside a solve: the gradient kernels' own interval (bench roofline), then back to PH_GRAD
+    if (P->timer) P->timer->mark(PH_GRAD_KERNEL);
     if (P->opts.world_size > 1) {
         grad_run(P->gplan, P->A.d(), P->b.d(), 0.0, X, nrhs, G, P->grad_work.d(), P->st, P->Arm.d());
+        if (P->timer) P->timer->mark(PH_GRAD);
         nccl_allreduce_sum(G, (size_t)nrhs * P->d, P->opts.nccl_comm, P->st);
         add_scaled(G, X, nu2, (int64_t)nrhs * P->d, P->st);
     } else {
         grad_run(P->gplan, P->A.d(), P->b.d(), nu2, X, nrhs, G, P->grad_work.d(), P->st, P->Arm.d());
+        if (P->timer) P->timer->mark(PH_GRAD);
     }
 }
 
@@ -753,6 +758,11 @@ ihs_status ihs_gpu_problem_create(const double* A, int64_t n, int64_t d, int64_t
         P->h_dots.ensure(24 * sizeof(double));
         for (auto& e : P->set_ev) CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         P->timer = std::make_unique<PhaseTimer>(P->st);
+        {
+            // IHS_PHASE_TIMER=0: no per-phase events (A/B of the timers' own cost)
+            const char* e = std::getenv("IHS_PHASE_TIMER");
+            P->timer->enabled = !(e && e[0] == '0');
+        }
         CUDA_CHECK(cudaStreamSynchronize(P->st));
         *out = P.release();
     });
@@ -770,6 +780,13 @@ void ihs_gpu_problem_destroy(ihs_gpu_problem* p) {
 
 int64_t ihs_gpu_problem_rows(const ihs_gpu_problem* p) { return p ? p->n : 0; }
 int64_t ihs_gpu_problem_cols(const ihs_gpu_problem* p) { return p ? p->d : 0; }
+
+ihs_status ihs_gpu_problem_set_phase_timing(ihs_gpu_problem* P, int32_t enabled) {
+    return guarded([&] {
+        if (!P || !P->timer) fail(IHS_INVALID_INPUT, "set_phase_timing: null problem");
+        P->timer->enabled = enabled != 0;
+    });
+}
 
 ihs_status ihs_gpu_problem_upload(ihs_gpu_problem* P, const double* A, int64_t lda, const double* b) {
     return guarded([&] {
@@ -1289,8 +1306,8 @@ ihs_status ihs_gpu_adaptive_solve(ihs_gpu_problem* P, const ihs_solver_config* c
         rep->tuning = tp;
         rep->recompute_r_after_resketch = cfg->recompute_r_after_resketch;
         rep->wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
-        double ph[5];
-        int64_t phn[5];
+        double ph[6];
+        int64_t phn[6];
         tm.collect(ph, phn);
         PT.alloc_ms = (double)(g_alloc_ns.load() - alloc0) * 1e-6;
         PT.host_rng_ms = (double)(g_host_rng_ns.load() - rng0) * 1e-6;
@@ -1299,7 +1316,9 @@ ihs_status ihs_gpu_adaptive_solve(ihs_gpu_problem* P, const ihs_solver_config* c
         rep->times.sketch_kernel_ms = ph[PH_SKETCH_KERNEL];
         rep->times.n_sketch_kernel = phn[PH_SKETCH_KERNEL];
         rep->times.factor_ms = ph[PH_FACTOR];
-        rep->times.gradient_ms = ph[PH_GRAD];
+        rep->times.gradient_ms = ph[PH_GRAD] + ph[PH_GRAD_KERNEL];
+        rep->times.gradient_kernel_ms = ph[PH_GRAD_KERNEL];
+        rep->times.n_gradient_kernel = phn[PH_GRAD_KERNEL];
         rep->times.solve_ms = ph[PH_SOLVE];
         rep->times.kernel_launches = g_launches.load() - launches0;
         sys.st = nullptr;  // owned by the problem

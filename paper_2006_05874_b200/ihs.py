@@ -321,6 +321,10 @@ class ProblemInstance:
     def handle(self):
         return self._h
 
+    def set_phase_timing(self, enabled: bool):
+        """Per-phase CUDA-event timing of adaptive solves (SolveReport.device_times); default on."""
+        _check(lib().ihs_gpu_problem_set_phase_timing(self._h, 1 if enabled else 0))
+
     def upload(self, A=None, b=None):
         """Re-upload A and/or b (same shape) to the device."""
         Af = _fortran(A) if A is not None else None
