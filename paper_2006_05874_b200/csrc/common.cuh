@@ -143,11 +143,20 @@ void grad_plan_attach_tma(GradPlan& p, const double* d_A);
 // to v4 when the geometry fits (the caller then keeps a row-major A)
 bool grad_plan_use_rowmajor(GradPlan& p);
 size_t grad_rm_smem(int64_t d, int R, int nrhs, int ns);
+// Heavy-ball candidates formed inside the gradient pass (solver.hpp:182,190):
+// nrhs 2 -> [x_polyak; x_gd], nrhs 1 -> x_gd; written to out (nrhs x d).
+struct CandSpec {
+    const double* x = nullptr;
+    const double* xprev = nullptr;
+    const double* gt = nullptr;
+    double mu_p = 0.0, beta_p = 0.0, mu_gd = 0.0;
+    double* out = nullptr;
+};
 // v5: register-resident rows for d <= 512 (row-major copy as well)
 size_t grad_rr_smem(int64_t d, int R, int ns);
 bool grad_rr_geometry(int64_t d, int64_t lda, int* R, int* ns);
 void grad_rr_run(const GradPlan& p, const double* Arm, const double* b, const double* X, int nrhs, double* work,
-                 cudaStream_t st);
+                 cudaStream_t st, const CandSpec* cs = nullptr);
 bool grad_rm_geometry(int64_t d, int64_t lda, int* R, int* ns);
 void transpose_to_rowmajor(const double* A, int64_t lda, int64_t rows, int64_t d, double* Arm, cudaStream_t st);
 void grad_rm_run(const GradPlan& p, const double* Arm, const double* b, const double* X, int nrhs, double* work,
@@ -156,9 +165,11 @@ size_t grad_tma_smem(int64_t d, int R, int nrhs, int ns);
 bool grad_tma_make_map(const double* A, int64_t lda, int64_t d, int R, void* map_out);
 void grad_tma_run(const GradPlan& p, const double* b, const double* X, int nrhs, double* work, cudaStream_t st);
 size_t grad_work_doubles(const GradPlan& p);
-// X: nrhs vectors of d (ld = d); G out: nrhs vectors of d
+// X: nrhs vectors of d (ld = d); G out: nrhs vectors of d. cs != nullptr: X = cs->out is formed from the
+// heavy-ball state first (inside the pass on the v5 kernel, else by candidates()).
 void grad_run(const GradPlan& p, const double* d_A, const double* d_b, double nu2, const double* d_X, int nrhs,
-              double* d_G, double* d_work, cudaStream_t st, const double* d_Arm = nullptr);
+              double* d_G, double* d_work, cudaStream_t st, const double* d_Arm = nullptr,
+              const CandSpec* cs = nullptr);
 
 // vecops.cu
 // out[k*d..] for the heavy-ball candidates (solver.hpp:182,190), no FMA contraction:
@@ -178,8 +189,9 @@ void woodbury_finish(const double* SA, int64_t m, int64_t d, const double* g, co
 // of each row block, one launch); work: gemv_tiled_work_doubles, whose counter
 // tail must be zeroed once by gemv_tiled_reset before the first use
 size_t gemv_tiled_work_doubles(int64_t M, int64_t N);
+// dots != nullptr (requires M == N): also the decrement dots x.y, x.x per RHS (like decrement_dots)
 void gemv_tiled(const double* A, int64_t M, int64_t N, int64_t lda, const double* x, int nrhs, int64_t ldx, double* y,
-                int64_t ldy, double* work, cudaStream_t st);
+                int64_t ldy, double* work, cudaStream_t st, double* dots = nullptr);
 void gemv_tiled_reset(double* work, int64_t M, int64_t N, cudaStream_t st);
 // Wl = lower triangle of W (upper zeroed), k x k
 void tril_copy(const double* W, int64_t k, double* Wl, cudaStream_t st);

@@ -201,7 +201,7 @@ constexpr int RTHREADS = 32 * RW;
 template <int NRHS, int KP, int RR, int NS>
 __global__ void __launch_bounds__(RTHREADS, 1)
 grad_rr_kernel(const double* __restrict__ Arm, int64_t d, int64_t npanels, const double* __restrict__ b,
-               const double* __restrict__ X, double* __restrict__ work) {
+               const double* __restrict__ X, double* __restrict__ work, CandSpec cs) {
     extern __shared__ __align__(128) double sm[];
     const int64_t stage = (int64_t)RR * d;
     double* panel = sm;
@@ -227,14 +227,45 @@ grad_rr_kernel(const double* __restrict__ Arm, int64_t d, int64_t npanels, const
     }
     {
         // ---------------- consumers
+        // x of the right-hand sides in registers: read, or (cs.x != nullptr) formed here from the
+        // heavy-ball state exactly like candidates_kernel (solver.hpp:182,190; no FMA contraction),
+        // CTA 0 publishing them for the caller
         double2 xr[NRHS][KP];
 #pragma unroll
-        for (int q = 0; q < NRHS; ++q)
+        for (int k = 0; k < KP; ++k) {
+            const int64_t j = 2 * lane + 64 * k;
+            if (j >= d) {
 #pragma unroll
-            for (int k = 0; k < KP; ++k) {
-                const int64_t j = 2 * lane + 64 * k;
-                xr[q][k] = j < d ? make_double2(X[q * d + j], X[q * d + j + 1]) : make_double2(0.0, 0.0);
+                for (int q = 0; q < NRHS; ++q) xr[q][k] = make_double2(0.0, 0.0);
+                continue;
             }
+            if (cs.x == nullptr) {
+#pragma unroll
+                for (int q = 0; q < NRHS; ++q) xr[q][k] = make_double2(X[q * d + j], X[q * d + j + 1]);
+                continue;
+            }
+            double xv[2][NRHS];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const double xi = cs.x[j + h], gi = cs.gt[j + h];
+                const double xg = __dsub_rn(xi, __dmul_rn(cs.mu_gd, gi));
+                if (NRHS == 2) {
+                    xv[h][0] = __dadd_rn(__dsub_rn(xi, __dmul_rn(cs.mu_p, gi)),
+                                         __dmul_rn(cs.beta_p, __dsub_rn(xi, cs.xprev[j + h])));
+                    xv[h][NRHS - 1] = xg;
+                } else {
+                    xv[h][0] = xg;
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < NRHS; ++q) {
+                xr[q][k] = make_double2(xv[0][q], xv[1][q]);
+                if (blockIdx.x == 0 && warp == 0) {
+                    cs.out[q * d + j] = xv[0][q];
+                    cs.out[q * d + j + 1] = xv[1][q];
+                }
+            }
+        }
         double2 g[NRHS][KP];
 #pragma unroll
         for (int q = 0; q < NRHS; ++q)
@@ -314,7 +345,8 @@ grad_rr_kernel(const double* __restrict__ Arm, int64_t d, int64_t npanels, const
 }
 
 template <int NRHS, int KP, int RR, int NS>
-void launch_rr(const GradPlan& p, const double* Arm, const double* b, const double* X, double* work, cudaStream_t st) {
+void launch_rr(const GradPlan& p, const double* Arm, const double* b, const double* X, double* work, cudaStream_t st,
+               const CandSpec& cs) {
     const size_t smem = grad_rr_smem(p.d, RR, NS);
     static bool attr = false;
     if (!attr) {
@@ -322,7 +354,7 @@ void launch_rr(const GradPlan& p, const double* Arm, const double* b, const doub
                                         227 * 1024));
         attr = true;
     }
-    LAUNCH((grad_rr_kernel<NRHS, KP, RR, NS>), p.grid, RTHREADS, smem, st, Arm, p.d, p.lda / RR, b, X, work);
+    LAUNCH((grad_rr_kernel<NRHS, KP, RR, NS>), p.grid, RTHREADS, smem, st, Arm, p.d, p.lda / RR, b, X, work, cs);
 }
 
 template <int NRHS, int RR, int NS>
@@ -374,13 +406,14 @@ bool grad_rr_geometry(int64_t d, int64_t lda, int* R, int* ns) {
 }
 
 void grad_rr_run(const GradPlan& p, const double* Arm, const double* b, const double* X, int nrhs, double* work,
-                 cudaStream_t st) {
+                 cudaStream_t st, const CandSpec* csp) {
+    const CandSpec cs = csp ? *csp : CandSpec{};
     const int kp = (int)ceil_div(p.d, 64);
     const int kpc = kp <= 2 ? 2 : kp <= 4 ? 4 : 8;
 #define IHS_RR(KPv, RRv, NSv)                                                                     \
     if (kpc == KPv && p.R == RRv && p.stages == NSv) {                                            \
-        if (nrhs == 1) launch_rr<1, KPv, RRv, NSv>(p, Arm, b, X, work, st);                        \
-        else launch_rr<2, KPv, RRv, NSv>(p, Arm, b, X, work, st);                                  \
+        if (nrhs == 1) launch_rr<1, KPv, RRv, NSv>(p, Arm, b, X, work, st, cs);                    \
+        else launch_rr<2, KPv, RRv, NSv>(p, Arm, b, X, work, st, cs);                              \
         return;                                                                                    \
     }
 #define IHS_RR_NS(KPv, RRv) IHS_RR(KPv, RRv, 2) IHS_RR(KPv, RRv, 3) IHS_RR(KPv, RRv, 4) IHS_RR(KPv, RRv, 5) IHS_RR(KPv, RRv, 6)

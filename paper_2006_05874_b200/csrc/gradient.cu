@@ -395,9 +395,15 @@ void grad_plan_attach_tma(GradPlan& p, const double* d_A) {
 }
 
 void grad_run(const GradPlan& p, const double* d_A, const double* d_b, double nu2, const double* d_X, int nrhs,
-              double* d_G, double* d_work, cudaStream_t st, const double* d_Arm) {
+              double* d_G, double* d_work, cudaStream_t st, const double* d_Arm, const CandSpec* cs) {
+    if (cs) {
+        d_X = cs->out;
+        if (p.version != 5)
+            candidates(cs->x, cs->xprev, cs->gt, cs->mu_p, cs->beta_p, cs->mu_gd, p.d, nrhs == 2 ? cs->out : nullptr,
+                       nrhs == 2 ? cs->out + p.d : cs->out, st);
+    }
     if (p.version >= 2) {
-        if (p.version == 5) grad_rr_run(p, d_Arm, d_b, d_X, nrhs, d_work, st);
+        if (p.version == 5) grad_rr_run(p, d_Arm, d_b, d_X, nrhs, d_work, st, cs);
         else if (p.version == 4) grad_rm_run(p, d_Arm, d_b, d_X, nrhs, d_work, st);
         else if (p.version == 3) grad_tma_run(p, d_b, d_X, nrhs, d_work, st);
         else if (nrhs == 1) launch_v2_dispatch<1>(p, d_A, d_b, d_X, d_work, st);

@@ -480,7 +480,7 @@ void system_factorize(ihs_gpu_system* S, ihs_counters* c) {
               splitk > 1 ? S->work.d() : nullptr, st);
     }
     const int64_t gm = S->kind == IHS_FACTOR_DIRECT_GRAM ? d : m;
-    S->gv.ensure(gemv_tiled_work_doubles(gm, d) * sizeof(double));
+    S->gv.ensure((gemv_tiled_work_doubles(gm, d) + 8) * sizeof(double));
     gemv_tiled_reset(S->gv.d(), gm, d, st);
     int h_info[2] = {0, 0};
     CUDA_CHECK(cudaMemcpyAsync(h_info, S->info.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -489,6 +489,18 @@ void system_factorize(ihs_gpu_system* S, ihs_counters* c) {
     if (h_info[0]) fail(IHS_NUMERICAL_BREAKDOWN, "SketchedSystem: Cholesky factorization failed");
     S->tmp.ensure((size_t)(4 * std::max(m, d) + cholesky_solve_work_doubles(k)) * sizeof(double));
     if (c) c->factor += S->factor_flops();
+}
+
+// z = H_S^{-1} g and the decrement dots (g.z, g.g per RHS) into dots; fused into the
+// mat-vec's last block on the direct-Gram path
+void system_solve_dev(const ihs_gpu_system* S, const double* g, double* z, int nrhs);
+void system_solve_dots(const ihs_gpu_system* S, const double* g, double* z, int nrhs, double* dots) {
+    if (S->kind == IHS_FACTOR_DIRECT_GRAM) {
+        gemv_tiled(S->Hinv.d(), S->d, S->d, S->d, g, nrhs, S->d, z, S->d, S->gv.d(), S->st, dots);
+    } else {
+        system_solve_dev(S, g, z, nrhs);
+        decrement_dots(g, z, S->d, nrhs, dots, S->st);
+    }
 }
 
 // z[:, q] = H_S^{-1} g[:, q] (sketched_system.hpp:40-49), device vectors, ld = d
@@ -527,17 +539,18 @@ void alloc_and_upload(ihs_gpu_problem* P, const double* A, int64_t lda_host, con
 // g = A^T(Ax - b) + nu^2 x; on a row-sharded problem the A_p^T(A_p x - b_p)
 // partials are summed over NCCL (identical bytes on every rank) before the
 // nu^2 x term is added once.
-void problem_grad(ihs_gpu_problem* P, const double* X, int nrhs, double* G) {
+void problem_grad(ihs_gpu_problem* P, const double* X, int nrhs, double* G, const CandSpec* cs = nullptr) {
     const double nu2 = P->nu * P->nu;
+    if (cs) X = cs->out;
     // inside a solve: the gradient kernels' own interval (bench roofline), then back to PH_GRAD
     if (P->timer) P->timer->mark(PH_GRAD_KERNEL);
     if (P->opts.world_size > 1) {
-        grad_run(P->gplan, P->A.d(), P->b.d(), 0.0, X, nrhs, G, P->grad_work.d(), P->st, P->Arm.d());
+        grad_run(P->gplan, P->A.d(), P->b.d(), 0.0, X, nrhs, G, P->grad_work.d(), P->st, P->Arm.d(), cs);
         if (P->timer) P->timer->mark(PH_GRAD);
         nccl_allreduce_sum(G, (size_t)nrhs * P->d, P->opts.nccl_comm, P->st);
         add_scaled(G, X, nu2, (int64_t)nrhs * P->d, P->st);
     } else {
-        grad_run(P->gplan, P->A.d(), P->b.d(), nu2, X, nrhs, G, P->grad_work.d(), P->st, P->Arm.d());
+        grad_run(P->gplan, P->A.d(), P->b.d(), nu2, X, nrhs, G, P->grad_work.d(), P->st, P->Arm.d(), cs);
         if (P->timer) P->timer->mark(PH_GRAD);
     }
 }
@@ -1159,18 +1172,24 @@ ihs_status ihs_gpu_adaptive_solve(ihs_gpu_problem* P, const ihs_solver_config* c
         auto enqueue_eval = [&](int k, const double* x, const double* xp, const double* gtv, bool polyak) {
             EvalSet& S = sets[k];
             tm.mark(PH_GRAD);
-            candidates(x, xp, gtv, tp.mu_p, tp.beta_p, tp.mu_gd, dim, polyak ? S.X2 : nullptr, S.X2 + dim, st);
             const int nr = polyak ? 2 : 1;
-            const double* Xe = polyak ? S.X2 : S.X2 + dim;
+            double* Xe = polyak ? S.X2 : S.X2 + dim;
             double* Ge = polyak ? S.G2 : S.G2 + dim;
             double* GTe = polyak ? S.GT2 : S.GT2 + dim;
-            problem_grad(P, Xe, nr, Ge);
+            CandSpec cs;  // the candidates are formed inside the gradient pass where the kernel supports it
+            cs.x = x;
+            cs.xprev = xp;
+            cs.gt = gtv;
+            cs.mu_p = tp.mu_p;
+            cs.beta_p = tp.beta_p;
+            cs.mu_gd = tp.mu_gd;
+            cs.out = Xe;
+            problem_grad(P, Xe, nr, Ge, &cs);
             PT.n_gradient++;
             PT.gradient_bytes += grad_pass_bytes;
             PT.n_solve += nr;
             tm.mark(PH_SOLVE);
-            system_solve_dev(&sys, Ge, GTe, nr);
-            decrement_dots(Ge, GTe, dim, nr, S.dots, st);
+            system_solve_dots(&sys, Ge, GTe, nr, S.dots);
             tm.mark(PH_END);
             CUDA_CHECK(cudaMemcpyAsync(S.hd, S.dots, (size_t)2 * nr * sizeof(double), cudaMemcpyDeviceToHost, st));
             CUDA_CHECK(cudaEventRecord(S.ev, st));

@@ -75,16 +75,16 @@ __global__ void gemv_n_kernel(const double* __restrict__ A, int64_t M, int64_t N
 // CTA of each row block (per-row-block arrival counter) sums the chunks in
 // chunk order, so the result is deterministic and one launch suffices. The
 // counters are reset by that last CTA for the next launch.
-constexpr int GV_ROWS = 64, GV_COLS = 64;
+constexpr int GV_ROWS = 32, GV_COLS = 64, GV_G = 256 / GV_ROWS;  // 8 column interleaves
 __global__ void __launch_bounds__(256) gemv_tiled_kernel(const double* __restrict__ A, int64_t M, int64_t N,
                                                          int64_t lda, const double* __restrict__ x, int nrhs,
                                                          int64_t ldx, double* __restrict__ part,
                                                          unsigned* __restrict__ arrivals, double* __restrict__ y,
-                                                         int64_t ldy) {
+                                                         int64_t ldy, double* __restrict__ dots) {
     const int64_t r0 = (int64_t)blockIdx.x * GV_ROWS, c0 = (int64_t)blockIdx.y * GV_COLS;
     const int64_t c1 = c0 + GV_COLS < N ? c0 + GV_COLS : N;
     __shared__ double xs[2][GV_COLS];
-    __shared__ double red[4][2][GV_ROWS];
+    __shared__ double red[GV_G][2][GV_ROWS];
     __shared__ unsigned last;
     for (int e = threadIdx.x; e < (int)(c1 - c0); e += blockDim.x)
         for (int q = 0; q < nrhs; ++q) xs[q][e] = x[q * ldx + c0 + e];
@@ -94,7 +94,7 @@ __global__ void __launch_bounds__(256) gemv_tiled_kernel(const double* __restric
     double acc[2] = {0.0, 0.0};
     if (row < M) {
 #pragma unroll 4
-        for (int64_t j = c0 + qg; j < c1; j += 4) {
+        for (int64_t j = c0 + qg; j < c1; j += GV_G) {
             const double a = A[row + j * lda];
             acc[0] = fma(a, xs[0][j - c0], acc[0]);
             if (nrhs > 1) acc[1] = fma(a, xs[1][j - c0], acc[1]);
@@ -104,8 +104,12 @@ __global__ void __launch_bounds__(256) gemv_tiled_kernel(const double* __restric
     red[qg][1][r] = acc[1];
     __syncthreads();
     if (threadIdx.x < GV_ROWS && row < M)
-        for (int q = 0; q < nrhs; ++q)
-            part[((int64_t)blockIdx.y * nrhs + q) * M + row] = (red[0][q][r] + red[1][q][r]) + (red[2][q][r] + red[3][q][r]);
+        for (int q = 0; q < nrhs; ++q) {
+            double sum = 0.0;
+#pragma unroll
+            for (int g = 0; g < GV_G; ++g) sum += red[g][q][r];
+            part[((int64_t)blockIdx.y * nrhs + q) * M + row] = sum;
+        }
     __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) last = atomicAdd(arrivals + blockIdx.x, 1u) == gridDim.y - 1;
@@ -119,6 +123,40 @@ __global__ void __launch_bounds__(256) gemv_tiled_kernel(const double* __restric
             y[q * ldy + row] = sum;
         }
     if (threadIdx.x == 0) arrivals[blockIdx.x] = 0u;
+    if (dots == nullptr) return;
+    // decrement dots (sketched_system.hpp:95-101) by the last row block to finish: x . y and x . x per
+    // right-hand side over all M = N rows, fixed-order tree -> deterministic
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(arrivals + gridDim.x, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    __shared__ double s1[256], s2[256];
+    for (int q = 0; q < nrhs; ++q) {
+        double a = 0.0, c = 0.0;
+        for (int64_t i = threadIdx.x; i < M; i += blockDim.x) {
+            const double gi = x[q * ldx + i];
+            a = fma(gi, __ldcg(y + q * ldy + i), a);
+            c = fma(gi, gi, c);
+        }
+        s1[threadIdx.x] = a;
+        s2[threadIdx.x] = c;
+        __syncthreads();
+        for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+            if ((int)threadIdx.x < w) {
+                s1[threadIdx.x] += s1[threadIdx.x + w];
+                s2[threadIdx.x] += s2[threadIdx.x + w];
+            }
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) {
+            dots[2 * q] = s1[0];
+            dots[2 * q + 1] = s2[0];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) arrivals[gridDim.x] = 0u;
 }
 
 // z[:,q] = (g[:,q] - SA^T w[:,q]) / nu2 ; one warp per column of SA
@@ -185,15 +223,15 @@ size_t gemv_tiled_work_doubles(int64_t M, int64_t N) {
 }
 
 void gemv_tiled(const double* A, int64_t M, int64_t N, int64_t lda, const double* x, int nrhs, int64_t ldx, double* y,
-                int64_t ldy, double* work, cudaStream_t st) {
+                int64_t ldy, double* work, cudaStream_t st, double* dots) {
     dim3 grid((unsigned)ceil_div(M, GV_ROWS), (unsigned)ceil_div(N, GV_COLS));
     unsigned* arrivals = reinterpret_cast<unsigned*>(work + (size_t)grid.y * 2 * (size_t)M);
-    LAUNCH(gemv_tiled_kernel, grid, 256, 0, st, A, M, N, lda, x, nrhs, ldx, work, arrivals, y, ldy);
+    LAUNCH(gemv_tiled_kernel, grid, 256, 0, st, A, M, N, lda, x, nrhs, ldx, work, arrivals, y, ldy, dots);
 }
 
 void gemv_tiled_reset(double* work, int64_t M, int64_t N, cudaStream_t st) {
     const size_t off = (size_t)ceil_div(N, GV_COLS) * 2 * (size_t)M;
-    CUDA_CHECK(cudaMemsetAsync(work + off, 0, (size_t)ceil_div(M, GV_ROWS) * sizeof(double), st));
+    CUDA_CHECK(cudaMemsetAsync(work + off, 0, ((size_t)ceil_div(M, GV_ROWS) + 8) * sizeof(double), st));
 }
 
 __global__ void tril_copy_kernel(const double* __restrict__ W, int64_t k, double* __restrict__ Wl) {
