@@ -14,6 +14,9 @@
 // substitution.
 #include "common.cuh"
 
+#include <cooperative_groups.h>
+namespace cg = cooperative_groups;
+
 namespace ihs_b200 {
 
 namespace {
@@ -213,6 +216,16 @@ __global__ void __launch_bounds__(32 * TRSM_WARPS) trsm_inv_panel_kernel(double*
     if (lane + 32 < nb) H[row + (k + lane + 32) * n] = s1;
 }
 
+// W's diagonal 32-blocks <- the block inverses of the cooperative factorization
+__global__ void place_diag_inv32_kernel(const double* __restrict__ Xd, int64_t n, double* __restrict__ W) {
+    const int64_t k = (int64_t)blockIdx.x * 32;
+    const double* X = Xd + (int64_t)blockIdx.x * 32 * 32;
+    for (int e = threadIdx.x; e < 32 * 32; e += blockDim.x) {
+        const int i = e & 31, j = e >> 5;
+        if (k + i < n && k + j < n && i >= j) W[(k + i) + (k + j) * n] = X[e];
+    }
+}
+
 // W's diagonal 64-blocks <- the block inverses computed during the factorization
 __global__ void place_diag_inv_kernel(const double* __restrict__ Xd, int64_t n, double* __restrict__ W) {
     const int64_t k = (int64_t)blockIdx.x * 64;
@@ -374,13 +387,163 @@ void trmv(const double* Wf, int64_t n, bool lower, const double* x, int nrhs, do
            (int)grid.y, (int)lower, y);
 }
 
+// ---------------------------------------------------------------- single-launch blocked LLT
+// The column-serial factorization of each diagonal block is latency-bound and,
+// launched per panel with its TRSM and trailing update, costs ~3 launches of
+// tens of microseconds per 64 columns. Here the whole right-looking LLT
+// (NB = 32) runs in one cooperative launch: per panel, CTA 0's first warp
+// factors the diagonal block in registers (row per lane, shuffles, no shared
+// round trip per column) and inverts it (column per lane), every warp of the
+// grid then forms one row of L21 = A21 X^T from that inverse, and the CTAs
+// share the 32x32 tiles of the trailing update A22 -= L21 L21^T; grid-wide
+// barriers separate the three steps. The 32x32 diagonal-block inverses are
+// kept (Xd) for the triangular inverse that follows.
+constexpr int CB = 32;           // panel width
+constexpr int CTHREADS = 256;    // 8 warps per CTA
+
+// lane i holds row i of the lower block (r[q] = a[i][q], q <= i); on return r holds row i of L.
+// Right-looking with a left shift per column so every register index is static.
+__device__ __forceinline__ void potrf32_regs(double (&r)[CB], int nvalid, int* info, int64_t kglob) {
+    const int lane = threadIdx.x & 31;
+    double out[CB];
+#pragma unroll
+    for (int q = 0; q < CB; ++q) out[q] = 0.0;
+#pragma unroll 1
+    for (int j = 0; j < CB; ++j) {
+        double dj = __shfl_sync(0xffffffffu, r[0], j);
+        if (!(dj > 0.0) || !isfinite(dj)) {
+            if (lane == 0 && j < nvalid) atomicCAS(info, 0, (int)(kglob + j + 1));
+            dj = 1.0;
+        }
+        const double ljj = sqrt(dj);
+        const double l = lane == j ? ljj : (lane > j ? r[0] / ljj : 0.0);
+#pragma unroll
+        for (int q = 1; q < CB; ++q) {
+            const double c = __shfl_sync(0xffffffffu, l, (j + q) & 31);
+            if (j + q < CB && lane >= j + q) r[q] = fma(-l, c, r[q]);
+        }
+        // out[j] = l, with j dynamic: rotate the output row instead (out[0] always receives)
+#pragma unroll
+        for (int q = 0; q < CB - 1; ++q) out[q] = out[q + 1];
+        out[CB - 1] = l;
+#pragma unroll
+        for (int q = 0; q < CB - 1; ++q) r[q] = r[q + 1];
+        r[CB - 1] = 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < CB; ++q) r[q] = out[q];
+}
+
+__global__ void __launch_bounds__(CTHREADS) chol_coop_kernel(double* __restrict__ H, int64_t k,
+                                                             double* __restrict__ Xd, int* __restrict__ info) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ double xs[CB][CB + 1];     // panel block inverse (or scratch)
+    __shared__ double ta[CB][CB + 1], tb[CB][CB + 1];
+    __shared__ double rowv[CTHREADS / 32][CB];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int nwarps_grid = gridDim.x * (CTHREADS / 32);
+    for (int64_t p = 0; p < k; p += CB) {
+        const int nb = (int)imin64(CB, k - p);
+        // ---- A: diagonal block factor + inverse (CTA 0, warp 0)
+        if (blockIdx.x == 0 && warp == 0) {
+            double r[CB];
+#pragma unroll
+            for (int q = 0; q < CB; ++q) {
+                double v = 0.0;
+                if (lane < nb && q < nb) v = q <= lane ? H[(p + lane) + (p + q) * k] : 0.0;
+                else if (lane == q) v = 1.0;  // identity padding of a ragged last panel
+                r[q] = v;
+            }
+            potrf32_regs(r, nb, info, p);
+#pragma unroll
+            for (int q = 0; q < CB; ++q) {
+                if (lane < nb && q < nb && q <= lane) H[(p + lane) + (p + q) * k] = r[q];
+                xs[lane][q] = q <= lane ? r[q] : 0.0;  // L block, row lane
+            }
+            __syncwarp();
+            // X = L^{-1}: lane = column c, rows in order
+            double xc[CB];
+#pragma unroll
+            for (int i = 0; i < CB; ++i) {
+                double s0 = (i == lane) ? 1.0 : 0.0, s1 = 0.0;
+#pragma unroll
+                for (int q = 0; q < i; q += 2) {
+                    s0 = fma(-xs[i][q], xc[q], s0);
+                    if (q + 1 < i) s1 = fma(-xs[i][q + 1], xc[q + 1], s1);
+                }
+                xc[i] = i < lane ? 0.0 : (s0 + s1) / xs[i][i];
+            }
+            double* X = Xd + (p / CB) * CB * CB;
+#pragma unroll
+            for (int i = 0; i < CB; ++i) X[i + CB * lane] = xc[i];  // column-major, X[i][lane]
+        }
+        grid.sync();
+        const int64_t rest = k - p - nb;
+        if (rest <= 0) break;
+        // ---- B: L21 = A21 X^T, one warp per row
+        {
+            const double* X = Xd + (p / CB) * CB * CB;
+            for (int e = tid; e < CB * CB; e += CTHREADS) xs[e % CB][e / CB] = __ldcg(X + e);  // xs[i][c] = X[i][c]
+            __syncthreads();
+            for (int64_t rr = (int64_t)blockIdx.x * (CTHREADS / 32) + warp; rr < rest; rr += nwarps_grid) {
+                const int64_t row = p + nb + rr;
+                rowv[warp][lane] = lane < nb ? __ldcg(H + row + (p + lane) * k) : 0.0;
+                __syncwarp();
+                // out[c] = sum_{q <= c} a[q] X[c][q]
+                double s = 0.0;
+                for (int q = 0; q <= lane; ++q) s = fma(rowv[warp][q], xs[lane][q], s);
+                if (lane < nb) H[row + (p + lane) * k] = s;
+                __syncwarp();
+            }
+        }
+        grid.sync();
+        // ---- C: trailing update of the lower tiles, A22 -= L21 L21^T
+        {
+            const int64_t nt = (rest + CB - 1) / CB;
+            const int64_t ntiles = nt * (nt + 1) / 2;
+            const int64_t base = p + nb;
+            for (int64_t tix = blockIdx.x; tix < ntiles; tix += gridDim.x) {
+                // tile (ti, tj), ti >= tj, enumerated row by row
+                int64_t ti = (int64_t)((sqrt(8.0 * (double)tix + 1.0) - 1.0) * 0.5);
+                while (ti * (ti + 1) / 2 > tix) --ti;
+                while ((ti + 1) * (ti + 2) / 2 <= tix) ++ti;
+                const int64_t tj = tix - ti * (ti + 1) / 2;
+                const int64_t i0 = base + ti * CB, j0 = base + tj * CB;
+                __syncthreads();
+                for (int e = tid; e < CB * CB; e += CTHREADS) {
+                    const int rr = e % CB, q = e / CB;
+                    ta[rr][q] = (i0 + rr < k && q < nb) ? __ldcg(H + (i0 + rr) + (p + q) * k) : 0.0;
+                    tb[rr][q] = (j0 + rr < k && q < nb) ? __ldcg(H + (j0 + rr) + (p + q) * k) : 0.0;
+                }
+                __syncthreads();
+                // thread -> (row i, 4 columns j = jq, jq+8, jq+16, jq+24)
+                const int i = tid % CB, jq = tid / CB;
+                double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll 8
+                for (int q = 0; q < CB; ++q) {
+                    const double a = ta[i][q];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) acc[u] = fma(a, tb[jq + 8 * u][q], acc[u]);
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int64_t gi = i0 + i, gj = j0 + jq + 8 * u;
+                    if (gi < k && gj < k && gi >= gj) H[gi + gj * k] -= acc[u];
+                }
+            }
+        }
+        grid.sync();
+    }
+}
+
 // W[n0:n0+size, n0:n0+size] <- L^{-1} of the same diagonal block (lower), with
 // the diagonal 64-blocks already inverted and the strict upper part zero.
-void tri_inv_rec(const double* L, double* W, int64_t n, int64_t n0, int64_t size, double* tmp, cudaStream_t st) {
-    if (size <= NB) return;
-    const int64_t h = ((size / 2 + NB - 1) / NB) * NB;  // split on a block boundary
-    tri_inv_rec(L, W, n, n0, h, tmp, st);
-    tri_inv_rec(L, W, n, n0 + h, size - h, tmp, st);
+void tri_inv_rec(const double* L, double* W, int64_t n, int64_t n0, int64_t size, double* tmp, cudaStream_t st,
+                 int base = NB) {
+    if (size <= base) return;
+    const int64_t h = ((size / 2 + base - 1) / base) * base;  // split on a block boundary
+    tri_inv_rec(L, W, n, n0, h, tmp, st, base);
+    tri_inv_rec(L, W, n, n0 + h, size - h, tmp, st, base);
     const int64_t m2 = size - h;
     // tmp (m2 x h, ld m2) = L21 * W11
     dgemm(false, false, m2, h, h, 1.0, L + (n0 + h) + n0 * n, n, W + n0 + n0 * n, n, 0.0, tmp, m2, false, 1, nullptr,
@@ -391,9 +554,14 @@ void tri_inv_rec(const double* L, double* W, int64_t n, int64_t n0, int64_t size
 }
 }  // namespace
 
-void cholesky_invert(const double* d_L, int64_t n, double* d_W, double* d_tmp, const double* d_Xd, cudaStream_t st) {
+void cholesky_invert(const double* d_L, int64_t n, double* d_W, double* d_tmp, const double* d_Xd, cudaStream_t st,
+                     int xd_block) {
     CUDA_CHECK(cudaMemsetAsync(d_W, 0, (size_t)n * n * sizeof(double), st));
-    if (d_Xd) {
+    int base = NB;
+    if (d_Xd && xd_block == 32) {
+        LAUNCH(place_diag_inv32_kernel, (unsigned)ceil_div(n, 32), 256, 0, st, d_Xd, n, d_W);
+        base = 32;
+    } else if (d_Xd) {
         LAUNCH(place_diag_inv_kernel, (unsigned)ceil_div(n, NB), 256, 0, st, d_Xd, n, d_W);
     } else {
         const size_t smem = (size_t)2 * NB * (NB + 1) * sizeof(double);
@@ -404,7 +572,7 @@ void cholesky_invert(const double* d_L, int64_t n, double* d_W, double* d_tmp, c
         }
         LAUNCH(tri_inv_diag_kernel, (unsigned)ceil_div(n, NB), 64, smem, st, d_L, n, d_W);
     }
-    tri_inv_rec(d_L, d_W, n, 0, n, d_tmp, st);
+    tri_inv_rec(d_L, d_W, n, 0, n, d_tmp, st, base);
     dim3 grid((unsigned)ceil_div(n, 32), (unsigned)ceil_div(n, 32));
     LAUNCH(mirror_upper_kernel, grid, dim3(32, 8), 0, st, d_W, n);
 }
@@ -419,7 +587,31 @@ void cholesky_solve_inv(const double* d_W, int64_t n, const double* d_R, double*
     trmv(d_W, n, false, y, nrhs, d_Z, part, st);   // z = L^{-T} y
 }
 
-size_t cholesky_diag_inv_doubles(int64_t n) { return (size_t)ceil_div(n, NB) * NB * NB; }
+size_t cholesky_diag_inv_doubles(int64_t n) {
+    return std::max((size_t)ceil_div(n, NB) * NB * NB, (size_t)ceil_div(n, CB) * CB * CB);
+}
+
+// One cooperative launch for the whole factorization (see chol_coop_kernel); false when the device
+// cannot co-schedule the grid (the caller then uses the per-panel kernels).
+bool cholesky_factor_coop(double* d_H, int64_t n, double* d_Xd, int* d_info, int num_sms, cudaStream_t st) {
+    static int per_sm = -1;
+    if (per_sm < 0) {
+        int supported = 0, dev = 0;
+        CUDA_CHECK(cudaGetDevice(&dev));
+        CUDA_CHECK(cudaDeviceGetAttribute(&supported, cudaDevAttrCooperativeLaunch, dev));
+        per_sm = 0;
+        if (supported) CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, chol_coop_kernel, CTHREADS, 0));
+    }
+    if (per_sm < 1) return false;
+    CUDA_CHECK(cudaMemsetAsync(d_info, 0, sizeof(int), st));
+    const int64_t nt = std::max<int64_t>(1, ceil_div(n - CB, CB));
+    const int64_t want = std::max<int64_t>(1, std::min<int64_t>(nt * (nt + 1) / 2, (int64_t)num_sms));
+    const int grid = (int)std::min<int64_t>(want, (int64_t)num_sms * per_sm);
+    void* args[] = {&d_H, &n, &d_Xd, &d_info};
+    CUDA_CHECK(cudaLaunchCooperativeKernel((const void*)chol_coop_kernel, dim3(grid), dim3(CTHREADS), args, 0, st));
+    note_launch();
+    return true;
+}
 
 void cholesky_factor(double* d_H, int64_t n, double* d_Xd, int* d_info, int num_sms, cudaStream_t st) {
     (void)num_sms;

@@ -117,9 +117,13 @@ int dgemm_pick_splitk(int64_t M, int64_t N, int64_t K, int num_sms);
 // receives the inverses of the 64x64 diagonal blocks of L.
 size_t cholesky_diag_inv_doubles(int64_t n);
 void cholesky_factor(double* d_H, int64_t n, double* d_Xd, int* d_info, int num_sms, cudaStream_t st);
+// single cooperative launch (32-column panels); d_Xd receives the 32x32 diagonal-block inverses
+bool cholesky_factor_coop(double* d_H, int64_t n, double* d_Xd, int* d_info, int num_sms, cudaStream_t st);
 // W = L^{-1} (lower) with W^T mirrored into the strict upper triangle;
 // d_tmp holds ceil(n/2)^2 doubles; d_Xd = the factorization's block inverses (or nullptr).
-void cholesky_invert(const double* d_L, int64_t n, double* d_W, double* d_tmp, const double* d_Xd, cudaStream_t st);
+// xd_block: 64 (potrf_inv_diag) or 32 (cholesky_factor_coop) when d_Xd is given
+void cholesky_invert(const double* d_L, int64_t n, double* d_W, double* d_tmp, const double* d_Xd, cudaStream_t st,
+                     int xd_block = 64);
 size_t cholesky_solve_work_doubles(int64_t n);
 // Z = L^{-T} L^{-1} R for nrhs columns (ld = n), two parallel triangular mat-vecs
 void cholesky_solve_inv(const double* d_W, int64_t n, const double* d_R, double* d_Z, int nrhs, double* d_work,

@@ -453,22 +453,29 @@ void system_factorize(ihs_gpu_system* S, ihs_counters* c) {
               splitk > 1 ? S->work.d() : nullptr, st);
     }
     add_diag(S->L.d(), k, nu2, st);
-    // IHS_CHOL_BLOCKINV=1: fused diagonal-block factor+inverse kernels (measured slower so far)
-    static const bool blockinv = [] {
-        const char* e = std::getenv("IHS_CHOL_BLOCKINV");
-        return e && e[0] == '1';
+    // IHS_CHOL_MODE: 2 (default) one cooperative launch; 1 per-panel kernels with fused diagonal
+    // factor+inverse; 0 per-panel column-serial kernels
+    static const int chol_mode = [] {
+        const char* e = std::getenv("IHS_CHOL_MODE");
+        return e ? std::atoi(e) : 2;
     }();
     double* Xd = nullptr;
-    if (blockinv) {
+    int xd_block = 64;
+    if (chol_mode >= 1) {
         S->Xd.ensure(cholesky_diag_inv_doubles(k) * sizeof(double));
         Xd = S->Xd.d();
     }
-    cholesky_factor(S->L.d(), k, Xd, S->info.as<int>(), S->num_sms, st);
+    if (chol_mode == 2 && cholesky_factor_coop(S->L.d(), k, Xd, S->info.as<int>(), S->num_sms, st)) {
+        xd_block = 32;
+    } else {
+        cholesky_factor(S->L.d(), k, chol_mode == 1 ? Xd : nullptr, S->info.as<int>(), S->num_sms, st);
+        if (chol_mode != 1) Xd = nullptr;
+    }
     // W = L^{-1} once per factorization; every later solve is two mat-vecs
     const int64_t hk = (k + 1) / 2 + 64;
     S->W.ensure((size_t)k * k * sizeof(double));
     S->inv_tmp.ensure((size_t)hk * hk * sizeof(double));
-    cholesky_invert(S->L.d(), k, S->W.d(), S->inv_tmp.d(), Xd, st);
+    cholesky_invert(S->L.d(), k, S->W.d(), S->inv_tmp.d(), Xd, st, xd_block);
     if (S->kind == IHS_FACTOR_DIRECT_GRAM) {
         // H_S^{-1} = (L^{-1})^T L^{-1} explicitly (DMMA, k^3 flop once per factorization): every solve
         // is then a single symmetric mat-vec instead of two dependent triangular ones

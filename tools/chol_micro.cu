@@ -250,6 +250,25 @@ int main() {
             for (int i = j; i < n; ++i) { md = fmax(md, fabs(a1[i + n * j] - a2[i + n * j])); ma = fmax(ma, fabs(a1[i + n * j])); }
         printf(", \"potrf64_reg_maxdiff_rel\": %.3e", md / ma);
     }
+    // whole factorizations: per-panel kernels vs one cooperative launch
+    for (int K : {64, 256, 512, 1024}) {
+        std::vector<double> hk((size_t)K * K);
+        for (int i = 0; i < K; ++i)
+            for (int j = 0; j < K; ++j) hk[i + (size_t)K * j] = (i == j ? K : 0.0) + 1.0 / (1.0 + i + j);
+        double *src, *dst, *xk;
+        cudaMalloc(&src, (size_t)K * K * 8);
+        cudaMalloc(&dst, (size_t)K * K * 8);
+        cudaMalloc(&xk, cholesky_diag_inv_doubles(K) * 8);
+        cudaMemcpy(src, hk.data(), (size_t)K * K * 8, cudaMemcpyHostToDevice);
+        auto rs = [&] { cudaMemcpyAsync(dst, src, (size_t)K * K * 8, cudaMemcpyDeviceToDevice); };
+        const float t_copy = time_it(rs, 50);
+        const float t_panel = time_it([&] { rs(); cholesky_factor(dst, K, nullptr, info, 148, 0); }, 50);
+        const float t_coop = time_it([&] { rs(); cholesky_factor_coop(dst, K, xk, info, 148, 0); }, 50);
+        printf(", \"k%d\": {\"copy_us\": %.1f, \"panel_us\": %.1f, \"coop_us\": %.1f}", K, t_copy, t_panel, t_coop);
+        cudaFree(src);
+        cudaFree(dst);
+        cudaFree(xk);
+    }
     printf(", \"err\": \"%s\"}\n", cudaGetErrorString(cudaGetLastError()));
     return 0;
 }
