@@ -286,15 +286,18 @@ grad_rr_kernel(const double* __restrict__ Arm, int64_t d, int64_t npanels, const
                     const int64_t j = 2 * lane + 64 * k;
                     a[k] = j < d ? *reinterpret_cast<const double2*>(P + row * d + j) : make_double2(0.0, 0.0);
                 }
+                // fp64 ops have ~130-cycle latency on B200 (tools/lat_micro.cu): the row dot product
+                // runs as four independent chains per right-hand side, summed in a fixed tree
                 double r[NRHS];
 #pragma unroll
                 for (int q = 0; q < NRHS; ++q) {
-                    double acc = 0.0;
+                    double c4[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
                     for (int k = 0; k < KP; ++k) {
-                        acc = fma(a[k].x, xr[q][k].x, acc);
-                        acc = fma(a[k].y, xr[q][k].y, acc);
+                        c4[(2 * k) & 3] = fma(a[k].x, xr[q][k].x, c4[(2 * k) & 3]);
+                        c4[(2 * k + 1) & 3] = fma(a[k].y, xr[q][k].y, c4[(2 * k + 1) & 3]);
                     }
+                    double acc = (c4[0] + c4[1]) + (c4[2] + c4[3]);
 #pragma unroll
                     for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
                     r[q] = acc - bi;

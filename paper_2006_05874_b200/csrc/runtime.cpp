@@ -457,7 +457,7 @@ void system_factorize(ihs_gpu_system* S, ihs_counters* c) {
     // factor+inverse; 0 per-panel column-serial kernels
     static const int chol_mode = [] {
         const char* e = std::getenv("IHS_CHOL_MODE");
-        return e ? std::atoi(e) : 2;
+        return e ? std::atoi(e) : 0;
     }();
     double* Xd = nullptr;
     int xd_block = 64;
