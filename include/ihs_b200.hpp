@@ -309,6 +309,7 @@ struct SolveReport {  // solver.hpp:70-87
     double wall_seconds = 0.0;
     TuningParams tuning;
     bool recompute_r_after_resketch = true;
+    Vector dual_final;  ///< final dual iterate z_T (underdetermined solves only, solver.hpp:82)
     ihs_phase_times device_times{};
 };
 
@@ -327,9 +328,10 @@ inline int override_tramp(void* user, int64_t m, uint64_t sub_seed, double* out)
 }
 }  // namespace detail
 
-inline SolveReport adaptive_solve(const ProblemInstance& p, const SolverConfig& cfg) {
-    if (p.orientation() != Orientation::Overdetermined)
-        throw InvalidInput("adaptive_solve: expects an overdetermined instance (use solve_underdetermined for d > n)");
+namespace detail {
+// adaptive_solve / solve_underdetermined through the C-ABI; dual: the iterates, warm start and
+// sketch_override live in the dual space (n), x is the primal d-vector
+inline SolveReport run_solve(const ProblemInstance& p, const SolverConfig& cfg, bool dual) {
     ihs_solver_config c;
     ihs_solver_config_default(&c);
     c.rho = cfg.rho;
@@ -345,7 +347,8 @@ inline SolveReport adaptive_solve(const ProblemInstance& p, const SolverConfig& 
     c.recompute_r_after_resketch = cfg.recompute_r_after_resketch;
     c.record_iterates = cfg.record_iterates;
     if (cfg.warm_start) {
-        if (cfg.warm_start->size() != p.cols()) throw InvalidInput("adaptive_solve: warm start has wrong dimension");
+        if (cfg.warm_start->size() != (dual ? p.rows() : p.cols()))
+            throw InvalidInput("adaptive_solve: warm start has wrong dimension");
         c.warm_start = cfg.warm_start->data();
     }
     if (cfg.tuning_override) {
@@ -353,18 +356,29 @@ inline SolveReport adaptive_solve(const ProblemInstance& p, const SolverConfig& 
         c.has_tuning_override = 1;
         c.tuning_override = {t.lam, t.Lam, t.mu_gd, t.c_gd, t.mu_p, t.beta_p, t.c_p};
     }
-    detail::OverrideCtx ctx{&cfg, &p.A()};
+    Matrix At;
+    if (dual && cfg.sketch_override) {
+        At = Matrix(p.cols(), p.rows());
+        for (Index j = 0; j < p.rows(); ++j)
+            for (Index i = 0; i < p.cols(); ++i) At(i, j) = p.A()(j, i);
+    }
+    detail::OverrideCtx ctx{&cfg, dual ? &At : &p.A()};
     if (cfg.sketch_override) {
         c.sketch_override = &detail::override_tramp;
         c.sketch_override_user = &ctx;
     }
-    const Index d = p.cols();
+    const Index d = dual ? p.rows() : p.cols();  // iterate dimension
     SolveReport out;
-    out.x = Vector(d);
+    out.x = Vector(p.cols());
+    if (dual) out.dual_final = Vector(p.rows());
     std::vector<ihs_iteration_record> log(4096);
     std::vector<double> its;
     ihs_solve_report r{};
     r.x = out.x.data();
+    if (dual) r.dual_final = out.dual_final.data();
+    auto call = [&] {
+        detail::check(dual ? ihs_gpu_solve_underdetermined(p.handle(), &c, &r) : ihs_gpu_adaptive_solve(p.handle(), &c, &r));
+    };
     r.log = log.data();
     r.log_capacity = static_cast<int64_t>(log.size());
     if (cfg.record_iterates) {
@@ -372,12 +386,12 @@ inline SolveReport adaptive_solve(const ProblemInstance& p, const SolverConfig& 
         r.iterates = its.data();
         r.iterates_capacity = cfg.max_iters + 1;
     }
-    detail::check(ihs_gpu_adaptive_solve(p.handle(), &c, &r));
+    call();
     if (r.log_size > r.log_capacity) {  // rare: rerun with a larger audit buffer
         log.resize(static_cast<size_t>(r.log_size));
         r.log = log.data();
         r.log_capacity = r.log_size;
-        detail::check(ihs_gpu_adaptive_solve(p.handle(), &c, &r));
+        call();
     }
     out.iterations = r.iterations;
     out.rejections = r.rejections;
@@ -404,6 +418,21 @@ inline SolveReport adaptive_solve(const ProblemInstance& p, const SolverConfig& 
     out.device_times = r.times;
     return out;
 }
+}  // namespace detail
+
+inline SolveReport adaptive_solve(const ProblemInstance& p, const SolverConfig& cfg) {  // solver.hpp:242-250
+    if (p.orientation() != Orientation::Overdetermined)
+        throw InvalidInput("adaptive_solve: expects an overdetermined instance (use solve_underdetermined for d > n)");
+    return detail::run_solve(p, cfg, false);
+}
+
+// dual.hpp:13-33: the dual ridge problem in A^T; x = A^T z_T, dual_final = z_T, iterates = dual trace
+inline SolveReport solve_underdetermined(const ProblemInstance& p, const SolverConfig& cfg) {
+    if (p.orientation() != Orientation::Underdetermined)
+        throw InvalidInput("solve_underdetermined: expects an underdetermined instance");
+    return detail::run_solve(p, cfg, true);
+}
+
 
 enum class FixedMode { Gradient, Polyak };
 

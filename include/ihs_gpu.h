@@ -149,6 +149,8 @@ typedef struct ihs_solve_report {
     int32_t recompute_r_after_resketch;
     int32_t _pad;
     ihs_phase_times times;          /* device-side breakdown (GPU only) */
+    double* dual_final;             /* n doubles, caller-allocated, may be NULL: final dual iterate z_T of
+                                       solve_underdetermined (solver.hpp:82); iterates then hold the dual trace */
 } ihs_solve_report;
 
 /* Device / sharding options of a problem handle. */
@@ -261,6 +263,9 @@ ihs_status ihs_newton_decrement(const double* g, const double* gt, int64_t d, do
  * whole loop runs against the device-resident problem; only the scalar
  * decrement r of each candidate crosses to the host for the accept/reject
  * decision, exactly as in the reference control flow. */
+/* solve_underdetermined (dual.hpp:13-33): adaptive IHS on the dual ridge problem in A^T (gradient
+ * A(A^T z) - b + nu^2 z, SRHT pads d); rep->x receives x = A^T z_T (d doubles), rep->dual_final z_T. */
+ihs_status ihs_gpu_solve_underdetermined(ihs_gpu_problem* p, const ihs_solver_config* cfg, ihs_solve_report* rep);
 ihs_status ihs_gpu_adaptive_solve(ihs_gpu_problem* p, const ihs_solver_config* cfg, ihs_solve_report* rep);
 
 /* fixed_sketch_ihs (solver.hpp:258-276): T steps with a fixed system. Writes

@@ -164,14 +164,18 @@ Mat apply_sketch(const Mat& A, SketchKind kind, Index m, std::uint64_t seed, Cos
 }
 
 // =============================================================== problem.hpp
-Problem::Problem(Mat A_, Vec b_, double nu_) : A(std::move(A_)), b(std::move(b_)), nu(nu_) {  // :22-33
+Problem::Problem(Mat A_, Vec b_, double nu_, bool underdetermined)
+    : A(std::move(A_)), b(std::move(b_)), nu(nu_) {  // :22-33
     if (!(nu > 0.0)) throw InvalidInput("ProblemInstance: nu must be strictly positive");
     if (A.rows < 1 || A.cols < 1) throw InvalidInput("ProblemInstance: empty matrix");
     if (static_cast<Index>(b.size()) != A.rows) throw InvalidInput("ProblemInstance: size of b must match rows of A");
     for (double v : A.a) if (!std::isfinite(v)) throw InvalidInput("ProblemInstance: non-finite input");
     for (double v : b) if (!std::isfinite(v)) throw InvalidInput("ProblemInstance: non-finite input");
     if (!std::isfinite(nu)) throw InvalidInput("ProblemInstance: non-finite input");
-    if (A.rows < A.cols) throw InvalidInput("ProblemInstance: overdetermined orientation requires n >= d");
+    if (!underdetermined && A.rows < A.cols)
+        throw InvalidInput("ProblemInstance: overdetermined orientation requires n >= d");
+    if (underdetermined && A.cols < A.rows)
+        throw InvalidInput("ProblemInstance: underdetermined orientation requires d >= n");
 }
 
 static double dot4(const double* a, const double* b, Index n) {
@@ -370,13 +374,13 @@ namespace {
 struct Candidate { Vec x, g, gt; double r; };
 }
 
-SolveReport adaptive_solve(const Problem& p, const SolverConfig& cfg) {  // :106-232 via :242-250
+SolveReport adaptive_solve_core(const Mat& A, double nu, const GradFn& grad, const SolverConfig& cfg) {  // :106-232
     if (!(cfg.eps > 0.0 && cfg.eps < 1.0)) throw InvalidInput("adaptive_solve: eps must be in (0,1)");
     if (cfg.m_initial < 1) throw InvalidInput("adaptive_solve: m_initial must be >= 1");
     if (cfg.max_iters < 1) throw InvalidInput("adaptive_solve: max_iters must be >= 1");
 
     const auto t_start = std::chrono::steady_clock::now();
-    const Index dim = p.A.cols, n_rows = p.A.rows;
+    const Index dim = A.cols, n_rows = A.rows;
 
     TuningParams tp;
     if (cfg.tuning_override) tp = *cfg.tuning_override;
@@ -397,16 +401,16 @@ SolveReport adaptive_solve(const Problem& p, const SolverConfig& cfg) {  // :106
     Index m = cfg.m_initial, K = 0;
 
     auto core_sketch = [&](Index mm, std::uint64_t sub_seed) -> Mat {  // :100-104
-        if (cfg.sketch_override) return cfg.sketch_override(p.A, mm, sub_seed);
-        return apply_sketch(p.A, cfg.sketch_kind, mm, sub_seed, &rep.counters);
+        if (cfg.sketch_override) return cfg.sketch_override(A, mm, sub_seed);
+        return apply_sketch(A, cfg.sketch_kind, mm, sub_seed, &rep.counters);
     };
-    SketchedSystem sys = SketchedSystem::factorize(core_sketch(m, derive_seed(cfg.seed, 0)), p.nu, &rep.counters);
+    SketchedSystem sys = SketchedSystem::factorize(core_sketch(m, derive_seed(cfg.seed, 0)), nu, &rep.counters);
 
     Vec x_cur = cfg.warm_start ? *cfg.warm_start : Vec(static_cast<size_t>(dim), 0.0);
     if (static_cast<Index>(x_cur.size()) != dim) throw InvalidInput("adaptive_solve: warm start has wrong dimension");
     Vec x_prev = x_cur;
 
-    Vec g = gradient(p, x_cur, &rep.counters);
+    Vec g = grad(x_cur, &rep.counters);
     Vec gt = sys.solve(g, &rep.counters);
     double r = newton_decrement(g, gt);
     const double r1 = r;
@@ -418,7 +422,7 @@ SolveReport adaptive_solve(const Problem& p, const SolverConfig& cfg) {  // :106
     bool checks_enabled = true;
 
     auto evaluate = [&](Vec xc) -> Candidate {  // :161-166
-        Vec gc = gradient(p, xc, &rep.counters);
+        Vec gc = grad(xc, &rep.counters);
         Vec gtc = sys.solve(gc, &rep.counters);
         const double rc = newton_decrement(gc, gtc);
         return {std::move(xc), std::move(gc), std::move(gtc), rc};
@@ -472,7 +476,7 @@ SolveReport adaptive_solve(const Problem& p, const SolverConfig& cfg) {  // :106
         }
         m *= 2;
         ++K;
-        sys = SketchedSystem::factorize(core_sketch(m, derive_seed(cfg.seed, static_cast<std::uint64_t>(K))), p.nu, &rep.counters);
+        sys = SketchedSystem::factorize(core_sketch(m, derive_seed(cfg.seed, static_cast<std::uint64_t>(K))), nu, &rep.counters);
         gt = sys.solve(g, &rep.counters);
         const double r_old = r;
         if (cfg.recompute_r_after_resketch) {
@@ -488,6 +492,51 @@ SolveReport adaptive_solve(const Problem& p, const SolverConfig& cfg) {  // :106
     rep.r_final = r;
     rep.converged = converged;
     rep.wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+    return rep;
+}
+
+SolveReport adaptive_solve(const Problem& p, const SolverConfig& cfg) {  // :242-250
+    return adaptive_solve_core(p.A, p.nu, [&p](const Vec& x, CostCounters* c) { return gradient(p, x, c); }, cfg);
+}
+
+// dual.hpp:13-33: the dual ridge problem in A^T, gradient A(A^T z) - b + nu^2 z, x = A^T z
+SolveReport solve_underdetermined(const Problem& p, const SolverConfig& cfg) {
+    if (p.A.rows > p.A.cols) throw InvalidInput("solve_underdetermined: expects an underdetermined instance");
+    // (an n == d instance is both; the caller constructs it with the underdetermined orientation)
+    const Index n = p.A.rows, d = p.A.cols;
+    Mat At(d, n);
+    for (Index j = 0; j < n; ++j)
+        for (Index i = 0; i < d; ++i) At(i, j) = p.A(j, i);
+    const double nu2 = p.nu * p.nu;
+    GradFn grad = [&p, n, d, nu2](const Vec& z, CostCounters* c) -> Vec {
+        Vec u(static_cast<size_t>(d), 0.0);  // u = A^T z
+        for (Index i = 0; i < d; ++i) {
+            double s = 0.0;
+            for (Index r = 0; r < n; ++r) s += p.A(r, i) * z[static_cast<size_t>(r)];
+            u[static_cast<size_t>(i)] = s;
+        }
+        Vec g(static_cast<size_t>(n), 0.0);  // g = A u - b + nu^2 z
+        for (Index i = 0; i < d; ++i) {
+            const double ui = u[static_cast<size_t>(i)];
+            for (Index r = 0; r < n; ++r) g[static_cast<size_t>(r)] += p.A(r, i) * ui;
+        }
+        for (Index r = 0; r < n; ++r) {
+            const size_t q = static_cast<size_t>(r);
+            g[q] = (g[q] - p.b[q]) + nu2 * z[q];
+        }
+        if (c) c->matvec += 2 * static_cast<std::uint64_t>(n) * static_cast<std::uint64_t>(d) +
+                            static_cast<std::uint64_t>(d) + 2 * static_cast<std::uint64_t>(n);
+        return g;
+    };
+    SolveReport rep = adaptive_solve_core(At, p.nu, grad, cfg);
+    rep.dual_final = rep.x;
+    Vec x(static_cast<size_t>(d), 0.0);  // x = A^T z
+    for (Index i = 0; i < d; ++i) {
+        double s = 0.0;
+        for (Index r = 0; r < n; ++r) s += p.A(r, i) * rep.dual_final[static_cast<size_t>(r)];
+        x[static_cast<size_t>(i)] = s;
+    }
+    rep.x = std::move(x);
     return rep;
 }
 

@@ -74,7 +74,7 @@ struct Problem {                                                         // prob
     Mat A;
     Vec b;
     double nu = 1.0;
-    Problem(Mat A_, Vec b_, double nu_);
+    Problem(Mat A_, Vec b_, double nu_, bool underdetermined = false);
 };
 Vec gradient(const Problem& p, const Vec& x, CostCounters* c = nullptr); // problem.hpp:59-69
 Vec direct_solve(const Problem& p);  // ridge normal equations (support.hpp:19-23), Cholesky
@@ -139,8 +139,12 @@ struct SolveReport {                                                     // :70-
     double wall_seconds = 0;
     TuningParams tuning;
     bool recompute_r_after_resketch = true;
+    Vec dual_final;  // underdetermined solves only (solver.hpp:82)
 };
-SolveReport adaptive_solve(const Problem& p, const SolverConfig& cfg);  // :106-250
+using GradFn = std::function<Vec(const Vec&, CostCounters*)>;
+SolveReport adaptive_solve_core(const Mat& A, double nu, const GradFn& grad, const SolverConfig& cfg);  // :106-232
+SolveReport adaptive_solve(const Problem& p, const SolverConfig& cfg);  // :242-250
+SolveReport solve_underdetermined(const Problem& p, const SolverConfig& cfg);  // dual.hpp:13-33
 enum class FixedMode { Gradient = 0, Polyak = 1 };
 std::vector<Vec> fixed_sketch_ihs(const Problem& p, const SketchedSystem& sys, const TuningParams& tp,
                                   Index T, FixedMode mode, const Vec* x_start = nullptr);  // :258-276

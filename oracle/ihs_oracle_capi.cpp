@@ -35,6 +35,68 @@ void add_counters(ihs_counters* out, const CostCounters& c) {
 }
 }  // namespace
 
+static int oracle_solve(bool dual, const double* A, int64_t n, int64_t d, int64_t lda, const double* b, double nu,
+                        const ihs_solver_config* c, ihs_solve_report* rep) {
+    return guarded([&] {
+        Problem p(to_mat(A, n, d, lda), Vec(b, b + n), nu, dual);
+        SolverConfig cfg;
+        cfg.rho = c->rho;
+        cfg.eta = c->eta;
+        cfg.sketch_kind = c->sketch_kind == IHS_SKETCH_SRHT ? SketchKind::SRHT : SketchKind::Gaussian;
+        cfg.m_initial = c->m_initial;
+        cfg.eps = c->eps;
+        cfg.max_iters = c->max_iters;
+        if (c->max_sketch > 0) cfg.max_sketch = c->max_sketch;
+        cfg.mode = c->mode == IHS_MODE_GRADIENT_ONLY ? SolveMode::GradientOnly : SolveMode::PolyakThenGradient;
+        cfg.seed = c->seed;
+        cfg.enforce_validity = c->enforce_validity != 0;
+        cfg.recompute_r_after_resketch = c->recompute_r_after_resketch != 0;
+        cfg.record_iterates = c->record_iterates != 0;
+        if (c->warm_start) cfg.warm_start = Vec(c->warm_start, c->warm_start + (dual ? n : d));
+        if (c->has_tuning_override) {
+            const auto& t = c->tuning_override;
+            cfg.tuning_override = TuningParams{t.lam, t.Lam, t.mu_gd, t.c_gd, t.mu_p, t.beta_p, t.c_p};
+        }
+        if (c->sketch_override) {
+            auto fn = c->sketch_override;
+            void* user = c->sketch_override_user;
+            cfg.sketch_override = [fn, user](const Mat& Am, Index mm, std::uint64_t sub) {
+                Mat SA(mm, Am.cols);
+                if (fn(user, mm, sub, SA.a.data()) != 0) throw InvalidInput("sketch_override failed");
+                return SA;
+            };
+        }
+        SolveReport r = dual ? solve_underdetermined(p, cfg) : adaptive_solve(p, cfg);
+        std::memcpy(rep->x, r.x.data(), sizeof(double) * static_cast<size_t>(d));
+        if (dual && rep->dual_final)
+            std::memcpy(rep->dual_final, r.dual_final.data(), sizeof(double) * static_cast<size_t>(n));
+        const int64_t dim = dual ? n : d;  // iterates: the dual trace for underdetermined solves
+        rep->iterations = r.iterations;
+        rep->rejections = r.rejections;
+        rep->final_m = r.final_m;
+        rep->r1 = r.r1;
+        rep->r_final = r.r_final;
+        rep->converged = r.converged;
+        rep->sketch_exhausted = r.sketch_exhausted;
+        rep->log_size = static_cast<int64_t>(r.log.size());
+        if (rep->log)
+            for (int64_t i = 0; i < rep->log_size && i < rep->log_capacity; ++i) {
+                const auto& e = r.log[static_cast<size_t>(i)];
+                rep->log[i] = {e.t, e.m, e.r, e.r_prev, static_cast<int32_t>(e.branch), 0};
+            }
+        rep->iterates_size = static_cast<int64_t>(r.iterates.size());
+        if (rep->iterates)
+            for (int64_t i = 0; i < rep->iterates_size && i < rep->iterates_capacity; ++i)
+                std::memcpy(rep->iterates + i * dim, r.iterates[static_cast<size_t>(i)].data(), sizeof(double) * static_cast<size_t>(dim));
+        rep->counters = {r.counters.sketch, r.counters.factor, r.counters.solve, r.counters.matvec};
+        rep->wall_seconds = r.wall_seconds;
+        const auto& t = r.tuning;
+        rep->tuning = {t.lam, t.Lam, t.mu_gd, t.c_gd, t.mu_p, t.beta_p, t.c_p};
+        rep->recompute_r_after_resketch = r.recompute_r_after_resketch;
+    });
+}
+
+
 extern "C" {
 
 const char* ihs_oracle_last_error(void) { return g_err.c_str(); }
@@ -127,60 +189,29 @@ int ihs_oracle_srht_targets(double rho, double* lam, double* Lam) {
 
 int ihs_oracle_adaptive_solve(const double* A, int64_t n, int64_t d, int64_t lda, const double* b, double nu,
                               const ihs_solver_config* c, ihs_solve_report* rep) {
+    return oracle_solve(false, A, n, d, lda, b, nu, c, rep);
+}
+
+// The reference tests' data helpers (proj/tests/support.hpp:32-47): gen = mt19937_64(seed);
+// M = random_matrix(rows, cols, gen) (column-major, one normal_distribution), then optionally
+// v = random_vector(vlen, gen) with a fresh distribution object on the same generator.
+int ihs_oracle_test_support_data(uint64_t seed, int64_t rows, int64_t cols, double* M, int64_t vlen, double* v) {
     return guarded([&] {
-        Problem p(to_mat(A, n, d, lda), Vec(b, b + n), nu);
-        SolverConfig cfg;
-        cfg.rho = c->rho;
-        cfg.eta = c->eta;
-        cfg.sketch_kind = c->sketch_kind == IHS_SKETCH_SRHT ? SketchKind::SRHT : SketchKind::Gaussian;
-        cfg.m_initial = c->m_initial;
-        cfg.eps = c->eps;
-        cfg.max_iters = c->max_iters;
-        if (c->max_sketch > 0) cfg.max_sketch = c->max_sketch;
-        cfg.mode = c->mode == IHS_MODE_GRADIENT_ONLY ? SolveMode::GradientOnly : SolveMode::PolyakThenGradient;
-        cfg.seed = c->seed;
-        cfg.enforce_validity = c->enforce_validity != 0;
-        cfg.recompute_r_after_resketch = c->recompute_r_after_resketch != 0;
-        cfg.record_iterates = c->record_iterates != 0;
-        if (c->warm_start) cfg.warm_start = Vec(c->warm_start, c->warm_start + d);
-        if (c->has_tuning_override) {
-            const auto& t = c->tuning_override;
-            cfg.tuning_override = TuningParams{t.lam, t.Lam, t.mu_gd, t.c_gd, t.mu_p, t.beta_p, t.c_p};
+        std::mt19937_64 gen(seed);
+        {
+            std::normal_distribution<double> dist;
+            for (int64_t j = 0; j < cols; ++j)
+                for (int64_t i = 0; i < rows; ++i) M[i + j * rows] = dist(gen);
         }
-        if (c->sketch_override) {
-            auto fn = c->sketch_override;
-            void* user = c->sketch_override_user;
-            cfg.sketch_override = [fn, user](const Mat& Am, Index mm, std::uint64_t sub) {
-                Mat SA(mm, Am.cols);
-                if (fn(user, mm, sub, SA.a.data()) != 0) throw InvalidInput("sketch_override failed");
-                return SA;
-            };
+        if (vlen > 0 && v) {
+            std::normal_distribution<double> dist;
+            for (int64_t i = 0; i < vlen; ++i) v[i] = dist(gen);
         }
-        SolveReport r = adaptive_solve(p, cfg);
-        std::memcpy(rep->x, r.x.data(), sizeof(double) * static_cast<size_t>(d));
-        rep->iterations = r.iterations;
-        rep->rejections = r.rejections;
-        rep->final_m = r.final_m;
-        rep->r1 = r.r1;
-        rep->r_final = r.r_final;
-        rep->converged = r.converged;
-        rep->sketch_exhausted = r.sketch_exhausted;
-        rep->log_size = static_cast<int64_t>(r.log.size());
-        if (rep->log)
-            for (int64_t i = 0; i < rep->log_size && i < rep->log_capacity; ++i) {
-                const auto& e = r.log[static_cast<size_t>(i)];
-                rep->log[i] = {e.t, e.m, e.r, e.r_prev, static_cast<int32_t>(e.branch), 0};
-            }
-        rep->iterates_size = static_cast<int64_t>(r.iterates.size());
-        if (rep->iterates)
-            for (int64_t i = 0; i < rep->iterates_size && i < rep->iterates_capacity; ++i)
-                std::memcpy(rep->iterates + i * d, r.iterates[static_cast<size_t>(i)].data(), sizeof(double) * static_cast<size_t>(d));
-        rep->counters = {r.counters.sketch, r.counters.factor, r.counters.solve, r.counters.matvec};
-        rep->wall_seconds = r.wall_seconds;
-        const auto& t = r.tuning;
-        rep->tuning = {t.lam, t.Lam, t.mu_gd, t.c_gd, t.mu_p, t.beta_p, t.c_p};
-        rep->recompute_r_after_resketch = r.recompute_r_after_resketch;
     });
+}
+int ihs_oracle_solve_underdetermined(const double* A, int64_t n, int64_t d, int64_t lda, const double* b, double nu,
+                                     const ihs_solver_config* c, ihs_solve_report* rep) {
+    return oracle_solve(true, A, n, d, lda, b, nu, c, rep);
 }
 
 int ihs_oracle_fixed_sketch_ihs(const double* A, int64_t n, int64_t d, int64_t lda, const double* b, double nu,

@@ -62,6 +62,9 @@ def lib():
         L.ihs_oracle_rates_from_bounds.argtypes = [C.c_double, C.c_double, P(abi.Tuning)]
         L.ihs_oracle_gaussian_targets.argtypes = [C.c_double, C.c_double, C.c_int, d, d]
         L.ihs_oracle_srht_targets.argtypes = [C.c_double, d, d]
+        L.ihs_oracle_test_support_data.argtypes = [C.c_uint64, C.c_int64, C.c_int64, d, C.c_int64, d]
+        L.ihs_oracle_solve_underdetermined.argtypes = [d, C.c_int64, C.c_int64, C.c_int64, d, C.c_double,
+                                                       C.POINTER(abi.SolverConfigC), C.POINTER(abi.SolveReportC)]
         L.ihs_oracle_adaptive_solve.argtypes = [d, C.c_int64, C.c_int64, C.c_int64, d, C.c_double,
                                                 P(abi.SolverConfigC), P(abi.SolveReportC)]
         L.ihs_oracle_fixed_sketch_ihs.argtypes = [d, C.c_int64, C.c_int64, C.c_int64, d, C.c_double, d, C.c_int64,
@@ -222,6 +225,41 @@ def adaptive_solve(A, b, nu, cfg: abi.SolverConfigC, log_capacity=4096, iterates
     if its is not None:
         its = its[: rep.iterates_size]
     return x, rep, log, its
+
+
+def test_support_data(seed, rows, cols, vlen=0):
+    """proj/tests/support.hpp:32-47: (random_matrix(rows, cols, gen), random_vector(vlen, gen)) from
+    one std::mt19937_64(seed), the reference tests' own data."""
+    M = np.empty((rows, cols), order="F")
+    v = np.empty(vlen)
+    _check(lib().ihs_oracle_test_support_data(seed, rows, cols, _dp(M), vlen, _dp(v) if vlen else None))
+    return M, v
+
+
+def solve_underdetermined(A, b, nu, cfg: abi.SolverConfigC, log_capacity=4096, iterates_capacity=0):
+    """dual.hpp:13-33. Returns (x, z (dual_final), report-struct, log list, dual iterates)."""
+    A = _fortran(A)
+    n, d = A.shape
+    b = _f64(b)
+    x = np.empty(d)
+    z = np.empty(n)
+    rep = abi.SolveReportC()
+    rep.x = _dp(x)
+    rep.dual_final = _dp(z)
+    logbuf = (abi.IterationRecordC * log_capacity)()
+    rep.log = logbuf
+    rep.log_capacity = log_capacity
+    its = None
+    if iterates_capacity:
+        its = np.empty((iterates_capacity, n))
+        rep.iterates = _dp(its)
+        rep.iterates_capacity = iterates_capacity
+    _check(lib().ihs_oracle_solve_underdetermined(_dp(A), n, d, n, _dp(b), nu, C.byref(cfg), C.byref(rep)))
+    log = [(int(e.t), int(e.m), float(e.r), float(e.r_prev), int(e.branch))
+           for e in logbuf[: min(rep.log_size, log_capacity)]]
+    if its is not None:
+        its = its[: rep.iterates_size]
+    return x, z, rep, log, its
 
 
 def fixed_sketch_ihs(A, b, nu, SA, tuning: abi.Tuning, T, mode, x_start=None):

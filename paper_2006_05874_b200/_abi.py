@@ -109,6 +109,7 @@ class SolveReportC(C.Structure):
         ("recompute_r_after_resketch", C.c_int32),
         ("_pad", C.c_int32),
         ("times", PhaseTimes),
+        ("dual_final", C.POINTER(C.c_double)),
     ]
 
 

@@ -162,7 +162,9 @@ bool grad_rr_geometry(int64_t d, int64_t lda, int* R, int* ns);
 void grad_rr_run(const GradPlan& p, const double* Arm, const double* b, const double* X, int nrhs, double* work,
                  cudaStream_t st, const CandSpec* cs = nullptr);
 bool grad_rm_geometry(int64_t d, int64_t lda, int* R, int* ns);
-void transpose_to_rowmajor(const double* A, int64_t lda, int64_t rows, int64_t d, double* Arm, cudaStream_t st);
+// Arm[i * ldo + j] = A[i + j * lda] (i < rows, j < d); ldo = 0 means d
+void transpose_to_rowmajor(const double* A, int64_t lda, int64_t rows, int64_t d, double* Arm, cudaStream_t st,
+                           int64_t ldo = 0);
 void grad_rm_run(const GradPlan& p, const double* Arm, const double* b, const double* X, int nrhs, double* work,
                  cudaStream_t st);
 size_t grad_tma_smem(int64_t d, int R, int nrhs, int ns);

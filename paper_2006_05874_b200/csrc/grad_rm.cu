@@ -166,9 +166,9 @@ grad_rm_kernel(const double* __restrict__ Arm, int64_t d, int64_t npanels, const
         }
 }
 
-// row-major copy: Arm[i * d + j] = A[i + j * lda], 32x32 tiles through smem
+// row-major copy: Arm[i * ldo + j] = A[i + j * lda], 32x32 tiles through smem
 __global__ void transpose_kernel(const double* __restrict__ A, int64_t lda, int64_t rows, int64_t d,
-                                 double* __restrict__ Arm) {
+                                 double* __restrict__ Arm, int64_t ldo) {
     __shared__ double tile[32][33];
     const int64_t i0 = (int64_t)blockIdx.x * 32, j0 = (int64_t)blockIdx.y * 32;
     const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
@@ -179,7 +179,7 @@ __global__ void transpose_kernel(const double* __restrict__ A, int64_t lda, int6
     __syncthreads();
     for (int k = ty; k < 32; k += 8) {
         const int64_t i = i0 + k, j = j0 + tx;
-        if (i < rows && j < d) Arm[i * d + j] = tile[tx][k];
+        if (i < rows && j < d) Arm[i * ldo + j] = tile[tx][k];
     }
 }
 
@@ -451,9 +451,10 @@ bool grad_rm_geometry(int64_t d, int64_t lda, int* R, int* ns) {
     return false;
 }
 
-void transpose_to_rowmajor(const double* A, int64_t lda, int64_t rows, int64_t d, double* Arm, cudaStream_t st) {
+void transpose_to_rowmajor(const double* A, int64_t lda, int64_t rows, int64_t d, double* Arm, cudaStream_t st,
+                           int64_t ldo) {
     dim3 grid((unsigned)ceil_div(rows, 32), (unsigned)ceil_div(d, 32));
-    LAUNCH(transpose_kernel, grid, dim3(32, 8), 0, st, A, lda, rows, d, Arm);
+    LAUNCH(transpose_kernel, grid, dim3(32, 8), 0, st, A, lda, rows, d, Arm, ldo > 0 ? ldo : d);
 }
 
 void grad_rm_run(const GradPlan& p, const double* Arm, const double* b, const double* X, int nrhs, double* work,

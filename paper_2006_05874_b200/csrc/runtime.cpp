@@ -275,6 +275,10 @@ struct ihs_gpu_problem {
     DevBuf dots;                 // 24 doubles (4 per evaluation set + first/resketch decrements)
     PinnedBuf h_dots;
     cudaEvent_t set_ev[4] = {nullptr, nullptr, nullptr, nullptr};  // evaluation-set completion events
+    // underdetermined instances (dual.hpp): the dual problem in A^T, built on first use, and on the dual
+    // problem itself the observation vector subtracted from every gradient (non-owning, n doubles)
+    std::unique_ptr<ihs_gpu_problem> dual;
+    const double* gsub = nullptr;
     ~ihs_gpu_problem() {
         for (auto e : set_ev)
             if (e) cudaEventDestroy(e);
@@ -560,12 +564,79 @@ void problem_grad(ihs_gpu_problem* P, const double* X, int nrhs, double* G, cons
         grad_run(P->gplan, P->A.d(), P->b.d(), nu2, X, nrhs, G, P->grad_work.d(), P->st, P->Arm.d(), cs);
         if (P->timer) P->timer->mark(PH_GRAD);
     }
+    // dual problem (dual.hpp:20-22): g = M^T(M z) + nu^2 z - b
+    if (P->gsub)
+        for (int q = 0; q < nrhs; ++q) add_scaled(G + (int64_t)q * P->d, P->gsub, -1.0, P->d, P->st);
 }
 
 }  // namespace
 }  // namespace ihs_b200
 
 // ============================================================== C-ABI
+// Gradient plan (+ row-major copy of A when it fits), solver vectors, events and the phase
+// timer of a problem whose A and b are on the device.
+void finish_setup(ihs_gpu_problem* Q) {
+    Q->gplan = grad_plan(Q->n, Q->d, Q->lda, Q->num_sms);
+    {
+        // row-major copy of A for the gradient when it fits comfortably in HBM
+        size_t free_b = 0, total_b = 0;
+        CUDA_CHECK(cudaMemGetInfo(&free_b, &total_b));
+        const size_t need = (size_t)Q->lda * Q->d * sizeof(double);
+        GradPlan rm = Q->gplan;
+        if (need * 3 < free_b && grad_plan_use_rowmajor(rm)) {
+            Q->gplan = rm;
+            Q->Arm.ensure(need);
+            transpose_to_rowmajor(Q->A.d(), Q->lda, Q->lda, Q->d, Q->Arm.d(), Q->st);
+        } else {
+            grad_plan_attach_tma(Q->gplan, Q->A.d());
+        }
+    }
+    Q->grad_work.ensure(grad_work_doubles(Q->gplan) * sizeof(double));
+    Q->vecs.ensure((size_t)28 * Q->d * sizeof(double));
+    Q->dots.ensure(24 * sizeof(double));
+    Q->h_dots.ensure(24 * sizeof(double));
+    for (auto& e : Q->set_ev) CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    Q->timer = std::make_unique<PhaseTimer>(Q->st);
+    {
+        // IHS_PHASE_TIMER=0: no per-phase events (A/B of the timers' own cost)
+        const char* e = std::getenv("IHS_PHASE_TIMER");
+        Q->timer->enabled = !(e && e[0] == '0');
+    }
+}
+
+// The dual of an underdetermined instance (dual.hpp:13-33): an overdetermined ridge problem in
+// M = A^T (d x n), observation vector 0 and gradient M^T(M z) + nu^2 z - b, built on the device.
+ihs_gpu_problem* dual_problem(ihs_gpu_problem* P) {
+    if (P->dual) return P->dual.get();
+    auto D = std::make_unique<ihs_gpu_problem>();
+    D->device = P->device;
+    D->opts = P->opts;
+    D->opts.world_size = 1;
+    D->opts.n_global = P->d;
+    D->opts.row_offset = 0;
+    D->n = P->d;
+    D->d = P->n;
+    D->nu = P->nu;
+    D->orientation = IHS_OVERDETERMINED;
+    D->num_sms = P->num_sms;
+    D->st = P->st;  // shares the instance's stream (no owner: P owns it)
+    D->lda = ceil_div(D->n, 32) * 32;
+    D->A.ensure((size_t)D->lda * D->d * sizeof(double));
+    D->b.ensure((size_t)D->lda * sizeof(double));
+    CUDA_CHECK(cudaMemsetAsync(D->A.p, 0, (size_t)D->lda * D->d * sizeof(double), D->st));
+    CUDA_CHECK(cudaMemsetAsync(D->b.p, 0, (size_t)D->lda * sizeof(double), D->st));
+    // D->A[i + j * lda_D] = A[j + i * lda]: A's rows become M's columns
+    transpose_to_rowmajor(P->A.d(), P->lda, P->n, P->d, D->A.d(), D->st, D->lda);
+    D->gsub = P->b.d();
+    finish_setup(D.get());
+    CUDA_CHECK(cudaStreamSynchronize(D->st));
+    P->dual = std::move(D);
+    return P->dual.get();
+}
+
+
+void adaptive_solve_impl(ihs_gpu_problem* P, const ihs_solver_config* cfg, ihs_solve_report* rep);
+
 extern "C" {
 
 const char* ihs_gpu_last_error(void) { return ihs_b200::g_last_error.c_str(); }
@@ -726,8 +797,8 @@ ihs_status ihs_gpu_problem_create(const double* A, int64_t n, int64_t d, int64_t
             fail(IHS_INVALID_INPUT, "ProblemInstance: overdetermined orientation requires n >= d");
         if (orientation == IHS_UNDERDETERMINED && d < n_global)
             fail(IHS_INVALID_INPUT, "ProblemInstance: underdetermined orientation requires d >= n");
-        if (orientation == IHS_UNDERDETERMINED)
-            fail(IHS_INVALID_INPUT, "ihs_gpu: underdetermined (dual) instances are not on the GPU path yet");
+        if (orientation == IHS_UNDERDETERMINED && opts && opts->world_size > 1)
+            fail(IHS_INVALID_INPUT, "ihs_gpu: underdetermined (dual) instances run on a single GPU");
         auto P = std::make_unique<ihs_gpu_problem>();
         P->device = opts ? opts->device : 0;
         if (opts) P->opts = *opts;
@@ -757,32 +828,7 @@ ihs_status ihs_gpu_problem_create(const double* A, int64_t n, int64_t d, int64_t
         P->owner.s = P->st;
         StreamScope scope(P->st);
         alloc_and_upload(P.get(), A, lda, b);
-        P->gplan = grad_plan(n, d, P->lda, P->num_sms);
-        {
-            // row-major copy of A for the gradient when it fits comfortably in HBM
-            size_t free_b = 0, total_b = 0;
-            CUDA_CHECK(cudaMemGetInfo(&free_b, &total_b));
-            const size_t need = (size_t)P->lda * d * sizeof(double);
-            GradPlan rm = P->gplan;
-            if (need * 3 < free_b && grad_plan_use_rowmajor(rm)) {
-                P->gplan = rm;
-                P->Arm.ensure(need);
-                transpose_to_rowmajor(P->A.d(), P->lda, P->lda, d, P->Arm.d(), P->st);
-            } else {
-                grad_plan_attach_tma(P->gplan, P->A.d());
-            }
-        }
-        P->grad_work.ensure(grad_work_doubles(P->gplan) * sizeof(double));
-        P->vecs.ensure((size_t)28 * d * sizeof(double));
-        P->dots.ensure(24 * sizeof(double));
-        P->h_dots.ensure(24 * sizeof(double));
-        for (auto& e : P->set_ev) CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-        P->timer = std::make_unique<PhaseTimer>(P->st);
-        {
-            // IHS_PHASE_TIMER=0: no per-phase events (A/B of the timers' own cost)
-            const char* e = std::getenv("IHS_PHASE_TIMER");
-            P->timer->enabled = !(e && e[0] == '0');
-        }
+        finish_setup(P.get());
         CUDA_CHECK(cudaStreamSynchronize(P->st));
         *out = P.release();
     });
@@ -1023,11 +1069,54 @@ ihs_status ihs_gpu_system_solve(const ihs_gpu_system* S, const double* g, double
 ihs_status ihs_gpu_adaptive_solve(ihs_gpu_problem* P, const ihs_solver_config* cfg, ihs_solve_report* rep) {
     return guarded([&] {
         if (!P || !cfg || !rep || !rep->x) fail(IHS_INVALID_INPUT, "adaptive_solve: null argument");
-        DeviceGuard dgd(P->device);
-        StreamScope scope(P->st);
-        // solver.hpp:243-245 and :107-109
+        // solver.hpp:243-245
         if (P->orientation != IHS_OVERDETERMINED)
             fail(IHS_INVALID_INPUT, "adaptive_solve: expects an overdetermined instance (use solve_underdetermined for d > n)");
+        adaptive_solve_impl(P, cfg, rep);
+    });
+}
+
+// dual.hpp:13-33: adaptive IHS on the dual problem in A^T, primal x = A^T z
+ihs_status ihs_gpu_solve_underdetermined(ihs_gpu_problem* P, const ihs_solver_config* cfg, ihs_solve_report* rep) {
+    return guarded([&] {
+        if (!P || !cfg || !rep || !rep->x) fail(IHS_INVALID_INPUT, "solve_underdetermined: null argument");
+        if (P->orientation != IHS_UNDERDETERMINED)
+            fail(IHS_INVALID_INPUT, "solve_underdetermined: expects an underdetermined instance");
+        DeviceGuard dgd(P->device);
+        StreamScope scope(P->st);
+        ihs_gpu_problem* D = dual_problem(P);
+        const int64_t n = P->n, d = P->d;
+        std::vector<double> z((size_t)n);
+        ihs_solve_report rd = *rep;
+        rd.x = z.data();
+        adaptive_solve_impl(D, cfg, &rd);
+        double* x_out = rep->x;
+        double* dual_out = rep->dual_final;
+        *rep = rd;
+        rep->x = x_out;
+        rep->dual_final = dual_out;
+        if (dual_out) std::memcpy(dual_out, z.data(), (size_t)n * sizeof(double));
+        // x = A^T z = M z (M = A^T, d x n on the dual problem)
+        DevBuf dz, dx, work;
+        dz.ensure((size_t)n * sizeof(double));
+        dx.ensure((size_t)d * sizeof(double));
+        work.ensure((gemv_tiled_work_doubles(d, n) + 8) * sizeof(double));
+        gemv_tiled_reset(work.d(), d, n, P->st);
+        CUDA_CHECK(cudaMemcpyAsync(dz.p, z.data(), (size_t)n * sizeof(double), cudaMemcpyHostToDevice, P->st));
+        gemv_tiled(D->A.d(), d, n, D->lda, dz.d(), 1, n, dx.d(), d, work.d(), P->st);
+        CUDA_CHECK(cudaMemcpyAsync(x_out, dx.p, (size_t)d * sizeof(double), cudaMemcpyDeviceToHost, P->st));
+        CUDA_CHECK(cudaStreamSynchronize(P->st));
+    });
+}
+
+}  // extern "C"
+
+// The adaptive loop (solver.hpp:106-232) on a device problem; throws Status.
+void adaptive_solve_impl(ihs_gpu_problem* P, const ihs_solver_config* cfg, ihs_solve_report* rep) {
+    {
+        DeviceGuard dgd(P->device);
+        StreamScope scope(P->st);
+        // solver.hpp:107-109
         if (!(cfg->eps > 0.0 && cfg->eps < 1.0)) fail(IHS_INVALID_INPUT, "adaptive_solve: eps must be in (0,1)");
         if (cfg->m_initial < 1) fail(IHS_INVALID_INPUT, "adaptive_solve: m_initial must be >= 1");
         if (cfg->max_iters < 1) fail(IHS_INVALID_INPUT, "adaptive_solve: max_iters must be >= 1");
@@ -1348,8 +1437,10 @@ ihs_status ihs_gpu_adaptive_solve(ihs_gpu_problem* P, const ihs_solver_config* c
         rep->times.solve_ms = ph[PH_SOLVE];
         rep->times.kernel_launches = g_launches.load() - launches0;
         sys.st = nullptr;  // owned by the problem
-    });
+    }
 }
+
+extern "C" {
 
 ihs_status ihs_gpu_fixed_sketch_ihs(ihs_gpu_problem* P, const ihs_gpu_system* S, const ihs_tuning* tp, int64_t T,
                                     int32_t mode, const double* x_start, double* iterates_out) {

@@ -26,6 +26,7 @@
 #include "tma.cuh"
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cmath>
 #include <vector>
@@ -570,8 +571,10 @@ srht_stream_kernel(const __grid_constant__ ChunkMaps maps, const double* __restr
                    int64_t nfull, const uint32_t* __restrict__ signbits, double* __restrict__ T, int64_t n_pad,
                    int64_t d, int lcpc, int G, int nslot, int ng, const int4* __restrict__ tiles, int n_tiles,
                    const int2* __restrict__ entries, int lo, double s1, double s2, double* __restrict__ SA, int64_t m,
-                   int* __restrict__ ctl, const uint32_t* __restrict__ mask, int logw, int dbg) {
+                   int* __restrict__ ctl, const uint32_t* __restrict__ mask, int logw, int dbg,
+                   unsigned long long* __restrict__ prof) {
     extern __shared__ unsigned char stream_raw[];
+    const long long t_start = clock64();
     double* base = align1024(stream_raw);
     double* xs_all = base + kP1Warps * 2 * kChunkDoubles;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -590,14 +593,18 @@ srht_stream_kernel(const __grid_constant__ ChunkMaps maps, const double* __restr
         const int64_t workers = (int64_t)gridDim.x * kEmitGroups;
         const int64_t me = (int64_t)blockIdx.x * kEmitGroups + k;
         int64_t first = 0;
+        long long w_wait = 0, w_busy = 0;
         for (int g = 0; g < ng; ++g) {
             const int gc = group_cols(g);
             const int items = gc * n_tiles;
             const int i0 = (int)((me - first % workers + workers) % workers);
             first += items;
             if (i0 >= items) continue;
+            const long long tw0 = clock64();
             if (t == 0) spin_until(done1 + g, (int)(gc * cpc));
             bar();
+            const long long tw1 = clock64();
+            w_wait += tw1 - tw0;
             int mine = 0;
             for (int i = i0; i < items; i += (int)workers) {
                 const int jj = i / n_tiles;
@@ -609,6 +616,13 @@ srht_stream_kernel(const __grid_constant__ ChunkMaps maps, const double* __restr
                 ++mine;
             }
             if (t == 0) atomicAdd(done2 + g, mine);
+            w_busy += clock64() - tw1;
+        }
+        if (prof && t == 0) {
+            atomicAdd(prof + 4, (unsigned long long)w_wait);
+            atomicAdd(prof + 5, (unsigned long long)w_busy);
+            atomicAdd(prof + 6, (unsigned long long)(clock64() - t_start));
+            atomicAdd(prof + 8, 1ull);
         }
         return;
     }
@@ -630,9 +644,12 @@ srht_stream_kernel(const __grid_constant__ ChunkMaps maps, const double* __restr
     };
     // finished-chunk counts not yet published: one release fence covers them all
     int pend_g[kFlushChunks], pend_c[kFlushChunks], npend = 0, since = 0;
+    long long c_spin = 0, c_mbar = 0, c_flush = 0;
     auto flush = [&]() {
         if (!npend) return;
+        const long long f0 = clock64();
         if (!(dbg & 2)) __threadfence();
+        c_flush += clock64() - f0;
         __syncwarp();
         if (lane == 0)
             for (int i = 0; i < npend; ++i) atomicAdd(done1 + pend_g[i], pend_c[i]);
@@ -652,14 +669,18 @@ srht_stream_kernel(const __grid_constant__ ChunkMaps maps, const double* __restr
             if (g >= nslot && !(dbg & 1)) {
                 // about to wait on the emits of group g - nslot: publish first
                 flush();
+                const long long s0 = clock64();
                 if (lane == 0) spin_until(done2 + g - nslot, group_cols(g - nslot) * n_tiles);
                 __syncwarp();
+                c_spin += clock64() - s0;
             }
         }
         const int64_t q = chunk & cmask, r0 = q << kChunkL;
         double* buf = ring + slot * kChunkDoubles;
         if (q < nfull) {
+            const long long m0 = clock64();
             tma::mbar_wait(&bars[slot], (parity >> slot) & 1u);
+            c_mbar += clock64() - m0;
             parity ^= 1u << slot;
         } else {
             p1_sync_load(buf, A + (int64_t)j * lda, n, r0);
@@ -677,6 +698,13 @@ srht_stream_kernel(const __grid_constant__ ChunkMaps maps, const double* __restr
         slot ^= 1;
     }
     flush();
+    if (prof && lane == 0) {
+        atomicAdd(prof + 0, (unsigned long long)c_spin);
+        atomicAdd(prof + 1, (unsigned long long)c_mbar);
+        atomicAdd(prof + 2, (unsigned long long)c_flush);
+        atomicAdd(prof + 3, (unsigned long long)(clock64() - t_start));
+        atomicAdd(prof + 7, 1ull);
+    }
 }
 
 // Row-sharded SRHT combine (H_{n_pad} = H_P (x) H_{n_pad/P}, shard index =
@@ -831,9 +859,26 @@ void launch_stream(const SrhtPlan& p, const ChunkMaps& maps, int64_t nfull, cons
     }
     const int ng = (int)ceil_div(p.d, G);
     CUDA_CHECK(cudaMemsetAsync(ctl, 0, 2 * sizeof(int) * (size_t)ng, st));
+    // IHS_SRHT_STREAM_PROF=1: per-role cycle accounting of the pipeline (debug, prints to stderr)
+    static const bool prof_on = std::getenv("IHS_SRHT_STREAM_PROF") != nullptr;
+    static unsigned long long* prof = nullptr;
+    if (prof_on && !prof) CUDA_CHECK(cudaMalloc(&prof, 16 * sizeof(unsigned long long)));
+    if (prof_on) CUDA_CHECK(cudaMemsetAsync(prof, 0, 16 * sizeof(unsigned long long), st));
     LAUNCH(srht_stream_kernel<HB>, (unsigned)grid, kStreamThreads, kStreamSmem, st, maps, A, p.n, p.lda, nfull,
            signbits, T, p.n_pad, p.d, p.logn - kChunkL, G, nslot, ng, tiles, n_tiles, entries, p.pass_lo[0], p.scale1,
-           p.scale2, SA, p.m, ctl, mask, logw, stream_dbg());
+           p.scale2, SA, p.m, ctl, mask, logw, stream_dbg(), prof_on ? prof : nullptr);
+    if (prof_on) {
+        unsigned long long h[16];
+        CUDA_CHECK(cudaMemcpyAsync(h, prof, sizeof(h), cudaMemcpyDeviceToHost, st));
+        CUDA_CHECK(cudaStreamSynchronize(st));
+        const double p1n = (double)std::max(1ull, h[7]), p2n = (double)std::max(1ull, h[8]);
+        fprintf(stderr,
+                "[srht stream m=%lld G=%d nslot=%d tiles=%d] P1 warps %llu: total %.0f cyc, slot-wait %.1f%%, tma-wait "
+                "%.1f%%, fence %.1f%% | P2 groups %llu: total %.0f cyc, done1-wait %.1f%%, busy %.1f%%\n",
+                (long long)p.m, G, nslot, n_tiles, h[7], h[3] / p1n, 100.0 * h[0] / std::max(1ull, h[3]),
+                100.0 * h[1] / std::max(1ull, h[3]), 100.0 * h[2] / std::max(1ull, h[3]), h[8], h[6] / p2n,
+                100.0 * h[4] / std::max(1ull, h[6]), 100.0 * h[5] / std::max(1ull, h[6]));
+    }
 }
 using StreamFn = void (*)(const SrhtPlan&, const ChunkMaps&, int64_t, const double*, const uint32_t*, double*, int, int,
                           const int4*, int, const int2*, double*, int*, int, const uint32_t*, int, cudaStream_t);

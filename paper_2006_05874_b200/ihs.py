@@ -562,29 +562,33 @@ class SolveReport:  # solver.hpp:70-87
     tuning: TuningParams = field(default_factory=TuningParams)
     recompute_r_after_resketch: bool = True
     device_times: dict = field(default_factory=dict)
+    dual_final: Optional[np.ndarray] = None  # underdetermined solves (solver.hpp:82)
 
 
-def adaptive_solve(p: ProblemInstance, cfg: SolverConfig, log_capacity: int = 1 << 14) -> SolveReport:
-    """Adaptive Polyak-IHS (solver.hpp:242-250) on the device-resident problem."""
-    if p.orientation() != Orientation.Overdetermined:
-        raise InvalidInput("adaptive_solve: expects an overdetermined instance (use solve_underdetermined for d > n)")
-    d = p.cols()
-    c, keep = cfg._c(p.A())
-    x = np.empty(d)
+def _run_solve(fn, p: ProblemInstance, cfg: SolverConfig, dim: int, sketch_matrix, out_dim: int,
+               log_capacity: int, dual: bool) -> SolveReport:
+    c, keep = cfg._c(sketch_matrix)
+    x = np.empty(out_dim)
     rep = abi.SolveReportC()
     rep.x = abi.dptr(x)
+    z = None
+    if dual:
+        z = np.empty(dim)
+        rep.dual_final = abi.dptr(z)
     logbuf = (abi.IterationRecordC * log_capacity)()
     rep.log = logbuf
     rep.log_capacity = log_capacity
     its = None
     if cfg.record_iterates:
         cap = cfg.max_iters + 1
-        its = np.empty((cap, d))
+        its = np.empty((cap, dim))
         rep.iterates = abi.dptr(its)
         rep.iterates_capacity = cap
-    _check(lib().ihs_gpu_adaptive_solve(p.handle, C.byref(c), C.byref(rep)))
+    _check(fn(p.handle, C.byref(c), C.byref(rep)))
     del keep
     out = SolveReport(x=x)
+    if z is not None:
+        out.dual_final = z
     out.iterations, out.rejections, out.final_m = int(rep.iterations), int(rep.rejections), int(rep.final_m)
     out.r1, out.r_final = float(rep.r1), float(rep.r_final)
     out.converged, out.sketch_exhausted = bool(rep.converged), bool(rep.sketch_exhausted)
@@ -598,6 +602,22 @@ def adaptive_solve(p: ProblemInstance, cfg: SolverConfig, log_capacity: int = 1 
     out.recompute_r_after_resketch = bool(rep.recompute_r_after_resketch)
     out.device_times = rep.times.as_dict()
     return out
+
+
+def adaptive_solve(p: ProblemInstance, cfg: SolverConfig, log_capacity: int = 1 << 14) -> SolveReport:
+    """Adaptive Polyak-IHS (solver.hpp:242-250) on the device-resident problem."""
+    if p.orientation() != Orientation.Overdetermined:
+        raise InvalidInput("adaptive_solve: expects an overdetermined instance (use solve_underdetermined for d > n)")
+    return _run_solve(lib().ihs_gpu_adaptive_solve, p, cfg, p.cols(), p.A(), p.cols(), log_capacity, False)
+
+
+def solve_underdetermined(p: ProblemInstance, cfg: SolverConfig, log_capacity: int = 1 << 14) -> SolveReport:
+    """Underdetermined case through the dual (dual.hpp:13-33): adaptive IHS on the ridge problem in A^T with
+    gradient A(A^T z) - b + nu^2 z (SRHT pads d); x = A^T z_T, dual_final = z_T, iterates hold the dual trace."""
+    if p.orientation() != Orientation.Underdetermined:
+        raise InvalidInput("solve_underdetermined: expects an underdetermined instance")
+    return _run_solve(lib().ihs_gpu_solve_underdetermined, p, cfg, p.rows(), np.asfortranarray(p.A().T), p.cols(),
+                      log_capacity, True)
 
 
 def fixed_sketch_ihs(p: ProblemInstance, sys: SketchedSystem, tp: TuningParams, T: int, mode: FixedMode,

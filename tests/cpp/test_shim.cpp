@@ -37,6 +37,38 @@ static Vector random_vector(Index n, std::mt19937_64& gen) {
     return v;
 }
 
+// x = A^T (A A^T + nu^2 I)^{-1} b (support.hpp ridge_kernel_form), Gauss-Jordan on the small n x n system
+static Vector ridge_kernel_form(const Matrix& A, const Vector& b, double nu) {
+    const Index n = A.rows(), d = A.cols();
+    std::vector<double> K(static_cast<size_t>(n * n)), rhs(static_cast<size_t>(n));
+    for (Index i = 0; i < n; ++i) {
+        for (Index j = 0; j < n; ++j) {
+            double s = 0.0;
+            for (Index k = 0; k < d; ++k) s += A(i, k) * A(j, k);
+            K[static_cast<size_t>(i + j * n)] = s + (i == j ? nu * nu : 0.0);
+        }
+        rhs[static_cast<size_t>(i)] = b(i);
+    }
+    for (Index c = 0; c < n; ++c) {
+        const double piv = K[static_cast<size_t>(c + c * n)];
+        for (Index j = 0; j < n; ++j) K[static_cast<size_t>(c + j * n)] /= piv;
+        rhs[static_cast<size_t>(c)] /= piv;
+        for (Index r = 0; r < n; ++r) {
+            if (r == c) continue;
+            const double f = K[static_cast<size_t>(r + c * n)];
+            for (Index j = 0; j < n; ++j) K[static_cast<size_t>(r + j * n)] -= f * K[static_cast<size_t>(c + j * n)];
+            rhs[static_cast<size_t>(r)] -= f * rhs[static_cast<size_t>(c)];
+        }
+    }
+    Vector x(d);
+    for (Index k = 0; k < d; ++k) {
+        double s = 0.0;
+        for (Index i = 0; i < n; ++i) s += A(i, k) * rhs[static_cast<size_t>(i)];
+        x(k) = s;
+    }
+    return x;
+}
+
 int main() {
     // ---- test_sketch.cpp
     {
@@ -177,6 +209,47 @@ int main() {
         cfg.sketch_override = [](const Matrix& M, Index, std::uint64_t) { return M; };
         SolveReport r = adaptive_solve(p, cfg);
         CHECK(r.converged && r.rejections == 0 && r.iterations == 2 && r.counters.sketch == 0);
+    }
+    // ---- test_dual.cpp (solve_underdetermined, dual.hpp:13-33)
+    {
+        Matrix A(1, 2);
+        A(0, 0) = 1.0;
+        A(0, 1) = 1.0;
+        ProblemInstance p(A, Vector{2.0}, 1.0, Orientation::Underdetermined);
+        SolverConfig cfg;
+        cfg.eps = 1e-14;
+        SolveReport rep = solve_underdetermined(p, cfg);
+        CHECK(rep.converged);
+        CHECK(std::abs(rep.x(0) - 2.0 / 3.0) <= 1e-8 && std::abs(rep.x(1) - 2.0 / 3.0) <= 1e-8);
+        CHECK(rep.dual_final.size() == 1 && std::abs(rep.dual_final(0) - 2.0 / 3.0) <= 1e-8);
+    }
+    {
+        std::mt19937_64 gen(61);
+        ProblemInstance p(random_matrix(4, 12, gen), Vector::Zero(4), 0.5, Orientation::Underdetermined);
+        SolveReport rep = solve_underdetermined(p, SolverConfig{});
+        CHECK(rep.converged && rep.x.norm() == 0.0);
+    }
+    {
+        std::mt19937_64 gen(62);
+        Matrix A = random_matrix(16, 64, gen);
+        Vector b = random_vector(16, gen);
+        ProblemInstance p(A, b, 0.8, Orientation::Underdetermined);
+        Vector x_ref = ridge_kernel_form(A, b, 0.8);
+        for (SketchKind k : {SketchKind::Gaussian, SketchKind::SRHT}) {
+            SolverConfig cfg;
+            cfg.eps = 1e-18;
+            cfg.sketch_kind = k;
+            if (k == SketchKind::SRHT) cfg.rho = 0.25;
+            SolveReport rep = solve_underdetermined(p, cfg);
+            CHECK(rep.converged);
+            CHECK(rep.final_m <= next_pow2(64));
+            CHECK((rep.x - x_ref).norm() <= 1e-8 * (1.0 + x_ref.norm()));
+        }
+    }
+    {
+        std::mt19937_64 gen(64);
+        ProblemInstance p(random_matrix(8, 3, gen), random_vector(8, gen), 1.0, Orientation::Overdetermined);
+        CHECK_THROWS_AS(solve_underdetermined(p, SolverConfig{}), InvalidInput);
     }
     std::printf("shim tests: %d passed, %d failed\n", g_pass, g_fail);
     return g_fail;

@@ -243,6 +243,44 @@ def test_adaptive_solve_matches_oracle(gpu, O, kind, mode, seed):
     assert _abar_rel(A, nu, rep.x, x_ref) <= 1e-10
 
 
+# ----------------------------------------------------------------- dual (dual.hpp:13-33)
+@pytest.mark.parametrize("kind,rho,n,d,seed", [(0, 0.1, 16, 64, 62), (1, 0.25, 16, 64, 62), (1, 0.25, 12, 48, 63),
+                                               (0, 0.15, 100, 700, 5), (1, 0.2, 300, 1000, 6)])
+def test_solve_underdetermined_matches_oracle(gpu, O, kind, rho, n, d, seed):
+    A, b = O.test_support_data(seed, n, d, n)
+    nu = 0.8
+    cfg, c_or = _cfg_pair(gpu, O, sketch_kind=gpu.SketchKind(kind), rho=rho, eps=1e-12)
+    p = gpu.ProblemInstance(A, b, nu, gpu.Orientation.Underdetermined)
+    rep = gpu.solve_underdetermined(p, cfg)
+    x_ref, z_ref, rep_ref, log_ref, _ = O.solve_underdetermined(A, b, nu, c_or)
+    assert rep.converged == bool(rep_ref.converged)
+    assert rep.rejections == rep_ref.rejections and rep.final_m == rep_ref.final_m
+    assert rep.iterations == rep_ref.iterations
+    assert [(e.t, e.m, int(e.branch)) for e in rep.log] == [(l[0], l[1], l[4]) for l in log_ref]
+    assert rep.counters.sketch == rep_ref.counters.sketch and rep.counters.matvec == rep_ref.counters.matvec
+    assert rep.counters.factor == rep_ref.counters.factor and rep.counters.solve == rep_ref.counters.solve
+    assert rep.dual_final.shape == (n,) and rep.x.shape == (d,)
+    np.testing.assert_allclose(rep.x, A.T @ rep.dual_final, rtol=1e-11, atol=1e-11 * np.abs(rep.x).max())
+    assert np.linalg.norm(rep.x - x_ref) <= 1e-8 * (1.0 + np.linalg.norm(x_ref))
+
+
+def test_solve_underdetermined_reference_cases(gpu, O):
+    # test_dual.cpp:10-31, 81-87
+    p = gpu.ProblemInstance(np.array([[1.0, 1.0]]), [2.0], 1.0, gpu.Orientation.Underdetermined)
+    rep = gpu.solve_underdetermined(p, gpu.SolverConfig(eps=1e-14))
+    assert rep.converged and np.allclose(rep.x, [2 / 3, 2 / 3], rtol=1e-8) and np.allclose(rep.dual_final, [2 / 3])
+    A, _ = O.test_support_data(61, 4, 12)
+    p = gpu.ProblemInstance(A, np.zeros(4), 0.5, gpu.Orientation.Underdetermined)
+    rep = gpu.solve_underdetermined(p, gpu.SolverConfig())
+    assert rep.converged and np.linalg.norm(rep.x) == 0.0
+    A, b = O.test_support_data(64, 8, 3, 8)
+    with pytest.raises(gpu.InvalidInput):
+        gpu.solve_underdetermined(gpu.ProblemInstance(A, b, 1.0), gpu.SolverConfig())
+    with pytest.raises(gpu.InvalidInput):
+        gpu.adaptive_solve(gpu.ProblemInstance(np.array([[1.0, 1.0]]), [2.0], 1.0, gpu.Orientation.Underdetermined),
+                           gpu.SolverConfig())
+
+
 def test_adaptive_solve_deterministic(gpu, O):
     A, b, _ = O.synth(1024, 32, decay=0.95, data_seed=9)
     p = gpu.ProblemInstance(A, b, 0.2)

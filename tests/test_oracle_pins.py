@@ -204,3 +204,54 @@ def test_synth_spectrum(O):
     col = np.linalg.norm(A, axis=0) / np.sqrt(4096)
     np.testing.assert_allclose(col, 0.5 ** np.arange(1, 9), rtol=0.05)
     np.testing.assert_array_equal(b, np.array([sum(A[i, j] * xt[j] for j in range(8)) for i in range(4096)]))
+
+
+# ------------------------------------------------------------ dual.hpp (test_dual.cpp, with the reference tests'
+# own data: support.hpp's random_matrix / random_vector replayed by O.test_support_data)
+def _ridge_kernel_form(A, b, nu):
+    return A.T @ np.linalg.solve(A @ A.T + nu * nu * np.eye(A.shape[0]), b)
+
+
+def test_dual_hand_example(O):  # test_dual.cpp:10-22
+    x, z, rep, log, _ = O.solve_underdetermined(np.array([[1.0, 1.0]]), np.array([2.0]), 1.0,
+                                                O.default_config(eps=1e-14))
+    assert rep.converged
+    assert abs(x[0] - 2 / 3) <= 1e-8 * 2 / 3 and abs(x[1] - 2 / 3) <= 1e-8 * 2 / 3
+    assert z.shape == (1,) and abs(z[0] - 2 / 3) <= 1e-8 * 2 / 3
+
+
+def test_dual_zero_observations(O):  # test_dual.cpp:24-31
+    A, _ = O.test_support_data(61, 4, 12)
+    x, z, rep, log, _ = O.solve_underdetermined(A, np.zeros(4), 0.5, O.default_config())
+    assert rep.converged and np.linalg.norm(x) == 0.0
+
+
+@pytest.mark.parametrize("kind,rho", [(0, 0.1), (1, 0.25)])
+def test_dual_matches_kernel_form(O, kind, rho):  # test_dual.cpp:33-56
+    A, b = O.test_support_data(62, 16, 64, 16)
+    x_ref = _ridge_kernel_form(A, b, 0.8)
+    x, z, rep, log, _ = O.solve_underdetermined(A, b, 0.8, O.default_config(eps=1e-18, sketch_kind=kind, rho=rho))
+    assert rep.converged and rep.final_m <= 64
+    assert np.linalg.norm(x - x_ref) <= 1e-8 * (1.0 + np.linalg.norm(x_ref))
+    # counters: the dual gradient's 2nd + d + 2n per evaluation (dual.hpp:23-27)
+    evals = rep.iterations + sum(1 for l in log if l[4] == O.abi.STEP_RESKETCH)
+    assert rep.counters.matvec % (2 * 16 * 64 + 64 + 2 * 16) == 0
+
+
+def test_dual_transfer_bound(O):  # test_dual.cpp:58-79
+    A, b = O.test_support_data(63, 12, 48, 12)
+    nu = 0.9
+    x_ref = _ridge_kernel_form(A, b, nu)
+    x, z, rep, log, _ = O.solve_underdetermined(A, b, nu, O.default_config(eps=1e-12, sketch_kind=1, rho=0.25))
+    assert rep.converged
+    sigma1 = np.linalg.svd(A, compute_uv=False)[0]
+    f_star = 0.5 * np.linalg.norm(A @ x_ref - b) ** 2 + 0.5 * nu * nu * np.linalg.norm(x_ref) ** 2
+    bound = 10.0 * np.sqrt(2.0 * 1e-12 * f_star) * sigma1 / (nu * nu)
+    assert np.linalg.norm(x - x_ref) / (1.0 + np.linalg.norm(x_ref)) <= bound
+
+
+def test_dual_rejects_overdetermined(O):  # test_dual.cpp:81-87
+    A, b = O.test_support_data(64, 8, 3, 8)
+    with pytest.raises(O.OracleError) as e:
+        O.solve_underdetermined(A, b, 1.0, O.default_config())
+    assert e.value.status == O.abi.IHS_INVALID_INPUT
