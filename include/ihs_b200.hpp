@@ -199,6 +199,14 @@ inline Vector gradient(const ProblemInstance& p, const Vector& x, CostCounters* 
     return g;
 }
 
+// problem.hpp:104-109
+inline double prediction_error(const ProblemInstance& p, const Vector& x, const Vector& x_star) {
+    if (x.size() != p.cols() || x_star.size() != p.cols()) throw InvalidInput("prediction_error: dimension mismatch");
+    double out = 0.0;
+    detail::check(ihs_gpu_prediction_error(p.handle(), x.data(), x_star.data(), &out));
+    return out;
+}
+
 // ------------------------------------------------------------ sketch.hpp
 enum class SketchKind { Gaussian, SRHT };
 struct SketchConfig { SketchKind kind = SketchKind::Gaussian; Index m = 1; std::uint64_t seed = 0; };

@@ -265,6 +265,8 @@ ihs_status ihs_newton_decrement(const double* g, const double* gt, int64_t d, do
  * decision, exactly as in the reference control flow. */
 /* solve_underdetermined (dual.hpp:13-33): adaptive IHS on the dual ridge problem in A^T (gradient
  * A(A^T z) - b + nu^2 z, SRHT pads d); rep->x receives x = A^T z_T (d doubles), rep->dual_final z_T. */
+/* prediction_error (problem.hpp:104-109): 1/2 ||A(x - x*)||^2 + nu^2/2 ||x - x*||^2; x, x_star: d doubles */
+ihs_status ihs_gpu_prediction_error(ihs_gpu_problem* p, const double* x, const double* x_star, double* out);
 ihs_status ihs_gpu_solve_underdetermined(ihs_gpu_problem* p, const ihs_solver_config* cfg, ihs_solve_report* rep);
 ihs_status ihs_gpu_adaptive_solve(ihs_gpu_problem* p, const ihs_solver_config* cfg, ihs_solve_report* rep);
 

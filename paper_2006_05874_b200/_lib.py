@@ -68,6 +68,7 @@ def lib():
         "ihs_newton_decrement": (C.c_int, [d, d, i64, d]),
         "ihs_gpu_adaptive_solve": (C.c_int, [vp, P(abi.SolverConfigC), P(abi.SolveReportC)]),
         "ihs_gpu_solve_underdetermined": (C.c_int, [vp, P(abi.SolverConfigC), P(abi.SolveReportC)]),
+        "ihs_gpu_prediction_error": (C.c_int, [vp, d, d, d]),
         "ihs_gpu_fixed_sketch_ihs": (C.c_int, [vp, vp, P(abi.Tuning), i64, i32, d, d]),
         "ihs_synth_generate": (C.c_int, [P(abi.SynthSpec), i64, i64, d, i64, d, d]),
         "ihs_gpu_shard_rows": (C.c_int, [i64, i32, i32, P(i64), P(i64)]),
@@ -92,7 +93,7 @@ EXPORTED_SYMBOLS = (
     "ihs_gpu_sketch_matrix", "ihs_gpu_rademacher_bits", "ihs_gpu_fill_gaussian", "ihs_gpu_mt19937_64",
     "ihs_sample_without_replacement", "ihs_gpu_system_factorize", "ihs_gpu_system_destroy", "ihs_gpu_system_kind",
     "ihs_gpu_system_m", "ihs_gpu_system_d", "ihs_gpu_system_factor_flops", "ihs_gpu_system_flops_per_solve",
-    "ihs_gpu_system_solve", "ihs_newton_decrement", "ihs_gpu_adaptive_solve", "ihs_gpu_solve_underdetermined", "ihs_gpu_fixed_sketch_ihs",
+    "ihs_gpu_system_solve", "ihs_newton_decrement", "ihs_gpu_adaptive_solve", "ihs_gpu_solve_underdetermined", "ihs_gpu_prediction_error", "ihs_gpu_fixed_sketch_ihs",
     "ihs_synth_generate", "ihs_gpu_shard_rows", "ihs_gpu_nccl_unique_id", "ihs_gpu_nccl_comm_create",
     "ihs_gpu_nccl_comm_destroy", "ihs_gpu_sketch_sharded_emulated",
 )

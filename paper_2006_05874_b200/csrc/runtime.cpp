@@ -879,6 +879,33 @@ ihs_status ihs_gpu_gradient(ihs_gpu_problem* P, const double* x, double* g, ihs_
     });
 }
 
+// problem.hpp:104-109: 1/2 ||A (x - x*)||^2 + nu^2/2 ||x - x*||^2 (one tiled mat-vec over A)
+ihs_status ihs_gpu_prediction_error(ihs_gpu_problem* P, const double* x, const double* x_star, double* out) {
+    return guarded([&] {
+        if (!P || !x || !x_star || !out) fail(IHS_INVALID_INPUT, "prediction_error: dimension mismatch");
+        DeviceGuard dg(P->device);
+        StreamScope scope(P->st);
+        const int64_t n = P->n, d = P->d;
+        DevBuf v, r, work, dots;
+        v.ensure((size_t)2 * d * sizeof(double));
+        r.ensure((size_t)n * sizeof(double));
+        work.ensure((gemv_tiled_work_doubles(n, d) + 8) * sizeof(double));
+        dots.ensure(8 * sizeof(double));
+        gemv_tiled_reset(work.d(), n, d, P->st);
+        CUDA_CHECK(cudaMemcpyAsync(v.p, x, (size_t)d * sizeof(double), cudaMemcpyHostToDevice, P->st));
+        CUDA_CHECK(cudaMemcpyAsync(v.d() + d, x_star, (size_t)d * sizeof(double), cudaMemcpyHostToDevice, P->st));
+        add_scaled(v.d(), v.d() + d, -1.0, d, P->st);  // diff = x - x*
+        gemv_tiled(P->A.d(), n, d, P->lda, v.d(), 1, d, r.d(), n, work.d(), P->st);
+        decrement_dots(r.d(), r.d(), n, 1, dots.d(), P->st);          // ||A diff||^2 (local rows)
+        decrement_dots(v.d(), v.d(), d, 1, dots.d() + 2, P->st);      // ||diff||^2
+        if (P->opts.world_size > 1) nccl_allreduce_sum(dots.d(), 1, P->opts.nccl_comm, P->st);
+        double h[4];
+        CUDA_CHECK(cudaMemcpyAsync(h, dots.p, sizeof(h), cudaMemcpyDeviceToHost, P->st));
+        CUDA_CHECK(cudaStreamSynchronize(P->st));
+        *out = 0.5 * h[0] + 0.5 * P->nu * P->nu * h[2];
+    });
+}
+
 ihs_status ihs_gpu_sketch(ihs_gpu_problem* P, int32_t kind, int64_t m, uint64_t seed, double* SA_out,
                           ihs_counters* c) {
     return guarded([&] {

@@ -344,6 +344,17 @@ def gradient(p: ProblemInstance, x, counters: Optional[CostCounters] = None) -> 
     return g
 
 
+def prediction_error(p: ProblemInstance, x, x_star) -> float:
+    """1/2 ||A (x - x*)||^2 + nu^2/2 ||x - x*||^2 (problem.hpp:104-109), on the device."""
+    x = np.ascontiguousarray(np.asarray(x, dtype=np.float64).reshape(-1))
+    xs = np.ascontiguousarray(np.asarray(x_star, dtype=np.float64).reshape(-1))
+    if x.size != p.cols() or xs.size != p.cols():
+        raise InvalidInput("prediction_error: dimension mismatch")
+    out = C.c_double()
+    _check(lib().ihs_gpu_prediction_error(p.handle, abi.dptr(x), abi.dptr(xs), C.byref(out)))
+    return float(out.value)
+
+
 # ------------------------------------------------------------------ sketch.hpp
 def fwht_inplace(v: np.ndarray) -> np.ndarray:
     """In-place normalized FWHT on the device (sketch.hpp:33-49)."""

@@ -160,6 +160,19 @@ def test_gradient_vs_oracle(gpu, O, n, d):
     assert np.linalg.norm(g - g_ref) <= 1e-12 * (np.linalg.norm(g_ref) + np.linalg.norm(A) * np.linalg.norm(b))
 
 
+@pytest.mark.parametrize("n,d", [(100, 3), (70000, 512), (5000, 130)])
+def test_prediction_error_vs_oracle(gpu, O, n, d):
+    A = rand_mat(n + 1, n, d)
+    b = RNG(3).standard_normal(n)
+    x, xs = RNG(4).standard_normal(d), RNG(5).standard_normal(d)
+    p = gpu.ProblemInstance(A, b, 0.3)
+    ref = O.prediction_error(A, b, 0.3, x, xs)
+    assert abs(gpu.prediction_error(p, x, xs) - ref) <= 1e-12 * ref
+    assert gpu.prediction_error(p, x, x) == 0.0
+    with pytest.raises(gpu.InvalidInput):
+        gpu.prediction_error(p, x[:-1], xs)
+
+
 def test_system_known_answers(gpu):
     sys = gpu.SketchedSystem.factorize(np.zeros((3, 4)), 2.0)
     g = np.array([4.0, -8.0, 0.0, 2.0])
