@@ -201,6 +201,14 @@ struct PhaseTimer {
         }
     }
 };
+// cap on the SRHT phase-1 scratch (larger sketches run over column batches); IHS_SRHT_SCRATCH_CAP_MB
+// overrides it (tests exercise the batched path on small problems)
+const int64_t kSrhtScratchCap = [] {
+    const char* e = std::getenv("IHS_SRHT_SCRATCH_CAP_MB");
+    const long long mb = e ? std::atoll(e) : 0;
+    return mb > 0 ? (int64_t)mb << 20 : (int64_t)16 << 30;
+}();
+
 // PH_SKETCH_KERNEL: the sketch's main kernels inside a PH_SKETCH interval
 // PH_GRAD_KERNEL: the gradient kernels (grad pass + fixed-order reduce) inside a PH_GRAD interval
 enum { PH_SKETCH = 0, PH_FACTOR = 1, PH_GRAD = 2, PH_SOLVE = 3, PH_SKETCH_KERNEL = 4, PH_GRAD_KERNEL = 5, PH_END = -1 };
@@ -354,11 +362,20 @@ void device_sketch(ihs_gpu_problem* P, int kind, int64_t m, uint64_t seed, doubl
             g_host_rng_ns +=
                 std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t_rng).count();
             upload_entries(P);
-            unsigned long long* ctl = srht_prepare_scratch(P, plan);
+            // columns are independent: when the phase-1 scratch of all d columns would exceed the cap,
+            // the transform runs over column batches that share one smaller scratch (and the row sample)
+            const int64_t cols_per_batch =
+                std::max<int64_t>(1, std::min<int64_t>(d, kSrhtScratchCap / (plan.n_pad * (int64_t)sizeof(double))));
+            SrhtPlan bp = plan;
+            bp.d = std::min<int64_t>(d, cols_per_batch);
+            unsigned long long* ctl = srht_prepare_scratch(P, bp);
             if (P->timer) P->timer->mark(PH_SKETCH_KERNEL);
-            srht_run_device(plan, P->A.d(), P->signbits.as<uint32_t>(), P->entries.as<int2>(), P->tiles.as<int4>(),
-                            (int)P->h_tiles.size(), P->T.d(), d_SA, st, ctl, P->num_sms,
-                            P->mask_valid ? P->srht_mask.as<uint32_t>() : nullptr);
+            for (int64_t j0 = 0; j0 < d; j0 += cols_per_batch) {
+                bp.d = std::min<int64_t>(cols_per_batch, d - j0);
+                srht_run_device(bp, P->A.d() + j0 * P->lda, P->signbits.as<uint32_t>(), P->entries.as<int2>(),
+                                P->tiles.as<int4>(), (int)P->h_tiles.size(), P->T.d(), d_SA + j0 * m, st, ctl,
+                                P->num_sms, P->mask_valid ? P->srht_mask.as<uint32_t>() : nullptr);
+            }
             if (P->timer) P->timer->mark(PH_SKETCH);
         } else {
             // shard p holds rows [p*n_loc, (p+1)*n_loc) of the padded index space
@@ -582,8 +599,12 @@ void finish_setup(ihs_gpu_problem* Q) {
         size_t free_b = 0, total_b = 0;
         CUDA_CHECK(cudaMemGetInfo(&free_b, &total_b));
         const size_t need = (size_t)Q->lda * Q->d * sizeof(double);
+        // keep room for the SRHT scratch (capped, see kSrhtScratchCap) and 8 GiB of other buffers
+        int64_t np = 1;
+        while (np < Q->n) np <<= 1;
+        const size_t srht_scratch = (size_t)std::min<int64_t>(np * Q->d * (int64_t)sizeof(double), kSrhtScratchCap);
         GradPlan rm = Q->gplan;
-        if (need * 3 < free_b && grad_plan_use_rowmajor(rm)) {
+        if (need + srht_scratch + (8ull << 30) < free_b && grad_plan_use_rowmajor(rm)) {
             Q->gplan = rm;
             Q->Arm.ensure(need);
             transpose_to_rowmajor(Q->A.d(), Q->lda, Q->lda, Q->d, Q->Arm.d(), Q->st);

@@ -355,3 +355,23 @@ def test_nccl_single_rank_communicator(gpu):
     comm = gpu.NcclComm(uid, 1, 0, 0)
     assert comm.handle
     del comm
+
+
+def test_srht_column_batches_bit_exact(gpu):
+    """Sketches whose phase-1 scratch exceeds the cap run over column batches (C4 at 2^22 rows): with a
+    1 MiB cap a 2^15-row problem runs 4 columns per batch and must stay bit-exact."""
+    import subprocess
+    import sys
+    code = ("import numpy as np\n"
+            "from paper_2006_05874_b200 import ihs\n"
+            "from oracle import oracle as O\n"
+            "rng = np.random.default_rng(7)\n"
+            "A = np.asfortranarray(rng.standard_normal(((1 << 15) - 5, 10)))\n"
+            "for m in (3, 700):\n"
+            "    assert np.array_equal(ihs.srht_sketch(A, m, 11 + m), O.srht_sketch(A, m, 11 + m)), m\n"
+            "print('ok')\n")
+    import os
+    env = dict(os.environ, IHS_SRHT_SCRATCH_CAP_MB="1")
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300, env=env,
+                       cwd=str(__import__("pathlib").Path(__file__).resolve().parents[1]))
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
