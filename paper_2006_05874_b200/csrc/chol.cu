@@ -14,6 +14,8 @@
 // substitution.
 #include "common.cuh"
 
+#include <cstdlib>
+
 #include <cooperative_groups.h>
 namespace cg = cooperative_groups;
 
@@ -320,6 +322,92 @@ __global__ void __launch_bounds__(64) tri_inv_diag_kernel(const double* __restri
     }
 }
 
+
+// Inverse of each 64x64 lower-triangular diagonal block, latency-shaped for
+// fp64 (each dependent fp64 op costs ~130 cycles on B200): eight 8x8 leaves
+// by forward substitution in parallel (lane = column, reciprocal diagonals
+// precomputed), then three 2x2 combine levels X21 = -X22 (L21 X11) as small
+// shared-memory products with four independent accumulators per output.
+// One CTA (8 warps) per block.
+constexpr int TI = 64, TIP = TI + 1;
+__device__ __forceinline__ double dot_strided4(const double* a, int as, const double* b, int bs, int q0, int q1) {
+    double c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0;
+    int q = q0;
+    for (; q + 3 < q1; q += 4) {
+        c0 = fma(a[q * as], b[q * bs], c0);
+        c1 = fma(a[(q + 1) * as], b[(q + 1) * bs], c1);
+        c2 = fma(a[(q + 2) * as], b[(q + 2) * bs], c2);
+        c3 = fma(a[(q + 3) * as], b[(q + 3) * bs], c3);
+    }
+    for (; q < q1; ++q) c0 = fma(a[q * as], b[q * bs], c0);
+    return (c0 + c1) + (c2 + c3);
+}
+
+__global__ void __launch_bounds__(256) tri_inv64_kernel(const double* __restrict__ L, int64_t n,
+                                                        double* __restrict__ W) {
+    extern __shared__ double ti_smem[];
+    double(*l)[TIP] = reinterpret_cast<double(*)[TIP]>(ti_smem);
+    double(*x)[TIP] = reinterpret_cast<double(*)[TIP]>(ti_smem + TI * TIP);
+    double(*tt)[TIP] = reinterpret_cast<double(*)[TIP]>(ti_smem + 2 * TI * TIP);
+    const int64_t k = (int64_t)blockIdx.x * TI;
+    const int nb = (int)imin64(TI, n - k);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int e = tid; e < TI * TI; e += 256) {
+        const int i = e & 63, j = e >> 6;
+        double v = 0.0;
+        if (i < nb && j < nb) v = i >= j ? L[(k + i) + (k + j) * n] : 0.0;
+        else if (i == j) v = 1.0;  // identity padding of a ragged last block
+        l[i][j] = v;
+        x[i][j] = 0.0;
+    }
+    __syncthreads();
+    // ---- leaves: warp w inverts the 8x8 block at (8w, 8w); lane c < 8 owns column c
+    {
+        const int o = 8 * warp, c = lane;
+        if (c < 8) {
+            double rd[8], xr[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) rd[i] = 1.0 / l[o + i][o + i];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                double s0 = (i == c) ? 1.0 : 0.0, s1 = 0.0;
+#pragma unroll
+                for (int q = 0; q < i; ++q) {
+                    const double t = l[o + i][o + q] * xr[q];
+                    if (q & 1) s1 -= t;
+                    else s0 -= t;
+                }
+                xr[i] = i < c ? 0.0 : (s0 + s1) * rd[i];
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i) x[o + i][o + c] = xr[i];
+        }
+    }
+    __syncthreads();
+    // ---- combine levels h = 8, 16, 32: pairs at offsets 2h*p; X21 = -X22 (L21 X11)
+    for (int h = 8; h < TI; h *= 2) {
+        const int npairs = TI / (2 * h);
+        // T = L21 X11 (X11 lower: q >= j) into tt at the X21 positions
+        for (int e = tid; e < npairs * h * h; e += 256) {
+            const int pr = e / (h * h), r = e % (h * h), i = r % h, j = r / h;
+            const int o = 2 * h * pr;
+            tt[o + h + i][o + j] = dot_strided4(&l[o + h + i][o], 1, &x[o][o + j], TIP, j, h);
+        }
+        __syncthreads();
+        // X21 = -X22 T (X22 lower: q <= i)
+        for (int e = tid; e < npairs * h * h; e += 256) {
+            const int pr = e / (h * h), r = e % (h * h), i = r % h, j = r / h;
+            const int o = 2 * h * pr;
+            x[o + h + i][o + j] = -dot_strided4(&x[o + h + i][o + h], 1, &tt[o + h][o + j], TIP, 0, i + 1);
+        }
+        __syncthreads();
+    }
+    for (int e = tid; e < nb * nb; e += 256) {
+        const int i = e % nb, j = e / nb;
+        if (i >= j) W[(k + i) + (k + j) * n] = x[i][j];
+    }
+}
+
 // y[:, q] (+)= T x[:, q] for a triangular T stored in Wf: lower (W) when
 // lower != 0, else upper (W^T mirrored into the strict upper triangle, with
 // the diagonal of W). CTA tile: 64 rows x 512 columns; partials per column
@@ -570,7 +658,21 @@ void cholesky_invert(const double* d_L, int64_t n, double* d_W, double* d_tmp, c
             CUDA_CHECK(cudaFuncSetAttribute(tri_inv_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             attr = true;
         }
-        LAUNCH(tri_inv_diag_kernel, (unsigned)ceil_div(n, NB), 64, smem, st, d_L, n, d_W);
+        static const bool old_inv = [] {
+            const char* e = std::getenv("IHS_TRI_INV_OLD");
+            return e && e[0] == '1';
+        }();
+        if (old_inv) LAUNCH(tri_inv_diag_kernel, (unsigned)ceil_div(n, NB), 64, smem, st, d_L, n, d_W);
+        else {
+            const size_t ti_smem = (size_t)3 * TI * TIP * sizeof(double);
+            static bool ti_attr = false;
+            if (!ti_attr) {
+                CUDA_CHECK(cudaFuncSetAttribute(tri_inv64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                (int)ti_smem));
+                ti_attr = true;
+            }
+            LAUNCH(tri_inv64_kernel, (unsigned)ceil_div(n, NB), 256, ti_smem, st, d_L, n, d_W);
+        }
     }
     tri_inv_rec(d_L, d_W, n, 0, n, d_tmp, st, base);
     dim3 grid((unsigned)ceil_div(n, 32), (unsigned)ceil_div(n, 32));

@@ -225,6 +225,10 @@ int main() {
         cudaFuncSetAttribute(tri_inv_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * NB * (NB + 1) * 8);
         tri_inv_diag_kernel<<<1, 64, 2 * NB * (NB + 1) * 8>>>(d, n, d + n * n);
     }, reps));
+    cudaFuncSetAttribute(tri_inv64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * TI * TIP * 8);
+    printf(", \"tri_inv64_us\": %.2f", time_it([&] {
+        tri_inv64_kernel<<<1, 256, 3 * TI * TIP * 8>>>(d, n, d + n * n);
+    }, reps));
     printf(", \"potrf_inv_diag_us\": %.2f", time_it([&] { restore(); potrf_inv_diag_kernel<<<1, 128, pi_smem>>>(d + n * n, n, 0, 64, xd, info); }, reps));
     printf(", \"only_potrf32_us\": %.2f", time_it([&] { restore(); only_potrf32<<<1, 128>>>(d + n * n, info); }, reps));
     printf(", \"only_trtri32_us\": %.2f", time_it([&] { only_trtri32<<<1, 128>>>(d); }, reps));
