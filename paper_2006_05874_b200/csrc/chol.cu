@@ -31,35 +31,52 @@ constexpr int TRSM_WARPS = 8;  // rows (warps) per CTA of the panel solves
 // rank-1 update (no integer division in the loops).
 __global__ void __launch_bounds__(256) potrf_diag_kernel(double* __restrict__ H, int64_t n, int64_t k, int nb,
                                                          int* __restrict__ info) {
+    // Right-looking elimination on the unscaled columns, a_ik -= a_ij (a_kj / a_jj), one barrier per
+    // column; the serial path per column is rcp + mul + fma and the factor l_ij = a_ij / sqrt(a_jj) is
+    // formed for all entries after the loop (the pivots a_jj are kept in piv).
     __shared__ double a[NB][NB + 1];
-    __shared__ double diag[NB];
+    __shared__ double piv[NB];
     const int i = threadIdx.x % NB, g = threadIdx.x / NB;  // row, column group (4)
     for (int jj = g; jj < nb; jj += 4) a[i][jj] = (i < nb && i >= jj) ? H[(k + i) + (k + jj) * n] : 0.0;
     __syncthreads();
     for (int j = 0; j < nb; ++j) {
-        const double s = a[j][j];
+        double s = a[j][j];
         const bool ok = (s > 0.0) && isfinite(s);
-        const double ljj = ok ? sqrt(s) : 1.0;  // a failed pivot is flagged; keep going harmlessly
+        if (!ok) s = 1.0;  // a failed pivot is flagged; keep going harmlessly
         if (threadIdx.x == 0) {
-            diag[j] = ljj;
+            piv[j] = s;
             if (!ok) atomicCAS(info, 0, (int)(k + j + 1));
         }
-        if (g == 0 && i > j && i < nb) a[i][j] = a[i][j] / ljj;
-        __syncthreads();
         if (i > j && i < nb) {
-            // independent updates of row i (columns g, g+4, ...): unrolled so the
-            // shared loads overlap instead of forming a chain
-            const double lij = a[i][j];
+            const double f = a[i][j] * __drcp_rn(s);
+            // all loads, then the independent fmas, then all stores (interleaving them would serialize
+            // on possible shared-memory aliasing)
+            double w[NB / 4], v[NB / 4];
 #pragma unroll
             for (int q = 0; q < NB / 4; ++q) {
                 const int jj = g + 4 * q;
-                if (jj > j && jj <= i) a[i][jj] -= lij * a[jj][j];
+                w[q] = a[jj][j];
+                v[q] = a[i][jj];
+            }
+#pragma unroll
+            for (int q = 0; q < NB / 4; ++q) {
+                const int jj = g + 4 * q;
+                if (jj > j && jj <= i) v[q] = fma(-f, w[q], v[q]);
+            }
+#pragma unroll
+            for (int q = 0; q < NB / 4; ++q) {
+                const int jj = g + 4 * q;
+                if (jj > j && jj <= i) a[i][jj] = v[q];
             }
         }
         __syncthreads();
     }
-    for (int jj = g; jj < nb; jj += 4)
-        if (i < nb && i >= jj) H[(k + i) + (k + jj) * n] = (i == jj) ? diag[i] : a[i][jj];
+    for (int jj = g; jj < nb; jj += 4) {
+        if (i < nb && i >= jj) {
+            const double pj = piv[jj];
+            H[(k + i) + (k + jj) * n] = (i == jj) ? sqrt(pj) : a[i][jj] * rsqrt(pj);
+        }
+    }
 }
 
 // ---- diagonal block: LLT and its inverse in one CTA (4 warps)
@@ -324,7 +341,7 @@ __global__ void __launch_bounds__(64) tri_inv_diag_kernel(const double* __restri
 
 
 // Inverse of each 64x64 lower-triangular diagonal block, latency-shaped for
-// fp64 (each dependent fp64 op costs ~130 cycles on B200): eight 8x8 leaves
+// parallelism: eight 8x8 leaves
 // by forward substitution in parallel (lane = column, reciprocal diagonals
 // precomputed), then three 2x2 combine levels X21 = -X22 (L21 X11) as small
 // shared-memory products with four independent accumulators per output.

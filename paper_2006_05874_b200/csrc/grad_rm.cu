@@ -286,8 +286,8 @@ grad_rr_kernel(const double* __restrict__ Arm, int64_t d, int64_t npanels, const
                     const int64_t j = 2 * lane + 64 * k;
                     a[k] = j < d ? *reinterpret_cast<const double2*>(P + row * d + j) : make_double2(0.0, 0.0);
                 }
-                // fp64 ops have ~130-cycle latency on B200 (tools/lat_micro.cu): the row dot product
-                // runs as four independent chains per right-hand side, summed in a fixed tree
+                // the row dot product runs as four independent chains per right-hand side, summed in a
+                // fixed tree
                 double r[NRHS];
 #pragma unroll
                 for (int q = 0; q < NRHS; ++q) {
