@@ -49,25 +49,16 @@ __global__ void __launch_bounds__(256) potrf_diag_kernel(double* __restrict__ H,
         }
         if (i > j && i < nb) {
             const double f = a[i][j] * __drcp_rn(s);
-            // all loads, then the independent fmas, then all stores (interleaving them would serialize
-            // on possible shared-memory aliasing)
-            double w[NB / 4], v[NB / 4];
-#pragma unroll
-            for (int q = 0; q < NB / 4; ++q) {
-                const int jj = g + 4 * q;
-                w[q] = a[jj][j];
-                v[q] = a[i][jj];
+            // only the active columns jj in (j, i] of this thread's interleave (jj = g mod 4): the
+            // work shrinks with j instead of sweeping all 16 slots every column
+            int jj = g + 4 * ((j + 4 - g) / 4);  // first jj = g (mod 4) with jj > j
+            for (; jj + 4 <= i; jj += 8) {
+                const double w0 = a[jj][j], w1 = a[jj + 4][j];
+                const double v0 = a[i][jj], v1 = a[i][jj + 4];
+                a[i][jj] = fma(-f, w0, v0);
+                a[i][jj + 4] = fma(-f, w1, v1);
             }
-#pragma unroll
-            for (int q = 0; q < NB / 4; ++q) {
-                const int jj = g + 4 * q;
-                if (jj > j && jj <= i) v[q] = fma(-f, w[q], v[q]);
-            }
-#pragma unroll
-            for (int q = 0; q < NB / 4; ++q) {
-                const int jj = g + 4 * q;
-                if (jj > j && jj <= i) a[i][jj] = v[q];
-            }
+            if (jj <= i) a[i][jj] = fma(-f, a[jj][j], a[i][jj]);
         }
         __syncthreads();
     }
