@@ -70,15 +70,26 @@ __global__ void __launch_bounds__(mt::THREADS) mt_substream_kernel(const uint64_
 }
 
 // Sign bits of draws [beg, end) into a shared bit buffer (bit g - beg).
+__device__ __forceinline__ void or_bits32(uint32_t* accw, int64_t o, uint32_t v) {
+    // bits [o, o + 32) |= v (o need not be word aligned)
+    if (!v) return;
+    const int sh = (int)(o & 31);
+    atomicOr(&accw[o >> 5], v << sh);
+    if (sh && (v >> (32 - sh))) atomicOr(&accw[(o >> 5) + 1], v >> (32 - sh));  // only bits inside the range
+}
+// one warp ballot per 32 draws instead of one atomic per set bit
 __device__ __forceinline__ void sign_bits_range(mt::Twister& tw, int64_t beg, int64_t end, uint32_t* accw) {
-    const int k = threadIdx.x;
+    const int k = threadIdx.x, lane = k & 31;
     for (int64_t base = beg; base < end; base += NN) {
-        uint64_t lo, hi;
+        uint64_t lo = 0, hi = 0;
         tw.next(lo, hi);
-        if (tw.worker()) {
-            const int64_t g0 = base + k, g1 = base + mt::MM + k;
-            if (g0 < end && (temper(lo) & 1ULL)) atomicOr(&accw[(g0 - beg) >> 5], 1u << ((g0 - beg) & 31));
-            if (g1 < end && (temper(hi) & 1ULL)) atomicOr(&accw[(g1 - beg) >> 5], 1u << ((g1 - beg) & 31));
+        const bool w = tw.worker();
+        const int64_t g0 = base + k, g1 = base + mt::MM + k;
+        const uint32_t b0 = __ballot_sync(0xffffffffu, w && g0 < end && (temper(lo) & 1ULL));
+        const uint32_t b1 = __ballot_sync(0xffffffffu, w && g1 < end && (temper(hi) & 1ULL));
+        if (lane == 0) {
+            or_bits32(accw, g0 - beg, b0);  // lane 0's draw is bit 0 of the ballot
+            or_bits32(accw, g1 - beg, b1);
         }
     }
 }
