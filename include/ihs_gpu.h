@@ -153,6 +153,25 @@ typedef struct ihs_solve_report {
                                        solve_underdetermined (solver.hpp:82); iterates then hold the dual trace */
 } ihs_solve_report;
 
+/* CgResult / PcgResult (baselines.hpp:16-36). residuals is caller-allocated
+ * (residuals_capacity entries, may be NULL); residuals_size = iterations + 1
+ * values were produced (only the first residuals_capacity written). */
+typedef struct ihs_cg_report {
+    double* x;                      /* d doubles, caller-allocated (required) */
+    double* residuals;              /* ||H x_k - A^T b||, k = 0..iterations */
+    int64_t residuals_capacity;
+    int64_t residuals_size;
+    int64_t iterations;
+    int32_t converged;
+    int32_t m_capped;               /* PCG: prescription exceeded n_pad and was capped */
+    int64_t m;                      /* PCG: sketch rows used (0 for CG) */
+    uint64_t setup_flops;           /* PCG: sketch + gram + Cholesky counter */
+    ihs_counters counters;
+    double wall_seconds;
+    double device_ms;               /* GPU: CUDA-event time of the solve on the device timeline */
+    int64_t kernel_launches;        /* GPU: kernels this library launched during the solve */
+} ihs_cg_report;
+
 /* Device / sharding options of a problem handle. */
 typedef struct ihs_gpu_options {
     int32_t device;                 /* CUDA device ordinal */
@@ -274,6 +293,20 @@ ihs_status ihs_gpu_adaptive_solve(ihs_gpu_problem* p, const ihs_solver_config* c
  * (T+1) iterates, x_start first, to iterates_out (d*(T+1) doubles). */
 ihs_status ihs_gpu_fixed_sketch_ihs(ihs_gpu_problem* p, const ihs_gpu_system* s, const ihs_tuning* tp,
                                     int64_t T, int32_t mode, const double* x_start, double* iterates_out);
+
+/* ------------------------------------------------ CG / PCG baselines */
+/* pcg_sketch_size (baselines.hpp:170-187): m = d/rho (Gaussian) or d ln(d)/rho (SRHT, capped at n_pad). */
+ihs_status ihs_pcg_sketch_size(int64_t n, int64_t d, int32_t kind, double rho, int64_t* m, int32_t* capped);
+/* cg_solve (baselines.hpp:40-92): CG on (A^T A + nu^2 I) x = A^T b, stops when
+ * ||H x - A^T b|| <= tol ||A^T b||; x0 (d doubles) may be NULL (zero start). */
+ihs_status ihs_gpu_cg_solve(ihs_gpu_problem* p, double tol, int64_t max_iters, const double* x0, ihs_cg_report* rep);
+/* pcg_solve_with (baselines.hpp:98-165): CG preconditioned by the Cholesky factor of
+ * SA^T SA + nu^2 I_d, SA a host m x d column-major sketch (leading dimension lds). */
+ihs_status ihs_gpu_pcg_solve_with(ihs_gpu_problem* p, const double* SA, int64_t m, int64_t lds, double tol,
+                                  int64_t max_iters, const double* x0, ihs_cg_report* rep);
+/* pcg_solve (baselines.hpp:190-200): sketch of the prescribed size on the device, then pcg_solve_with. */
+ihs_status ihs_gpu_pcg_solve(ihs_gpu_problem* p, int32_t kind, uint64_t seed, double rho, double tol,
+                             int64_t max_iters, const double* x0, ihs_cg_report* rep);
 
 /* ---------------------------------------------------- synthetic data
  * SURVEY.md §8(d) generator shared by bench and tests: A = G diag(sigma),

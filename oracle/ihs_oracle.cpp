@@ -165,7 +165,7 @@ Mat apply_sketch(const Mat& A, SketchKind kind, Index m, std::uint64_t seed, Cos
 
 // =============================================================== problem.hpp
 Problem::Problem(Mat A_, Vec b_, double nu_, bool underdetermined)
-    : A(std::move(A_)), b(std::move(b_)), nu(nu_) {  // :22-33
+    : A(std::move(A_)), b(std::move(b_)), nu(nu_), underdetermined(underdetermined) {  // :22-33
     if (!(nu > 0.0)) throw InvalidInput("ProblemInstance: nu must be strictly positive");
     if (A.rows < 1 || A.cols < 1) throw InvalidInput("ProblemInstance: empty matrix");
     if (static_cast<Index>(b.size()) != A.rows) throw InvalidInput("ProblemInstance: size of b must match rows of A");
@@ -558,6 +558,162 @@ std::vector<Vec> fixed_sketch_ihs(const Problem& p, const SketchedSystem& sys, c
         its.push_back(x);
     }
     return its;
+}
+
+// =============================================================== baselines.hpp
+namespace {
+double sq_norm(const Vec& v) {
+    double s = 0;
+    for (double x : v) s += x * x;
+    return s;
+}
+double dotv(const Vec& a, const Vec& b) {
+    double s = 0;
+    for (size_t i = 0; i < a.size(); ++i) s += a[i] * b[i];
+    return s;
+}
+// H v = A^T (A v) + nu^2 v (baselines.hpp:50-53, :115-118), counted as 2nd + 2d
+Vec apply_h(const Problem& p, const Vec& v, CostCounters& c) {
+    const Index n = p.A.rows, d = p.A.cols;
+    Vec r(static_cast<size_t>(n), 0.0);
+    for (Index j = 0; j < d; ++j) {
+        const double vj = v[static_cast<size_t>(j)];
+        const double* a = p.A.col(j);
+        for (Index i = 0; i < n; ++i) r[static_cast<size_t>(i)] += a[i] * vj;
+    }
+    const double nu2 = p.nu * p.nu;
+    Vec h(static_cast<size_t>(d));
+    for (Index j = 0; j < d; ++j) h[static_cast<size_t>(j)] = dot4(p.A.col(j), r.data(), n) + nu2 * v[static_cast<size_t>(j)];
+    c.matvec += 2 * static_cast<std::uint64_t>(n) * static_cast<std::uint64_t>(d) + 2 * static_cast<std::uint64_t>(d);
+    return h;
+}
+Vec atb_of(const Problem& p) {
+    Vec z(static_cast<size_t>(p.A.cols));
+    for (Index j = 0; j < p.A.cols; ++j) z[static_cast<size_t>(j)] = dot4(p.A.col(j), p.b.data(), p.A.rows);
+    return z;
+}
+// r = A^T b - H x; x = x0 or 0 (baselines.hpp:55-58, :126-129)
+Vec cg_start(const Problem& p, CgResult& res, const Vec* x0, const Vec& atb) {
+    const size_t d = static_cast<size_t>(p.A.cols);
+    if (x0 && x0->size() != d) throw InvalidInput("cg_solve: dimension mismatch");
+    res.x = x0 ? *x0 : Vec(d, 0.0);
+    Vec hx = apply_h(p, res.x, res.counters);
+    Vec r(d);
+    for (size_t i = 0; i < d; ++i) r[i] = atb[i] - hx[i];
+    res.residuals.push_back(std::sqrt(sq_norm(r)));
+    return r;
+}
+}  // namespace
+
+CgResult cg_solve(const Problem& p, double tol, Index max_iters, const Vec* x0) {  // baselines.hpp:40-92
+    if (p.underdetermined) throw InvalidInput("cg_solve: expects an overdetermined instance");
+    const size_t d = static_cast<size_t>(p.A.cols);
+    CgResult res;
+    const Vec atb = atb_of(p);
+    const double target = tol * std::sqrt(sq_norm(atb));
+    Vec r = cg_start(p, res, x0, atb);
+    if (res.residuals.back() <= target) {
+        res.converged = true;
+        return res;
+    }
+    Vec pdir = r;
+    double rr = sq_norm(r);
+    for (Index k = 0; k < max_iters; ++k) {
+        Vec hp = apply_h(p, pdir, res.counters);
+        const double alpha = rr / dotv(pdir, hp);
+        for (size_t i = 0; i < d; ++i) res.x[i] += alpha * pdir[i];
+        for (size_t i = 0; i < d; ++i) r[i] -= alpha * hp[i];
+        ++res.iterations;
+        const double rr_new = sq_norm(r);
+        res.residuals.push_back(std::sqrt(rr_new));
+        if (res.residuals.back() <= target) {
+            res.converged = true;
+            break;
+        }
+        const double beta = rr_new / rr;
+        for (size_t i = 0; i < d; ++i) pdir[i] = r[i] + beta * pdir[i];
+        rr = rr_new;
+    }
+    return res;
+}
+
+CgResult pcg_solve_with(const Problem& p, const Mat& SA, double tol, Index max_iters, CgResult res,
+                        const Vec* x0) {  // baselines.hpp:98-165
+    if (p.underdetermined) throw InvalidInput("pcg_solve: expects an overdetermined instance");
+    const Index d = p.A.cols, m = SA.rows;
+    if (SA.cols != d) throw InvalidInput("pcg_solve: dimension mismatch");
+    const auto dd = static_cast<std::uint64_t>(d), mm = static_cast<std::uint64_t>(m);
+    res.m = m;
+    // gram = SA^T SA + nu^2 I_d, lower Cholesky; applied by two triangular substitutions
+    Mat L(d, d);
+    for (Index j = 0; j < d; ++j)
+        for (Index i = j; i < d; ++i) L(i, j) = L(j, i) = dot4(SA.col(i), SA.col(j), m);
+    for (Index j = 0; j < d; ++j) L(j, j) += p.nu * p.nu;
+    if (!cholesky_lower(L)) throw NumericalBreakdown("pcg_solve: preconditioner factorization failed");
+    res.setup_flops += dd * dd * mm + dd * dd * dd / 3;
+    res.counters.factor += dd * dd * mm + dd * dd * dd / 3;
+    auto apply_minv = [&](const Vec& v) {
+        res.counters.solve += 2 * dd * dd;
+        Vec z = v;
+        chol_solve(L, z.data());
+        return z;
+    };
+    const size_t du = static_cast<size_t>(d);
+    const Vec atb = atb_of(p);
+    const double target = tol * std::sqrt(sq_norm(atb));
+    Vec r = cg_start(p, res, x0, atb);
+    if (res.residuals.back() <= target) {
+        res.converged = true;
+        return res;
+    }
+    Vec z = apply_minv(r);
+    Vec pdir = z;
+    double rz = dotv(r, z);
+    for (Index k = 0; k < max_iters; ++k) {
+        Vec hp = apply_h(p, pdir, res.counters);
+        const double alpha = rz / dotv(pdir, hp);
+        for (size_t i = 0; i < du; ++i) res.x[i] += alpha * pdir[i];
+        for (size_t i = 0; i < du; ++i) r[i] -= alpha * hp[i];
+        ++res.iterations;
+        res.residuals.push_back(std::sqrt(sq_norm(r)));
+        if (res.residuals.back() <= target) {
+            res.converged = true;
+            break;
+        }
+        z = apply_minv(r);
+        const double rz_new = dotv(r, z);
+        const double beta = rz_new / rz;
+        for (size_t i = 0; i < du; ++i) pdir[i] = z[i] + beta * pdir[i];
+        rz = rz_new;
+    }
+    return res;
+}
+
+std::pair<Index, bool> pcg_sketch_size(Index n, Index d, SketchKind kind, double rho) {  // baselines.hpp:170-187
+    if (!(rho > 0.0 && rho < 1.0)) throw InvalidInput("pcg_sketch_size: rho must be in (0,1)");
+    const double m_raw = kind == SketchKind::Gaussian
+                             ? static_cast<double>(d) / rho
+                             : static_cast<double>(d) * std::log(static_cast<double>(d)) / rho;
+    Index m = std::max<Index>(static_cast<Index>(std::ceil(m_raw)), 1);
+    bool capped = false;
+    if (kind == SketchKind::SRHT) {
+        const Index n_pad = next_pow2(n);
+        if (m > n_pad) {
+            m = n_pad;
+            capped = true;
+        }
+    }
+    return {m, capped};
+}
+
+CgResult pcg_solve(const Problem& p, SketchKind kind, std::uint64_t seed, double rho, double tol, Index max_iters,
+                   const Vec* x0) {  // baselines.hpp:190-200
+    auto [m, capped] = pcg_sketch_size(p.A.rows, p.A.cols, kind, rho);
+    CgResult res;
+    res.m_capped = capped;
+    Mat SA = apply_sketch(p.A, kind, m, seed, &res.counters);
+    res.setup_flops += res.counters.sketch;
+    return pcg_solve_with(p, SA, tol, max_iters, std::move(res), x0);
 }
 
 // =============================================================== synthetic data

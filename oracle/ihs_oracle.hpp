@@ -74,6 +74,7 @@ struct Problem {                                                         // prob
     Mat A;
     Vec b;
     double nu = 1.0;
+    bool underdetermined = false;  // Orientation (problem.hpp:14)
     Problem(Mat A_, Vec b_, double nu_, bool underdetermined = false);
 };
 Vec gradient(const Problem& p, const Vec& x, CostCounters* c = nullptr); // problem.hpp:59-69
@@ -148,6 +149,24 @@ SolveReport solve_underdetermined(const Problem& p, const SolverConfig& cfg);  /
 enum class FixedMode { Gradient = 0, Polyak = 1 };
 std::vector<Vec> fixed_sketch_ihs(const Problem& p, const SketchedSystem& sys, const TuningParams& tp,
                                   Index T, FixedMode mode, const Vec* x_start = nullptr);  // :258-276
+
+// ---------------------------------------------------------------- baselines.hpp
+struct CgResult {  // CgResult / PcgResult (baselines.hpp:16-36); the PCG fields stay 0 for plain CG
+    Vec x;
+    Index iterations = 0;
+    std::vector<double> residuals;  // ||H x_k - A^T b|| per iteration, incl. the start
+    bool converged = false;
+    Index m = 0;
+    bool m_capped = false;
+    std::uint64_t setup_flops = 0;
+    CostCounters counters;
+};
+CgResult cg_solve(const Problem& p, double tol, Index max_iters, const Vec* x0 = nullptr);  // :40-92
+CgResult pcg_solve_with(const Problem& p, const Mat& SA, double tol, Index max_iters, CgResult res = {},
+                        const Vec* x0 = nullptr);                                          // :98-165
+std::pair<Index, bool> pcg_sketch_size(Index n, Index d, SketchKind kind, double rho);     // :170-187
+CgResult pcg_solve(const Problem& p, SketchKind kind, std::uint64_t seed, double rho, double tol, Index max_iters,
+                   const Vec* x0 = nullptr);                                               // :190-200
 
 // ---------------------------------------------------------------- synthetic data
 struct SynthSpec {

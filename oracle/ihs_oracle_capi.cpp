@@ -258,4 +258,40 @@ int ihs_oracle_synth(const ihs_synth_spec* s, double* A, double* b, double* x_tr
     });
 }
 
+// baselines.hpp: method 0 = cg_solve, 1 = pcg_solve_with(SA), 2 = pcg_solve(kind, seed, rho)
+int ihs_oracle_cg(const double* A, int64_t n, int64_t d, int64_t lda, const double* b, double nu, int32_t method,
+                  const double* SA, int64_t m, int64_t lds, int32_t kind, uint64_t seed, double rho, double tol,
+                  int64_t max_iters, const double* x0, ihs_cg_report* rep) {
+    return guarded([&] {
+        Problem p(to_mat(A, n, d, lda), Vec(b, b + n), nu);
+        Vec xs;
+        if (x0) xs.assign(x0, x0 + d);
+        const Vec* xp = x0 ? &xs : nullptr;
+        const SketchKind k = kind == IHS_SKETCH_SRHT ? SketchKind::SRHT : SketchKind::Gaussian;
+        CgResult r = method == 0   ? cg_solve(p, tol, max_iters, xp)
+                     : method == 1 ? pcg_solve_with(p, to_mat(SA, m, d, lds), tol, max_iters, CgResult{}, xp)
+                                   : pcg_solve(p, k, seed, rho, tol, max_iters, xp);
+        std::memcpy(rep->x, r.x.data(), sizeof(double) * static_cast<size_t>(d));
+        rep->residuals_size = static_cast<int64_t>(r.residuals.size());
+        if (rep->residuals)
+            for (int64_t i = 0; i < rep->residuals_size && i < rep->residuals_capacity; ++i)
+                rep->residuals[i] = r.residuals[static_cast<size_t>(i)];
+        rep->iterations = r.iterations;
+        rep->converged = r.converged;
+        rep->m = r.m;
+        rep->m_capped = r.m_capped;
+        rep->setup_flops = r.setup_flops;
+        rep->counters = ihs_counters{};
+        add_counters(&rep->counters, r.counters);
+    });
+}
+
+int ihs_oracle_pcg_sketch_size(int64_t n, int64_t d, int32_t kind, double rho, int64_t* m, int32_t* capped) {
+    return guarded([&] {
+        auto [mm, c] = pcg_sketch_size(n, d, kind == IHS_SKETCH_SRHT ? SketchKind::SRHT : SketchKind::Gaussian, rho);
+        *m = mm;
+        *capped = c;
+    });
+}
+
 }  // extern "C"

@@ -72,6 +72,11 @@ def lib():
         L.ihs_oracle_direct_solve.argtypes = [d, C.c_int64, C.c_int64, C.c_int64, d, C.c_double, d]
         L.ihs_oracle_prediction_error.argtypes = [d, C.c_int64, C.c_int64, C.c_int64, d, C.c_double, d, d, d]
         L.ihs_oracle_synth.argtypes = [P(abi.SynthSpec), d, d, d]
+        L.ihs_oracle_cg.argtypes = [d, C.c_int64, C.c_int64, C.c_int64, d, C.c_double, C.c_int32, d, C.c_int64,
+                                    C.c_int64, C.c_int32, C.c_uint64, C.c_double, C.c_double, C.c_int64, d,
+                                    P(abi.CgReportC)]
+        L.ihs_oracle_pcg_sketch_size.argtypes = [C.c_int64, C.c_int64, C.c_int32, C.c_double, P(C.c_int64),
+                                                 P(C.c_int32)]
         _lib = L
     return _lib
 
@@ -320,3 +325,44 @@ def default_config(**kw) -> abi.SolverConfigC:
     for k, v in kw.items():
         setattr(c, k, v)
     return c
+
+
+def _cg(method, A, b, nu, tol, max_iters, x0=None, SA=None, kind=0, seed=0, rho=0.5):
+    A = _fortran(A)
+    n, d = A.shape
+    b = _f64(b)
+    x = np.empty(d)
+    cap = max_iters + 1
+    res = np.empty(cap)
+    rep = abi.CgReportC()
+    rep.x = _dp(x)
+    rep.residuals = _dp(res)
+    rep.residuals_capacity = cap
+    SAf = _fortran(SA) if SA is not None else None
+    x0 = _f64(x0) if x0 is not None else None
+    _check(lib().ihs_oracle_cg(_dp(A), n, d, n, _dp(b), nu, method, _dp(SAf) if SAf is not None else None,
+                               SAf.shape[0] if SAf is not None else 0, SAf.shape[0] if SAf is not None else 0,
+                               kind, seed, rho, tol, max_iters, _dp(x0) if x0 is not None else None, C.byref(rep)))
+    return x, res[: min(rep.residuals_size, cap)].copy(), rep
+
+
+def cg_solve(A, b, nu, tol, max_iters, x0=None):
+    """baselines.hpp:40-92. Returns (x, residuals, report-struct)."""
+    return _cg(0, A, b, nu, tol, max_iters, x0)
+
+
+def pcg_solve_with(A, b, nu, SA, tol, max_iters, x0=None):
+    """baselines.hpp:98-165."""
+    return _cg(1, A, b, nu, tol, max_iters, x0, SA=SA)
+
+
+def pcg_solve(A, b, nu, kind, seed, rho, tol, max_iters, x0=None):
+    """baselines.hpp:190-200."""
+    return _cg(2, A, b, nu, tol, max_iters, x0, kind=kind, seed=seed, rho=rho)
+
+
+def pcg_sketch_size(n, d, kind, rho):
+    """baselines.hpp:170-187 -> (m, capped)."""
+    m, c = C.c_int64(), C.c_int32()
+    _check(lib().ihs_oracle_pcg_sketch_size(n, d, kind, rho, C.byref(m), C.byref(c)))
+    return m.value, bool(c.value)

@@ -113,6 +113,25 @@ class SolveReportC(C.Structure):
     ]
 
 
+class CgReportC(C.Structure):
+    """ihs_cg_report: CgResult / PcgResult (baselines.hpp:16-36)."""
+    _fields_ = [
+        ("x", C.POINTER(C.c_double)),
+        ("residuals", C.POINTER(C.c_double)),
+        ("residuals_capacity", C.c_int64),
+        ("residuals_size", C.c_int64),
+        ("iterations", C.c_int64),
+        ("converged", C.c_int32),
+        ("m_capped", C.c_int32),
+        ("m", C.c_int64),
+        ("setup_flops", C.c_uint64),
+        ("counters", Counters),
+        ("wall_seconds", C.c_double),
+        ("device_ms", C.c_double),
+        ("kernel_launches", C.c_int64),
+    ]
+
+
 class GpuOptions(C.Structure):
     _fields_ = [("device", C.c_int32), ("world_size", C.c_int32), ("rank", C.c_int32), ("_pad", C.c_int32),
                 ("nccl_comm", C.c_void_p), ("n_global", C.c_int64), ("row_offset", C.c_int64)]

@@ -186,6 +186,16 @@ void fixed_step(const double* x, const double* xprev, const double* step, double
                 double* xn, cudaStream_t st);
 // deterministic dots: out[2*k] = g_k . gt_k, out[2*k+1] = g_k . g_k
 void decrement_dots(const double* g, const double* gt, int64_t d, int nrhs, double* out, cudaStream_t st);
+
+// cg.cu: CG / PCG recurrences (baselines.hpp:40-200) with a device-resident state
+size_t cg_state_bytes();
+int64_t cg_state_iter(const void* h_state);
+bool cg_state_done(const void* h_state);
+void cg_begin(const double* g0, const double* hx, double* r, double* p, double tol, int64_t d, void* state,
+              double* resid, bool pcg, cudaStream_t st);
+void cg_step(void* state, double* p, const double* hp, double* x, double* r, double* resid, int64_t base, int64_t d,
+             bool pcg, cudaStream_t st);
+void cg_dir(void* state, const double* z, const double* dots, double* p, int64_t d, bool first, cudaStream_t st);
 // Woodbury pieces: u = SA g (m), z = (g - SA^T w) / nu2
 void gemv_n(const double* A, int64_t M, int64_t N, int64_t lda, const double* x, int nrhs, int64_t ldx, double* y,
             int64_t ldy, cudaStream_t st);

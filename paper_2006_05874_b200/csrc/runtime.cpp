@@ -228,6 +228,7 @@ struct ihs_gpu_system {
     int64_t m = 0, d = 0;
     double nu = 0.0;
     int kind = IHS_FACTOR_DIRECT_GRAM;
+    bool force_gram = false;  // PCG preconditioner: the d x d Gram form whatever m (baselines.hpp:111-114)
     cudaStream_t st = nullptr;
     int num_sms = 148;
     DevBuf SA;    // m x d
@@ -287,6 +288,11 @@ struct ihs_gpu_problem {
     // problem itself the observation vector subtracted from every gradient (non-owning, n doubles)
     std::unique_ptr<ihs_gpu_problem> dual;
     const double* gsub = nullptr;
+    // CG / PCG baselines: zero observation vector (H v = gradient pass with b = 0), the recurrence
+    // vectors + device state, and its pinned read-back
+    DevBuf zb, cgv;
+    PinnedBuf h_cg;
+    bool zb_ready = false;
     ~ihs_gpu_problem() {
         for (auto e : set_ev)
             if (e) cudaEventDestroy(e);
@@ -456,7 +462,7 @@ void system_factorize(ihs_gpu_system* S, ihs_counters* c) {
     int* d_flag = S->info.as<int>() + 1;
     CUDA_CHECK(cudaMemsetAsync(d_flag, 0, sizeof(int), st));
     if (m * d > 0) check_finite(S->SA.d(), m * d, d_flag, st);
-    S->kind = m < d ? IHS_FACTOR_WOODBURY_INNER : IHS_FACTOR_DIRECT_GRAM;
+    S->kind = m < d && !S->force_gram ? IHS_FACTOR_WOODBURY_INNER : IHS_FACTOR_DIRECT_GRAM;
     const int64_t k = S->k();
     S->L.ensure((size_t)k * k * sizeof(double));
     const double nu2 = S->nu * S->nu;
@@ -567,23 +573,128 @@ void alloc_and_upload(ihs_gpu_problem* P, const double* A, int64_t lda_host, con
 // g = A^T(Ax - b) + nu^2 x; on a row-sharded problem the A_p^T(A_p x - b_p)
 // partials are summed over NCCL (identical bytes on every rank) before the
 // nu^2 x term is added once.
-void problem_grad(ihs_gpu_problem* P, const double* X, int nrhs, double* G, const CandSpec* cs = nullptr) {
+void problem_grad(ihs_gpu_problem* P, const double* X, int nrhs, double* G, const CandSpec* cs = nullptr,
+                  const double* bvec = nullptr) {
     const double nu2 = P->nu * P->nu;
+    const double* b = bvec ? bvec : P->b.d();
     if (cs) X = cs->out;
     // inside a solve: the gradient kernels' own interval (bench roofline), then back to PH_GRAD
     if (P->timer) P->timer->mark(PH_GRAD_KERNEL);
     if (P->opts.world_size > 1) {
-        grad_run(P->gplan, P->A.d(), P->b.d(), 0.0, X, nrhs, G, P->grad_work.d(), P->st, P->Arm.d(), cs);
+        grad_run(P->gplan, P->A.d(), b, 0.0, X, nrhs, G, P->grad_work.d(), P->st, P->Arm.d(), cs);
         if (P->timer) P->timer->mark(PH_GRAD);
         nccl_allreduce_sum(G, (size_t)nrhs * P->d, P->opts.nccl_comm, P->st);
         add_scaled(G, X, nu2, (int64_t)nrhs * P->d, P->st);
     } else {
-        grad_run(P->gplan, P->A.d(), P->b.d(), nu2, X, nrhs, G, P->grad_work.d(), P->st, P->Arm.d(), cs);
+        grad_run(P->gplan, P->A.d(), b, nu2, X, nrhs, G, P->grad_work.d(), P->st, P->Arm.d(), cs);
         if (P->timer) P->timer->mark(PH_GRAD);
     }
     // dual problem (dual.hpp:20-22): g = M^T(M z) + nu^2 z - b
     if (P->gsub)
         for (int q = 0; q < nrhs; ++q) add_scaled(G + (int64_t)q * P->d, P->gsub, -1.0, P->d, P->st);
+}
+
+// CG / sketch-preconditioned CG (baselines.hpp:40-92, 98-165) on the device-resident problem.
+// S: the preconditioner (direct-Gram system with explicit H_S^{-1}: M^{-1} r is one mat-vec whose
+// last CTA also forms r.z) or nullptr for plain CG. Iterations are enqueued in batches of B between
+// read-backs of the device state (B ~ 256 MB of A traffic per batch, 1..16); a batch that passes the
+// stopping point only runs no-op recurrence kernels after it (their H p passes are wasted work, not
+// a change of result). Counters follow the reference's analytic formulas (baselines.hpp:51,117,120).
+void cg_run(ihs_gpu_problem* P, const ihs_gpu_system* S, double tol, int64_t max_iters, const double* x0,
+            ihs_cg_report* rep, ihs_counters& C) {
+    const int64_t d = P->d, n = P->n;
+    cudaStream_t st = P->st;
+    const bool pcg = S != nullptr;
+    const uint64_t nn = (uint64_t)(P->opts.world_size > 1 ? P->opts.n_global : n), dd = (uint64_t)d;
+    const uint64_t hv_count = 2 * nn * dd + 2 * dd, minv_count = 2 * dd * dd;
+    const double pass_bytes = 8.0 * (double)n * (double)d;
+    const int64_t B = std::max<int64_t>(1, std::min<int64_t>(16, (int64_t)(256e6 / std::max(pass_bytes, 1.0))));
+    if (!P->zb_ready) {
+        P->zb.ensure((size_t)P->lda * sizeof(double));
+        CUDA_CHECK(cudaMemsetAsync(P->zb.p, 0, (size_t)P->lda * sizeof(double), st));
+        P->zb_ready = true;
+    }
+    const size_t nvec = (size_t)7 * d + 8 + (size_t)(B + 1) + 8;
+    P->cgv.ensure(nvec * sizeof(double) + cg_state_bytes());
+    double* x = P->cgv.d();
+    double *r = x + d, *p = r + d, *hp = p + d, *z = hp + d, *g0 = z + d, *hx = g0 + d, *dots = hx + d;
+    double* resid = dots + 8;
+    void* state = resid + B + 1 + 8;
+    const size_t sb = cg_state_bytes();
+    P->h_cg.ensure(sb + (size_t)(B + 1) * sizeof(double));
+    void* h_state = P->h_cg.p;
+    double* h_resid = reinterpret_cast<double*>(static_cast<char*>(P->h_cg.p) + sb);
+    auto read_back = [&](int64_t from, int64_t count) {
+        CUDA_CHECK(cudaMemcpyAsync(h_state, state, sb, cudaMemcpyDeviceToHost, st));
+        if (count > 0)
+            CUDA_CHECK(cudaMemcpyAsync(h_resid + from, resid + from, (size_t)count * sizeof(double),
+                                       cudaMemcpyDeviceToHost, st));
+        CUDA_CHECK(cudaStreamSynchronize(st));
+    };
+    // atb = -(A^T(A 0 - b) + nu^2 0); not counted (baselines.hpp:55 is outside apply_h)
+    CUDA_CHECK(cudaMemsetAsync(z, 0, (size_t)d * sizeof(double), st));
+    problem_grad(P, z, 1, g0);
+    if (x0) {
+        CUDA_CHECK(cudaMemcpyAsync(x, x0, (size_t)d * sizeof(double), cudaMemcpyHostToDevice, st));
+        problem_grad(P, x, 1, hx, nullptr, P->zb.d());  // H x0
+    } else {
+        CUDA_CHECK(cudaMemsetAsync(x, 0, (size_t)d * sizeof(double), st));
+    }
+    C.matvec += hv_count;  // the starting residual's H x (baselines.hpp:57 / :128)
+    cg_begin(g0, x0 ? hx : nullptr, r, p, tol, d, state, resid, pcg, st);
+    if (pcg) {
+        gemv_tiled(S->Hinv.d(), d, d, d, r, 1, d, z, d, S->gv.d(), st, dots);
+        cg_dir(state, z, dots, p, d, true, st);
+    }
+    read_back(0, 1);
+    std::vector<double> residuals{h_resid[0]};
+    bool done = cg_state_done(h_state);
+    if (!done && pcg) C.solve += minv_count;
+    int64_t launched = 0;
+    while (!done && launched < max_iters) {
+        const int64_t nb = std::min(B, max_iters - launched);
+        for (int64_t k = 0; k < nb; ++k) {
+            problem_grad(P, p, 1, hp, nullptr, P->zb.d());  // hp = A^T(A p) + nu^2 p
+            cg_step(state, p, hp, x, r, resid, launched, d, pcg, st);
+            if (pcg) {
+                gemv_tiled(S->Hinv.d(), d, d, d, r, 1, d, z, d, S->gv.d(), st, dots);
+                cg_dir(state, z, dots, p, d, false, st);
+            }
+        }
+        read_back(1, nb);
+        const int64_t it = cg_state_iter(h_state);
+        for (int64_t j = 1; j <= it - launched; ++j) residuals.push_back(h_resid[j]);
+        done = cg_state_done(h_state);
+        launched += nb;
+    }
+    const int64_t iters = (int64_t)residuals.size() - 1;
+    C.matvec += (uint64_t)iters * hv_count;
+    if (pcg && iters > 0) C.solve += (uint64_t)(done ? iters - 1 : iters) * minv_count;
+    CUDA_CHECK(cudaMemcpyAsync(rep->x, x, (size_t)d * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CUDA_CHECK(cudaStreamSynchronize(st));
+    rep->iterations = iters;
+    rep->converged = done;
+    rep->residuals_size = (int64_t)residuals.size();
+    if (rep->residuals)
+        for (int64_t i = 0; i < rep->residuals_size && i < rep->residuals_capacity; ++i)
+            rep->residuals[i] = residuals[(size_t)i];
+}
+
+// pcg_sketch_size (baselines.hpp:170-187)
+std::pair<int64_t, bool> pcg_sketch_size_impl(int64_t n, int64_t d, int32_t kind, double rho) {
+    if (!(rho > 0.0 && rho < 1.0)) fail(IHS_INVALID_INPUT, "pcg_sketch_size: rho must be in (0,1)");
+    const double m_raw = kind == IHS_SKETCH_GAUSSIAN ? (double)d / rho : (double)d * std::log((double)d) / rho;
+    int64_t m = std::max<int64_t>((int64_t)std::ceil(m_raw), 1);
+    bool capped = false;
+    if (kind == IHS_SKETCH_SRHT) {
+        int64_t n_pad = 1;
+        while (n_pad < n) n_pad <<= 1;
+        if (m > n_pad) {
+            m = n_pad;
+            capped = true;
+        }
+    }
+    return {m, capped};
 }
 
 }  // namespace
@@ -897,6 +1008,122 @@ ihs_status ihs_gpu_gradient(ihs_gpu_problem* P, const double* x, double* g, ihs_
         CUDA_CHECK(cudaMemcpyAsync(g, G, (size_t)d * sizeof(double), cudaMemcpyDeviceToHost, P->st));
         CUDA_CHECK(cudaStreamSynchronize(P->st));
         if (c) c->matvec += 2 * (uint64_t)P->n * (uint64_t)d + (uint64_t)P->n + 2 * (uint64_t)d;  // problem.hpp:66
+    });
+}
+
+// ------------------------------------------------ CG / PCG baselines (baselines.hpp)
+ihs_status ihs_pcg_sketch_size(int64_t n, int64_t d, int32_t kind, double rho, int64_t* m, int32_t* capped) {
+    return guarded([&] {
+        if (!m || !capped) fail(IHS_INVALID_INPUT, "pcg_sketch_size: null output");
+        auto [mm, c] = pcg_sketch_size_impl(n, d, kind, rho);
+        *m = mm;
+        *capped = c;
+    });
+}
+
+extern "C++" {
+namespace {
+// shared frame of the three entry points: validation, device/stream scope, wall clock, device
+// events and launch count; `body` runs the solve and fills the counters
+template <class F>
+ihs_status cg_entry(ihs_gpu_problem* P, const char* who, ihs_cg_report* rep, F&& body) {
+    return guarded([&] {
+        const auto t0 = std::chrono::steady_clock::now();
+        if (!P || !rep || !rep->x) fail(IHS_INVALID_INPUT, std::string(who) + ": null argument");
+        DeviceGuard dg(P->device);
+        StreamScope scope(P->st);
+        const int64_t l0 = g_launches.load();
+        cudaEvent_t ev[2];
+        for (auto& e : ev) CUDA_CHECK(cudaEventCreate(&e));
+        CUDA_CHECK(cudaEventRecord(ev[0], P->st));
+        ihs_counters C{};
+        rep->m = 0;
+        rep->m_capped = 0;
+        rep->setup_flops = 0;
+        try {
+            body(C);
+        } catch (...) {
+            for (auto e : ev) cudaEventDestroy(e);
+            throw;
+        }
+        CUDA_CHECK(cudaEventRecord(ev[1], P->st));
+        CUDA_CHECK(cudaEventSynchronize(ev[1]));
+        float ms = 0.f;
+        CUDA_CHECK(cudaEventElapsedTime(&ms, ev[0], ev[1]));
+        for (auto e : ev) CUDA_CHECK(cudaEventDestroy(e));
+        rep->counters = C;
+        rep->device_ms = ms;
+        rep->kernel_launches = g_launches.load() - l0;
+        rep->wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    });
+}
+
+// the preconditioner from a device sketch SA (m x d, already in sys.SA): Gram form + Cholesky + H_S^{-1}
+void pcg_factor(ihs_gpu_problem* P, ihs_gpu_system& sys, ihs_counters& C, ihs_cg_report* rep) {
+    try {
+        system_factorize(&sys, nullptr);
+    } catch (const Status& e) {
+        if (e.code == IHS_NUMERICAL_BREAKDOWN)
+            fail(IHS_NUMERICAL_BREAKDOWN, "pcg_solve: preconditioner factorization failed");
+        throw;
+    }
+    const uint64_t dd = (uint64_t)sys.d, mm = (uint64_t)sys.m;
+    C.factor += dd * dd * mm + dd * dd * dd / 3;  // baselines.hpp:119-120
+    rep->setup_flops += dd * dd * mm + dd * dd * dd / 3;
+    rep->m = sys.m;
+}
+
+void pcg_system_init(ihs_gpu_problem* P, ihs_gpu_system& sys, int64_t m) {
+    sys.device = P->device;
+    sys.d = P->d;
+    sys.m = m;
+    sys.nu = P->nu;
+    sys.st = P->st;
+    sys.num_sms = P->num_sms;
+    sys.force_gram = true;
+    sys.SA.ensure((size_t)m * P->d * sizeof(double));
+}
+}  // namespace
+}  // extern "C++"
+
+ihs_status ihs_gpu_cg_solve(ihs_gpu_problem* P, double tol, int64_t max_iters, const double* x0,
+                            ihs_cg_report* rep) {
+    return cg_entry(P, "cg_solve", rep, [&](ihs_counters& C) {
+        if (P->orientation != IHS_OVERDETERMINED) fail(IHS_INVALID_INPUT, "cg_solve: expects an overdetermined instance");
+        cg_run(P, nullptr, tol, max_iters, x0, rep, C);
+    });
+}
+
+ihs_status ihs_gpu_pcg_solve_with(ihs_gpu_problem* P, const double* SA, int64_t m, int64_t lds, double tol,
+                                  int64_t max_iters, const double* x0, ihs_cg_report* rep) {
+    return cg_entry(P, "pcg_solve", rep, [&](ihs_counters& C) {
+        if (P->orientation != IHS_OVERDETERMINED)
+            fail(IHS_INVALID_INPUT, "pcg_solve: expects an overdetermined instance");
+        if (!SA || m < 1 || lds < m) fail(IHS_INVALID_INPUT, "pcg_solve: bad sketch shape");
+        ihs_gpu_system sys;
+        pcg_system_init(P, sys, m);
+        CUDA_CHECK(cudaMemcpy2DAsync(sys.SA.p, (size_t)m * sizeof(double), SA, (size_t)lds * sizeof(double),
+                                     (size_t)m * sizeof(double), (size_t)P->d, cudaMemcpyHostToDevice, P->st));
+        pcg_factor(P, sys, C, rep);
+        cg_run(P, &sys, tol, max_iters, x0, rep, C);
+    });
+}
+
+ihs_status ihs_gpu_pcg_solve(ihs_gpu_problem* P, int32_t kind, uint64_t seed, double rho, double tol,
+                             int64_t max_iters, const double* x0, ihs_cg_report* rep) {
+    return cg_entry(P, "pcg_solve", rep, [&](ihs_counters& C) {
+        const int64_t n_rows = P->opts.world_size > 1 ? P->opts.n_global : P->n;
+        auto [m, capped] = pcg_sketch_size_impl(n_rows, P->d, kind, rho);
+        if (P->orientation != IHS_OVERDETERMINED)
+            fail(IHS_INVALID_INPUT, "pcg_solve: expects an overdetermined instance");
+        rep->m_capped = capped;
+        ihs_gpu_system sys;
+        pcg_system_init(P, sys, m);
+        device_sketch(P, kind, m, seed, sys.SA.d(), &C);  // apply_sketch(A, {kind, m, seed}) (baselines.hpp:195)
+        rep->setup_flops += C.sketch;
+        pcg_factor(P, sys, C, rep);
+        rep->m_capped = capped;
+        cg_run(P, &sys, tol, max_iters, x0, rep, C);
     });
 }
 

@@ -643,6 +643,80 @@ def fixed_sketch_ihs(p: ProblemInstance, sys: SketchedSystem, tp: TuningParams, 
     return [out[i].copy() for i in range(T + 1)]
 
 
+# ------------------------------------------------------------------ baselines.hpp
+@dataclass
+class CgResult:
+    """CgResult / PcgResult (baselines.hpp:16-36); m, m_capped, setup_flops stay 0 for plain CG."""
+    x: np.ndarray
+    iterations: int = 0
+    residuals: List[float] = field(default_factory=list)
+    converged: bool = False
+    m: int = 0
+    m_capped: bool = False
+    setup_flops: int = 0
+    counters: CostCounters = field(default_factory=CostCounters)
+    wall_seconds: float = 0.0
+    device_ms: float = 0.0
+    kernel_launches: int = 0
+
+
+PcgResult = CgResult
+
+
+def _run_cg(fn, p: ProblemInstance, max_iters: int, x0, *args) -> CgResult:
+    d = p.cols()
+    x = np.empty(d)
+    cap = max(0, int(max_iters)) + 1
+    res = np.empty(cap)
+    rep = abi.CgReportC()
+    rep.x = abi.dptr(x)
+    rep.residuals = abi.dptr(res)
+    rep.residuals_capacity = cap
+    xs = _vec(x0, d) if x0 is not None else None
+    _check(fn(p.handle, *args, abi.dptr(xs), C.byref(rep)))
+    out = CgResult(x=x, iterations=int(rep.iterations), residuals=res[: min(rep.residuals_size, cap)].tolist(),
+                   converged=bool(rep.converged), m=int(rep.m), m_capped=bool(rep.m_capped),
+                   setup_flops=int(rep.setup_flops), wall_seconds=float(rep.wall_seconds),
+                   device_ms=float(rep.device_ms), kernel_launches=int(rep.kernel_launches))
+    out.counters._absorb(rep.counters)
+    return out
+
+
+def cg_solve(p: ProblemInstance, tol: float, max_iters: int, x0=None) -> CgResult:
+    """CG on the regularized normal equations (baselines.hpp:40-92), H p as one pass over the resident A."""
+    if x0 is not None and np.asarray(x0).size != p.cols():
+        raise InvalidInput("cg_solve: dimension mismatch")
+    return _run_cg(lib().ihs_gpu_cg_solve, p, max_iters, x0, float(tol), int(max_iters))
+
+
+def pcg_solve_with(p: ProblemInstance, SA, tol: float, max_iters: int, x0=None) -> CgResult:
+    """CG preconditioned by the Cholesky factor of SA^T SA + nu^2 I (baselines.hpp:98-165)."""
+    SA = _fortran(SA)
+    if SA.ndim != 2 or SA.shape[1] != p.cols():
+        raise InvalidInput("pcg_solve: dimension mismatch")
+    if x0 is not None and np.asarray(x0).size != p.cols():
+        raise InvalidInput("pcg_solve: dimension mismatch")
+    return _run_cg(lib().ihs_gpu_pcg_solve_with, p, max_iters, x0, abi.dptr(SA), SA.shape[0], SA.shape[0],
+                   float(tol), int(max_iters))
+
+
+def pcg_sketch_size(n: int, d: int, kind: SketchKind, rho: float):
+    """baselines.hpp:170-187 -> (m, capped)."""
+    m, c = C.c_int64(), C.c_int32()
+    _check(lib().ihs_pcg_sketch_size(int(n), int(d), int(kind), float(rho), C.byref(m), C.byref(c)))
+    return int(m.value), bool(c.value)
+
+
+def pcg_solve(p: ProblemInstance, kind: SketchKind, seed: int, rho: float, tol: float, max_iters: int,
+              x0=None) -> CgResult:
+    """Sketch-preconditioned CG with the prescribed sketch size (baselines.hpp:190-200); the sketch, Gram,
+    Cholesky and inverse all run on the device."""
+    if x0 is not None and np.asarray(x0).size != p.cols():
+        raise InvalidInput("pcg_solve: dimension mismatch")
+    return _run_cg(lib().ihs_gpu_pcg_solve, p, max_iters, x0, int(kind), int(seed), float(rho), float(tol),
+                   int(max_iters))
+
+
 # ------------------------------------------------------------------ synthetic data
 def synth_generate(n: int, d: int, spectrum: int = 0, decay: float = 0.95, noise_std: float = 0.01,
                    outlier_frac: float = 0.0, outlier_scale: float = 100.0, data_seed: int = 0, threads: int = 0,
