@@ -10,7 +10,12 @@ through the public API with the H2D upload of A and b from pinned host
 memory and the D2H of x inside the timed region.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config c1..c5]
-                  [--impl b200|reference] [--no-cpu-baseline]
+                  [--impl b200|reference] [--no-cpu-baseline] [--solver ihs|pcg|cg]
+
+--solver pcg|cg times the paper's comparators on the same data instead
+(baselines.hpp: sketch-preconditioned CG with the prescribed sketch size
+m = d/rho or d ln d/rho at bench.hpp's default rho = 0.1, and plain CG), to
+tol 1e-10 on ||H x - A^T b|| <= tol ||A^T b||, max 2000 iterations.
 
 Multi-GPU (torchrun, one rank per GPU): A is row-sharded over the ranks
 (strong scaling of the same problem; --replicas for independent copies),
@@ -51,6 +56,10 @@ CONFIGS = {
                mode="PolyakThenGradient", rho=0.1, m_initial=1, max_sketch=None, enforce_validity=True),
 }
 METRIC = "adaptive-IHS time-to-1e-10 error (r_t/r_1 <= 1e-10)"
+METRICS = {"ihs": METRIC,
+           "pcg": "PCG time-to-1e-10 (||H x - A^T b|| <= 1e-10 ||A^T b||, sketch-preconditioned, baselines.hpp)",
+           "cg": "CG time-to-1e-10 (||H x - A^T b|| <= 1e-10 ||A^T b||, baselines.hpp)"}
+PCG_RHO, CG_TOL, CG_MAX_ITERS = 0.1, 1e-10, 2000  # bench.hpp:32-36 SolverSpec defaults
 L2_BYTES = 126 * 2**20
 
 
@@ -162,20 +171,28 @@ def run_reference(args, c, rank, world):
     times = []
     for i in range(args.warmup_ref + args.steps):
         t0 = time.perf_counter()
-        x, rep, log, _ = O.adaptive_solve(A, b, c["nu"], cfg)
-        dt = time.perf_counter() - t0
+        if args.solver == "ihs":
+            x, rep, log, _ = O.adaptive_solve(A, b, c["nu"], cfg)
+            wall = rep.wall_seconds
+        else:
+            kind = 1 if c["sketch"] == "SRHT" else 0
+            x, _, rep = (O.pcg_solve(A, b, c["nu"], kind, 0, PCG_RHO, CG_TOL, CG_MAX_ITERS) if args.solver == "pcg"
+                         else O.cg_solve(A, b, c["nu"], CG_TOL, CG_MAX_ITERS))
+            wall = time.perf_counter() - t0
         if i >= args.warmup_ref:
-            times.append(rep.wall_seconds)
+            times.append(wall)
     v = float(np.mean(times))
-    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "s", "n_gpus": world, "steps": args.steps,
+    extra = ({"rejections": int(rep.rejections), "final_m": int(rep.final_m)} if args.solver == "ihs"
+             else {"m": int(rep.m), "converged": bool(rep.converged)})
+    line = {"impl": "reference", "metric": METRICS[args.solver], "value": v, "unit": "s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": v * 1e3, "higher_is_better": False, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, SURVEY §8(d) generator)",
             "config": {"workload": c["desc"], **{k: c[k] for k in ("n", "d", "nu", "sketch", "mode", "rho")}},
             "cpu_baseline": {"value": v, "unit": "s", "cores": 1, "kind": "port",
-                             "sample": f"full adaptive_solve of {args.config.upper()} per step (oracle C++ "
+                             "sample": f"full {args.solver} solve of {args.config.upper()} per step (oracle C++ "
                                        "restatement, single thread like the reference)"},
             "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-            "iterations": int(rep.iterations), "rejections": int(rep.rejections), "final_m": int(rep.final_m)}
+            "iterations": int(rep.iterations), **extra}
     print(json.dumps(line), flush=True)
     return 0
 
@@ -193,6 +210,8 @@ def main():
     ap.add_argument("--no-clocks", action="store_true", help="do not sample nvidia-smi during the timed steps")
     ap.add_argument("--out", default=None, help="also write the JSON line here")
     ap.add_argument("--replicas", action="store_true", help="N > 1: independent replicas instead of row sharding")
+    ap.add_argument("--solver", default="ihs", choices=["ihs", "pcg", "cg"],
+                    help="ihs: adaptive Polyak-IHS (the headline); pcg / cg: the baselines.hpp comparators")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     args.warmup_ref = 0  # the CPU reference has nothing to warm up; W is reported as given
@@ -252,6 +271,13 @@ def main():
     else:
         p = ihs.ProblemInstance(A, b, nu, device=local)
     cfg = solver_config(ihs, c)
+    kind = getattr(ihs.SketchKind, c["sketch"])
+    if args.solver == "ihs":
+        solve = lambda: ihs.adaptive_solve(p, cfg)  # noqa: E731
+    elif args.solver == "pcg":
+        solve = lambda: ihs.pcg_solve(p, kind, 0, PCG_RHO, CG_TOL, CG_MAX_ITERS)  # noqa: E731
+    else:
+        solve = lambda: ihs.cg_solve(p, CG_TOL, CG_MAX_ITERS)  # noqa: E731
     flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.float32, device=f"cuda:{local}")
 
     def barrier():
@@ -261,7 +287,7 @@ def main():
         torch.cuda.synchronize()
 
     for _ in range(args.warmup):
-        rep = ihs.adaptive_solve(p, cfg)
+        rep = solve()
     # per-phase CUDA events cost host time on the solve's critical path (~15% of a C2 step): the timed
     # steps run without them; the roofline comes from one instrumented solve right after (see below)
     p.set_phase_timing(False)
@@ -279,7 +305,7 @@ def main():
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record()
-            rep = ihs.adaptive_solve(p, cfg)
+            rep = solve()
             e1.record()
             torch.cuda.synchronize()
             step_ms.append(e0.elapsed_time(e1))
@@ -302,7 +328,7 @@ def main():
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             p.upload(A, b)
-            rep_e = ihs.adaptive_solve(p, cfg)
+            rep_e = solve()
             torch.cuda.synchronize()
             if i > 0:
                 e2e_ms.append((time.perf_counter() - t0) * 1e3)
@@ -320,7 +346,7 @@ def main():
     p.set_phase_timing(True)
     flush.zero_()
     torch.cuda.synchronize()
-    inst = ihs.adaptive_solve(p, cfg)
+    inst = solve()
     last = reps[-1]
     t = inst.device_times
     hbm, peak_kind = peaks()
@@ -332,7 +358,8 @@ def main():
         per_pass = t["gradient_bytes"] / max(1, t["n_gradient"])
         ach = per_pass * t["n_gradient_kernel"] / (t["gradient_kernel_ms"] * 1e-3) / 1e9
         kern["gradient"] = {"kernel": "grad_rr/grad_rm kernel (+grad_reduce) — fused A^T(Ax-b)+nu^2 x, 1-2 RHS, "
-                                      "one pass over A",
+                                      "one pass over A" + (" (b = 0: the CG product H p)" if args.solver != "ihs"
+                                                           else ""),
                             "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
                             "per_launch_ms": t["gradient_kernel_ms"] / t["n_gradient_kernel"],
                             "algorithmic_bytes_per_launch": per_pass,
@@ -369,6 +396,22 @@ def main():
         cpu = {"value": None, "unit": "s", "cores": 1, "kind": "port",
                "sample": "not run: a single-thread oracle solve of this config exceeds the few-minute bench budget "
                          "(the default config C2 carries the CPU baseline)"}
+    elif rank == 0 and world == 1 and not args.no_cpu_baseline and args.solver == "pcg" and \
+            kind == ihs.SketchKind.Gaussian and last.m * n * d > (1 << 34):
+        cpu = {"value": None, "unit": "s", "cores": 1, "kind": "port",
+               "sample": f"not run: the oracle's single-thread Gaussian sketch (m={last.m}) of this config exceeds "
+                         "the few-minute bench budget"}
+    elif rank == 0 and world == 1 and not args.no_cpu_baseline and args.solver != "ihs":
+        from oracle import oracle as O
+        t0 = time.perf_counter()
+        x_ref, _, orep = (O.pcg_solve(A, b, nu, int(kind), 0, PCG_RHO, CG_TOL, CG_MAX_ITERS) if args.solver == "pcg"
+                          else O.cg_solve(A, b, nu, CG_TOL, CG_MAX_ITERS))
+        cpu = {"value": time.perf_counter() - t0, "unit": "s", "cores": 1, "kind": "port",
+               "sample": f"one full {args.solver} solve of {args.config.upper()} (oracle C++ restatement, 1 thread)",
+               "iterations": int(orep.iterations), "same_iterations": int(orep.iterations) == last.iterations}
+        Ad = np.concatenate([A @ (last.x - x_ref), nu * (last.x - x_ref)])
+        Ar = np.concatenate([A @ x_ref, nu * x_ref])
+        cpu["abar_rel_err_vs_oracle"] = float(np.linalg.norm(Ad) / np.linalg.norm(Ar))
     elif rank == 0 and world == 1 and not args.no_cpu_baseline:
         from oracle import oracle as O
         ocfg = oracle_config(O, c)
@@ -382,24 +425,34 @@ def main():
         cpu["abar_rel_err_vs_oracle"] = float(np.linalg.norm(Ad) / np.linalg.norm(Ar))
 
     if rank == 0:
-        line = {"metric": METRIC, "value": ms / 1e3, "unit": "s", "n_gpus": world, "steps": args.steps,
+        if args.solver == "ihs":
+            summary = {"iterations": last.iterations, "rejections": last.rejections, "final_m": last.final_m,
+                       "converged": last.converged, "m_schedule": [e.m for e in last.log if int(e.branch) == 2]}
+            cfg_extra = {"rho": c["rho"], "m_initial": c["m_initial"], "max_sketch": c["max_sketch"],
+                         "enforce_validity": c["enforce_validity"], "eps": 1e-10}
+        else:
+            summary = {"iterations": last.iterations, "converged": last.converged, "m": last.m,
+                       "m_capped": last.m_capped, "residual_ratio": last.residuals[-1] / last.residuals[0]}
+            cfg_extra = {"solver": args.solver, "tol": CG_TOL, "max_iters": CG_MAX_ITERS,
+                         **({"rho": PCG_RHO} if args.solver == "pcg" else {})}
+        summary.update({"lib_total_ms": float(np.mean(lib_ms)), "step_ms": step_ms,
+                        "kernel_launches_per_solve": t["kernel_launches"]})
+        line = {"metric": METRICS[args.solver], "value": ms / 1e3, "unit": "s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
                 "scaling": "strong" if sharded else "weak",
                 "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic (seeded SURVEY §8(d) generator: A = G diag(sigma), x_true, noise)",
-                "config": {"workload": c["desc"], "n": n, "d": d, "nu": nu, "sketch": c["sketch"], "mode": c["mode"],
-                           "rho": c["rho"], "m_initial": c["m_initial"], "max_sketch": c["max_sketch"],
-                           "enforce_validity": c["enforce_validity"], "eps": 1e-10,
+                "config": {"workload": c["desc"] if args.solver == "ihs" else
+                           f"{args.solver.upper()} on the {args.config.upper()} data (n={n}, d={d}, nu={nu})",
+                           "n": n, "d": d, "nu": nu, "sketch": c["sketch"],
+                           **({"mode": c["mode"]} if args.solver == "ihs" else {}), **cfg_extra,
                            "l2": ("inputs larger than L2 (A = %.0f MiB) and L2 flushed between steps"
                                   % (8 * n * d / 2**20)) if 8 * n * d > L2_BYTES else
                                  "L2 flushed (256 MiB write) between timed steps",
                            "parallelism": parallelism},
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
                 "clocks": clocks,
-                "solve": {"iterations": last.iterations, "rejections": last.rejections, "final_m": last.final_m,
-                          "converged": last.converged, "lib_total_ms": float(np.mean(lib_ms)),
-                          "step_ms": step_ms, "kernel_launches_per_solve": t["kernel_launches"],
-                          "m_schedule": [e.m for e in last.log if int(e.branch) == 2]},
+                "solve": summary,
                 "datagen_s": gen_s}
         s = json.dumps(line)
         print(s, flush=True)

@@ -170,6 +170,7 @@ typedef struct ihs_cg_report {
     double wall_seconds;
     double device_ms;               /* GPU: CUDA-event time of the solve on the device timeline */
     int64_t kernel_launches;        /* GPU: kernels this library launched during the solve */
+    ihs_phase_times times;          /* GPU: per-phase device time (sketch, factor, H p passes, recurrences) */
 } ihs_cg_report;
 
 /* Device / sharding options of a problem handle. */
@@ -233,6 +234,14 @@ ihs_status ihs_gpu_problem_upload(ihs_gpu_problem* p, const double* A, int64_t l
 /* Per-phase CUDA-event timing of adaptive solves on this problem (ihs_phase_times; default on).
  * The events cost host time on the solve's critical path, so timed benchmark runs switch them off. */
 ihs_status ihs_gpu_problem_set_phase_timing(ihs_gpu_problem* p, int32_t enabled);
+
+/* Change nu of a resident problem (ProblemInstance checks, problem.hpp:24-32) without re-uploading A:
+ * the regularization path solves one A at a decreasing sequence of nu (bench.hpp:131-171). */
+ihs_status ihs_gpu_problem_set_nu(ihs_gpu_problem* p, double nu);
+/* direct_solve (problem.hpp:73-82): the exact ridge minimizer (d doubles), computed on the device
+ * from the Gram matrix of the resident A (DMMA), its Cholesky factor and iterative refinement with
+ * the fused gradient pass; underdetermined instances through the kernel form x = A^T (A A^T + nu^2 I)^{-1} b. */
+ihs_status ihs_gpu_direct_solve(ihs_gpu_problem* p, double* x_out);
 
 /* gradient (problem.hpp:59-69): g = A^T(Ax - b) + nu^2 x, host in/out. */
 ihs_status ihs_gpu_gradient(ihs_gpu_problem* p, const double* x, double* g, ihs_counters* counters);

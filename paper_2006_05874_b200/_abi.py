@@ -129,6 +129,7 @@ class CgReportC(C.Structure):
         ("wall_seconds", C.c_double),
         ("device_ms", C.c_double),
         ("kernel_launches", C.c_int64),
+        ("times", PhaseTimes),
     ]
 
 

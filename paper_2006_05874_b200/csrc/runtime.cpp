@@ -229,6 +229,9 @@ struct ihs_gpu_system {
     double nu = 0.0;
     int kind = IHS_FACTOR_DIRECT_GRAM;
     bool force_gram = false;  // PCG preconditioner: the d x d Gram form whatever m (baselines.hpp:111-114)
+    const double* SA_view = nullptr;  // factor a matrix owned elsewhere (direct_solve: the problem's A, ld lds_view)
+    int64_t lds_view = 0;
+    void* gram_comm = nullptr;        // row-sharded A: all-reduce the Gram partials before the factorization
     cudaStream_t st = nullptr;
     int num_sms = 148;
     DevBuf SA;    // m x d
@@ -458,10 +461,12 @@ void system_factorize(ihs_gpu_system* S, ihs_counters* c) {
     const int64_t m = S->m, d = S->d;
     cudaStream_t st = S->st;
     if (!(S->nu > 0.0)) fail(IHS_INVALID_INPUT, "SketchedSystem: nu must be positive");
+    const double* SA = S->SA_view ? S->SA_view : S->SA.d();
+    const int64_t lds = S->SA_view ? S->lds_view : m;
     S->info.ensure(2 * sizeof(int));
     int* d_flag = S->info.as<int>() + 1;
     CUDA_CHECK(cudaMemsetAsync(d_flag, 0, sizeof(int), st));
-    if (m * d > 0) check_finite(S->SA.d(), m * d, d_flag, st);
+    if (m * d > 0 && !S->SA_view) check_finite(SA, m * d, d_flag, st);
     S->kind = m < d && !S->force_gram ? IHS_FACTOR_WOODBURY_INNER : IHS_FACTOR_DIRECT_GRAM;
     const int64_t k = S->k();
     S->L.ensure((size_t)k * k * sizeof(double));
@@ -470,14 +475,15 @@ void system_factorize(ihs_gpu_system* S, ihs_counters* c) {
         // inner = SA SA^T + nu^2 I_m (lower)
         const int splitk = dgemm_pick_splitk(m, m, d, S->num_sms);
         if (splitk > 1) S->work.ensure((size_t)splitk * m * m * sizeof(double));
-        dgemm(false, true, m, m, d, 1.0, S->SA.d(), m, S->SA.d(), m, 0.0, S->L.d(), m, true, splitk,
+        dgemm(false, true, m, m, d, 1.0, SA, lds, SA, lds, 0.0, S->L.d(), m, true, splitk,
               splitk > 1 ? S->work.d() : nullptr, st);
     } else {
         // gram = SA^T SA + nu^2 I_d (lower)
         const int splitk = dgemm_pick_splitk(d, d, m, S->num_sms);
         if (splitk > 1) S->work.ensure((size_t)splitk * d * d * sizeof(double));
-        dgemm(true, false, d, d, m, 1.0, S->SA.d(), m, S->SA.d(), m, 0.0, S->L.d(), d, true, splitk,
+        dgemm(true, false, d, d, m, 1.0, SA, lds, SA, lds, 0.0, S->L.d(), d, true, splitk,
               splitk > 1 ? S->work.d() : nullptr, st);
+        if (S->gram_comm) nccl_allreduce_sum(S->L.d(), (size_t)d * d, S->gram_comm, st);
     }
     add_diag(S->L.d(), k, nu2, st);
     // IHS_CHOL_MODE: 2 (default) one cooperative launch; 1 per-panel kernels with fused diagonal
@@ -631,8 +637,14 @@ void cg_run(ihs_gpu_problem* P, const ihs_gpu_system* S, double tol, int64_t max
                                        cudaMemcpyDeviceToHost, st));
         CUDA_CHECK(cudaStreamSynchronize(st));
     };
+    PhaseTimer* tm = P->timer.get();
+    auto mark = [&](int ph) {
+        if (tm) tm->mark(ph);
+    };
+    int64_t passes = 1 + (x0 ? 1 : 0);
     // atb = -(A^T(A 0 - b) + nu^2 0); not counted (baselines.hpp:55 is outside apply_h)
     CUDA_CHECK(cudaMemsetAsync(z, 0, (size_t)d * sizeof(double), st));
+    mark(PH_GRAD);
     problem_grad(P, z, 1, g0);
     if (x0) {
         CUDA_CHECK(cudaMemcpyAsync(x, x0, (size_t)d * sizeof(double), cudaMemcpyHostToDevice, st));
@@ -641,11 +653,13 @@ void cg_run(ihs_gpu_problem* P, const ihs_gpu_system* S, double tol, int64_t max
         CUDA_CHECK(cudaMemsetAsync(x, 0, (size_t)d * sizeof(double), st));
     }
     C.matvec += hv_count;  // the starting residual's H x (baselines.hpp:57 / :128)
+    mark(PH_SOLVE);
     cg_begin(g0, x0 ? hx : nullptr, r, p, tol, d, state, resid, pcg, st);
     if (pcg) {
         gemv_tiled(S->Hinv.d(), d, d, d, r, 1, d, z, d, S->gv.d(), st, dots);
         cg_dir(state, z, dots, p, d, true, st);
     }
+    mark(PH_END);
     read_back(0, 1);
     std::vector<double> residuals{h_resid[0]};
     bool done = cg_state_done(h_state);
@@ -654,13 +668,17 @@ void cg_run(ihs_gpu_problem* P, const ihs_gpu_system* S, double tol, int64_t max
     while (!done && launched < max_iters) {
         const int64_t nb = std::min(B, max_iters - launched);
         for (int64_t k = 0; k < nb; ++k) {
+            mark(PH_GRAD);
             problem_grad(P, p, 1, hp, nullptr, P->zb.d());  // hp = A^T(A p) + nu^2 p
+            mark(PH_SOLVE);
             cg_step(state, p, hp, x, r, resid, launched, d, pcg, st);
             if (pcg) {
                 gemv_tiled(S->Hinv.d(), d, d, d, r, 1, d, z, d, S->gv.d(), st, dots);
                 cg_dir(state, z, dots, p, d, false, st);
             }
         }
+        mark(PH_END);
+        passes += nb;
         read_back(1, nb);
         const int64_t it = cg_state_iter(h_state);
         for (int64_t j = 1; j <= it - launched; ++j) residuals.push_back(h_resid[j]);
@@ -668,6 +686,8 @@ void cg_run(ihs_gpu_problem* P, const ihs_gpu_system* S, double tol, int64_t max
         launched += nb;
     }
     const int64_t iters = (int64_t)residuals.size() - 1;
+    rep->times.n_gradient += passes;
+    rep->times.gradient_bytes += (double)passes * (8.0 * (double)n * (double)d + 8.0 * (double)n);
     C.matvec += (uint64_t)iters * hv_count;
     if (pcg && iters > 0) C.solve += (uint64_t)(done ? iters - 1 : iters) * minv_count;
     CUDA_CHECK(cudaMemcpyAsync(rep->x, x, (size_t)d * sizeof(double), cudaMemcpyDeviceToHost, st));
@@ -678,6 +698,49 @@ void cg_run(ihs_gpu_problem* P, const ihs_gpu_system* S, double tol, int64_t max
     if (rep->residuals)
         for (int64_t i = 0; i < rep->residuals_size && i < rep->residuals_capacity; ++i)
             rep->residuals[i] = residuals[(size_t)i];
+}
+
+// Ridge minimizer of Q (problem.hpp:73-82's direct_solve, reached on the device by the normal
+// equations instead of the stacked QR): H = A^T A + nu^2 I from one DMMA Gram over the resident A
+// (all-reduced over NCCL on a row-sharded problem), its Cholesky factor and explicit inverse, then
+// x = H^{-1} (-grad(0)) and fixed-count iterative refinement x -= H^{-1} grad(x) with the fused
+// gradient pass: each step shrinks the normal-equations error by ~cond(H) eps, so the result matches
+// the QR solve to working accuracy on the conditioning the suite uses. x: device, d doubles.
+void direct_solve_dev(ihs_gpu_problem* Q, double* x, int refinements = 3) {
+    const int64_t d = Q->d;
+    cudaStream_t st = Q->st;
+    ihs_gpu_system S;
+    S.device = Q->device;
+    S.d = d;
+    S.m = Q->lda;
+    S.nu = Q->nu;
+    S.st = st;
+    S.num_sms = Q->num_sms;
+    S.force_gram = true;
+    S.SA_view = Q->A.d();
+    S.lds_view = Q->lda;
+    S.gram_comm = Q->opts.world_size > 1 ? Q->opts.nccl_comm : nullptr;
+    try {
+        system_factorize(&S, nullptr);
+    } catch (const Status& e) {
+        if (e.code == IHS_NUMERICAL_BREAKDOWN) fail(IHS_NUMERICAL_BREAKDOWN, "direct_solve: factorization failed");
+        throw;
+    }
+    DevBuf v;
+    v.ensure((size_t)3 * d * sizeof(double));
+    double *g = v.d(), *dx = g + d, *zero = dx + d;
+    CUDA_CHECK(cudaMemsetAsync(zero, 0, (size_t)d * sizeof(double), st));
+    problem_grad(Q, zero, 1, g);  // -rhs
+    gemv_tiled(S.Hinv.d(), d, d, d, g, 1, d, dx, d, S.gv.d(), st);
+    CUDA_CHECK(cudaMemsetAsync(x, 0, (size_t)d * sizeof(double), st));
+    add_scaled(x, dx, -1.0, d, st);
+    for (int it = 0; it < refinements; ++it) {
+        problem_grad(Q, x, 1, g);
+        gemv_tiled(S.Hinv.d(), d, d, d, g, 1, d, dx, d, S.gv.d(), st);
+        add_scaled(x, dx, -1.0, d, st);
+    }
+    CUDA_CHECK(cudaStreamSynchronize(st));
+    S.st = nullptr;
 }
 
 // pcg_sketch_size (baselines.hpp:170-187)
@@ -992,6 +1055,10 @@ ihs_status ihs_gpu_problem_upload(ihs_gpu_problem* P, const double* A, int64_t l
         DeviceGuard g(P->device);
         if (A && lda < P->n) fail(IHS_INVALID_INPUT, "lda < n");
         upload_Ab(P, A, lda, b);
+        if (A && P->dual) {  // the dual problem holds a transposed copy of A: rebuild it on next use
+            CUDA_CHECK(cudaStreamSynchronize(P->st));
+            P->dual.reset();
+        }
         CUDA_CHECK(cudaStreamSynchronize(P->st));
     });
 }
@@ -1040,26 +1107,48 @@ ihs_status cg_entry(ihs_gpu_problem* P, const char* who, ihs_cg_report* rep, F&&
         rep->m = 0;
         rep->m_capped = 0;
         rep->setup_flops = 0;
+        rep->times = ihs_phase_times{};
+        if (P->timer) P->timer->reset();
         try {
             body(C);
         } catch (...) {
+            if (P->timer) P->timer->active = false;
             for (auto e : ev) cudaEventDestroy(e);
             throw;
         }
         CUDA_CHECK(cudaEventRecord(ev[1], P->st));
         CUDA_CHECK(cudaEventSynchronize(ev[1]));
+        if (P->timer) {
+            double ph[6];
+            int64_t phn[6];
+            P->timer->collect(ph, phn);
+            ihs_phase_times& T = rep->times;
+            T.sketch_ms = ph[PH_SKETCH] + ph[PH_SKETCH_KERNEL];
+            T.sketch_kernel_ms = ph[PH_SKETCH_KERNEL];
+            T.n_sketch_kernel = phn[PH_SKETCH_KERNEL];
+            T.factor_ms = ph[PH_FACTOR];
+            T.gradient_ms = ph[PH_GRAD] + ph[PH_GRAD_KERNEL];
+            T.gradient_kernel_ms = ph[PH_GRAD_KERNEL];
+            T.n_gradient_kernel = phn[PH_GRAD_KERNEL];
+            T.solve_ms = ph[PH_SOLVE];
+            T.n_solve = phn[PH_SOLVE];
+        }
         float ms = 0.f;
         CUDA_CHECK(cudaEventElapsedTime(&ms, ev[0], ev[1]));
         for (auto e : ev) CUDA_CHECK(cudaEventDestroy(e));
         rep->counters = C;
         rep->device_ms = ms;
         rep->kernel_launches = g_launches.load() - l0;
+        rep->times.kernel_launches = rep->kernel_launches;
+        rep->times.total_ms = ms;
         rep->wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     });
 }
 
 // the preconditioner from a device sketch SA (m x d, already in sys.SA): Gram form + Cholesky + H_S^{-1}
 void pcg_factor(ihs_gpu_problem* P, ihs_gpu_system& sys, ihs_counters& C, ihs_cg_report* rep) {
+    if (P->timer) P->timer->mark(PH_FACTOR);
+    rep->times.n_factor = 1;
     try {
         system_factorize(&sys, nullptr);
     } catch (const Status& e) {
@@ -1119,11 +1208,56 @@ ihs_status ihs_gpu_pcg_solve(ihs_gpu_problem* P, int32_t kind, uint64_t seed, do
         rep->m_capped = capped;
         ihs_gpu_system sys;
         pcg_system_init(P, sys, m);
+        if (P->timer) P->timer->mark(PH_SKETCH);
         device_sketch(P, kind, m, seed, sys.SA.d(), &C);  // apply_sketch(A, {kind, m, seed}) (baselines.hpp:195)
+        rep->times.n_sketch = 1;
+        if (kind == IHS_SKETCH_SRHT)
+            rep->times.sketch_bytes = 8.0 * (double)P->n * (double)P->d + 8.0 * (double)m * (double)P->d;
+        else
+            rep->times.sketch_flops = 2.0 * (double)m * (double)P->n * (double)P->d;
         rep->setup_flops += C.sketch;
         pcg_factor(P, sys, C, rep);
         rep->m_capped = capped;
         cg_run(P, &sys, tol, max_iters, x0, rep, C);
+    });
+}
+
+// direct_solve (problem.hpp:73-82): the exact ridge minimizer. Underdetermined instances go
+// through the dual problem in A^T (x = A^T z*, z* = (A A^T + nu^2 I)^{-1} b).
+ihs_status ihs_gpu_direct_solve(ihs_gpu_problem* P, double* x_out) {
+    return guarded([&] {
+        if (!P || !x_out) fail(IHS_INVALID_INPUT, "direct_solve: null argument");
+        DeviceGuard dg(P->device);
+        StreamScope scope(P->st);
+        DevBuf xb;
+        if (P->orientation == IHS_OVERDETERMINED) {
+            xb.ensure((size_t)P->d * sizeof(double));
+            direct_solve_dev(P, xb.d());
+        } else {
+            if (P->opts.world_size > 1) fail(IHS_INVALID_INPUT, "direct_solve: underdetermined sharded instance");
+            ihs_gpu_problem* D = dual_problem(P);
+            xb.ensure((size_t)(P->n + P->d) * sizeof(double));
+            double* z = xb.d() + P->d;
+            direct_solve_dev(D, z);
+            DevBuf work;
+            work.ensure((gemv_tiled_work_doubles(D->n, D->d) + 8) * sizeof(double));
+            gemv_tiled_reset(work.d(), D->n, D->d, P->st);
+            gemv_tiled(D->A.d(), D->n, D->d, D->lda, z, 1, D->d, xb.d(), D->n, work.d(), P->st);  // x = A^T z
+        }
+        CUDA_CHECK(cudaMemcpyAsync(x_out, xb.p, (size_t)P->d * sizeof(double), cudaMemcpyDeviceToHost, P->st));
+        CUDA_CHECK(cudaStreamSynchronize(P->st));
+    });
+}
+
+// nu of a resident problem (ProblemInstance ctor checks, problem.hpp:24-32): the regularization path
+// keeps A on the device across its nu values (bench.hpp:131-171 rebuilds the instance each time)
+ihs_status ihs_gpu_problem_set_nu(ihs_gpu_problem* P, double nu) {
+    return guarded([&] {
+        if (!P) fail(IHS_INVALID_INPUT, "null problem");
+        if (!(nu > 0.0)) fail(IHS_INVALID_INPUT, "ProblemInstance: nu must be strictly positive");
+        if (!std::isfinite(nu)) fail(IHS_INVALID_INPUT, "ProblemInstance: non-finite input");
+        P->nu = nu;
+        if (P->dual) P->dual->nu = nu;
     });
 }
 

@@ -325,6 +325,12 @@ class ProblemInstance:
         """Per-phase CUDA-event timing of adaptive solves (SolveReport.device_times); default on."""
         _check(lib().ihs_gpu_problem_set_phase_timing(self._h, 1 if enabled else 0))
 
+    def set_nu(self, nu: float):
+        """Change nu in place, A staying resident on the device (the regularization path's A-resident
+        sweep; bench.hpp:131-171 rebuilds the instance per nu instead)."""
+        _check(lib().ihs_gpu_problem_set_nu(self._h, float(nu)))
+        self._nu = float(nu)
+
     def upload(self, A=None, b=None):
         """Re-upload A and/or b (same shape) to the device."""
         Af = _fortran(A) if A is not None else None
@@ -342,6 +348,14 @@ def gradient(p: ProblemInstance, x, counters: Optional[CostCounters] = None) -> 
     _check(lib().ihs_gpu_gradient(p.handle, abi.dptr(x), abi.dptr(g), ca.ptr()))
     ca.done()
     return g
+
+
+def direct_solve(p: ProblemInstance) -> np.ndarray:
+    """Exact ridge minimizer (problem.hpp:73-82) on the device: DMMA Gram of the resident A, Cholesky,
+    iterative refinement with the fused gradient; the kernel form through the dual when d > n."""
+    x = np.empty(p.cols())
+    _check(lib().ihs_gpu_direct_solve(p.handle, abi.dptr(x)))
+    return x
 
 
 def prediction_error(p: ProblemInstance, x, x_star) -> float:
@@ -658,6 +672,7 @@ class CgResult:
     wall_seconds: float = 0.0
     device_ms: float = 0.0
     kernel_launches: int = 0
+    device_times: dict = field(default_factory=dict)
 
 
 PcgResult = CgResult
@@ -677,7 +692,8 @@ def _run_cg(fn, p: ProblemInstance, max_iters: int, x0, *args) -> CgResult:
     out = CgResult(x=x, iterations=int(rep.iterations), residuals=res[: min(rep.residuals_size, cap)].tolist(),
                    converged=bool(rep.converged), m=int(rep.m), m_capped=bool(rep.m_capped),
                    setup_flops=int(rep.setup_flops), wall_seconds=float(rep.wall_seconds),
-                   device_ms=float(rep.device_ms), kernel_launches=int(rep.kernel_launches))
+                   device_ms=float(rep.device_ms), kernel_launches=int(rep.kernel_launches),
+                   device_times=rep.times.as_dict())
     out.counters._absorb(rep.counters)
     return out
 
