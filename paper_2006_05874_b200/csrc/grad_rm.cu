@@ -198,16 +198,24 @@ __global__ void transpose_kernel(const double* __restrict__ A, int64_t lda, int6
 constexpr int RW = 8;  // consumer warps
 constexpr int RTHREADS = 32 * RW;
 
-template <int NRHS, int KP, int RR, int NS>
+// CG column groups: a row's d columns are split over CG warps (64 KP columns each; CG = 1 for d <= 512),
+// so x and the column partials of every warp stay in registers up to d = 4096. The CG warps of a row
+// group (RW / CG of them run side by side) combine their partial row dots through shared memory and one
+// named barrier per row, summing them in column-group order: every warp of the group forms the same r.
+template <int NRHS, int KP, int RR, int NS, int CG>
 __global__ void __launch_bounds__(RTHREADS, 1)
 grad_rr_kernel(const double* __restrict__ Arm, int64_t d, int64_t npanels, const double* __restrict__ b,
                const double* __restrict__ X, double* __restrict__ work, CandSpec cs) {
+    constexpr int RG = RW / CG;  // row groups (rows in flight)
     extern __shared__ __align__(128) double sm[];
     const int64_t stage = (int64_t)RR * d;
     double* panel = sm;
     uint64_t* full = reinterpret_cast<uint64_t*>(panel + NS * stage);
     uint64_t* empty = full + NS;
+    double* dotp = reinterpret_cast<double*>(empty + NS);  // [2][RG][CG][NRHS] partial row dots
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const int cg = warp % CG, rg = warp / CG;
+    const int64_t c0 = (int64_t)cg * 64 * KP;  // first column of this warp
     if (t == 0) {
         for (int s = 0; s < NS; ++s) {
             mbar_init(&full[s], 1);
@@ -233,7 +241,7 @@ grad_rr_kernel(const double* __restrict__ Arm, int64_t d, int64_t npanels, const
         double2 xr[NRHS][KP];
 #pragma unroll
         for (int k = 0; k < KP; ++k) {
-            const int64_t j = 2 * lane + 64 * k;
+            const int64_t j = c0 + 2 * lane + 64 * k;
             if (j >= d) {
 #pragma unroll
                 for (int q = 0; q < NRHS; ++q) xr[q][k] = make_double2(0.0, 0.0);
@@ -260,7 +268,7 @@ grad_rr_kernel(const double* __restrict__ Arm, int64_t d, int64_t npanels, const
 #pragma unroll
             for (int q = 0; q < NRHS; ++q) {
                 xr[q][k] = make_double2(xv[0][q], xv[1][q]);
-                if (blockIdx.x == 0 && warp == 0) {
+                if (blockIdx.x == 0 && rg == 0) {
                     cs.out[q * d + j] = xv[0][q];
                     cs.out[q * d + j + 1] = xv[1][q];
                 }
@@ -273,21 +281,22 @@ grad_rr_kernel(const double* __restrict__ Arm, int64_t d, int64_t npanels, const
             for (int k = 0; k < KP; ++k) g[q][k] = make_double2(0.0, 0.0);
         int s = 0;
         uint32_t ph = 0;
+        int par = 0;  // dotp buffer parity (alternates per row)
         for (int64_t p = blockIdx.x; p < npanels; p += gridDim.x) {
             mbar_wait(&full[s], ph);
             const double* P = panel + s * stage;
 #pragma unroll 1
-            for (int rr = 0; rr < RR / RW; ++rr) {
-                const int row = warp + RW * rr;
+            for (int rr = 0; rr < RR / RG; ++rr) {
+                const int row = rg + RG * rr;
                 const double bi = __ldg(b + p * RR + row);
                 double2 a[KP];
 #pragma unroll
                 for (int k = 0; k < KP; ++k) {
-                    const int64_t j = 2 * lane + 64 * k;
+                    const int64_t j = c0 + 2 * lane + 64 * k;
                     a[k] = j < d ? *reinterpret_cast<const double2*>(P + row * d + j) : make_double2(0.0, 0.0);
                 }
                 // the row dot product runs as four independent chains per right-hand side, summed in a
-                // fixed tree
+                // fixed tree (then over the column groups in order)
                 double r[NRHS];
 #pragma unroll
                 for (int q = 0; q < NRHS; ++q) {
@@ -300,8 +309,27 @@ grad_rr_kernel(const double* __restrict__ Arm, int64_t d, int64_t npanels, const
                     double acc = (c4[0] + c4[1]) + (c4[2] + c4[3]);
 #pragma unroll
                     for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-                    r[q] = acc - bi;
+                    r[q] = acc;
                 }
+                if constexpr (CG > 1) {
+                    double* slot = dotp + ((par * RG + rg) * CG) * NRHS;
+                    if (lane == 0)
+#pragma unroll
+                        for (int q = 0; q < NRHS; ++q) slot[cg * NRHS + q] = r[q];
+                    // the group's CG warps; the next row uses the other buffer, and this barrier of the
+                    // next row orders its writes after every read below
+                    asm volatile("bar.sync %0, %1;" ::"r"(1 + rg), "r"(32 * CG) : "memory");
+#pragma unroll
+                    for (int q = 0; q < NRHS; ++q) {
+                        double acc = slot[q];
+#pragma unroll
+                        for (int c = 1; c < CG; ++c) acc += slot[c * NRHS + q];
+                        r[q] = acc;
+                    }
+                    par ^= 1;
+                }
+#pragma unroll
+                for (int q = 0; q < NRHS; ++q) r[q] -= bi;
 #pragma unroll
                 for (int q = 0; q < NRHS; ++q)
 #pragma unroll
@@ -326,38 +354,39 @@ grad_rr_kernel(const double* __restrict__ Arm, int64_t d, int64_t npanels, const
                 ph ^= 1u;
             }
         }
-        // per-warp partials -> shared [warp][q][d] (the ring is free once every warp is here)
+        // per-row-group partials -> shared [rg][q][d] (the ring is free once every warp is here)
         __syncthreads();
         double* red = panel;
 #pragma unroll
         for (int q = 0; q < NRHS; ++q)
 #pragma unroll
             for (int k = 0; k < KP; ++k) {
-                const int64_t j = 2 * lane + 64 * k;
-                if (j < d) *reinterpret_cast<double2*>(red + ((int64_t)warp * NRHS + q) * d + j) = g[q][k];
+                const int64_t j = c0 + 2 * lane + 64 * k;
+                if (j < d) *reinterpret_cast<double2*>(red + ((int64_t)rg * NRHS + q) * d + j) = g[q][k];
             }
         __syncthreads();
         for (int64_t e = t; e < NRHS * d; e += 32 * RW) {
             const int64_t q = e / d, j = e % d;
             double sum = 0.0;
 #pragma unroll
-            for (int w = 0; w < RW; ++w) sum += red[((int64_t)w * NRHS + q) * d + j];
+            for (int w = 0; w < RG; ++w) sum += red[((int64_t)w * NRHS + q) * d + j];
             work[((int64_t)blockIdx.x * NRHS + q) * d + j] = sum;
         }
     }
 }
 
-template <int NRHS, int KP, int RR, int NS>
+template <int NRHS, int KP, int RR, int NS, int CG>
 void launch_rr(const GradPlan& p, const double* Arm, const double* b, const double* X, double* work, cudaStream_t st,
                const CandSpec& cs) {
     const size_t smem = grad_rr_smem(p.d, RR, NS);
     static bool attr = false;
     if (!attr) {
-        CUDA_CHECK(cudaFuncSetAttribute(grad_rr_kernel<NRHS, KP, RR, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        227 * 1024));
+        CUDA_CHECK(cudaFuncSetAttribute(grad_rr_kernel<NRHS, KP, RR, NS, CG>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
         attr = true;
     }
-    LAUNCH((grad_rr_kernel<NRHS, KP, RR, NS>), p.grid, RTHREADS, smem, st, Arm, p.d, p.lda / RR, b, X, work, cs);
+    LAUNCH((grad_rr_kernel<NRHS, KP, RR, NS, CG>), p.grid, RTHREADS, smem, st, Arm, p.d, p.lda / RR, b, X, work,
+           cs);
 }
 
 template <int NRHS, int RR, int NS>
@@ -387,14 +416,26 @@ size_t grad_rm_smem(int64_t d, int R, int nrhs, int ns) {
            (size_t)ns * 8 + 128;
 }
 
+// column groups per row (power of two): 64 * 8 columns per warp at most
+int rr_cg(int64_t d) { return d <= 512 ? 1 : d <= 1024 ? 2 : d <= 2048 ? 4 : 8; }
+
 size_t grad_rr_smem(int64_t d, int R, int ns) {
-    const size_t red = (size_t)RW * 2 * d * sizeof(double);
-    return std::max((size_t)ns * R * d * sizeof(double), red) + (size_t)2 * ns * 8 + 128;
+    const size_t red = (size_t)(RW / rr_cg(d)) * 2 * d * sizeof(double);
+    return std::max((size_t)ns * R * d * sizeof(double), red) + (size_t)2 * ns * 8 + 2 * RW * 2 * 8 + 128;
 }
 
-// v5 geometry: d <= 512 (even), 16-row panels (8-row when 16 do not fit), as many stages as fit 200 KiB (<= 6)
+// v5 geometry: d <= 4096 (even). d <= 512: 16-row panels (8-row when 16 do not fit), as many stages as fit
+// 200 KiB (<= 6); wider rows: 64 KiB panels (8 / 4 / 2 rows for 2 / 4 / 8 column groups), 3 stages
 bool grad_rr_geometry(int64_t d, int64_t lda, int* R, int* ns) {
-    if (d > 512 || d % 2 || d < 2) return false;
+    if (d > 4096 || d % 2 || d < 2) return false;
+    const int cg = rr_cg(d);
+    if (cg > 1) {
+        const int r = 16 / cg;
+        if (lda % r) return false;
+        *R = r;
+        *ns = 3;
+        return grad_rr_smem(d, r, 3) <= 200u * 1024;
+    }
     for (int r : {16, 8}) {
         if (lda % r) continue;
         int k = 6;
@@ -411,17 +452,20 @@ bool grad_rr_geometry(int64_t d, int64_t lda, int* R, int* ns) {
 void grad_rr_run(const GradPlan& p, const double* Arm, const double* b, const double* X, int nrhs, double* work,
                  cudaStream_t st, const CandSpec* csp) {
     const CandSpec cs = csp ? *csp : CandSpec{};
-    const int kp = (int)ceil_div(p.d, 64);
+    const int cg = rr_cg(p.d);
+    const int kp = (int)ceil_div(ceil_div(p.d, cg), 64);
     const int kpc = kp <= 2 ? 2 : kp <= 4 ? 4 : 8;
-#define IHS_RR(KPv, RRv, NSv)                                                                     \
-    if (kpc == KPv && p.R == RRv && p.stages == NSv) {                                            \
-        if (nrhs == 1) launch_rr<1, KPv, RRv, NSv>(p, Arm, b, X, work, st, cs);                    \
-        else launch_rr<2, KPv, RRv, NSv>(p, Arm, b, X, work, st, cs);                              \
+#define IHS_RR(KPv, RRv, NSv, CGv)                                                                \
+    if (cg == CGv && kpc == KPv && p.R == RRv && p.stages == NSv) {                               \
+        if (nrhs == 1) launch_rr<1, KPv, RRv, NSv, CGv>(p, Arm, b, X, work, st, cs);               \
+        else launch_rr<2, KPv, RRv, NSv, CGv>(p, Arm, b, X, work, st, cs);                         \
         return;                                                                                    \
     }
-#define IHS_RR_NS(KPv, RRv) IHS_RR(KPv, RRv, 2) IHS_RR(KPv, RRv, 3) IHS_RR(KPv, RRv, 4) IHS_RR(KPv, RRv, 5) IHS_RR(KPv, RRv, 6)
+#define IHS_RR_NS(KPv, RRv) \
+    IHS_RR(KPv, RRv, 2, 1) IHS_RR(KPv, RRv, 3, 1) IHS_RR(KPv, RRv, 4, 1) IHS_RR(KPv, RRv, 5, 1) IHS_RR(KPv, RRv, 6, 1)
     IHS_RR_NS(2, 16) IHS_RR_NS(4, 16) IHS_RR_NS(8, 16)
     IHS_RR_NS(2, 8) IHS_RR_NS(4, 8) IHS_RR_NS(8, 8)
+    IHS_RR(8, 8, 3, 2) IHS_RR(8, 4, 3, 4) IHS_RR(8, 2, 3, 8)  // wider rows: 257..512 columns per warp
 #undef IHS_RR_NS
 #undef IHS_RR
     fail(IHS_INTERNAL_ERROR, "gradient (register rows): no kernel for the chosen geometry");

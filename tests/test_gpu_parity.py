@@ -148,8 +148,10 @@ def test_gradient_known_answer(gpu):
     assert c.matvec == 2 * 2 * 2 + 2 + 2 * 2  # test_problem.cpp:74-78
 
 
-# d <= 512 even: register-row kernel; odd or wider d: panel kernels
-@pytest.mark.parametrize("n,d", [(100, 3), (4096, 64), (65536 + 7, 130), (20000, 1000), (3000, 77), (70000, 512)])
+# even d <= 4096: register-row kernel (1, 2, 4 or 8 column groups per row); odd d: panel kernels
+@pytest.mark.parametrize("n,d", [(100, 3), (4096, 64), (65536 + 7, 130), (20000, 1000), (3000, 77), (70000, 512),
+                                 (20000 + 3, 1024), (9000, 1538), (5000, 2048), (3001, 3000), (5000, 4096),
+                                 (2000, 1001)])
 def test_gradient_vs_oracle(gpu, O, n, d):
     A = rand_mat(n, n, d)
     b = RNG(1).standard_normal(n)
@@ -292,6 +294,20 @@ def test_solve_underdetermined_reference_cases(gpu, O):
     with pytest.raises(gpu.InvalidInput):
         gpu.adaptive_solve(gpu.ProblemInstance(np.array([[1.0, 1.0]]), [2.0], 1.0, gpu.Orientation.Underdetermined),
                            gpu.SolverConfig())
+
+
+@pytest.mark.parametrize("n,d,kind,decay,nu", [(8192, 1024, "SRHT", 0.997, 0.5), (3000, 2050, "Gaussian", 0.99, 5.0)])
+def test_adaptive_solve_wide_rows_matches_oracle(gpu, O, n, d, kind, decay, nu):
+    # d > 512: the register-row gradient with 2 / 8 column groups per row, candidates formed in-kernel
+    A, b, _ = O.synth(n, d, decay=decay, noise_std=0.05, data_seed=4)
+    cfg, c_or = _cfg_pair(gpu, O, sketch_kind=getattr(gpu.SketchKind, kind), seed=3, rho=0.25,
+                          enforce_validity=False)
+    rep = gpu.adaptive_solve(gpu.ProblemInstance(A, b, nu), cfg)
+    x_ref, rep_ref, log_ref, _ = O.adaptive_solve(A, b, nu, c_or)
+    assert rep.converged and rep_ref.converged
+    assert (rep.rejections, rep.final_m, rep.iterations) == (rep_ref.rejections, rep_ref.final_m, rep_ref.iterations)
+    assert [(e.t, e.m, int(e.branch)) for e in rep.log] == [(l[0], l[1], l[4]) for l in log_ref]
+    assert _abar_rel(A, nu, rep.x, x_ref) <= 1e-10
 
 
 def test_adaptive_solve_deterministic(gpu, O):
