@@ -72,6 +72,15 @@ def peaks():
         return 6650.0, "fallback"
 
 
+def read_stream_peak():
+    """Measured read-only HBM stream (the gradient's and SRHT phase 1's access pattern): tools/hbm_read_bw.cu ->
+    profiles/hbm_read_bw.json. A kernel that only reads A can exceed the copy figure of MEASURED_PEAKS.json."""
+    try:
+        return float(json.loads((ROOT / "profiles" / "hbm_read_bw.json").read_text())["read_gbs"])
+    except Exception:  # noqa: BLE001
+        return None
+
+
 def fp64_peak():
     """Measured fp64 tensor (DMMA) peak: tools/fp64_peak.cu -> profiles/fp64_peak.json."""
     try:
@@ -351,6 +360,7 @@ def main():
     t = inst.device_times
     hbm, peak_kind = peaks()
     fp64, fp64_kind = fp64_peak()
+    rd_peak = read_stream_peak()
     phases = {"gradient": t["gradient_ms"], "sketch": t["sketch_ms"], "factor": t["factor_ms"], "solve": t["solve_ms"]}
     kern = {}
     if t["n_gradient_kernel"] > 0 and t["gradient_kernel_ms"] > 0:
@@ -364,7 +374,8 @@ def main():
                             "per_launch_ms": t["gradient_kernel_ms"] / t["n_gradient_kernel"],
                             "algorithmic_bytes_per_launch": per_pass,
                             "launches": t["n_gradient_kernel"], "total_ms": t["gradient_kernel_ms"],
-                            "peak_source": peak_kind}
+                            "peak_source": peak_kind + " copy bandwidth (MEASURED_PEAKS.json hbm_gbs)",
+                            "read_stream_peak": rd_peak, "frac_read_stream": ach / rd_peak if rd_peak else None}
     if t["n_sketch_kernel"] > 0 and t["sketch_kernel_ms"] > 0:
         sk_ms = t["sketch_kernel_ms"]
         if c["sketch"] == "SRHT":

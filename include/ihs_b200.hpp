@@ -14,6 +14,7 @@
 
 #include "ihs_gpu.h"
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -23,6 +24,7 @@
 #include <stdexcept>
 #include <string>
 #include <utility>
+#include <type_traits>
 #include <vector>
 
 #ifdef IHS_B200_USE_EIGEN
@@ -205,6 +207,14 @@ inline double prediction_error(const ProblemInstance& p, const Vector& x, const 
     double out = 0.0;
     detail::check(ihs_gpu_prediction_error(p.handle(), x.data(), x_star.data(), &out));
     return out;
+}
+
+// problem.hpp:73-82: the exact minimizer (device Gram + Cholesky + iterative refinement; the kernel form
+// through the dual for underdetermined instances)
+inline Vector direct_solve(const ProblemInstance& p) {
+    Vector x(p.cols());
+    detail::check(ihs_gpu_direct_solve(p.handle(), x.data()));
+    return x;
 }
 
 // ------------------------------------------------------------ sketch.hpp
@@ -459,6 +469,84 @@ inline std::vector<Vector> fixed_sketch_ihs(const ProblemInstance& p, const Sket
         out.push_back(std::move(v));
     }
     return out;
+}
+
+// ------------------------------------------------------------ baselines.hpp
+struct CgResult {  // baselines.hpp:16-23
+    Vector x;
+    Index iterations = 0;
+    std::vector<double> residuals;
+    bool converged = false;
+    CostCounters counters;
+    double wall_seconds = 0.0;
+};
+struct PcgResult {  // baselines.hpp:25-36
+    Vector x;
+    Index iterations = 0;
+    std::vector<double> residuals;
+    bool converged = false;
+    Index m = 0;
+    bool m_capped = false;
+    std::uint64_t setup_flops = 0;
+    CostCounters counters;
+    double wall_seconds = 0.0;
+};
+
+namespace detail {
+template <class R, class F>
+R run_cg(const ProblemInstance& p, Index max_iters, const Vector* x0, F&& call) {
+    if (x0 && x0->size() != p.cols()) throw InvalidInput("cg_solve: dimension mismatch");
+    R res;
+    res.x = Vector(p.cols());
+    const Index cap = (max_iters > 0 ? max_iters : 0) + 1;
+    res.residuals.assign(static_cast<size_t>(cap), 0.0);
+    ihs_cg_report rep{};
+    rep.x = res.x.data();
+    rep.residuals = res.residuals.data();
+    rep.residuals_capacity = cap;
+    check(call(x0 ? x0->data() : nullptr, &rep));
+    res.residuals.resize(static_cast<size_t>(std::min<int64_t>(rep.residuals_size, cap)));
+    res.iterations = rep.iterations;
+    res.converged = rep.converged != 0;
+    res.counters = CostCounters{rep.counters.sketch, rep.counters.factor, rep.counters.solve, rep.counters.matvec};
+    res.wall_seconds = rep.wall_seconds;
+    if constexpr (std::is_same_v<R, PcgResult>) {
+        res.m = rep.m;
+        res.m_capped = rep.m_capped != 0;
+        res.setup_flops = rep.setup_flops;
+    }
+    return res;
+}
+}  // namespace detail
+
+inline CgResult cg_solve(const ProblemInstance& p, double tol, Index max_iters, const Vector* x0 = nullptr) {
+    return detail::run_cg<CgResult>(p, max_iters, x0, [&](const double* x0p, ihs_cg_report* r) {
+        return ihs_gpu_cg_solve(p.handle(), tol, max_iters, x0p, r);
+    });
+}
+
+inline PcgResult pcg_solve_with(const ProblemInstance& p, const Matrix& SA, double tol, Index max_iters,
+                                const Vector* x0 = nullptr) {
+    if (SA.cols() != p.cols()) throw InvalidInput("pcg_solve: dimension mismatch");
+    return detail::run_cg<PcgResult>(p, max_iters, x0, [&](const double* x0p, ihs_cg_report* r) {
+        return ihs_gpu_pcg_solve_with(p.handle(), SA.data(), SA.rows(), SA.rows(), tol, max_iters, x0p, r);
+    });
+}
+
+inline std::pair<Index, bool> pcg_sketch_size(Index n, Index d, SketchKind kind, double rho) {
+    int64_t m = 0;
+    int32_t capped = 0;
+    detail::check(ihs_pcg_sketch_size(n, d, kind == SketchKind::SRHT ? IHS_SKETCH_SRHT : IHS_SKETCH_GAUSSIAN, rho,
+                                      &m, &capped));
+    return {static_cast<Index>(m), capped != 0};
+}
+
+inline PcgResult pcg_solve(const ProblemInstance& p, SketchKind kind, std::uint64_t seed, double rho, double tol,
+                           Index max_iters, const Vector* x0 = nullptr) {
+    return detail::run_cg<PcgResult>(p, max_iters, x0, [&](const double* x0p, ihs_cg_report* r) {
+        return ihs_gpu_pcg_solve(p.handle(), kind == SketchKind::SRHT ? IHS_SKETCH_SRHT : IHS_SKETCH_GAUSSIAN, seed,
+                                 rho, tol, max_iters, x0p, r);
+    });
 }
 
 }  // namespace ihs

@@ -49,6 +49,18 @@ class NumericalBreakdown(Error):
     pass
 
 
+class ParseError(Error):
+    """Text-format parse failure; remembers the 1-based line number (errors.hpp:42-51)."""
+
+    def __init__(self, what: str, line: int):
+        super().__init__(f"{what} (line {line})")
+        self.line = line
+
+
+class ShapeError(Error):
+    """Rows of a parsed dataset disagree on width (errors.hpp:53-57)."""
+
+
 class DeviceError(Error):
     """CUDA / NCCL failure (no reference counterpart)."""
 

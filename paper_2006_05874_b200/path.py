@@ -23,6 +23,7 @@ from typing import List, Optional, Sequence
 import numpy as np
 
 from . import ihs
+from .datasets import Dataset
 
 
 class SolverId(enum.IntEnum):  # bench.hpp:17
@@ -50,13 +51,6 @@ class SolverSpec:  # bench.hpp:29-41
 
     def name(self) -> str:
         return self.label if self.label else solver_name(self.id)
-
-
-@dataclass
-class Dataset:
-    """The (A, b) pair a path runs on (datasets.hpp's Dataset, data only)."""
-    A: np.ndarray
-    b: np.ndarray
 
 
 @dataclass

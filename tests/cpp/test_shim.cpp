@@ -251,6 +251,77 @@ int main() {
         ProblemInstance p(random_matrix(8, 3, gen), random_vector(8, gen), 1.0, Orientation::Overdetermined);
         CHECK_THROWS_AS(solve_underdetermined(p, SolverConfig{}), InvalidInput);
     }
+    // ---------------------------------------------------- baselines.hpp (test_baselines.cpp:10-99)
+    {
+        Vector b2(2);
+        b2(0) = 1.0;
+        b2(1) = 2.0;
+        ProblemInstance p(Matrix::Identity(2, 2), b2, 1.0, Orientation::Overdetermined);
+        CgResult r = cg_solve(p, 1e-12, 10);
+        CHECK(r.converged && r.iterations <= 2);
+        CHECK(std::abs(r.x(0) - 0.5) <= 1e-10 && std::abs(r.x(1) - 1.0) <= 1e-10);
+        CHECK(static_cast<Index>(r.residuals.size()) == r.iterations + 1);
+    }
+    {
+        std::mt19937_64 gen(71);
+        Matrix A = random_matrix(12, 4, gen);
+        Vector b = random_vector(12, gen);
+        ProblemInstance p(A, b, 0.6, Orientation::Overdetermined);
+        Vector xs = direct_solve(p);
+        CgResult r = cg_solve(p, 1e-10, 50, &xs);
+        CHECK(r.converged && r.iterations == 0);
+    }
+    {
+        std::mt19937_64 gen(72);
+        Matrix A = random_matrix(30, 6, gen);
+        Vector b = random_vector(30, gen);
+        ProblemInstance p(A, b, 1.0, Orientation::Overdetermined);
+        CgResult r = cg_solve(p, 1e-12, 200);
+        CHECK(r.converged && (r.x - direct_solve(p)).norm() <= 1e-10 * (1.0 + r.x.norm()));
+    }
+    {
+        std::mt19937_64 gen(73);
+        ProblemInstance p(random_matrix(40, 20, gen), random_vector(40, gen), 1e-3, Orientation::Overdetermined);
+        CHECK(!cg_solve(p, 1e-14, 1).converged);
+    }
+    {
+        // an exact preconditioner (SA^T SA = A^T A; the reference uses an orthogonal sketch) converges in one step
+        std::mt19937_64 gen(74);
+        Matrix A = random_matrix(16, 5, gen);
+        Vector b = random_vector(16, gen);
+        ProblemInstance p(A, b, 0.7, Orientation::Overdetermined);
+        PcgResult r = pcg_solve_with(p, A, 1e-10, 20);
+        CHECK(r.converged && r.iterations == 1 && r.m == 16);
+        CHECK((r.x - direct_solve(p)).norm() <= 1e-8 * (1.0 + r.x.norm()));
+    }
+    {
+        auto [mg, cg_capped] = pcg_sketch_size(4096, 32, SketchKind::Gaussian, 0.25);
+        CHECK(mg == 128 && !cg_capped);
+        auto [ms, cs] = pcg_sketch_size(4096, 32, SketchKind::SRHT, 0.25);
+        CHECK(ms == static_cast<Index>(std::ceil(32.0 * std::log(32.0) / 0.25)) && !cs);
+        auto [mc, cc] = pcg_sketch_size(64, 32, SketchKind::SRHT, 0.25);
+        CHECK(mc == 64 && cc);
+        CHECK_THROWS_AS(pcg_sketch_size(64, 32, SketchKind::Gaussian, 1.0), InvalidInput);
+    }
+    {
+        std::mt19937_64 gen(75);
+        Matrix A = random_matrix(64, 8, gen);
+        Vector b = random_vector(64, gen);
+        ProblemInstance p(A, b, 0.5, Orientation::Overdetermined);
+        PcgResult r = pcg_solve(p, SketchKind::Gaussian, 1, 0.25, 1e-8, 50);
+        const std::uint64_t m = static_cast<std::uint64_t>(r.m);
+        CHECK(r.converged && r.setup_flops == m * 64 * 8 + 8 * 8 * m + 8 * 8 * 8 / 3);
+        CHECK((r.x - direct_solve(p)).norm() <= 1e-6 * (1.0 + r.x.norm()));
+    }
+    {
+        std::mt19937_64 gen(62);
+        Matrix A = random_matrix(16, 64, gen);
+        Vector b = random_vector(16, gen);
+        ProblemInstance p(A, b, 0.8, Orientation::Underdetermined);
+        Vector x_ref = ridge_kernel_form(A, b, 0.8);
+        CHECK((direct_solve(p) - x_ref).norm() <= 1e-10 * (1.0 + x_ref.norm()));
+        CHECK_THROWS_AS(cg_solve(p, 1e-8, 5), InvalidInput);
+    }
     std::printf("shim tests: %d passed, %d failed\n", g_pass, g_fail);
     return g_fail;
 }
