@@ -283,12 +283,16 @@ grad_rr_kernel(const double* __restrict__ Arm, int64_t d, int64_t npanels, const
         uint32_t ph = 0;
         int par = 0;  // dotp buffer parity (alternates per row)
         for (int64_t p = blockIdx.x; p < npanels; p += gridDim.x) {
+            // this warp's observations of the panel, loaded while the panel's TMA completes
+            double bq[RR / RG];
+#pragma unroll
+            for (int rr = 0; rr < RR / RG; ++rr) bq[rr] = __ldg(b + p * RR + rg + RG * rr);
             mbar_wait(&full[s], ph);
             const double* P = panel + s * stage;
-#pragma unroll 1
+#pragma unroll
             for (int rr = 0; rr < RR / RG; ++rr) {
                 const int row = rg + RG * rr;
-                const double bi = __ldg(b + p * RR + row);
+                const double bi = bq[rr];
                 double2 a[KP];
 #pragma unroll
                 for (int k = 0; k < KP; ++k) {
