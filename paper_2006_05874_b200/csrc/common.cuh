@@ -29,6 +29,26 @@ inline void cuda_check(cudaError_t e, const char* what, const char* file, int li
 // Every kernel launch of this library goes through LAUNCH so the count of
 // native launches is observable (ihs_gpu_kernel_launch_count).
 void note_launch();
+// Programmatic dependent launch: the kernel may be scheduled while the previous kernel on the stream
+// drains; it must execute griddepcontrol.wait (pdl_wait) before touching that kernel's results.
+#define LAUNCH_PDL(kernel, grid, block, smem, strm_, ...)                                  \
+    do {                                                                                 \
+        cudaLaunchConfig_t cfg_{};                                                       \
+        cfg_.gridDim = (grid);                                                           \
+        cfg_.blockDim = (block);                                                         \
+        cfg_.dynamicSmemBytes = (smem);                                                  \
+        cfg_.stream = (strm_);                                                          \
+        cudaLaunchAttribute at_[1];                                                      \
+        at_[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;                  \
+        at_[0].val.programmaticStreamSerializationAllowed = 1;                           \
+        cfg_.attrs = at_;                                                                \
+        cfg_.numAttrs = 1;                                                               \
+        CUDA_CHECK(cudaLaunchKernelEx(&cfg_, kernel, __VA_ARGS__));                      \
+        ::ihs_b200::note_launch();                                                       \
+    } while (0)
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 #define LAUNCH(kernel, grid, block, smem, stream, ...)                                   \
     do {                                                                                 \
         kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);                     \

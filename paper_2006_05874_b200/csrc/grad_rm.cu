@@ -239,38 +239,47 @@ grad_rr_kernel(const double* __restrict__ Arm, int64_t d, int64_t npanels, const
         // heavy-ball state exactly like candidates_kernel (solver.hpp:182,190; no FMA contraction),
         // CTA 0 publishing them for the caller
         double2 xr[NRHS][KP];
+        if (cs.x == nullptr) {
 #pragma unroll
-        for (int k = 0; k < KP; ++k) {
-            const int64_t j = c0 + 2 * lane + 64 * k;
-            if (j >= d) {
+            for (int k = 0; k < KP; ++k) {
+                const int64_t j = c0 + 2 * lane + 64 * k;
 #pragma unroll
-                for (int q = 0; q < NRHS; ++q) xr[q][k] = make_double2(0.0, 0.0);
-                continue;
+                for (int q = 0; q < NRHS; ++q)
+                    xr[q][k] = j < d ? *reinterpret_cast<const double2*>(X + q * d + j) : make_double2(0.0, 0.0);
             }
-            if (cs.x == nullptr) {
+        } else {
+            // all loads first (16-byte, independent), then the candidate arithmetic
+            double2 xa[KP], ga[KP], pa[KP];
 #pragma unroll
-                for (int q = 0; q < NRHS; ++q) xr[q][k] = make_double2(X[q * d + j], X[q * d + j + 1]);
-                continue;
+            for (int k = 0; k < KP; ++k) {
+                const int64_t j = c0 + 2 * lane + 64 * k;
+                const bool in = j < d;
+                xa[k] = in ? *reinterpret_cast<const double2*>(cs.x + j) : make_double2(0.0, 0.0);
+                ga[k] = in ? *reinterpret_cast<const double2*>(cs.gt + j) : make_double2(0.0, 0.0);
+                pa[k] = in && NRHS == 2 ? *reinterpret_cast<const double2*>(cs.xprev + j) : make_double2(0.0, 0.0);
             }
-            double xv[2][NRHS];
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const double xi = cs.x[j + h], gi = cs.gt[j + h];
-                const double xg = __dsub_rn(xi, __dmul_rn(cs.mu_gd, gi));
-                if (NRHS == 2) {
-                    xv[h][0] = __dadd_rn(__dsub_rn(xi, __dmul_rn(cs.mu_p, gi)),
-                                         __dmul_rn(cs.beta_p, __dsub_rn(xi, cs.xprev[j + h])));
-                    xv[h][NRHS - 1] = xg;
-                } else {
-                    xv[h][0] = xg;
+            for (int k = 0; k < KP; ++k) {
+                const int64_t j = c0 + 2 * lane + 64 * k;
+                double xv[2][NRHS];
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const double xi = h ? xa[k].y : xa[k].x, gi = h ? ga[k].y : ga[k].x;
+                    const double xg = __dsub_rn(xi, __dmul_rn(cs.mu_gd, gi));
+                    if (NRHS == 2) {
+                        const double xp = h ? pa[k].y : pa[k].x;
+                        xv[h][0] = __dadd_rn(__dsub_rn(xi, __dmul_rn(cs.mu_p, gi)),
+                                             __dmul_rn(cs.beta_p, __dsub_rn(xi, xp)));
+                        xv[h][NRHS - 1] = xg;
+                    } else {
+                        xv[h][0] = xg;
+                    }
                 }
-            }
 #pragma unroll
-            for (int q = 0; q < NRHS; ++q) {
-                xr[q][k] = make_double2(xv[0][q], xv[1][q]);
-                if (blockIdx.x == 0 && rg == 0) {
-                    cs.out[q * d + j] = xv[0][q];
-                    cs.out[q * d + j + 1] = xv[1][q];
+                for (int q = 0; q < NRHS; ++q) {
+                    xr[q][k] = j < d ? make_double2(xv[0][q], xv[1][q]) : make_double2(0.0, 0.0);
+                    if (blockIdx.x == 0 && rg == 0 && j < d)
+                        *reinterpret_cast<double2*>(cs.out + q * d + j) = make_double2(xv[0][q], xv[1][q]);
                 }
             }
         }
@@ -282,11 +291,16 @@ grad_rr_kernel(const double* __restrict__ Arm, int64_t d, int64_t npanels, const
         int s = 0;
         uint32_t ph = 0;
         int par = 0;  // dotp buffer parity (alternates per row)
-        for (int64_t p = blockIdx.x; p < npanels; p += gridDim.x) {
-            // this warp's observations of the panel, loaded while the panel's TMA completes
-            double bq[RR / RG];
+        // this warp's observations one panel ahead (global-load latency hidden behind a whole panel)
+        double bq[RR / RG];
 #pragma unroll
-            for (int rr = 0; rr < RR / RG; ++rr) bq[rr] = __ldg(b + p * RR + rg + RG * rr);
+        for (int rr = 0; rr < RR / RG; ++rr)
+            bq[rr] = (int64_t)blockIdx.x < npanels ? __ldg(b + (int64_t)blockIdx.x * RR + rg + RG * rr) : 0.0;
+        for (int64_t p = blockIdx.x; p < npanels; p += gridDim.x) {
+            double bn[RR / RG];
+            const int64_t pn_b = p + gridDim.x < npanels ? p + gridDim.x : p;
+#pragma unroll
+            for (int rr = 0; rr < RR / RG; ++rr) bn[rr] = __ldg(b + pn_b * RR + rg + RG * rr);
             mbar_wait(&full[s], ph);
             const double* P = panel + s * stage;
 #pragma unroll
@@ -357,8 +371,11 @@ grad_rr_kernel(const double* __restrict__ Arm, int64_t d, int64_t npanels, const
                 s = 0;
                 ph ^= 1u;
             }
+#pragma unroll
+            for (int rr = 0; rr < RR / RG; ++rr) bq[rr] = bn[rr];
         }
         // per-row-group partials -> shared [rg][q][d] (the ring is free once every warp is here)
+        pdl_trigger();  // the fixed-order reduce may be scheduled now; it waits for this grid to finish
         __syncthreads();
         double* red = panel;
 #pragma unroll

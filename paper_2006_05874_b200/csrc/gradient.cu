@@ -294,6 +294,7 @@ __global__ void __launch_bounds__(256) grad_reduce_kernel(const double* __restri
                                                           int nrhs, const double* __restrict__ X, double nu2,
                                                           double* __restrict__ G) {
     __shared__ double s[16][17];
+    pdl_wait();  // launched programmatically after the partial-sum kernel
     const int64_t total = (int64_t)nrhs * d;
     const int c = threadIdx.x % 16, g = threadIdx.x / 16;
     const int64_t e = (int64_t)blockIdx.x * 16 + c;
@@ -409,8 +410,8 @@ void grad_run(const GradPlan& p, const double* d_A, const double* d_b, double nu
         else if (nrhs == 1) launch_v2_dispatch<1>(p, d_A, d_b, d_X, d_work, st);
         else launch_v2_dispatch<2>(p, d_A, d_b, d_X, d_work, st);
         const int64_t total = (int64_t)nrhs * p.d;
-        LAUNCH(grad_reduce_kernel, (unsigned)ceil_div(total, 16), 256, 0, st, d_work, p.grid, p.d, nrhs, d_X, nu2,
-               d_G);
+        LAUNCH_PDL(grad_reduce_kernel, dim3((unsigned)ceil_div(total, 16)), dim3(256), 0, st, (const double*)d_work,
+                   p.grid, p.d, nrhs, d_X, nu2, d_G);
         return;
     }
     const size_t smem = grad_smem(p.d, nrhs);
