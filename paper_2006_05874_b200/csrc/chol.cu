@@ -25,47 +25,52 @@ namespace {
 constexpr int NB = 64;
 constexpr int TRSM_WARPS = 8;  // rows (warps) per CTA of the panel solves
 
-// Unblocked LLT of the nb x nb diagonal block at (k,k), in shared memory.
-// 256 threads = 64 rows x 4 column groups; per column: every thread derives
-// the pivot itself, one barrier after the column scaling, one after the
-// rank-1 update (no integer division in the loops).
+// Unblocked LLT of the nb x nb diagonal block at (k,k): right-looking elimination on the unscaled
+// columns, a_ik -= a_ij (a_kj / a_jj), with the factor l_ij = a_ij / sqrt(a_jj) formed after the loop
+// from the kept pivots. 256 threads = 64 rows x 4 column interleaves; thread (i, g) keeps its entries
+// a_i,jj (jj = g mod 4) in registers for the whole factorization, so a column step is: read the
+// pivot column (broadcast shared reads), rcp + 16 predicated FMAs on registers, and the owner of
+// column j+1 publishes it into the other half of a double-buffered column — one barrier per column.
 __global__ void __launch_bounds__(256) potrf_diag_kernel(double* __restrict__ H, int64_t n, int64_t k, int nb,
                                                          int* __restrict__ info) {
-    // Right-looking elimination on the unscaled columns, a_ik -= a_ij (a_kj / a_jj), one barrier per
-    // column; the serial path per column is rcp + mul + fma and the factor l_ij = a_ij / sqrt(a_jj) is
-    // formed for all entries after the loop (the pivots a_jj are kept in piv).
-    __shared__ double a[NB][NB + 1];
+    __shared__ double col[2][NB];  // the current pivot column (unscaled), double-buffered
+    __shared__ double out[NB][NB + 1];
     __shared__ double piv[NB];
-    const int i = threadIdx.x % NB, g = threadIdx.x / NB;  // row, column group (4)
-    for (int jj = g; jj < nb; jj += 4) a[i][jj] = (i < nb && i >= jj) ? H[(k + i) + (k + jj) * n] : 0.0;
+    const int i = threadIdx.x % NB, g = threadIdx.x / NB;  // row, column interleave (4)
+    double r[NB / 4];
+#pragma unroll
+    for (int t = 0; t < NB / 4; ++t) {
+        const int jj = g + 4 * t;
+        r[t] = (i < nb && jj < nb && i >= jj) ? H[(k + i) + (k + jj) * n] : 0.0;
+    }
+    if (g == 0) col[0][i] = r[0];  // column 0 is owned by interleave 0
     __syncthreads();
     for (int j = 0; j < nb; ++j) {
-        double s = a[j][j];
+        const double* cj = col[j & 1];
+        double s = cj[j];
         const bool ok = (s > 0.0) && isfinite(s);
         if (!ok) s = 1.0;  // a failed pivot is flagged; keep going harmlessly
         if (threadIdx.x == 0) {
             piv[j] = s;
             if (!ok) atomicCAS(info, 0, (int)(k + j + 1));
         }
-        if (i > j && i < nb) {
-            const double f = a[i][j] * __drcp_rn(s);
-            // only the active columns jj in (j, i] of this thread's interleave (jj = g mod 4): the
-            // work shrinks with j instead of sweeping all 16 slots every column
-            int jj = g + 4 * ((j + 4 - g) / 4);  // first jj = g (mod 4) with jj > j
-            for (; jj + 4 <= i; jj += 8) {
-                const double w0 = a[jj][j], w1 = a[jj + 4][j];
-                const double v0 = a[i][jj], v1 = a[i][jj + 4];
-                a[i][jj] = fma(-f, w0, v0);
-                a[i][jj + 4] = fma(-f, w1, v1);
-            }
-            if (jj <= i) a[i][jj] = fma(-f, a[jj][j], a[i][jj]);
+        if (g == (j & 3) && i >= j) out[i][j] = cj[i];  // final (unscaled) column j
+        const bool act = i > j && i < nb;
+        const double f = act ? cj[i] * __drcp_rn(s) : 0.0;
+        // owner of column j+1 first (it feeds the next step), then the rest of this thread's columns
+        const int jn = j + 1;
+#pragma unroll
+        for (int t = 0; t < NB / 4; ++t) {
+            const int jj = g + 4 * t;
+            if (act && jj > j && jj <= i) r[t] = fma(-f, cj[jj], r[t]);
+            if (jj == jn) col[jn & 1][i] = r[t];
         }
         __syncthreads();
     }
     for (int jj = g; jj < nb; jj += 4) {
         if (i < nb && i >= jj) {
             const double pj = piv[jj];
-            H[(k + i) + (k + jj) * n] = (i == jj) ? sqrt(pj) : a[i][jj] * rsqrt(pj);
+            H[(k + i) + (k + jj) * n] = (i == jj) ? sqrt(pj) : out[i][jj] * rsqrt(pj);
         }
     }
 }

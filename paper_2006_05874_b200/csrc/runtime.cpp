@@ -232,6 +232,11 @@ struct ihs_gpu_system {
     const double* SA_view = nullptr;  // factor a matrix owned elsewhere (direct_solve: the problem's A, ld lds_view)
     int64_t lds_view = 0;
     void* gram_comm = nullptr;        // row-sharded A: all-reduce the Gram partials before the factorization
+    // adaptive loop: the factorization's status is read back with the next host synchronization the
+    // loop makes anyway (system_check) instead of a dedicated round trip per factorization
+    bool defer_info = false;
+    bool info_pending = false;
+    PinnedBuf h_info;
     cudaStream_t st = nullptr;
     int num_sms = 148;
     DevBuf SA;    // m x d
@@ -457,6 +462,16 @@ void device_sketch(ihs_gpu_problem* P, int kind, int64_t m, uint64_t seed, doubl
 // ---------------------------------------------------- sketched system (device)
 // SketchedSystem::factorize (sketched_system.hpp:25-31, 69-84) of a device SA
 // already stored in sys->SA.
+// Raise the status of the last factorization (sketched_system.hpp:82-83); the stream must have
+// passed the factorization's status copy (a synchronization after it).
+void system_check(ihs_gpu_system* S) {
+    if (!S->info_pending) return;
+    S->info_pending = false;
+    const int* h = static_cast<const int*>(S->h_info.p);
+    if (h[1]) fail(IHS_INVALID_INPUT, "SketchedSystem: non-finite sketched matrix");
+    if (h[0]) fail(IHS_NUMERICAL_BREAKDOWN, "SketchedSystem: Cholesky factorization failed");
+}
+
 void system_factorize(ihs_gpu_system* S, ihs_counters* c) {
     const int64_t m = S->m, d = S->d;
     cudaStream_t st = S->st;
@@ -522,11 +537,13 @@ void system_factorize(ihs_gpu_system* S, ihs_counters* c) {
     const int64_t gm = S->kind == IHS_FACTOR_DIRECT_GRAM ? d : m;
     S->gv.ensure((gemv_tiled_work_doubles(gm, d) + 8) * sizeof(double));
     gemv_tiled_reset(S->gv.d(), gm, d, st);
-    int h_info[2] = {0, 0};
-    CUDA_CHECK(cudaMemcpyAsync(h_info, S->info.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
-    CUDA_CHECK(cudaStreamSynchronize(st));
-    if (h_info[1]) fail(IHS_INVALID_INPUT, "SketchedSystem: non-finite sketched matrix");
-    if (h_info[0]) fail(IHS_NUMERICAL_BREAKDOWN, "SketchedSystem: Cholesky factorization failed");
+    S->h_info.ensure(2 * sizeof(int));
+    CUDA_CHECK(cudaMemcpyAsync(S->h_info.p, S->info.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+    S->info_pending = true;
+    if (!S->defer_info) {
+        CUDA_CHECK(cudaStreamSynchronize(st));
+        system_check(S);
+    }
     S->tmp.ensure((size_t)(4 * std::max(m, d) + cholesky_solve_work_doubles(k)) * sizeof(double));
     if (c) c->factor += S->factor_flops();
 }
@@ -1579,6 +1596,7 @@ void adaptive_solve_impl(ihs_gpu_problem* P, const ihs_solver_config* cfg, ihs_s
         sys.nu = P->nu;
         sys.st = st;
         sys.num_sms = P->num_sms;
+        sys.defer_info = true;
         auto sketch_and_factor = [&](int64_t mm, uint64_t sub_seed) {
             sys.m = mm;
             sys.SA.ensure((size_t)mm * dim * sizeof(double));
@@ -1660,6 +1678,7 @@ void adaptive_solve_impl(ihs_gpu_problem* P, const ihs_solver_config* cfg, ihs_s
         tm.mark(PH_END);
         CUDA_CHECK(cudaMemcpyAsync(hd, dots, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
         CUDA_CHECK(cudaStreamSynchronize(st));
+        system_check(&sys);
         double r = decrement(hd[0], hd[1]);
         const double r1 = r;
         push_iterate(xcur);
@@ -1748,6 +1767,7 @@ void adaptive_solve_impl(ihs_gpu_problem* P, const ihs_solver_config* cfg, ihs_s
                 enqueue_eval(spec, S.X2 + spec_slot * dim, xcur, S.GT2 + spec_slot * dim, want_polyak);
             }
             CUDA_CHECK(cudaEventSynchronize(S.ev));
+            system_check(&sys);
             const double* hv = S.hd;
             const uint64_t grad_cost = 2 * (uint64_t)n_rows * (uint64_t)dim + (uint64_t)n_rows + 2 * (uint64_t)dim;
             if (want_polyak) {
@@ -1796,6 +1816,7 @@ void adaptive_solve_impl(ihs_gpu_problem* P, const ihs_solver_config* cfg, ihs_s
                 tm.mark(PH_END);
                 CUDA_CHECK(cudaMemcpyAsync(hd, dots, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
                 CUDA_CHECK(cudaStreamSynchronize(st));
+                system_check(&sys);
                 r = decrement(hd[0], hd[1]);
                 converged = r <= cfg->eps * r1;
             } else {
@@ -1810,6 +1831,7 @@ void adaptive_solve_impl(ihs_gpu_problem* P, const ihs_solver_config* cfg, ihs_s
         CUDA_CHECK(cudaMemcpyAsync(rep->x, xcur, (size_t)dim * 8, cudaMemcpyDeviceToHost, st));
         CUDA_CHECK(cudaEventRecord(ev_end, st));
         CUDA_CHECK(cudaStreamSynchronize(st));
+        system_check(&sys);
         {
             float ms = 0.f;
             CUDA_CHECK(cudaEventElapsedTime(&ms, ev_begin, ev_end));
