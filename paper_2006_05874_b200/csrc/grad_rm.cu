@@ -225,7 +225,8 @@ grad_rr_kernel(const double* __restrict__ Arm, int64_t d, int64_t npanels, const
     }
     __syncthreads();
     const uint32_t stage_bytes = (uint32_t)(stage * sizeof(double));
-    // prologue: the first NS panels
+    // prologue: the first NS panels (A is constant for the whole solve, so these loads may overlap the
+    // tail of the previous kernel under programmatic dependent launch)
     if (t == 0) {
         int64_t p = blockIdx.x;
         for (int k = 0; k < NS && p < npanels; ++k, p += gridDim.x) {
@@ -233,6 +234,7 @@ grad_rr_kernel(const double* __restrict__ Arm, int64_t d, int64_t npanels, const
             bulk_load(panel + k * stage, Arm + p * stage, stage_bytes, &full[k]);
         }
     }
+    pdl_wait();  // x / the heavy-ball state and the work buffer belong to the previous kernels
     {
         // ---------------- consumers
         // x of the right-hand sides in registers: read, or (cs.x != nullptr) formed here from the
@@ -406,8 +408,8 @@ void launch_rr(const GradPlan& p, const double* Arm, const double* b, const doub
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
         attr = true;
     }
-    LAUNCH((grad_rr_kernel<NRHS, KP, RR, NS, CG>), p.grid, RTHREADS, smem, st, Arm, p.d, p.lda / RR, b, X, work,
-           cs);
+    LAUNCH_PDL((grad_rr_kernel<NRHS, KP, RR, NS, CG>), dim3(p.grid), dim3(RTHREADS), smem, st, Arm, p.d,
+               p.lda / RR, b, X, work, cs);
 }
 
 template <int NRHS, int RR, int NS>

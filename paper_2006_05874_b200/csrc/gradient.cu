@@ -295,6 +295,7 @@ __global__ void __launch_bounds__(256) grad_reduce_kernel(const double* __restri
                                                           double* __restrict__ G) {
     __shared__ double s[16][17];
     pdl_wait();  // launched programmatically after the partial-sum kernel
+    pdl_trigger();
     const int64_t total = (int64_t)nrhs * d;
     const int c = threadIdx.x % 16, g = threadIdx.x / 16;
     const int64_t e = (int64_t)blockIdx.x * 16 + c;

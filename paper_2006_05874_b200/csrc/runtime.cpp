@@ -292,6 +292,11 @@ struct ihs_gpu_problem {
     DevBuf dots;                 // 24 doubles (4 per evaluation set + first/resketch decrements)
     PinnedBuf h_dots;
     cudaEvent_t set_ev[4] = {nullptr, nullptr, nullptr, nullptr};  // evaluation-set completion events
+    cudaEvent_t set_ready[4] = {nullptr, nullptr, nullptr, nullptr};  // evaluation results ready on st
+    // side stream for the decision read-backs: the main stream then runs the evaluation kernels back
+    // to back, so each may launch programmatically while its predecessor drains
+    cudaStream_t st2 = nullptr;
+    StreamOwner owner2;
     // underdetermined instances (dual.hpp): the dual problem in A^T, built on first use, and on the dual
     // problem itself the observation vector subtracted from every gradient (non-owning, n doubles)
     std::unique_ptr<ihs_gpu_problem> dual;
@@ -303,6 +308,8 @@ struct ihs_gpu_problem {
     bool zb_ready = false;
     ~ihs_gpu_problem() {
         for (auto e : set_ev)
+            if (e) cudaEventDestroy(e);
+        for (auto e : set_ready)
             if (e) cudaEventDestroy(e);
     }
     std::unique_ptr<PhaseTimer> timer;
@@ -808,6 +815,9 @@ void finish_setup(ihs_gpu_problem* Q) {
     Q->dots.ensure(24 * sizeof(double));
     Q->h_dots.ensure(24 * sizeof(double));
     for (auto& e : Q->set_ev) CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    for (auto& e : Q->set_ready) CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    CUDA_CHECK(cudaStreamCreateWithFlags(&Q->st2, cudaStreamNonBlocking));
+    Q->owner2.s = Q->st2;
     Q->timer = std::make_unique<PhaseTimer>(Q->st);
     {
         // IHS_PHASE_TIMER=0: no per-phase events (A/B of the timers' own cost)
@@ -1635,7 +1645,7 @@ void adaptive_solve_impl(ihs_gpu_problem* P, const ihs_solver_config* cfg, ihs_s
         double* gt = base + 3 * dim;
         struct EvalSet {
             double *X2, *G2, *GT2, *dots, *hd;
-            cudaEvent_t ev;
+            cudaEvent_t ev, ready;
             bool polyak;  // both candidates evaluated
         } sets[NSETS];
         P->dots.ensure(24 * sizeof(double));
@@ -1645,7 +1655,7 @@ void adaptive_solve_impl(ihs_gpu_problem* P, const ihs_solver_config* cfg, ihs_s
         for (int k = 0; k < NSETS; ++k) {
             double* sb = base + (4 + 6 * k) * dim;
             sets[k] = EvalSet{sb, sb + 2 * dim, sb + 4 * dim, P->dots.d() + 4 * k,
-                              static_cast<double*>(P->h_dots.p) + 4 * k, P->set_ev[k], false};
+                              static_cast<double*>(P->h_dots.p) + 4 * k, P->set_ev[k], P->set_ready[k], false};
         }
 
         auto decrement = [&](double dotv, double sq) -> double {  // sketched_system.hpp:95-101
@@ -1715,8 +1725,10 @@ void adaptive_solve_impl(ihs_gpu_problem* P, const ihs_solver_config* cfg, ihs_s
             tm.mark(PH_SOLVE);
             system_solve_dots(&sys, Ge, GTe, nr, S.dots);
             tm.mark(PH_END);
-            CUDA_CHECK(cudaMemcpyAsync(S.hd, S.dots, (size_t)2 * nr * sizeof(double), cudaMemcpyDeviceToHost, st));
-            CUDA_CHECK(cudaEventRecord(S.ev, st));
+            CUDA_CHECK(cudaEventRecord(S.ready, st));
+            CUDA_CHECK(cudaStreamWaitEvent(P->st2, S.ready, 0));
+            CUDA_CHECK(cudaMemcpyAsync(S.hd, S.dots, (size_t)2 * nr * sizeof(double), cudaMemcpyDeviceToHost, P->st2));
+            CUDA_CHECK(cudaEventRecord(S.ev, P->st2));
             S.polyak = polyak;
         };
         // Speculation: while the host waits for evaluation t, the evaluation of t+1 under the predicted

@@ -81,6 +81,7 @@ __global__ void __launch_bounds__(256) gemv_tiled_kernel(const double* __restric
                                                          int64_t ldx, double* __restrict__ part,
                                                          unsigned* __restrict__ arrivals, double* __restrict__ y,
                                                          int64_t ldy, double* __restrict__ dots) {
+    pdl_wait();  // x is the previous kernel's output when launched programmatically
     const int64_t r0 = (int64_t)blockIdx.x * GV_ROWS, c0 = (int64_t)blockIdx.y * GV_COLS;
     const int64_t c1 = c0 + GV_COLS < N ? c0 + GV_COLS : N;
     __shared__ double xs[2][GV_COLS];
@@ -226,7 +227,7 @@ void gemv_tiled(const double* A, int64_t M, int64_t N, int64_t lda, const double
                 int64_t ldy, double* work, cudaStream_t st, double* dots) {
     dim3 grid((unsigned)ceil_div(M, GV_ROWS), (unsigned)ceil_div(N, GV_COLS));
     unsigned* arrivals = reinterpret_cast<unsigned*>(work + (size_t)grid.y * 2 * (size_t)M);
-    LAUNCH(gemv_tiled_kernel, grid, 256, 0, st, A, M, N, lda, x, nrhs, ldx, work, arrivals, y, ldy, dots);
+    LAUNCH_PDL(gemv_tiled_kernel, grid, dim3(256), 0, st, A, M, N, lda, x, nrhs, ldx, work, arrivals, y, ldy, dots);
 }
 
 void gemv_tiled_reset(double* work, int64_t M, int64_t N, cudaStream_t st) {
