@@ -46,6 +46,7 @@ __global__ void __launch_bounds__(CG_T) cg_begin_kernel(const double* __restrict
                                                         double* __restrict__ r, double* __restrict__ p, double tol,
                                                         int64_t d, CgState* __restrict__ s, double* __restrict__ resid,
                                                         int pcg) {
+    pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible after this
     __shared__ double red[32];
     double sa = 0.0, sr = 0.0;
     for (int64_t i = threadIdx.x; i < d; i += blockDim.x) {
@@ -74,6 +75,7 @@ __global__ void __launch_bounds__(CG_T) cg_step_kernel(CgState* __restrict__ s, 
                                                        const double* __restrict__ hp, double* __restrict__ x,
                                                        double* __restrict__ r, double* __restrict__ resid,
                                                        int64_t base, int64_t d, int pcg) {
+    pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible after this
     __shared__ double red[32];
     if (s->done) return;
     const double rz = s->rz, target = s->target;
@@ -106,6 +108,7 @@ __global__ void __launch_bounds__(CG_T) cg_step_kernel(CgState* __restrict__ s, 
 __global__ void __launch_bounds__(CG_T) cg_dir_kernel(CgState* __restrict__ s, const double* __restrict__ z,
                                                       const double* __restrict__ dots, double* __restrict__ p,
                                                       int64_t d, int first) {
+    pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible after this
     if (s->done) return;
     const double rz_new = dots[0];
     const double beta = first ? 0.0 : rz_new / s->rz;
@@ -122,16 +125,16 @@ bool cg_state_done(const void* h_state) { return static_cast<const CgState*>(h_s
 
 void cg_begin(const double* g0, const double* hx, double* r, double* p, double tol, int64_t d, void* state,
               double* resid, bool pcg, cudaStream_t st) {
-    LAUNCH(cg_begin_kernel, 1, CG_T, 0, st, g0, hx, r, p, tol, d, static_cast<CgState*>(state), resid, (int)pcg);
+    LAUNCH_PDL(cg_begin_kernel, 1, CG_T, 0, st, g0, hx, r, p, tol, d, static_cast<CgState*>(state), resid, (int)pcg);
 }
 
 void cg_step(void* state, double* p, const double* hp, double* x, double* r, double* resid, int64_t base, int64_t d,
              bool pcg, cudaStream_t st) {
-    LAUNCH(cg_step_kernel, 1, CG_T, 0, st, static_cast<CgState*>(state), p, hp, x, r, resid, base, d, (int)pcg);
+    LAUNCH_PDL(cg_step_kernel, 1, CG_T, 0, st, static_cast<CgState*>(state), p, hp, x, r, resid, base, d, (int)pcg);
 }
 
 void cg_dir(void* state, const double* z, const double* dots, double* p, int64_t d, bool first, cudaStream_t st) {
-    LAUNCH(cg_dir_kernel, 1, CG_T, 0, st, static_cast<CgState*>(state), z, dots, p, d, (int)first);
+    LAUNCH_PDL(cg_dir_kernel, 1, CG_T, 0, st, static_cast<CgState*>(state), z, dots, p, d, (int)first);
 }
 
 }  // namespace ihs_b200

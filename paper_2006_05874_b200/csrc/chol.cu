@@ -33,6 +33,7 @@ constexpr int TRSM_WARPS = 8;  // rows (warps) per CTA of the panel solves
 // column j+1 publishes it into the other half of a double-buffered column — one barrier per column.
 __global__ void __launch_bounds__(256) potrf_diag_kernel(double* __restrict__ H, int64_t n, int64_t k, int nb,
                                                          int* __restrict__ info) {
+    pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible after this
     __shared__ double col[2][NB];  // the current pivot column (unscaled), double-buffered
     __shared__ double out[NB][NB + 1];
     __shared__ double piv[NB];
@@ -136,6 +137,7 @@ __device__ __noinline__ void trtri32_warp(const double (*__restrict__ a)[PB], do
 
 __global__ void __launch_bounds__(128) potrf_inv_diag_kernel(double* __restrict__ H, int64_t n, int64_t k, int nb,
                                                              double* __restrict__ Xd, int* __restrict__ info) {
+    pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible after this
     extern __shared__ double pi_smem[];
     double(*a)[PB] = reinterpret_cast<double(*)[PB]>(pi_smem);
     double(*x)[PB] = reinterpret_cast<double(*)[PB]>(pi_smem + 64 * PB);
@@ -212,6 +214,7 @@ __global__ void __launch_bounds__(128) potrf_inv_diag_kernel(double* __restrict_
 // one warp per row, lane c produces columns c and c + 32 (no sequential chain).
 __global__ void __launch_bounds__(32 * TRSM_WARPS) trsm_inv_panel_kernel(double* __restrict__ H, int64_t n, int64_t k,
                                                                          int nb, const double* __restrict__ Xd) {
+    pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible after this
     __shared__ double xs[64][PB];
     __shared__ double rowv[TRSM_WARPS][64];
     const double* X = Xd + (k / 64) * 64 * 64;
@@ -233,6 +236,7 @@ __global__ void __launch_bounds__(32 * TRSM_WARPS) trsm_inv_panel_kernel(double*
 
 // W's diagonal 32-blocks <- the block inverses of the cooperative factorization
 __global__ void place_diag_inv32_kernel(const double* __restrict__ Xd, int64_t n, double* __restrict__ W) {
+    pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible after this
     const int64_t k = (int64_t)blockIdx.x * 32;
     const double* X = Xd + (int64_t)blockIdx.x * 32 * 32;
     for (int e = threadIdx.x; e < 32 * 32; e += blockDim.x) {
@@ -243,6 +247,7 @@ __global__ void place_diag_inv32_kernel(const double* __restrict__ Xd, int64_t n
 
 // W's diagonal 64-blocks <- the block inverses computed during the factorization
 __global__ void place_diag_inv_kernel(const double* __restrict__ Xd, int64_t n, double* __restrict__ W) {
+    pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible after this
     const int64_t k = (int64_t)blockIdx.x * 64;
     const double* X = Xd + (int64_t)blockIdx.x * 64 * 64;
     for (int e = threadIdx.x; e < 64 * 64; e += blockDim.x) {
@@ -256,6 +261,7 @@ __global__ void place_diag_inv_kernel(const double* __restrict__ Xd, int64_t n, 
 // the row; column c is finished by its owner lane and broadcast by shuffle.
 __global__ void __launch_bounds__(32 * TRSM_WARPS) trsm_panel_kernel(double* __restrict__ H, int64_t n, int64_t k,
                                                                      int nb) {
+    pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible after this
     __shared__ double l[NB][NB + 1];
     __shared__ double rdiag[NB];
     for (int e = threadIdx.x; e < NB * NB; e += blockDim.x) {
@@ -288,6 +294,7 @@ __global__ void __launch_bounds__(32 * TRSM_WARPS) trsm_panel_kernel(double* __r
 
 // strict upper triangle <- L^T (H[i + j n] = H[j + i n] for i < j)
 __global__ void mirror_upper_kernel(double* __restrict__ H, int64_t n) {
+    pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible after this
     // 32x32 tiles through shared memory for coalescing on both sides
     __shared__ double tile[32][33];
     const int64_t bi = blockIdx.x, bj = blockIdx.y;
@@ -310,6 +317,7 @@ __global__ void mirror_upper_kernel(double* __restrict__ H, int64_t n) {
 // One CTA per block, one thread per column of the inverse.
 __global__ void __launch_bounds__(64) tri_inv_diag_kernel(const double* __restrict__ L, int64_t n,
                                                           double* __restrict__ W) {
+    pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible after this
     extern __shared__ double tri_smem[];
     double(*l)[NB + 1] = reinterpret_cast<double(*)[NB + 1]>(tri_smem);
     double(*x)[NB + 1] = reinterpret_cast<double(*)[NB + 1]>(tri_smem + NB * (NB + 1));
@@ -358,6 +366,7 @@ __device__ __forceinline__ double dot_strided4(const double* a, int as, const do
 
 __global__ void __launch_bounds__(256) tri_inv64_kernel(const double* __restrict__ L, int64_t n,
                                                         double* __restrict__ W) {
+    pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible after this
     extern __shared__ double ti_smem[];
     double(*l)[TIP] = reinterpret_cast<double(*)[TIP]>(ti_smem);
     double(*x)[TIP] = reinterpret_cast<double(*)[TIP]>(ti_smem + TI * TIP);
@@ -429,6 +438,7 @@ constexpr int TR_ROWS = 64, TR_COLS = 64;  // 16 columns per thread: short, inde
 __global__ void __launch_bounds__(256) trmv_partial_kernel(const double* __restrict__ Wf, int64_t n, int lower,
                                                            const double* __restrict__ x, int nrhs,
                                                            double* __restrict__ part) {
+    pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible after this
     const int64_t r0 = (int64_t)blockIdx.x * TR_ROWS;
     const int64_t c0 = (int64_t)blockIdx.y * TR_COLS;
     const int64_t c1 = imin64(n, c0 + TR_COLS);
@@ -465,6 +475,7 @@ __global__ void __launch_bounds__(256) trmv_partial_kernel(const double* __restr
 
 __global__ void trmv_reduce_kernel(const double* __restrict__ part, int64_t n, int nrhs, int nchunks, int lower,
                                    double* __restrict__ y) {
+    pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible after this
     const int64_t total = (int64_t)nrhs * n;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
         const int64_t q = e / n, row = e % n;
@@ -482,9 +493,9 @@ __global__ void trmv_reduce_kernel(const double* __restrict__ part, int64_t n, i
 
 void trmv(const double* Wf, int64_t n, bool lower, const double* x, int nrhs, double* y, double* part, cudaStream_t st) {
     dim3 grid((unsigned)ceil_div(n, TR_ROWS), (unsigned)ceil_div(n, TR_COLS));
-    LAUNCH(trmv_partial_kernel, grid, 256, 0, st, Wf, n, (int)lower, x, nrhs, part);
+    LAUNCH_PDL(trmv_partial_kernel, grid, 256, 0, st, Wf, n, (int)lower, x, nrhs, part);
     const int64_t total = (int64_t)nrhs * n;
-    LAUNCH(trmv_reduce_kernel, (unsigned)std::min<int64_t>(ceil_div(total, 256), 1024), 256, 0, st, part, n, nrhs,
+    LAUNCH_PDL(trmv_reduce_kernel, (unsigned)std::min<int64_t>(ceil_div(total, 256), 1024), 256, 0, st, part, n, nrhs,
            (int)grid.y, (int)lower, y);
 }
 
@@ -537,6 +548,7 @@ __device__ __forceinline__ void potrf32_regs(double (&r)[CB], int nvalid, int* i
 
 __global__ void __launch_bounds__(CTHREADS) chol_coop_kernel(double* __restrict__ H, int64_t k,
                                                              double* __restrict__ Xd, int* __restrict__ info) {
+    pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible after this
     cg::grid_group grid = cg::this_grid();
     __shared__ double xs[CB][CB + 1];     // panel block inverse (or scratch)
     __shared__ double ta[CB][CB + 1], tb[CB][CB + 1];
@@ -660,10 +672,10 @@ void cholesky_invert(const double* d_L, int64_t n, double* d_W, double* d_tmp, c
     CUDA_CHECK(cudaMemsetAsync(d_W, 0, (size_t)n * n * sizeof(double), st));
     int base = NB;
     if (d_Xd && xd_block == 32) {
-        LAUNCH(place_diag_inv32_kernel, (unsigned)ceil_div(n, 32), 256, 0, st, d_Xd, n, d_W);
+        LAUNCH_PDL(place_diag_inv32_kernel, (unsigned)ceil_div(n, 32), 256, 0, st, d_Xd, n, d_W);
         base = 32;
     } else if (d_Xd) {
-        LAUNCH(place_diag_inv_kernel, (unsigned)ceil_div(n, NB), 256, 0, st, d_Xd, n, d_W);
+        LAUNCH_PDL(place_diag_inv_kernel, (unsigned)ceil_div(n, NB), 256, 0, st, d_Xd, n, d_W);
     } else {
         const size_t smem = (size_t)2 * NB * (NB + 1) * sizeof(double);
         static bool attr = false;
@@ -675,7 +687,7 @@ void cholesky_invert(const double* d_L, int64_t n, double* d_W, double* d_tmp, c
             const char* e = std::getenv("IHS_TRI_INV_OLD");
             return e && e[0] == '1';
         }();
-        if (old_inv) LAUNCH(tri_inv_diag_kernel, (unsigned)ceil_div(n, NB), 64, smem, st, d_L, n, d_W);
+        if (old_inv) LAUNCH_PDL(tri_inv_diag_kernel, (unsigned)ceil_div(n, NB), 64, smem, st, d_L, n, d_W);
         else {
             const size_t ti_smem = (size_t)3 * TI * TIP * sizeof(double);
             static bool ti_attr = false;
@@ -684,12 +696,12 @@ void cholesky_invert(const double* d_L, int64_t n, double* d_W, double* d_tmp, c
                                                 (int)ti_smem));
                 ti_attr = true;
             }
-            LAUNCH(tri_inv64_kernel, (unsigned)ceil_div(n, NB), 256, ti_smem, st, d_L, n, d_W);
+            LAUNCH_PDL(tri_inv64_kernel, (unsigned)ceil_div(n, NB), 256, ti_smem, st, d_L, n, d_W);
         }
     }
     tri_inv_rec(d_L, d_W, n, 0, n, d_tmp, st, base);
     dim3 grid((unsigned)ceil_div(n, 32), (unsigned)ceil_div(n, 32));
-    LAUNCH(mirror_upper_kernel, grid, dim3(32, 8), 0, st, d_W, n);
+    LAUNCH_PDL(mirror_upper_kernel, grid, dim3(32, 8), 0, st, d_W, n);
 }
 
 size_t cholesky_solve_work_doubles(int64_t n) { return (size_t)ceil_div(n, TR_COLS) * 2 * n + 2 * n; }
@@ -739,15 +751,15 @@ void cholesky_factor(double* d_H, int64_t n, double* d_Xd, int* d_info, int num_
     }
     for (int64_t k = 0; k < n; k += NB) {
         const int nb = (int)std::min<int64_t>(NB, n - k);
-        if (d_Xd) LAUNCH(potrf_inv_diag_kernel, 1, 128, pi_smem, st, d_H, n, k, nb, d_Xd, d_info);
-        else LAUNCH(potrf_diag_kernel, 1, 256, 0, st, d_H, n, k, nb, d_info);
+        if (d_Xd) LAUNCH_PDL(potrf_inv_diag_kernel, 1, 128, pi_smem, st, d_H, n, k, nb, d_Xd, d_info);
+        else LAUNCH_PDL(potrf_diag_kernel, 1, 256, 0, st, d_H, n, k, nb, d_info);
         const int64_t rest = n - k - nb;
         if (rest > 0) {
             if (d_Xd)
-                LAUNCH(trsm_inv_panel_kernel, (unsigned)ceil_div(rest, TRSM_WARPS), 32 * TRSM_WARPS, 0, st, d_H, n, k,
+                LAUNCH_PDL(trsm_inv_panel_kernel, (unsigned)ceil_div(rest, TRSM_WARPS), 32 * TRSM_WARPS, 0, st, d_H, n, k,
                        nb, d_Xd);
             else
-                LAUNCH(trsm_panel_kernel, (unsigned)ceil_div(rest, TRSM_WARPS), 32 * TRSM_WARPS, 0, st, d_H, n, k, nb);
+                LAUNCH_PDL(trsm_panel_kernel, (unsigned)ceil_div(rest, TRSM_WARPS), 32 * TRSM_WARPS, 0, st, d_H, n, k, nb);
             // A22 -= L21 L21^T (lower)
             double* L21 = d_H + (k + nb) + k * n;
             double* A22 = d_H + (k + nb) + (k + nb) * n;

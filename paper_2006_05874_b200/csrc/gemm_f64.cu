@@ -29,6 +29,7 @@ __global__ void __launch_bounds__(THREADS)
 dgemm_kernel(int64_t M, int64_t N, int64_t K, double alpha, const double* __restrict__ A, int64_t lda,
              const double* __restrict__ B, int64_t ldb, double beta, double* __restrict__ C, int64_t ldc,
              int lower_only, int64_t k_per_split, double* __restrict__ work) {
+    pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible after this
     const int64_t m0 = (int64_t)blockIdx.x * BM;
     const int64_t n0 = (int64_t)blockIdx.y * BN;
     if (lower_only && n0 > m0 + BM - 1) return;
@@ -151,6 +152,7 @@ __global__ void __launch_bounds__(GTHREADS, 1)
 dgemm_nn_big_kernel(int64_t M, int64_t N, int64_t K, double alpha, const double* __restrict__ A, int64_t lda,
                     const double* __restrict__ B, int64_t ldb, double beta, double* __restrict__ C, int64_t ldc,
                     int64_t k_per_split, double* __restrict__ work) {
+    pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible after this
     extern __shared__ double gsm[];
     const int64_t m0 = (int64_t)blockIdx.x * GBM, n0 = (int64_t)blockIdx.y * GBN;
     const int64_t kbeg = (int64_t)blockIdx.z * k_per_split;
@@ -243,6 +245,7 @@ dgemm_nn_big_kernel(int64_t M, int64_t N, int64_t K, double alpha, const double*
 // C = alpha * sum_z work[z] + beta * C, splits summed in fixed order
 __global__ void splitk_reduce_kernel(int64_t M, int64_t N, int splits, const double* __restrict__ work, double alpha,
                                      double beta, double* __restrict__ C, int64_t ldc, int lower_only) {
+    pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible after this
     const int64_t total = M * N;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
         const int64_t gm = e % M, gn = e / M;
@@ -311,29 +314,29 @@ void dgemm(bool transA, bool transB, int64_t M, int64_t N, int64_t K, double alp
         // no products: run the reduce with zero splits semantics via a 1-split pass of zeros
         const int64_t total = M * N;
         const int blocks = (int)std::min<int64_t>(ceil_div(total, 256), 148 * 8);
-        LAUNCH(splitk_reduce_kernel, blocks, 256, 0, st, M, N, 0, (const double*)nullptr, alpha, beta, C, ldc,
+        LAUNCH_PDL(splitk_reduce_kernel, blocks, 256, 0, st, M, N, 0, (const double*)nullptr, alpha, beta, C, ldc,
                (int)lower_only);
         return;
     }
     if (!transA && !transB && big)
-        LAUNCH(dgemm_nn_big_kernel, grid, GTHREADS, kBigSmem, st, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kps,
+        LAUNCH_PDL(dgemm_nn_big_kernel, grid, GTHREADS, kBigSmem, st, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kps,
                work);
     else if (!transA && !transB)
-        LAUNCH((dgemm_kernel<false, false>), grid, THREADS, 0, st, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc,
+        LAUNCH_PDL((dgemm_kernel<false, false>), grid, THREADS, 0, st, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc,
                (int)lower_only, kps, work);
     else if (transA && !transB)
-        LAUNCH((dgemm_kernel<true, false>), grid, THREADS, 0, st, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc,
+        LAUNCH_PDL((dgemm_kernel<true, false>), grid, THREADS, 0, st, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc,
                (int)lower_only, kps, work);
     else if (!transA && transB)
-        LAUNCH((dgemm_kernel<false, true>), grid, THREADS, 0, st, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc,
+        LAUNCH_PDL((dgemm_kernel<false, true>), grid, THREADS, 0, st, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc,
                (int)lower_only, kps, work);
     else
-        LAUNCH((dgemm_kernel<true, true>), grid, THREADS, 0, st, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc,
+        LAUNCH_PDL((dgemm_kernel<true, true>), grid, THREADS, 0, st, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc,
                (int)lower_only, kps, work);
     if (work) {
         const int64_t total = M * N;
         const int blocks = (int)std::min<int64_t>(ceil_div(total, 256), 148 * 8);
-        LAUNCH(splitk_reduce_kernel, blocks, 256, 0, st, M, N, splits, work, alpha, beta, C, ldc, (int)lower_only);
+        LAUNCH_PDL(splitk_reduce_kernel, blocks, 256, 0, st, M, N, splits, work, alpha, beta, C, ldc, (int)lower_only);
     }
 }
 

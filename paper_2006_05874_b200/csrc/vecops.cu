@@ -12,6 +12,7 @@ namespace {
 __global__ void candidates_kernel(const double* __restrict__ x, const double* __restrict__ xprev,
                                   const double* __restrict__ gt, double mu_p, double beta_p, double mu_gd, int64_t d,
                                   double* __restrict__ xp, double* __restrict__ xg) {
+    pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible after this
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < d; i += (int64_t)gridDim.x * blockDim.x) {
         const double xi = x[i], gi = gt[i];
         if (xp) xp[i] = __dadd_rn(__dsub_rn(xi, __dmul_rn(mu_p, gi)), __dmul_rn(beta_p, __dsub_rn(xi, xprev[i])));
@@ -22,6 +23,7 @@ __global__ void candidates_kernel(const double* __restrict__ x, const double* __
 __global__ void fixed_step_kernel(const double* __restrict__ x, const double* __restrict__ xprev,
                                   const double* __restrict__ step, double mu, double beta, int64_t d,
                                   double* __restrict__ xn) {
+    pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible after this
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < d; i += (int64_t)gridDim.x * blockDim.x) {
         const double xi = x[i];
         xn[i] = __dadd_rn(__dsub_rn(xi, __dmul_rn(mu, step[i])), __dmul_rn(beta, __dsub_rn(xi, xprev[i])));
@@ -31,6 +33,7 @@ __global__ void fixed_step_kernel(const double* __restrict__ x, const double* __
 __global__ void __launch_bounds__(1024) decrement_dots_kernel(const double* __restrict__ g,
                                                               const double* __restrict__ gt, int64_t d, int nrhs,
                                                               double* __restrict__ out) {
+    pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible after this
     __shared__ double s1[1024], s2[1024];
     for (int q = 0; q < nrhs; ++q) {
         double a = 0.0, c = 0.0;
@@ -61,6 +64,7 @@ __global__ void __launch_bounds__(1024) decrement_dots_kernel(const double* __re
 __global__ void gemv_n_kernel(const double* __restrict__ A, int64_t M, int64_t N, int64_t lda,
                               const double* __restrict__ x, int nrhs, int64_t ldx, double* __restrict__ y,
                               int64_t ldy) {
+    pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible after this
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < M; i += (int64_t)gridDim.x * blockDim.x) {
         for (int q = 0; q < nrhs; ++q) {
             double s = 0.0;
@@ -164,6 +168,7 @@ __global__ void __launch_bounds__(256) gemv_tiled_kernel(const double* __restric
 __global__ void woodbury_finish_kernel(const double* __restrict__ SA, int64_t m, int64_t d,
                                        const double* __restrict__ g, const double* __restrict__ w, double nu2,
                                        int nrhs, double* __restrict__ z) {
+    pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible after this
     const int lane = threadIdx.x & 31;
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -179,16 +184,19 @@ __global__ void woodbury_finish_kernel(const double* __restrict__ SA, int64_t m,
 }
 
 __global__ void add_scaled_kernel(double* __restrict__ y, const double* __restrict__ x, double a, int64_t n) {
+    pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible after this
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         y[i] = y[i] + a * x[i];
 }
 
 __global__ void add_diag_kernel(double* __restrict__ H, int64_t n, double v) {
+    pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible after this
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         H[i + i * n] += v;
 }
 
 __global__ void check_finite_kernel(const double* __restrict__ v, int64_t count, int* __restrict__ flag) {
+    pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible after this
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
         if (!isfinite(v[i])) *flag = 1;
 }
@@ -200,21 +208,21 @@ int blocks_for(int64_t n, int threads, int cap = 148 * 8) {
 
 void candidates(const double* x, const double* xprev, const double* gt, double mu_p, double beta_p, double mu_gd,
                 int64_t d, double* xp, double* xg, cudaStream_t st) {
-    LAUNCH(candidates_kernel, blocks_for(d, 256), 256, 0, st, x, xprev, gt, mu_p, beta_p, mu_gd, d, xp, xg);
+    LAUNCH_PDL(candidates_kernel, blocks_for(d, 256), 256, 0, st, x, xprev, gt, mu_p, beta_p, mu_gd, d, xp, xg);
 }
 
 void fixed_step(const double* x, const double* xprev, const double* step, double mu, double beta, int64_t d,
                 double* xn, cudaStream_t st) {
-    LAUNCH(fixed_step_kernel, blocks_for(d, 256), 256, 0, st, x, xprev, step, mu, beta, d, xn);
+    LAUNCH_PDL(fixed_step_kernel, blocks_for(d, 256), 256, 0, st, x, xprev, step, mu, beta, d, xn);
 }
 
 void decrement_dots(const double* g, const double* gt, int64_t d, int nrhs, double* out, cudaStream_t st) {
-    LAUNCH(decrement_dots_kernel, 1, 1024, 0, st, g, gt, d, nrhs, out);
+    LAUNCH_PDL(decrement_dots_kernel, 1, 1024, 0, st, g, gt, d, nrhs, out);
 }
 
 void gemv_n(const double* A, int64_t M, int64_t N, int64_t lda, const double* x, int nrhs, int64_t ldx, double* y,
             int64_t ldy, cudaStream_t st) {
-    LAUNCH(gemv_n_kernel, blocks_for(M, 128), 128, 0, st, A, M, N, lda, x, nrhs, ldx, y, ldy);
+    LAUNCH_PDL(gemv_n_kernel, blocks_for(M, 128), 128, 0, st, A, M, N, lda, x, nrhs, ldx, y, ldy);
 }
 
 // partials (nchunks x 2 x M) followed by the per-row-block arrival counters
@@ -236,6 +244,7 @@ void gemv_tiled_reset(double* work, int64_t M, int64_t N, cudaStream_t st) {
 }
 
 __global__ void tril_copy_kernel(const double* __restrict__ W, int64_t k, double* __restrict__ Wl) {
+    pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible after this
     const int64_t total = k * k;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
         const int64_t i = e % k, j = e / k;
@@ -244,24 +253,24 @@ __global__ void tril_copy_kernel(const double* __restrict__ W, int64_t k, double
 }
 
 void tril_copy(const double* W, int64_t k, double* Wl, cudaStream_t st) {
-    LAUNCH(tril_copy_kernel, blocks_for(k * k, 256), 256, 0, st, W, k, Wl);
+    LAUNCH_PDL(tril_copy_kernel, blocks_for(k * k, 256), 256, 0, st, W, k, Wl);
 }
 
 void woodbury_finish(const double* SA, int64_t m, int64_t d, const double* g, const double* w, double nu2, int nrhs,
                      double* z, cudaStream_t st) {
-    LAUNCH(woodbury_finish_kernel, blocks_for(d * 32, 256), 256, 0, st, SA, m, d, g, w, nu2, nrhs, z);
+    LAUNCH_PDL(woodbury_finish_kernel, blocks_for(d * 32, 256), 256, 0, st, SA, m, d, g, w, nu2, nrhs, z);
 }
 
 void add_scaled(double* y, const double* x, double a, int64_t n, cudaStream_t st) {
-    LAUNCH(add_scaled_kernel, blocks_for(n, 256), 256, 0, st, y, x, a, n);
+    LAUNCH_PDL(add_scaled_kernel, blocks_for(n, 256), 256, 0, st, y, x, a, n);
 }
 
 void add_diag(double* H, int64_t n, double v, cudaStream_t st) {
-    LAUNCH(add_diag_kernel, blocks_for(n, 256), 256, 0, st, H, n, v);
+    LAUNCH_PDL(add_diag_kernel, blocks_for(n, 256), 256, 0, st, H, n, v);
 }
 
 void check_finite(const double* v, int64_t count, int* d_flag, cudaStream_t st) {
-    LAUNCH(check_finite_kernel, blocks_for(count, 256), 256, 0, st, v, count, d_flag);
+    LAUNCH_PDL(check_finite_kernel, blocks_for(count, 256), 256, 0, st, v, count, d_flag);
 }
 
 }  // namespace ihs_b200
