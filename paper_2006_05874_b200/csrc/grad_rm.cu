@@ -49,6 +49,7 @@ template <int NRHS, int RR, int MAXC, int NS>
 __global__ void __launch_bounds__(TT, 1)
 grad_rm_kernel(const double* __restrict__ Arm, int64_t d, int64_t npanels, const double* __restrict__ b,
                const double* __restrict__ X, double* __restrict__ work) {
+    pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible after this
     extern __shared__ __align__(128) double sm[];
     const int64_t stage = (int64_t)RR * d;
     double* panel = sm;
@@ -169,6 +170,7 @@ grad_rm_kernel(const double* __restrict__ Arm, int64_t d, int64_t npanels, const
 // row-major copy: Arm[i * ldo + j] = A[i + j * lda], 32x32 tiles through smem
 __global__ void transpose_kernel(const double* __restrict__ A, int64_t lda, int64_t rows, int64_t d,
                                  double* __restrict__ Arm, int64_t ldo) {
+    pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible after this
     __shared__ double tile[32][33];
     const int64_t i0 = (int64_t)blockIdx.x * 32, j0 = (int64_t)blockIdx.y * 32;
     const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
@@ -424,7 +426,7 @@ void launch_rm(const GradPlan& p, const double* Arm, const double* b, const doub
                                             cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));              \
             attr = true;                                                                                            \
         }                                                                                                           \
-        LAUNCH((grad_rm_kernel<NRHS, RR, MC, NS>), p.grid, TT, smem, st, Arm, p.d, p.lda / RR, b, X, work);         \
+        LAUNCH_PDL((grad_rm_kernel<NRHS, RR, MC, NS>), p.grid, TT, smem, st, Arm, p.d, p.lda / RR, b, X, work);         \
     } while (0)
     if (maxc <= 1) IHS_RM(1);
     else if (maxc <= 2) IHS_RM(2);
@@ -521,7 +523,7 @@ bool grad_rm_geometry(int64_t d, int64_t lda, int* R, int* ns) {
 void transpose_to_rowmajor(const double* A, int64_t lda, int64_t rows, int64_t d, double* Arm, cudaStream_t st,
                            int64_t ldo) {
     dim3 grid((unsigned)ceil_div(rows, 32), (unsigned)ceil_div(d, 32));
-    LAUNCH(transpose_kernel, grid, dim3(32, 8), 0, st, A, lda, rows, d, Arm, ldo > 0 ? ldo : d);
+    LAUNCH_PDL(transpose_kernel, grid, dim3(32, 8), 0, st, A, lda, rows, d, Arm, ldo > 0 ? ldo : d);
 }
 
 void grad_rm_run(const GradPlan& p, const double* Arm, const double* b, const double* X, int nrhs, double* work,

@@ -62,6 +62,7 @@ template <int NRHS, int RR, int MAXC, int NS>
 __global__ void __launch_bounds__(TT, 1)
 grad_tma_kernel(const __grid_constant__ CUtensorMap tmap, int64_t d, int64_t npanels, const double* __restrict__ b,
                 const double* __restrict__ X, double* __restrict__ work) {
+    pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible after this
     extern __shared__ __align__(1024) double sm_raw[];
     // swizzled TMA destinations need 1024-byte aligned stages
     double* sm = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
@@ -251,7 +252,7 @@ void launch_tma(const GradPlan& p, const double* b, const double* X, double* wor
                                             cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));              \
             attr = true;                                                                                            \
         }                                                                                                           \
-        LAUNCH((grad_tma_kernel<NRHS, RR, MC, NS>), p.grid, TT, smem, st, *map, p.d, p.lda / RR, b, X, work);       \
+        LAUNCH_PDL((grad_tma_kernel<NRHS, RR, MC, NS>), p.grid, TT, smem, st, *map, p.d, p.lda / RR, b, X, work);       \
     } while (0)
     if (maxc <= 1) IHS_TMA(1);
     else if (maxc <= 2) IHS_TMA(2);

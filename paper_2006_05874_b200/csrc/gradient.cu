@@ -31,6 +31,7 @@ template <int NRHS>
 __global__ void __launch_bounds__(THREADS, 2)
 grad_partial_kernel(const double* __restrict__ A, int64_t n, int64_t d, int64_t lda, const double* __restrict__ b,
                     const double* __restrict__ X, double* __restrict__ work) {
+    pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible after this
     extern __shared__ double sm[];
     double* xs = sm;                          // NRHS * d
     double* gp = xs + NRHS * d;               // NRHS * d   per-CTA column partials
@@ -149,6 +150,7 @@ template <int NRHS, int RR, int MAXC, int NS>
 __global__ void __launch_bounds__(T2, 1)
 grad_smem_kernel(const double* __restrict__ A, int64_t d, int64_t lda, const double* __restrict__ b,
                  const double* __restrict__ X, double* __restrict__ work) {
+    pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible after this
     extern __shared__ double sm[];
     const int64_t stage = d * RR;
     double* panel = sm;                       // NS stages
@@ -264,7 +266,7 @@ void launch_v2(const GradPlan& p, const double* A, const double* b, const double
                                             cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));              \
             attr = true;                                                                                            \
         }                                                                                                           \
-        LAUNCH((grad_smem_kernel<NRHS, RR, MC, NS>), p.grid, T2, smem, st, A, p.d, p.lda, b, X, work);              \
+        LAUNCH_PDL((grad_smem_kernel<NRHS, RR, MC, NS>), p.grid, T2, smem, st, A, p.d, p.lda, b, X, work);              \
     } while (0)
     if (maxc <= 1) IHS_V2(1);
     else if (maxc <= 2) IHS_V2(2);
@@ -423,11 +425,11 @@ void grad_run(const GradPlan& p, const double* d_A, const double* d_b, double nu
         attr = true;
     }
     if (nrhs == 1)
-        LAUNCH(grad_partial_kernel<1>, p.grid, THREADS, smem, st, d_A, p.n, p.d, p.lda, d_b, d_X, d_work);
+        LAUNCH_PDL(grad_partial_kernel<1>, p.grid, THREADS, smem, st, d_A, p.n, p.d, p.lda, d_b, d_X, d_work);
     else
-        LAUNCH(grad_partial_kernel<2>, p.grid, THREADS, smem, st, d_A, p.n, p.d, p.lda, d_b, d_X, d_work);
+        LAUNCH_PDL(grad_partial_kernel<2>, p.grid, THREADS, smem, st, d_A, p.n, p.d, p.lda, d_b, d_X, d_work);
     const int64_t total = (int64_t)nrhs * p.d;
-    LAUNCH(grad_reduce_kernel, (unsigned)ceil_div(total, 16), 256, 0, st, d_work, p.grid, p.d, nrhs, d_X, nu2, d_G);
+    LAUNCH_PDL(grad_reduce_kernel, (unsigned)ceil_div(total, 16), 256, 0, st, d_work, p.grid, p.d, nrhs, d_X, nu2, d_G);
 }
 
 }  // namespace ihs_b200

@@ -31,6 +31,7 @@ using mt::temper;
 
 // Single-stream raw generator: draws [0, count) of mt19937_64(seed).
 __global__ void __launch_bounds__(mt::THREADS) mt_raw_kernel(uint64_t seed, int64_t count, uint64_t* __restrict__ out) {
+    pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible after this
     __shared__ uint64_t buf[2 * NN];
     mt::seed_array(buf, seed);
     __syncthreads();
@@ -51,6 +52,7 @@ __global__ void __launch_bounds__(mt::THREADS) mt_raw_kernel(uint64_t seed, int6
 // [q*stride, min((q+1)*stride, count)).
 __global__ void __launch_bounds__(mt::THREADS) mt_substream_kernel(const uint64_t* __restrict__ starts, int64_t stride,
                                                                    int64_t count, uint64_t* __restrict__ out) {
+    pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible after this
     __shared__ uint64_t buf[2 * NN];
     const int64_t q = blockIdx.x;
     for (int i = threadIdx.x; i < NN; i += blockDim.x) buf[i] = starts[q * NN + i];
@@ -96,6 +98,7 @@ __device__ __forceinline__ void sign_bits_range(mt::Twister& tw, int64_t beg, in
 
 // Sign bits, single stream: chunks of 32 blocks (9984 draws = 312 words).
 __global__ void __launch_bounds__(mt::THREADS) mt_signbits_kernel(uint64_t seed, int64_t n, uint32_t* __restrict__ bits) {
+    pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible after this
     __shared__ uint64_t buf[2 * NN];
     __shared__ uint32_t acc[NN];
     mt::seed_array(buf, seed);
@@ -121,6 +124,7 @@ __global__ void __launch_bounds__(mt::THREADS) mt_signbits_kernel(uint64_t seed,
 __global__ void __launch_bounds__(mt::THREADS) mt_signbits_sub_kernel(const uint64_t* __restrict__ starts,
                                                                       int64_t stride, int64_t n,
                                                                       uint32_t* __restrict__ bits) {
+    pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible after this
     extern __shared__ uint32_t accw[];
     __shared__ uint64_t buf[2 * NN];
     const int64_t q = blockIdx.x;
@@ -153,6 +157,7 @@ __device__ __forceinline__ bool polar_attempt(const uint64_t* raw, int64_t a, do
 }
 
 __global__ void polar_flags_kernel(const uint64_t* __restrict__ raw, int64_t attempts, int* __restrict__ flags) {
+    pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible after this
     for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < attempts; a += (int64_t)gridDim.x * blockDim.x) {
         double x, y, r2;
         flags[a] = polar_attempt(raw, a, x, y, r2) ? 1 : 0;
@@ -162,6 +167,7 @@ __global__ void polar_flags_kernel(const uint64_t* __restrict__ raw, int64_t att
 // normals [first, first + count) of the stream -> out[0 .. count)
 __global__ void polar_emit_kernel(const uint64_t* __restrict__ raw, int64_t attempts, const int* __restrict__ pos,
                                   int64_t first, int64_t count, double stddev, double* __restrict__ out) {
+    pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible after this
     const int64_t end = first + count;
     for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < attempts; a += (int64_t)gridDim.x * blockDim.x) {
         const int64_t k = 2 * (int64_t)pos[a];
@@ -176,6 +182,7 @@ __global__ void polar_emit_kernel(const uint64_t* __restrict__ raw, int64_t atte
 
 __global__ void last_total_kernel(const int* __restrict__ pos, const int* __restrict__ flags, int64_t attempts,
                                   long long* __restrict__ total) {
+    pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible after this
     *total = (long long)pos[attempts - 1] + flags[attempts - 1];
 }
 
@@ -195,7 +202,7 @@ void mt_seed_host(uint64_t seed, MTState& s) {
 
 void mt_generate_raw(uint64_t seed, int64_t count, uint64_t* d_out, cudaStream_t st) {
     if (count <= 0) return;
-    LAUNCH(mt_raw_kernel, 1, 160, 0, st, seed, count, d_out);
+    LAUNCH_PDL(mt_raw_kernel, 1, 160, 0, st, seed, count, d_out);
 }
 
 size_t rademacher_scratch_bytes(int64_t n) {
@@ -206,14 +213,14 @@ size_t rademacher_scratch_bytes(int64_t n) {
 void mt_rademacher_bits(uint64_t seed, int64_t n, uint32_t* d_bits, void* d_scratch, cudaStream_t st) {
     if (n <= 0) return;
     if (n <= 2 * kSignStride || d_scratch == nullptr) {
-        LAUNCH(mt_signbits_kernel, 1, 160, 0, st, seed, n, d_bits);
+        LAUNCH_PDL(mt_signbits_kernel, 1, 160, 0, st, seed, n, d_bits);
         return;
     }
     const int64_t nsub = ceil_div(n, kSignStride);
     uint64_t* starts = static_cast<uint64_t*>(d_scratch);
     uint64_t* xseq = starts + nsub * NN;
     mt_jump_starts(seed, kSignStride, nsub, starts, xseq, st);
-    LAUNCH(mt_signbits_sub_kernel, (unsigned)nsub, 160, (size_t)(kSignStride / 32) * 4, st, starts,
+    LAUNCH_PDL(mt_signbits_sub_kernel, (unsigned)nsub, 160, (size_t)(kSignStride / 32) * 4, st, starts,
            (int64_t)kSignStride, n, d_bits);
 }
 
@@ -255,19 +262,19 @@ void mt_fill_gaussian(uint64_t seed, int64_t first, int64_t count, double stddev
         // jump-ahead start windows for substreams q*stride (host F2 polynomial
         // arithmetic, cached per stride), expanded on the device
         mt_jump_starts(seed, kJumpStride, nsub, starts, xseq, st);
-        LAUNCH(mt_substream_kernel, (unsigned)nsub, 160, 0, st, starts, (int64_t)kJumpStride, draws, raw);
+        LAUNCH_PDL(mt_substream_kernel, (unsigned)nsub, 160, 0, st, starts, (int64_t)kJumpStride, draws, raw);
     }
     const int threads = 256;
     const int blocks = (int)std::min<int64_t>(ceil_div(attempts, threads), 148 * 16);
-    LAUNCH(polar_flags_kernel, blocks, threads, 0, st, raw, attempts, flags);
+    LAUNCH_PDL(polar_flags_kernel, blocks, threads, 0, st, raw, attempts, flags);
     CUDA_CHECK(cub::DeviceScan::ExclusiveSum(temp, temp_bytes, flags, pos, (int)attempts, st));
     note_launch();
-    LAUNCH(last_total_kernel, 1, 1, 0, st, pos, flags, attempts, total);
+    LAUNCH_PDL(last_total_kernel, 1, 1, 0, st, pos, flags, attempts, total);
     long long h_total = 0;
     CUDA_CHECK(cudaMemcpyAsync(&h_total, total, sizeof(long long), cudaMemcpyDeviceToHost, st));
     CUDA_CHECK(cudaStreamSynchronize(st));
     if (2 * h_total < first + count) fail(IHS_INTERNAL_ERROR, "fill_gaussian: draw estimate too small");
-    LAUNCH(polar_emit_kernel, blocks, threads, 0, st, raw, attempts, pos, first, count, stddev, d_out);
+    LAUNCH_PDL(polar_emit_kernel, blocks, threads, 0, st, raw, attempts, pos, first, count, stddev, d_out);
 }
 
 }  // namespace ihs_b200

@@ -191,6 +191,7 @@ PolyRing& ring() {
 
 // untempered word sequence x_0 .. x_{nx-1} of mt19937_64(seed)
 __global__ void __launch_bounds__(mt::THREADS) mt_wordseq_kernel(uint64_t seed, int nx, uint64_t* __restrict__ X) {
+    pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible after this
     __shared__ uint64_t buf[2 * NN];
     mt::seed_array(buf, seed);
     __syncthreads();
@@ -220,6 +221,7 @@ __global__ void __launch_bounds__(kApplyThreads) mt_jump_apply_kernel(const uint
                                                                       const uint16_t* __restrict__ pos,
                                                                       const int* __restrict__ ptr,
                                                                       uint64_t* __restrict__ starts) {
+    pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible after this
     __shared__ uint64_t xs[kSpan + NN];
     __shared__ unsigned long long red[NN];
     const int q = blockIdx.x, chunk = blockIdx.y;
@@ -330,8 +332,8 @@ void mt_jump_starts(uint64_t seed, int64_t stride, int64_t nsub, uint64_t* d_sta
         }
     }
     CUDA_CHECK(cudaMemsetAsync(d_starts, 0, (size_t)nsub * NN * 8, st));
-    LAUNCH(mt_wordseq_kernel, 1, mt::THREADS, 0, st, seed, NX, d_X);
-    LAUNCH(mt_jump_apply_kernel, dim3((unsigned)nsub, kChunks), kApplyThreads, 0, st, d_X, L.pos, L.ptr, d_starts);
+    LAUNCH_PDL(mt_wordseq_kernel, 1, mt::THREADS, 0, st, seed, NX, d_X);
+    LAUNCH_PDL(mt_jump_apply_kernel, dim3((unsigned)nsub, kChunks), kApplyThreads, 0, st, d_X, L.pos, L.ptr, d_starts);
 }
 
 }  // namespace ihs_b200

@@ -61,6 +61,7 @@ __global__ void __launch_bounds__((1 << L) / 16 > 0 ? (1 << L) / 16 : 1)
 srht_small_kernel(const double* __restrict__ A, int64_t n, int64_t lda, const uint32_t* __restrict__ signbits,
                   const int2* __restrict__ entries, int n_entries, double s1, double s2, double* __restrict__ SA,
                   int64_t m) {
+    pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible after this
     constexpr int N = 1 << L;
     constexpr int THREADS = N / 16 > 0 ? N / 16 : 1;
     constexpr int E = N / THREADS;
@@ -317,6 +318,7 @@ __global__ void __launch_bounds__(32 * kP1TWarps, 1)
 srht_phase1_tma_kernel(const __grid_constant__ ChunkMaps maps, const double* __restrict__ A, int64_t n, int64_t lda,
                        const uint32_t* __restrict__ signbits, double* __restrict__ T, int64_t n_pad, int lcpc,
                        int64_t nfull, int64_t total_chunks, const uint32_t* __restrict__ mask, int logw) {
+    pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible after this
     extern __shared__ unsigned char p1t_raw[];
     double* base = align1024(p1t_raw);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -364,6 +366,7 @@ __global__ void __launch_bounds__(32 * kP1AWarps, 1)
 srht_phase1_kernel(const double* __restrict__ A, int64_t n, int64_t lda, const uint32_t* __restrict__ signbits,
                    double* __restrict__ T, int64_t n_pad, int lcpc, int64_t total_chunks,
                    const uint32_t* __restrict__ mask, int logw) {
+    pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible after this
     extern __shared__ double p1_smem[];  // kP1AWarps x 2 x kP1Buf doubles
     const int64_t cmask = (int64_t{1} << lcpc) - 1;  // chunks per column = 2^lcpc
     const int warp = threadIdx.x >> 5;
@@ -512,6 +515,7 @@ template <int HB, int TH>
 __global__ void __launch_bounds__(TH)
 srht_phase2_kernel(double* __restrict__ T, int64_t n_pad, int lo, const int4* __restrict__ tiles, int emit,
                    const int2* __restrict__ entries, double s1, double s2, double* __restrict__ SA, int64_t m) {
+    pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible after this
     extern __shared__ double xs[];
     constexpr int LOGW = P2Geom<HB, TH>::LOGW;
     const int64_t j = blockIdx.y;
@@ -573,6 +577,7 @@ srht_stream_kernel(const __grid_constant__ ChunkMaps maps, const double* __restr
                    const int2* __restrict__ entries, int lo, double s1, double s2, double* __restrict__ SA, int64_t m,
                    int* __restrict__ ctl, const uint32_t* __restrict__ mask, int logw, int dbg,
                    unsigned long long* __restrict__ prof) {
+    pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible after this
     extern __shared__ unsigned char stream_raw[];
     const long long t_start = clock64();
     double* base = align1024(stream_raw);
@@ -715,6 +720,7 @@ srht_stream_kernel(const __grid_constant__ ChunkMaps maps, const double* __restr
 template <int LOGP>
 __global__ void srht_combine_kernel(const double* __restrict__ U, int64_t m, int64_t d,
                                     const uint8_t* __restrict__ hi, double s1, double s2, double* __restrict__ SA) {
+    pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible after this
     constexpr int P = 1 << LOGP;
     const int64_t md = m * d;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < md; e += (int64_t)gridDim.x * blockDim.x) {
@@ -754,7 +760,7 @@ void launch_small(const SrhtPlan& p, const double* A, const uint32_t* signbits, 
     constexpr int N = 1 << L;
     constexpr int THREADS = N / 16 > 0 ? N / 16 : 1;
     const size_t smem = (size_t)padded(N) * sizeof(double) + 64;
-    LAUNCH(srht_small_kernel<L>, (unsigned)p.d, THREADS, smem, st, A, p.n, p.lda, signbits, entries, (int)p.m,
+    LAUNCH_PDL(srht_small_kernel<L>, (unsigned)p.d, THREADS, smem, st, A, p.n, p.lda, signbits, entries, (int)p.m,
            p.scale1, p.scale2, SA, p.m);
 }
 using SmallFn = void (*)(const SrhtPlan&, const double*, const uint32_t*, const int2*, double*, cudaStream_t);
@@ -776,7 +782,7 @@ void launch_pass(const SrhtPlan& p, double* T, int lo, const int4* tiles, int n_
     const unsigned gx = emit ? (unsigned)n_tiles : (unsigned)tiles_per_col;
     if (gx == 0) return;
     dim3 grid(gx, (unsigned)p.d);
-    LAUNCH((srht_phase2_kernel<HB, TH>), grid, TH, smem, st, T, p.n_pad, lo, tiles, emit ? 1 : 0, entries, p.scale1,
+    LAUNCH_PDL((srht_phase2_kernel<HB, TH>), grid, TH, smem, st, T, p.n_pad, lo, tiles, emit ? 1 : 0, entries, p.scale1,
            p.scale2, SA, p.m);
 }
 
@@ -864,7 +870,7 @@ void launch_stream(const SrhtPlan& p, const ChunkMaps& maps, int64_t nfull, cons
     static unsigned long long* prof = nullptr;
     if (prof_on && !prof) CUDA_CHECK(cudaMalloc(&prof, 16 * sizeof(unsigned long long)));
     if (prof_on) CUDA_CHECK(cudaMemsetAsync(prof, 0, 16 * sizeof(unsigned long long), st));
-    LAUNCH(srht_stream_kernel<HB>, (unsigned)grid, kStreamThreads, kStreamSmem, st, maps, A, p.n, p.lda, nfull,
+    LAUNCH_PDL(srht_stream_kernel<HB>, (unsigned)grid, kStreamThreads, kStreamSmem, st, maps, A, p.n, p.lda, nfull,
            signbits, T, p.n_pad, p.d, p.logn - kChunkL, G, nslot, ng, tiles, n_tiles, entries, p.pass_lo[0], p.scale1,
            p.scale2, SA, p.m, ctl, mask, logw, stream_dbg(), prof_on ? prof : nullptr);
     if (prof_on) {
@@ -983,11 +989,11 @@ void srht_combine(const double* d_U, int P, int64_t m, int64_t d, const uint8_t*
     const int64_t md = m * d;
     const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(md, 256), 148 * 16));
     switch (P) {
-        case 1: LAUNCH(srht_combine_kernel<0>, blocks, 256, 0, st, d_U, m, d, d_hi, s1, s2, d_SA); break;
-        case 2: LAUNCH(srht_combine_kernel<1>, blocks, 256, 0, st, d_U, m, d, d_hi, s1, s2, d_SA); break;
-        case 4: LAUNCH(srht_combine_kernel<2>, blocks, 256, 0, st, d_U, m, d, d_hi, s1, s2, d_SA); break;
-        case 8: LAUNCH(srht_combine_kernel<3>, blocks, 256, 0, st, d_U, m, d, d_hi, s1, s2, d_SA); break;
-        case 16: LAUNCH(srht_combine_kernel<4>, blocks, 256, 0, st, d_U, m, d, d_hi, s1, s2, d_SA); break;
+        case 1: LAUNCH_PDL(srht_combine_kernel<0>, blocks, 256, 0, st, d_U, m, d, d_hi, s1, s2, d_SA); break;
+        case 2: LAUNCH_PDL(srht_combine_kernel<1>, blocks, 256, 0, st, d_U, m, d, d_hi, s1, s2, d_SA); break;
+        case 4: LAUNCH_PDL(srht_combine_kernel<2>, blocks, 256, 0, st, d_U, m, d, d_hi, s1, s2, d_SA); break;
+        case 8: LAUNCH_PDL(srht_combine_kernel<3>, blocks, 256, 0, st, d_U, m, d, d_hi, s1, s2, d_SA); break;
+        case 16: LAUNCH_PDL(srht_combine_kernel<4>, blocks, 256, 0, st, d_U, m, d, d_hi, s1, s2, d_SA); break;
         default: fail(IHS_INVALID_INPUT, "srht shard: number of shards must be 1, 2, 4, 8 or 16");
     }
 }
@@ -1096,7 +1102,7 @@ void srht_run_device(const SrhtPlan& p, const double* d_A, const uint32_t* d_sig
             attr = true;
         }
         const int64_t blocks = std::min<int64_t>(ceil_div(total, kP1TWarps), (int64_t)num_sms);
-        LAUNCH(srht_phase1_tma_kernel, (unsigned)blocks, 32 * kP1TWarps, kP1TSmem, st, maps, d_A, p.n, p.lda,
+        LAUNCH_PDL(srht_phase1_tma_kernel, (unsigned)blocks, 32 * kP1TWarps, kP1TSmem, st, maps, d_A, p.n, p.lda,
                d_signbits, d_T, p.n_pad, p.logn - kChunkL, nfull, total, masked ? d_mask : nullptr, logw);
     } else {
         const int64_t blocks = std::min<int64_t>(ceil_div(total, kP1AWarps), (int64_t)num_sms);
@@ -1106,7 +1112,7 @@ void srht_run_device(const SrhtPlan& p, const double* d_A, const uint32_t* d_sig
             CUDA_CHECK(cudaFuncSetAttribute(srht_phase1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             attr = true;
         }
-        LAUNCH(srht_phase1_kernel, (unsigned)blocks, 32 * kP1AWarps, smem, st, d_A, p.n, p.lda, d_signbits, d_T,
+        LAUNCH_PDL(srht_phase1_kernel, (unsigned)blocks, 32 * kP1AWarps, smem, st, d_A, p.n, p.lda, d_signbits, d_T,
                p.n_pad, p.logn - kChunkL, total, masked ? d_mask : nullptr, logw);
     }
     for (int i = 0; i < p.npass; ++i) {
