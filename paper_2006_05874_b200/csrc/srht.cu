@@ -448,7 +448,67 @@ __device__ __forceinline__ void p2_tile(double* __restrict__ xs, double* __restr
 #pragma unroll
         for (int c = 0; c < E; ++c)
             if (!(c & (1 << s))) bfly(v[c], v[c | (1 << s)]);
-    if constexpr (RB2 > 0) {
+    if constexpr (HB > 10) {
+        // three rounds (pass bits [0,5), [5,10), [10,HB)), in the reference's bit order; thread group g
+        // (NG = 2^(HB-5) of them) covers the bits a round does not hold in registers
+        constexpr int NG = 1 << (HB - RB1);
+        constexpr int RB3 = HB - 10, G3 = 1 << RB3, GRPS3 = E / G3;
+        static_assert(E == 32 && NG * E == (1 << HB), "three-round tile geometry");
+#pragma unroll
+        for (int c = 0; c < E; ++c) xs[pad32(((g << RB1) | c) * W + w)] = v[c];
+        bar();
+        // round 2: registers = bits [5,10); g = bits [0,5) | bits [10,HB) << 5
+#pragma unroll
+        for (int c2 = 0; c2 < E; ++c2) {
+            const int b = (g & 31) | (c2 << 5) | ((g >> 5) << 10);
+            v[c2] = xs[pad32(b * W + w)];
+        }
+#pragma unroll
+        for (int s = 0; s < 5; ++s)
+#pragma unroll
+            for (int c = 0; c < E; ++c)
+                if (!(c & (1 << s))) bfly(v[c], v[c | (1 << s)]);
+        bar();  // every round-2 read is done before the buffer is rewritten
+#pragma unroll
+        for (int c2 = 0; c2 < E; ++c2) {
+            const int b = (g & 31) | (c2 << 5) | ((g >> 5) << 10);
+            xs[pad32(b * W + w)] = v[c2];
+        }
+        bar();
+        // round 3: registers (grp, c3) = bits [10,HB) = c3, bits [0,10) = g + grp * NG
+#pragma unroll
+        for (int grp = 0; grp < GRPS3; ++grp)
+#pragma unroll
+            for (int c3 = 0; c3 < G3; ++c3) {
+                const int b = (g + grp * NG) | (c3 << 10);
+                v[grp * G3 + c3] = xs[pad32(b * W + w)];
+            }
+#pragma unroll
+        for (int s = 0; s < RB3; ++s)
+#pragma unroll
+            for (int grp = 0; grp < GRPS3; ++grp)
+#pragma unroll
+                for (int c3 = 0; c3 < G3; ++c3)
+                    if (!(c3 & (1 << s))) bfly(v[grp * G3 + c3], v[grp * G3 + (c3 | (1 << s))]);
+        if (!emit) {
+#pragma unroll
+            for (int grp = 0; grp < GRPS3; ++grp)
+#pragma unroll
+                for (int c3 = 0; c3 < G3; ++c3) {
+                    const int b = (g + grp * NG) | (c3 << 10);
+                    Tcol[((int64_t)b << lo) + w] = v[grp * G3 + c3];
+                }
+            return;
+        }
+        bar();
+#pragma unroll
+        for (int grp = 0; grp < GRPS3; ++grp)
+#pragma unroll
+            for (int c3 = 0; c3 < G3; ++c3) {
+                const int b = (g + grp * NG) | (c3 << 10);
+                xs[pad32(b * W + w)] = v[grp * G3 + c3];
+            }
+    } else if constexpr (RB2 > 0) {
         // exchange: element (b, w) at xs[pad32(b*W + w)]
 #pragma unroll
         for (int c = 0; c < E; ++c) xs[pad32(((g << RB1) | c) * W + w)] = v[c];
@@ -903,7 +963,7 @@ const PassFn kPass[11] = {nullptr,
                           launch_pass<8, 256>,
                           launch_pass<9, 256>,
                           launch_pass<10, 256>};
-const PassFn kPass512[11] = {nullptr,
+const PassFn kPass512[13] = {nullptr,
                              launch_pass<1, 512>,
                              launch_pass<2, 512>,
                              launch_pass<3, 512>,
@@ -913,7 +973,9 @@ const PassFn kPass512[11] = {nullptr,
                              launch_pass<7, 512>,
                              launch_pass<8, 512>,
                              launch_pass<9, 512>,
-                             launch_pass<10, 512>};
+                             launch_pass<10, 512>,
+                             launch_pass<11, 512>,   // three-round tiles: 2^21 / 2^22 rows in one pass
+                             launch_pass<12, 512>};
 const PassFn kPass128[11] = {nullptr,
                              launch_pass<1, 128>,
                              launch_pass<2, 128>,
@@ -956,6 +1018,18 @@ SrhtPlan srht_plan(int64_t n, int64_t d, int64_t lda, int64_t m) {
     } else {
         p.L = kChunkL;
         p.H = logn - kChunkL;
+        if (p.H > 10 && p.H <= 12) {
+            // one pass of 11-12 high bits with 512-thread three-round tiles (W = 8 / 4 low indices):
+            // saves the T -> T round trip of a second pass (n_pad = 2^21, 2^22)
+            p.npass = 1;
+            p.pass_lo[0] = kChunkL;
+            p.pass_hb[0] = p.H;
+            p.scale1 = 1.0 / std::sqrt(static_cast<double>(np));
+            p.scale2 = std::sqrt(static_cast<double>(np) / static_cast<double>(m));
+            p.p2t = 512;
+            p.stream = 0;
+            return p;
+        }
         // split H into passes of <= 10 bits, as even as possible
         const int np_ = (p.H + 9) / 10;
         int lo = kChunkL;
@@ -1044,7 +1118,8 @@ bool srht_plan_stream(SrhtPlan& p, int num_sms) {
         return e && e[0] == '1';
     }();
     int G = 0, nslot = 0;
-    if (!enabled || (p.n >> kChunkL) == 0 || !srht_stream_geometry(p, num_sms, &G, &nslot)) return false;
+    if (!enabled || (p.n >> kChunkL) == 0 || p.pass_hb[0] > 10 || !srht_stream_geometry(p, num_sms, &G, &nslot))
+        return false;
     p.p2t = kEmitThreads;
     p.stream = 1;
     return true;

@@ -78,7 +78,9 @@ def test_fwht_rejects_non_pow2(gpu):
 
 @pytest.mark.parametrize("n,d,m,seed", [
     (12, 4, 8, 77), (1000, 2, 16, 0), (8192, 16, 100, 5), (8192, 8, 8192, 1), (5000, 7, 333, 2),
-    (20000, 5, 1000, 3), (1 << 15, 4, 4096, 4), (100000, 3, 20000, 9), ((1 << 20) - 17, 2, 5000, 6)])
+    (20000, 5, 1000, 3), (1 << 15, 4, 4096, 4), (100000, 3, 20000, 9), ((1 << 20) - 17, 2, 5000, 6),
+    # n_pad = 2^21 / 2^22: one 11- / 12-bit pass of three-round 512-thread tiles
+    ((1 << 20) + 5, 2, 3000, 8), ((1 << 21) + 1, 2, 40000, 10), ((1 << 22) - 3, 2, 777, 12)])
 def test_srht_sketch_bit_exact(gpu, O, n, d, m, seed):
     A = rand_mat(n + d, n, d)
     c_gpu = gpu.CostCounters()
@@ -91,7 +93,7 @@ def test_srht_sketch_bit_exact(gpu, O, n, d, m, seed):
 
 @pytest.mark.parametrize("n,d,m,seed,shards", [
     (1000, 3, 64, 11, 2), (4096, 5, 4096, 2, 2), (3500, 4, 333, 5, 4), (100000, 3, 5000, 7, 8),
-    ((1 << 20) - 5, 2, 20000, 1, 8), (1 << 16, 6, 1024, 3, 16)])
+    ((1 << 20) - 5, 2, 20000, 1, 8), (1 << 16, 6, 1024, 3, 16), ((1 << 22) - 9, 2, 3000, 4, 2)])
 def test_sharded_srht_kernels_bit_exact(gpu, O, n, d, m, seed, shards):
     """The row-sharded SRHT kernels (shard transform + all-gather layout + combine),
     run as P virtual shards on one device, equal the unsharded sketch bit for bit."""
