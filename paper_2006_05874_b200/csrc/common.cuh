@@ -88,11 +88,17 @@ struct SrhtPlan {
     double scale1, scale2;   // 1/sqrt(n_pad), sqrt(n_pad/m) (host-computed, :47 and :95)
     int p2t;                 // threads per phase-2 tile (128; 256 for the 64 KiB-tile variant)
     int stream;              // 1: streamed single-launch kernel (srht_plan_stream)
+    int compact;             // 1: compact T (only the sampled low indices; srht_plan_compact)
 };
 SrhtPlan srht_plan(int64_t n, int64_t d, int64_t lda, int64_t m);
 // switch the plan to the streamed single-launch kernel when it applies (sets
 // p2t before the entries are built); false = two-kernel path
 bool srht_plan_stream(SrhtPlan& p, int num_sms);
+// switch a two-kernel plan with 10 high bits (n_pad = 2^20) to compact T when the sample has few distinct
+// low indices (U <= 256): phase 1 stores, per chunk, only the low indices some sampled row has
+// (T[j][h][u]) and the emitting pass runs one warp per (u, column). Set before the entries are built (they then carry U tiles followed by the 1024-entry
+// low-index -> u map).
+bool srht_plan_compact(SrhtPlan& p, const int64_t* rows);
 size_t srht_scratch_bytes(const SrhtPlan& p);  // T buffer (phase-1 output) when H > 0
 // Host: bucket the sampled rows (draw order k -> row rows[k]) by phase-2
 // tile. entries = (row, k) pairs grouped by tile; tiles = (rlo0, begin, end).

@@ -378,6 +378,7 @@ void device_sketch(ihs_gpu_problem* P, int kind, int64_t m, uint64_t seed, doubl
         const int shards = world > 1 ? world : std::max(1, emulate_shards);
         if (shards == 1) {
             srht_plan_stream(plan, P->num_sms);  // decides the emitting-tile shape before the entries are built
+            srht_plan_compact(plan, P->h_rows.data());
             srht_build_entries(plan, P->h_rows.data(), P->h_entries, P->h_tiles);
             P->mask_valid = srht_build_mask(plan, P->h_tiles, P->h_mask);
             g_host_rng_ns +=
@@ -389,12 +390,14 @@ void device_sketch(ihs_gpu_problem* P, int kind, int64_t m, uint64_t seed, doubl
                 std::max<int64_t>(1, std::min<int64_t>(d, kSrhtScratchCap / (plan.n_pad * (int64_t)sizeof(double))));
             SrhtPlan bp = plan;
             bp.d = std::min<int64_t>(d, cols_per_batch);
+            // compact plans carry the low-index map (128 int4) after their tiles
+            const int n_tiles = (int)P->h_tiles.size() - (plan.compact ? (int)(1024 * sizeof(short) / sizeof(int4)) : 0);
             unsigned long long* ctl = srht_prepare_scratch(P, bp);
             if (P->timer) P->timer->mark(PH_SKETCH_KERNEL);
             for (int64_t j0 = 0; j0 < d; j0 += cols_per_batch) {
                 bp.d = std::min<int64_t>(cols_per_batch, d - j0);
                 srht_run_device(bp, P->A.d() + j0 * P->lda, P->signbits.as<uint32_t>(), P->entries.as<int2>(),
-                                P->tiles.as<int4>(), (int)P->h_tiles.size(), P->T.d(), d_SA + j0 * m, st, ctl,
+                                P->tiles.as<int4>(), n_tiles, P->T.d(), d_SA + j0 * m, st, ctl,
                                 P->num_sms, P->mask_valid ? P->srht_mask.as<uint32_t>() : nullptr);
             }
             if (P->timer) P->timer->mark(PH_SKETCH);

@@ -25,6 +25,8 @@
 #include "common.cuh"
 #include "tma.cuh"
 
+#include <cstring>
+
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -176,9 +178,30 @@ __device__ __forceinline__ double flip_sign(double a, uint32_t flip_bit31) {
     return __hiloint2double(__double2hiint(a) ^ (int)flip_bit31, __double2loint(a));
 }
 
+// Store a transformed chunk (lane holds element 32c + lane in v[c]): masked, the kept low-index groups
+// to dst[element]; compact (lmap), element l to dst[lmap[l] * cstride] when some sampled row has low
+// index l (lmap[l] = its rank u among the distinct low indices, else -1).
+__device__ __forceinline__ void p1_store(const double (&v)[32], double* __restrict__ dst, uint32_t store_bits,
+                                         const short* __restrict__ lmap, int64_t cstride) {
+    const int lane = threadIdx.x & 31;
+    if (lmap) {
+#pragma unroll
+        for (int c = 0; c < 32; ++c) {
+            const int u = __ldg(lmap + ((c << 5) | lane));
+            if (u >= 0) dst[(int64_t)u * cstride] = v[c];
+        }
+        return;
+    }
+    double* out = dst + lane;
+#pragma unroll
+    for (int c = 0; c < 32; ++c)
+        if ((store_bits >> c) & 1u) out[c << 5] = v[c];
+}
+
 // Transform the chunk staged in buf and store the kept elements to dst.
 __device__ __forceinline__ void p1_transform_store(double* buf, const uint32_t* __restrict__ signbits, int64_t n,
-                                                   int64_t r0, double* __restrict__ dst, uint32_t store_bits) {
+                                                   int64_t r0, double* __restrict__ dst, uint32_t store_bits,
+                                                   const short* __restrict__ lmap = nullptr, int64_t cstride = 0) {
     const int lane = threadIdx.x & 31;
     const int64_t rl = r0 + (lane << 5);
     // flip bit c = row rl + c gets -1 (sign bit 0); padded rows stay +0.0
@@ -206,10 +229,7 @@ __device__ __forceinline__ void p1_transform_store(double* buf, const uint32_t* 
 #pragma unroll
         for (int c = 0; c < 32; ++c)
             if (!(c & (1 << s))) bfly(v[c], v[c | (1 << s)]);
-    double* out = dst + lane;
-#pragma unroll
-    for (int c = 0; c < 32; ++c)
-        if ((store_bits >> c) & 1u) out[c << 5] = v[c];
+    p1_store(v, dst, store_bits, lmap, cstride);
     __syncwarp();  // the buffer is refilled by the next issue
 }
 
@@ -255,7 +275,9 @@ __device__ __forceinline__ void p1_tma_issue(double* buf, const ChunkMaps* maps,
 }
 
 __device__ __forceinline__ void p1_transform_store_swz(double* buf, const uint32_t* __restrict__ signbits, int64_t n,
-                                                       int64_t r0, double* __restrict__ dst, uint32_t store_bits) {
+                                                       int64_t r0, double* __restrict__ dst, uint32_t store_bits,
+                                                       const short* __restrict__ lmap = nullptr,
+                                                       int64_t cstride = 0) {
     const int lane = threadIdx.x & 31;
     const int64_t rl = r0 + (lane << 5);
     uint32_t flip = 0u;
@@ -299,10 +321,7 @@ __device__ __forceinline__ void p1_transform_store_swz(double* buf, const uint32
 #pragma unroll
         for (int c = 0; c < 32; ++c)
             if (!(c & (1 << s))) bfly(v[c], v[c | (1 << s)]);
-    double* out = dst + lane;
-#pragma unroll
-    for (int c = 0; c < 32; ++c)
-        if ((store_bits >> c) & 1u) out[c << 5] = v[c];
+    p1_store(v, dst, store_bits, lmap, cstride);
     __syncwarp();  // the buffer is refilled by the next issue
 }
 
@@ -317,7 +336,8 @@ constexpr size_t kP1TSmem = (size_t)kP1TWarps * 2 * kChunkDoubles * sizeof(doubl
 __global__ void __launch_bounds__(32 * kP1TWarps, 1)
 srht_phase1_tma_kernel(const __grid_constant__ ChunkMaps maps, const double* __restrict__ A, int64_t n, int64_t lda,
                        const uint32_t* __restrict__ signbits, double* __restrict__ T, int64_t n_pad, int lcpc,
-                       int64_t nfull, int64_t total_chunks, const uint32_t* __restrict__ mask, int logw) {
+                       int64_t nfull, int64_t total_chunks, const uint32_t* __restrict__ mask, int logw,
+                       const short* __restrict__ lmap, int64_t U) {
     pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible after this
     extern __shared__ unsigned char p1t_raw[];
     double* base = align1024(p1t_raw);
@@ -352,7 +372,11 @@ srht_phase1_tma_kernel(const __grid_constant__ ChunkMaps maps, const double* __r
         } else {
             p1_sync_load(buf, A + j * lda, n, r0);
         }
-        p1_transform_store_swz(buf, signbits, n, r0, T + j * n_pad + r0, store_bits);
+        if (lmap)  // compact T[j][q][u]: this chunk's U kept values are one contiguous run
+            p1_transform_store_swz(buf, signbits, n, r0, T + (j * (cmask + 1) + q) * ((U + 7) & ~int64_t{7}), 0u,
+                                   lmap, 1);
+        else
+            p1_transform_store_swz(buf, signbits, n, r0, T + j * n_pad + r0, store_bits);
         slot ^= 1;
     }
 }
@@ -365,7 +389,7 @@ constexpr int kP1AWarps = 12;
 __global__ void __launch_bounds__(32 * kP1AWarps, 1)
 srht_phase1_kernel(const double* __restrict__ A, int64_t n, int64_t lda, const uint32_t* __restrict__ signbits,
                    double* __restrict__ T, int64_t n_pad, int lcpc, int64_t total_chunks,
-                   const uint32_t* __restrict__ mask, int logw) {
+                   const uint32_t* __restrict__ mask, int logw, const short* __restrict__ lmap, int64_t U) {
     pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible after this
     extern __shared__ double p1_smem[];  // kP1AWarps x 2 x kP1Buf doubles
     const int64_t cmask = (int64_t{1} << lcpc) - 1;  // chunks per column = 2^lcpc
@@ -388,7 +412,11 @@ srht_phase1_kernel(const double* __restrict__ A, int64_t n, int64_t lda, const u
         __syncwarp();
         const int64_t j = chunk >> lcpc;
         const int64_t r0 = (chunk & cmask) << kChunkL;
-        p1_transform_store(ring + slot * kP1Buf, signbits, n, r0, T + j * n_pad + r0, store_bits);
+        if (lmap)
+            p1_transform_store(ring + slot * kP1Buf, signbits, n, r0,
+                               T + (j * (cmask + 1) + (chunk & cmask)) * ((U + 7) & ~int64_t{7}), 0u, lmap, 1);
+        else
+            p1_transform_store(ring + slot * kP1Buf, signbits, n, r0, T + j * n_pad + r0, store_bits);
         slot ^= 1;
     }
     cp_async_wait0();
@@ -591,6 +619,63 @@ srht_phase2_kernel(double* __restrict__ T, int64_t n_pad, int lo, const int4* __
         base = ((tid % low_tiles) << LOGW) | ((tid / low_tiles) << (lo + HB));
     }
     p2_tile<HB, false, CtaBar, TH>(xs, T + j * n_pad + base, lo, emit != 0, tile, entries, j, s1, s2, SA, m);
+}
+
+// Compact emitting pass (n_pad = 2^20, compact T[j][h][u] with u padded to 8, h = row bits 10..19): a CTA takes 8
+// consecutive low-index ranks u of column j, stages their 1024 x 8 values in shared memory with
+// coalesced reads, and warp w transforms rank u0 + w: the ten high butterflies in the reference's order —
+// bits 0-4 of h across lanes (shuffles; the upper lane forms s - t from its partner's s, the lower s + t),
+// bits 5-9 in registers — then emits the sampled rows with that low index, scaled twice.
+constexpr int kCmpU = 8, kCmpLd = kCmpU + 1;  // ranks per CTA, padded shared row (conflict-free columns)
+__global__ void __launch_bounds__(256) srht_phase2_compact_kernel(const double* __restrict__ Tc, int64_t U,
+                                                                  const int4* __restrict__ ranges,
+                                                                  const int2* __restrict__ entries, double s1,
+                                                                  double s2, double* __restrict__ SA, int64_t m) {
+    pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible after this
+    extern __shared__ double ct[];  // [1024][kCmpLd]
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t u0 = (int64_t)blockIdx.x * kCmpU, j = blockIdx.y;
+    const int nu = (int)(U - u0 < kCmpU ? U - u0 : kCmpU);
+    const int64_t Up = (U + 7) & ~int64_t{7};  // row stride: 64-byte aligned runs of 8 ranks
+    const double* src = Tc + j * 1024 * Up + u0;
+    {
+        // 32 independent loads per thread (8 ranks x 32 h per instruction round), like a phase-2 tile
+        const int uu = threadIdx.x % kCmpU, h0 = threadIdx.x / kCmpU;
+        double t[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) t[i] = uu < nu ? __ldcs(src + (int64_t)(h0 + 32 * i) * Up + uu) : 0.0;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) ct[(h0 + 32 * i) * kCmpLd + uu] = t[i];
+    }
+    __syncthreads();
+    if (warp >= nu) return;
+    double v[32];
+#pragma unroll
+    for (int c = 0; c < 32; ++c) v[c] = ct[((c << 5) | lane) * kCmpLd + warp];  // h = 32c + lane
+#pragma unroll
+    for (int s = 0; s < 5; ++s) {
+        const bool upper = (lane >> s) & 1;
+#pragma unroll
+        for (int c = 0; c < 32; ++c) {
+            const double o = __shfl_xor_sync(0xffffffffu, v[c], 1 << s);
+            v[c] = upper ? __dsub_rn(o, v[c]) : __dadd_rn(v[c], o);
+        }
+    }
+#pragma unroll
+    for (int s = 0; s < 5; ++s)
+#pragma unroll
+        for (int c = 0; c < 32; ++c)
+            if (!(c & (1 << s))) bfly(v[c], v[c | (1 << s)]);
+    const int4 rg = ranges[u0 + warp];
+    for (int q = rg.y; q < rg.z; ++q) {
+        const int2 e = entries[q];
+        const int h = e.x >> 10;
+        double sel = 0.0;
+#pragma unroll
+        for (int c = 0; c < 32; ++c) sel = c == (h >> 5) ? v[c] : sel;
+        const double val = __shfl_sync(0xffffffffu, sel, h & 31);
+        if (lane == 0) SA[(int64_t)e.y + j * m] = __dmul_rn(__dmul_rn(val, s1), s2);
+    }
 }
 
 // ------------------------------------------------------------ streamed (one pass of high bits)
@@ -1028,6 +1113,7 @@ SrhtPlan srht_plan(int64_t n, int64_t d, int64_t lda, int64_t m) {
             p.scale2 = std::sqrt(static_cast<double>(np) / static_cast<double>(m));
             p.p2t = 512;
             p.stream = 0;
+            p.compact = 0;
             return p;
         }
         // split H into passes of <= 10 bits, as even as possible
@@ -1046,6 +1132,7 @@ SrhtPlan srht_plan(int64_t n, int64_t d, int64_t lda, int64_t m) {
     p.scale2 = std::sqrt(static_cast<double>(np) / static_cast<double>(m));
     p.p2t = p2_threads_default();
     p.stream = 0;
+    p.compact = 0;
     return p;
 }
 
@@ -1074,9 +1161,57 @@ void srht_combine(const double* d_U, int P, int64_t m, int64_t d, const uint8_t*
 
 size_t srht_scratch_bytes(const SrhtPlan& p) { return p.H > 0 ? (size_t)p.n_pad * (size_t)p.d * sizeof(double) : 0; }
 
+bool srht_plan_compact(SrhtPlan& p, const int64_t* rows) {
+    // IHS_SRHT_NO_COMPACT=1 disables it; IHS_SRHT_COMPACT_MAX overrides the distinct-low-index limit
+    static const bool disabled = [] {
+        const char* e = std::getenv("IHS_SRHT_NO_COMPACT");
+        return e && e[0] == '1';
+    }();
+    static const int umax = [] {
+        const char* e = std::getenv("IHS_SRHT_COMPACT_MAX");
+        return e ? std::atoi(e) : 256;
+    }();
+    if (disabled || p.H != 10 || p.npass != 1 || p.stream) return false;
+    // measured (profiles/r01_srht_compact.txt): compact wins while its emitting pass stays small, i.e. up
+    // to ~256 distinct low indices; beyond that the tiled pass over the masked T is faster
+    std::vector<uint8_t> seen(1024, 0);
+    int U = 0;
+    for (int64_t k = 0; k < p.m && U <= umax; ++k) {
+        uint8_t& f = seen[(size_t)(rows[k] & 1023)];
+        if (!f) f = 1, ++U;
+    }
+    if (U > umax) return false;
+    p.compact = 1;
+    return true;
+}
+
 void srht_build_entries(const SrhtPlan& p, const int64_t* rows, std::vector<int2>& entries, std::vector<int4>& tiles) {
     entries.clear();
     tiles.clear();
+    if (p.compact) {
+        // U tiles (l, begin, end) over the distinct low indices in increasing order, then the low-index ->
+        // rank map as 1024 shorts packed into 128 trailing int4
+        std::vector<int> cnt(1025, 0);
+        for (int64_t k = 0; k < p.m; ++k) {
+            if (rows[k] < 0 || rows[k] >= p.n_pad) fail(IHS_INTERNAL_ERROR, "srht: sampled row outside the padded range");
+            cnt[(size_t)(rows[k] & 1023) + 1]++;
+        }
+        std::vector<short> lmap(1024, -1);
+        int U = 0;
+        for (int l = 0; l < 1024; ++l)
+            if (cnt[(size_t)l + 1] > 0) lmap[(size_t)l] = (short)U++;
+        for (int l = 0; l < 1024; ++l) cnt[(size_t)l + 1] += cnt[(size_t)l];
+        entries.resize((size_t)p.m);
+        std::vector<int> fill(cnt.begin(), cnt.end() - 1);
+        for (int64_t k = 0; k < p.m; ++k)
+            entries[(size_t)fill[(size_t)(rows[k] & 1023)]++] = make_int2((int)rows[k], (int)k);
+        for (int l = 0; l < 1024; ++l)
+            if (lmap[(size_t)l] >= 0) tiles.push_back(make_int4(l, cnt[(size_t)l], cnt[(size_t)l + 1], 0));
+        const size_t base = tiles.size();
+        tiles.resize(base + 1024 * sizeof(short) / sizeof(int4));
+        std::memcpy(tiles.data() + base, lmap.data(), 1024 * sizeof(short));
+        return;
+    }
     if (p.H == 0) {
         entries.resize((size_t)p.m);
         for (int64_t k = 0; k < p.m; ++k) entries[(size_t)k] = make_int2((int)rows[k], (int)k);
@@ -1166,8 +1301,11 @@ void srht_run_device(const SrhtPlan& p, const double* d_A, const uint32_t* d_sig
     }
     const int64_t chunks_per_col = p.n_pad >> kChunkL;
     const int64_t total = chunks_per_col * p.d;
+    // compact T: n_tiles distinct low indices, their rank map after the tiles
+    const short* lmap = p.compact ? reinterpret_cast<const short*>(d_tiles + n_tiles) : nullptr;
+    const int64_t U = p.compact ? n_tiles : 0;
     // single pass: phase 1 writes only the groups the emitting pass reads
-    const bool masked = p.npass == 1 && d_mask != nullptr;
+    const bool masked = p.npass == 1 && d_mask != nullptr && !p.compact;
     const int logw = masked ? pass_logw(p) : 0;
     if (nfull > 0 && srht_chunk_maps(d_A, p.lda, nfull, p.d, &maps)) {
         static bool attr = false;
@@ -1178,7 +1316,7 @@ void srht_run_device(const SrhtPlan& p, const double* d_A, const uint32_t* d_sig
         }
         const int64_t blocks = std::min<int64_t>(ceil_div(total, kP1TWarps), (int64_t)num_sms);
         LAUNCH_PDL(srht_phase1_tma_kernel, (unsigned)blocks, 32 * kP1TWarps, kP1TSmem, st, maps, d_A, p.n, p.lda,
-               d_signbits, d_T, p.n_pad, p.logn - kChunkL, nfull, total, masked ? d_mask : nullptr, logw);
+               d_signbits, d_T, p.n_pad, p.logn - kChunkL, nfull, total, masked ? d_mask : nullptr, logw, lmap, U);
     } else {
         const int64_t blocks = std::min<int64_t>(ceil_div(total, kP1AWarps), (int64_t)num_sms);
         const size_t smem = (size_t)kP1AWarps * 2 * kP1Buf * sizeof(double);
@@ -1188,7 +1326,20 @@ void srht_run_device(const SrhtPlan& p, const double* d_A, const uint32_t* d_sig
             attr = true;
         }
         LAUNCH_PDL(srht_phase1_kernel, (unsigned)blocks, 32 * kP1AWarps, smem, st, d_A, p.n, p.lda, d_signbits, d_T,
-               p.n_pad, p.logn - kChunkL, total, masked ? d_mask : nullptr, logw);
+               p.n_pad, p.logn - kChunkL, total, masked ? d_mask : nullptr, logw, lmap, U);
+    }
+    if (p.compact) {
+        constexpr size_t smem = (size_t)1024 * kCmpLd * sizeof(double);
+        static bool attr = false;
+        if (!attr) {
+            CUDA_CHECK(cudaFuncSetAttribute(srht_phase2_compact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)smem));
+            attr = true;
+        }
+        if (U > 0)
+            LAUNCH_PDL(srht_phase2_compact_kernel, dim3((unsigned)ceil_div(U, kCmpU), (unsigned)p.d), 256, smem, st,
+                       (const double*)d_T, U, d_tiles, d_entries, p.scale1, p.scale2, d_SA, p.m);
+        return;
     }
     for (int i = 0; i < p.npass; ++i) {
         const bool last = i == p.npass - 1;

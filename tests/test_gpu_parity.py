@@ -79,6 +79,8 @@ def test_fwht_rejects_non_pow2(gpu):
 @pytest.mark.parametrize("n,d,m,seed", [
     (12, 4, 8, 77), (1000, 2, 16, 0), (8192, 16, 100, 5), (8192, 8, 8192, 1), (5000, 7, 333, 2),
     (20000, 5, 1000, 3), (1 << 15, 4, 4096, 4), (100000, 3, 20000, 9), ((1 << 20) - 17, 2, 5000, 6),
+    # n_pad = 2^20: compact T (one warp per distinct low index) from 1 to ~1000 distinct low indices
+    ((1 << 19) + 3, 3, 1, 13), ((1 << 20) - 1, 2, 3, 14), (700000, 3, 100, 15), ((1 << 20), 2, 1024, 16),
     # n_pad = 2^21 / 2^22: one 11- / 12-bit pass of three-round 512-thread tiles
     ((1 << 20) + 5, 2, 3000, 8), ((1 << 21) + 1, 2, 40000, 10), ((1 << 22) - 3, 2, 777, 12)])
 def test_srht_sketch_bit_exact(gpu, O, n, d, m, seed):
@@ -298,7 +300,8 @@ def test_solve_underdetermined_reference_cases(gpu, O):
                            gpu.SolverConfig())
 
 
-@pytest.mark.parametrize("n,d,kind,decay,nu", [(8192, 1024, "SRHT", 0.997, 0.5), (3000, 2050, "Gaussian", 0.99, 5.0)])
+@pytest.mark.parametrize("n,d,kind,decay,nu", [(8192, 1024, "SRHT", 0.997, 0.5), (3000, 2050, "Gaussian", 0.99, 5.0),
+                                               (600000, 8, "SRHT", 0.9, 0.5)])
 def test_adaptive_solve_wide_rows_matches_oracle(gpu, O, n, d, kind, decay, nu):
     # d > 512: the register-row gradient with 2 / 8 column groups per row, candidates formed in-kernel
     A, b, _ = O.synth(n, d, decay=decay, noise_std=0.05, data_seed=4)
@@ -393,3 +396,24 @@ def test_srht_column_batches_bit_exact(gpu):
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300, env=env,
                        cwd=str(__import__("pathlib").Path(__file__).resolve().parents[1]))
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
+
+def test_srht_compact_modes_bit_exact(gpu):
+    """Compact T (n_pad = 2^20, few distinct low indices) is forced for every sample size, and also combined
+    with column batches (8 MiB cap = one column per batch): the sketches stay bit-exact."""
+    import os
+    import subprocess
+    import sys
+    code = ("import numpy as np\n"
+            "from paper_2006_05874_b200 import ihs\n"
+            "from oracle import oracle as O\n"
+            "rng = np.random.default_rng(8)\n"
+            "A = np.asfortranarray(rng.standard_normal(((1 << 20) - 9, 3)))\n"
+            "for m in (2, 300, 2500):\n"
+            "    assert np.array_equal(ihs.srht_sketch(A, m, 5 + m), O.srht_sketch(A, m, 5 + m)), m\n"
+            "print('ok')\n")
+    root = str(__import__("pathlib").Path(__file__).resolve().parents[1])
+    for extra in ({}, {"IHS_SRHT_SCRATCH_CAP_MB": "8"}):
+        env = dict(os.environ, IHS_SRHT_COMPACT_MAX="1024", **extra)
+        r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300, env=env, cwd=root)
+        assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
