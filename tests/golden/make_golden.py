@@ -45,6 +45,24 @@ def main():
                                                 dtype=np.int64)
         out[f"solve_{name}_counters"] = np.array([rep.counters.sketch, rep.counters.factor, rep.counters.solve,
                                                   rep.counters.matvec], dtype=np.uint64)
+    # the CG / PCG comparators (baselines.hpp) and the exact minimizer on the same data
+    for kind, name in [(0, "gauss"), (1, "srht")]:
+        x, res, rep = O.pcg_solve(A, b, 0.05, kind, 4, 0.5, 1e-10, 100)
+        out[f"pcg_{name}_x"] = x
+        out[f"pcg_{name}_res"] = res
+        out[f"pcg_{name}_summary"] = np.array([rep.iterations, rep.m, rep.converged, rep.setup_flops], dtype=np.int64)
+    x, res, rep = O.cg_solve(A, b, 0.05, 1e-8, 200)
+    out["cg_x"], out["cg_res"] = x, res
+    out["cg_summary"] = np.array([rep.iterations, rep.converged], dtype=np.int64)
+    out["direct_x"] = O.direct_solve(A, b, 0.05)
+    # the dual solver (dual.hpp) on an underdetermined instance (40 x 300)
+    Au, bu, _ = O.synth(300, 40, decay=0.95, noise_std=0.01, data_seed=8)
+    Au = np.asfortranarray(Au.T)
+    bu = bu[:40].copy()
+    out["Au"], out["bu"] = Au, bu
+    x, z, rep, log, _ = O.solve_underdetermined(Au, bu, 0.3, O.default_config(seed=5))
+    out["dual_x"], out["dual_z"] = x, z
+    out["dual_summary"] = np.array([rep.iterations, rep.rejections, rep.final_m, rep.converged], dtype=np.int64)
     np.savez_compressed(HERE / "golden.npz", **out)
     print("wrote", HERE / "golden.npz", len(out), "arrays")
 

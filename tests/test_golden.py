@@ -66,3 +66,37 @@ def test_gpu_solves_match_golden(gpu, kind, name):
     num = np.linalg.norm(np.concatenate([A @ (rep.x - x_ref), 0.05 * (rep.x - x_ref)]))
     den = np.linalg.norm(np.concatenate([A @ x_ref, 0.05 * x_ref]))
     assert num <= 1e-10 * den
+
+
+def test_oracle_reproduces_golden_baselines_and_dual(O):
+    A, b = G["A"], G["b"]
+    for kind, name in [(0, "gauss"), (1, "srht")]:
+        x, res, rep = O.pcg_solve(A, b, 0.05, kind, 4, 0.5, 1e-10, 100)
+        assert np.array_equal(x, G[f"pcg_{name}_x"]) and np.array_equal(res, G[f"pcg_{name}_res"])
+    x, res, rep = O.cg_solve(A, b, 0.05, 1e-8, 200)
+    assert np.array_equal(x, G["cg_x"]) and np.array_equal(res, G["cg_res"])
+    assert np.array_equal(O.direct_solve(A, b, 0.05), G["direct_x"])
+    x, z, rep, _, _ = O.solve_underdetermined(G["Au"], G["bu"], 0.3, O.default_config(seed=5))
+    assert np.array_equal(x, G["dual_x"]) and np.array_equal(z, G["dual_z"])
+
+
+def _rel(x, ref):
+    return np.linalg.norm(x - ref) / (1 + np.linalg.norm(ref))
+
+
+@pytest.mark.gpu
+def test_gpu_baselines_and_dual_match_golden(gpu):
+    A, b = G["A"], G["b"]
+    p = gpu.ProblemInstance(A, b, 0.05)
+    for kind, name in [(0, "gauss"), (1, "srht")]:
+        r = gpu.pcg_solve(p, gpu.SketchKind(kind), 4, 0.5, 1e-10, 100)
+        it, m, conv, setup = (int(v) for v in G[f"pcg_{name}_summary"])
+        assert (r.m, int(r.converged), r.setup_flops) == (m, conv, setup) and abs(r.iterations - it) <= 1
+        assert _rel(r.x, G[f"pcg_{name}_x"]) <= 1e-9
+    r = gpu.cg_solve(p, 1e-8, 200)
+    assert r.converged and abs(r.iterations - int(G["cg_summary"][0])) <= 1 and _rel(r.x, G["cg_x"]) <= 1e-7
+    assert _rel(gpu.direct_solve(p), G["direct_x"]) <= 1e-11
+    q = gpu.ProblemInstance(G["Au"], G["bu"], 0.3, orientation=gpu.Orientation.Underdetermined)
+    rep = gpu.solve_underdetermined(q, gpu.SolverConfig(seed=5))
+    assert [rep.iterations, rep.rejections, rep.final_m, int(rep.converged)] == list(G["dual_summary"])
+    assert _rel(rep.x, G["dual_x"]) <= 1e-9 and _rel(rep.dual_final, G["dual_z"]) <= 1e-9
