@@ -231,6 +231,11 @@ int64_t ihs_gpu_problem_rows(const ihs_gpu_problem* p);
 int64_t ihs_gpu_problem_cols(const ihs_gpu_problem* p);
 /* re-upload A/b in place (same shape), e.g. for an end-to-end timed step */
 ihs_status ihs_gpu_problem_upload(ihs_gpu_problem* p, const double* A, int64_t lda, const double* b);
+/* Asynchronous re-upload: enqueues the copies of A / b (and the device row-major copy) on the problem's
+ * side stream and returns; the next call on the problem orders its first A-reading kernel after them, so
+ * A-independent work (Gaussian sketch RNG, SRHT signs and row sample) overlaps the transfer. The host
+ * buffers (pinned for a true overlap) must stay valid until the next call on the problem returns. */
+ihs_status ihs_gpu_problem_upload_async(ihs_gpu_problem* p, const double* A, int64_t lda, const double* b);
 /* Per-phase CUDA-event timing of adaptive solves on this problem (ihs_phase_times; default on).
  * The events cost host time on the solve's critical path, so timed benchmark runs switch them off. */
 ihs_status ihs_gpu_problem_set_phase_timing(ihs_gpu_problem* p, int32_t enabled);

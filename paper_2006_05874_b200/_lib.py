@@ -78,6 +78,7 @@ def lib():
         "ihs_gpu_sketch_sharded_emulated": (C.c_int, [vp, i32, i64, u64, i32, d]),
         "ihs_pcg_sketch_size": (C.c_int, [i64, i64, i32, C.c_double, P(i64), P(i32)]),
         "ihs_gpu_problem_set_nu": (C.c_int, [vp, C.c_double]),
+        "ihs_gpu_problem_upload_async": (C.c_int, [vp, d, i64, d]),
         "ihs_gpu_direct_solve": (C.c_int, [vp, d]),
         "ihs_gpu_cg_solve": (C.c_int, [vp, C.c_double, i64, d, P(abi.CgReportC)]),
         "ihs_gpu_pcg_solve_with": (C.c_int, [vp, d, i64, i64, C.c_double, i64, d, P(abi.CgReportC)]),
@@ -103,4 +104,5 @@ EXPORTED_SYMBOLS = (
     "ihs_synth_generate", "ihs_gpu_shard_rows", "ihs_gpu_nccl_unique_id", "ihs_gpu_nccl_comm_create",
     "ihs_gpu_nccl_comm_destroy", "ihs_gpu_sketch_sharded_emulated", "ihs_pcg_sketch_size", "ihs_gpu_cg_solve",
     "ihs_gpu_pcg_solve_with", "ihs_gpu_pcg_solve", "ihs_gpu_problem_set_nu", "ihs_gpu_direct_solve",
+    "ihs_gpu_problem_upload_async",
 )

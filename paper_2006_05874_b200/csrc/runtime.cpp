@@ -297,6 +297,11 @@ struct ihs_gpu_problem {
     // to back, so each may launch programmatically while its predecessor drains
     cudaStream_t st2 = nullptr;
     StreamOwner owner2;
+    // asynchronous re-upload (ihs_gpu_problem_upload_async): A, b and the row-major copy are written on st2;
+    // the first kernel that reads them waits for a_ready (ensure_A), so A-independent work — the Gaussian
+    // sketch's RNG, the SRHT's signs and row sample — overlaps the host-to-device copy
+    cudaEvent_t a_ready = nullptr;
+    bool a_pending = false;
     // underdetermined instances (dual.hpp): the dual problem in A^T, built on first use, and on the dual
     // problem itself the observation vector subtracted from every gradient (non-owning, n doubles)
     std::unique_ptr<ihs_gpu_problem> dual;
@@ -311,6 +316,7 @@ struct ihs_gpu_problem {
             if (e) cudaEventDestroy(e);
         for (auto e : set_ready)
             if (e) cudaEventDestroy(e);
+        if (a_ready) cudaEventDestroy(a_ready);
     }
     std::unique_ptr<PhaseTimer> timer;
 };
@@ -357,6 +363,7 @@ void upload_entries(ihs_gpu_problem* P) {
 // exchange it over NCCL; `emulate_shards` > 1 runs the same sharded SRHT
 // decomposition on one device (shards back to back), which the tests use to
 // prove the decomposition bit-exact.
+void ensure_A(ihs_gpu_problem* P);
 void device_sketch(ihs_gpu_problem* P, int kind, int64_t m, uint64_t seed, double* d_SA, ihs_counters* c,
                    int emulate_shards = 1) {
     const int64_t n = P->n, d = P->d;
@@ -388,6 +395,7 @@ void device_sketch(ihs_gpu_problem* P, int kind, int64_t m, uint64_t seed, doubl
             // the transform runs over column batches that share one smaller scratch (and the row sample)
             const int64_t cols_per_batch =
                 std::max<int64_t>(1, std::min<int64_t>(d, kSrhtScratchCap / (plan.n_pad * (int64_t)sizeof(double))));
+            ensure_A(P);  // the signs and the row sample above did not need A
             SrhtPlan bp = plan;
             bp.d = std::min<int64_t>(d, cols_per_batch);
             // compact plans carry the low-index map (128 int4) after their tiles
@@ -419,6 +427,7 @@ void device_sketch(ihs_gpu_problem* P, int kind, int64_t m, uint64_t seed, doubl
             upload_entries(P);
             P->shard_hi.ensure((size_t)m + 16);
             CUDA_CHECK(cudaMemcpyAsync(P->shard_hi.p, hi.data(), (size_t)m, cudaMemcpyHostToDevice, st));
+            ensure_A(P);
             P->shard_U.ensure((size_t)shards * m * d * sizeof(double));
             unsigned long long* ctl = srht_prepare_scratch(P, sp);
             double* U = P->shard_U.d();
@@ -458,6 +467,7 @@ void device_sketch(ihs_gpu_problem* P, int kind, int64_t m, uint64_t seed, doubl
         // SA = S * A on the DMMA path (sketch.hpp:68)
         const int splitk = dgemm_pick_splitk(m, d, n, P->num_sms);
         if (splitk > 1) P->gemm_work.ensure((size_t)splitk * m * d * sizeof(double));
+        ensure_A(P);  // S was generated without A
         if (P->timer) P->timer->mark(PH_SKETCH_KERNEL);
         dgemm(false, false, m, d, n, 1.0, P->S.d(), m, P->A.d(), P->lda, 0.0, d_SA, m, false, splitk,
               splitk > 1 ? P->gemm_work.d() : nullptr, st);
@@ -587,13 +597,21 @@ void system_solve_dev(const ihs_gpu_system* S, const double* g, double* z, int n
 }
 
 // Device copy of A with 32-row-aligned columns (zero padding rows) and b.
-void upload_Ab(ihs_gpu_problem* P, const double* A, int64_t lda_host, const double* b) {
+void upload_Ab(ihs_gpu_problem* P, const double* A, int64_t lda_host, const double* b, cudaStream_t st = nullptr) {
+    if (!st) st = P->st;
     if (A)
         CUDA_CHECK(cudaMemcpy2DAsync(P->A.p, (size_t)P->lda * sizeof(double), A, (size_t)lda_host * sizeof(double),
-                                     (size_t)P->n * sizeof(double), (size_t)P->d, cudaMemcpyHostToDevice, P->st));
-    if (b) CUDA_CHECK(cudaMemcpyAsync(P->b.p, b, (size_t)P->n * sizeof(double), cudaMemcpyHostToDevice, P->st));
-    if (A && P->Arm.p) transpose_to_rowmajor(P->A.d(), P->lda, P->lda, P->d, P->Arm.d(), P->st);
+                                     (size_t)P->n * sizeof(double), (size_t)P->d, cudaMemcpyHostToDevice, st));
+    if (b) CUDA_CHECK(cudaMemcpyAsync(P->b.p, b, (size_t)P->n * sizeof(double), cudaMemcpyHostToDevice, st));
+    if (A && P->Arm.p) transpose_to_rowmajor(P->A.d(), P->lda, P->lda, P->d, P->Arm.d(), st);
 }
+// order the problem's stream after a pending asynchronous upload of A / b
+void ensure_A(ihs_gpu_problem* P) {
+    if (!P->a_pending) return;
+    CUDA_CHECK(cudaStreamWaitEvent(P->st, P->a_ready, 0));
+    P->a_pending = false;
+}
+
 void alloc_and_upload(ihs_gpu_problem* P, const double* A, int64_t lda_host, const double* b) {
     P->lda = ceil_div(P->n, 32) * 32;
     P->A.ensure((size_t)P->lda * P->d * sizeof(double));
@@ -608,6 +626,7 @@ void alloc_and_upload(ihs_gpu_problem* P, const double* A, int64_t lda_host, con
 // nu^2 x term is added once.
 void problem_grad(ihs_gpu_problem* P, const double* X, int nrhs, double* G, const CandSpec* cs = nullptr,
                   const double* bvec = nullptr) {
+    ensure_A(P);
     const double nu2 = P->nu * P->nu;
     const double* b = bvec ? bvec : P->b.d();
     if (cs) X = cs->out;
@@ -734,6 +753,7 @@ void cg_run(ihs_gpu_problem* P, const ihs_gpu_system* S, double tol, int64_t max
 // gradient pass: each step shrinks the normal-equations error by ~cond(H) eps, so the result matches
 // the QR solve to working accuracy on the conditioning the suite uses. x: device, d doubles.
 void direct_solve_dev(ihs_gpu_problem* Q, double* x, int refinements = 3) {
+    ensure_A(Q);
     const int64_t d = Q->d;
     cudaStream_t st = Q->st;
     ihs_gpu_system S;
@@ -821,6 +841,7 @@ void finish_setup(ihs_gpu_problem* Q) {
     for (auto& e : Q->set_ready) CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     CUDA_CHECK(cudaStreamCreateWithFlags(&Q->st2, cudaStreamNonBlocking));
     Q->owner2.s = Q->st2;
+    CUDA_CHECK(cudaEventCreateWithFlags(&Q->a_ready, cudaEventDisableTiming));
     Q->timer = std::make_unique<PhaseTimer>(Q->st);
     {
         // IHS_PHASE_TIMER=0: no per-phase events (A/B of the timers' own cost)
@@ -832,6 +853,7 @@ void finish_setup(ihs_gpu_problem* Q) {
 // The dual of an underdetermined instance (dual.hpp:13-33): an overdetermined ridge problem in
 // M = A^T (d x n), observation vector 0 and gradient M^T(M z) + nu^2 z - b, built on the device.
 ihs_gpu_problem* dual_problem(ihs_gpu_problem* P) {
+    ensure_A(P);
     if (P->dual) return P->dual.get();
     auto D = std::make_unique<ihs_gpu_problem>();
     D->device = P->device;
@@ -1084,12 +1106,31 @@ ihs_status ihs_gpu_problem_upload(ihs_gpu_problem* P, const double* A, int64_t l
         if (!P) fail(IHS_INVALID_INPUT, "null problem");
         DeviceGuard g(P->device);
         if (A && lda < P->n) fail(IHS_INVALID_INPUT, "lda < n");
+        ensure_A(P);
         upload_Ab(P, A, lda, b);
         if (A && P->dual) {  // the dual problem holds a transposed copy of A: rebuild it on next use
             CUDA_CHECK(cudaStreamSynchronize(P->st));
             P->dual.reset();
         }
         CUDA_CHECK(cudaStreamSynchronize(P->st));
+    });
+}
+
+ihs_status ihs_gpu_problem_upload_async(ihs_gpu_problem* P, const double* A, int64_t lda, const double* b) {
+    return guarded([&] {
+        if (!P) fail(IHS_INVALID_INPUT, "null problem");
+        DeviceGuard g(P->device);
+        if (A && lda < P->n) fail(IHS_INVALID_INPUT, "lda < n");
+        // the copy must not overtake work still reading the previous A (or a previous pending copy)
+        CUDA_CHECK(cudaEventRecord(P->a_ready, P->st));
+        CUDA_CHECK(cudaStreamWaitEvent(P->st2, P->a_ready, 0));
+        upload_Ab(P, A, lda, b, P->st2);
+        CUDA_CHECK(cudaEventRecord(P->a_ready, P->st2));
+        P->a_pending = true;
+        if (A && P->dual) {  // rebuilt from the new A on next use (after ensure_A)
+            CUDA_CHECK(cudaStreamSynchronize(P->st));
+            P->dual.reset();
+        }
     });
 }
 
@@ -1297,6 +1338,7 @@ ihs_status ihs_gpu_prediction_error(ihs_gpu_problem* P, const double* x, const d
         if (!P || !x || !x_star || !out) fail(IHS_INVALID_INPUT, "prediction_error: dimension mismatch");
         DeviceGuard dg(P->device);
         StreamScope scope(P->st);
+        ensure_A(P);
         const int64_t n = P->n, d = P->d;
         DevBuf v, r, work, dots;
         v.ensure((size_t)2 * d * sizeof(double));

@@ -349,6 +349,19 @@ class ProblemInstance:
         bf = _vec(b, self.rows()) if b is not None else None
         _check(lib().ihs_gpu_problem_upload(self._h, abi.dptr(Af), self.rows(), abi.dptr(bf)))
 
+    def upload_async(self, A=None, b=None):
+        """Re-upload A and/or b without waiting: the next solve's A-independent work (sketch RNG) overlaps the
+        copy. A and b must be contiguous float64 (column-major A; pinned for a true overlap) and stay alive
+        and unchanged until the next call on this instance returns."""
+        Af = _fortran(A) if A is not None else None
+        bf = _vec(b, self.rows()) if b is not None else None
+        def copied(orig, used):  # a conversion copy would die before the transfer reads it
+            return orig is not None and np.asarray(orig).__array_interface__["data"][0] != used.ctypes.data
+        if copied(A, Af) or copied(b, bf):
+            raise InvalidInput("upload_async: A must be Fortran-ordered float64 and b contiguous float64")
+        self._pending_upload = (Af, bf)  # keep the host buffers alive until the next call
+        _check(lib().ihs_gpu_problem_upload_async(self._h, abi.dptr(Af), self.rows(), abi.dptr(bf)))
+
 
 def gradient(p: ProblemInstance, x, counters: Optional[CostCounters] = None) -> np.ndarray:
     x = np.asarray(x, dtype=np.float64).reshape(-1)

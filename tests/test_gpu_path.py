@@ -179,3 +179,28 @@ def test_path_entries_match_oracle_path(gpu, O, P, sid, sketch):
         else:
             assert e.final_m == m and abs(e.iterations - it) <= 2
         assert np.linalg.norm(e.x - xo) <= 1e-8 * (1 + np.linalg.norm(xo))
+
+
+def test_upload_async_matches_sync(gpu, O):
+    """ihs_gpu_problem_upload_async: the next solve / gradient / sketch / CG orders its first A-reading kernel
+    after the side-stream copy; results equal those after a synchronous upload."""
+    A, b, _ = O.synth(20000, 64, decay=0.97, noise_std=0.05)
+    A2 = np.asfortranarray(A * 1.5)
+    b2 = np.ascontiguousarray(b * 0.5)
+    ref = gpu.ProblemInstance(A2, b2, 0.1)
+    for kind in (0, 1):
+        p = gpu.ProblemInstance(A, b, 0.1)
+        p.upload_async(A2, b2)
+        cfg = gpu.SolverConfig(sketch_kind=gpu.SketchKind(kind), seed=2)
+        r1 = gpu.adaptive_solve(p, cfg)
+        r0 = gpu.adaptive_solve(ref, cfg)
+        assert np.array_equal(r1.x, r0.x) and r1.iterations == r0.iterations
+    p = gpu.ProblemInstance(A, b, 0.1)
+    x = RNG(4).standard_normal(64)
+    p.upload_async(A2, b2)
+    assert np.array_equal(gpu.gradient(p, x), gpu.gradient(ref, x))
+    p.upload_async(A, b)
+    assert np.array_equal(gpu.pcg_solve(p, gpu.SketchKind.SRHT, 1, 0.5, 1e-10, 50).x,
+                          gpu.pcg_solve(gpu.ProblemInstance(A, b, 0.1), gpu.SketchKind.SRHT, 1, 0.5, 1e-10, 50).x)
+    with pytest.raises(gpu.InvalidInput):
+        p.upload_async(np.ascontiguousarray(A), b)  # C-ordered: would need a copy that dies before the transfer
