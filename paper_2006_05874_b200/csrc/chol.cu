@@ -25,54 +25,94 @@ namespace {
 constexpr int NB = 64;
 constexpr int TRSM_WARPS = 8;  // rows (warps) per CTA of the panel solves
 
-// Unblocked LLT of the nb x nb diagonal block at (k,k): right-looking elimination on the unscaled
-// columns, a_ik -= a_ij (a_kj / a_jj), with the factor l_ij = a_ij / sqrt(a_jj) formed after the loop
-// from the kept pivots. 256 threads = 64 rows x 4 column interleaves; thread (i, g) keeps its entries
-// a_i,jj (jj = g mod 4) in registers for the whole factorization, so a column step is: read the
-// pivot column (broadcast shared reads), rcp + 16 predicated FMAs on registers, and the owner of
-// column j+1 publishes it into the other half of a double-buffered column — one barrier per column.
+// LLT of the nb x nb diagonal block at (k,k), in shared memory, blocked by 16 columns: warp 0 factors
+// each 16 x 16 diagonal sub-block in registers (lane = row; the pivot and the column broadcast by
+// shuffles, reciprocal square roots instead of sqrt + division, no CTA barrier per column), one thread
+// per row solves the panel below against it, and all 256 threads apply the rank-16 trailing update.
+// The serial part is 16 short column steps per sub-block instead of a barrier-separated step per column
+// of the whole block. A non-positive or non-finite pivot sets *info = column + 1 (a harmless pivot is
+// substituted so the kernel completes).
+constexpr int PD_B = 16;
 __global__ void __launch_bounds__(256) potrf_diag_kernel(double* __restrict__ H, int64_t n, int64_t k, int nb,
                                                          int* __restrict__ info) {
     pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible after this
-    __shared__ double col[2][NB];  // the current pivot column (unscaled), double-buffered
-    __shared__ double out[NB][NB + 1];
-    __shared__ double piv[NB];
-    const int i = threadIdx.x % NB, g = threadIdx.x / NB;  // row, column interleave (4)
-    double r[NB / 4];
-#pragma unroll
-    for (int t = 0; t < NB / 4; ++t) {
-        const int jj = g + 4 * t;
-        r[t] = (i < nb && jj < nb && i >= jj) ? H[(k + i) + (k + jj) * n] : 0.0;
+    __shared__ double a[NB][NB + 1];
+    __shared__ double rdiag[PD_B];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int e = tid; e < NB * NB; e += 256) {
+        const int i = e % NB, jj = e / NB;
+        a[i][jj] = (i < nb && jj < nb && i >= jj) ? H[(k + i) + (k + jj) * n] : 0.0;
     }
-    if (g == 0) col[0][i] = r[0];  // column 0 is owned by interleave 0
     __syncthreads();
-    for (int j = 0; j < nb; ++j) {
-        const double* cj = col[j & 1];
-        double s = cj[j];
-        const bool ok = (s > 0.0) && isfinite(s);
-        if (!ok) s = 1.0;  // a failed pivot is flagged; keep going harmlessly
-        if (threadIdx.x == 0) {
-            piv[j] = s;
-            if (!ok) atomicCAS(info, 0, (int)(k + j + 1));
-        }
-        if (g == (j & 3) && i >= j) out[i][j] = cj[i];  // final (unscaled) column j
-        const bool act = i > j && i < nb;
-        const double f = act ? cj[i] * __drcp_rn(s) : 0.0;
-        // owner of column j+1 first (it feeds the next step), then the rest of this thread's columns
-        const int jn = j + 1;
+    for (int kb = 0; kb < nb; kb += PD_B) {
+        const int bs = nb - kb < PD_B ? nb - kb : PD_B;
+        if (warp == 0) {
+            // 1. the diagonal sub-block: lane i < bs holds row kb + i
+            double r[PD_B];
 #pragma unroll
-        for (int t = 0; t < NB / 4; ++t) {
-            const int jj = g + 4 * t;
-            if (act && jj > j && jj <= i) r[t] = fma(-f, cj[jj], r[t]);
-            if (jj == jn) col[jn & 1][i] = r[t];
+            for (int q = 0; q < PD_B; ++q) r[q] = (lane < bs && q <= lane) ? a[kb + lane][kb + q] : 0.0;
+#pragma unroll
+            for (int j = 0; j < PD_B; ++j) {
+                if (j < bs) {
+                    double dj = __shfl_sync(0xffffffffu, r[j], j);
+                    if (!(dj > 0.0) || !isfinite(dj)) {
+                        if (lane == 0) atomicCAS(info, 0, (int)(k + kb + j + 1));
+                        dj = 1.0;
+                    }
+                    const double rs = rsqrt(dj);
+                    const double l = lane == j ? dj * rs : (lane > j ? r[j] * rs : 0.0);
+                    r[j] = l;
+                    if (lane == j) rdiag[j] = rs;  // 1 / l_jj for the panel solve
+#pragma unroll
+                    for (int q = j + 1; q < PD_B; ++q) {
+                        const double lq = __shfl_sync(0xffffffffu, l, q);
+                        if (lane >= q) r[q] = fma(-l, lq, r[q]);
+                    }
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < PD_B; ++q)
+                if (lane < bs && q <= lane) a[kb + lane][kb + q] = r[q];
+        }
+        __syncthreads();
+        const int rows = nb - kb - bs;
+        if (rows <= 0) break;
+        // 2. the panel below: row i solves l_i,kb+j = (a_i,kb+j - sum_t<j l_i,kb+t l_kb+j,kb+t) / l_jj
+        if (tid < rows) {
+            const int i = kb + bs + tid;
+            double x[PD_B];
+#pragma unroll
+            for (int j = 0; j < PD_B; ++j) x[j] = j < bs ? a[i][kb + j] : 0.0;
+#pragma unroll
+            for (int j = 0; j < PD_B; ++j) {
+                if (j < bs) {
+                    double s = x[j];
+#pragma unroll
+                    for (int t = 0; t < j; ++t) s = fma(-x[t], a[kb + j][kb + t], s);
+                    x[j] = s * rdiag[j];
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < PD_B; ++j)
+                if (j < bs) a[i][kb + j] = x[j];
+        }
+        __syncthreads();
+        // 3. trailing update of the lower part: A22 -= L21 L21^T (rank bs)
+        const int r0 = kb + bs;
+        for (int e = tid; e < rows * rows; e += 256) {
+            const int ii = e % rows, jj = e / rows;
+            if (ii < jj) continue;
+            double s = a[r0 + ii][r0 + jj];
+#pragma unroll
+            for (int t = 0; t < PD_B; ++t)
+                if (t < bs) s = fma(-a[r0 + ii][kb + t], a[r0 + jj][kb + t], s);
+            a[r0 + ii][r0 + jj] = s;
         }
         __syncthreads();
     }
-    for (int jj = g; jj < nb; jj += 4) {
-        if (i < nb && i >= jj) {
-            const double pj = piv[jj];
-            H[(k + i) + (k + jj) * n] = (i == jj) ? sqrt(pj) : out[i][jj] * rsqrt(pj);
-        }
+    for (int e = tid; e < NB * NB; e += 256) {
+        const int i = e % NB, jj = e / NB;
+        if (i < nb && jj < nb && i >= jj) H[(k + i) + (k + jj) * n] = a[i][jj];
     }
 }
 
