@@ -235,6 +235,10 @@ size_t gemv_tiled_work_doubles(int64_t M, int64_t N);
 void gemv_tiled(const double* A, int64_t M, int64_t N, int64_t lda, const double* x, int nrhs, int64_t ldx, double* y,
                 int64_t ldy, double* work, cudaStream_t st, double* dots = nullptr);
 void gemv_tiled_reset(double* work, int64_t M, int64_t N, cudaStream_t st);
+// y = H x for a symmetric k x k column-major H (one warp per output column), optional fused decrement dots
+// (as gemv_tiled); work as gemv_tiled(k, k)
+void symv_col(const double* H, int64_t k, const double* x, int nrhs, int64_t ldx, double* y, int64_t ldy,
+              double* work, cudaStream_t st, double* dots = nullptr);
 // Wl = lower triangle of W (upper zeroed), k x k
 void tril_copy(const double* W, int64_t k, double* Wl, cudaStream_t st);
 void add_diag(double* H, int64_t n, double v, cudaStream_t st);

@@ -573,7 +573,7 @@ void system_factorize(ihs_gpu_system* S, ihs_counters* c) {
 void system_solve_dev(const ihs_gpu_system* S, const double* g, double* z, int nrhs);
 void system_solve_dots(const ihs_gpu_system* S, const double* g, double* z, int nrhs, double* dots) {
     if (S->kind == IHS_FACTOR_DIRECT_GRAM) {
-        gemv_tiled(S->Hinv.d(), S->d, S->d, S->d, g, nrhs, S->d, z, S->d, S->gv.d(), S->st, dots);
+        symv_col(S->Hinv.d(), S->d, g, nrhs, S->d, z, S->d, S->gv.d(), S->st, dots);
     } else {
         system_solve_dev(S, g, z, nrhs);
         decrement_dots(g, z, S->d, nrhs, dots, S->st);
@@ -592,7 +592,7 @@ void system_solve_dev(const ihs_gpu_system* S, const double* g, double* z, int n
         cholesky_solve_inv(S->W.d(), m, u, w, nrhs, work, st);
         woodbury_finish(S->SA.d(), m, d, g, w, S->nu * S->nu, nrhs, z, st);
     } else {
-        gemv_tiled(S->Hinv.d(), d, d, d, g, nrhs, d, z, d, S->gv.d(), st);
+        symv_col(S->Hinv.d(), d, g, nrhs, d, z, d, S->gv.d(), st);
     }
 }
 
@@ -702,7 +702,7 @@ void cg_run(ihs_gpu_problem* P, const ihs_gpu_system* S, double tol, int64_t max
     mark(PH_SOLVE);
     cg_begin(g0, x0 ? hx : nullptr, r, p, tol, d, state, resid, pcg, st);
     if (pcg) {
-        gemv_tiled(S->Hinv.d(), d, d, d, r, 1, d, z, d, S->gv.d(), st, dots);
+        symv_col(S->Hinv.d(), d, r, 1, d, z, d, S->gv.d(), st, dots);
         cg_dir(state, z, dots, p, d, true, st);
     }
     mark(PH_END);
@@ -719,7 +719,7 @@ void cg_run(ihs_gpu_problem* P, const ihs_gpu_system* S, double tol, int64_t max
             mark(PH_SOLVE);
             cg_step(state, p, hp, x, r, resid, launched, d, pcg, st);
             if (pcg) {
-                gemv_tiled(S->Hinv.d(), d, d, d, r, 1, d, z, d, S->gv.d(), st, dots);
+                symv_col(S->Hinv.d(), d, r, 1, d, z, d, S->gv.d(), st, dots);
                 cg_dir(state, z, dots, p, d, false, st);
             }
         }
@@ -778,12 +778,12 @@ void direct_solve_dev(ihs_gpu_problem* Q, double* x, int refinements = 3) {
     double *g = v.d(), *dx = g + d, *zero = dx + d;
     CUDA_CHECK(cudaMemsetAsync(zero, 0, (size_t)d * sizeof(double), st));
     problem_grad(Q, zero, 1, g);  // -rhs
-    gemv_tiled(S.Hinv.d(), d, d, d, g, 1, d, dx, d, S.gv.d(), st);
+    symv_col(S.Hinv.d(), d, g, 1, d, dx, d, S.gv.d(), st);
     CUDA_CHECK(cudaMemsetAsync(x, 0, (size_t)d * sizeof(double), st));
     add_scaled(x, dx, -1.0, d, st);
     for (int it = 0; it < refinements; ++it) {
         problem_grad(Q, x, 1, g);
-        gemv_tiled(S.Hinv.d(), d, d, d, g, 1, d, dx, d, S.gv.d(), st);
+        symv_col(S.Hinv.d(), d, g, 1, d, dx, d, S.gv.d(), st);
         add_scaled(x, dx, -1.0, d, st);
     }
     CUDA_CHECK(cudaStreamSynchronize(st));

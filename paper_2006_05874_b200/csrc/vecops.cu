@@ -164,6 +164,86 @@ __global__ void __launch_bounds__(256) gemv_tiled_kernel(const double* __restric
     if (threadIdx.x == 0) arrivals[gridDim.x] = 0u;
 }
 
+// y = H x for a symmetric k x k H (column-major; H_S^{-1} of the direct-Gram system): y_i = column i . x,
+// one warp per output over a contiguous column, no cross-CTA partial sums. With dots != nullptr the
+// decrement dots x.y and x.x per right-hand side are finished by the last CTA from per-CTA partials in
+// CTA order (deterministic). part: 4 * gridDim.x doubles; counter: zero before the launch, reset after.
+// work (symv_col): gemv_tiled_work_doubles(k, k) + 8, reset by gemv_tiled_reset.
+constexpr int SV_W = 8;  // outputs (warps) per CTA
+__global__ void __launch_bounds__(32 * SV_W) symv_col_kernel(const double* __restrict__ H, int64_t k,
+                                                             const double* __restrict__ x, int nrhs, int64_t ldx,
+                                                             double* __restrict__ y, int64_t ldy,
+                                                             double* __restrict__ dots, double* __restrict__ part,
+                                                             unsigned* __restrict__ counter) {
+    pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible after this
+    extern __shared__ double xs[];  // nrhs x k
+    __shared__ double pd[SV_W][4];
+    __shared__ unsigned last;
+    for (int64_t e = threadIdx.x; e < (int64_t)nrhs * k; e += blockDim.x) {
+        const int64_t q = e / k, t = e % k;
+        xs[e] = x[q * ldx + t];
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t i = (int64_t)blockIdx.x * SV_W + w;
+    double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+    if (i < k) {
+        const double* col = H + i * k;
+        int64_t t = lane;
+        for (; t + 32 < k; t += 64) {
+            const double a0 = col[t], a1 = col[t + 32];
+            acc[0][0] = fma(a0, xs[t], acc[0][0]);
+            acc[0][1] = fma(a1, xs[t + 32], acc[0][1]);
+            if (nrhs > 1) {
+                acc[1][0] = fma(a0, xs[k + t], acc[1][0]);
+                acc[1][1] = fma(a1, xs[k + t + 32], acc[1][1]);
+            }
+        }
+        if (t < k) {
+            const double a0 = col[t];
+            acc[0][0] = fma(a0, xs[t], acc[0][0]);
+            if (nrhs > 1) acc[1][0] = fma(a0, xs[k + t], acc[1][0]);
+        }
+    }
+    double yv[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+        double v = acc[q][0] + acc[q][1];
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+        yv[q] = v;
+    }
+    if (lane == 0) {
+        for (int q = 0; q < 4; ++q) pd[w][q] = 0.0;
+        if (i < k)
+            for (int q = 0; q < nrhs; ++q) {
+                y[q * ldy + i] = yv[q];
+                const double xi = xs[q * k + i];
+                pd[w][2 * q] = xi * yv[q];
+                pd[w][2 * q + 1] = xi * xi;
+            }
+    }
+    if (dots == nullptr) return;
+    __syncthreads();
+    if (threadIdx.x < 4) {
+        double s = 0.0;
+        for (int ww = 0; ww < SV_W; ++ww) s += pd[ww][threadIdx.x];
+        part[(int64_t)blockIdx.x * 4 + threadIdx.x] = s;
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(counter, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    if (threadIdx.x < 2 * nrhs) {
+        double s = 0.0;
+        for (unsigned c = 0; c < gridDim.x; ++c) s += __ldcg(part + (int64_t)c * 4 + threadIdx.x);
+        dots[threadIdx.x] = s;
+    }
+    if (threadIdx.x == 0) *counter = 0u;
+}
+
 // z[:,q] = (g[:,q] - SA^T w[:,q]) / nu2 ; one warp per column of SA
 __global__ void woodbury_finish_kernel(const double* __restrict__ SA, int64_t m, int64_t d,
                                        const double* __restrict__ g, const double* __restrict__ w, double nu2,
@@ -236,6 +316,28 @@ void gemv_tiled(const double* A, int64_t M, int64_t N, int64_t lda, const double
     dim3 grid((unsigned)ceil_div(M, GV_ROWS), (unsigned)ceil_div(N, GV_COLS));
     unsigned* arrivals = reinterpret_cast<unsigned*>(work + (size_t)grid.y * 2 * (size_t)M);
     LAUNCH_PDL(gemv_tiled_kernel, grid, dim3(256), 0, st, A, M, N, lda, x, nrhs, ldx, work, arrivals, y, ldy, dots);
+}
+
+// y = H x, H symmetric k x k (column-major); work: gemv_tiled_work_doubles(k, k) (its counter tail is
+// reset by gemv_tiled_reset, and this kernel leaves it zero)
+void symv_col(const double* H, int64_t k, const double* x, int nrhs, int64_t ldx, double* y, int64_t ldy,
+              double* work, cudaStream_t st, double* dots) {
+    // the counter sits in the zeroed tail of the gemv_tiled layout, past gemv_tiled's own arrival counters;
+    // the per-CTA partials at the front (or, for k <= 2 where the front is shorter, in the 8 spare doubles
+    // the factorization allocates after the tail)
+    const size_t front = (size_t)ceil_div(k, GV_COLS) * 2 * (size_t)k;
+    double* tail = work + front;
+    unsigned* counter = reinterpret_cast<unsigned*>(tail + ceil_div(k, GV_ROWS) + 4);
+    const unsigned grid = (unsigned)ceil_div(k, SV_W);
+    double* part = (size_t)4 * grid <= front ? work : tail + ceil_div(k, GV_ROWS) + 8;
+    const size_t smem = (size_t)nrhs * k * sizeof(double);
+    static int attr_bytes = 48 * 1024;
+    if ((int)smem > attr_bytes) {
+        CUDA_CHECK(cudaFuncSetAttribute(symv_col_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr_bytes = (int)smem;
+    }
+    LAUNCH_PDL(symv_col_kernel, dim3(grid), dim3(32 * SV_W), smem, st, H, k, x, nrhs, ldx, y, ldy, dots, part,
+               counter);
 }
 
 void gemv_tiled_reset(double* work, int64_t M, int64_t N, cudaStream_t st) {
