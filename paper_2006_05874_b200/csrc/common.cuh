@@ -95,7 +95,7 @@ SrhtPlan srht_plan(int64_t n, int64_t d, int64_t lda, int64_t m);
 // p2t before the entries are built); false = two-kernel path
 bool srht_plan_stream(SrhtPlan& p, int num_sms);
 // switch a two-kernel plan with 10 high bits (n_pad = 2^20) to compact T when the sample has few distinct
-// low indices (U <= 256): phase 1 stores, per chunk, only the low indices some sampled row has
+// low indices (U <= 640): phase 1 stores, per chunk, only the low indices some sampled row has
 // (T[j][h][u]) and the emitting pass runs one warp per (u, column). Set before the entries are built (they then carry U tiles followed by the 1024-entry
 // low-index -> u map).
 bool srht_plan_compact(SrhtPlan& p, const int64_t* rows);

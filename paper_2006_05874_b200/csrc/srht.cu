@@ -621,46 +621,54 @@ srht_phase2_kernel(double* __restrict__ T, int64_t n_pad, int lo, const int4* __
     p2_tile<HB, false, CtaBar, TH>(xs, T + j * n_pad + base, lo, emit != 0, tile, entries, j, s1, s2, SA, m);
 }
 
-// Compact emitting pass (n_pad = 2^20, compact T[j][h][u] with u padded to 8, h = row bits 10..19): a CTA takes 8
-// consecutive low-index ranks u of column j, stages their 1024 x 8 values in shared memory with
-// coalesced reads, and warp w transforms rank u0 + w: the ten high butterflies in the reference's order —
-// bits 0-4 of h across lanes (shuffles; the upper lane forms s - t from its partner's s, the lower s + t),
-// bits 5-9 in registers — then emits the sampled rows with that low index, scaled twice.
-constexpr int kCmpU = 8, kCmpLd = kCmpU + 1;  // ranks per CTA, padded shared row (conflict-free columns)
-__global__ void __launch_bounds__(256) srht_phase2_compact_kernel(const double* __restrict__ Tc, int64_t U,
-                                                                  const int4* __restrict__ ranges,
-                                                                  const int2* __restrict__ entries, double s1,
-                                                                  double s2, double* __restrict__ SA, int64_t m) {
+// Compact emitting pass (n_pad = 2^20, compact T[j][h][u] with u padded to 8, h = row bits 10..19): a CTA
+// stages 8 consecutive ranks of column j with coalesced 64-byte reads into per-rank shared rows (element h
+// at the XOR swizzle row h>>5, column (h ^ (h>>5)) & 31, so both orientations below are conflict-free);
+// warp w then runs the ten high butterflies of rank u0 + w in the reference's order entirely in
+// registers — bits 0-4 with the register index = h bits 0-4, a write-back, bits 5-9 with the register
+// index = h bits 5-9 — and emits the sampled rows with that low index, scaled twice.
+constexpr int kCmpU = 8;      // ranks (warps) per CTA
+constexpr int kCmpRow = 1025;  // shared row per rank (odd: ranks start on different banks)
+__device__ __forceinline__ int cmp_swz(int row, int col) { return (row << 5) | (col ^ row); }
+__global__ void __launch_bounds__(32 * kCmpU) srht_phase2_compact_kernel(const double* __restrict__ Tc, int64_t U,
+                                                                         const int4* __restrict__ ranges,
+                                                                         const int2* __restrict__ entries,
+                                                                         double s1, double s2,
+                                                                         double* __restrict__ SA, int64_t m) {
     pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible after this
-    extern __shared__ double ct[];  // [1024][kCmpLd]
+    extern __shared__ double cbuf[];  // [kCmpU][kCmpRow]
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t u0 = (int64_t)blockIdx.x * kCmpU, j = blockIdx.y;
     const int nu = (int)(U - u0 < kCmpU ? U - u0 : kCmpU);
     const int64_t Up = (U + 7) & ~int64_t{7};  // row stride: 64-byte aligned runs of 8 ranks
-    const double* src = Tc + j * 1024 * Up + u0;
     {
-        // 32 independent loads per thread (8 ranks x 32 h per instruction round), like a phase-2 tile
-        const int uu = threadIdx.x % kCmpU, h0 = threadIdx.x / kCmpU;
+        const double* src = Tc + j * 1024 * Up + u0;
+        const int uu = threadIdx.x % kCmpU, h0 = threadIdx.x / kCmpU;  // 32 h per pass, 8 ranks each
         double t[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i) t[i] = uu < nu ? __ldcs(src + (int64_t)(h0 + 32 * i) * Up + uu) : 0.0;
 #pragma unroll
-        for (int i = 0; i < 32; ++i) ct[(h0 + 32 * i) * kCmpLd + uu] = t[i];
+        for (int i = 0; i < 32; ++i) {
+            const int h = h0 + 32 * i;
+            cbuf[uu * kCmpRow + cmp_swz(h >> 5, h & 31)] = t[i];
+        }
     }
     __syncthreads();
     if (warp >= nu) return;
+    double* buf = cbuf + warp * kCmpRow;
     double v[32];
 #pragma unroll
-    for (int c = 0; c < 32; ++c) v[c] = ct[((c << 5) | lane) * kCmpLd + warp];  // h = 32c + lane
+    for (int c = 0; c < 32; ++c) v[c] = buf[cmp_swz(lane, c)];  // h = 32 lane + c: bits 0-4 in the register
 #pragma unroll
-    for (int s = 0; s < 5; ++s) {
-        const bool upper = (lane >> s) & 1;
+    for (int s = 0; s < 5; ++s)
 #pragma unroll
-        for (int c = 0; c < 32; ++c) {
-            const double o = __shfl_xor_sync(0xffffffffu, v[c], 1 << s);
-            v[c] = upper ? __dsub_rn(o, v[c]) : __dadd_rn(v[c], o);
-        }
-    }
+        for (int c = 0; c < 32; ++c)
+            if (!(c & (1 << s))) bfly(v[c], v[c | (1 << s)]);
+#pragma unroll
+    for (int c = 0; c < 32; ++c) buf[cmp_swz(lane, c)] = v[c];
+    __syncwarp();
+#pragma unroll
+    for (int c = 0; c < 32; ++c) v[c] = buf[cmp_swz(c, lane)];  // h = 32 c + lane: bits 5-9 in the register
 #pragma unroll
     for (int s = 0; s < 5; ++s)
 #pragma unroll
@@ -1169,11 +1177,11 @@ bool srht_plan_compact(SrhtPlan& p, const int64_t* rows) {
     }();
     static const int umax = [] {
         const char* e = std::getenv("IHS_SRHT_COMPACT_MAX");
-        return e ? std::atoi(e) : 256;
+        return e ? std::atoi(e) : 640;
     }();
     if (disabled || p.H != 10 || p.npass != 1 || p.stream) return false;
-    // measured (profiles/r01_srht_compact.txt): compact wins while its emitting pass stays small, i.e. up
-    // to ~256 distinct low indices; beyond that the tiled pass over the masked T is faster
+    // measured (profiles/r01_srht_compact.txt): compact phase 1 + emitting pass beat the masked T up to
+    // ~640 distinct low indices (m ~ 1000 at n_pad = 2^20); beyond that the tiled pass is faster
     std::vector<uint8_t> seen(1024, 0);
     int U = 0;
     for (int64_t k = 0; k < p.m && U <= umax; ++k) {
@@ -1329,7 +1337,7 @@ void srht_run_device(const SrhtPlan& p, const double* d_A, const uint32_t* d_sig
                p.n_pad, p.logn - kChunkL, total, masked ? d_mask : nullptr, logw, lmap, U);
     }
     if (p.compact) {
-        constexpr size_t smem = (size_t)1024 * kCmpLd * sizeof(double);
+        constexpr size_t smem = (size_t)kCmpU * kCmpRow * sizeof(double);
         static bool attr = false;
         if (!attr) {
             CUDA_CHECK(cudaFuncSetAttribute(srht_phase2_compact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
