@@ -417,3 +417,23 @@ def test_srht_compact_modes_bit_exact(gpu):
         env = dict(os.environ, IHS_SRHT_COMPACT_MAX="1024", **extra)
         r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300, env=env, cwd=root)
         assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
+
+def test_srht_three_round_pass_column_batches_bit_exact(gpu):
+    """n_pad = 2^22 (one 12-bit emitting pass of three-round tiles) over column batches (40 MiB cap = one
+    32 MiB column per batch), as C4 runs it: bit-exact."""
+    import os
+    import subprocess
+    import sys
+    code = ("import numpy as np\n"
+            "from paper_2006_05874_b200 import ihs\n"
+            "from oracle import oracle as O\n"
+            "rng = np.random.default_rng(9)\n"
+            "A = np.asfortranarray(rng.standard_normal(((1 << 22) - 3, 3)))\n"
+            "for m in (7, 500):\n"
+            "    assert np.array_equal(ihs.srht_sketch(A, m, 2 + m), O.srht_sketch(A, m, 2 + m)), m\n"
+            "print('ok')\n")
+    root = str(__import__("pathlib").Path(__file__).resolve().parents[1])
+    env = dict(os.environ, IHS_SRHT_SCRATCH_CAP_MB="40")
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300, env=env, cwd=root)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
