@@ -51,6 +51,9 @@ CONFIGS = {
     "c4": dict(desc="C4 SRHT adaptive Polyak-IHS n=2^22 d=2048 sigma=1/j", n=1 << 22, d=2048, spectrum=1,
                decay=0.0, noise=0.01, nu=1e-4, outliers=0.0, sketch="SRHT", mode="PolyakThenGradient", rho=0.1,
                m_initial=1, max_sketch=None, enforce_validity=True),
+    "c4g": dict(desc="C4 Gaussian adaptive Polyak-IHS n=2^22 d=2048 sigma=1/j (streamed S)", n=1 << 22, d=2048,
+                spectrum=1, decay=0.0, noise=0.01, nu=1e-4, outliers=0.0, sketch="Gaussian", mode="PolyakThenGradient",
+                rho=0.1, m_initial=1, max_sketch=None, enforce_validity=True),
     "c5": dict(desc="C5 SRHT adaptive Polyak-IHS n=10^6 (pad 2^20) d=4096 +1% x100 outliers", n=10**6, d=4096,
                spectrum=0, decay=0.999, noise=0.01, nu=1e-5, outliers=0.01, sketch="SRHT",
                mode="PolyakThenGradient", rho=0.1, m_initial=1, max_sketch=None, enforce_validity=True),

@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <functional>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -78,6 +79,18 @@ size_t gaussian_scratch_bytes(int64_t count);
 // normals [first, first + count) of the stream (first > 0: a row shard's columns of S)
 void mt_fill_gaussian(uint64_t seed, int64_t first, int64_t count, double stddev, double* d_out, void* d_scratch,
                       cudaStream_t st);
+
+// Streamed normals [first, first + count) for the Gaussian sketch of tall matrices (S never materialised):
+// the stream is generated in chunks of jump-ahead substreams with a carried acceptance count; normals are
+// emitted into buf (capacity cap; buf[0] = normal `base`), and once at least `block` are ready (or the range
+// is complete) consume(base, ready) is called and returns how many leading normals it used (whole columns;
+// block must hold at least two columns). d_scratch: gaussian_stream_scratch_bytes(); cap >= block +
+// 2 * gaussian_stream_chunk_attempts().
+size_t gaussian_stream_scratch_bytes();
+int64_t gaussian_stream_chunk_attempts();
+void mt_gaussian_stream(uint64_t seed, int64_t first, int64_t count, double stddev, double* buf, int64_t cap,
+                        int64_t block, void* d_scratch, cudaStream_t st,
+                        const std::function<int64_t(int64_t, int64_t)>& consume);
 
 // srht.cu — SRHT sketch SA = sqrt(n_pad/m) R H D A (sketch.hpp:77-108)
 struct SrhtPlan {

@@ -18,6 +18,8 @@
 // start states are obtained by F2-linear jump-ahead (mt_jump.cpp) and run one
 // CTA per substream.
 #include "common.cuh"
+
+#include <functional>
 #include "mt_core.cuh"
 #include "mt_jump.h"
 
@@ -166,11 +168,12 @@ __global__ void polar_flags_kernel(const uint64_t* __restrict__ raw, int64_t att
 
 // normals [first, first + count) of the stream -> out[0 .. count)
 __global__ void polar_emit_kernel(const uint64_t* __restrict__ raw, int64_t attempts, const int* __restrict__ pos,
-                                  int64_t first, int64_t count, double stddev, double* __restrict__ out) {
+                                  int64_t first, int64_t count, double stddev, double* __restrict__ out,
+                                  int64_t carry) {
     pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible after this
     const int64_t end = first + count;
     for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < attempts; a += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t k = 2 * (int64_t)pos[a];
+        const int64_t k = carry + 2 * (int64_t)pos[a];  // normal index (carry: normals of earlier chunks)
         if (k >= end || k + 1 < first) continue;
         double x, y, r2;
         if (!polar_attempt(raw, a, x, y, r2)) continue;
@@ -274,7 +277,87 @@ void mt_fill_gaussian(uint64_t seed, int64_t first, int64_t count, double stddev
     CUDA_CHECK(cudaMemcpyAsync(&h_total, total, sizeof(long long), cudaMemcpyDeviceToHost, st));
     CUDA_CHECK(cudaStreamSynchronize(st));
     if (2 * h_total < first + count) fail(IHS_INTERNAL_ERROR, "fill_gaussian: draw estimate too small");
-    LAUNCH_PDL(polar_emit_kernel, blocks, threads, 0, st, raw, attempts, pos, first, count, stddev, d_out);
+    LAUNCH_PDL(polar_emit_kernel, blocks, threads, 0, st, raw, attempts, pos, first, count, stddev, d_out,
+               (int64_t)0);
+}
+
+// ---- streamed normals (the Gaussian sketch of tall matrices, S never materialised)
+namespace {
+int64_t stream_subs() {  // substreams per chunk (IHS_GAUSS_STREAM_SUBS overrides; tests use 1)
+    static const int64_t v = [] {
+        const char* e = std::getenv("IHS_GAUSS_STREAM_SUBS");
+        const long long x = e ? std::atoll(e) : 0;
+        return x > 0 ? (int64_t)x : (int64_t)64;
+    }();
+    return v;
+}
+}  // namespace
+
+int64_t gaussian_stream_chunk_attempts() { return stream_subs() * kStreamStride / 2; }
+
+size_t gaussian_stream_scratch_bytes() {
+    const int64_t draws = stream_subs() * kStreamStride, attempts = draws / 2;
+    size_t temp = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, temp, (int*)nullptr, (int*)nullptr, (int)attempts);
+    return (size_t)draws * 8 + (size_t)attempts * 8 + temp + 256 + (size_t)stream_subs() * NN * 8 +
+           (size_t)kJumpSeqWords * 8 + 1024;
+}
+
+void mt_gaussian_stream(uint64_t seed, int64_t first, int64_t count, double stddev, double* buf, int64_t cap,
+                        int64_t block, void* d_scratch, cudaStream_t st,
+                        const std::function<int64_t(int64_t, int64_t)>& consume) {
+    if (count <= 0) return;
+    const int64_t Q = stream_subs(), draws = Q * kStreamStride, attempts = draws / 2;
+    char* p = static_cast<char*>(d_scratch);
+    uint64_t* raw = reinterpret_cast<uint64_t*>(p);
+    p += (size_t)draws * 8;
+    int* flags = reinterpret_cast<int*>(p);
+    int* pos = flags + attempts;
+    p += (size_t)attempts * 8;
+    long long* total = reinterpret_cast<long long*>(p);
+    p += 256;
+    uint64_t* starts = reinterpret_cast<uint64_t*>(p);
+    p += (size_t)Q * NN * 8;
+    uint64_t* xseq = reinterpret_cast<uint64_t*>(p);
+    p += (size_t)kJumpSeqWords * 8;
+    void* temp = p;
+    size_t temp_bytes = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, temp_bytes, flags, pos, (int)attempts);
+    const int threads = 256;
+    const int blocks = (int)std::min<int64_t>(ceil_div(attempts, threads), 148 * 16);
+    const int64_t end = first + count;
+    int64_t carry = 0;   // normals produced by the chunks so far
+    int64_t base = first; // normal index held by buf[0]
+    for (int64_t c = 0; carry < end; ++c) {
+        // chunk c: substreams [c Q, (c + 1) Q) of kStreamStride draws, attempts from draw 2 c Q stride
+        mt_jump_starts(seed, kStreamStride, Q, starts, xseq, st, c * Q);
+        LAUNCH_PDL(mt_substream_kernel, (unsigned)Q, 160, 0, st, starts, (int64_t)kStreamStride, draws, raw);
+        LAUNCH_PDL(polar_flags_kernel, blocks, threads, 0, st, raw, attempts, flags);
+        CUDA_CHECK(cub::DeviceScan::ExclusiveSum(temp, temp_bytes, flags, pos, (int)attempts, st));
+        note_launch();
+        LAUNCH_PDL(last_total_kernel, 1, 1, 0, st, pos, flags, attempts, total);
+        long long h_total = 0;
+        CUDA_CHECK(cudaMemcpyAsync(&h_total, total, sizeof(long long), cudaMemcpyDeviceToHost, st));
+        CUDA_CHECK(cudaStreamSynchronize(st));
+        const int64_t produced = 2 * (int64_t)h_total;
+        if (carry + produced > first) {
+            if (std::min(carry + produced, end) - base > cap) fail(IHS_INTERNAL_ERROR, "gaussian stream: buffer too small");
+            // normals [max(carry, base), min(carry + produced, end)) -> buf[k - base]
+            LAUNCH_PDL(polar_emit_kernel, blocks, threads, 0, st, raw, attempts, pos, base, end - base, stddev, buf,
+                       carry);
+        }
+        carry += produced;
+        const int64_t ready = std::min(carry, end) - base;
+        if (ready >= block || carry >= end) {
+            const int64_t used = consume(base, ready);
+            const int64_t left = ready - used;
+            if (left > used) fail(IHS_INTERNAL_ERROR, "gaussian stream: block smaller than two columns");
+            if (left > 0)
+                CUDA_CHECK(cudaMemcpyAsync(buf, buf + used, (size_t)left * sizeof(double), cudaMemcpyDeviceToDevice,
+                                           st));
+            base += used;
+        }
+    }
 }
 
 }  // namespace ihs_b200

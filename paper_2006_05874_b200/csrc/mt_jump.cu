@@ -285,7 +285,9 @@ const std::vector<uint64_t>& mt_jump_polys(int64_t stride, int64_t nsub) {
     return vec;
 }
 
-void mt_jump_starts(uint64_t seed, int64_t stride, int64_t nsub, uint64_t* d_starts, uint64_t* d_X, cudaStream_t st) {
+void mt_jump_starts(uint64_t seed, int64_t stride, int64_t nsub, uint64_t* d_starts, uint64_t* d_X, cudaStream_t st,
+                    int64_t q0) {
+    const int64_t qend = q0 + nsub;  // substreams [q0, qend)
     // device copies of the set-bit lists of x^(q*stride) mod P, cached per
     // (device, stride) and grown on demand (seed-independent)
     struct DevLists {
@@ -302,12 +304,13 @@ void mt_jump_starts(uint64_t seed, int64_t stride, int64_t nsub, uint64_t* d_sta
         std::lock_guard<std::mutex> lk(mu);
         auto key = std::make_pair(dev_id, stride);
         auto it = dev.find(key);
-        if (it == dev.end() || it->second.count < nsub) {
-            const std::vector<uint64_t>& polys = mt_jump_polys(stride, nsub);
+        if (it == dev.end() || it->second.count < qend) {
+            const int64_t nall = qend;
+            const std::vector<uint64_t>& polys = mt_jump_polys(stride, nall);
             std::vector<uint16_t> pos;
-            std::vector<int> ptr((size_t)nsub * (kChunks + 1));
-            pos.reserve((size_t)nsub * DEG / 2 + 64);
-            for (int64_t q = 0; q < nsub; ++q) {
+            std::vector<int> ptr((size_t)nall * (kChunks + 1));
+            pos.reserve((size_t)nall * DEG / 2 + 64);
+            for (int64_t q = 0; q < nall; ++q) {
                 const uint64_t* a = polys.data() + (size_t)q * PW;
                 for (int c = 0; c < kChunks; ++c) {
                     ptr[(size_t)q * (kChunks + 1) + c] = (int)pos.size();
@@ -325,7 +328,7 @@ void mt_jump_starts(uint64_t seed, int64_t stride, int64_t nsub, uint64_t* d_sta
             CUDA_CHECK(cudaMalloc(&L.ptr, ptr.size() * sizeof(int)));
             CUDA_CHECK(cudaMemcpy(L.pos, pos.data(), pos.size() * sizeof(uint16_t), cudaMemcpyHostToDevice));
             CUDA_CHECK(cudaMemcpy(L.ptr, ptr.data(), ptr.size() * sizeof(int), cudaMemcpyHostToDevice));
-            L.count = nsub;
+            L.count = nall;
             dev[key] = L;
         } else {
             L = it->second;
@@ -333,7 +336,8 @@ void mt_jump_starts(uint64_t seed, int64_t stride, int64_t nsub, uint64_t* d_sta
     }
     CUDA_CHECK(cudaMemsetAsync(d_starts, 0, (size_t)nsub * NN * 8, st));
     LAUNCH_PDL(mt_wordseq_kernel, 1, mt::THREADS, 0, st, seed, NX, d_X);
-    LAUNCH_PDL(mt_jump_apply_kernel, dim3((unsigned)nsub, kChunks), kApplyThreads, 0, st, d_X, L.pos, L.ptr, d_starts);
+    LAUNCH_PDL(mt_jump_apply_kernel, dim3((unsigned)nsub, kChunks), kApplyThreads, 0, st, d_X, L.pos,
+               L.ptr + q0 * (kChunks + 1), d_starts);
 }
 
 }  // namespace ihs_b200

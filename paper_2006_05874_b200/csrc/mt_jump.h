@@ -22,6 +22,10 @@ constexpr int64_t kJumpSeqWords = 19937 + 312 - 1;
 // Device: write the 312-word start window of substream q (state after
 // q*stride draws of mt19937_64(seed)) to d_starts[q*312 ...]; d_X is
 // kJumpSeqWords words of scratch.
-void mt_jump_starts(uint64_t seed, int64_t stride, int64_t nsub, uint64_t* d_starts, uint64_t* d_X, cudaStream_t st);
+// q0 > 0: substreams q0 .. q0+nsub-1 (start windows still written from d_starts[0]).
+void mt_jump_starts(uint64_t seed, int64_t stride, int64_t nsub, uint64_t* d_starts, uint64_t* d_X, cudaStream_t st,
+                    int64_t q0 = 0);
+// Draws per substream of the streamed (block-by-block) Gaussian generation.
+constexpr int64_t kStreamStride = int64_t{1} << 22;
 
 }  // namespace ihs_b200

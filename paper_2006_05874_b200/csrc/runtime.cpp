@@ -460,18 +460,59 @@ void device_sketch(ihs_gpu_problem* P, int kind, int64_t m, uint64_t seed, doubl
         // a shard holds the columns of its rows, i.e. normals [row0*m, (row0+n)*m)
         const int64_t count = m * n;
         const int64_t first = world > 1 ? P->opts.row_offset * m : 0;
-        P->S.ensure((size_t)count * sizeof(double));
-        P->gauss_scratch.ensure(gaussian_scratch_bytes(first + count));
         const double stddev = 1.0 / std::sqrt(static_cast<double>(m));
-        mt_fill_gaussian(derive_seed(seed, 0), first, count, stddev, P->S.d(), P->gauss_scratch.p, st);
-        // SA = S * A on the DMMA path (sketch.hpp:68)
-        const int splitk = dgemm_pick_splitk(m, d, n, P->num_sms);
-        if (splitk > 1) P->gemm_work.ensure((size_t)splitk * m * d * sizeof(double));
-        ensure_A(P);  // S was generated without A
-        if (P->timer) P->timer->mark(PH_SKETCH_KERNEL);
-        dgemm(false, false, m, d, n, 1.0, P->S.d(), m, P->A.d(), P->lda, 0.0, d_SA, m, false, splitk,
-              splitk > 1 ? P->gemm_work.d() : nullptr, st);
-        if (P->timer) P->timer->mark(PH_SKETCH);
+        // materialise S when it and the generator's scratch fit comfortably; otherwise stream it in column
+        // blocks into an accumulating GEMM (IHS_GAUSS_STREAM=1 forces, IHS_GAUSS_STREAM_COLS sets the block)
+        static const int force_stream = [] {
+            const char* e = std::getenv("IHS_GAUSS_STREAM");
+            return e ? std::atoi(e) : -1;
+        }();
+        const size_t full_bytes = (size_t)count * sizeof(double) + gaussian_scratch_bytes(first + count);
+        size_t free_b = 0, total_b = 0;
+        CUDA_CHECK(cudaMemGetInfo(&free_b, &total_b));
+        const bool stream = force_stream == 1 || (force_stream != 0 && full_bytes + (8ull << 30) > free_b + P->S.bytes +
+                                                                        P->gauss_scratch.bytes);
+        if (!stream) {
+            P->S.ensure((size_t)count * sizeof(double));
+            P->gauss_scratch.ensure(gaussian_scratch_bytes(first + count));
+            mt_fill_gaussian(derive_seed(seed, 0), first, count, stddev, P->S.d(), P->gauss_scratch.p, st);
+            // SA = S * A on the DMMA path (sketch.hpp:68)
+            const int splitk = dgemm_pick_splitk(m, d, n, P->num_sms);
+            if (splitk > 1) P->gemm_work.ensure((size_t)splitk * m * d * sizeof(double));
+            ensure_A(P);  // S was generated without A
+            if (P->timer) P->timer->mark(PH_SKETCH_KERNEL);
+            dgemm(false, false, m, d, n, 1.0, P->S.d(), m, P->A.d(), P->lda, 0.0, d_SA, m, false, splitk,
+                  splitk > 1 ? P->gemm_work.d() : nullptr, st);
+            if (P->timer) P->timer->mark(PH_SKETCH);
+        } else {
+            static const int64_t env_cols = [] {
+                const char* e = std::getenv("IHS_GAUSS_STREAM_COLS");
+                return e ? (int64_t)std::atoll(e) : (int64_t)0;
+            }();
+            // column blocks of ~1 GiB of S (>= 2 columns), the buffer also holds one chunk's normals
+            const int64_t cols = std::max<int64_t>(2, env_cols > 0 ? env_cols : (int64_t)(128ll << 20) / m);
+            const int64_t block = cols * m;
+            const int64_t cap = block + 2 * gaussian_stream_chunk_attempts() + 2 * m + 16;
+            P->S.ensure((size_t)cap * sizeof(double));
+            P->gauss_scratch.ensure(gaussian_stream_scratch_bytes());
+            ensure_A(P);
+            int64_t col_done = 0;
+            auto consume = [&](int64_t base, int64_t ready) -> int64_t {
+                const int64_t ncols = std::min<int64_t>(ready / m, n - col_done);
+                if (ncols <= 0) return 0;
+                const int splitk = dgemm_pick_splitk(m, d, ncols, P->num_sms);
+                if (splitk > 1) P->gemm_work.ensure((size_t)splitk * m * d * sizeof(double));
+                if (P->timer) P->timer->mark(PH_SKETCH_KERNEL);
+                dgemm(false, false, m, d, ncols, 1.0, P->S.d(), m, P->A.d() + col_done, P->lda, col_done ? 1.0 : 0.0,
+                      d_SA, m, false, splitk, splitk > 1 ? P->gemm_work.d() : nullptr, st);
+                if (P->timer) P->timer->mark(PH_SKETCH);
+                col_done += ncols;
+                return ncols * m;
+            };
+            mt_gaussian_stream(derive_seed(seed, 0), first, count, stddev, P->S.d(), cap, block, P->gauss_scratch.p,
+                               st, consume);
+            if (col_done != n) fail(IHS_INTERNAL_ERROR, "gaussian stream: incomplete sketch");
+        }
         if (world > 1) nccl_allreduce_sum(d_SA, (size_t)(m * d), P->opts.nccl_comm, st);
         if (c) c->sketch += (uint64_t)m * (uint64_t)n_glob * (uint64_t)d;  // sketch.hpp:65-67
     } else {
