@@ -467,11 +467,14 @@ void device_sketch(ihs_gpu_problem* P, int kind, int64_t m, uint64_t seed, doubl
             const char* e = std::getenv("IHS_GAUSS_STREAM");
             return e ? std::atoi(e) : -1;
         }();
-        const size_t full_bytes = (size_t)count * sizeof(double) + gaussian_scratch_bytes(first + count);
-        size_t free_b = 0, total_b = 0;
-        CUDA_CHECK(cudaMemGetInfo(&free_b, &total_b));
-        const bool stream = force_stream == 1 || (force_stream != 0 && full_bytes + (8ull << 30) > free_b + P->S.bytes +
-                                                                        P->gauss_scratch.bytes);
+        const size_t s_bytes = (size_t)count * sizeof(double), g_bytes = gaussian_scratch_bytes(first + count);
+        bool stream = force_stream == 1;
+        if (force_stream != 1 && force_stream != 0 && (P->S.bytes < s_bytes || P->gauss_scratch.bytes < g_bytes)) {
+            // the buffers would grow: materialise only while that leaves room (the query is skipped when they fit)
+            size_t free_b = 0, total_b = 0;
+            CUDA_CHECK(cudaMemGetInfo(&free_b, &total_b));
+            stream = s_bytes + g_bytes + (8ull << 30) > free_b + P->S.bytes + P->gauss_scratch.bytes;
+        }
         if (!stream) {
             P->S.ensure((size_t)count * sizeof(double));
             P->gauss_scratch.ensure(gaussian_scratch_bytes(first + count));
