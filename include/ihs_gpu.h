@@ -270,6 +270,10 @@ ihs_status ihs_gpu_rademacher_bits(uint64_t stream_seed, int64_t n, uint32_t* ou
 /* fill_gaussian (rng.hpp:35-40) of a rows x cols column-major matrix. */
 ihs_status ihs_gpu_fill_gaussian(uint64_t stream_seed, int64_t rows, int64_t cols, double stddev,
                                  double* out);
+/* normals [first, first + count) of the same stream (a row shard's window of S); streamed != 0 runs the
+ * chunked generator of tall Gaussian sketches (blocks of `block` >= 2 normals) */
+ihs_status ihs_gpu_fill_gaussian_window(uint64_t stream_seed, int64_t first, int64_t count, double stddev,
+                                        int32_t streamed, int64_t block, double* out);
 /* raw mt19937_64(stream_seed) draws 0..count-1 (device generator) */
 ihs_status ihs_gpu_mt19937_64(uint64_t stream_seed, int64_t count, uint64_t* out);
 /* sample_without_replacement (rng.hpp:56-66), host-side sparse Fisher-Yates */

@@ -55,6 +55,7 @@ def lib():
         "ihs_gpu_sketch_matrix": (C.c_int, [d, i64, i64, i64, i32, i64, u64, d, P(abi.Counters)]),
         "ihs_gpu_rademacher_bits": (C.c_int, [u64, i64, P(C.c_uint32)]),
         "ihs_gpu_fill_gaussian": (C.c_int, [u64, i64, i64, C.c_double, d]),
+        "ihs_gpu_fill_gaussian_window": (C.c_int, [u64, i64, i64, C.c_double, i32, i64, d]),
         "ihs_gpu_mt19937_64": (C.c_int, [u64, i64, P(C.c_uint64)]),
         "ihs_sample_without_replacement": (C.c_int, [u64, i64, i64, P(C.c_int64)]),
         "ihs_gpu_system_factorize": (C.c_int, [d, i64, i64, i64, C.c_double, i32, P(abi.Counters), P(vp)]),
@@ -104,5 +105,5 @@ EXPORTED_SYMBOLS = (
     "ihs_synth_generate", "ihs_gpu_shard_rows", "ihs_gpu_nccl_unique_id", "ihs_gpu_nccl_comm_create",
     "ihs_gpu_nccl_comm_destroy", "ihs_gpu_sketch_sharded_emulated", "ihs_pcg_sketch_size", "ihs_gpu_cg_solve",
     "ihs_gpu_pcg_solve_with", "ihs_gpu_pcg_solve", "ihs_gpu_problem_set_nu", "ihs_gpu_direct_solve",
-    "ihs_gpu_problem_upload_async",
+    "ihs_gpu_problem_upload_async", "ihs_gpu_fill_gaussian_window",
 )

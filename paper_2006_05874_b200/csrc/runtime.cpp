@@ -1521,6 +1521,40 @@ ihs_status ihs_gpu_fill_gaussian(uint64_t stream_seed, int64_t rows, int64_t col
     });
 }
 
+// normals [first, first + count) of fill_gaussian(make_stream) — a row shard's columns of S; streamed != 0
+// uses the chunked generator of tall Gaussian sketches (in blocks of `block` normals)
+ihs_status ihs_gpu_fill_gaussian_window(uint64_t stream_seed, int64_t first, int64_t count, double stddev,
+                                        int32_t streamed, int64_t block, double* out) {
+    return guarded([&] {
+        if (first < 0 || count < 0) fail(IHS_INVALID_INPUT, "fill_gaussian: negative window");
+        if (count == 0) return;
+        DevBuf o, scratch;
+        if (!streamed) {
+            o.ensure((size_t)count * 8);
+            scratch.ensure(gaussian_scratch_bytes(first + count));
+            mt_fill_gaussian(stream_seed, first, count, stddev, o.d(), scratch.p, 0);
+            CUDA_CHECK(cudaMemcpy(out, o.p, (size_t)count * 8, cudaMemcpyDeviceToHost));
+            return;
+        }
+        if (block < 2) fail(IHS_INVALID_INPUT, "fill_gaussian: block must be >= 2");
+        const int64_t cap = block + 2 * gaussian_stream_chunk_attempts() + 16;
+        o.ensure((size_t)cap * 8);
+        scratch.ensure(gaussian_stream_scratch_bytes());
+        int64_t done = 0;
+        auto consume = [&](int64_t base, int64_t ready) -> int64_t {
+            const int64_t use = ready & ~int64_t{1};  // any even prefix: the window is not column-structured here
+            if (use <= 0) return 0;
+            CUDA_CHECK(cudaMemcpy(out + (base - first), o.p, (size_t)use * 8, cudaMemcpyDeviceToHost));
+            done += use;
+            return use;
+        };
+        mt_gaussian_stream(stream_seed, first, count, stddev, o.d(), cap, block, scratch.p, 0, consume);
+        if (done < count) {  // an odd tail left in the buffer
+            CUDA_CHECK(cudaMemcpy(out + done, o.p, (size_t)(count - done) * 8, cudaMemcpyDeviceToHost));
+        }
+    });
+}
+
 ihs_status ihs_gpu_mt19937_64(uint64_t stream_seed, int64_t count, uint64_t* out) {
     return guarded([&] {
         if (count <= 0) return;

@@ -212,6 +212,16 @@ def fill_gaussian(stream_seed: int, rows: int, cols: int, stddev: float = 1.0) -
     return out
 
 
+def fill_gaussian_window(stream_seed: int, first: int, count: int, stddev: float = 1.0, streamed: bool = False,
+                         block: int = 1 << 20) -> np.ndarray:
+    """Normals [first, first + count) of fill_gaussian's stream (a row shard's window of S); streamed uses the
+    chunked generator of tall Gaussian sketches."""
+    out = np.empty(count)
+    _check(lib().ihs_gpu_fill_gaussian_window(stream_seed, first, count, stddev, int(bool(streamed)), block,
+                                              abi.dptr(out)))
+    return out
+
+
 def mt19937_64(stream_seed: int, count: int) -> np.ndarray:
     out = np.empty(count, dtype=np.uint64)
     _check(lib().ihs_gpu_mt19937_64(stream_seed, count, out.ctypes.data_as(C.POINTER(C.c_uint64))))

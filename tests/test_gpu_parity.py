@@ -466,3 +466,24 @@ def test_gaussian_streamed_sketch_matches(gpu):
     env = dict(os.environ, IHS_GAUSS_STREAM="1", IHS_GAUSS_STREAM_SUBS="1", IHS_GAUSS_STREAM_COLS="64")
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600, env=env, cwd=root)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-3000:]
+
+
+@pytest.mark.parametrize("streamed", [False, True])
+def test_fill_gaussian_window(gpu, streamed):
+    """A row shard's window of the normal stream (sharded Gaussian sketch: normals [row0 m, (row0 + n_loc) m)),
+    materialised or through the chunked streamed generator, equals the slice of the full stream."""
+    import os
+    import subprocess
+    import sys
+    code = ("import numpy as np\n"
+            "from paper_2006_05874_b200 import ihs\n"
+            "full = ihs.fill_gaussian(12345, 7000000, 1, 0.5).reshape(-1)\n"
+            f"streamed = {streamed}\n"
+            "for first, count in ((0, 1000), (1, 999), (3000001, 2500000), (6999990, 10)):\n"
+            "    w = ihs.fill_gaussian_window(12345, first, count, 0.5, streamed, 4097)\n"
+            "    assert np.array_equal(w, full[first:first + count]), (first, count)\n"
+            "print('ok')\n")
+    root = str(__import__("pathlib").Path(__file__).resolve().parents[1])
+    env = dict(os.environ, IHS_GAUSS_STREAM_SUBS="1")  # 2^22-draw chunks: several per window
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600, env=env, cwd=root)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-3000:]
