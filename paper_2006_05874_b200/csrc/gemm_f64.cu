@@ -11,6 +11,8 @@
 // next K tile, deterministic split-K through a workspace (fixed-order sum).
 #include "common.cuh"
 
+#include <cstdlib>
+
 namespace ihs_b200 {
 
 namespace {
@@ -279,10 +281,15 @@ int dgemm_pick_splitk(int64_t M, int64_t N, int64_t K, int num_sms) {
         }
         return best;
     }
+    // small tile counts (the k x k products of the factor phase) split K down to IHS_SPLITK_MIN_K per split
+    static const int64_t min_k = [] {
+        const char* e = std::getenv("IHS_SPLITK_MIN_K");
+        return e ? std::max<int64_t>(16, std::atoll(e)) : int64_t{128};
+    }();
     const int64_t tiles = ceil_div(M, BM) * ceil_div(N, BN);
     const int64_t want = (int64_t)num_sms * 4;
     int s = 1;
-    while (tiles * s < want && K / (s * 2) >= 512) s *= 2;
+    while (tiles * s < want && K / (s * 2) >= min_k) s *= 2;
     return s;
 }
 
