@@ -134,11 +134,18 @@ class ClockSampler:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
                                           "--format=csv,noheader,nounits", "-lms", "100"],
                                          stdout=self.f, stderr=subprocess.DEVNULL)
+            # nvidia-smi takes a few hundred ms to start: wait for its first row so the samples cover the
+            # timed region from its start (a short region still yields only a few rows at 100 ms)
+            t_end = time.time() + 3.0
+            while time.time() < t_end and self.proc.poll() is None and self.path.stat().st_size == 0:
+                time.sleep(0.01)
         except Exception:  # noqa: BLE001
             self.proc = None
+        self.t0 = time.time()
         return self
 
     def __exit__(self, *a):
+        self.window_ms = 1e3 * (time.time() - self.t0)
         if self.proc:
             self.proc.terminate()
             try:
@@ -161,7 +168,8 @@ class ClockSampler:
         reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
         return {"sm_mhz": statistics.median(load) if load else None,
                 "sm_max_mhz": float(rows[0][2]) if rows[0][2].replace(".", "").isdigit() else None,
-                "reasons": reasons, "samples": len(rows)}
+                "reasons": reasons, "samples": len(rows), "interval_ms": 100,
+                "window_ms": round(getattr(self, "window_ms", 0.0), 1)}
 
 
 class _Null:
