@@ -17,6 +17,10 @@ from paper_2006_05874_b200 import _abi as abi
 
 HERE = pathlib.Path(__file__).resolve().parent
 LIB_PATH = HERE / "libihs_oracle.so"
+# the reference's own headers compiled against oracle/eigen_stub (oracle/Makefile `ref`; see ref_capi.cpp):
+# same entry points with the prefix ihs_ref_, loaded by oracle/ref.py through this very module
+REF_LIB_PATH = HERE / "_ref" / "libihs_ref.so"
+_PREFIX = "ihs_oracle_"
 
 _STATUS_EXC = {}
 
@@ -33,14 +37,32 @@ def build(force: bool = False) -> pathlib.Path:
     return LIB_PATH
 
 
+class _Prefixed:
+    """Maps the ihs_oracle_* names used below onto a library exporting them under another prefix."""
+
+    def __init__(self, cdll, prefix):
+        self._cdll = cdll
+        self._prefix = prefix
+
+    def __getattr__(self, name):
+        if name.startswith("ihs_oracle_"):
+            name = self._prefix + name[len("ihs_oracle_"):]
+        return getattr(self._cdll, name)
+
+
 _lib = None
 
 
 def lib():
     global _lib
     if _lib is None:
-        build()
-        L = C.CDLL(str(LIB_PATH))
+        if _PREFIX == "ihs_oracle_":
+            build()
+            L = C.CDLL(str(LIB_PATH))
+        else:
+            if not REF_LIB_PATH.exists():
+                raise OSError(f"{REF_LIB_PATH} not built (make -C {HERE} ref; needs /root/reference)")
+            L = _Prefixed(C.CDLL(str(REF_LIB_PATH)), _PREFIX)
         P = C.POINTER
         d = P(C.c_double)
         L.ihs_oracle_last_error.restype = C.c_char_p

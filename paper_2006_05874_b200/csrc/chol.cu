@@ -718,11 +718,7 @@ void cholesky_invert(const double* d_L, int64_t n, double* d_W, double* d_tmp, c
         LAUNCH_PDL(place_diag_inv_kernel, (unsigned)ceil_div(n, NB), 256, 0, st, d_Xd, n, d_W);
     } else {
         const size_t smem = (size_t)2 * NB * (NB + 1) * sizeof(double);
-        static bool attr = false;
-        if (!attr) {
-            CUDA_CHECK(cudaFuncSetAttribute(tri_inv_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            attr = true;
-        }
+        IHS_SMEM_ATTR(tri_inv_diag_kernel, (int)smem);
         static const bool old_inv = [] {
             const char* e = std::getenv("IHS_TRI_INV_OLD");
             return e && e[0] == '1';
@@ -730,12 +726,7 @@ void cholesky_invert(const double* d_L, int64_t n, double* d_W, double* d_tmp, c
         if (old_inv) LAUNCH_PDL(tri_inv_diag_kernel, (unsigned)ceil_div(n, NB), 64, smem, st, d_L, n, d_W);
         else {
             const size_t ti_smem = (size_t)3 * TI * TIP * sizeof(double);
-            static bool ti_attr = false;
-            if (!ti_attr) {
-                CUDA_CHECK(cudaFuncSetAttribute(tri_inv64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                (int)ti_smem));
-                ti_attr = true;
-            }
+            IHS_SMEM_ATTR(tri_inv64_kernel, (int)ti_smem);
             LAUNCH_PDL(tri_inv64_kernel, (unsigned)ceil_div(n, NB), 256, ti_smem, st, d_L, n, d_W);
         }
     }
@@ -784,11 +775,7 @@ void cholesky_factor(double* d_H, int64_t n, double* d_Xd, int* d_info, int num_
     (void)num_sms;
     CUDA_CHECK(cudaMemsetAsync(d_info, 0, sizeof(int), st));
     const size_t pi_smem = (size_t)(64 + 64 + 32) * PB * sizeof(double);
-    static bool attr = false;
-    if (!attr) {
-        CUDA_CHECK(cudaFuncSetAttribute(potrf_inv_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pi_smem));
-        attr = true;
-    }
+    IHS_SMEM_ATTR(potrf_inv_diag_kernel, (int)pi_smem);
     for (int64_t k = 0; k < n; k += NB) {
         const int nb = (int)std::min<int64_t>(NB, n - k);
         if (d_Xd) LAUNCH_PDL(potrf_inv_diag_kernel, 1, 128, pi_smem, st, d_H, n, k, nb, d_Xd, d_info);

@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <atomic>
 #include <cstdint>
 #include <functional>
 #include <stdexcept>
@@ -55,6 +56,21 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
         kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);                     \
         ::ihs_b200::note_launch();                                                       \
         CUDA_CHECK(cudaGetLastError());                                                  \
+    } while (0)
+
+// Opt a kernel into more than 48 KiB of dynamic shared memory. The attribute is per device, so the
+// "already set" flag is a per-call-site bit mask over device ordinals (atomic: concurrent first calls from
+// two threads both set it, which is harmless); a process that uses several devices sets it on each.
+#define IHS_SMEM_ATTR(kernel, bytes)                                                                      \
+    do {                                                                                                  \
+        static std::atomic<uint64_t> ihs_attr_mask_{0};                                                   \
+        int ihs_dev_ = 0;                                                                                 \
+        CUDA_CHECK(cudaGetDevice(&ihs_dev_));                                                             \
+        const uint64_t ihs_bit_ = 1ull << (ihs_dev_ & 63);                                                \
+        if (!(ihs_attr_mask_.load(std::memory_order_acquire) & ihs_bit_)) {                               \
+            CUDA_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(bytes))); \
+            ihs_attr_mask_.fetch_or(ihs_bit_, std::memory_order_release);                                 \
+        }                                                                                                 \
     } while (0)
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }

@@ -267,6 +267,8 @@ bool dgemm_use_big(bool transA, bool transB, int64_t M, int64_t N, int64_t K, in
                    bool lower_only) {
     return !transA && !transB && !lower_only && M >= 256 && N >= 128 && K >= 4096 && lda % 2 == 0 && ldb % 2 == 0;
 }
+// ... and its 16-byte cp.async loads need 16-byte aligned operand base pointers as well
+static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 int dgemm_pick_splitk(int64_t M, int64_t N, int64_t K, int num_sms) {
     if (dgemm_use_big(false, false, M, N, K, M + (M & 1), 2, false)) {
@@ -302,14 +304,9 @@ void dgemm(bool transA, bool transB, int64_t M, int64_t N, int64_t K, double alp
         splitk = 1;
     }
     if (splitk < 1) splitk = 1;
-    const bool big = dgemm_use_big(transA, transB, M, N, K, lda, ldb, lower_only);
+    const bool big = dgemm_use_big(transA, transB, M, N, K, lda, ldb, lower_only) && aligned16(A) && aligned16(B);
     if (big) {
-        static bool attr = false;
-        if (!attr) {
-            CUDA_CHECK(cudaFuncSetAttribute(dgemm_nn_big_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            (int)kBigSmem));
-            attr = true;
-        }
+        IHS_SMEM_ATTR(dgemm_nn_big_kernel, (int)kBigSmem);
     }
     int64_t kps = ceil_div(std::max<int64_t>(K, 1), splitk);
     kps = ceil_div(kps, BK) * BK;

@@ -404,12 +404,7 @@ template <int NRHS, int KP, int RR, int NS, int CG>
 void launch_rr(const GradPlan& p, const double* Arm, const double* b, const double* X, double* work, cudaStream_t st,
                const CandSpec& cs) {
     const size_t smem = grad_rr_smem(p.d, RR, NS);
-    static bool attr = false;
-    if (!attr) {
-        CUDA_CHECK(cudaFuncSetAttribute(grad_rr_kernel<NRHS, KP, RR, NS, CG>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-        attr = true;
-    }
+    IHS_SMEM_ATTR((grad_rr_kernel<NRHS, KP, RR, NS, CG>), 227 * 1024);
     LAUNCH_PDL((grad_rr_kernel<NRHS, KP, RR, NS, CG>), dim3(p.grid), dim3(RTHREADS), smem, st, Arm, p.d,
                p.lda / RR, b, X, work, cs);
 }
@@ -420,12 +415,7 @@ void launch_rm(const GradPlan& p, const double* Arm, const double* b, const doub
     const int maxc = (int)ceil_div(p.d, TT);
 #define IHS_RM(MC)                                                                                                  \
     do {                                                                                                            \
-        static bool attr = false;                                                                                   \
-        if (!attr) {                                                                                                \
-            CUDA_CHECK(cudaFuncSetAttribute(grad_rm_kernel<NRHS, RR, MC, NS>,                                       \
-                                            cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));              \
-            attr = true;                                                                                            \
-        }                                                                                                           \
+        IHS_SMEM_ATTR((grad_rm_kernel<NRHS, RR, MC, NS>), 227 * 1024);                                                                                                           \
         LAUNCH_PDL((grad_rm_kernel<NRHS, RR, MC, NS>), p.grid, TT, smem, st, Arm, p.d, p.lda / RR, b, X, work);         \
     } while (0)
     if (maxc <= 1) IHS_RM(1);

@@ -246,12 +246,7 @@ void launch_tma(const GradPlan& p, const double* b, const double* X, double* wor
     const CUtensorMap* map = reinterpret_cast<const CUtensorMap*>(p.tmap);
 #define IHS_TMA(MC)                                                                                                 \
     do {                                                                                                            \
-        static bool attr = false;                                                                                   \
-        if (!attr) {                                                                                                \
-            CUDA_CHECK(cudaFuncSetAttribute(grad_tma_kernel<NRHS, RR, MC, NS>,                                      \
-                                            cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));              \
-            attr = true;                                                                                            \
-        }                                                                                                           \
+        IHS_SMEM_ATTR((grad_tma_kernel<NRHS, RR, MC, NS>), 227 * 1024);                                                                                                           \
         LAUNCH_PDL((grad_tma_kernel<NRHS, RR, MC, NS>), p.grid, TT, smem, st, *map, p.d, p.lda / RR, b, X, work);       \
     } while (0)
     if (maxc <= 1) IHS_TMA(1);

@@ -260,12 +260,7 @@ void launch_v2(const GradPlan& p, const double* A, const double* b, const double
     const int maxc = (int)ceil_div(p.d, T2);
 #define IHS_V2(MC)                                                                                                  \
     do {                                                                                                            \
-        static bool attr = false;                                                                                   \
-        if (!attr) {                                                                                                \
-            CUDA_CHECK(cudaFuncSetAttribute(grad_smem_kernel<NRHS, RR, MC, NS>,                                     \
-                                            cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));              \
-            attr = true;                                                                                            \
-        }                                                                                                           \
+        IHS_SMEM_ATTR((grad_smem_kernel<NRHS, RR, MC, NS>), 220 * 1024);                                                                                                           \
         LAUNCH_PDL((grad_smem_kernel<NRHS, RR, MC, NS>), p.grid, T2, smem, st, A, p.d, p.lda, b, X, work);              \
     } while (0)
     if (maxc <= 1) IHS_V2(1);
@@ -418,12 +413,8 @@ void grad_run(const GradPlan& p, const double* d_A, const double* d_b, double nu
         return;
     }
     const size_t smem = grad_smem(p.d, nrhs);
-    static bool attr = false;
-    if (!attr) {
-        CUDA_CHECK(cudaFuncSetAttribute(grad_partial_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-        CUDA_CHECK(cudaFuncSetAttribute(grad_partial_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-        attr = true;
-    }
+    IHS_SMEM_ATTR((grad_partial_kernel<1>), 220 * 1024);
+    IHS_SMEM_ATTR((grad_partial_kernel<2>), 220 * 1024);
     if (nrhs == 1)
         LAUNCH_PDL(grad_partial_kernel<1>, p.grid, THREADS, smem, st, d_A, p.n, p.d, p.lda, d_b, d_X, d_work);
     else

@@ -501,7 +501,9 @@ void device_sketch(ihs_gpu_problem* P, int kind, int64_t m, uint64_t seed, doubl
             ensure_A(P);
             int64_t col_done = 0;
             auto consume = [&](int64_t base, int64_t ready) -> int64_t {
-                const int64_t ncols = std::min<int64_t>(ready / m, n - col_done);
+                int64_t ncols = std::min<int64_t>(ready / m, n - col_done);
+                // an even column count keeps the next block's A operand (A + col_done) 16-byte aligned
+                if (col_done + ncols < n) ncols &= ~int64_t{1};
                 if (ncols <= 0) return 0;
                 const int splitk = dgemm_pick_splitk(m, d, ncols, P->num_sms);
                 if (splitk > 1) P->gemm_work.ensure((size_t)splitk * m * d * sizeof(double));
@@ -696,6 +698,13 @@ void problem_grad(ihs_gpu_problem* P, const double* X, int nrhs, double* G, cons
 // read-backs of the device state (B ~ 256 MB of A traffic per batch, 1..16); a batch that passes the
 // stopping point only runs no-op recurrence kernels after it (their H p passes are wasted work, not
 // a change of result). Counters follow the reference's analytic formulas (baselines.hpp:51,117,120).
+// Rows of the largest shard: the same on every rank of a sharded problem (n for a single GPU).
+// Host-side plans that change the number of collectives a rank issues must be derived from this.
+int64_t shard_rows_max(const ihs_gpu_problem* P) {
+    if (P->opts.world_size <= 1) return P->n;
+    return ihs_next_pow2(P->opts.n_global) / P->opts.world_size;
+}
+
 void cg_run(ihs_gpu_problem* P, const ihs_gpu_system* S, double tol, int64_t max_iters, const double* x0,
             ihs_cg_report* rep, ihs_counters& C) {
     const int64_t d = P->d, n = P->n;
@@ -703,7 +712,9 @@ void cg_run(ihs_gpu_problem* P, const ihs_gpu_system* S, double tol, int64_t max
     const bool pcg = S != nullptr;
     const uint64_t nn = (uint64_t)(P->opts.world_size > 1 ? P->opts.n_global : n), dd = (uint64_t)d;
     const uint64_t hv_count = 2 * nn * dd + 2 * dd, minv_count = 2 * dd * dd;
-    const double pass_bytes = 8.0 * (double)n * (double)d;
+    // B must agree on every rank (each H p pass all-reduces): size it from the largest shard's rows,
+    // a rank-invariant value, not from this rank's own row count
+    const double pass_bytes = 8.0 * (double)shard_rows_max(P) * (double)d;
     const int64_t B = std::max<int64_t>(1, std::min<int64_t>(16, (int64_t)(256e6 / std::max(pass_bytes, 1.0))));
     if (!P->zb_ready) {
         P->zb.ensure((size_t)P->lda * sizeof(double));
@@ -1542,16 +1553,15 @@ ihs_status ihs_gpu_fill_gaussian_window(uint64_t stream_seed, int64_t first, int
         scratch.ensure(gaussian_stream_scratch_bytes());
         int64_t done = 0;
         auto consume = [&](int64_t base, int64_t ready) -> int64_t {
-            const int64_t use = ready & ~int64_t{1};  // any even prefix: the window is not column-structured here
+            // any even prefix (the window is not column-structured here); the window's end is taken whole
+            const int64_t use = base + ready >= first + count ? ready : (ready & ~int64_t{1});
             if (use <= 0) return 0;
             CUDA_CHECK(cudaMemcpy(out + (base - first), o.p, (size_t)use * 8, cudaMemcpyDeviceToHost));
             done += use;
             return use;
         };
         mt_gaussian_stream(stream_seed, first, count, stddev, o.d(), cap, block, scratch.p, 0, consume);
-        if (done < count) {  // an odd tail left in the buffer
-            CUDA_CHECK(cudaMemcpy(out + done, o.p, (size_t)(count - done) * 8, cudaMemcpyDeviceToHost));
-        }
+        if (done != count) fail(IHS_INTERNAL_ERROR, "fill_gaussian: incomplete window");
     });
 }
 
@@ -1857,7 +1867,9 @@ void adaptive_solve_impl(ihs_gpu_problem* P, const ihs_solver_config* cfg, ihs_s
         // Speculation: while the host waits for evaluation t, the evaluation of t+1 under the predicted
         // outcome (the previous accepted candidate kind) is already queued, hiding the host round trip.
         // Only for cheap passes over A (a wasted evaluation costs one pass) and only after an accept.
-        const bool cheap_pass = grad_pass_bytes < (double)(1ll << 30);
+        // rank-invariant (every speculative evaluation all-reduces its gradient partials, so all ranks must
+        // speculate alike): decided from the largest shard's rows, not this rank's own row count
+        const bool cheap_pass = 8.0 * (double)shard_rows_max(P) * (double)(dim + 1) < (double)(1ll << 30);
         int cur = 0;        // set holding the evaluation for the current state
         int spec = -1;      // set holding a speculative evaluation (or -1)
         int spec_slot = -1; // candidate slot the speculation assumed accepted

@@ -925,12 +925,7 @@ template <int HB, int TH>
 void launch_pass(const SrhtPlan& p, double* T, int lo, const int4* tiles, int n_tiles, bool emit, const int2* entries,
                  double* SA, cudaStream_t st) {
     const size_t smem = (size_t)pad32((int)pass_tile_elems(HB, TH)) * sizeof(double) + 64;
-    static bool attr = false;
-    if (!attr) {
-        CUDA_CHECK(cudaFuncSetAttribute(srht_phase2_kernel<HB, TH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)smem));
-        attr = true;
-    }
+    IHS_SMEM_ATTR((srht_phase2_kernel<HB, TH>), (int)smem);
     const int64_t tiles_per_col = p.n_pad / pass_tile_elems(HB, TH);
     const unsigned gx = emit ? (unsigned)n_tiles : (unsigned)tiles_per_col;
     if (gx == 0) return;
@@ -1010,12 +1005,7 @@ template <int HB>
 void launch_stream(const SrhtPlan& p, const ChunkMaps& maps, int64_t nfull, const double* A, const uint32_t* signbits,
                    double* T, int G, int nslot, const int4* tiles, int n_tiles, const int2* entries, double* SA,
                    int* ctl, int grid, const uint32_t* mask, int logw, cudaStream_t st) {
-    static bool attr = false;
-    if (!attr) {
-        CUDA_CHECK(cudaFuncSetAttribute(srht_stream_kernel<HB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)kStreamSmem));
-        attr = true;
-    }
+    IHS_SMEM_ATTR((srht_stream_kernel<HB>), (int)kStreamSmem);
     const int ng = (int)ceil_div(p.d, G);
     CUDA_CHECK(cudaMemsetAsync(ctl, 0, 2 * sizeof(int) * (size_t)ng, st));
     // IHS_SRHT_STREAM_PROF=1: per-role cycle accounting of the pipeline (debug, prints to stderr)
@@ -1316,34 +1306,20 @@ void srht_run_device(const SrhtPlan& p, const double* d_A, const uint32_t* d_sig
     const bool masked = p.npass == 1 && d_mask != nullptr && !p.compact;
     const int logw = masked ? pass_logw(p) : 0;
     if (nfull > 0 && srht_chunk_maps(d_A, p.lda, nfull, p.d, &maps)) {
-        static bool attr = false;
-        if (!attr) {
-            CUDA_CHECK(cudaFuncSetAttribute(srht_phase1_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            (int)kP1TSmem));
-            attr = true;
-        }
+        IHS_SMEM_ATTR(srht_phase1_tma_kernel, (int)kP1TSmem);
         const int64_t blocks = std::min<int64_t>(ceil_div(total, kP1TWarps), (int64_t)num_sms);
         LAUNCH_PDL(srht_phase1_tma_kernel, (unsigned)blocks, 32 * kP1TWarps, kP1TSmem, st, maps, d_A, p.n, p.lda,
                d_signbits, d_T, p.n_pad, p.logn - kChunkL, nfull, total, masked ? d_mask : nullptr, logw, lmap, U);
     } else {
         const int64_t blocks = std::min<int64_t>(ceil_div(total, kP1AWarps), (int64_t)num_sms);
         const size_t smem = (size_t)kP1AWarps * 2 * kP1Buf * sizeof(double);
-        static bool attr = false;
-        if (!attr) {
-            CUDA_CHECK(cudaFuncSetAttribute(srht_phase1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            attr = true;
-        }
+        IHS_SMEM_ATTR(srht_phase1_kernel, (int)smem);
         LAUNCH_PDL(srht_phase1_kernel, (unsigned)blocks, 32 * kP1AWarps, smem, st, d_A, p.n, p.lda, d_signbits, d_T,
                p.n_pad, p.logn - kChunkL, total, masked ? d_mask : nullptr, logw, lmap, U);
     }
     if (p.compact) {
         constexpr size_t smem = (size_t)kCmpU * kCmpRow * sizeof(double);
-        static bool attr = false;
-        if (!attr) {
-            CUDA_CHECK(cudaFuncSetAttribute(srht_phase2_compact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            (int)smem));
-            attr = true;
-        }
+        IHS_SMEM_ATTR(srht_phase2_compact_kernel, (int)smem);
         if (U > 0)
             LAUNCH_PDL(srht_phase2_compact_kernel, dim3((unsigned)ceil_div(U, kCmpU), (unsigned)p.d), 256, smem, st,
                        (const double*)d_T, U, d_tiles, d_entries, p.scale1, p.scale2, d_SA, p.m);

@@ -6,6 +6,8 @@
 // repeated solves are bit-identical.
 #include "common.cuh"
 
+#include <mutex>
+
 namespace ihs_b200 {
 
 namespace {
@@ -331,10 +333,16 @@ void symv_col(const double* H, int64_t k, const double* x, int nrhs, int64_t ldx
     const unsigned grid = (unsigned)ceil_div(k, SV_W);
     double* part = (size_t)4 * grid <= front ? work : tail + ceil_div(k, GV_ROWS) + 8;
     const size_t smem = (size_t)nrhs * k * sizeof(double);
-    static int attr_bytes = 48 * 1024;
-    if ((int)smem > attr_bytes) {
-        CUDA_CHECK(cudaFuncSetAttribute(symv_col_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr_bytes = (int)smem;
+    if (smem > 48 * 1024) {  // opt in per device, raised to the largest request seen on that device
+        static std::mutex mu;
+        static int attr_bytes[64] = {};
+        int dev = 0;
+        CUDA_CHECK(cudaGetDevice(&dev));
+        std::lock_guard<std::mutex> lock(mu);
+        if ((int)smem > attr_bytes[dev & 63]) {
+            CUDA_CHECK(cudaFuncSetAttribute(symv_col_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            attr_bytes[dev & 63] = (int)smem;
+        }
     }
     LAUNCH_PDL(symv_col_kernel, dim3(grid), dim3(32 * SV_W), smem, st, H, k, x, nrhs, ldx, y, ldy, dots, part,
                counter);

@@ -22,6 +22,22 @@ def O():
 
 
 @pytest.fixture(scope="session")
+def R():
+    """The reference's own headers compiled against oracle/eigen_stub (oracle/_ref/libihs_ref.so). Built here
+    from /root/reference (make -C oracle ref); elsewhere the prebuilt library that travels with the repo."""
+    import pathlib
+    import subprocess
+
+    from oracle import ref
+
+    if pathlib.Path("/root/reference/proj/include/ihs").is_dir():
+        subprocess.run(["make", "-s", "-C", str(pathlib.Path(ROOT) / "oracle"), "ref"], check=True)
+    elif not ref.REF_LIB_PATH.exists():
+        pytest.skip("oracle/_ref not built and /root/reference absent")
+    return ref
+
+
+@pytest.fixture(scope="session")
 def ihs():
     from paper_2006_05874_b200 import ihs as m
 

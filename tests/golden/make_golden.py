@@ -1,12 +1,15 @@
 #!/usr/bin/env python3
-"""Generate the golden fixtures of tests/golden/ from the pinned CPU oracle.
+"""Generate the golden fixtures of tests/golden/ from the REFERENCE ITSELF.
 
-The reference ships no stored vectors for the hot path; these are
-produced by the oracle (oracle/ihs_oracle.cpp, libstdc++ 13.3 RNG types) in
-this container and committed, so the GPU box can check the CUDA path against
-fixed bytes even without rebuilding the oracle.
+The reference ships no stored vectors for the hot path. These are
+produced in this container by oracle/_ref/libihs_ref.so — the reference's own
+headers (/root/reference/proj/include/ihs/*.hpp) compiled unchanged against
+the Eigen-API subset in oracle/eigen_stub (`make -C oracle ref`, libstdc++ 13.3
+RNG types) — and committed, so the GPU box (where /root/reference does not
+exist) checks the CUDA path and the oracle restatement against the reference's
+bytes. tests/test_golden.py holds the oracle to them as well.
 
-    python tests/golden/make_golden.py   # rewrites tests/golden/golden.npz
+    make -C oracle ref && python tests/golden/make_golden.py   # rewrites tests/golden/golden.npz
 """
 import pathlib
 import sys
@@ -16,11 +19,13 @@ import numpy as np
 HERE = pathlib.Path(__file__).resolve().parent
 sys.path.insert(0, str(HERE.parents[1]))
 
-from oracle import oracle as O  # noqa: E402
+from oracle import ref as O  # noqa: E402  (the reference code; same signatures as oracle/oracle.py)
 
 
 def main():
-    out = {}
+    if not O.AVAILABLE:
+        raise SystemExit("oracle/_ref/libihs_ref.so missing: run `make -C oracle ref` (needs /root/reference)")
+    out = {"generator": np.array("oracle/_ref: reference headers proj/include/ihs/*.hpp + oracle/eigen_stub")}
     # raw streams and the derived D / P of a few sub-seeds (rng.hpp:30-66)
     for i, (seed, K) in enumerate([(0, 0), (0, 5), (12345, 11)]):
         sub = O.derive_seed(seed, K)
