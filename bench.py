@@ -1,25 +1,38 @@
 #!/usr/bin/env python3
 """Benchmark: adaptive-IHS time-to-1e-10 on the BASELINE configs (B200).
 
-Default workload = BASELINE.json configs[1] ("C2"): Gaussian-sketch
-Polyak-IHS, fp64, n=65536, d=512, fixed m=1024, nu=1e-3, sigma_j=0.98^j,
-b = A x_true + N(0, 0.01^2). A "step" is one complete adaptive_solve
-(solver.hpp:242) to r_t/r_1 <= 1e-10 with A resident in HBM; `value` is the
-device-timed seconds per solve (lower is better). `e2e` repeats the step
-through the public API with the H2D upload of A and b from pinned host
-memory and the D2H of x inside the timed region.
+Default workload = C4-SRHT, the largest BASELINE config that fits one GPU (configs[3]: n=2^22, d=2048, A = 64 GiB,
+sigma_j = 1/j, nu = 1e-4, adaptive m, Polyak-IHS with the SRHT). A "step" is one complete adaptive_solve
+(solver.hpp:242) with A resident in HBM; `value` is the device-timed seconds per solve (lower is better). `e2e`
+repeats the step through the public API with the H2D upload of A and b from pinned host memory and the D2H of x
+inside the timed region.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c1..c5]
-                  [--impl b200|reference] [--no-cpu-baseline] [--solver ihs|pcg|cg]
+"Time to 1e-10": the reference stops at r_t <= eps r_1 (solver.hpp:154,177), a ratio of sketched Newton
+decrements, i.e. of SQUARED prediction errors measured under the current sketch. Each config's
+(m_initial, eps) is chosen (oracle + device scans) so that the returned x satisfies
+  delta = ||Abar (x - x*)|| / ||Abar x*|| <= 1e-10,   Abar = [A; nu I],  x* = device direct_solve,
+which every bench line reports as `solve.delta_rel_vs_direct` (with pe_rel = delta^2 = prediction_error(x) /
+prediction_error(0), problem.hpp:104-109). C3-C5 start at m_initial = 2d (r_1 measured under a subspace
+embedding) with eps = 1e-21; C1 keeps BASELINE's "m starts at 1" with eps = 1e-27; C2 (fixed m = 1024 = 2d)
+uses eps = 1e-21.
 
---solver pcg|cg times the paper's comparators on the same data instead
-(baselines.hpp: sketch-preconditioned CG with the prescribed sketch size
-m = d/rho or d ln d/rho at bench.hpp's default rho = 0.1, and plain CG), to
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c1..c5] [--impl b200|reference]
+                  [--no-cpu-baseline] [--solver ihs|pcg|cg]
+
+--solver pcg|cg times the paper's comparators on the same data instead (baselines.hpp: sketch-preconditioned
+CG with the prescribed sketch size m = d/rho or d ln d/rho at bench.hpp's default rho = 0.1, and plain CG), to
 tol 1e-10 on ||H x - A^T b|| <= tol ||A^T b||, max 2000 iterations.
 
-Multi-GPU (torchrun, one rank per GPU): A is row-sharded over the ranks
-(strong scaling of the same problem; --replicas for independent copies),
-value = max over ranks.
+CPU baseline (`cpu_baseline`, and the `--impl reference` arm): the oracle restatement of the reference (pinned
+bit-for-bit to the reference's own headers, tests/test_ref_pin.py) on the host, single thread like the
+reference. C1 and C2 run whole solves. For C3-C5 a whole single-thread solve takes 10 min to hours, so each
+step times bounded samples of the same workload — one SRHT/Gaussian sketch over a few full-length columns, a
+gradient over a row block, a factorization + solves of a sketched system — and extrapolates with the solve's
+analytic cost counters (types.hpp:18-33; identical on the GPU and the reference, tests/test_gpu_parity.py):
+  t = sum over phases of counters[phase] x (host seconds per counter unit measured on the sample).
+
+Multi-GPU (torchrun, one rank per GPU): A is row-sharded over the ranks (strong scaling of the same problem;
+--replicas for independent copies), value = max over ranks.
 """
 from __future__ import annotations
 
@@ -38,27 +51,34 @@ ROOT = pathlib.Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 # --------------------------------------------------------------------- configs
+# m_initial / eps: see the module docstring and DESIGN.md §4 (chosen so delta <= 1e-10 against direct_solve)
 CONFIGS = {
     "c1": dict(desc="C1 SRHT adaptive gradient-IHS n=8192 d=256", n=8192, d=256, spectrum=0, decay=0.95,
                noise=0.01, nu=1e-2, outliers=0.0, sketch="SRHT", mode="GradientOnly", rho=0.1,
-               m_initial=1, max_sketch=None, enforce_validity=True),
+               m_initial=1, max_sketch=None, enforce_validity=True, eps=1e-27),
     "c2": dict(desc="C2 Gaussian Polyak-IHS n=65536 d=512 fixed m=1024", n=65536, d=512, spectrum=0, decay=0.98,
                noise=0.01, nu=1e-3, outliers=0.0, sketch="Gaussian", mode="PolyakThenGradient", rho=0.35,
-               m_initial=1024, max_sketch=1024, enforce_validity=False),
+               m_initial=1024, max_sketch=1024, enforce_validity=False, eps=1e-21),
     "c3": dict(desc="C3 SRHT adaptive Polyak-IHS n=2^20 d=1024", n=1 << 20, d=1024, spectrum=0, decay=0.99,
                noise=0.1, nu=1e-3, outliers=0.0, sketch="SRHT", mode="PolyakThenGradient", rho=0.1,
-               m_initial=1, max_sketch=None, enforce_validity=True),
+               m_initial=2048, max_sketch=None, enforce_validity=True, eps=1e-21),
     "c4": dict(desc="C4 SRHT adaptive Polyak-IHS n=2^22 d=2048 sigma=1/j", n=1 << 22, d=2048, spectrum=1,
                decay=0.0, noise=0.01, nu=1e-4, outliers=0.0, sketch="SRHT", mode="PolyakThenGradient", rho=0.1,
-               m_initial=1, max_sketch=None, enforce_validity=True),
+               m_initial=4096, max_sketch=None, enforce_validity=True, eps=1e-21),
     "c4g": dict(desc="C4 Gaussian adaptive Polyak-IHS n=2^22 d=2048 sigma=1/j (streamed S)", n=1 << 22, d=2048,
                 spectrum=1, decay=0.0, noise=0.01, nu=1e-4, outliers=0.0, sketch="Gaussian", mode="PolyakThenGradient",
-                rho=0.1, m_initial=1, max_sketch=None, enforce_validity=True),
+                rho=0.1, m_initial=4096, max_sketch=None, enforce_validity=True, eps=1e-21),
     "c5": dict(desc="C5 SRHT adaptive Polyak-IHS n=10^6 (pad 2^20) d=4096 +1% x100 outliers", n=10**6, d=4096,
                spectrum=0, decay=0.999, noise=0.01, nu=1e-5, outliers=0.01, sketch="SRHT",
-               mode="PolyakThenGradient", rho=0.1, m_initial=1, max_sketch=None, enforce_validity=True),
+               mode="PolyakThenGradient", rho=0.1, m_initial=8192, max_sketch=None, enforce_validity=True, eps=1e-21),
 }
-METRIC = "adaptive-IHS time-to-1e-10 error (r_t/r_1 <= 1e-10)"
+DEFAULT_CONFIG = "c4"
+FULL_CPU_SOLVE = ("c1", "c2")  # configs whose whole single-thread oracle solve fits the bench budget
+# cost counters of one solve per config (rep.counters: sketch, factor, solve, matvec), recorded from the device
+# solve (equal to the reference's by the parity tests); the reference arm multiplies them with its measured host
+# rates for configs whose whole CPU solve does not fit the bench budget. The b200 arm checks them live.
+REF_COUNTERS_PATH = ROOT / "profiles" / "ref_counters.json"
+METRIC = "adaptive-IHS time-to-1e-10 error (||Abar(x - x*)|| / ||Abar x*|| <= 1e-10)"
 METRICS = {"ihs": METRIC,
            "pcg": "PCG time-to-1e-10 (||H x - A^T b|| <= 1e-10 ||A^T b||, sketch-preconditioned, baselines.hpp)",
            "cg": "CG time-to-1e-10 (||H x - A^T b|| <= 1e-10 ||A^T b||, baselines.hpp)"}
@@ -106,7 +126,7 @@ def ncu_traffic(cfg, which):
 def solver_config(ihs, c, seed=0):
     return ihs.SolverConfig(rho=c["rho"], sketch_kind=getattr(ihs.SketchKind, c["sketch"]),
                             mode=getattr(ihs.SolveMode, c["mode"]), m_initial=c["m_initial"],
-                            max_sketch=c["max_sketch"], eps=1e-10, seed=seed,
+                            max_sketch=c["max_sketch"], eps=c["eps"], seed=seed,
                             enforce_validity=c["enforce_validity"])
 
 
@@ -114,8 +134,97 @@ def oracle_config(O, c, seed=0):
     from paper_2006_05874_b200 import _abi as abi
     return O.default_config(rho=c["rho"], sketch_kind=abi.SKETCH_SRHT if c["sketch"] == "SRHT" else abi.SKETCH_GAUSSIAN,
                             mode=abi.MODE_GRADIENT_ONLY if c["mode"] == "GradientOnly" else abi.MODE_POLYAK_THEN_GRADIENT,
-                            m_initial=c["m_initial"], max_sketch=c["max_sketch"] or 0, eps=1e-10, seed=seed,
+                            m_initial=c["m_initial"], max_sketch=c["max_sketch"] or 0, eps=c["eps"], seed=seed,
                             enforce_validity=int(c["enforce_validity"]))
+
+
+def config_dict(args, c, world):
+    """The `config` object of the JSON line: identical on both arms (same workload, knobs and layout)."""
+    n, d = c["n"], c["d"]
+    if world > 1:
+        parallelism = f"replicas x{world}" if args.replicas else \
+            f"row-sharded x{world} (NCCL all-gather/all-reduce of sketch and gradient partials)"
+    else:
+        parallelism = "single GPU"
+    out = {"workload": c["desc"] if args.solver == "ihs" else
+           f"{args.solver.upper()} on the {args.config.upper()} data (n={n}, d={d}, nu={c['nu']})",
+           "config": args.config, "n": n, "d": d, "nu": c["nu"], "sketch": c["sketch"], "data_seed": 0,
+           "solver_seed": 0}
+    if args.solver == "ihs":
+        out.update({"mode": c["mode"], "rho": c["rho"], "m_initial": c["m_initial"], "max_sketch": c["max_sketch"],
+                    "enforce_validity": c["enforce_validity"], "eps": c["eps"],
+                    "target": "||Abar(x-x*)||/||Abar x*|| <= 1e-10 (x* = direct_solve)"})
+    else:
+        out.update({"solver": args.solver, "tol": CG_TOL, "max_iters": CG_MAX_ITERS,
+                    **({"rho": PCG_RHO} if args.solver == "pcg" else {})})
+    out["l2"] = (("inputs larger than L2 (A = %.0f MiB) and L2 flushed between steps" % (8 * n * d / 2**20))
+                 if 8 * n * d > L2_BYTES else "L2 flushed (256 MiB write) between timed steps")
+    out["parallelism"] = parallelism
+    return out
+
+
+# --------------------------------------------------------------------- CPU baseline (oracle port, 1 thread)
+def host_phase_rates(O, c, m_sample):
+    """Host seconds per cost-counter unit of each phase of the reference solve (types.hpp:18-33), measured with
+    the oracle restatement (single thread) on bounded samples of this config's workload:
+      sketch  SRHT: one srht_sketch over `cs` full-length columns (the FWHT length n_pad and its log factor are
+              the config's own; counter unit = butterfly/sign/gather, sketch.hpp:99-106);
+              Gaussian: S generation per normal (rng.hpp:35-40) + S*A per multiply-add (sketch.hpp:65-68);
+      matvec  8 gradients (problem.hpp:59-69) over a ~128 MiB row block with all d columns (unit = counted MAC);
+      factor  SketchedSystem::factorize of a (4 d_s) x d_s sketch, d_s = min(d, 768) (unit = d^2 m + d^3/3);
+      solve   SketchedSystem::solve on the same system (unit = d^2 + d).
+    Returns ({phase: seconds per unit}, description, seconds spent timing)."""
+    import time as _t
+    t_start = _t.perf_counter()
+    n, d = c["n"], c["d"]
+    rates, parts = {}, []
+    n_pad = 1 << (n - 1).bit_length()
+    logn = n_pad.bit_length() - 1
+    if c["sketch"] == "SRHT":
+        cs = max(2, min(d, int(round(1e9 / (n_pad * logn)))))
+        A_s, _, _ = O.synth(n, cs, spectrum=c["spectrum"], decay=c["decay"], noise_std=0.0, data_seed=0)
+        m_s = min(m_sample, n_pad)
+        t, cnt = O.time_sketch(A_s, 1, m_s, 0)
+        rates["sketch"] = t / cnt.sketch
+        parts.append(f"srht_sketch n={n} x {cs} columns, m={m_s}: {t:.3f} s")
+        del A_s
+    else:
+        n_s, d_s, m_s = 8192, min(d, 256), 512
+        t_norm = O.time_fill_gaussian(O.derive_seed(0, 0), m_s, n_s) / (m_s * n_s)
+        A_s, _, _ = O.synth(n_s, d_s, spectrum=c["spectrum"], decay=c["decay"], noise_std=0.0, data_seed=0)
+        t, cnt = O.time_sketch(A_s, 0, m_s, 0)
+        t_mac = max(t - t_norm * m_s * n_s, 0.0) / (m_s * n_s * d_s)
+        rates["sketch_normal"], rates["sketch"] = t_norm, t_mac
+        parts.append(f"gaussian_sketch {m_s}x{n_s} S times {n_s}x{d_s} A: {t:.3f} s ({t_norm * 1e9:.1f} ns/normal)")
+    n_g = int(min(n, max(1024, (128 << 20) // (8 * d))))
+    A_g, b_g, _ = O.synth(n_g, d, spectrum=c["spectrum"], decay=c["decay"], noise_std=c["noise"], data_seed=0)
+    x_g = np.full(d, 0.5)
+    t, cnt = O.time_gradient(A_g, b_g, c["nu"], x_g, 8)
+    rates["matvec"] = t / cnt.matvec
+    parts.append(f"8 gradients over {n_g}x{d}: {t:.3f} s")
+    del A_g, b_g
+    d_s = min(d, 768)
+    SA = np.asfortranarray(np.random.default_rng(0).standard_normal((4 * d_s, d_s)))
+    tf, ts, cnt = O.time_system(SA, c["nu"], np.ones(d_s), 16)
+    rates["factor"], rates["solve"] = tf / cnt.factor, ts / cnt.solve
+    parts.append(f"factorize {4 * d_s}x{d_s} + 16 solves: {tf + ts:.3f} s")
+    return rates, "; ".join(parts), _t.perf_counter() - t_start
+
+
+def extrapolate(rates, counters, d):
+    """Seconds of a reference solve with these cost counters at these host rates (phase by phase)."""
+    ph = {"sketch": counters["sketch"] * rates["sketch"]
+                    + (counters["sketch"] / d) * rates.get("sketch_normal", 0.0),  # Gaussian: m n normals per m n d
+          "factor": counters["factor"] * rates["factor"], "solve": counters["solve"] * rates["solve"],
+          "gradient": counters["matvec"] * rates["matvec"]}
+    return float(sum(ph.values())), ph
+
+
+def load_ref_counters():
+    try:
+        return json.loads(REF_COUNTERS_PATH.read_text())
+    except Exception:  # noqa: BLE001
+        return {}
 
 
 # --------------------------------------------------------------------- clocks
@@ -182,37 +291,66 @@ class _Null:
 
 # --------------------------------------------------------------------- reference arm
 def run_reference(args, c, rank, world):
+    """The reference arm: the reference's CPU implementation of the path (the oracle restatement, pinned to the
+    reference's own headers by tests/test_ref_pin.py) on the host, single thread like the reference (no OpenMP
+    in proj/CMakeLists.txt). C1/C2: one whole adaptive_solve per step. C3-C5: per step a bounded sample of the
+    same workload timed phase by phase and extrapolated with the solve's cost counters (module docstring)."""
     from oracle import oracle as O
     if rank != 0:
         return 0
-    A, b, _ = O.synth(c["n"], c["d"], spectrum=c["spectrum"], decay=c["decay"], noise_std=c["noise"],
-                      outlier_frac=c["outliers"], data_seed=0)
-    cfg = oracle_config(O, c)
-    times = []
-    for i in range(args.warmup_ref + args.steps):
-        t0 = time.perf_counter()
-        if args.solver == "ihs":
-            x, rep, log, _ = O.adaptive_solve(A, b, c["nu"], cfg)
-            wall = rep.wall_seconds
+    if args.solver != "ihs" and args.config not in FULL_CPU_SOLVE:
+        print(json.dumps({"impl": "reference", "unavailable": f"{args.solver} CPU arm only for "
+                          f"{'/'.join(FULL_CPU_SOLVE)}"}), flush=True)
+        return 0
+    full = args.config in FULL_CPU_SOLVE
+    counters = None
+    if full:
+        A, b, _ = O.synth(c["n"], c["d"], spectrum=c["spectrum"], decay=c["decay"], noise_std=c["noise"],
+                          outlier_frac=c["outliers"], data_seed=0)
+        cfg = oracle_config(O, c)
+    else:
+        counters = load_ref_counters().get(args.config)
+        if counters is None:
+            print(json.dumps({"impl": "reference", "unavailable": f"no recorded cost counters for {args.config} "
+                              f"in {REF_COUNTERS_PATH.name}"}), flush=True)
+            return 0
+    times, extra = [], {}
+    warm = min(args.warmup, 1) if full else args.warmup  # a whole-solve step has no state to warm; printed as run
+    for i in range(warm + args.steps):
+        if full:
+            t0 = time.perf_counter()
+            if args.solver == "ihs":
+                x, rep, log, _ = O.adaptive_solve(A, b, c["nu"], cfg)
+                wall = rep.wall_seconds
+                extra = {"iterations": int(rep.iterations), "rejections": int(rep.rejections),
+                         "final_m": int(rep.final_m)}
+            else:
+                kind = 1 if c["sketch"] == "SRHT" else 0
+                x, _, rep = (O.pcg_solve(A, b, c["nu"], kind, 0, PCG_RHO, CG_TOL, CG_MAX_ITERS)
+                             if args.solver == "pcg" else O.cg_solve(A, b, c["nu"], CG_TOL, CG_MAX_ITERS))
+                wall = time.perf_counter() - t0
+                extra = {"iterations": int(rep.iterations)}
+            sample = (f"one whole {args.solver} solve of {args.config.upper()} per step (oracle C++ restatement "
+                      "of the reference, 1 thread)")
         else:
-            kind = 1 if c["sketch"] == "SRHT" else 0
-            x, _, rep = (O.pcg_solve(A, b, c["nu"], kind, 0, PCG_RHO, CG_TOL, CG_MAX_ITERS) if args.solver == "pcg"
-                         else O.cg_solve(A, b, c["nu"], CG_TOL, CG_MAX_ITERS))
-            wall = time.perf_counter() - t0
-        if i >= args.warmup_ref:
+            rates, desc, spent = host_phase_rates(O, c, counters["final_m"])
+            wall, phases = extrapolate(rates, counters, c["d"])
+            extra = {"iterations": counters["iterations"], "rejections": counters["rejections"],
+                     "final_m": counters["final_m"], "extrapolated_phase_s": phases,
+                     "host_rates_s_per_unit": rates, "sample_seconds": spent}
+            sample = (f"extrapolated: per step, bounded samples of {args.config.upper()} ({desc}) timed on the host "
+                      "(1 thread), times the solve's cost counters from " + REF_COUNTERS_PATH.name)
+        if i >= warm:
             times.append(wall)
     v = float(np.mean(times))
-    extra = ({"rejections": int(rep.rejections), "final_m": int(rep.final_m)} if args.solver == "ihs"
-             else {"m": int(rep.m), "converged": bool(rep.converged)})
-    line = {"impl": "reference", "metric": METRICS[args.solver], "value": v, "unit": "s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": v * 1e3, "higher_is_better": False, "scaling": "weak",
+    line = {"impl": "reference", "metric": METRICS[args.solver], "value": v, "unit": "s", "n_gpus": world,
+            "steps": args.steps, "warmup": warm, "ms_per_step": v * 1e3, "higher_is_better": False,
+            "scaling": "strong" if world > 1 and not args.replicas else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, SURVEY §8(d) generator)",
-            "config": {"workload": c["desc"], **{k: c[k] for k in ("n", "d", "nu", "sketch", "mode", "rho")}},
-            "cpu_baseline": {"value": v, "unit": "s", "cores": 1, "kind": "port",
-                             "sample": f"full {args.solver} solve of {args.config.upper()} per step (oracle C++ "
-                                       "restatement, single thread like the reference)"},
+            "config": config_dict(args, c, world),
+            "cpu_baseline": {"value": v, "unit": "s", "cores": 1, "kind": "port", "sample": sample},
             "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-            "iterations": int(rep.iterations), **extra}
+            "step_s": times, **extra}
     print(json.dumps(line), flush=True)
     return 0
 
@@ -223,18 +361,19 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-clocks", action="store_true", help="do not sample nvidia-smi during the timed steps")
     ap.add_argument("--out", default=None, help="also write the JSON line here")
     ap.add_argument("--replicas", action="store_true", help="N > 1: independent replicas instead of row sharding")
+    ap.add_argument("--record-counters", action="store_true",
+                    help=f"write this config's solve counters into profiles/{REF_COUNTERS_PATH.name}")
     ap.add_argument("--solver", default="ihs", choices=["ihs", "pcg", "cg"],
                     help="ihs: adaptive Polyak-IHS (the headline); pcg / cg: the baselines.hpp comparators")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
-    args.warmup_ref = 0  # the CPU reference has nothing to warm up; W is reported as given
     c = CONFIGS[args.config]
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -263,7 +402,6 @@ def main():
     # space, the sketch partials and gradient partials are combined over NCCL inside the library, and every
     # rank runs the same replicated small solve. --replicas runs N independent copies instead.
     sharded = world > 1 and not args.replicas
-    parallelism = "single GPU"
     row0, rows = 0, n
     comm = None
     if sharded:
@@ -271,9 +409,6 @@ def main():
         uid = [ihs.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         comm = ihs.NcclComm(uid[0], world, rank, local)
-        parallelism = f"row-sharded x{world} (NCCL all-gather/all-reduce of sketch and gradient partials)"
-    elif world > 1:
-        parallelism = f"replicas x{world}"
     # inputs in pinned host memory (torch is plumbing only)
     A_t = torch.empty((d, rows), dtype=torch.float64, pin_memory=True)  # column-major rows x d
     b_t = torch.empty((rows,), dtype=torch.float64, pin_memory=True)
@@ -373,7 +508,8 @@ def main():
     hbm, peak_kind = peaks()
     fp64, fp64_kind = fp64_peak()
     rd_peak = read_stream_peak()
-    phases = {"gradient": t["gradient_ms"], "sketch": t["sketch_ms"], "factor": t["factor_ms"], "solve": t["solve_ms"]}
+    phases = {"gradient": t["gradient_ms"], "sketch": t["sketch_ms"], "factor": t["factor_ms"], "solve": t["solve_ms"],
+              "total": t["total_ms"], "host_alloc": t["alloc_ms"], "host_rng": t["host_rng_ms"]}
     kern = {}
     if t["n_gradient_kernel"] > 0 and t["gradient_kernel_ms"] > 0:
         # gradient_bytes counts every pass the solve made (speculative ones included), as do the timers
@@ -398,7 +534,8 @@ def main():
                               "peak_source": peak_kind}
         else:
             ach = t["sketch_flops"] / (sk_ms * 1e-3) / 1e12
-            kern["sketch"] = {"kernel": "dgemm_kernel<0,0> S*A (mma.sync m8n8k4 f64 = DMMA)", "bound": "tensor",
+            kern["sketch"] = {"kernel": "dgemm_nn_big_kernel S*A (128x128 cp.async tiles, mma.sync m8n8k4 f64 = "
+                                        "DMMA)", "bound": "tensor",
                               "achieved": ach, "peak": fp64, "unit": "TFLOP/s", "frac": ach / fp64 if fp64 else None,
                               "algorithmic_flops_per_launch": t["sketch_flops"] / t["n_sketch_kernel"],
                               "peak_source": fp64_kind}
@@ -414,50 +551,71 @@ def main():
     roof["timing"] = ("CUDA events around the kernels on the library stream, in one instrumented solve after the "
                       "timed steps (the timed steps run with phase events off)")
 
+    # ---- accuracy of the returned x against the exact minimizer (problem.hpp:73-82, 104-109), off the clock
+    acc = {}
+    if args.solver == "ihs":
+        try:
+            x_star = ihs.direct_solve(p)
+            pe0 = ihs.prediction_error(p, np.zeros(d), x_star)
+            pe = ihs.prediction_error(p, last.x, x_star)
+            acc = {"delta_rel_vs_direct": float(np.sqrt(pe / pe0)), "pe_rel": float(pe / pe0),
+                   "delta_target": 1e-10, "meets_target": bool(np.sqrt(pe / pe0) <= 1e-10)}
+        except Exception as e:  # noqa: BLE001
+            acc = {"delta_rel_vs_direct": None, "delta_error": str(e)[:200]}
+    counters = {"sketch": last.counters.sketch, "factor": last.counters.factor, "solve": last.counters.solve,
+                "matvec": last.counters.matvec} if args.solver == "ihs" else None
+
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline and n * d > (1 << 26):
-        cpu = {"value": None, "unit": "s", "cores": 1, "kind": "port",
-               "sample": "not run: a single-thread oracle solve of this config exceeds the few-minute bench budget "
-                         "(the default config C2 carries the CPU baseline)"}
-    elif rank == 0 and world == 1 and not args.no_cpu_baseline and args.solver == "pcg" and \
-            kind == ihs.SketchKind.Gaussian and last.m * n * d > (1 << 34):
-        cpu = {"value": None, "unit": "s", "cores": 1, "kind": "port",
-               "sample": f"not run: the oracle's single-thread Gaussian sketch (m={last.m}) of this config exceeds "
-                         "the few-minute bench budget"}
-    elif rank == 0 and world == 1 and not args.no_cpu_baseline and args.solver != "ihs":
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
         from oracle import oracle as O
-        t0 = time.perf_counter()
-        x_ref, _, orep = (O.pcg_solve(A, b, nu, int(kind), 0, PCG_RHO, CG_TOL, CG_MAX_ITERS) if args.solver == "pcg"
-                          else O.cg_solve(A, b, nu, CG_TOL, CG_MAX_ITERS))
-        cpu = {"value": time.perf_counter() - t0, "unit": "s", "cores": 1, "kind": "port",
-               "sample": f"one full {args.solver} solve of {args.config.upper()} (oracle C++ restatement, 1 thread)",
-               "iterations": int(orep.iterations), "same_iterations": int(orep.iterations) == last.iterations}
-        Ad = np.concatenate([A @ (last.x - x_ref), nu * (last.x - x_ref)])
-        Ar = np.concatenate([A @ x_ref, nu * x_ref])
-        cpu["abar_rel_err_vs_oracle"] = float(np.linalg.norm(Ad) / np.linalg.norm(Ar))
-    elif rank == 0 and world == 1 and not args.no_cpu_baseline:
-        from oracle import oracle as O
-        ocfg = oracle_config(O, c)
-        x_ref, orep, olog, _ = O.adaptive_solve(A, b, nu, ocfg)
-        cpu = {"value": float(orep.wall_seconds), "unit": "s", "cores": 1, "kind": "port",
-               "sample": f"one full adaptive_solve of {args.config.upper()} (oracle C++ restatement, 1 thread)",
-               "same_m_schedule": bool(orep.rejections == last.rejections and orep.final_m == last.final_m
-                                      and orep.iterations == last.iterations)}
-        Ad = np.concatenate([A @ (last.x - x_ref), nu * (last.x - x_ref)])
-        Ar = np.concatenate([A @ x_ref, nu * x_ref])
-        cpu["abar_rel_err_vs_oracle"] = float(np.linalg.norm(Ad) / np.linalg.norm(Ar))
+        if args.config in FULL_CPU_SOLVE:
+            t0 = time.perf_counter()
+            if args.solver == "ihs":
+                x_ref, orep, olog, _ = O.adaptive_solve(A, b, nu, oracle_config(O, c))
+                cpu = {"value": float(orep.wall_seconds), "unit": "s", "cores": 1, "kind": "port",
+                       "sample": f"one whole adaptive_solve of {args.config.upper()} (oracle C++ restatement of the "
+                                 "reference, 1 thread)",
+                       "same_m_schedule": bool([(e[0], e[1], e[4]) for e in olog] ==
+                                               [(e.t, e.m, int(e.branch)) for e in last.log]),
+                       "same_counters": bool((orep.counters.sketch, orep.counters.factor, orep.counters.solve,
+                                              orep.counters.matvec) == tuple(counters.values()))}
+            else:
+                x_ref, _, orep = (O.pcg_solve(A, b, nu, int(kind), 0, PCG_RHO, CG_TOL, CG_MAX_ITERS)
+                                  if args.solver == "pcg" else O.cg_solve(A, b, nu, CG_TOL, CG_MAX_ITERS))
+                cpu = {"value": time.perf_counter() - t0, "unit": "s", "cores": 1, "kind": "port",
+                       "sample": f"one whole {args.solver} solve of {args.config.upper()} (oracle, 1 thread)",
+                       "iterations": int(orep.iterations), "same_iterations": int(orep.iterations) == last.iterations}
+            Ad = np.concatenate([A @ (last.x - x_ref), nu * (last.x - x_ref)])
+            Ar = np.concatenate([A @ x_ref, nu * x_ref])
+            cpu["abar_rel_err_vs_oracle"] = float(np.linalg.norm(Ad) / np.linalg.norm(Ar))
+        elif args.solver == "ihs":
+            rates, desc, spent = host_phase_rates(O, c, last.final_m)
+            v, phases = extrapolate(rates, counters, d)
+            cpu = {"value": v, "unit": "s", "cores": 1, "kind": "port",
+                   "sample": f"extrapolated: bounded samples of {args.config.upper()} ({desc}) timed on the host "
+                             "(oracle restatement, 1 thread) x this solve's cost counters",
+                   "extrapolated_phase_s": phases, "host_rates_s_per_unit": rates, "sample_seconds": spent}
+        else:
+            cpu = {"value": None, "unit": "s", "cores": 1, "kind": "port",
+                   "sample": f"not run: the single-thread {args.solver} of this config exceeds the bench budget"}
 
     if rank == 0:
         if args.solver == "ihs":
             summary = {"iterations": last.iterations, "rejections": last.rejections, "final_m": last.final_m,
-                       "converged": last.converged, "m_schedule": [e.m for e in last.log if int(e.branch) == 2]}
-            cfg_extra = {"rho": c["rho"], "m_initial": c["m_initial"], "max_sketch": c["max_sketch"],
-                         "enforce_validity": c["enforce_validity"], "eps": 1e-10}
+                       "converged": last.converged, "m_schedule": [e.m for e in last.log if int(e.branch) == 2],
+                       **acc, "counters": counters}
+            rec = load_ref_counters().get(args.config)
+            if rec is not None and world == 1:
+                summary["counters_match_recorded"] = rec == {**counters, "iterations": last.iterations,
+                                                             "rejections": last.rejections, "final_m": last.final_m}
+            if args.record_counters and world == 1:
+                allc = load_ref_counters()
+                allc[args.config] = {**counters, "iterations": last.iterations, "rejections": last.rejections,
+                                     "final_m": last.final_m}
+                REF_COUNTERS_PATH.write_text(json.dumps(allc, indent=1, sort_keys=True) + "\n")
         else:
             summary = {"iterations": last.iterations, "converged": last.converged, "m": last.m,
                        "m_capped": last.m_capped, "residual_ratio": last.residuals[-1] / last.residuals[0]}
-            cfg_extra = {"solver": args.solver, "tol": CG_TOL, "max_iters": CG_MAX_ITERS,
-                         **({"rho": PCG_RHO} if args.solver == "pcg" else {})}
         summary.update({"lib_total_ms": float(np.mean(lib_ms)), "step_ms": step_ms,
                         "kernel_launches_per_solve": t["kernel_launches"]})
         line = {"metric": METRICS[args.solver], "value": ms / 1e3, "unit": "s", "n_gpus": world, "steps": args.steps,
@@ -465,14 +623,7 @@ def main():
                 "scaling": "strong" if sharded else "weak",
                 "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic (seeded SURVEY §8(d) generator: A = G diag(sigma), x_true, noise)",
-                "config": {"workload": c["desc"] if args.solver == "ihs" else
-                           f"{args.solver.upper()} on the {args.config.upper()} data (n={n}, d={d}, nu={nu})",
-                           "n": n, "d": d, "nu": nu, "sketch": c["sketch"],
-                           **({"mode": c["mode"]} if args.solver == "ihs" else {}), **cfg_extra,
-                           "l2": ("inputs larger than L2 (A = %.0f MiB) and L2 flushed between steps"
-                                  % (8 * n * d / 2**20)) if 8 * n * d > L2_BYTES else
-                                 "L2 flushed (256 MiB write) between timed steps",
-                           "parallelism": parallelism},
+                "config": config_dict(args, c, world),
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
                 "clocks": clocks,
                 "solve": summary,

@@ -118,6 +118,8 @@ struct SrhtPlan {
     int p2t;                 // threads per phase-2 tile (128; 256 for the 64 KiB-tile variant)
     int stream;              // 1: streamed single-launch kernel (srht_plan_stream)
     int compact;             // 1: compact T (only the sampled low indices; srht_plan_compact)
+    int l2;                  // 1: L2-resident single launch (srht_plan_l2): T is a ring of l2_ns column slots
+    int l2_ns;               // ring depth (column slots)
 };
 SrhtPlan srht_plan(int64_t n, int64_t d, int64_t lda, int64_t m);
 // switch the plan to the streamed single-launch kernel when it applies (sets
@@ -129,6 +131,12 @@ bool srht_plan_stream(SrhtPlan& p, int num_sms);
 // low-index -> u map).
 bool srht_plan_compact(SrhtPlan& p, const int64_t* rows);
 size_t srht_scratch_bytes(const SrhtPlan& p);  // T buffer (phase-1 output) when H > 0
+// switch a single-pass plan with 8..12 high bits to the L2-resident single launch (sets p2t before the entries
+// are built; the tiles then carry 4 trailing int4 of tile-occupancy bits); false = keep the plan
+bool srht_plan_l2(SrhtPlan& p);
+// T ring + control block of the L2-resident launch
+size_t srht_l2_scratch_bytes(const SrhtPlan& p);
+size_t srht_l2_ctl_bytes(const SrhtPlan& p);
 // Host: bucket the sampled rows (draw order k -> row rows[k]) by phase-2
 // tile. entries = (row, k) pairs grouped by tile; tiles = (rlo0, begin, end).
 void srht_build_entries(const SrhtPlan& p, const int64_t* rows, std::vector<int2>& entries,
@@ -165,7 +173,8 @@ void nccl_allgather(const double* send, double* recv, size_t count_per_rank, voi
 void dgemm(bool transA, bool transB, int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t lda,
            const double* B, int64_t ldb, double beta, double* C, int64_t ldc, bool lower_only, int splitk,
            double* d_work, cudaStream_t st);
-int dgemm_pick_splitk(int64_t M, int64_t N, int64_t K, int num_sms);
+int dgemm_pick_splitk(int64_t M, int64_t N, int64_t K, int num_sms, bool transA = false, bool transB = false,
+                      bool lower_only = false);
 
 // chol.cu — blocked Cholesky (lower, in place). d_info: int (0 ok, j+1 = failed pivot).
 // d_Xd (cholesky_diag_inv_doubles(n), or nullptr for the column-serial kernels)

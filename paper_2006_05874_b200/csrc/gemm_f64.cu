@@ -136,56 +136,86 @@ dgemm_kernel(int64_t M, int64_t N, int64_t K, double alpha, const double* __rest
 }
 
 
-// ---- large NN GEMM (S*A): 128x128 CTA tile, 8 warps of 64x32, 4-stage cp.async ring.
-// A (M x K, col-major: m contiguous) is staged k-major As[k][m] (row stride 132),
-// B (K x N, col-major: k contiguous) n-major Bs[n][k] (row stride 20), so both
-// the 16-byte cp.async writes and the m8n8k4 fragment reads are conflict-free.
+// ---- large GEMM: 128x128 CTA tile, 8 warps of 64x32, 4-stage cp.async ring, any transposition.
+// Each operand is staged so its 16-byte cp.async writes and the m8n8k4 fragment reads are conflict-free:
+//   m-contiguous A (NN/NT: A(m,k) at A + m + k lda) -> k-major As[k][m], row stride 132;
+//   k-contiguous A (TN/TT: A(m,k) at A + k + m lda) -> m-major As[m][k], row stride 20;
+//   k-contiguous B (NN/TN: B(k,n) at B + k + n ldb) -> n-major Bs[n][k], row stride 20;
+//   n-contiguous B (NT/TT: B(k,n) at B + n + k ldb) -> k-major Bs[k][n], row stride 132.
+// Used for S*A (NN), the Gram SYRK SA^T SA (TN, lower tiles only), the Woodbury inner SA SA^T (NT, lower) and
+// H_S^{-1} = W^T W (TN). lower_only skips the CTA tiles strictly above the diagonal (the consumers read the
+// lower triangle); per-split partials go to a workspace summed in fixed order (deterministic split-K).
 constexpr int GBM = 128, GBN = 128, GBK = 16, GST = 4;
 constexpr int GLA = 132, GLB = 20;
 constexpr int GTHREADS = 256;
-constexpr size_t kBigSmem = (size_t)GST * (GBK * GLA + GBN * GLB) * sizeof(double);
+constexpr int big_stage_doubles(bool kmajor_a, bool kmajor_b) {
+    return (kmajor_a ? GBK * GLA : GBM * GLB) + (kmajor_b ? GBK * GLA : GBN * GLB);
+}
+template <bool TA, bool TB>
+constexpr size_t big_smem() { return (size_t)GST * big_stage_doubles(!TA, TB) * sizeof(double); }
 
 __device__ __forceinline__ void cp16(double* dst, const double* src, int bytes) {
     const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(src), "r"(bytes) : "memory");
 }
 
+template <bool TA, bool TB>
 __global__ void __launch_bounds__(GTHREADS, 1)
-dgemm_nn_big_kernel(int64_t M, int64_t N, int64_t K, double alpha, const double* __restrict__ A, int64_t lda,
-                    const double* __restrict__ B, int64_t ldb, double beta, double* __restrict__ C, int64_t ldc,
-                    int64_t k_per_split, double* __restrict__ work) {
+dgemm_big_kernel(int64_t M, int64_t N, int64_t K, double alpha, const double* __restrict__ A, int64_t lda,
+                 const double* __restrict__ B, int64_t ldb, double beta, double* __restrict__ C, int64_t ldc,
+                 int64_t k_per_split, double* __restrict__ work, int lower_only) {
+    constexpr bool KA = !TA;  // A staged k-major ([k][m])
+    constexpr bool KB = TB;   // B staged k-major ([k][n])
+    constexpr int SA_D = KA ? GBK * GLA : GBM * GLB;
+    constexpr int SB_D = KB ? GBK * GLA : GBN * GLB;
+    const int64_t m0 = (int64_t)blockIdx.x * GBM, n0 = (int64_t)blockIdx.y * GBN;
+    if (lower_only && n0 > m0 + GBM - 1) return;
     pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible after this
     extern __shared__ double gsm[];
-    const int64_t m0 = (int64_t)blockIdx.x * GBM, n0 = (int64_t)blockIdx.y * GBN;
     const int64_t kbeg = (int64_t)blockIdx.z * k_per_split;
     const int64_t kend = min(K, kbeg + k_per_split);
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const int wm = (warp & 1) * 64, wn = (warp >> 1) * 32;
     double* As0 = gsm;
-    double* Bs0 = gsm + GST * GBK * GLA;
-    // per-thread copy assignments (4 A chunks, 4 B chunks of 16 B per stage)
-    // A: chunk c = t + 256 u -> k = c / 64, m pair = c % 64
-    // B: chunk c = t + 256 u -> n = c / 8,  k pair = c % 8
+    double* Bs0 = gsm + GST * SA_D;
+    // 1024 16-byte chunks per operand per stage, 4 per thread: k-major c -> (k = c / 64, pair = c % 64),
+    // row-major c -> (row = c / 8, k pair = c % 8)
     auto issue = [&](int64_t k0, int stage) {
-        double* As = As0 + stage * GBK * GLA;
-        double* Bs = Bs0 + stage * GBN * GLB;
+        double* As = As0 + stage * SA_D;
+        double* Bs = Bs0 + stage * SB_D;
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             const int c = t + GTHREADS * u;
-            const int kk = c >> 6, mm = (c & 63) * 2;
-            const int64_t gk = k0 + kk, gm = m0 + mm;
-            int bytes = 0;
-            if (gk < kend) bytes = gm + 1 < M ? 16 : (gm < M ? 8 : 0);
-            cp16(As + kk * GLA + mm, bytes ? A + gm + gk * lda : A, bytes);
+            if (KA) {
+                const int kk = c >> 6, mm = (c & 63) * 2;
+                const int64_t gk = k0 + kk, gm = m0 + mm;
+                int bytes = 0;
+                if (gk < kend) bytes = gm + 1 < M ? 16 : (gm < M ? 8 : 0);
+                cp16(As + kk * GLA + mm, bytes ? A + gm + gk * lda : A, bytes);
+            } else {
+                const int mm = c >> 3, kk = (c & 7) * 2;
+                const int64_t gm = m0 + mm, gk = k0 + kk;
+                int bytes = 0;
+                if (gm < M) bytes = gk + 1 < kend ? 16 : (gk < kend ? 8 : 0);
+                cp16(As + mm * GLB + kk, bytes ? A + gk + gm * lda : A, bytes);
+            }
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             const int c = t + GTHREADS * u;
-            const int nn = c >> 3, kk = (c & 7) * 2;
-            const int64_t gn = n0 + nn, gk = k0 + kk;
-            int bytes = 0;
-            if (gn < N) bytes = gk + 1 < kend ? 16 : (gk < kend ? 8 : 0);
-            cp16(Bs + nn * GLB + kk, bytes ? B + gk + gn * ldb : B, bytes);
+            if (KB) {
+                const int kk = c >> 6, nn = (c & 63) * 2;
+                const int64_t gk = k0 + kk, gn = n0 + nn;
+                int bytes = 0;
+                if (gk < kend) bytes = gn + 1 < N ? 16 : (gn < N ? 8 : 0);
+                cp16(Bs + kk * GLA + nn, bytes ? B + gn + gk * ldb : B, bytes);
+            } else {
+                const int nn = c >> 3, kk = (c & 7) * 2;
+                const int64_t gn = n0 + nn, gk = k0 + kk;
+                int bytes = 0;
+                if (gn < N) bytes = gk + 1 < kend ? 16 : (gk < kend ? 8 : 0);
+                cp16(Bs + nn * GLB + kk, bytes ? B + gk + gn * ldb : B, bytes);
+            }
         }
         asm volatile("cp.async.commit_group;\n" ::: "memory");
     };
@@ -208,15 +238,15 @@ dgemm_nn_big_kernel(int64_t M, int64_t N, int64_t K, double alpha, const double*
         if (nx < ntiles) issue(kbeg + nx * GBK, (int)(nx % GST));
         else asm volatile("cp.async.commit_group;\n" ::: "memory");
         const int stage = (int)(it % GST);
-        const double* As = As0 + stage * GBK * GLA + wm + fr;
-        const double* Bs = Bs0 + stage * GBN * GLB + (wn + fr) * GLB;
+        const double* As = As0 + stage * SA_D + (KA ? wm + fr : (wm + fr) * GLB);
+        const double* Bs = Bs0 + stage * SB_D + (KB ? wn + fr : (wn + fr) * GLB);
 #pragma unroll
         for (int kk = 0; kk < GBK; kk += 4) {
             double af[8], bf[4];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) af[i] = As[(kk + fk) * GLA + i * 8];
+            for (int i = 0; i < 8; ++i) af[i] = KA ? As[(kk + fk) * GLA + i * 8] : As[i * 8 * GLB + kk + fk];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) bf[j] = Bs[j * 8 * GLB + kk + fk];
+            for (int j = 0; j < 4; ++j) bf[j] = KB ? Bs[(kk + fk) * GLA + j * 8] : Bs[j * 8 * GLB + kk + fk];
 #pragma unroll
             for (int i = 0; i < 8; ++i)
 #pragma unroll
@@ -261,22 +291,32 @@ __global__ void splitk_reduce_kernel(int64_t M, int64_t N, int splits, const dou
 }
 }  // namespace
 
-// the 128x128 cp.async kernel: plain NN products with enough work and 16-byte
-// aligned columns (S*A of the Gaussian sketch)
+// the 128x128 cp.async kernel: enough work per tile and even leading dimensions (16-byte chunks along the
+// contiguous index of both operands; the base pointers are checked in dgemm)
 bool dgemm_use_big(bool transA, bool transB, int64_t M, int64_t N, int64_t K, int64_t lda, int64_t ldb,
                    bool lower_only) {
-    return !transA && !transB && !lower_only && M >= 256 && N >= 128 && K >= 4096 && lda % 2 == 0 && ldb % 2 == 0;
+    (void)transA;
+    (void)transB;
+    (void)lower_only;
+    return M >= 256 && N >= 128 && K >= 1024 && lda % 2 == 0 && ldb % 2 == 0;
 }
 // ... and its 16-byte cp.async loads need 16-byte aligned operand base pointers as well
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
-int dgemm_pick_splitk(int64_t M, int64_t N, int64_t K, int num_sms) {
-    if (dgemm_use_big(false, false, M, N, K, M + (M & 1), 2, false)) {
+int dgemm_pick_splitk(int64_t M, int64_t N, int64_t K, int num_sms, bool transA, bool transB, bool lower_only) {
+    if (dgemm_use_big(transA, transB, M, N, K, M + (M & 1), 2, lower_only)) {
         // one CTA per SM: the split count whose last wave is fullest (>= 1024 rows of K per split)
-        const int64_t tiles = ceil_div(M, GBM) * ceil_div(N, GBN);
+        const int64_t tm = ceil_div(M, GBM), tn = ceil_div(N, GBN);
+        int64_t tiles = tm * tn;
+        if (lower_only) {  // tiles on or below the diagonal
+            tiles = 0;
+            for (int64_t bm = 0; bm < tm; ++bm) tiles += std::min<int64_t>(tn, (bm * GBM + GBM - 1) / GBN + 1);
+        }
         int best = 1;
         double best_eff = 0.0;
-        for (int s = 1; s <= 16 && K / s >= 1024; ++s) {
+        // workspace (s partial M x N products) kept within 1 GiB
+        const int smax = (int)std::max<int64_t>(1, std::min<int64_t>(32, (int64_t)(1ll << 30) / (8 * M * N)));
+        for (int s = 1; s <= smax && K / s >= 1024; ++s) {
             const int64_t ctas = tiles * s;
             const double eff = (double)ctas / (double)(ceil_div(ctas, num_sms) * num_sms);
             if (eff > best_eff + 1e-9) { best_eff = eff; best = s; }
@@ -305,9 +345,6 @@ void dgemm(bool transA, bool transB, int64_t M, int64_t N, int64_t K, double alp
     }
     if (splitk < 1) splitk = 1;
     const bool big = dgemm_use_big(transA, transB, M, N, K, lda, ldb, lower_only) && aligned16(A) && aligned16(B);
-    if (big) {
-        IHS_SMEM_ATTR(dgemm_nn_big_kernel, (int)kBigSmem);
-    }
     int64_t kps = ceil_div(std::max<int64_t>(K, 1), splitk);
     kps = ceil_div(kps, BK) * BK;
     const int splits = (int)std::max<int64_t>(1, ceil_div(std::max<int64_t>(K, 1), kps));
@@ -322,9 +359,17 @@ void dgemm(bool transA, bool transB, int64_t M, int64_t N, int64_t K, double alp
                (int)lower_only);
         return;
     }
-    if (!transA && !transB && big)
-        LAUNCH_PDL(dgemm_nn_big_kernel, grid, GTHREADS, kBigSmem, st, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kps,
-               work);
+#define IHS_BIG(TA_, TB_)                                                                                       \
+    do {                                                                                                        \
+        IHS_SMEM_ATTR((dgemm_big_kernel<TA_, TB_>), (int)(big_smem<TA_, TB_>()));                               \
+        LAUNCH_PDL((dgemm_big_kernel<TA_, TB_>), grid, GTHREADS, (big_smem<TA_, TB_>()), st, M, N, K, alpha, A, lda, B,\
+                   ldb, beta, C, ldc, kps, work, (int)lower_only);                                              \
+    } while (0)
+    if (big && !transA && !transB) IHS_BIG(false, false);
+    else if (big && transA && !transB) IHS_BIG(true, false);
+    else if (big && !transA && transB) IHS_BIG(false, true);
+    else if (big) IHS_BIG(true, true);
+#undef IHS_BIG
     else if (!transA && !transB)
         LAUNCH_PDL((dgemm_kernel<false, false>), grid, THREADS, 0, st, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc,
                (int)lower_only, kps, work);

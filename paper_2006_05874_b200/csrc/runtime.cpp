@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <cstdio>
 #include <cmath>
 #include <cstring>
 #include <memory>
@@ -329,6 +330,11 @@ namespace {
 // two-kernel path (default: measured faster; IHS_SRHT_FUSED=1 selects the
 // persistent single-launch kernel for A/B measurements).
 unsigned long long* srht_prepare_scratch(ihs_gpu_problem* P, const SrhtPlan& plan) {
+    if (plan.l2) {  // L2-resident single launch: a ring of column slots + the work/completion counters
+        P->T.ensure(srht_l2_scratch_bytes(plan));
+        P->fused_ctl.ensure(srht_l2_ctl_bytes(plan));
+        return P->fused_ctl.as<unsigned long long>();
+    }
     if (!plan.stream) {  // two-kernel path (srht_plan_stream declined)
         P->T.ensure(srht_scratch_bytes(plan));
         return nullptr;
@@ -385,7 +391,7 @@ void device_sketch(ihs_gpu_problem* P, int kind, int64_t m, uint64_t seed, doubl
         const int shards = world > 1 ? world : std::max(1, emulate_shards);
         if (shards == 1) {
             srht_plan_stream(plan, P->num_sms);  // decides the emitting-tile shape before the entries are built
-            srht_plan_compact(plan, P->h_rows.data());
+            if (!srht_plan_compact(plan, P->h_rows.data())) srht_plan_l2(plan);
             srht_build_entries(plan, P->h_rows.data(), P->h_entries, P->h_tiles);
             P->mask_valid = srht_build_mask(plan, P->h_tiles, P->h_mask);
             g_host_rng_ns +=
@@ -394,12 +400,14 @@ void device_sketch(ihs_gpu_problem* P, int kind, int64_t m, uint64_t seed, doubl
             // columns are independent: when the phase-1 scratch of all d columns would exceed the cap,
             // the transform runs over column batches that share one smaller scratch (and the row sample)
             const int64_t cols_per_batch =
-                std::max<int64_t>(1, std::min<int64_t>(d, kSrhtScratchCap / (plan.n_pad * (int64_t)sizeof(double))));
+                plan.l2 ? d  // the L2-resident launch needs only its slot ring, whatever d
+                        : std::max<int64_t>(1, std::min<int64_t>(d, kSrhtScratchCap / (plan.n_pad * (int64_t)sizeof(double))));
             ensure_A(P);  // the signs and the row sample above did not need A
             SrhtPlan bp = plan;
             bp.d = std::min<int64_t>(d, cols_per_batch);
             // compact plans carry the low-index map (128 int4) after their tiles
-            const int n_tiles = (int)P->h_tiles.size() - (plan.compact ? (int)(1024 * sizeof(short) / sizeof(int4)) : 0);
+            const int n_tiles = (int)P->h_tiles.size() - (plan.compact ? (int)(1024 * sizeof(short) / sizeof(int4)) : 0) -
+                                (plan.l2 ? 4 : 0);
             unsigned long long* ctl = srht_prepare_scratch(P, bp);
             if (P->timer) P->timer->mark(PH_SKETCH_KERNEL);
             for (int64_t j0 = 0; j0 < d; j0 += cols_per_batch) {
@@ -554,13 +562,13 @@ void system_factorize(ihs_gpu_system* S, ihs_counters* c) {
     const double nu2 = S->nu * S->nu;
     if (S->kind == IHS_FACTOR_WOODBURY_INNER) {
         // inner = SA SA^T + nu^2 I_m (lower)
-        const int splitk = dgemm_pick_splitk(m, m, d, S->num_sms);
+        const int splitk = dgemm_pick_splitk(m, m, d, S->num_sms, false, true, true);
         if (splitk > 1) S->work.ensure((size_t)splitk * m * m * sizeof(double));
         dgemm(false, true, m, m, d, 1.0, SA, lds, SA, lds, 0.0, S->L.d(), m, true, splitk,
               splitk > 1 ? S->work.d() : nullptr, st);
     } else {
         // gram = SA^T SA + nu^2 I_d (lower)
-        const int splitk = dgemm_pick_splitk(d, d, m, S->num_sms);
+        const int splitk = dgemm_pick_splitk(d, d, m, S->num_sms, true, false, true);
         if (splitk > 1) S->work.ensure((size_t)splitk * d * d * sizeof(double));
         dgemm(true, false, d, d, m, 1.0, SA, lds, SA, lds, 0.0, S->L.d(), d, true, splitk,
               splitk > 1 ? S->work.d() : nullptr, st);
@@ -595,7 +603,7 @@ void system_factorize(ihs_gpu_system* S, ihs_counters* c) {
         // is then a single symmetric mat-vec instead of two dependent triangular ones
         S->Hinv.ensure((size_t)k * k * sizeof(double));
         tril_copy(S->W.d(), k, S->L.d(), st);  // the factor itself is not needed after the inverse
-        const int splitk = dgemm_pick_splitk(k, k, k, S->num_sms);
+        const int splitk = dgemm_pick_splitk(k, k, k, S->num_sms, true, false, false);
         if (splitk > 1) S->work.ensure((size_t)splitk * k * k * sizeof(double));
         dgemm(true, false, k, k, k, 1.0, S->L.d(), k, S->L.d(), k, 0.0, S->Hinv.d(), k, false, splitk,
               splitk > 1 ? S->work.d() : nullptr, st);
@@ -1691,6 +1699,16 @@ void adaptive_solve_impl(ihs_gpu_problem* P, const ihs_solver_config* cfg, ihs_s
         if (cfg->max_iters < 1) fail(IHS_INVALID_INPUT, "adaptive_solve: max_iters must be >= 1");
 
         const auto t_start = std::chrono::steady_clock::now();
+        // IHS_TRACE=1: host-side timeline of the solve on stderr (where the host blocks and for how long)
+        static const bool trace_on = [] {
+            const char* e = std::getenv("IHS_TRACE");
+            return e && e[0] == '1';
+        }();
+        auto trace = [&](const char* what, double a = 0.0) {
+            if (!trace_on) return;
+            const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
+            std::fprintf(stderr, "[ihs-trace] %9.3f ms  %s %g\n", ms, what, a);
+        };
         const int64_t dim = P->d;
         const int64_t n_rows = P->opts.world_size > 1 ? P->opts.n_global : P->n;
         cudaStream_t st = P->st;
@@ -1741,6 +1759,7 @@ void adaptive_solve_impl(ihs_gpu_problem* P, const ihs_solver_config* cfg, ihs_s
         sys.num_sms = P->num_sms;
         sys.defer_info = true;
         auto sketch_and_factor = [&](int64_t mm, uint64_t sub_seed) {
+            trace("sketch+factor enqueue begin m=", (double)mm);
             sys.m = mm;
             sys.SA.ensure((size_t)mm * dim * sizeof(double));
             tm.mark(PH_SKETCH);
@@ -1759,9 +1778,11 @@ void adaptive_solve_impl(ihs_gpu_problem* P, const ihs_solver_config* cfg, ihs_s
             } else {
                 device_sketch(P, cfg->sketch_kind, mm, sub_seed, sys.SA.d(), &C);
             }
+            trace("sketch enqueued");
             tm.mark(PH_FACTOR);
             system_factorize(&sys, &C);
             tm.mark(PH_END);
+            trace("factor enqueued");
         };
 
         // Device vectors. x0/xprev0/g0/gt0 hold the starting state; candidate evaluations rotate over
@@ -1913,7 +1934,9 @@ void adaptive_solve_impl(ihs_gpu_problem* P, const ihs_solver_config* cfg, ihs_s
                 spec = (cur + 1) % NSETS;
                 enqueue_eval(spec, S.X2 + spec_slot * dim, xcur, S.GT2 + spec_slot * dim, want_polyak);
             }
+            trace("wait eval t=", (double)t);
             CUDA_CHECK(cudaEventSynchronize(S.ev));
+            trace("eval ready");
             system_check(&sys);
             const double* hv = S.hd;
             const uint64_t grad_cost = 2 * (uint64_t)n_rows * (uint64_t)dim + (uint64_t)n_rows + 2 * (uint64_t)dim;
@@ -1962,7 +1985,9 @@ void adaptive_solve_impl(ihs_gpu_problem* P, const ihs_solver_config* cfg, ihs_s
                 decrement_dots(g, gt, dim, 1, dots, st);
                 tm.mark(PH_END);
                 CUDA_CHECK(cudaMemcpyAsync(hd, dots, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+                trace("wait resketch decrement");
                 CUDA_CHECK(cudaStreamSynchronize(st));
+                trace("resketch decrement ready");
                 system_check(&sys);
                 r = decrement(hd[0], hd[1]);
                 converged = r <= cfg->eps * r1;
@@ -1977,7 +2002,9 @@ void adaptive_solve_impl(ihs_gpu_problem* P, const ihs_solver_config* cfg, ihs_s
 
         CUDA_CHECK(cudaMemcpyAsync(rep->x, xcur, (size_t)dim * 8, cudaMemcpyDeviceToHost, st));
         CUDA_CHECK(cudaEventRecord(ev_end, st));
+        trace("wait end");
         CUDA_CHECK(cudaStreamSynchronize(st));
+        trace("end");
         system_check(&sys);
         {
             float ms = 0.f;

@@ -454,10 +454,13 @@ struct GroupBar {
     }
 };
 
-template <int HB, bool CG, class Bar = CtaBar, int TH = kP2Threads>
+// CMAJOR: the tile is stored c-major (element (b, w) at (b & 31) TH + (b >> 5) W + w, the layout the L2-resident
+// kernel writes), so round 1's load of register c is one contiguous TH-double run across the threads
+template <int HB, bool CG, class Bar = CtaBar, int TH = kP2Threads, bool CMAJOR = false>
 __device__ __forceinline__ void p2_tile(double* __restrict__ xs, double* __restrict__ Tcol, int lo, bool emit,
                                         int4 tile, const int2* __restrict__ entries, int64_t j, double s1, double s2,
-                                        double* __restrict__ SA, int64_t m, int t = threadIdx.x, Bar bar = Bar()) {
+                                        double* __restrict__ SA, int64_t m, int t = threadIdx.x, Bar bar = Bar(),
+                                        int row_lo = -1) {
     constexpr int RB1 = P2Geom<HB, TH>::RB1;
     constexpr int RB2 = HB - RB1;
     constexpr int E = P2Geom<HB, TH>::E;
@@ -468,7 +471,7 @@ __device__ __forceinline__ void p2_tile(double* __restrict__ xs, double* __restr
     // round 1: register c = pass bits [0, RB1), g = pass bits [RB1, HB)
 #pragma unroll
     for (int c = 0; c < E; ++c) {
-        const double* src = Tcol + ((int64_t)((g << RB1) | c) << lo) + w;
+        const double* src = CMAJOR ? Tcol + c * TH + t : Tcol + ((int64_t)((g << RB1) | c) << lo) + w;
         v[c] = CG ? __ldcg(src) : *src;
     }
 #pragma unroll
@@ -589,10 +592,11 @@ __device__ __forceinline__ void p2_tile(double* __restrict__ xs, double* __restr
     }
     bar();
     const int64_t bmask = (int64_t{1} << HB) - 1;
+    const int rlo = row_lo >= 0 ? row_lo : lo;  // row bit where the pass bits start (tile-major T: 10)
     for (int q = tile.y + t; q < tile.z; q += TH) {
         const int2 rk = entries[q];
         const int64_t r = rk.x;
-        const int b = (int)((r >> lo) & bmask);
+        const int b = (int)((r >> rlo) & bmask);
         const int ww = (int)(r & (W - 1));
         SA[(int64_t)rk.y + j * m] = __dmul_rn(__dmul_rn(xs[pad32(b * W + ww)], s1), s2);
     }
@@ -686,6 +690,252 @@ __global__ void __launch_bounds__(32 * kCmpU) srht_phase2_compact_kernel(const d
     }
 }
 
+// ------------------------------------------------------------ L2-resident single launch (default)
+// The two-kernel path moves every column three times through HBM (A read, T write, T read: 8.6 GB -> ~26 GB
+// at C3, 69 GB -> ~200 GB at C4). This persistent kernel keeps T on chip in the 126 MB L2 instead:
+//   * T is a ring of NS column slots (NS x n_pad doubles, <= ~64 MB), stored TILE-MAJOR: the emitting tile of
+//     W consecutive low indices x 2^HB high combinations is one contiguous 8192-double block, so the emitting
+//     pass reads it with fully coalesced L2 loads and then drops its lines with discard.global.L2 (no
+//     write-back: T never reaches HBM unless L2 pressure evicts it first);
+//   * work items (8 phase-1 chunks of a column, or one emitting tile of a column) are handed out in
+//     dependency order by one atomic counter: P1(col 0..NS-1), then per column j the emitting tiles of j
+//     followed by the P1 items of column j + NS. An emitting tile waits (one thread spinning on an acquire
+//     load) until all P1 items of its column have stored; a P1 item of column j + NS waits until every tile of
+//     column j has been emitted (its slot is free). Every item is handed out only after all items it waits
+//     for, and all CTAs are co-resident (grid = resident CTA count), so no wait can deadlock;
+//   * A arrives by TMA with an L2 evict-first hint (read once), T is stored with evict-last.
+// Butterfly order, the sign flip and the two scalings are exactly those of the two-kernel path.
+constexpr int kL2P1Warps = 8;                         // phase-1 warps (each a 2-slot TMA ring)
+constexpr int kL2EmitThreads = 256;                   // emitting group
+constexpr int kL2Threads = kL2P1Warps * 32 + kL2EmitThreads;
+constexpr int kL2TileElems = kL2EmitThreads * 32;
+// phase-1 rings (8 warps x 2 x 8 KiB) + exchange buffer pad32(8192) doubles + mbarriers + 1 KiB alignment slack
+constexpr size_t kL2Smem =
+    (size_t)(kL2P1Warps * 2 * kChunkDoubles + pad32(kL2TileElems) + 2 * kL2P1Warps) * sizeof(double) + 1024 + 64;
+
+__device__ __forceinline__ void red_release_add(int* p, int v) {
+    asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ int ld_acquire(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ void st_hint(double* p, double v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void st2_hint(double* p, double a, double b, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(a), "d"(b), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void discard_l2(const void* p) {
+    asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
+}
+__device__ __forceinline__ void load_4d_hint(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
+                                             uint64_t* bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, "
+        "%3, %4, %5}], [%6], %7;" ::"r"(tma::smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(tma::smem_u32(bar)), "l"(pol)
+        : "memory");
+}
+
+template <int HB>
+__global__ void __launch_bounds__(kL2Threads, 1)
+srht_l2_kernel(const __grid_constant__ ChunkMaps maps, const double* __restrict__ A, int64_t n, int64_t lda,
+               const uint32_t* __restrict__ signbits, double* __restrict__ T, int64_t nfull, int64_t d, int ns,
+               const int4* __restrict__ tiles, int n_tiles, const uint32_t* __restrict__ tile_bits,
+               const int2* __restrict__ entries, double s1, double s2, double* __restrict__ SA, int64_t m,
+               int* __restrict__ ctl, int discard) {
+    constexpr int W = P2Geom<HB, kL2EmitThreads>::W;
+    constexpr int LOGW = P2Geom<HB, kL2EmitThreads>::LOGW;
+    constexpr int TE = W << HB;  // tile elements (= kL2TileElems)
+    static_assert(TE == kL2TileElems && LOGW <= 5, "tile geometry");
+    constexpr int64_t NPAD = int64_t{1} << (HB + kChunkL);
+    constexpr int CPC = 1 << HB;  // chunks per column
+    pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible after this
+    extern __shared__ unsigned char l2_raw[];
+    double* base = align1024(l2_raw);
+    double* rings = base;                                   // kL2P1Warps x 2 chunk buffers (1 KiB aligned)
+    double* xs = base + kL2P1Warps * 2 * kChunkDoubles;     // emitting-tile exchange buffer
+    uint64_t* bars = reinterpret_cast<uint64_t*>(xs + pad32(TE));  // 2 per phase-1 warp
+    __shared__ int s_p2;
+    const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+    int* p1_counter = ctl;
+    int* p2_counter = ctl + 1;
+    int* done1 = ctl + 2;
+    int* done2 = ctl + 2 + d;
+    const int64_t P2N = n_tiles;
+    if (warp < kL2P1Warps) {
+        // ---- phase-1 warp: chunks in global (column-major) order through its own 2-slot TMA ring
+        double* ring = rings + warp * 2 * kChunkDoubles;
+        uint64_t* bar = bars + 2 * warp;
+        if (lane == 0) {
+            tma::mbar_init(&bar[0], 1);
+            tma::mbar_init(&bar[1], 1);
+            tma::fence_mbar_init();
+        }
+        __syncwarp();
+        const int64_t total = d * CPC;
+        const uint64_t pol_first = policy_evict_first(), pol_last = policy_evict_last();
+        uint32_t store_bits = 0u;  // bit c: element 32c + lane lies in a tile some sampled row reads
+#pragma unroll
+        for (int c = 0; c < 32; ++c) {
+            const int te = ((c << 5) + lane) >> LOGW;
+            store_bits |= ((__ldg(tile_bits + (te >> 5)) >> (te & 31)) & 1u) << c;
+        }
+        auto claim = [&]() -> int64_t {
+            int v = 0;
+            if (lane == 0) v = atomicAdd(p1_counter, 1);
+            return __shfl_sync(0xffffffffu, v, 0);
+        };
+        auto issue = [&](int64_t it, int sl) {
+            if (it >= total) return;
+            const int64_t q = it & (CPC - 1), col = it >> HB;
+            if (q >= nfull || lane != 0) return;
+            double* buf = ring + sl * kChunkDoubles;
+            tma::fence_proxy_async();
+            tma::mbar_expect_tx(&bar[sl], kChunkDoubles * sizeof(double));
+            load_4d_hint(buf, &maps.even, 0, 0, (int)q, (int)col, &bar[sl], pol_first);
+            load_4d_hint(buf + kChunkDoubles / 2, &maps.odd, 0, 0, (int)q, (int)col, &bar[sl], pol_first);
+        };
+        uint32_t phase = 0u;  // bit s: parity of slot s
+        int sl = 0;
+        // completions are released once per (warp, column) run of chunks, and the slot of a column is checked
+        // once per run: a warp's claims only ever move to later columns
+        int64_t run_col = -1, slot_ok_col = -1;
+        int run_cnt = 0;
+        int64_t cur = claim();
+        issue(cur, 0);
+        while (cur < total) {
+            const int64_t nxt = claim();
+            issue(nxt, sl ^ 1);
+            const int64_t q = cur & (CPC - 1), col = cur >> HB;
+            const int64_t r0 = q << kChunkL;
+            double* buf = ring + sl * kChunkDoubles;
+            if (q < nfull) {
+                tma::mbar_wait(&bar[sl], (phase >> sl) & 1u);
+                phase ^= 1u << sl;
+            } else {
+                p1_sync_load(buf, A + col * lda, n, r0);
+            }
+            // the ten low stages (as p1_transform_store_swz)
+            const int64_t rl = r0 + (lane << 5);
+            uint32_t flip = 0u;
+            if (rl < n) {
+                flip = ~__ldg(signbits + (rl >> 5));
+                if (rl + 32 > n) flip &= (1u << (n - rl)) - 1u;
+            }
+            double v[32];
+            double* row0 = buf + (lane << 4);
+            double* row1 = buf + ((32 + lane) << 4);
+            const int x = lane & 7;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const double2 a = *reinterpret_cast<const double2*>(row0 + ((u ^ x) << 1));
+                const double2 b = *reinterpret_cast<const double2*>(row1 + ((u ^ x) << 1));
+                v[2 * u] = a.x;
+                v[2 * u + 1] = a.y;
+                v[16 + 2 * u] = b.x;
+                v[17 + 2 * u] = b.y;
+            }
+#pragma unroll
+            for (int c = 0; c < 32; ++c) v[c] = flip_sign(v[c], (flip << (31 - c)) & 0x80000000u);
+#pragma unroll
+            for (int s_ = 0; s_ < 5; ++s_)
+#pragma unroll
+                for (int c = 0; c < 32; ++c)
+                    if (!(c & (1 << s_))) bfly(v[c], v[c | (1 << s_)]);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                *reinterpret_cast<double2*>(row0 + ((u ^ x) << 1)) = make_double2(v[2 * u], v[2 * u + 1]);
+                *reinterpret_cast<double2*>(row1 + ((u ^ x) << 1)) = make_double2(v[16 + 2 * u], v[17 + 2 * u]);
+            }
+            __syncwarp();
+            const double* colp = buf + ((lane >> 4) << 9) + (lane & 1);
+            const int lu = (lane & 15) >> 1;
+#pragma unroll
+            for (int c = 0; c < 32; ++c) v[c] = colp[(c << 4) + ((lu ^ (c & 7)) << 1)];
+            __syncwarp();  // the buffer may be refilled by the TMA issued next iteration
+#pragma unroll
+            for (int s_ = 0; s_ < 5; ++s_)
+#pragma unroll
+                for (int c = 0; c < 32; ++c)
+                    if (!(c & (1 << s_))) bfly(v[c], v[c | (1 << s_)]);
+            // the slot's previous column must be fully emitted before it is overwritten
+            if (col >= ns && col != slot_ok_col) {
+                if (lane == 0)
+                    while (ld_acquire(done2 + (col - ns)) < (int)P2N) __nanosleep(64);
+                __syncwarp();
+                slot_ok_col = col;
+            }
+            // element e = 32c + lane of chunk q (high index b = q) -> tile e >> LOGW, at (q & 31) 256 + (q >> 5) W
+            // + (e & (W - 1)) inside it (c-major tile: round 1 of the emitting pass loads contiguous runs)
+            double* dst = T + (col % ns) * NPAD + (q & 31) * kL2EmitThreads + (q >> 5) * W + (lane & (W - 1)) +
+                          (int64_t)(lane >> LOGW) * TE;
+#pragma unroll
+            for (int c = 0; c < 32; ++c)
+                if ((store_bits >> c) & 1u) st_hint(dst + (int64_t)(c << (5 - LOGW)) * TE, v[c], pol_last);
+            if (col != run_col) {
+                if (run_cnt > 0) {  // the previous column's chunks of this warp were stored before these
+                    __syncwarp();
+                    if (lane == 0) red_release_add(done1 + run_col, run_cnt);
+                }
+                run_col = col;
+                run_cnt = 0;
+            }
+            ++run_cnt;
+            // the run ends when the next claim is in another column (or there is none): release it now
+            if (nxt >= total || (nxt >> HB) != col) {
+                __syncwarp();
+                if (lane == 0) red_release_add(done1 + col, run_cnt);
+                run_cnt = 0;
+            }
+            sl ^= 1;
+            cur = nxt;
+        }
+        return;
+    }
+    // ---- emitting group (warps kL2P1Warps.., named barrier 1): tiles in (column, tile) order
+    const int gt = t - kL2P1Warps * 32;
+    const GroupBar gbar{1, kL2EmitThreads};
+    const int64_t total2 = d * P2N;
+    if (gt == 0) s_p2 = atomicAdd(p2_counter, 1);
+    gbar();
+    int64_t item = s_p2;
+    while (item < total2) {
+        int nxt = 0;
+        if (gt == 0) nxt = atomicAdd(p2_counter, 1);  // claimed early: its round trip overlaps this tile
+        const int64_t col = item / P2N, ti = item % P2N;
+        const int4 tile = __ldg(tiles + ti);
+        if (gt == 0)
+            while (ld_acquire(done1 + col) < CPC) __nanosleep(32);
+        gbar();
+        const double* tptr = T + (col % ns) * NPAD + (int64_t)(tile.x >> LOGW) * TE;
+        p2_tile<HB, true, GroupBar, kL2EmitThreads, true>(xs, const_cast<double*>(tptr), LOGW, true, tile, entries,
+                                                           col, s1, s2, SA, m, gt, gbar, kChunkL);
+        // thread gt loaded doubles c 256 + gt (c < 32): the 32 lines of register c of this warp's 32 threads are
+        // read by this warp only; lane l drops the two lines of c = l once the warp has consumed its loads
+        __syncwarp();
+        if (discard) {
+            const double* lines = tptr + (gt & 31) * kL2EmitThreads + (gt & ~31);
+            discard_l2(lines);
+            discard_l2(lines + 16);
+        }
+        gbar();
+        if (gt == 0) {
+            red_release_add(done2 + col, 1);
+            s_p2 = nxt;
+        }
+        gbar();
+        item = s_p2;
+    }
+}
+
 // ------------------------------------------------------------ streamed (one pass of high bits)
 // Persistent single-launch SRHT, warp-specialised: phase 1 and the emitting
 // pass run concurrently so T lives in an L2-resident ring of nslot slots x G
@@ -701,11 +951,6 @@ __global__ void __launch_bounds__(32 * kCmpU) srht_phase2_compact_kernel(const d
 // Phase-1 warps wait only for emits of earlier groups, whose chunks precede
 // theirs in every warp's order, and emitting warps never block phase-1 warps
 // of their own CTA, so the pipeline cannot deadlock for any G or nslot.
-__device__ __forceinline__ int ld_acquire(const int* p) {
-    int v;
-    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
 __device__ __forceinline__ void spin_until(const int* ctr, int target) {
     while (ld_acquire(ctr) < target) __nanosleep(100);
 }
@@ -1035,7 +1280,7 @@ const StreamFn kStream[11] = {nullptr,          launch_stream<1>, launch_stream<
                               launch_stream<4>, launch_stream<5>, launch_stream<6>, launch_stream<7>,
                               launch_stream<8>, launch_stream<9>, launch_stream<10>};
 using PassFn = void (*)(const SrhtPlan&, double*, int, const int4*, int, bool, const int2*, double*, cudaStream_t);
-const PassFn kPass[11] = {nullptr,
+const PassFn kPass[13] = {nullptr,
                           launch_pass<1, 256>,
                           launch_pass<2, 256>,
                           launch_pass<3, 256>,
@@ -1045,7 +1290,9 @@ const PassFn kPass[11] = {nullptr,
                           launch_pass<7, 256>,
                           launch_pass<8, 256>,
                           launch_pass<9, 256>,
-                          launch_pass<10, 256>};
+                          launch_pass<10, 256>,
+                          launch_pass<11, 256>,
+                          launch_pass<12, 256>};
 const PassFn kPass512[13] = {nullptr,
                              launch_pass<1, 512>,
                              launch_pass<2, 512>,
@@ -1109,7 +1356,11 @@ SrhtPlan srht_plan(int64_t n, int64_t d, int64_t lda, int64_t m) {
             p.pass_hb[0] = p.H;
             p.scale1 = 1.0 / std::sqrt(static_cast<double>(np));
             p.scale2 = std::sqrt(static_cast<double>(np) / static_cast<double>(m));
-            p.p2t = 512;
+            static const int p2t_env = [] {  // IHS_SRHT_P2T=256: 256-thread three-round tiles (A/B)
+                const char* e = std::getenv("IHS_SRHT_P2T");
+                return e ? std::atoi(e) : 0;
+            }();
+            p.p2t = p2t_env == 256 ? 256 : 512;
             p.stream = 0;
             p.compact = 0;
             return p;
@@ -1158,6 +1409,30 @@ void srht_combine(const double* d_U, int P, int64_t m, int64_t d, const uint8_t*
 }
 
 size_t srht_scratch_bytes(const SrhtPlan& p) { return p.H > 0 ? (size_t)p.n_pad * (size_t)p.d * sizeof(double) : 0; }
+
+bool srht_plan_l2(SrhtPlan& p) {
+    // opt-in (IHS_SRHT_L2=1; IHS_SRHT_L2_NS sets the ring depth): T stays in L2 and HBM sees only A and SA
+    // (ncu: 68.8 GB read + 2.2 GB written per C4 sketch, the algorithmic bytes), but the emitting tiles then
+    // bound the sketch and it measured slower than the two-kernel path (C4 m = 131072: 69 vs 59 ms; C3: 7.7 vs
+    // 6.9 ms), so the two-kernel path stays the default
+    static const bool disabled = [] {
+        const char* e = std::getenv("IHS_SRHT_L2");
+        return !(e && e[0] == '1');
+    }();
+    static const int ns_env = [] {
+        const char* e = std::getenv("IHS_SRHT_L2_NS");
+        return e ? std::atoi(e) : 0;
+    }();
+
+    if (disabled || p.H < 8 || p.H > 12 || p.npass != 1 || p.compact || p.stream) return false;
+    p.l2 = 1;
+    p.p2t = kL2EmitThreads;
+    const int64_t col_bytes = p.n_pad * (int64_t)sizeof(double);
+    p.l2_ns = ns_env > 0 ? ns_env : (int)std::max<int64_t>(2, std::min<int64_t>(8, (64ll << 20) / col_bytes));
+    return true;
+}
+size_t srht_l2_scratch_bytes(const SrhtPlan& p) { return (size_t)p.l2_ns * (size_t)p.n_pad * sizeof(double); }
+size_t srht_l2_ctl_bytes(const SrhtPlan& p) { return (size_t)(2 + 2 * p.d) * sizeof(int) + 64; }
 
 bool srht_plan_compact(SrhtPlan& p, const int64_t* rows) {
     // IHS_SRHT_NO_COMPACT=1 disables it; IHS_SRHT_COMPACT_MAX overrides the distinct-low-index limit
@@ -1243,6 +1518,14 @@ void srht_build_entries(const SrhtPlan& p, const int64_t* rows, std::vector<int2
             const int64_t base = ((t % low_tiles) * W) | ((t / low_tiles) << (lo + hb));
             tiles.push_back(make_int4((int)base, count[(size_t)t], count[(size_t)t + 1], 0));
         }
+    if (p.l2) {  // occupancy bits of the (<= 512) low-index tiles, packed into 4 trailing int4
+        uint32_t bits[16] = {};
+        for (int64_t t = 0; t < ntiles; ++t)
+            if (count[(size_t)t + 1] > count[(size_t)t]) bits[t >> 5] |= 1u << (t & 31);
+        const size_t b0 = tiles.size();
+        tiles.resize(b0 + 4);
+        std::memcpy(tiles.data() + b0, bits, sizeof(bits));
+    }
 }
 
 bool srht_plan_stream(SrhtPlan& p, int num_sms) {
@@ -1277,10 +1560,41 @@ bool srht_build_mask(const SrhtPlan& p, const std::vector<int4>& tiles, uint32_t
     return true;
 }
 
+template <int HB>
+void launch_l2(const SrhtPlan& p, const ChunkMaps& maps, int64_t nfull, const double* A, const uint32_t* signbits,
+               double* T, const int4* tiles, int n_tiles, const int2* entries, double* SA, int* ctl, int num_sms,
+               cudaStream_t st) {
+    IHS_SMEM_ATTR(srht_l2_kernel<HB>, (int)kL2Smem);
+    static const bool discard = [] {  // IHS_SRHT_L2_DISCARD=0: keep the consumed T lines (A/B of the discard)
+        const char* e = std::getenv("IHS_SRHT_L2_DISCARD");
+        return !(e && e[0] == '0');
+    }();
+    CUDA_CHECK(cudaMemsetAsync(ctl, 0, srht_l2_ctl_bytes(p), st));
+    const uint32_t* bits = reinterpret_cast<const uint32_t*>(tiles + n_tiles);
+    // one CTA per SM; all must be co-resident (the warps wait on each other's progress), which the
+    // launch-bounds/smem footprint guarantees for a grid of num_sms
+    LAUNCH_PDL(srht_l2_kernel<HB>, (unsigned)num_sms, kL2Threads, kL2Smem, st, maps, A, p.n, p.lda, signbits, T, nfull,
+               p.d, p.l2_ns, tiles, n_tiles, bits, entries, p.scale1, p.scale2, SA, p.m, ctl, discard ? 1 : 0);
+}
+using L2Fn = void (*)(const SrhtPlan&, const ChunkMaps&, int64_t, const double*, const uint32_t*, double*, const int4*,
+                      int, const int2*, double*, int*, int, cudaStream_t);
+const L2Fn kL2[13] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+                      launch_l2<8>, launch_l2<9>, launch_l2<10>, launch_l2<11>, launch_l2<12>};
+
 void srht_run_device(const SrhtPlan& p, const double* d_A, const uint32_t* d_signbits, const int2* d_entries,
                      const int4* d_tiles, int n_tiles, double* d_T, double* d_SA, cudaStream_t st,
                      unsigned long long* d_ctl, int num_sms, const uint32_t* d_mask) {
     if (p.d == 0) return;
+    if (p.l2) {
+        ChunkMaps maps{};
+        const int64_t nfull = p.n >> kChunkL;
+        if (!(nfull > 0 && srht_chunk_maps(d_A, p.lda, nfull, p.d, &maps)))
+            fail(IHS_INTERNAL_ERROR, "srht: the L2-resident launch needs TMA chunk maps");
+        if (n_tiles > 0)
+            kL2[p.H](p, maps, nfull, d_A, d_signbits, d_T, d_tiles, n_tiles, d_entries, d_SA,
+                     reinterpret_cast<int*>(d_ctl), num_sms, st);
+        return;
+    }
     if (p.H == 0) {
         kSmall[p.L](p, d_A, d_signbits, d_entries, d_SA, st);
         return;

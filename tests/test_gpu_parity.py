@@ -189,7 +189,10 @@ def test_system_known_answers(gpu):
     np.testing.assert_allclose(sys.solve(np.ones(3)), [0.5, 1.0, 1.0], rtol=1e-14)
 
 
-@pytest.mark.parametrize("m,d", [(4, 6), (9, 5), (6, 20), (20, 6), (8, 8), (300, 257), (100, 513), (2000, 700)])
+@pytest.mark.parametrize("m,d", [(4, 6), (9, 5), (6, 20), (20, 6), (8, 8), (300, 257), (100, 513), (2000, 700),
+                                 # 128x128 DMMA kernels: Gram TN + W^T W (lower tiles, ragged edges), inner NT,
+                                 # odd leading dimension (falls back to the 64x64 kernel)
+                                 (4096, 512), (5000, 1300), (300, 2048), (1500, 1100), (4095, 300)])
 def test_system_solve_vs_oracle(gpu, O, m, d):
     SA = rand_mat(m * d, m, d)
     g = RNG(m + d).standard_normal(d)
@@ -378,6 +381,42 @@ def test_nccl_single_rank_communicator(gpu):
     comm = gpu.NcclComm(uid, 1, 0, 0)
     assert comm.handle
     del comm
+
+
+# n_pad = 2^18 .. 2^22 (8 .. 12 high bits): ragged n (partial and virtual chunks), d above the L2-resident
+# launch's ring depth, sparse and dense tile occupancy
+@pytest.mark.parametrize("n,d,m,seed", [((1 << 18) + 7, 9, 5000, 21), ((1 << 19) - 1, 6, 300, 22),
+                                        ((1 << 20) - 3, 11, 30000, 23), ((1 << 21) + 3, 5, 70000, 24),
+                                        ((1 << 22) - 3, 4, 131072, 25), ((1 << 22), 3, 9, 26)])
+def test_srht_l2_resident_bit_exact(gpu, O, n, d, m, seed):
+    A = rand_mat(seed, n, d)
+    assert np.array_equal(gpu.srht_sketch(A, m, seed), O.srht_sketch(A, m, seed))
+
+
+def test_srht_l2_ring_depths_and_two_kernel_path_agree(gpu):
+    """The opt-in L2-resident launch (IHS_SRHT_L2=1) at ring depths 2 and 3 (every slot reused), with sparse
+    tiles at n_pad = 2^20 (compact T disabled), at 2^22 rows, and the default two-kernel path all give the
+    oracle's bytes."""
+    import os
+    import subprocess
+    import sys
+    code = ("import numpy as np\n"
+            "from paper_2006_05874_b200 import ihs\n"
+            "from oracle import oracle as O\n"
+            "rng = np.random.default_rng(10)\n"
+            "A = np.asfortranarray(rng.standard_normal(((1 << 20) - 77, 7)))\n"
+            "for m in (5, 900, 40000):\n"
+            "    assert np.array_equal(ihs.srht_sketch(A, m, 3 + m), O.srht_sketch(A, m, 3 + m)), m\n"
+            "B = np.asfortranarray(rng.standard_normal(((1 << 22) - 3, 3)))\n"
+            "for m in (9, 131072):\n"
+            "    assert np.array_equal(ihs.srht_sketch(B, m, 4 + m), O.srht_sketch(B, m, 4 + m)), m\n"
+            "print('ok')\n")
+    root = str(__import__("pathlib").Path(__file__).resolve().parents[1])
+    for extra in ({"IHS_SRHT_L2": "1", "IHS_SRHT_L2_NS": "2"},
+                  {"IHS_SRHT_L2": "1", "IHS_SRHT_L2_NS": "3", "IHS_SRHT_NO_COMPACT": "1"}, {}):
+        env = dict(os.environ, **extra)
+        r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300, env=env, cwd=root)
+        assert r.returncode == 0 and "ok" in r.stdout, (extra, r.stderr[-2000:])
 
 
 def test_srht_column_batches_bit_exact(gpu):
