@@ -215,6 +215,10 @@ ihs_status ihs_gpu_nccl_unique_id(uint8_t out[128]);
 ihs_status ihs_gpu_nccl_comm_create(const uint8_t id[128], int32_t world_size, int32_t rank, int32_t device,
                                     void** comm);
 void ihs_gpu_nccl_comm_destroy(void* comm);
+/* world_size EMULATED ranks of this process (comms[r] for rank r; free each with ihs_gpu_nccl_comm_destroy):
+ * the row-sharded code runs unchanged with one host thread per rank, collectives become host barriers plus
+ * device copies ordered by events (tests and single-GPU development of the sharded path). */
+ihs_status ihs_gpu_emu_comm_create(int32_t world_size, int32_t device, void** comms);
 /* The sharded SRHT decomposition run back to back on one device (P virtual
  * shards of a single-GPU problem): proves the decomposition bit-exact. */
 ihs_status ihs_gpu_sketch_sharded_emulated(ihs_gpu_problem* p, int32_t kind, int64_t m, uint64_t seed,

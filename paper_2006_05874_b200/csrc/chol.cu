@@ -752,13 +752,15 @@ size_t cholesky_diag_inv_doubles(int64_t n) {
 // One cooperative launch for the whole factorization (see chol_coop_kernel); false when the device
 // cannot co-schedule the grid (the caller then uses the per-panel kernels).
 bool cholesky_factor_coop(double* d_H, int64_t n, double* d_Xd, int* d_info, int num_sms, cudaStream_t st) {
-    static int per_sm = -1;
+    static std::atomic<int> per_sm_cache{-1};
+    int per_sm = per_sm_cache.load();
     if (per_sm < 0) {
         int supported = 0, dev = 0;
         CUDA_CHECK(cudaGetDevice(&dev));
         CUDA_CHECK(cudaDeviceGetAttribute(&supported, cudaDevAttrCooperativeLaunch, dev));
         per_sm = 0;
         if (supported) CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, chol_coop_kernel, CTHREADS, 0));
+        per_sm_cache.store(per_sm);
     }
     if (per_sm < 1) return false;
     CUDA_CHECK(cudaMemsetAsync(d_info, 0, sizeof(int), st));

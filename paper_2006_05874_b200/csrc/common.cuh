@@ -162,6 +162,8 @@ void srht_combine(const double* d_U, int P, int64_t m, int64_t d, const uint8_t*
 void nccl_unique_id(uint8_t out[128]);
 void* nccl_comm_create(const uint8_t id[128], int world, int rank);
 void nccl_comm_destroy(void* comm);
+// world_size emulated ranks of this process (out[r] = rank r's communicator; host threads drive the ranks)
+void emu_comm_create(int world, void** out);
 void nccl_allreduce_sum(double* buf, size_t count, void* comm, cudaStream_t st);
 void nccl_allgather(const double* send, double* recv, size_t count_per_rank, void* comm, cudaStream_t st);
 

@@ -1066,6 +1066,14 @@ ihs_status ihs_gpu_nccl_comm_create(const uint8_t id[128], int32_t world_size, i
     });
 }
 
+ihs_status ihs_gpu_emu_comm_create(int32_t world_size, int32_t device, void** comms) {
+    return guarded([&] {
+        if (!comms || world_size < 1 || world_size > 64) fail(IHS_INVALID_INPUT, "emu_comm_create: bad arguments");
+        DeviceGuard g(device);
+        emu_comm_create(world_size, comms);
+    });
+}
+
 void ihs_gpu_nccl_comm_destroy(void* comm) {
     try {
         nccl_comm_destroy(comm);

@@ -31,6 +31,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cmath>
+#include <mutex>
 #include <vector>
 
 namespace ihs_b200 {
@@ -1195,6 +1196,8 @@ bool srht_chunk_maps(const double* A, int64_t lda, int64_t nfull, int64_t d, Chu
         ChunkMaps maps;
     };
     static std::vector<Entry> cache;
+    static std::mutex mu;  // rank threads of an emulated group share the process
+    std::lock_guard<std::mutex> lock(mu);
     for (const Entry& e : cache)
         if (e.A == A && e.lda == lda && e.nfull == nfull && e.d == d) {
             *out = e.maps;

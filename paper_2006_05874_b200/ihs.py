@@ -278,6 +278,34 @@ class NcclComm:
             self.handle = None
 
 
+class EmuComm:
+    """One rank's communicator of an EMULATED group (ihs_gpu_emu_comm_create): world_size ranks of this process,
+    each driven by its own host thread, run the library's real row-sharded code on one device; collectives are
+    host barriers plus device copies. Use EmuComm.group(world_size) and one thread per rank."""
+
+    def __init__(self, handle, group):
+        self.handle = handle
+        self._group = group  # keeps the sibling handles alive together
+
+    @staticmethod
+    def group(world_size: int, device: int = 0):
+        arr = (C.c_void_p * world_size)()
+        _check(lib().ihs_gpu_emu_comm_create(world_size, device, arr))
+        grp = _EmuGroup([arr[r] for r in range(world_size)])
+        return [EmuComm(C.c_void_p(arr[r]), grp) for r in range(world_size)]
+
+
+class _EmuGroup:
+    def __init__(self, handles):
+        self.handles = handles
+
+    def __del__(self):
+        for h in self.handles:
+            if h:
+                lib().ihs_gpu_nccl_comm_destroy(h)
+        self.handles = []
+
+
 class ProblemInstance:
     """A regularized least-squares instance, uploaded to the device once.
 

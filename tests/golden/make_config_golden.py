@@ -2,7 +2,7 @@
 """Golden adaptive solves of the BASELINE configs at n/16 (tests/golden/configs_n16.npz).
 
 SURVEY §8(d): parity for C3-C5 runs on down-scaled instances — the same seeded generator, d, nu and sigma,
-n / 16 rows — where a single-thread CPU solve completes. Each case is solved here by the CPU oracle (pinned
+n / 16 rows (n / 64 for the Gaussian C4) — where a single-thread CPU solve completes. Each case is solved here by the CPU oracle (pinned
 bit-for-bit to the reference's own headers by tests/test_ref_pin.py; the configs' dense algebra makes a
 reference-stub run of C4/C5 take hours) and the audit trail, counters and final iterate are committed; the GPU
 test (tests/test_gpu_configs.py) regenerates the same data on the box (ihs.synth_generate, bit-exact with the
@@ -26,7 +26,8 @@ CASES = [
     ("c3_n16_default", "c3", 1 << 16, dict(m_initial=1, eps=1e-10)),
     ("c3_n16_norecompute", "c3", 1 << 16, dict(recompute_r_after_resketch=0)),
     ("c4_n16", "c4", 1 << 18, {}),
-    ("c4g_n16", "c4g", 1 << 18, dict(m_initial=4096, max_sketch=4096)),  # S = 4096 x 2^18 (8 GiB) on the host
+    # C4-Gaussian at n/64: the oracle's S*A at m = 8192 and n/16 would take hours single-threaded
+    ("c4g_n64", "c4g", 1 << 16, dict(m_initial=4096, max_sketch=8192)),
     ("c5_n16", "c5", 62500, {}),
 ]
 

@@ -1,0 +1,102 @@
+"""The library's REAL row-sharded code path (world_size > 1) on one device: P emulated ranks
+(ihs_gpu_emu_comm_create), one host thread per rank, each with its own problem handle on its shard of the rows
+(ihs.shard_rows: rows [r n_loc, (r+1) n_loc) of the padded index space) — the sharded SRHT transform and
+exchange, the Gaussian sketch window + all-reduce, the gradient all-reduce and a full adaptive_solve, exactly as
+`bench.py --gpus N` runs them over NCCL, with device copies standing in for NCCL (no kernel waits on another).
+
+Checks (sketch.hpp:58-108, problem.hpp:59-69, solver.hpp:106-232):
+* every rank holds the same bytes after each collective (SA, gradients, the solution);
+* the sharded SRHT sketch equals the single-GPU (and oracle) sketch bit for bit;
+* Gaussian sketches / gradients equal the single-GPU ones to fp64 tolerance (partial sums in another order);
+* the sharded adaptive solve takes the single-GPU solve's m-schedule, branches and counters and returns x within
+  1e-10 of it in the Abar norm.
+"""
+import threading
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _run_ranks(P, fn):
+    out, err = [None] * P, []
+
+    def body(r):
+        try:
+            out[r] = fn(r)
+        except Exception as e:  # noqa: BLE001
+            err.append((r, e))
+
+    th = [threading.Thread(target=body, args=(r,)) for r in range(P)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=600)
+    assert not any(t.is_alive() for t in th), "a rank thread hung"
+    assert not err, err
+    return out
+
+
+def _shards(gpu, A, b, nu, P):
+    n = A.shape[0]
+    comms = gpu.EmuComm.group(P)
+    probs = []
+    for r in range(P):
+        row0, rows = gpu.shard_rows(n, P, r)
+        probs.append(gpu.ProblemInstance(np.asfortranarray(A[row0:row0 + rows]), b[row0:row0 + rows].copy(), nu,
+                                         world_size=P, rank=r, comm=comms[r], n_global=n))
+    return comms, probs
+
+
+def _abar_rel(A, nu, x, xr):
+    num = np.linalg.norm(np.concatenate([A @ (x - xr), nu * (x - xr)]))
+    den = np.linalg.norm(np.concatenate([A @ xr, nu * xr]))
+    return num / den
+
+
+@pytest.mark.parametrize("P", [2, 4, 8])
+def test_sharded_sketches_and_gradient(gpu, O, P):
+    n, d = 60000, 24  # n_pad = 65536: every rank holds rows, the last one a ragged block
+    A, b, _ = gpu.synth_generate(n, d, decay=0.95, noise_std=0.01, data_seed=5)
+    nu = 1e-2
+    comms, probs = _shards(gpu, A, b, nu, P)
+    single = gpu.ProblemInstance(A, b, nu)
+    x = np.random.default_rng(P).standard_normal(d)
+
+    def work(r):
+        p = probs[r]
+        return (gpu.srht_sketch(p, 3000, 7), gpu.srht_sketch(p, 64, 8), gpu.gaussian_sketch(p, 200, 9),
+                gpu.gradient(p, x))
+
+    res = _run_ranks(P, work)
+    for r in range(1, P):
+        for a, b_ in zip(res[0], res[r]):
+            assert np.array_equal(a, b_), f"rank {r} differs from rank 0"
+    SA_s, SA_s2, SA_g, g = res[0]
+    assert np.array_equal(SA_s, O.srht_sketch(A, 3000, 7))
+    assert np.array_equal(SA_s2, gpu.srht_sketch(single, 64, 8))
+    ref = gpu.gaussian_sketch(single, 200, 9)
+    assert np.max(np.abs(SA_g - ref)) <= 1e-12 * np.max(np.abs(ref))
+    g1 = gpu.gradient(single, x)
+    assert np.max(np.abs(g - g1)) <= 1e-12 * np.max(np.abs(g1))
+    del probs, comms
+
+
+@pytest.mark.parametrize("P,kind", [(2, "SRHT"), (4, "SRHT"), (8, "SRHT"), (2, "Gaussian"), (4, "Gaussian")])
+def test_sharded_adaptive_solve(gpu, P, kind):
+    n, d = 60000, 48
+    A, b, _ = gpu.synth_generate(n, d, decay=0.97, noise_std=0.01, data_seed=6)
+    nu = 1e-3
+    cfg = gpu.SolverConfig(sketch_kind=getattr(gpu.SketchKind, kind), m_initial=2 * d, eps=1e-21, seed=3)
+    comms, probs = _shards(gpu, A, b, nu, P)
+    reps = _run_ranks(P, lambda r: gpu.adaptive_solve(probs[r], cfg))
+    ref = gpu.adaptive_solve(gpu.ProblemInstance(A, b, nu), cfg)
+    for r in range(P):
+        assert np.array_equal(reps[r].x, reps[0].x)
+        assert [(e.t, e.m, int(e.branch)) for e in reps[r].log] == [(e.t, e.m, int(e.branch)) for e in ref.log]
+        c, c1 = reps[r].counters, ref.counters
+        assert (c.sketch, c.factor, c.solve, c.matvec) == (c1.sketch, c1.factor, c1.solve, c1.matvec)
+    assert reps[0].converged and reps[0].iterations > 1
+    assert _abar_rel(A, nu, reps[0].x, ref.x) <= 1e-10
+    del probs, comms
