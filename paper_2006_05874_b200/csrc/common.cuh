@@ -111,6 +111,7 @@ void mt_gaussian_stream(uint64_t seed, int64_t first, int64_t count, double stdd
 // srht.cu — SRHT sketch SA = sqrt(n_pad/m) R H D A (sketch.hpp:77-108)
 struct SrhtPlan {
     int64_t n, d, lda, n_pad, m;
+    int64_t sa_ld;           // stride between SA columns (m; rows-per-owner for the sharded owner-block layout)
     int logn, L, H;          // n_pad = 2^logn, low bits L done in phase 1, H = logn - L
     int npass;               // phase-2 passes over the H high bits (<= 10 bits each)
     int pass_lo[3], pass_hb[3];
@@ -157,6 +158,8 @@ bool srht_build_mask(const SrhtPlan& p, const std::vector<int4>& tiles, uint32_t
 SrhtPlan srht_plan_shard(int64_t n_real, int64_t n_loc, int64_t d, int64_t lda, int64_t m);
 void srht_combine(const double* d_U, int P, int64_t m, int64_t d, const uint8_t* d_hi, double s1, double s2,
                   double* d_SA, cudaStream_t st);
+// owner-block layout G[q][kk + j mq] (rows k = q mq + kk of owner q) -> SA[k + j m], k < m
+void srht_unpack_blocks(const double* d_G, int P, int64_t mq, int64_t m, int64_t d, double* d_SA, cudaStream_t st);
 
 // nccl_comm.cpp — collectives of the row-sharded path (NCCL loaded at run time)
 void nccl_unique_id(uint8_t out[128]);
@@ -166,6 +169,8 @@ void nccl_comm_destroy(void* comm);
 void emu_comm_create(int world, void** out);
 void nccl_allreduce_sum(double* buf, size_t count, void* comm, cudaStream_t st);
 void nccl_allgather(const double* send, double* recv, size_t count_per_rank, void* comm, cudaStream_t st);
+// all-to-all: block p of send (count doubles) goes to rank p, block p of recv comes from rank p
+void nccl_alltoall(const double* send, double* recv, size_t count_per_rank, void* comm, cudaStream_t st);
 
 // gemm_f64.cu — DMMA (mma.sync m8n8k4 f64) GEMM
 // C[M x N] (ldc) = alpha * op(A) * op(B) + beta * C ; op(A) is M x K, op(B) K x N.

@@ -28,6 +28,10 @@ struct NcclApi {
     ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
     ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
     const char* (*GetErrorString)(ncclResult_t) = nullptr;
     bool ok = false;
 };
@@ -45,7 +49,12 @@ NcclApi& api() {
         a.AllReduce = reinterpret_cast<decltype(a.AllReduce)>(dlsym(h, "ncclAllReduce"));
         a.AllGather = reinterpret_cast<decltype(a.AllGather)>(dlsym(h, "ncclAllGather"));
         a.GetErrorString = reinterpret_cast<decltype(a.GetErrorString)>(dlsym(h, "ncclGetErrorString"));
-        a.ok = a.GetUniqueId && a.CommInitRank && a.CommDestroy && a.AllReduce && a.AllGather && a.GetErrorString;
+        a.Send = reinterpret_cast<decltype(a.Send)>(dlsym(h, "ncclSend"));
+        a.Recv = reinterpret_cast<decltype(a.Recv)>(dlsym(h, "ncclRecv"));
+        a.GroupStart = reinterpret_cast<decltype(a.GroupStart)>(dlsym(h, "ncclGroupStart"));
+        a.GroupEnd = reinterpret_cast<decltype(a.GroupEnd)>(dlsym(h, "ncclGroupEnd"));
+        a.ok = a.GetUniqueId && a.CommInitRank && a.CommDestroy && a.AllReduce && a.AllGather && a.GetErrorString &&
+               a.Send && a.Recv && a.GroupStart && a.GroupEnd;
     });
     if (!a.ok) fail(IHS_NCCL_ERROR, "libnccl.so.2 could not be loaded");
     return a;
@@ -157,6 +166,15 @@ void emu_allgather(Comm* c, const double* send, double* recv, size_t count, cuda
     emu_finish(c, st);
 }
 
+void emu_alltoall(Comm* c, const double* send, double* recv, size_t count, cudaStream_t st) {
+    EmuGroup& g = *c->grp;
+    emu_post(c, send, st);
+    for (int p = 0; p < g.world; ++p)  // block `rank` of rank p's send buffer
+        CUDA_CHECK(cudaMemcpyAsync(recv + (size_t)p * count, g.src[p] + (size_t)c->rank * count, count * sizeof(double),
+                                   cudaMemcpyDeviceToDevice, st));
+    emu_finish(c, st);
+}
+
 void nccl_unique_id(uint8_t out[128]) {
     ncclUniqueId id;
     check(api().GetUniqueId(&id), "ncclGetUniqueId");
@@ -205,6 +223,18 @@ void nccl_allgather(const double* send, double* recv, size_t count_per_rank, voi
     auto* c = static_cast<Comm*>(comm);
     if (c->emulated) return emu_allgather(c, send, recv, count_per_rank, st);
     check(api().AllGather(send, recv, count_per_rank, ncclFloat64, c->nccl, st), "ncclAllGather");
+}
+
+void nccl_alltoall(const double* send, double* recv, size_t count_per_rank, void* comm, cudaStream_t st) {
+    auto* c = static_cast<Comm*>(comm);
+    if (c->emulated) return emu_alltoall(c, send, recv, count_per_rank, st);
+    NcclApi& a = api();
+    check(a.GroupStart(), "ncclGroupStart");
+    for (int p = 0; p < c->world; ++p) {
+        check(a.Send(send + (size_t)p * count_per_rank, count_per_rank, ncclFloat64, p, c->nccl, st), "ncclSend");
+        check(a.Recv(recv + (size_t)p * count_per_rank, count_per_rank, ncclFloat64, p, c->nccl, st), "ncclRecv");
+    }
+    check(a.GroupEnd(), "ncclGroupEnd");
 }
 
 }  // namespace ihs_b200

@@ -432,11 +432,18 @@ void device_sketch(ihs_gpu_problem* P, int kind, int64_t m, uint64_t seed, doubl
             P->mask_valid = srht_build_mask(sp, P->h_tiles, P->h_mask);
             g_host_rng_ns +=
                 std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t_rng).count();
-            upload_entries(P);
-            P->shard_hi.ensure((size_t)m + 16);
-            CUDA_CHECK(cudaMemcpyAsync(P->shard_hi.p, hi.data(), (size_t)m, cudaMemcpyHostToDevice, st));
+            if (world <= 1) upload_entries(P);  // (the sharded exchange remaps the entries first)
+            // r_hi(k), zero-padded to whole owner blocks
+            const int64_t mq_pad = ceil_div(m, shards) * shards;
+            hi.resize((size_t)mq_pad, 0);
+            P->shard_hi.ensure((size_t)mq_pad + 16);
+            CUDA_CHECK(cudaMemcpyAsync(P->shard_hi.p, hi.data(), (size_t)mq_pad, cudaMemcpyHostToDevice, st));
             ensure_A(P);
-            P->shard_U.ensure((size_t)shards * m * d * sizeof(double));
+            // emulated shards: [P][m][d] partials; a rank of a sharded problem: send/recv owner blocks, its own
+            // combined block and the gathered blocks ((2 P + 1 + P) mq d doubles)
+            const int64_t mq = ceil_div(m, shards);
+            P->shard_U.ensure(world > 1 ? (size_t)(3 * shards + 1) * mq * d * sizeof(double)
+                                        : (size_t)shards * m * d * sizeof(double));
             unsigned long long* ctl = srht_prepare_scratch(P, sp);
             double* U = P->shard_U.d();
             auto run_shard = [&](int p, const double* A_p, int64_t n_real) {
@@ -447,16 +454,40 @@ void device_sketch(ihs_gpu_problem* P, int kind, int64_t m, uint64_t seed, doubl
                                 ctl, P->num_sms, P->mask_valid ? P->srht_mask.as<uint32_t>() : nullptr);
             };
             if (world > 1) {
+                // owner-reduce exchange (per rank ~2 m d doubles received instead of the P m d of an all-gather of
+                // the partials): rank q owns sampled rows [q mq, (q+1) mq). The shard's emitting pass writes its
+                // partials straight into owner blocks (entries remapped to q mq d + kk, column stride mq); an
+                // all-to-all hands every owner the P partials of its rows, the owner combines them in the
+                // reference's butterfly order (bit-exact), and an all-gather + unpack assemble SA on every rank.
                 const int r = P->opts.rank;
-                run_shard(r, P->A.d(), n);
-                nccl_allgather(U + (int64_t)r * m * d, U, (size_t)(m * d), P->opts.nccl_comm, st);
+                const int64_t mq = ceil_div(m, world);
+                for (int2& e : P->h_entries) {
+                    const int64_t k = e.y, q = k / mq;
+                    e.y = (int)(q * mq * d + (k - q * mq));
+                }
+                upload_entries(P);
+                double* send = U;                                  // [q][mq x d] partial blocks
+                double* recv = U + (int64_t)world * mq * d;        // [p][mq x d] partials of my rows
+                double* own = recv + (int64_t)world * mq * d;      // my combined rows (mq x d)
+                double* gathered = own + mq * d;                   // [q][mq x d] combined blocks
+                SrhtPlan s = sp;
+                s.n = n;
+                s.sa_ld = mq;
+                srht_run_device(s, P->A.d(), P->signbits.as<uint32_t>() + (r * n_loc) / 32, P->entries.as<int2>(),
+                                P->tiles.as<int4>(), (int)P->h_tiles.size(), P->T.d(), send, st, ctl, P->num_sms,
+                                P->mask_valid ? P->srht_mask.as<uint32_t>() : nullptr);
+                nccl_alltoall(send, recv, (size_t)(mq * d), P->opts.nccl_comm, st);
+                srht_combine(recv, world, mq, d, P->shard_hi.as<uint8_t>() + (int64_t)r * mq, plan.scale1, plan.scale2,
+                             own, st);
+                nccl_allgather(own, gathered, (size_t)(mq * d), P->opts.nccl_comm, st);
+                srht_unpack_blocks(gathered, world, mq, m, d, d_SA, st);
             } else {
                 for (int p = 0; p < shards; ++p) {
                     const int64_t n_real = std::max<int64_t>(0, std::min<int64_t>(n_loc, n - p * n_loc));
                     run_shard(p, P->A.d() + p * n_loc, n_real);
                 }
+                srht_combine(U, shards, m, d, P->shard_hi.as<uint8_t>(), plan.scale1, plan.scale2, d_SA, st);
             }
-            srht_combine(U, shards, m, d, P->shard_hi.as<uint8_t>(), plan.scale1, plan.scale2, d_SA, st);
         }
         if (c) {  // sketch.hpp:99-106
             const uint64_t np = (uint64_t)plan.n_pad, dd = (uint64_t)d;

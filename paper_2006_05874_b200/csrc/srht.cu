@@ -1160,7 +1160,7 @@ void launch_small(const SrhtPlan& p, const double* A, const uint32_t* signbits, 
     constexpr int THREADS = N / 16 > 0 ? N / 16 : 1;
     const size_t smem = (size_t)padded(N) * sizeof(double) + 64;
     LAUNCH_PDL(srht_small_kernel<L>, (unsigned)p.d, THREADS, smem, st, A, p.n, p.lda, signbits, entries, (int)p.m,
-           p.scale1, p.scale2, SA, p.m);
+           p.scale1, p.scale2, SA, p.sa_ld);
 }
 using SmallFn = void (*)(const SrhtPlan&, const double*, const uint32_t*, const int2*, double*, cudaStream_t);
 const SmallFn kSmall[kSmallL + 1] = {launch_small<0>, launch_small<1>, launch_small<2>, launch_small<3>,
@@ -1177,7 +1177,7 @@ void launch_pass(const SrhtPlan& p, double* T, int lo, const int4* tiles, int n_
     if (gx == 0) return;
     dim3 grid(gx, (unsigned)p.d);
     LAUNCH_PDL((srht_phase2_kernel<HB, TH>), grid, TH, smem, st, T, p.n_pad, lo, tiles, emit ? 1 : 0, entries, p.scale1,
-           p.scale2, SA, p.m);
+           p.scale2, SA, p.sa_ld);
 }
 
 // Tensor maps of the full 1024-row chunks of A (even / odd 128-byte rows of
@@ -1263,7 +1263,7 @@ void launch_stream(const SrhtPlan& p, const ChunkMaps& maps, int64_t nfull, cons
     if (prof_on) CUDA_CHECK(cudaMemsetAsync(prof, 0, 16 * sizeof(unsigned long long), st));
     LAUNCH_PDL(srht_stream_kernel<HB>, (unsigned)grid, kStreamThreads, kStreamSmem, st, maps, A, p.n, p.lda, nfull,
            signbits, T, p.n_pad, p.d, p.logn - kChunkL, G, nslot, ng, tiles, n_tiles, entries, p.pass_lo[0], p.scale1,
-           p.scale2, SA, p.m, ctl, mask, logw, stream_dbg(), prof_on ? prof : nullptr);
+           p.scale2, SA, p.sa_ld, ctl, mask, logw, stream_dbg(), prof_on ? prof : nullptr);
     if (prof_on) {
         unsigned long long h[16];
         CUDA_CHECK(cudaMemcpyAsync(h, prof, sizeof(h), cudaMemcpyDeviceToHost, st));
@@ -1338,6 +1338,7 @@ SrhtPlan srht_plan(int64_t n, int64_t d, int64_t lda, int64_t m) {
     p.d = d;
     p.lda = lda;
     p.m = m;
+    p.sa_ld = m;
     int64_t np = 1;
     int logn = 0;
     while (np < n) { np <<= 1; ++logn; }
@@ -1409,6 +1410,23 @@ void srht_combine(const double* d_U, int P, int64_t m, int64_t d, const uint8_t*
         case 16: LAUNCH_PDL(srht_combine_kernel<4>, blocks, 256, 0, st, d_U, m, d, d_hi, s1, s2, d_SA); break;
         default: fail(IHS_INVALID_INPUT, "srht shard: number of shards must be 1, 2, 4, 8 or 16");
     }
+}
+
+__global__ void srht_unpack_kernel(const double* __restrict__ G, int64_t mq, int64_t m, int64_t d,
+                                   double* __restrict__ SA) {
+    pdl_wait();
+    const int64_t md = m * d;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < md; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t k = e % m, j = e / m;
+        const int64_t q = k / mq, kk = k - q * mq;
+        SA[e] = G[q * mq * d + kk + j * mq];
+    }
+}
+
+void srht_unpack_blocks(const double* d_G, int P, int64_t mq, int64_t m, int64_t d, double* d_SA, cudaStream_t st) {
+    (void)P;
+    const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(m * d, 256), 148 * 16));
+    LAUNCH_PDL(srht_unpack_kernel, blocks, 256, 0, st, d_G, mq, m, d, d_SA);
 }
 
 size_t srht_scratch_bytes(const SrhtPlan& p) { return p.H > 0 ? (size_t)p.n_pad * (size_t)p.d * sizeof(double) : 0; }
@@ -1577,7 +1595,7 @@ void launch_l2(const SrhtPlan& p, const ChunkMaps& maps, int64_t nfull, const do
     // one CTA per SM; all must be co-resident (the warps wait on each other's progress), which the
     // launch-bounds/smem footprint guarantees for a grid of num_sms
     LAUNCH_PDL(srht_l2_kernel<HB>, (unsigned)num_sms, kL2Threads, kL2Smem, st, maps, A, p.n, p.lda, signbits, T, nfull,
-               p.d, p.l2_ns, tiles, n_tiles, bits, entries, p.scale1, p.scale2, SA, p.m, ctl, discard ? 1 : 0);
+               p.d, p.l2_ns, tiles, n_tiles, bits, entries, p.scale1, p.scale2, SA, p.sa_ld, ctl, discard ? 1 : 0);
 }
 using L2Fn = void (*)(const SrhtPlan&, const ChunkMaps&, int64_t, const double*, const uint32_t*, double*, const int4*,
                       int, const int2*, double*, int*, int, cudaStream_t);
@@ -1639,7 +1657,7 @@ void srht_run_device(const SrhtPlan& p, const double* d_A, const uint32_t* d_sig
         IHS_SMEM_ATTR(srht_phase2_compact_kernel, (int)smem);
         if (U > 0)
             LAUNCH_PDL(srht_phase2_compact_kernel, dim3((unsigned)ceil_div(U, kCmpU), (unsigned)p.d), 256, smem, st,
-                       (const double*)d_T, U, d_tiles, d_entries, p.scale1, p.scale2, d_SA, p.m);
+                       (const double*)d_T, U, d_tiles, d_entries, p.scale1, p.scale2, d_SA, p.sa_ld);
         return;
     }
     for (int i = 0; i < p.npass; ++i) {

@@ -6,7 +6,9 @@ exchange, the Gaussian sketch window + all-reduce, the gradient all-reduce and a
 
 Checks (sketch.hpp:58-108, problem.hpp:59-69, solver.hpp:106-232):
 * every rank holds the same bytes after each collective (SA, gradients, the solution);
-* the sharded SRHT sketch equals the single-GPU (and oracle) sketch bit for bit;
+* the sharded SRHT sketch — owner-reduce exchange: an all-to-all of owner blocks, the exact butterfly combine by
+  each row's owner and an all-gather, ~2 m d doubles received per rank — equals the single-GPU (and oracle)
+  sketch bit for bit, including m not divisible by P and m < P;
 * Gaussian sketches / gradients equal the single-GPU ones to fp64 tolerance (partial sums in another order);
 * the sharded adaptive solve takes the single-GPU solve's m-schedule, branches and counters and returns x within
   1e-10 of it in the Abar norm.
@@ -67,14 +69,17 @@ def test_sharded_sketches_and_gradient(gpu, O, P):
     def work(r):
         p = probs[r]
         return (gpu.srht_sketch(p, 3000, 7), gpu.srht_sketch(p, 64, 8), gpu.gaussian_sketch(p, 200, 9),
-                gpu.gradient(p, x))
+                gpu.gradient(p, x), gpu.srht_sketch(p, 1001, 11), gpu.srht_sketch(p, 1, 12))
 
     res = _run_ranks(P, work)
     for r in range(1, P):
         for a, b_ in zip(res[0], res[r]):
             assert np.array_equal(a, b_), f"rank {r} differs from rank 0"
-    SA_s, SA_s2, SA_g, g = res[0]
+    SA_s, SA_s2, SA_g, g, SA_odd, SA_one = res[0]
     assert np.array_equal(SA_s, O.srht_sketch(A, 3000, 7))
+    # m not a multiple of P (ragged last owner block) and m = 1 (owners without rows)
+    assert np.array_equal(SA_odd, O.srht_sketch(A, 1001, 11))
+    assert np.array_equal(SA_one, O.srht_sketch(A, 1, 12))
     assert np.array_equal(SA_s2, gpu.srht_sketch(single, 64, 8))
     ref = gpu.gaussian_sketch(single, 200, 9)
     assert np.max(np.abs(SA_g - ref)) <= 1e-12 * np.max(np.abs(ref))
