@@ -368,6 +368,7 @@ def main():
     ap.add_argument("--no-clocks", action="store_true", help="do not sample nvidia-smi during the timed steps")
     ap.add_argument("--out", default=None, help="also write the JSON line here")
     ap.add_argument("--replicas", action="store_true", help="N > 1: independent replicas instead of row sharding")
+    ap.add_argument("--no-delta", action="store_true", help="skip the direct_solve accuracy check (profiling runs)")
     ap.add_argument("--record-counters", action="store_true",
                     help=f"write this config's solve counters into profiles/{REF_COUNTERS_PATH.name}")
     ap.add_argument("--solver", default="ihs", choices=["ihs", "pcg", "cg"],
@@ -553,7 +554,7 @@ def main():
 
     # ---- accuracy of the returned x against the exact minimizer (problem.hpp:73-82, 104-109), off the clock
     acc = {}
-    if args.solver == "ihs":
+    if args.solver == "ihs" and not args.no_delta:
         try:
             x_star = ihs.direct_solve(p)
             pe0 = ihs.prediction_error(p, np.zeros(d), x_star)

@@ -344,7 +344,10 @@ void dgemm(bool transA, bool transB, int64_t M, int64_t N, int64_t K, double alp
         splitk = 1;
     }
     if (splitk < 1) splitk = 1;
-    const bool big = dgemm_use_big(transA, transB, M, N, K, lda, ldb, lower_only) && aligned16(A) && aligned16(B);
+    // the 128x128 tiles need enough CTAs to fill the GPU (the factor phase's recursive products at k/2..k/8
+    // without split-K would launch 16-64 of them); small grids stay on the 64x64 kernel
+    const bool big = dgemm_use_big(transA, transB, M, N, K, lda, ldb, lower_only) && aligned16(A) && aligned16(B) &&
+                     ceil_div(M, GBM) * ceil_div(N, GBN) * std::max(splitk, 1) >= 96;
     int64_t kps = ceil_div(std::max<int64_t>(K, 1), splitk);
     kps = ceil_div(kps, BK) * BK;
     const int splits = (int)std::max<int64_t>(1, ceil_div(std::max<int64_t>(K, 1), kps));
