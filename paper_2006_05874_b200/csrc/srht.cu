@@ -626,6 +626,99 @@ srht_phase2_kernel(double* __restrict__ T, int64_t n_pad, int lo, const int4* __
     p2_tile<HB, false, CtaBar, TH>(xs, T + j * n_pad + base, lo, emit != 0, tile, entries, j, s1, s2, SA, m);
 }
 
+// Two-round emitting pass for 11-12 high bits (n_pad = 2^21, 2^22): 256 threads x 64 registers hold the same
+// 16384-element tile as the 512-thread three-round pass (W = 8 / 4 low indices, so the host's tiles and entries
+// are shared), but cover 6 pass bits per round: round 1 = pass bits [0, 6) straight from T, one shared-memory
+// exchange, round 2 = pass bits [6, HB), then the tile is staged once for the emission. One exchange instead of
+// two (three shared-memory passes over the tile instead of five, three barriers instead of five); the padding
+// (4 doubles per 256) keeps every exchange access conflict-free for both thread mappings.
+__host__ __device__ constexpr int pad_r2(int i) { return i + ((i >> 8) << 2); }
+constexpr int kR2Threads = 256;
+template <int HB>
+constexpr size_t r2_smem() { return (size_t)pad_r2(kR2Threads * 64) * sizeof(double) + 128; }
+
+// TMA (tmap != nullptr): the tile arrives by ONE 4-D tensor copy (low index w, pass bits [6, HB), pass bits
+// [0, 6), column) into xs as w + W g + 256 c, so round 1 reads register c of all threads as one conflict-free run
+// and no thread issues global loads; the exchange then rewrites the buffer in the padded layout.
+template <int HB, bool TMAP>
+__global__ void __launch_bounds__(kR2Threads, 1)
+srht_phase2_r2_kernel(const __grid_constant__ CUtensorMap tmap, const double* __restrict__ T, int64_t n_pad,
+                      const int4* __restrict__ tiles, const int2* __restrict__ entries, double s1, double s2,
+                      double* __restrict__ SA, int64_t m) {
+    static_assert(HB == 11 || HB == 12, "two-round tile geometry");
+    constexpr int E = 64;
+    constexpr int R2 = HB - 6;                     // bits of round 2 (5 or 6)
+    constexpr int W = kR2Threads * E >> HB;        // low indices per tile (8 or 4)
+    constexpr int NG = kR2Threads / W;             // thread groups of round 1 (= 2^(HB - 6))
+    constexpr int GR = E >> R2;                    // round-2 columns per thread (2 or 1)
+    constexpr int lo = kChunkL;
+    pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible after this
+    extern __shared__ unsigned char r2_raw[];
+    double* xs = reinterpret_cast<double*>(r2_raw + ((128u - (tma::smem_u32(r2_raw) & 127u)) & 127u));
+    const int t = threadIdx.x;
+    const int w = t % W, g = t / W;
+    const int64_t j = blockIdx.y;
+    const int4 tile = tiles[blockIdx.x];
+    double v[E];
+    // round 1: register c = pass bits [0, 6), g = pass bits [6, HB)
+    if constexpr (TMAP) {
+        __shared__ alignas(8) uint64_t bar;
+        if (t == 0) {
+            tma::mbar_init(&bar, 1);
+            tma::fence_mbar_init();
+        }
+        __syncthreads();
+        if (t == 0) {
+            tma::mbar_expect_tx(&bar, kR2Threads * E * sizeof(double));
+            tma::load_4d(xs, &tmap, tile.x, 0, 0, (int)j, &bar);
+        }
+        tma::mbar_wait(&bar, 0);
+#pragma unroll
+        for (int c = 0; c < E; ++c) v[c] = xs[c * kR2Threads + t];
+        __syncthreads();  // the copy's layout is read once; the exchange below rewrites the buffer
+    } else {
+        const double* Tcol = T + j * n_pad + tile.x;
+#pragma unroll
+        for (int c = 0; c < E; ++c) v[c] = Tcol[((int64_t)((g << 6) | c) << lo) + w];
+    }
+#pragma unroll
+    for (int s_ = 0; s_ < 6; ++s_)
+#pragma unroll
+        for (int c = 0; c < E; ++c)
+            if (!(c & (1 << s_))) bfly(v[c], v[c | (1 << s_)]);
+#pragma unroll
+    for (int c = 0; c < E; ++c) xs[pad_r2((((g << 6) | c) * W) + w)] = v[c];
+    __syncthreads();
+    // round 2: register (grp, c2) = pass bits [6, HB) = c2, pass bits [0, 6) = g + grp NG
+#pragma unroll
+    for (int grp = 0; grp < GR; ++grp)
+#pragma unroll
+        for (int c2 = 0; c2 < (1 << R2); ++c2)
+            v[grp * (1 << R2) + c2] = xs[pad_r2(((c2 << 6) | (g + grp * NG)) * W + w)];
+#pragma unroll
+    for (int s_ = 0; s_ < R2; ++s_)
+#pragma unroll
+        for (int grp = 0; grp < GR; ++grp)
+#pragma unroll
+            for (int c2 = 0; c2 < (1 << R2); ++c2)
+                if (!(c2 & (1 << s_))) bfly(v[grp * (1 << R2) + c2], v[grp * (1 << R2) + (c2 | (1 << s_))]);
+    __syncthreads();  // every round-2 read is done before the buffer is rewritten
+#pragma unroll
+    for (int grp = 0; grp < GR; ++grp)
+#pragma unroll
+        for (int c2 = 0; c2 < (1 << R2); ++c2)
+            xs[pad_r2(((c2 << 6) | (g + grp * NG)) * W + w)] = v[grp * (1 << R2) + c2];
+    __syncthreads();
+    constexpr int64_t bmask = (int64_t{1} << HB) - 1;
+    for (int q = tile.y + t; q < tile.z; q += kR2Threads) {
+        const int2 rk = entries[q];
+        const int64_t r = rk.x;
+        const int b = (int)((r >> lo) & bmask);
+        const int ww = (int)(r & (W - 1));
+        SA[(int64_t)rk.y + j * m] = __dmul_rn(__dmul_rn(xs[pad_r2(b * W + ww)], s1), s2);
+    }
+}
+
 // Compact emitting pass (n_pad = 2^20, compact T[j][h][u] with u padded to 8, h = row bits 10..19): a CTA
 // stages 8 consecutive ranks of column j with coalesced 64-byte reads into per-rank shared rows (element h
 // at the XOR swizzle row h>>5, column (h ^ (h>>5)) & 31, so both orientations below are conflict-free);
@@ -1167,6 +1260,42 @@ const SmallFn kSmall[kSmallL + 1] = {launch_small<0>, launch_small<1>, launch_sm
                                      launch_small<4>, launch_small<5>, launch_small<6>, launch_small<7>,
                                      launch_small<8>, launch_small<9>, launch_small<10>};
 
+// 4-D map of the phase-1 output T (n_pad x d, column-major) for the two-round tiles: dims (low index, pass
+// bits [6, HB), pass bits [0, 6), column), box (W, 2^(HB-6), 64, 1)
+bool r2_tensor_map(const double* T, int64_t n_pad, int64_t d, int HB, CUtensorMap* out) {
+    static const bool disabled = [] {
+        const char* e = std::getenv("IHS_SRHT_R2_TMA");
+        return e && e[0] == '0';
+    }();
+    if (disabled || (reinterpret_cast<uintptr_t>(T) & 15) != 0) return false;
+    const int W = kR2Threads * 64 >> HB, NG = 1 << (HB - 6);
+    const cuuint64_t dims[4] = {(cuuint64_t)1 << kChunkL, (cuuint64_t)NG, 64, (cuuint64_t)d};
+    const cuuint64_t strides[3] = {(cuuint64_t)64 << (kChunkL + 3), (cuuint64_t)1 << (kChunkL + 3),
+                                   (cuuint64_t)n_pad * sizeof(double)};
+    const cuuint32_t box[4] = {(cuuint32_t)W, (cuuint32_t)NG, 64, 1};
+    const cuuint32_t estr[4] = {1, 1, 1, 1};
+    return tma_encode_fn()(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(T), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int HB>
+void launch_r2(const SrhtPlan& p, const double* T, const int4* tiles, int n_tiles, const int2* entries, double* SA,
+               cudaStream_t st) {
+    dim3 grid((unsigned)n_tiles, (unsigned)p.d);
+    CUtensorMap map;
+    if (r2_tensor_map(T, p.n_pad, p.d, HB, &map)) {
+        IHS_SMEM_ATTR((srht_phase2_r2_kernel<HB, true>), (int)r2_smem<HB>());
+        LAUNCH_PDL((srht_phase2_r2_kernel<HB, true>), grid, kR2Threads, r2_smem<HB>(), st, map, T, p.n_pad, tiles,
+                   entries, p.scale1, p.scale2, SA, p.sa_ld);
+    } else {
+        std::memset(&map, 0, sizeof(map));
+        IHS_SMEM_ATTR((srht_phase2_r2_kernel<HB, false>), (int)r2_smem<HB>());
+        LAUNCH_PDL((srht_phase2_r2_kernel<HB, false>), grid, kR2Threads, r2_smem<HB>(), st, map, T, p.n_pad, tiles,
+                   entries, p.scale1, p.scale2, SA, p.sa_ld);
+    }
+}
+
 template <int HB, int TH>
 void launch_pass(const SrhtPlan& p, double* T, int lo, const int4* tiles, int n_tiles, bool emit, const int2* entries,
                  double* SA, cudaStream_t st) {
@@ -1660,9 +1789,18 @@ void srht_run_device(const SrhtPlan& p, const double* d_A, const uint32_t* d_sig
                        (const double*)d_T, U, d_tiles, d_entries, p.scale1, p.scale2, d_SA, p.sa_ld);
         return;
     }
+    static const bool r2 = [] {  // IHS_SRHT_R2=0: the three-round 512-thread emitting pass (A/B)
+        const char* e = std::getenv("IHS_SRHT_R2");
+        return !(e && e[0] == '0');
+    }();
     for (int i = 0; i < p.npass; ++i) {
         const bool last = i == p.npass - 1;
         if (last && n_tiles == 0) break;
+        if (r2 && last && p.npass == 1 && p.p2t == 512 && (p.pass_hb[i] == 11 || p.pass_hb[i] == 12)) {
+            if (p.pass_hb[i] == 11) launch_r2<11>(p, d_T, d_tiles, n_tiles, d_entries, d_SA, st);
+            else launch_r2<12>(p, d_T, d_tiles, n_tiles, d_entries, d_SA, st);
+            continue;
+        }
         (p.p2t == 128 ? kPass128 : p.p2t == 512 ? kPass512 : kPass)[p.pass_hb[i]](p, d_T, p.pass_lo[i], d_tiles,
                                                                                   n_tiles, last, d_entries, d_SA, st);
     }
