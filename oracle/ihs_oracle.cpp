@@ -272,19 +272,19 @@ SketchedSystem::SketchedSystem(Mat SA, double nu)  // :69-84
     : SA_(std::move(SA)), nu_(nu), kind_(SA_.rows < SA_.cols ? FactorKind::WoodburyInner : FactorKind::DirectGram) {
     const double nu2 = nu_ * nu_;
     const Index m = SA_.rows, d = SA_.cols;
+    // Both products are full dense GEMMs like Eigen's `SA_ * SA_.transpose()` / `SA_.transpose() * SA_` (the
+    // counted m^2 d / d^2 m multiply-adds), formed by the blocked axpy-form gemm_nn over a transposed copy so
+    // every entry accumulates its inner index in ascending order.
+    Mat SAT(d, m);
+    for (Index j = 0; j < d; ++j)
+        for (Index i = 0; i < m; ++i) SAT(j, i) = SA_(i, j);
     if (kind_ == FactorKind::WoodburyInner) {  // inner = SA SA^T + nu^2 I_m
         L_ = Mat(m, m);
-        for (Index j = 0; j < m; ++j)
-            for (Index i = j; i < m; ++i) {
-                double s = 0;
-                for (Index k = 0; k < d; ++k) s += SA_(i, k) * SA_(j, k);
-                L_(i, j) = L_(j, i) = s;
-            }
+        gemm_nn(SA_.a.data(), m, d, SAT.a.data(), d, m, L_.a.data());
         for (Index j = 0; j < m; ++j) L_(j, j) += nu2;
     } else {  // gram = SA^T SA + nu^2 I_d
         L_ = Mat(d, d);
-        for (Index j = 0; j < d; ++j)
-            for (Index i = j; i < d; ++i) L_(i, j) = L_(j, i) = dot4(SA_.col(i), SA_.col(j), m);
+        gemm_nn(SAT.a.data(), d, m, SA_.a.data(), m, d, L_.a.data());
         for (Index j = 0; j < d; ++j) L_(j, j) += nu2;
     }
     if (!cholesky_lower(L_)) throw NumericalBreakdown("SketchedSystem: Cholesky factorization failed");

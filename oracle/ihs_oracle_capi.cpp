@@ -4,6 +4,7 @@
 #include "ihs_oracle.hpp"
 #include "../include/ihs_gpu.h"
 
+#include <chrono>
 #include <cstring>
 #include <string>
 
@@ -291,6 +292,69 @@ int ihs_oracle_pcg_sketch_size(int64_t n, int64_t d, int32_t kind, double rho, i
         auto [mm, c] = pcg_sketch_size(n, d, kind == IHS_SKETCH_SRHT ? SketchKind::SRHT : SketchKind::Gaussian, rho);
         *m = mm;
         *capped = c;
+    });
+}
+
+// ---- bench.py cpu_baseline: host timings of the restated reference operations on bounded samples. Inputs are
+// built outside the timed region (the reference builds ProblemInstance / SketchedSystem once per solve); the
+// steady_clock scope is the operation itself, as in SolveReport::wall_seconds (solver.hpp:111, 229-230).
+static double secs_since(std::chrono::steady_clock::time_point t0) {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+int ihs_oracle_time_sketch(const double* A, int64_t n, int64_t d, int64_t lda, int32_t kind, int64_t m, uint64_t seed,
+                           double* seconds, ihs_counters* counters) {
+    return guarded([&] {
+        const Mat Am = to_mat(A, n, d, lda);
+        CostCounters c;
+        const auto t0 = std::chrono::steady_clock::now();
+        const Mat R = apply_sketch(Am, kind == IHS_SKETCH_SRHT ? SketchKind::SRHT : SketchKind::Gaussian, m, seed, &c);
+        *seconds = secs_since(t0);
+        add_counters(counters, c);
+        if (R.rows != m) throw InvalidInput("time_sketch: bad result");
+    });
+}
+
+int ihs_oracle_time_fill_gaussian(uint64_t stream_seed, int64_t rows, int64_t cols, double* seconds) {
+    return guarded([&] {
+        Mat S(rows, cols);
+        std::mt19937_64 gen(stream_seed);
+        const auto t0 = std::chrono::steady_clock::now();
+        fill_gaussian(S.a.data(), rows, cols, gen, 1.0);
+        *seconds = secs_since(t0);
+    });
+}
+
+int ihs_oracle_time_gradient(const double* A, int64_t n, int64_t d, int64_t lda, const double* b, double nu,
+                             const double* x, int32_t reps, double* seconds, ihs_counters* counters) {
+    return guarded([&] {
+        const Problem p(to_mat(A, n, d, lda), Vec(b, b + n), nu);
+        const Vec xv(x, x + d);
+        CostCounters c;
+        double sink = 0.0;
+        const auto t0 = std::chrono::steady_clock::now();
+        for (int32_t r = 0; r < reps; ++r) sink += gradient(p, xv, &c)[0];
+        *seconds = secs_since(t0);
+        add_counters(counters, c);
+        if (!std::isfinite(sink)) throw InvalidInput("time_gradient: non-finite");
+    });
+}
+
+int ihs_oracle_time_system(const double* SA, int64_t m, int64_t d, int64_t lds, double nu, const double* g,
+                           int32_t solves, double* t_factor, double* t_solve, ihs_counters* counters) {
+    return guarded([&] {
+        Mat S = to_mat(SA, m, d, lds);
+        const Vec gv(g, g + d);
+        CostCounters c;
+        auto t0 = std::chrono::steady_clock::now();
+        auto sys = SketchedSystem::factorize(std::move(S), nu, &c);
+        *t_factor = secs_since(t0);
+        double sink = 0.0;
+        t0 = std::chrono::steady_clock::now();
+        for (int32_t r = 0; r < solves; ++r) sink += sys.solve(gv, &c)[0];
+        *t_solve = secs_since(t0);
+        add_counters(counters, c);
+        if (!std::isfinite(sink)) throw InvalidInput("time_system: non-finite");
     });
 }
 

@@ -99,6 +99,16 @@ def lib():
                                     P(abi.CgReportC)]
         L.ihs_oracle_pcg_sketch_size.argtypes = [C.c_int64, C.c_int64, C.c_int32, C.c_double, P(C.c_int64),
                                                  P(C.c_int32)]
+        if not hasattr(L, "ihs_oracle_time_sketch"):  # the reference build (oracle/ref.py) has no timing hooks
+            _lib = L
+            return _lib
+        L.ihs_oracle_time_sketch.argtypes = [d, C.c_int64, C.c_int64, C.c_int64, C.c_int32, C.c_int64, C.c_uint64, d,
+                                             P(abi.Counters)]
+        L.ihs_oracle_time_fill_gaussian.argtypes = [C.c_uint64, C.c_int64, C.c_int64, d]
+        L.ihs_oracle_time_gradient.argtypes = [d, C.c_int64, C.c_int64, C.c_int64, d, C.c_double, d, C.c_int32, d,
+                                               P(abi.Counters)]
+        L.ihs_oracle_time_system.argtypes = [d, C.c_int64, C.c_int64, C.c_int64, C.c_double, d, C.c_int32, d, d,
+                                             P(abi.Counters)]
         _lib = L
     return _lib
 
@@ -388,3 +398,42 @@ def pcg_sketch_size(n, d, kind, rho):
     m, c = C.c_int64(), C.c_int32()
     _check(lib().ihs_oracle_pcg_sketch_size(n, d, kind, rho, C.byref(m), C.byref(c)))
     return m.value, bool(c.value)
+
+
+# ----------------------------------------------------------------- host phase timings (bench.py cpu_baseline)
+def time_sketch(A, kind, m, seed):
+    """Seconds of one apply_sketch (sketch.hpp:110-117) on A (inputs prepared outside the timer), counters."""
+    A = _fortran(A)
+    n, d = A.shape
+    t = C.c_double()
+    c = abi.Counters()
+    _check(lib().ihs_oracle_time_sketch(_dp(A), n, d, n, kind, m, seed, C.byref(t), C.byref(c)))
+    return t.value, c
+
+
+def time_fill_gaussian(stream_seed, rows, cols):
+    t = C.c_double()
+    _check(lib().ihs_oracle_time_fill_gaussian(stream_seed, rows, cols, C.byref(t)))
+    return t.value
+
+
+def time_gradient(A, b, nu, x, reps=1):
+    """Seconds of `reps` gradient calls (problem.hpp:59-69) on a problem built outside the timer, counters."""
+    A = _fortran(A)
+    n, d = A.shape
+    t = C.c_double()
+    c = abi.Counters()
+    _check(lib().ihs_oracle_time_gradient(_dp(A), n, d, n, _dp(_f64(b)), nu, _dp(_f64(x)), reps, C.byref(t),
+                                          C.byref(c)))
+    return t.value, c
+
+
+def time_system(SA, nu, g, solves=1):
+    """(seconds of SketchedSystem::factorize, seconds of `solves` solves, counters) (sketched_system.hpp)."""
+    SA = _fortran(SA)
+    m, d = SA.shape
+    tf, ts = C.c_double(), C.c_double()
+    c = abi.Counters()
+    _check(lib().ihs_oracle_time_system(_dp(SA), m, d, m, nu, _dp(_f64(g)), solves, C.byref(tf), C.byref(ts),
+                                        C.byref(c)))
+    return tf.value, ts.value, c

@@ -645,7 +645,7 @@ __global__ void __launch_bounds__(kR2Threads, 1)
 srht_phase2_r2_kernel(const __grid_constant__ CUtensorMap tmap, const double* __restrict__ T, int64_t n_pad,
                       const int4* __restrict__ tiles, const int2* __restrict__ entries, double s1, double s2,
                       double* __restrict__ SA, int64_t m) {
-    static_assert(HB == 11 || HB == 12, "two-round tile geometry");
+    static_assert(HB >= 8 && HB <= 12, "two-round tile geometry");
     constexpr int E = 64;
     constexpr int R2 = HB - 6;                     // bits of round 2 (5 or 6)
     constexpr int W = kR2Threads * E >> HB;        // low indices per tile (8 or 4)
@@ -1796,8 +1796,9 @@ void srht_run_device(const SrhtPlan& p, const double* d_A, const uint32_t* d_sig
     for (int i = 0; i < p.npass; ++i) {
         const bool last = i == p.npass - 1;
         if (last && n_tiles == 0) break;
-        if (r2 && last && p.npass == 1 && p.p2t == 512 && (p.pass_hb[i] == 11 || p.pass_hb[i] == 12)) {
-            if (p.pass_hb[i] == 11) launch_r2<11>(p, d_T, d_tiles, n_tiles, d_entries, d_SA, st);
+        if (r2 && last && p.npass == 1 && p.p2t == 512 && p.pass_hb[i] >= 10 && p.pass_hb[i] <= 12) {
+            if (p.pass_hb[i] == 10) launch_r2<10>(p, d_T, d_tiles, n_tiles, d_entries, d_SA, st);
+            else if (p.pass_hb[i] == 11) launch_r2<11>(p, d_T, d_tiles, n_tiles, d_entries, d_SA, st);
             else launch_r2<12>(p, d_T, d_tiles, n_tiles, d_entries, d_SA, st);
             continue;
         }
