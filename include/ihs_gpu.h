@@ -219,6 +219,9 @@ void ihs_gpu_nccl_comm_destroy(void* comm);
  * the row-sharded code runs unchanged with one host thread per rank, collectives become host barriers plus
  * device copies ordered by events (tests and single-GPU development of the sharded path). */
 ihs_status ihs_gpu_emu_comm_create(int32_t world_size, int32_t device, void** comms);
+/* MT19937-64 draws the calling thread's Gaussian sketches have generated so far (count and emission passes over
+ * whole substreams): a row shard's share of the stream's generation work. */
+int64_t ihs_gpu_thread_generated_draws(void);
 /* The sharded SRHT decomposition run back to back on one device (P virtual
  * shards of a single-GPU problem): proves the decomposition bit-exact. */
 ihs_status ihs_gpu_sketch_sharded_emulated(ihs_gpu_problem* p, int32_t kind, int64_t m, uint64_t seed,

@@ -88,25 +88,29 @@ void mt_generate_raw(uint64_t seed, int64_t count, uint64_t* d_out, cudaStream_t
 // vectors run as jump-ahead substreams (d_scratch: rademacher_scratch_bytes(n))
 size_t rademacher_scratch_bytes(int64_t n);
 void mt_rademacher_bits(uint64_t seed, int64_t n, uint32_t* d_bits, void* d_scratch, cudaStream_t st);
-// fill_gaussian of a (rows*cols) column-major block with stddev, exact stream
-// order (polar method with cached second value); d_scratch sized by
-// gaussian_scratch_bytes(count).
-size_t gaussian_scratch_bytes(int64_t count);
-// normals [first, first + count) of the stream (first > 0: a row shard's columns of S)
-void mt_fill_gaussian(uint64_t seed, int64_t first, int64_t count, double stddev, double* d_out, void* d_scratch,
-                      cudaStream_t st);
-
-// Streamed normals [first, first + count) for the Gaussian sketch of tall matrices (S never materialised):
-// the stream is generated in chunks of jump-ahead substreams with a carried acceptance count; normals are
-// emitted into buf (capacity cap; buf[0] = normal `base`), and once at least `block` are ready (or the range
-// is complete) consume(base, ready) is called and returns how many leading normals it used (whole columns;
-// block must hold at least two columns). d_scratch: gaussian_stream_scratch_bytes(); cap >= block +
-// 2 * gaussian_stream_chunk_attempts().
-size_t gaussian_stream_scratch_bytes();
-int64_t gaussian_stream_chunk_attempts();
-void mt_gaussian_stream(uint64_t seed, int64_t first, int64_t count, double stddev, double* buf, int64_t cap,
-                        int64_t block, void* d_scratch, cudaStream_t st,
-                        const std::function<int64_t(int64_t, int64_t)>& consume);
+// polar.cu — the normal stream in two passes over jump-ahead substreams (count accepted attempts, scan, emit a
+// window); any substream range, so a row shard generates only its share.
+struct GaussPlan {
+    int64_t stride, draws, nsub;  // draws per substream, draws covering the stream, substreams
+};
+struct GaussScratch {
+    uint64_t* starts;  // start windows of substreams [starts_q0, ...)
+    uint64_t* xseq;
+    long long* base;   // nsub + 1: first accepted attempt of each substream (exclusive prefix)
+    int* cnt;          // nsub accepted-attempt counts
+    int64_t starts_q0;
+};
+GaussPlan gauss_plan(int64_t total_normals, int64_t stride);
+size_t gauss_scratch_bytes(const GaussPlan& g, int64_t nstarts);
+GaussScratch gauss_scratch(const GaussPlan& g, int64_t nstarts, void* d_scratch);
+void gauss_starts(uint64_t seed, const GaussPlan& g, int64_t q0, int64_t nq, GaussScratch& s, cudaStream_t st);
+void gauss_count(const GaussPlan& g, int64_t q0, int64_t nq, const GaussScratch& s, cudaStream_t st);
+void gauss_scan(const GaussPlan& g, const GaussScratch& s, cudaStream_t st);
+void gauss_emit(const GaussPlan& g, int64_t q0, int64_t nq, const GaussScratch& s, int64_t first, int64_t count,
+                double stddev, double* d_out, cudaStream_t st);
+void gauss_window_range(const std::vector<long long>& h_base, int64_t first, int64_t count, int64_t* q0, int64_t* nq);
+void gauss_counts_to_double(const GaussScratch& s, int64_t q0, int64_t nq, int64_t len, double* d_out, cudaStream_t st);
+void gauss_counts_from_double(const double* d_in, const GaussPlan& g, const GaussScratch& s, cudaStream_t st);
 
 // srht.cu — SRHT sketch SA = sqrt(n_pad/m) R H D A (sketch.hpp:77-108)
 struct SrhtPlan {

@@ -23,7 +23,6 @@
 #include "mt_core.cuh"
 #include "mt_jump.h"
 
-#include <cub/device/device_scan.cuh>
 
 namespace ihs_b200 {
 
@@ -143,59 +142,6 @@ __global__ void __launch_bounds__(mt::THREADS) mt_signbits_sub_kernel(const uint
     for (int64_t w = beg / 32 + threadIdx.x; w < w_end; w += blockDim.x) bits[w] = accw[w - beg / 32];
 }
 
-// libstdc++ generate_canonical<double,53>(mt19937_64): one draw.
-__device__ __forceinline__ double canonical(uint64_t raw) {
-    double u = __dmul_rn(__ull2double_rn(raw), 0x1p-64);
-    if (u >= 1.0) u = 0x1.fffffffffffffp-1;  // nextafter(1, 0)
-    return u;
-}
-
-// Polar attempt a consumes draws 2a, 2a+1 (random.tcc normal_distribution).
-__device__ __forceinline__ bool polar_attempt(const uint64_t* raw, int64_t a, double& x, double& y, double& r2) {
-    x = __dsub_rn(__dmul_rn(2.0, canonical(raw[2 * a])), 1.0);
-    y = __dsub_rn(__dmul_rn(2.0, canonical(raw[2 * a + 1])), 1.0);
-    r2 = __dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y));
-    return !(r2 > 1.0 || r2 == 0.0);
-}
-
-__global__ void polar_flags_kernel(const uint64_t* __restrict__ raw, int64_t attempts, int* __restrict__ flags) {
-    pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible after this
-    for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < attempts; a += (int64_t)gridDim.x * blockDim.x) {
-        double x, y, r2;
-        flags[a] = polar_attempt(raw, a, x, y, r2) ? 1 : 0;
-    }
-}
-
-// normals [first, first + count) of the stream -> out[0 .. count)
-__global__ void polar_emit_kernel(const uint64_t* __restrict__ raw, int64_t attempts, const int* __restrict__ pos,
-                                  int64_t first, int64_t count, double stddev, double* __restrict__ out,
-                                  int64_t carry) {
-    pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible after this
-    const int64_t end = first + count;
-    for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < attempts; a += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t k = carry + 2 * (int64_t)pos[a];  // normal index (carry: normals of earlier chunks)
-        if (k >= end || k + 1 < first) continue;
-        double x, y, r2;
-        if (!polar_attempt(raw, a, x, y, r2)) continue;
-        const double mult = __dsqrt_rn(__ddiv_rn(__dmul_rn(-2.0, log(r2)), r2));
-        if (k >= first) out[k - first] = __dadd_rn(__dmul_rn(__dmul_rn(y, mult), stddev), 0.0);
-        if (k + 1 >= first && k + 1 < end) out[k + 1 - first] = __dadd_rn(__dmul_rn(__dmul_rn(x, mult), stddev), 0.0);
-    }
-}
-
-__global__ void last_total_kernel(const int* __restrict__ pos, const int* __restrict__ flags, int64_t attempts,
-                                  long long* __restrict__ total) {
-    pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible after this
-    *total = (long long)pos[attempts - 1] + flags[attempts - 1];
-}
-
-// number of draws to generate so that `count` normals are almost surely covered
-int64_t draws_for(int64_t count) {
-    const double pairs = (double)((count + 1) / 2);
-    const double attempts = pairs / 0.7853981633974483 * 1.002 + 6.0 * std::sqrt(pairs) + 64.0;
-    int64_t a = (int64_t)attempts;
-    return 2 * a;
-}
 }  // namespace
 
 void mt_seed_host(uint64_t seed, MTState& s) {
@@ -225,139 +171,6 @@ void mt_rademacher_bits(uint64_t seed, int64_t n, uint32_t* d_bits, void* d_scra
     mt_jump_starts(seed, kSignStride, nsub, starts, xseq, st);
     LAUNCH_PDL(mt_signbits_sub_kernel, (unsigned)nsub, 160, (size_t)(kSignStride / 32) * 4, st, starts,
            (int64_t)kSignStride, n, d_bits);
-}
-
-size_t gaussian_scratch_bytes(int64_t count) {
-    const int64_t draws = draws_for(count);
-    const int64_t attempts = draws / 2;
-    size_t temp = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, temp, (int*)nullptr, (int*)nullptr, (int)attempts);
-    const int64_t nsub = ceil_div(draws, kJumpStride);
-    return (size_t)draws * 8 + (size_t)attempts * 8 + temp + 256 + (size_t)nsub * NN * 8 + (size_t)kJumpSeqWords * 8 + 1024;
-}
-
-void mt_fill_gaussian(uint64_t seed, int64_t first, int64_t count, double stddev, double* d_out, void* d_scratch,
-                      cudaStream_t st) {
-    if (count <= 0) return;
-    const int64_t draws = draws_for(first + count);
-    const int64_t attempts = draws / 2;
-    if (attempts >= (int64_t)INT32_MAX) fail(IHS_INVALID_INPUT, "fill_gaussian: stream longer than 2^31 attempts");
-    char* p = static_cast<char*>(d_scratch);
-    uint64_t* raw = reinterpret_cast<uint64_t*>(p);
-    p += (size_t)draws * 8;
-    int* flags = reinterpret_cast<int*>(p);
-    int* pos = flags + attempts;
-    p += (size_t)attempts * 8;
-    long long* total = reinterpret_cast<long long*>(p);
-    p += 256;
-    uint64_t* starts = reinterpret_cast<uint64_t*>(p);
-    const int64_t nsub = ceil_div(draws, kJumpStride);
-    p += (size_t)nsub * NN * 8;
-    uint64_t* xseq = reinterpret_cast<uint64_t*>(p);
-    p += (size_t)kJumpSeqWords * 8;
-    void* temp = p;
-    size_t temp_bytes = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, temp_bytes, flags, pos, (int)attempts);
-
-    if (nsub <= 1) {
-        mt_generate_raw(seed, draws, raw, st);
-    } else {
-        // jump-ahead start windows for substreams q*stride (host F2 polynomial
-        // arithmetic, cached per stride), expanded on the device
-        mt_jump_starts(seed, kJumpStride, nsub, starts, xseq, st);
-        LAUNCH_PDL(mt_substream_kernel, (unsigned)nsub, 160, 0, st, starts, (int64_t)kJumpStride, draws, raw);
-    }
-    const int threads = 256;
-    const int blocks = (int)std::min<int64_t>(ceil_div(attempts, threads), 148 * 16);
-    LAUNCH_PDL(polar_flags_kernel, blocks, threads, 0, st, raw, attempts, flags);
-    CUDA_CHECK(cub::DeviceScan::ExclusiveSum(temp, temp_bytes, flags, pos, (int)attempts, st));
-    note_launch();
-    LAUNCH_PDL(last_total_kernel, 1, 1, 0, st, pos, flags, attempts, total);
-    long long h_total = 0;
-    CUDA_CHECK(cudaMemcpyAsync(&h_total, total, sizeof(long long), cudaMemcpyDeviceToHost, st));
-    CUDA_CHECK(cudaStreamSynchronize(st));
-    if (2 * h_total < first + count) fail(IHS_INTERNAL_ERROR, "fill_gaussian: draw estimate too small");
-    LAUNCH_PDL(polar_emit_kernel, blocks, threads, 0, st, raw, attempts, pos, first, count, stddev, d_out,
-               (int64_t)0);
-}
-
-// ---- streamed normals (the Gaussian sketch of tall matrices, S never materialised)
-namespace {
-int64_t stream_subs() {  // substreams per chunk (IHS_GAUSS_STREAM_SUBS overrides; tests use 1)
-    static const int64_t v = [] {
-        const char* e = std::getenv("IHS_GAUSS_STREAM_SUBS");
-        const long long x = e ? std::atoll(e) : 0;
-        return x > 0 ? (int64_t)x : (int64_t)64;
-    }();
-    return v;
-}
-}  // namespace
-
-int64_t gaussian_stream_chunk_attempts() { return stream_subs() * kStreamStride / 2; }
-
-size_t gaussian_stream_scratch_bytes() {
-    const int64_t draws = stream_subs() * kStreamStride, attempts = draws / 2;
-    size_t temp = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, temp, (int*)nullptr, (int*)nullptr, (int)attempts);
-    return (size_t)draws * 8 + (size_t)attempts * 8 + temp + 256 + (size_t)stream_subs() * NN * 8 +
-           (size_t)kJumpSeqWords * 8 + 1024;
-}
-
-void mt_gaussian_stream(uint64_t seed, int64_t first, int64_t count, double stddev, double* buf, int64_t cap,
-                        int64_t block, void* d_scratch, cudaStream_t st,
-                        const std::function<int64_t(int64_t, int64_t)>& consume) {
-    if (count <= 0) return;
-    const int64_t Q = stream_subs(), draws = Q * kStreamStride, attempts = draws / 2;
-    char* p = static_cast<char*>(d_scratch);
-    uint64_t* raw = reinterpret_cast<uint64_t*>(p);
-    p += (size_t)draws * 8;
-    int* flags = reinterpret_cast<int*>(p);
-    int* pos = flags + attempts;
-    p += (size_t)attempts * 8;
-    long long* total = reinterpret_cast<long long*>(p);
-    p += 256;
-    uint64_t* starts = reinterpret_cast<uint64_t*>(p);
-    p += (size_t)Q * NN * 8;
-    uint64_t* xseq = reinterpret_cast<uint64_t*>(p);
-    p += (size_t)kJumpSeqWords * 8;
-    void* temp = p;
-    size_t temp_bytes = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, temp_bytes, flags, pos, (int)attempts);
-    const int threads = 256;
-    const int blocks = (int)std::min<int64_t>(ceil_div(attempts, threads), 148 * 16);
-    const int64_t end = first + count;
-    int64_t carry = 0;   // normals produced by the chunks so far
-    int64_t base = first; // normal index held by buf[0]
-    for (int64_t c = 0; carry < end; ++c) {
-        // chunk c: substreams [c Q, (c + 1) Q) of kStreamStride draws, attempts from draw 2 c Q stride
-        mt_jump_starts(seed, kStreamStride, Q, starts, xseq, st, c * Q);
-        LAUNCH_PDL(mt_substream_kernel, (unsigned)Q, 160, 0, st, starts, (int64_t)kStreamStride, draws, raw);
-        LAUNCH_PDL(polar_flags_kernel, blocks, threads, 0, st, raw, attempts, flags);
-        CUDA_CHECK(cub::DeviceScan::ExclusiveSum(temp, temp_bytes, flags, pos, (int)attempts, st));
-        note_launch();
-        LAUNCH_PDL(last_total_kernel, 1, 1, 0, st, pos, flags, attempts, total);
-        long long h_total = 0;
-        CUDA_CHECK(cudaMemcpyAsync(&h_total, total, sizeof(long long), cudaMemcpyDeviceToHost, st));
-        CUDA_CHECK(cudaStreamSynchronize(st));
-        const int64_t produced = 2 * (int64_t)h_total;
-        if (carry + produced > first) {
-            if (std::min(carry + produced, end) - base > cap) fail(IHS_INTERNAL_ERROR, "gaussian stream: buffer too small");
-            // normals [max(carry, base), min(carry + produced, end)) -> buf[k - base]
-            LAUNCH_PDL(polar_emit_kernel, blocks, threads, 0, st, raw, attempts, pos, base, end - base, stddev, buf,
-                       carry);
-        }
-        carry += produced;
-        const int64_t ready = std::min(carry, end) - base;
-        if (ready >= block || carry >= end) {
-            const int64_t used = consume(base, ready);
-            const int64_t left = ready - used;
-            if (left > used) fail(IHS_INTERNAL_ERROR, "gaussian stream: block smaller than two columns");
-            if (left > 0)
-                CUDA_CHECK(cudaMemcpyAsync(buf, buf + used, (size_t)left * sizeof(double), cudaMemcpyDeviceToDevice,
-                                           st));
-            base += used;
-        }
-    }
 }
 
 }  // namespace ihs_b200

@@ -632,24 +632,33 @@ srht_phase2_kernel(double* __restrict__ T, int64_t n_pad, int lo, const int4* __
 // exchange, round 2 = pass bits [6, HB), then the tile is staged once for the emission. One exchange instead of
 // two (three shared-memory passes over the tile instead of five, three barriers instead of five); the padding
 // (4 doubles per 256) keeps every exchange access conflict-free for both thread mappings.
-__host__ __device__ constexpr int pad_r2(int i) { return i + ((i >> 8) << 2); }
-constexpr int kR2Threads = 256;
+// threads per two-round tile: 128 for 12 high bits (W = 2; 64 KiB tiles, two CTAs per SM so one CTA's copy
+// overlaps the other's butterflies), 256 for 11 (W = 8)
 template <int HB>
-constexpr size_t r2_smem() { return (size_t)pad_r2(kR2Threads * 64) * sizeof(double) + 128; }
+constexpr int r2_threads() { return HB == 12 ? 128 : 256; }
+// padding of the exchange buffer: W doubles per TH (both thread mappings then hit distinct banks)
+template <int TH, int W>
+__host__ __device__ constexpr int pad_r2(int i) { return i + ((i >> ilog2c(TH)) << ilog2c(W)); }
+template <int HB>
+constexpr size_t r2_smem() {
+    constexpr int TH = r2_threads<HB>();
+    return (size_t)pad_r2<TH, (TH * 64 >> HB)>(TH * 64) * sizeof(double) + 128;
+}
 
 // TMA (tmap != nullptr): the tile arrives by ONE 4-D tensor copy (low index w, pass bits [6, HB), pass bits
 // [0, 6), column) into xs as w + W g + 256 c, so round 1 reads register c of all threads as one conflict-free run
 // and no thread issues global loads; the exchange then rewrites the buffer in the padded layout.
-template <int HB, bool TMAP>
-__global__ void __launch_bounds__(kR2Threads, 1)
+template <int HB, bool TMAP, int kR2Threads = r2_threads<HB>()>
+__global__ void __launch_bounds__(kR2Threads, kR2Threads == 128 ? 2 : 1)
 srht_phase2_r2_kernel(const __grid_constant__ CUtensorMap tmap, const double* __restrict__ T, int64_t n_pad,
                       const int4* __restrict__ tiles, const int2* __restrict__ entries, double s1, double s2,
                       double* __restrict__ SA, int64_t m) {
     static_assert(HB >= 8 && HB <= 12, "two-round tile geometry");
     constexpr int E = 64;
     constexpr int R2 = HB - 6;                     // bits of round 2 (5 or 6)
-    constexpr int W = kR2Threads * E >> HB;        // low indices per tile (8 or 4)
+    constexpr int W = kR2Threads * E >> HB;        // low indices per tile
     constexpr int NG = kR2Threads / W;             // thread groups of round 1 (= 2^(HB - 6))
+    auto pad_r2 = [](int i) { return ihs_b200::pad_r2<kR2Threads, W>(i); };
     constexpr int GR = E >> R2;                    // round-2 columns per thread (2 or 1)
     constexpr int lo = kChunkL;
     pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible after this
@@ -1268,7 +1277,7 @@ bool r2_tensor_map(const double* T, int64_t n_pad, int64_t d, int HB, CUtensorMa
         return e && e[0] == '0';
     }();
     if (disabled || (reinterpret_cast<uintptr_t>(T) & 15) != 0) return false;
-    const int W = kR2Threads * 64 >> HB, NG = 1 << (HB - 6);
+    const int W = (HB == 12 ? 128 : 256) * 64 >> HB, NG = 1 << (HB - 6);
     const cuuint64_t dims[4] = {(cuuint64_t)1 << kChunkL, (cuuint64_t)NG, 64, (cuuint64_t)d};
     const cuuint64_t strides[3] = {(cuuint64_t)64 << (kChunkL + 3), (cuuint64_t)1 << (kChunkL + 3),
                                    (cuuint64_t)n_pad * sizeof(double)};
@@ -1286,12 +1295,12 @@ void launch_r2(const SrhtPlan& p, const double* T, const int4* tiles, int n_tile
     CUtensorMap map;
     if (r2_tensor_map(T, p.n_pad, p.d, HB, &map)) {
         IHS_SMEM_ATTR((srht_phase2_r2_kernel<HB, true>), (int)r2_smem<HB>());
-        LAUNCH_PDL((srht_phase2_r2_kernel<HB, true>), grid, kR2Threads, r2_smem<HB>(), st, map, T, p.n_pad, tiles,
+        LAUNCH_PDL((srht_phase2_r2_kernel<HB, true>), grid, r2_threads<HB>(), r2_smem<HB>(), st, map, T, p.n_pad, tiles,
                    entries, p.scale1, p.scale2, SA, p.sa_ld);
     } else {
         std::memset(&map, 0, sizeof(map));
         IHS_SMEM_ATTR((srht_phase2_r2_kernel<HB, false>), (int)r2_smem<HB>());
-        LAUNCH_PDL((srht_phase2_r2_kernel<HB, false>), grid, kR2Threads, r2_smem<HB>(), st, map, T, p.n_pad, tiles,
+        LAUNCH_PDL((srht_phase2_r2_kernel<HB, false>), grid, r2_threads<HB>(), r2_smem<HB>(), st, map, T, p.n_pad, tiles,
                    entries, p.scale1, p.scale2, SA, p.sa_ld);
     }
 }
@@ -1493,7 +1502,13 @@ SrhtPlan srht_plan(int64_t n, int64_t d, int64_t lda, int64_t m) {
                 const char* e = std::getenv("IHS_SRHT_P2T");
                 return e ? std::atoi(e) : 0;
             }();
-            p.p2t = p2t_env == 256 ? 256 : 512;
+            static const bool r2_plan = [] {  // the two-round emitting pass (default; IHS_SRHT_R2=0: three rounds)
+                const char* e = std::getenv("IHS_SRHT_R2");
+                return !(e && e[0] == '0');
+            }();
+            // host tiles match the emitting pass: two-round 128-thread tiles for 12 bits (W = 2 = the 256-thread
+            // three-round geometry), 256-thread ones for 11 (W = 8 = the 512-thread geometry)
+            p.p2t = r2_plan ? (p.H == 12 ? 256 : 512) : (p2t_env == 256 ? 256 : 512);
             p.stream = 0;
             p.compact = 0;
             return p;
@@ -1796,9 +1811,8 @@ void srht_run_device(const SrhtPlan& p, const double* d_A, const uint32_t* d_sig
     for (int i = 0; i < p.npass; ++i) {
         const bool last = i == p.npass - 1;
         if (last && n_tiles == 0) break;
-        if (r2 && last && p.npass == 1 && p.p2t == 512 && p.pass_hb[i] >= 10 && p.pass_hb[i] <= 12) {
-            if (p.pass_hb[i] == 10) launch_r2<10>(p, d_T, d_tiles, n_tiles, d_entries, d_SA, st);
-            else if (p.pass_hb[i] == 11) launch_r2<11>(p, d_T, d_tiles, n_tiles, d_entries, d_SA, st);
+        if (r2 && last && p.npass == 1 && ((p.p2t == 256 && p.pass_hb[i] == 12) || (p.p2t == 512 && p.pass_hb[i] == 11))) {
+            if (p.pass_hb[i] == 11) launch_r2<11>(p, d_T, d_tiles, n_tiles, d_entries, d_SA, st);
             else launch_r2<12>(p, d_T, d_tiles, n_tiles, d_entries, d_SA, st);
             continue;
         }

@@ -811,6 +811,11 @@ def synth_generate(n: int, d: int, spectrum: int = 0, decay: float = 0.95, noise
     return A, b, xt
 
 
+def thread_generated_draws() -> int:
+    """MT19937-64 draws this thread's Gaussian sketches generated so far (a row shard's generation work)."""
+    return int(lib().ihs_gpu_thread_generated_draws())
+
+
 def kernel_launch_count() -> int:
     return int(lib().ihs_gpu_kernel_launch_count())
 

@@ -23,8 +23,11 @@ def main():
     ap.add_argument("--kind", default="srht", choices=["srht", "gaussian"])
     ap.add_argument("--ms", default="8192,32768,131072")
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--d", type=int, default=0, help="override the column count (profiling at the config's n)")
     a = ap.parse_args()
-    c = bench.CONFIGS[a.config]
+    c = dict(bench.CONFIGS[a.config])
+    if a.d:
+        c["d"] = a.d
     A = np.empty((c["n"], c["d"]), order="F")
     b = np.empty(c["n"])
     ihs.synth_generate(c["n"], c["d"], spectrum=c["spectrum"], decay=c["decay"], noise_std=c["noise"],

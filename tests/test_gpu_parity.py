@@ -504,7 +504,7 @@ def test_gaussian_streamed_sketch_matches(gpu):
             "assert np.linalg.norm(r.x - x) <= 1e-9 * (1 + np.linalg.norm(x))\n"
             "print('ok')\n")
     root = str(__import__("pathlib").Path(__file__).resolve().parents[1])
-    env = dict(os.environ, IHS_GAUSS_STREAM="1", IHS_GAUSS_STREAM_SUBS="1", IHS_GAUSS_STREAM_COLS="64")
+    env = dict(os.environ, IHS_GAUSS_STREAM="1", IHS_GAUSS_STREAM_COLS="64")
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600, env=env, cwd=root)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-3000:]
 
@@ -512,7 +512,7 @@ def test_gaussian_streamed_sketch_matches(gpu):
 @pytest.mark.parametrize("streamed", [False, True])
 def test_fill_gaussian_window(gpu, streamed):
     """A row shard's window of the normal stream (sharded Gaussian sketch: normals [row0 m, (row0 + n_loc) m)),
-    materialised or through the chunked streamed generator, equals the slice of the full stream."""
+    emitted at once or in blocks (the streamed sketch's scheme), equals the slice of the full stream."""
     import os
     import subprocess
     import sys
@@ -526,6 +526,5 @@ def test_fill_gaussian_window(gpu, streamed):
             "    assert np.array_equal(w, full[first:first + count]), (first, count)\n"
             "print('ok')\n")
     root = str(__import__("pathlib").Path(__file__).resolve().parents[1])
-    env = dict(os.environ, IHS_GAUSS_STREAM_SUBS="1")  # 2^22-draw chunks: several per window
-    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600, env=env, cwd=root)
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600, cwd=root)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-3000:]

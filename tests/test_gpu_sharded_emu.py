@@ -105,3 +105,37 @@ def test_sharded_adaptive_solve(gpu, P, kind):
     assert reps[0].converged and reps[0].iterations > 1
     assert _abar_rel(A, nu, reps[0].x, ref.x) <= 1e-10
     del probs, comms
+
+
+@pytest.mark.parametrize("P", [2, 4, 8])
+def test_sharded_gaussian_generation_is_one_pth(gpu, P):
+    """Each shard counts only its share of the stream's substreams (counts all-gathered) and emits only the
+    substreams reaching into its own window, so its generation work is ~2/P of the single-GPU generator's
+    (which counts and emits the whole stream), and the sketch is unchanged."""
+    n, d, m = 60000, 16, 512
+    A, b, _ = gpu.synth_generate(n, d, decay=0.95, noise_std=0.01, data_seed=7)
+    comms, probs = _shards(gpu, A, b, 1e-2, P)
+
+    def work(r):
+        d0 = gpu.thread_generated_draws()
+        SA = gpu.gaussian_sketch(probs[r], m, 21)
+        return SA, gpu.thread_generated_draws() - d0
+
+    res = _run_ranks(P, work)
+    single = gpu.ProblemInstance(A, b, 1e-2)
+    d0 = gpu.thread_generated_draws()
+    ref = gpu.gaussian_sketch(single, m, 21)
+    total = gpu.thread_generated_draws() - d0
+    for SA, _ in res:
+        assert np.array_equal(SA, res[0][0])
+    assert np.max(np.abs(res[0][0] - ref)) <= 1e-12 * np.max(np.abs(ref))
+    # one pass over the stream = total / 2 draws; shard r counts a 1/P share of the substreams and emits those
+    # covering its rows (rows_r / n of the stream: shards are n_pad / P rows, the last ones shorter), plus at most
+    # a couple of boundary substreams
+    one_pass = total / 2
+    for r, (_, draws) in enumerate(res):
+        rows = gpu.shard_rows(n, P, r)[1]
+        bound = one_pass * (1.0 / P + rows / n) + 4 * (1 << 18)
+        assert draws <= bound, (r, draws, bound, total, P)
+        assert draws < 0.8 * total  # well below the single-GPU generator's work
+    del probs, comms
