@@ -91,25 +91,31 @@ void mt_rademacher_bits(uint64_t seed, int64_t n, uint32_t* d_bits, void* d_scra
 // polar.cu — the normal stream in two passes over jump-ahead substreams (count accepted attempts, scan, emit a
 // window); any substream range, so a row shard generates only its share.
 struct GaussPlan {
-    int64_t stride, draws, nsub;  // draws per substream, draws covering the stream, substreams
+    int64_t draws;       // draws covering the stream
+    int64_t big, fine;   // draws per jump-ahead (counting) substream, per emitting substream (fine divides big)
+    int64_t nbig, nsub;  // counting substreams, emitting substreams
 };
 struct GaussScratch {
-    uint64_t* starts;  // start windows of substreams [starts_q0, ...)
+    uint64_t* jwin;      // start windows of jump substreams [j0, ...)
+    uint64_t* fwin;      // start windows of emitting substreams [f0, ...) (= jwin when big == fine)
     uint64_t* xseq;
-    long long* base;   // nsub + 1: first accepted attempt of each substream (exclusive prefix)
-    int* cnt;          // nsub accepted-attempt counts
-    int64_t starts_q0;
+    long long* base;     // nsub + 1: first accepted attempt of each emitting substream (exclusive prefix)
+    int* cnt;            // nsub accepted-attempt counts
+    int64_t j0, f0;
 };
-GaussPlan gauss_plan(int64_t total_normals, int64_t stride);
-size_t gauss_scratch_bytes(const GaussPlan& g, int64_t nstarts);
-GaussScratch gauss_scratch(const GaussPlan& g, int64_t nstarts, void* d_scratch);
-void gauss_starts(uint64_t seed, const GaussPlan& g, int64_t q0, int64_t nq, GaussScratch& s, cudaStream_t st);
-void gauss_count(const GaussPlan& g, int64_t q0, int64_t nq, const GaussScratch& s, cudaStream_t st);
+GaussPlan gauss_plan(int64_t total_normals);
+size_t gauss_scratch_bytes(const GaussPlan& g, int64_t nbig_win, int64_t nfine_win);
+GaussScratch gauss_scratch(const GaussPlan& g, int64_t nbig_win, int64_t nfine_win, void* d_scratch);
+void gauss_jump(uint64_t seed, const GaussPlan& g, int64_t bq0, int64_t bnq, GaussScratch& s, cudaStream_t st);
+// counts of the emitting substreams inside jump substreams [bq0, bq0 + bnq); dump: also their start windows
+void gauss_count(const GaussPlan& g, int64_t bq0, int64_t bnq, GaussScratch& s, bool dump, cudaStream_t st);
 void gauss_scan(const GaussPlan& g, const GaussScratch& s, cudaStream_t st);
-void gauss_emit(const GaussPlan& g, int64_t q0, int64_t nq, const GaussScratch& s, int64_t first, int64_t count,
+// start windows of emitting substreams [fq0, fq0 + fnq) (jump, plus a dump pass when big > fine)
+void gauss_fine_windows(uint64_t seed, const GaussPlan& g, int64_t fq0, int64_t fnq, GaussScratch& s, cudaStream_t st);
+void gauss_emit(const GaussPlan& g, int64_t fq0, int64_t fnq, const GaussScratch& s, int64_t first, int64_t count,
                 double stddev, double* d_out, cudaStream_t st);
 void gauss_window_range(const std::vector<long long>& h_base, int64_t first, int64_t count, int64_t* q0, int64_t* nq);
-void gauss_counts_to_double(const GaussScratch& s, int64_t q0, int64_t nq, int64_t len, double* d_out, cudaStream_t st);
+void gauss_counts_to_double(const GaussScratch& s, int64_t f0, int64_t nf, int64_t len, double* d_out, cudaStream_t st);
 void gauss_counts_from_double(const double* d_in, const GaussPlan& g, const GaussScratch& s, cudaStream_t st);
 
 // srht.cu — SRHT sketch SA = sqrt(n_pad/m) R H D A (sketch.hpp:77-108)

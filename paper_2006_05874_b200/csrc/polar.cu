@@ -1,19 +1,21 @@
-// polar.cu — the reference's Gaussian stream (fill_gaussian, rng.hpp:35-40) in two passes over jump-ahead
-// substreams, with no raw-draw buffer, no library scan and no host round trip.
+// polar.cu — the reference's Gaussian stream (fill_gaussian, rng.hpp:35-40) in two passes over substreams, with
+// no raw-draw buffer, no library scan and (on one GPU, S materialised) no host round trip.
 //
 // libstdc++'s normal_distribution (polar method) turns attempt a = draws (2a, 2a+1) of mt19937_64 into two
-// normals when it is accepted (y * mult first, the cached x * mult second). The position of a normal in the
-// stream therefore depends on how many attempts before it were accepted. Substream q (draws
-// [q stride, (q+1) stride), its start state obtained by F2 jump-ahead, mt_jump.cu) is generated by one CTA:
-//   pass 1 (polar_count_kernel): count the accepted attempts of each substream;
-//   scan   (count_scan_kernel):  exclusive prefix over substreams, in one CTA -> first normal of each substream;
-//   pass 2 (polar_emit_kernel):  regenerate the substream and write each accepted attempt's two normals at
-//                                2 (prefix + rank) — the rank inside a twist from warp ballots — keeping only the
-//                                requested window [first, first + count).
-// The draws are regenerated instead of stored (a twist costs a few instructions per word; storing and re-reading
-// 16 bytes per attempt costs more), and because the passes take any substream range, a row shard of the Gaussian
-// sketch counts only its 1/P share of the substreams, all-gathers the counts and emits only its own window
-// (runtime.cpp): its generation work is ~2/P of the whole stream instead of its O(prefix).
+// normals when it is accepted (y * mult first, the cached x * mult second), so the position of a normal depends
+// on how many attempts before it were accepted. The draws are split into emitting substreams of `fine` draws:
+//   count  (polar_count_kernel): one CTA per jump-ahead substream of `big` draws (start state by F2 jump-ahead,
+//          mt_jump.cu; big = fine unless that would need more than ~32k jump polynomials) counts the accepted
+//          attempts of each of its fine substreams, and can dump the 312-word MT state at each fine boundary;
+//   scan   (count_scan_kernel): exclusive prefix over the fine substreams in one CTA -> first normal of each;
+//   emit   (polar_emit_kernel): one CTA per fine substream regenerates it from its window and writes each
+//          accepted attempt's pair (the rank inside a twist from warp ballots) — raw (y, x) for pairs inside the
+//          requested window, finished on the spot at its two edges — keeping only [first, first + count);
+//   finish (polar_finish_kernel): mult = sqrt(-2 log r2 / r2) for every interior pair, fully parallel (the log
+//          is off the regeneration's serial critical path).
+// Draws are regenerated rather than stored (a twist costs a few instructions per word; storing 16 bytes per
+// attempt and reading them back costs more), and any substream range can be counted or emitted, which is what lets
+// a row shard count only its 1/P share and emit only its own window (runtime.cpp).
 #include "common.cuh"
 
 #include "mt_core.cuh"
@@ -21,6 +23,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 namespace ihs_b200 {
@@ -29,6 +32,8 @@ namespace {
 using mt::MM;
 using mt::NN;
 using mt::temper;
+constexpr int64_t kFine = kJumpStride;   // 2^18 draws per emitting substream
+constexpr int64_t kMaxJumpSubs = 32768;  // jump polynomials kept per stride (about 650 MB of bit lists)
 
 // libstdc++ generate_canonical<double,53>(mt19937_64): one draw, clamped below 1.
 __device__ __forceinline__ double canonical(uint64_t raw) {
@@ -41,6 +46,13 @@ __device__ __forceinline__ bool polar_accept(uint64_t d0, uint64_t d1, double& x
     y = __dsub_rn(__dmul_rn(2.0, canonical(d1)), 1.0);
     r2 = __dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y));
     return !(r2 > 1.0 || r2 == 0.0);
+}
+__device__ __forceinline__ double polar_mult(double x, double y) {
+    const double r2 = __dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y));
+    return __dsqrt_rn(__ddiv_rn(__dmul_rn(-2.0, log(r2)), r2));
+}
+__device__ __forceinline__ double polar_out(double v, double mult, double stddev) {
+    return __dadd_rn(__dmul_rn(__dmul_rn(v, mult), stddev), 0.0);  // ret * stddev + mean, mean = 0
 }
 
 // Thread k (even, < 156) of a twist owns attempt pairs (base + k, base + k + 1) (lo words) and
@@ -65,30 +77,69 @@ __device__ __forceinline__ TwistPairs twist_pairs(mt::Twister& tw, int64_t base,
     return p;
 }
 
-__global__ void __launch_bounds__(mt::THREADS) polar_count_kernel(const uint64_t* __restrict__ starts, int64_t stride,
-                                                                   int64_t q0, int64_t draws, int* __restrict__ cnt) {
+__device__ __forceinline__ int block_sum(int c, int* wsum) {
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_down_sync(0xffffffffu, c, o);
+    if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = c;
+    __syncthreads();
+    int s = 0;
+#pragma unroll
+    for (int w = 0; w < (int)(mt::THREADS / 32); ++w) s += wsum[w];
+    __syncthreads();
+    return s;
+}
+
+// CTA = jump substream bq0 + blockIdx.x of `big` draws: accepted-attempt counts of its fine substreams
+// (cnt[fine index]); with fwin, also the 312-word window (the state words preceding the fine substream's first
+// draw) of each of them at fwin[(fine index - fwin0) * 312].
+__global__ void __launch_bounds__(mt::THREADS) polar_count_kernel(const uint64_t* __restrict__ jwin, int64_t big,
+                                                                   int64_t fine, int64_t bq0, int64_t draws,
+                                                                   int* __restrict__ cnt, uint64_t* __restrict__ fwin,
+                                                                   int64_t fwin0) {
     pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible after this
     __shared__ uint64_t buf[2 * NN];
     __shared__ int wsum[mt::THREADS / 32];
     const int64_t qr = blockIdx.x;
-    for (int i = threadIdx.x; i < NN; i += blockDim.x) buf[i] = starts[qr * NN + i];
+    for (int i = threadIdx.x; i < NN; i += blockDim.x) buf[i] = jwin[qr * NN + i];
     __syncthreads();
+    const int64_t beg = (bq0 + qr) * big, end = min(draws, beg + big);
+    const int64_t f_first = beg / fine;
+    if (fwin)  // the first fine substream starts at the jump window itself
+        for (int i = threadIdx.x; i < NN; i += blockDim.x) fwin[(f_first - fwin0) * NN + i] = buf[i];
     mt::Twister tw{buf, 0};
-    const int64_t beg = (q0 + qr) * stride, end = min(draws, beg + stride);
-    int c = 0;
+    int64_t seg_end = min(end, beg + fine);  // current fine substream [seg_end - fine, seg_end)
+    int64_t f = f_first;
+    int c_cur = 0, c_next = 0;
     for (int64_t base = beg; base < end; base += NN) {
         const TwistPairs p = twist_pairs(tw, base, end);
         double x, y, r2;
-        c += (p.lo_ok && polar_accept(p.lo0, p.lo1, x, y, r2)) ? 1 : 0;
-        c += (p.hi_ok && polar_accept(p.hi0, p.hi1, x, y, r2)) ? 1 : 0;
-    }
-    for (int o = 16; o > 0; o >>= 1) c += __shfl_down_sync(0xffffffffu, c, o);
-    if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = c;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        int s = 0;
-        for (int w = 0; w < (int)(mt::THREADS / 32); ++w) s += wsum[w];
-        cnt[q0 + qr] = s;
+        // an attempt belongs to the fine substream of its first draw (fine boundaries are even)
+        if (p.lo_ok && polar_accept(p.lo0, p.lo1, x, y, r2)) {
+            if (base + threadIdx.x < seg_end) ++c_cur;
+            else ++c_next;
+        }
+        if (p.hi_ok && polar_accept(p.hi0, p.hi1, x, y, r2)) {
+            if (base + MM + threadIdx.x < seg_end) ++c_cur;
+            else ++c_next;
+        }
+        if (base + NN >= seg_end) {  // the fine boundary seg_end falls in this block (uniform decision)
+            const int s = block_sum(c_cur, wsum);
+            if (threadIdx.x == 0) cnt[f] = s;
+            c_cur = c_next;
+            c_next = 0;
+            if (fwin && seg_end < end) {
+                // window of the next fine substream: state words [seg_end - 312, seg_end), spread over the
+                // previous block [base - 312, base) and this one [base, base + 312)
+                const uint64_t* cur = buf + tw.cur * NN;
+                const uint64_t* prev = buf + (tw.cur ^ 1) * NN;
+                for (int i = threadIdx.x; i < NN; i += blockDim.x) {
+                    const int64_t j = seg_end - NN + i;
+                    fwin[(f + 1 - fwin0) * NN + i] = j < base ? prev[j - (base - NN)] : cur[j - base];
+                }
+                __syncthreads();  // the next twist overwrites the previous block
+            }
+            ++f;
+            seg_end = min(end, seg_end + fine);
+        }
     }
 }
 
@@ -126,31 +177,44 @@ __global__ void __launch_bounds__(1024) count_scan_kernel(const int* __restrict_
     if (t == 1023) base[nsub] = wpart[31];
 }
 
-// normals [first, first + count) -> out[0 .. count); a window not covered by the generated draws poisons its
-// last entry with NaN (the sketch then fails the finite check of SketchedSystem::factorize instead of going on silently)
-__global__ void __launch_bounds__(mt::THREADS) polar_emit_kernel(const uint64_t* __restrict__ starts, int64_t stride,
-                                                                  int64_t q0, int64_t draws,
+// CTA = fine substream fq0 + blockIdx.x (window fwin[(f - fwin0) * 312]): normals of [first, first + count)
+// -> out[k - first]. Pairs inside the window are written raw (y at k, x at k + 1; polar_finish_kernel applies
+// the multiplier), the at most two pairs straddling an edge are finished here. A window not covered by the
+// generated draws poisons its last entry with NaN (no CTA writes it, so the sketch fails the finite check of
+// SketchedSystem::factorize instead of going on silently).
+__global__ void __launch_bounds__(mt::THREADS) polar_emit_kernel(const uint64_t* __restrict__ fwin, int64_t fwin0,
+                                                                  int64_t fine, int64_t fq0, int64_t draws,
                                                                   const long long* __restrict__ base, int64_t nsub,
                                                                   int64_t first, int64_t count, double stddev,
                                                                   double* __restrict__ out) {
     pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible after this
     __shared__ uint64_t buf[2 * NN];
     __shared__ int wl[2][mt::THREADS / 32], wh[2][mt::THREADS / 32];
-    const int64_t qr = blockIdx.x, q = q0 + qr;
+    const int64_t f = fq0 + blockIdx.x;
     const int64_t end_n = first + count;
-    // (the last normal of an uncovered window is never written by any CTA, so its poison survives)
-    if (q == nsub - 1 && threadIdx.x == 0 && 2 * base[nsub] < end_n)
+    if (f == nsub - 1 && threadIdx.x == 0 && 2 * base[nsub] < end_n)
         out[count - 1] = __longlong_as_double(0x7ff8000000000000LL);
-    const int64_t n_beg = 2 * base[q], n_end = 2 * base[q + 1];
+    const int64_t n_beg = 2 * base[f], n_end = 2 * base[f + 1];
     if (n_end <= first || n_beg >= end_n) return;  // no normal of this substream lies in the window
-    for (int i = threadIdx.x; i < NN; i += blockDim.x) buf[i] = starts[qr * NN + i];
+    for (int i = threadIdx.x; i < NN; i += blockDim.x) buf[i] = fwin[(f - fwin0) * NN + i];
     __syncthreads();
     mt::Twister tw{buf, 0};
-    const int64_t beg = q * stride, end = min(draws, beg + stride);
+    const int64_t beg = f * fine, end = min(draws, beg + fine);
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const unsigned lt = (1u << lane) - 1u;
     int64_t running = n_beg;  // normal index of the next accepted attempt's first normal
     int par = 0;
+    auto put = [&](int64_t k, double x, double y) {
+        if (k + 1 < first || k >= end_n) return;
+        if (k >= first && k + 1 < end_n) {  // interior pair: raw values, finished in bulk
+            out[k - first] = y;
+            out[k + 1 - first] = x;
+            return;
+        }
+        const double mult = polar_mult(x, y);  // an edge pair: one of its two normals is in the window
+        if (k >= first) out[k - first] = polar_out(y, mult, stddev);
+        else out[k + 1 - first] = polar_out(x, mult, stddev);
+    };
     for (int64_t b = beg; b < end && running < end_n; b += NN) {
         const TwistPairs p = twist_pairs(tw, b, end);
         double xl = 0, yl = 0, rl = 0, xh = 0, yh = 0, rh = 0;
@@ -171,21 +235,37 @@ __global__ void __launch_bounds__(mt::THREADS) polar_emit_kernel(const uint64_t*
             tot_h += wh[par][v];
         }
         // lo attempts precede hi attempts in the draw order
-        const int64_t kl = running + 2 * (int64_t)(before_l + __popc(bl & lt));
-        const int64_t kh = running + 2 * (int64_t)(tot_l + before_h + __popc(bh & lt));
-        if (al && kl + 1 >= first && kl < end_n) {
-            const double mult = __dsqrt_rn(__ddiv_rn(__dmul_rn(-2.0, log(rl)), rl));
-            if (kl >= first) out[kl - first] = __dadd_rn(__dmul_rn(__dmul_rn(yl, mult), stddev), 0.0);
-            if (kl + 1 < end_n) out[kl + 1 - first] = __dadd_rn(__dmul_rn(__dmul_rn(xl, mult), stddev), 0.0);
-        }
-        if (ah && kh + 1 >= first && kh < end_n) {
-            const double mult = __dsqrt_rn(__ddiv_rn(__dmul_rn(-2.0, log(rh)), rh));
-            if (kh >= first) out[kh - first] = __dadd_rn(__dmul_rn(__dmul_rn(yh, mult), stddev), 0.0);
-            if (kh + 1 < end_n) out[kh + 1 - first] = __dadd_rn(__dmul_rn(__dmul_rn(xh, mult), stddev), 0.0);
-        }
+        if (al) put(running + 2 * (int64_t)(before_l + __popc(bl & lt)), xl, yl);
+        if (ah) put(running + 2 * (int64_t)(tot_l + before_h + __popc(bh & lt)), xh, yh);
         running += 2 * (int64_t)(tot_l + tot_h);
         par ^= 1;  // the next twist writes the other slot (its barrier orders the reuse)
     }
+}
+
+// interior pairs of the window (stream index k even, k >= first, k + 1 < first + count): (y, x) -> normals
+__global__ void polar_finish_kernel(double* __restrict__ out, int64_t first, int64_t count, double stddev) {
+    pdl_wait();
+    const int64_t k0 = first + (first & 1);  // first even stream index in the window
+    const int64_t npairs = (first + count - k0) / 2;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < npairs; i += (int64_t)gridDim.x * blockDim.x) {
+        double* o = out + (k0 - first) + 2 * i;
+        const double y = o[0], x = o[1];
+        const double mult = polar_mult(x, y);
+        o[0] = polar_out(y, mult, stddev);
+        o[1] = polar_out(x, mult, stddev);
+    }
+}
+
+__global__ void counts_to_double_kernel(const int* __restrict__ cnt, int64_t f0, int64_t nf, int64_t len,
+                                        double* __restrict__ out) {
+    pdl_wait();
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < len; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = i < nf ? (double)cnt[f0 + i] : 0.0;
+}
+__global__ void counts_from_double_kernel(const double* __restrict__ in, int64_t nsub, int* __restrict__ cnt) {
+    pdl_wait();
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nsub; i += (int64_t)gridDim.x * blockDim.x)
+        cnt[i] = (int)in[i];
 }
 
 // number of draws to generate so that `count` normals are almost surely covered (+6 sigma)
@@ -194,25 +274,38 @@ int64_t polar_draws_for(int64_t count) {
     const double attempts = pairs / 0.7853981633974483 * 1.002 + 6.0 * std::sqrt(pairs) + 64.0;
     return 2 * (int64_t)attempts;
 }
+unsigned grid_for(int64_t n) { return (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 256), 148 * 8)); }
 }  // namespace
 
-GaussPlan gauss_plan(int64_t total_normals, int64_t stride) {
+GaussPlan gauss_plan(int64_t total_normals) {
+    static const int64_t max_jump = [] {  // IHS_GAUSS_MAX_JUMP_SUBS: tests force big > fine on small streams
+        const char* e = std::getenv("IHS_GAUSS_MAX_JUMP_SUBS");
+        const long long v = e ? std::atoll(e) : 0;
+        return v > 0 ? (int64_t)v : kMaxJumpSubs;
+    }();
     GaussPlan g{};
-    g.stride = stride;
     g.draws = polar_draws_for(total_normals);
-    g.nsub = ceil_div(g.draws, stride);
+    g.fine = kFine;
+    g.nsub = ceil_div(g.draws, g.fine);
+    g.big = g.fine;
+    while (ceil_div(g.draws, g.big) > max_jump) g.big *= 2;
+    g.nbig = ceil_div(g.draws, g.big);
     return g;
 }
 
-size_t gauss_scratch_bytes(const GaussPlan& g, int64_t nstarts) {
-    return (size_t)nstarts * NN * 8 + (size_t)kJumpSeqWords * 8 + (size_t)g.nsub * 4 + (size_t)(g.nsub + 1) * 8 + 1024;
+size_t gauss_scratch_bytes(const GaussPlan& g, int64_t nbig_win, int64_t nfine_win) {
+    const int64_t fw = g.big == g.fine ? 0 : nfine_win;
+    return (size_t)(nbig_win + fw) * NN * 8 + (size_t)kJumpSeqWords * 8 + (size_t)g.nsub * 4 +
+           (size_t)(g.nsub + 1) * 8 + 1024;
 }
 
-GaussScratch gauss_scratch(const GaussPlan& g, int64_t nstarts, void* d_scratch) {
+GaussScratch gauss_scratch(const GaussPlan& g, int64_t nbig_win, int64_t nfine_win, void* d_scratch) {
     GaussScratch s{};
     char* p = static_cast<char*>(d_scratch);
-    s.starts = reinterpret_cast<uint64_t*>(p);
-    p += (size_t)nstarts * NN * 8;
+    s.jwin = reinterpret_cast<uint64_t*>(p);
+    p += (size_t)nbig_win * NN * 8;
+    s.fwin = g.big == g.fine ? s.jwin : reinterpret_cast<uint64_t*>(p);  // fine = jump substreams: one set
+    if (g.big != g.fine) p += (size_t)nfine_win * NN * 8;
     s.xseq = reinterpret_cast<uint64_t*>(p);
     p += (size_t)kJumpSeqWords * 8;
     s.base = reinterpret_cast<long long*>(p);
@@ -221,63 +314,63 @@ GaussScratch gauss_scratch(const GaussPlan& g, int64_t nstarts, void* d_scratch)
     return s;
 }
 
-void gauss_starts(uint64_t seed, const GaussPlan& g, int64_t q0, int64_t nq, GaussScratch& s, cudaStream_t st) {
-    s.starts_q0 = q0;
-    if (nq > 0) mt_jump_starts(seed, g.stride, nq, s.starts, s.xseq, st, q0);
+void gauss_jump(uint64_t seed, const GaussPlan& g, int64_t bq0, int64_t bnq, GaussScratch& s, cudaStream_t st) {
+    s.j0 = bq0;
+    if (g.big == g.fine) s.f0 = bq0;  // the jump windows are the fine windows
+    if (bnq > 0) mt_jump_starts(seed, g.big, bnq, s.jwin, s.xseq, st, bq0);
 }
 
-void gauss_count(const GaussPlan& g, int64_t q0, int64_t nq, const GaussScratch& s, cudaStream_t st) {
-    if (nq > 0)
-        LAUNCH_PDL(polar_count_kernel, (unsigned)nq, mt::THREADS, 0, st, (const uint64_t*)(s.starts + (q0 - s.starts_q0) * NN),
-                   g.stride, q0, g.draws, s.cnt);
+void gauss_count(const GaussPlan& g, int64_t bq0, int64_t bnq, GaussScratch& s, bool dump, cudaStream_t st) {
+    if (bnq <= 0) return;
+    uint64_t* fwin = nullptr;
+    if (dump && g.big != g.fine) {
+        fwin = s.fwin;
+        s.f0 = bq0 * (g.big / g.fine);
+    }
+    LAUNCH_PDL(polar_count_kernel, (unsigned)bnq, mt::THREADS, 0, st, (const uint64_t*)(s.jwin + (bq0 - s.j0) * NN),
+               g.big, g.fine, bq0, g.draws, s.cnt, fwin, s.f0);
 }
 
 void gauss_scan(const GaussPlan& g, const GaussScratch& s, cudaStream_t st) {
     LAUNCH_PDL(count_scan_kernel, 1, 1024, 0, st, (const int*)s.cnt, g.nsub, s.base);
 }
 
-void gauss_emit(const GaussPlan& g, int64_t q0, int64_t nq, const GaussScratch& s, int64_t first, int64_t count,
+void gauss_fine_windows(uint64_t seed, const GaussPlan& g, int64_t fq0, int64_t fnq, GaussScratch& s,
+                        cudaStream_t st) {
+    if (fnq <= 0) return;
+    const int64_t ratio = g.big / g.fine;
+    const int64_t bq0 = fq0 / ratio, bq1 = ceil_div(fq0 + fnq, ratio);
+    gauss_jump(seed, g, bq0, bq1 - bq0, s, st);
+    if (g.big != g.fine) gauss_count(g, bq0, bq1 - bq0, s, true, st);  // dump pass (recounts identical values)
+}
+
+void gauss_emit(const GaussPlan& g, int64_t fq0, int64_t fnq, const GaussScratch& s, int64_t first, int64_t count,
                 double stddev, double* d_out, cudaStream_t st) {
-    if (nq > 0 && count > 0)
-        LAUNCH_PDL(polar_emit_kernel, (unsigned)nq, mt::THREADS, 0, st,
-                   (const uint64_t*)(s.starts + (q0 - s.starts_q0) * NN), g.stride, q0, g.draws,
-                   (const long long*)s.base, g.nsub, first, count, stddev, d_out);
+    if (fnq <= 0 || count <= 0) return;
+    LAUNCH_PDL(polar_emit_kernel, (unsigned)fnq, mt::THREADS, 0, st, (const uint64_t*)s.fwin, s.f0, g.fine, fq0,
+               g.draws, (const long long*)s.base, g.nsub, first, count, stddev, d_out);
+    LAUNCH_PDL(polar_finish_kernel, grid_for(count / 2 + 1), 256, 0, st, d_out, first, count, stddev);
 }
 
-__global__ void counts_to_double_kernel(const int* __restrict__ cnt, int64_t q0, int64_t nq, int64_t len,
-                                        double* __restrict__ out) {
-    pdl_wait();
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < len; i += (int64_t)gridDim.x * blockDim.x)
-        out[i] = i < nq ? (double)cnt[q0 + i] : 0.0;
-}
-__global__ void counts_from_double_kernel(const double* __restrict__ in, int64_t nsub, int* __restrict__ cnt) {
-    pdl_wait();
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nsub; i += (int64_t)gridDim.x * blockDim.x)
-        cnt[i] = (int)in[i];
-}
-
-// counts of substreams [q0, q0 + nq) as doubles, zero-padded to len (the all-gather payload of a shard)
-void gauss_counts_to_double(const GaussScratch& s, int64_t q0, int64_t nq, int64_t len, double* d_out, cudaStream_t st) {
-    LAUNCH_PDL(counts_to_double_kernel, (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(len, 256), 1184)), 256,
-               0, st, (const int*)s.cnt, q0, nq, len, d_out);
+void gauss_counts_to_double(const GaussScratch& s, int64_t f0, int64_t nf, int64_t len, double* d_out, cudaStream_t st) {
+    LAUNCH_PDL(counts_to_double_kernel, grid_for(len), 256, 0, st, (const int*)s.cnt, f0, nf, len, d_out);
 }
 void gauss_counts_from_double(const double* d_in, const GaussPlan& g, const GaussScratch& s, cudaStream_t st) {
-    LAUNCH_PDL(counts_from_double_kernel, (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(g.nsub, 256), 1184)),
-               256, 0, st, d_in, g.nsub, s.cnt);
+    LAUNCH_PDL(counts_from_double_kernel, grid_for(g.nsub), 256, 0, st, d_in, g.nsub, s.cnt);
 }
 
-// Substreams whose normals intersect [first, first + count), from the host copy of base (nsub + 1 entries).
+// Fine substreams whose normals intersect [first, first + count), from the host copy of base (nsub + 1 entries).
 void gauss_window_range(const std::vector<long long>& h_base, int64_t first, int64_t count, int64_t* q0,
                         int64_t* nq) {
     const int64_t nsub = (int64_t)h_base.size() - 1;
-    // first q with 2 base[q + 1] > first, last q with 2 base[q] < first + count
+    // first q with 2 base[q + 1] > first, then the first q with 2 base[q] >= first + count
     int64_t lo = 0, hi = nsub;
     while (lo < hi) {
         const int64_t mid = (lo + hi) / 2;
         if (2 * h_base[(size_t)mid + 1] > first) hi = mid;
         else lo = mid + 1;
     }
-    int64_t a = lo;
+    const int64_t a = lo;
     lo = a, hi = nsub;
     while (lo < hi) {
         const int64_t mid = (lo + hi) / 2;

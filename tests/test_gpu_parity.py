@@ -504,9 +504,11 @@ def test_gaussian_streamed_sketch_matches(gpu):
             "assert np.linalg.norm(r.x - x) <= 1e-9 * (1 + np.linalg.norm(x))\n"
             "print('ok')\n")
     root = str(__import__("pathlib").Path(__file__).resolve().parents[1])
-    env = dict(os.environ, IHS_GAUSS_STREAM="1", IHS_GAUSS_STREAM_COLS="64")
-    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600, env=env, cwd=root)
-    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-3000:]
+    for extra in ({}, {"IHS_GAUSS_MAX_JUMP_SUBS": "3"}):
+        env = dict(os.environ, IHS_GAUSS_STREAM="1", IHS_GAUSS_STREAM_COLS="64", **extra)
+        r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600, env=env,
+                           cwd=root)
+        assert r.returncode == 0 and "ok" in r.stdout, (extra, r.stderr[-3000:])
 
 
 @pytest.mark.parametrize("streamed", [False, True])
@@ -526,5 +528,9 @@ def test_fill_gaussian_window(gpu, streamed):
             "    assert np.array_equal(w, full[first:first + count]), (first, count)\n"
             "print('ok')\n")
     root = str(__import__("pathlib").Path(__file__).resolve().parents[1])
-    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600, cwd=root)
-    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-3000:]
+    # default plan (emitting substreams = jump substreams) and a forced two-level plan (4 jump substreams, each
+    # dumping the windows of its emitting substreams), the one long streams take
+    for extra in ({}, {"IHS_GAUSS_MAX_JUMP_SUBS": "4"}):
+        r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600, cwd=root,
+                           env=dict(os.environ, **extra))
+        assert r.returncode == 0 and "ok" in r.stdout, (extra, r.stderr[-3000:])

@@ -139,3 +139,28 @@ def test_sharded_gaussian_generation_is_one_pth(gpu, P):
         assert draws <= bound, (r, draws, bound, total, P)
         assert draws < 0.8 * total  # well below the single-GPU generator's work
     del probs, comms
+
+
+def test_sharded_gaussian_two_level_plan(gpu):
+    """Long streams count over few jump substreams and dump the emitting windows (IHS_GAUSS_MAX_JUMP_SUBS forces
+    that plan here): the sharded Gaussian sketch still equals the single-GPU one on every rank."""
+    import os
+    import subprocess
+    import sys
+    code = ("import sys, threading\n"
+            "sys.path.insert(0, 'tests')\n"
+            "import numpy as np\n"
+            "from paper_2006_05874_b200 import ihs\n"
+            "import test_gpu_sharded_emu as T\n"
+            "A, b, _ = ihs.synth_generate(60000, 8, decay=0.95, noise_std=0.01, data_seed=9)\n"
+            "ref = ihs.gaussian_sketch(ihs.ProblemInstance(A, b, 1e-2), 300, 5)\n"
+            "for P in (2, 4):\n"
+            "    comms, probs = T._shards(ihs, A, b, 1e-2, P)\n"
+            "    res = T._run_ranks(P, lambda r: ihs.gaussian_sketch(probs[r], 300, 5))\n"
+            "    for SA in res:\n"
+            "        assert np.array_equal(SA, res[0]) and np.max(np.abs(SA - ref)) <= 1e-12 * np.max(np.abs(ref))\n"
+            "print('ok')\n")
+    root = str(__import__("pathlib").Path(__file__).resolve().parents[1])
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600, cwd=root,
+                       env=dict(os.environ, IHS_GAUSS_MAX_JUMP_SUBS="5"))
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-3000:]
