@@ -283,9 +283,16 @@ GaussPlan gauss_plan(int64_t total_normals) {
         const long long v = e ? std::atoll(e) : 0;
         return v > 0 ? (int64_t)v : kMaxJumpSubs;
     }();
+    static const int fine_log2 = [] {  // IHS_GAUSS_FINE_LOG2: emitting-substream length (A/B)
+        const char* e = std::getenv("IHS_GAUSS_FINE_LOG2");
+        return e ? std::atoi(e) : 0;
+    }();
     GaussPlan g{};
     g.draws = polar_draws_for(total_normals);
-    g.fine = kFine;
+    // shorter emitting substreams for short streams: the per-CTA regeneration is latency-bound, so more CTAs
+    // win until the jump-ahead (linear in the substream count) dominates (C2: 2^17 -> ~1300 CTAs)
+    g.fine = fine_log2 >= 12 && fine_log2 <= 24 ? int64_t{1} << fine_log2
+                                                : (g.draws < (int64_t{1} << 31) ? kFine / 2 : kFine);
     g.nsub = ceil_div(g.draws, g.fine);
     g.big = g.fine;
     while (ceil_div(g.draws, g.big) > max_jump) g.big *= 2;
