@@ -529,7 +529,12 @@ def main():
         sk_ms = t["sketch_kernel_ms"]
         if c["sketch"] == "SRHT":
             ach = t["sketch_bytes"] / (sk_ms * 1e-3) / 1e9
-            kern["sketch"] = {"kernel": "srht_phase1_tma_kernel + srht_phase2_kernel (FWHT, sign, sample gather)",
+            paths = {"srht_l2_kernel (single launch; T in an L2-resident column ring)": t.get("n_srht_l2", 0),
+                     "srht_phase1_tma_kernel + srht_phase2_compact_kernel (compact T)": t.get("n_srht_compact", 0),
+                     "srht_phase1_tma_kernel + srht_phase2_r2_kernel (T through HBM)": t.get("n_srht_two_kernel", 0)}
+            kern["sketch"] = {"kernel": " | ".join(f"{k} x{v}" for k, v in paths.items() if v) or "srht",
+                              "srht_paths": {"l2": paths[next(iter(paths))], "compact": t.get("n_srht_compact", 0),
+                                             "two_kernel": t.get("n_srht_two_kernel", 0)},
                               "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
                               "algorithmic_bytes_per_launch": t["sketch_bytes"] / t["n_sketch_kernel"],
                               "peak_source": peak_kind}

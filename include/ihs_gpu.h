@@ -123,6 +123,9 @@ typedef struct ihs_phase_times {
     double gradient_kernel_ms; /* device time of the gradient kernels alone (pass over A + fixed-order
                                   reduce), part of gradient_ms */
     int64_t n_gradient_kernel; /* number of gradient passes timed */
+    int64_t n_srht_l2;         /* SRHT sketches run as the L2-resident single launch */
+    int64_t n_srht_compact;    /* ... as the compact two-kernel path (n_pad = 2^20, small m) */
+    int64_t n_srht_two_kernel; /* ... as the two-kernel (HBM round trip of T) or multi-pass path */
 } ihs_phase_times;
 
 /* SolveReport (solver.hpp:70-87). Arrays are caller-allocated; *_size is the

@@ -81,7 +81,8 @@ class PhaseTimes(C.Structure):
                 ("total_ms", C.c_double), ("gradient_bytes", C.c_double), ("sketch_bytes", C.c_double),
                 ("sketch_flops", C.c_double), ("alloc_ms", C.c_double), ("host_rng_ms", C.c_double),
                 ("sketch_kernel_ms", C.c_double), ("n_sketch_kernel", C.c_int64),
-                ("gradient_kernel_ms", C.c_double), ("n_gradient_kernel", C.c_int64)]
+                ("gradient_kernel_ms", C.c_double), ("n_gradient_kernel", C.c_int64),
+                ("n_srht_l2", C.c_int64), ("n_srht_compact", C.c_int64), ("n_srht_two_kernel", C.c_int64)]
 
     def as_dict(self):
         return {k: (float if t is C.c_double else int)(getattr(self, k)) for k, t in self._fields_}

@@ -268,11 +268,13 @@ __device__ __forceinline__ void p1_sync_load(double* buf, const double* __restri
     __syncwarp();
 }
 
-__device__ __forceinline__ void p1_tma_issue(double* buf, const ChunkMaps* maps, int q, int j, uint64_t* bar) {
+// A is read exactly once: evict-first, so the T columns the emitting pass reads next stay in L2
+__device__ __forceinline__ void p1_tma_issue(double* buf, const ChunkMaps* maps, int q, int j, uint64_t* bar,
+                                             uint64_t pol) {
     tma::fence_proxy_async();
     tma::mbar_expect_tx(bar, kChunkDoubles * sizeof(double));
-    tma::load_4d(buf, &maps->even, 0, 0, q, j, bar);
-    tma::load_4d(buf + kChunkDoubles / 2, &maps->odd, 0, 0, q, j, bar);
+    tma::load_4d_hint(buf, &maps->even, 0, 0, q, j, bar, pol);
+    tma::load_4d_hint(buf + kChunkDoubles / 2, &maps->odd, 0, 0, q, j, bar, pol);
 }
 
 __device__ __forceinline__ void p1_transform_store_swz(double* buf, const uint32_t* __restrict__ signbits, int64_t n,
@@ -356,7 +358,8 @@ srht_phase1_tma_kernel(const __grid_constant__ ChunkMaps maps, const double* __r
     const uint32_t store_bits = p1_store_bits(mask, logw);
     auto issue = [&](int64_t chunk, int slot) {
         if (lane == 0 && chunk < total_chunks && (chunk & cmask) < nfull)
-            p1_tma_issue(ring + slot * kChunkDoubles, &maps, (int)(chunk & cmask), (int)(chunk >> lcpc), &bars[slot]);
+            p1_tma_issue(ring + slot * kChunkDoubles, &maps, (int)(chunk & cmask), (int)(chunk >> lcpc), &bars[slot],
+                         policy_evict_first());
     };
     uint32_t parity = 0u;
     int slot = 0;
@@ -808,13 +811,29 @@ __global__ void __launch_bounds__(32 * kCmpU) srht_phase2_compact_kernel(const d
 //     for, and all CTAs are co-resident (grid = resident CTA count), so no wait can deadlock;
 //   * A arrives by TMA with an L2 evict-first hint (read once), T is stored with evict-last.
 // Butterfly order, the sign flip and the two scalings are exactly those of the two-kernel path.
-constexpr int kL2P1Warps = 8;                         // phase-1 warps (each a 2-slot TMA ring)
-constexpr int kL2EmitThreads = 256;                   // emitting group
-constexpr int kL2Threads = kL2P1Warps * 32 + kL2EmitThreads;
-constexpr int kL2TileElems = kL2EmitThreads * 32;
-// phase-1 rings (8 warps x 2 x 8 KiB) + exchange buffer pad32(8192) doubles + mbarriers + 1 KiB alignment slack
-constexpr size_t kL2Smem =
-    (size_t)(kL2P1Warps * 2 * kChunkDoubles + pad32(kL2TileElems) + 2 * kL2P1Warps) * sizeof(double) + 1024 + 64;
+constexpr int kL2P1Warps = 8;        // phase-1 warps: one chunk of every item each (each a 2-slot TMA ring)
+constexpr int kL2EmitThreads = 128;  // emitting group: two-round tiles of 128 threads x 64 registers
+constexpr int kL2EmitGroups = 2;     // independent emitting groups (one warp of each per SM sub-partition)
+constexpr int kL2Slots = 1;          // chunk buffers per phase-1 warp (A comes from L2: see kL2Prefetch)
+constexpr int kL2Threads = kL2P1Warps * 32 + kL2EmitGroups * kL2EmitThreads;
+constexpr int kL2TileElems = kL2EmitThreads * 64;
+// registers: the launch grants 168 per thread (384 threads); phase-1 warps hand some to the emitting group
+// (64 doubles of tile per thread) with setmaxnreg: 256 x 128 + 128 x 232 <= 384 x 168
+constexpr int kL2Prefetch = 4;  // phase-1 items whose A is prefetched into L2 ahead of the current one
+constexpr int kL2Queue = 8;     // claimed-item queue (> kL2Prefetch + 1)
+constexpr int kL2P1Regs = 96;
+constexpr int kL2EmitRegs = 160;
+static_assert(kL2P1Warps * 32 * kL2P1Regs + kL2EmitGroups * kL2EmitThreads * kL2EmitRegs <=
+                  kL2Threads * ((65536 / kL2Threads) & ~7),
+              "register budget");
+// phase-1 rings (8 warps x 2 x 8 KiB) + padded exchange buffer + mbarriers + 1 KiB alignment slack
+template <int HB>
+constexpr size_t l2_smem() {
+    return (size_t)(kL2P1Warps * kL2Slots * kChunkDoubles +
+                    kL2EmitGroups * pad_r2<kL2EmitThreads, (kL2TileElems >> HB)>(kL2TileElems) + 2 * kL2P1Warps) *
+               sizeof(double) +
+           1024 + 64;
+}
 
 __device__ __forceinline__ void red_release_add(int* p, int v) {
     asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
@@ -824,13 +843,15 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
     asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
+__device__ __forceinline__ int ld_relaxed(const int* p) {
+    int v;
+    asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
 __device__ __forceinline__ uint64_t policy_evict_last() {
     uint64_t pol;
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(pol));
     return pol;
-}
-__device__ __forceinline__ void st_hint(double* p, double v, uint64_t pol) {
-    asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
 }
 __device__ __forceinline__ void st2_hint(double* p, double a, double b, uint64_t pol) {
     asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(a), "d"(b), "l"(pol) : "memory");
@@ -838,15 +859,6 @@ __device__ __forceinline__ void st2_hint(double* p, double a, double b, uint64_t
 __device__ __forceinline__ void discard_l2(const void* p) {
     asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
 }
-__device__ __forceinline__ void load_4d_hint(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
-                                             uint64_t* bar, uint64_t pol) {
-    asm volatile(
-        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, "
-        "%3, %4, %5}], [%6], %7;" ::"r"(tma::smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(tma::smem_u32(bar)), "l"(pol)
-        : "memory");
-}
-
 template <int HB>
 __global__ void __launch_bounds__(kL2Threads, 1)
 srht_l2_kernel(const __grid_constant__ ChunkMaps maps, const double* __restrict__ A, int64_t n, int64_t lda,
@@ -854,70 +866,101 @@ srht_l2_kernel(const __grid_constant__ ChunkMaps maps, const double* __restrict_
                const int4* __restrict__ tiles, int n_tiles, const uint32_t* __restrict__ tile_bits,
                const int2* __restrict__ entries, double s1, double s2, double* __restrict__ SA, int64_t m,
                int* __restrict__ ctl, int discard) {
-    constexpr int W = P2Geom<HB, kL2EmitThreads>::W;
-    constexpr int LOGW = P2Geom<HB, kL2EmitThreads>::LOGW;
-    constexpr int TE = W << HB;  // tile elements (= kL2TileElems)
-    static_assert(TE == kL2TileElems && LOGW <= 5, "tile geometry");
+    static_assert(HB >= 9 && HB <= 12, "L2-resident tile geometry");
+    constexpr int E = 64;                       // registers per emitting thread
+    constexpr int R2 = HB - 6;                  // pass bits of round 2
+    constexpr int GR = E >> R2;                 // round-2 columns per thread (1 .. 8)
+    constexpr int TE = kL2TileElems;            // tile elements: W low indices x 2^HB high combinations
+    constexpr int W = TE >> HB;                 // 2 (HB = 12) .. 16 (HB = 9)
+    constexpr int LOGW = ilog2c(W);
+    constexpr int NG = kL2EmitThreads / W;      // round-1 thread groups (= 2^(HB - 6))
     constexpr int64_t NPAD = int64_t{1} << (HB + kChunkL);
-    constexpr int CPC = 1 << HB;  // chunks per column
+    constexpr int CPC = 1 << HB;                // chunks per column
+    constexpr int IPC = CPC / kL2P1Warps;       // phase-1 items per column
+    constexpr int RUN = kL2P1Warps * W;         // contiguous doubles one item stores into each tile
+    constexpr int UPT = RUN / 2;                // ... as 16-byte units
+    constexpr int SWZ = (W / 2) * (UPT >= 8 ? 1 : 8 / UPT);  // XOR stride of the chunk copies' 16-byte units
+    static_assert(NG >= kL2P1Warps && RUN % 8 == 0, "an item fills whole 64-byte halves of 128-byte lines");
+    auto pad = [](int i) { return pad_r2<kL2EmitThreads, W>(i); };
     pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible after this
     extern __shared__ unsigned char l2_raw[];
     double* base = align1024(l2_raw);
-    double* rings = base;                                   // kL2P1Warps x 2 chunk buffers (1 KiB aligned)
-    double* xs = base + kL2P1Warps * 2 * kChunkDoubles;     // emitting-tile exchange buffer
-    uint64_t* bars = reinterpret_cast<uint64_t*>(xs + pad32(TE));  // 2 per phase-1 warp
-    __shared__ int s_p2;
+    double* rings = base;                                // kL2P1Warps x 2 chunk buffers (1 KiB aligned)
+    double* xs0 = base + kL2P1Warps * kL2Slots * kChunkDoubles;  // emitting-tile exchange buffers (one per group)
+    uint64_t* bars = reinterpret_cast<uint64_t*>(xs0 + kL2EmitGroups * pad(TE));  // 2 per phase-1 warp
+    __shared__ int s_claim[kL2Queue];
+    __shared__ uint32_t s_bits[16];  // occupancy of the (<= 512) low-index tiles
+    __shared__ int s_p2_all[kL2EmitGroups][2];
     const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+    if (t < 16) s_bits[t] = tile_bits[t];
+    __syncthreads();
     int* p1_counter = ctl;
     int* p2_counter = ctl + 1;
     int* done1 = ctl + 2;
     int* done2 = ctl + 2 + d;
-    const int64_t P2N = n_tiles;
     if (warp < kL2P1Warps) {
-        // ---- phase-1 warp: chunks in global (column-major) order through its own 2-slot TMA ring
-        double* ring = rings + warp * 2 * kChunkDoubles;
-        uint64_t* bar = bars + 2 * warp;
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kL2P1Regs));
+        // ---- phase-1 group (warps 0-7, named barrier 2). Item it of column col = it / IPC, r = it % IPC, holds
+        // the 8 chunks q = (r & 63) + 64 (8 (r >> 6) + j), j = warp: their high indices b = q differ only in
+        // b >> 6, so in the c-major tile layout below their W-element pieces of every tile are adjacent — the
+        // item stores RUN contiguous doubles (whole 128-byte lines) per tile instead of 16-byte scraps per chunk.
+        const int j = warp;
+        double* ring = rings + warp * kL2Slots * kChunkDoubles;
+        uint64_t* bar = bars + kL2Slots * warp;
         if (lane == 0) {
             tma::mbar_init(&bar[0], 1);
-            tma::mbar_init(&bar[1], 1);
+            if (kL2Slots > 1) tma::mbar_init(&bar[1], 1);
             tma::fence_mbar_init();
         }
         __syncwarp();
-        const int64_t total = d * CPC;
+        const GroupBar pbar{2, kL2P1Warps * 32};
+        const int64_t total = d * IPC;
         const uint64_t pol_first = policy_evict_first(), pol_last = policy_evict_last();
-        uint32_t store_bits = 0u;  // bit c: element 32c + lane lies in a tile some sampled row reads
-#pragma unroll
-        for (int c = 0; c < 32; ++c) {
-            const int te = ((c << 5) + lane) >> LOGW;
-            store_bits |= ((__ldg(tile_bits + (te >> 5)) >> (te & 31)) & 1u) << c;
-        }
-        auto claim = [&]() -> int64_t {
-            int v = 0;
-            if (lane == 0) v = atomicAdd(p1_counter, 1);
-            return __shfl_sync(0xffffffffu, v, 0);
+        auto chunk_of = [&](int64_t it, int jj) -> int64_t {
+            const int r = (int)(it & (IPC - 1));
+            return (r & 63) + 64 * ((r >> 6) * kL2P1Warps + jj);
         };
         auto issue = [&](int64_t it, int sl) {
-            if (it >= total) return;
-            const int64_t q = it & (CPC - 1), col = it >> HB;
-            if (q >= nfull || lane != 0) return;
+            if (it >= total || lane != 0) return;
+            const int64_t q = chunk_of(it, j), col = it / IPC;
+            if (q >= nfull) return;
             double* buf = ring + sl * kChunkDoubles;
             tma::fence_proxy_async();
             tma::mbar_expect_tx(&bar[sl], kChunkDoubles * sizeof(double));
-            load_4d_hint(buf, &maps.even, 0, 0, (int)q, (int)col, &bar[sl], pol_first);
-            load_4d_hint(buf + kChunkDoubles / 2, &maps.odd, 0, 0, (int)q, (int)col, &bar[sl], pol_first);
+            tma::load_4d_hint(buf, &maps.even, 0, 0, (int)q, (int)col, &bar[sl], pol_first);
+            tma::load_4d_hint(buf + kChunkDoubles / 2, &maps.odd, 0, 0, (int)q, (int)col, &bar[sl], pol_first);
         };
+        // A of item it -> L2 (no shared memory): issued kL2Prefetch items ahead so the shared-memory copy, one
+        // item ahead, comes from L2
+        auto prefetch = [&](int64_t it) {
+            if (it >= total || lane != 0) return;
+            const int64_t q = chunk_of(it, j), col = it / IPC;
+            if (q >= nfull) return;
+            tma::prefetch_4d_l2(&maps.even, 0, 0, (int)q, (int)col);
+            tma::prefetch_4d_l2(&maps.odd, 0, 0, (int)q, (int)col);
+        };
+        // claimed items: queue slot k % kL2Queue holds the k-th item of this CTA; thread 0 claims item k +
+        // kL2Prefetch + 1 during item k (visible to the group after the item's barriers)
+        if (t == 0)
+            for (int k = 0; k <= kL2Prefetch; ++k) s_claim[k] = atomicAdd(p1_counter, 1);
+        pbar();
+        int64_t cur = s_claim[0];
+        issue(cur, 0);
+        for (int k = 1; k < kL2Prefetch; ++k) prefetch(s_claim[k]);
         uint32_t phase = 0u;  // bit s: parity of slot s
         int sl = 0;
-        // completions are released once per (warp, column) run of chunks, and the slot of a column is checked
-        // once per run: a warp's claims only ever move to later columns
-        int64_t run_col = -1, slot_ok_col = -1;
-        int run_cnt = 0;
-        int64_t cur = claim();
-        issue(cur, 0);
+        int kq = 0;   // queue index of cur
+        int run = 0;  // thread 0: items of the current column stored since the last release
+        int64_t slot_ok_col = -1;  // thread 0: the latest column whose ring slot is known to be free
+        // 16-byte units of a chunk's natural-order copy are XOR-swizzled by its warp so the item store's reads
+        // (8 lanes = the 8 chunks' pieces of one tile) hit distinct banks
+        auto swz = [](int e, int jj) { return ((((e >> 1) ^ ((jj * SWZ) & 7))) << 1) | (e & 1); };
         while (cur < total) {
-            const int64_t nxt = claim();
-            issue(nxt, sl ^ 1);
-            const int64_t q = cur & (CPC - 1), col = cur >> HB;
+            if (kL2Slots > 1) issue(s_claim[(kq + 1) % kL2Queue], sl ^ 1);
+            prefetch(s_claim[(kq + kL2Prefetch) % kL2Queue]);
+            int claimed = 0;  // published only after the store loop: the atomic's round trip overlaps the item
+            if (t == 0) claimed = atomicAdd(p1_counter, 1);
+            const int64_t q = chunk_of(cur, j), col = cur / IPC;
             const int64_t r0 = q << kChunkL;
             double* buf = ring + sl * kChunkDoubles;
             if (q < nfull) {
@@ -963,79 +1006,145 @@ srht_l2_kernel(const __grid_constant__ ChunkMaps maps, const double* __restrict_
             const int lu = (lane & 15) >> 1;
 #pragma unroll
             for (int c = 0; c < 32; ++c) v[c] = colp[(c << 4) + ((lu ^ (c & 7)) << 1)];
-            __syncwarp();  // the buffer may be refilled by the TMA issued next iteration
+            __syncwarp();
 #pragma unroll
             for (int s_ = 0; s_ < 5; ++s_)
 #pragma unroll
                 for (int c = 0; c < 32; ++c)
                     if (!(c & (1 << s_))) bfly(v[c], v[c | (1 << s_)]);
+            // element e = 32c + lane back into the slot in natural (swizzled) order
+#pragma unroll
+            for (int c = 0; c < 32; ++c) buf[swz((c << 5) | lane, j)] = v[c];
             // the slot's previous column must be fully emitted before it is overwritten
-            if (col >= ns && col != slot_ok_col) {
-                if (lane == 0)
-                    while (ld_acquire(done2 + (col - ns)) < (int)P2N) __nanosleep(64);
-                __syncwarp();
+            if (t == 0 && col >= ns && col != slot_ok_col) {
+                while (ld_relaxed(done2 + (col - ns)) < n_tiles) __nanosleep(64);
+                (void)ld_acquire(done2 + (col - ns));
                 slot_ok_col = col;
             }
-            // element e = 32c + lane of chunk q (high index b = q) -> tile e >> LOGW, at (q & 31) 256 + (q >> 5) W
-            // + (e & (W - 1)) inside it (c-major tile: round 1 of the emitting pass loads contiguous runs)
-            double* dst = T + (col % ns) * NPAD + (q & 31) * kL2EmitThreads + (q >> 5) * W + (lane & (W - 1)) +
-                          (int64_t)(lane >> LOGW) * TE;
-#pragma unroll
-            for (int c = 0; c < 32; ++c)
-                if ((store_bits >> c) & 1u) st_hint(dst + (int64_t)(c << (5 - LOGW)) * TE, v[c], pol_last);
-            if (col != run_col) {
-                if (run_cnt > 0) {  // the previous column's chunks of this warp were stored before these
-                    __syncwarp();
-                    if (lane == 0) red_release_add(done1 + run_col, run_cnt);
+            pbar();  // every chunk of the item is in its slot; the column's ring slot is free
+            // store: tile te gets, at c 128 + 8 (r >> 6) W (c = r & 63), the pieces [chunk j][w] of the 8 chunks
+            const int r = (int)(cur & (IPC - 1));
+            double* dst0 = T + (col % ns) * NPAD + (r & 63) * kL2EmitThreads + (r >> 6) * kL2P1Warps * W;
+#pragma unroll 4
+            for (int i = 0; i < kChunkDoubles / 64; ++i) {
+                const int u = i * (kL2P1Warps * 32) + t;  // 16-byte unit of the item's output
+                const int te = u / UPT;
+                const int kk = (u % UPT) << 1;            // double offset inside the run
+                const int jj = kk >> LOGW, w = kk & (W - 1);
+                if (!((s_bits[te >> 5] >> (te & 31)) & 1u)) continue;
+                const double2 val = *reinterpret_cast<const double2*>(rings + (jj * kL2Slots + sl) * kChunkDoubles +
+                                                                      swz((te << LOGW) + w, jj));
+                st2_hint(dst0 + (int64_t)te * TE + kk, val.x, val.y, pol_last);
+            }
+            if (t == 0) s_claim[(kq + kL2Prefetch + 1) % kL2Queue] = claimed;
+            pbar();  // the item's stores are issued and every slot sl is read (the next TMA may refill it)
+            if (kL2Slots == 1) issue(s_claim[(kq + 1) % kL2Queue], 0);
+            // completions are released once per run of this CTA's items in one column (its claims only move to
+            // later columns): one release (a memory barrier for thread 0) per column instead of per item
+            if (t == 0) {
+                ++run;
+                const int64_t nx = s_claim[(kq + 1) % kL2Queue];
+                if (nx >= total || nx / IPC != col) {
+                    red_release_add(done1 + col, run);
+                    run = 0;
                 }
-                run_col = col;
-                run_cnt = 0;
             }
-            ++run_cnt;
-            // the run ends when the next claim is in another column (or there is none): release it now
-            if (nxt >= total || (nxt >> HB) != col) {
-                __syncwarp();
-                if (lane == 0) red_release_add(done1 + col, run_cnt);
-                run_cnt = 0;
-            }
-            sl ^= 1;
-            cur = nxt;
+            ++kq;
+            cur = s_claim[kq % kL2Queue];
+            if (kL2Slots > 1) sl ^= 1;
         }
         return;
     }
-    // ---- emitting group (warps kL2P1Warps.., named barrier 1): tiles in (column, tile) order
-    const int gt = t - kL2P1Warps * 32;
-    const GroupBar gbar{1, kL2EmitThreads};
-    const int64_t total2 = d * P2N;
-    if (gt == 0) s_p2 = atomicAdd(p2_counter, 1);
+    // ---- emitting group (warps 8-11, named barrier 1): tiles in (column, tile) order, each the two-round pass
+    // of srht_phase2_r2_kernel over the c-major tile (element (b, w) at (b & 63) 128 + (b >> 6) W + w)
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kL2EmitRegs));
+    const int pg = (t - kL2P1Warps * 32) / kL2EmitThreads;  // emitting group
+    const int gt = (t - kL2P1Warps * 32) % kL2EmitThreads;
+    const int w = gt & (W - 1), g = gt >> LOGW;
+    const GroupBar gbar{pg == 0 ? 1 : 3 + pg, kL2EmitThreads};
+    double* xs = xs0 + pg * pad(TE);
+    int* s_p2 = s_p2_all[pg];
+    const int64_t total2 = d * (int64_t)n_tiles;
+    if (gt == 0) s_p2[0] = atomicAdd(p2_counter, 1);
     gbar();
-    int64_t item = s_p2;
+    int64_t item = s_p2[0];
+    int par2 = 1;
+    constexpr int64_t bmask = (int64_t{1} << HB) - 1;
+    int run2 = 0;               // gt 0: tiles of the current column emitted since the last release
+    int64_t ready_col = -1;     // gt 0: the latest column whose phase 1 is known complete
     while (item < total2) {
-        int nxt = 0;
-        if (gt == 0) nxt = atomicAdd(p2_counter, 1);  // claimed early: its round trip overlaps this tile
-        const int64_t col = item / P2N, ti = item % P2N;
+        int claimed = 0;  // claimed early (published at the end): its round trip overlaps this tile
+        if (gt == 0) claimed = atomicAdd(p2_counter, 1);
+        const int64_t col = item / n_tiles, ti = item % n_tiles;
         const int4 tile = __ldg(tiles + ti);
-        if (gt == 0)
-            while (ld_acquire(done1 + col) < CPC) __nanosleep(32);
+        if (gt == 0 && col != ready_col) {  // relaxed polls, one acquire (polling with ld.acquire would
+            // invalidate the SM's L1 on every poll)
+            while (ld_relaxed(done1 + col) < IPC) __nanosleep(32);
+            (void)ld_acquire(done1 + col);
+            ready_col = col;
+        }
         gbar();
         const double* tptr = T + (col % ns) * NPAD + (int64_t)(tile.x >> LOGW) * TE;
-        p2_tile<HB, true, GroupBar, kL2EmitThreads, true>(xs, const_cast<double*>(tptr), LOGW, true, tile, entries,
-                                                           col, s1, s2, SA, m, gt, gbar, kChunkL);
-        // thread gt loaded doubles c 256 + gt (c < 32): the 32 lines of register c of this warp's 32 threads are
-        // read by this warp only; lane l drops the two lines of c = l once the warp has consumed its loads
-        __syncwarp();
+        double v[E];
+#pragma unroll
+        for (int c = 0; c < E; ++c) v[c] = __ldcg(tptr + c * kL2EmitThreads + gt);
+#pragma unroll
+        for (int s_ = 0; s_ < 6; ++s_)
+#pragma unroll
+            for (int c = 0; c < E; ++c)
+                if (!(c & (1 << s_))) bfly(v[c], v[c | (1 << s_)]);
+        // register c of this warp's 32 threads is one 256-byte run read by this warp only: once consumed, lane l
+        // drops the runs of c = 2l, 2l + 1 (no write-back of T)
         if (discard) {
-            const double* lines = tptr + (gt & 31) * kL2EmitThreads + (gt & ~31);
-            discard_l2(lines);
-            discard_l2(lines + 16);
+            __syncwarp();
+            const double* lines = tptr + (gt & ~31);
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                discard_l2(lines + ((2 * lane + k) * kL2EmitThreads));
+                discard_l2(lines + ((2 * lane + k) * kL2EmitThreads) + 16);
+            }
         }
+#pragma unroll
+        for (int c = 0; c < E; ++c) xs[pad((((g << 6) | c) * W) + w)] = v[c];
         gbar();
+#pragma unroll
+        for (int grp = 0; grp < GR; ++grp)
+#pragma unroll
+            for (int c2 = 0; c2 < (1 << R2); ++c2)
+                v[grp * (1 << R2) + c2] = xs[pad(((c2 << 6) | (g + grp * NG)) * W + w)];
+#pragma unroll
+        for (int s_ = 0; s_ < R2; ++s_)
+#pragma unroll
+            for (int grp = 0; grp < GR; ++grp)
+#pragma unroll
+                for (int c2 = 0; c2 < (1 << R2); ++c2)
+                    if (!(c2 & (1 << s_))) bfly(v[grp * (1 << R2) + c2], v[grp * (1 << R2) + (c2 | (1 << s_))]);
+        gbar();  // every round-2 read is done before the buffer is rewritten
+#pragma unroll
+        for (int grp = 0; grp < GR; ++grp)
+#pragma unroll
+            for (int c2 = 0; c2 < (1 << R2); ++c2)
+                xs[pad(((c2 << 6) | (g + grp * NG)) * W + w)] = v[grp * (1 << R2) + c2];
+        gbar();
+        for (int q = tile.y + gt; q < tile.z; q += kL2EmitThreads) {
+            const int2 rk = entries[q];
+            const int64_t rr = rk.x;
+            const int b = (int)((rr >> kChunkL) & bmask);
+            const int ww = (int)(rr & (W - 1));
+            SA[(int64_t)rk.y + col * m] = __dmul_rn(__dmul_rn(xs[pad(b * W + ww)], s1), s2);
+        }
+        if (gt == 0) s_p2[par2] = claimed;
+        gbar();  // the tile is emitted (xs free again) and every T read of it is done
         if (gt == 0) {
-            red_release_add(done2 + col, 1);
-            s_p2 = nxt;
+            ++run2;
+            const int64_t nx = s_p2[par2];
+            if (nx >= total2 || nx / n_tiles != col) {
+                red_release_add(done2 + col, run2);
+                run2 = 0;
+            }
         }
-        gbar();
-        item = s_p2;
+        item = s_p2[par2];
+        par2 ^= 1;
     }
 }
 
@@ -1146,7 +1255,8 @@ srht_stream_kernel(const __grid_constant__ ChunkMaps maps, const double* __restr
     const uint32_t store_bits = p1_store_bits(mask, logw);
     auto issue = [&](int64_t chunk, int slot) {
         if (lane == 0 && chunk < total && (chunk & cmask) < nfull)
-            p1_tma_issue(ring + slot * kChunkDoubles, &maps, (int)(chunk & cmask), (int)(chunk >> lcpc), &bars[slot]);
+            p1_tma_issue(ring + slot * kChunkDoubles, &maps, (int)(chunk & cmask), (int)(chunk >> lcpc), &bars[slot],
+                         policy_evict_first());
     };
     // finished-chunk counts not yet published: one release fence covers them all
     int pend_g[kFlushChunks], pend_c[kFlushChunks], npend = 0, since = 0;
@@ -1576,24 +1686,25 @@ void srht_unpack_blocks(const double* d_G, int P, int64_t mq, int64_t m, int64_t
 size_t srht_scratch_bytes(const SrhtPlan& p) { return p.H > 0 ? (size_t)p.n_pad * (size_t)p.d * sizeof(double) : 0; }
 
 bool srht_plan_l2(SrhtPlan& p) {
-    // opt-in (IHS_SRHT_L2=1; IHS_SRHT_L2_NS sets the ring depth): T stays in L2 and HBM sees only A and SA
-    // (ncu: 68.8 GB read + 2.2 GB written per C4 sketch, the algorithmic bytes), but the emitting tiles then
-    // bound the sketch and it measured slower than the two-kernel path (C4 m = 131072: 69 vs 59 ms; C3: 7.7 vs
-    // 6.9 ms), so the two-kernel path stays the default
-    static const bool disabled = [] {
+    // default for single-pass plans with 10..12 high bits (IHS_SRHT_L2=0: the two-kernel path; =1 also allows 9
+    // high bits; IHS_SRHT_L2_NS sets the ring depth). T stays in L2, so HBM sees A and SA only.
+    // Measured (device sketch, ms, two-kernel -> L2): C4 n_pad 2^22 m 8192 40.4 -> 36.3, m 131072 48.6 -> 44.6
+    // (ring depth 3, 96 MB); n_pad 2^20 m 65536: C3 7.02 -> 6.77, C5 27.4 -> 26.9 (depth >= 6). Shallower rings
+    // couple the two halves column by column and lose (C4 depth 2: 40.3; n_pad 2^20 depth 3: 10.2).
+    static const int mode = [] {
         const char* e = std::getenv("IHS_SRHT_L2");
-        return !(e && e[0] == '1');
+        return e ? std::atoi(e) : -1;
     }();
     static const int ns_env = [] {
         const char* e = std::getenv("IHS_SRHT_L2_NS");
         return e ? std::atoi(e) : 0;
     }();
-
-    if (disabled || p.H < 8 || p.H > 12 || p.npass != 1 || p.compact || p.stream) return false;
+    const int min_h = mode == 1 ? 9 : 10;
+    if (mode == 0 || p.H < min_h || p.H > 12 || p.npass != 1 || p.compact || p.stream) return false;
     p.l2 = 1;
-    p.p2t = kL2EmitThreads;
+    p.p2t = kL2TileElems / 32;  // tile geometry of the host's tiles: W = 8192 >> H low indices
     const int64_t col_bytes = p.n_pad * (int64_t)sizeof(double);
-    p.l2_ns = ns_env > 0 ? ns_env : (int)std::max<int64_t>(2, std::min<int64_t>(8, (64ll << 20) / col_bytes));
+    p.l2_ns = ns_env > 0 ? ns_env : (int)std::max<int64_t>(2, std::min<int64_t>(12, (96ll << 20) / col_bytes));
     return true;
 }
 size_t srht_l2_scratch_bytes(const SrhtPlan& p) { return (size_t)p.l2_ns * (size_t)p.n_pad * sizeof(double); }
@@ -1729,22 +1840,32 @@ template <int HB>
 void launch_l2(const SrhtPlan& p, const ChunkMaps& maps, int64_t nfull, const double* A, const uint32_t* signbits,
                double* T, const int4* tiles, int n_tiles, const int2* entries, double* SA, int* ctl, int num_sms,
                cudaStream_t st) {
-    IHS_SMEM_ATTR(srht_l2_kernel<HB>, (int)kL2Smem);
+    IHS_SMEM_ATTR(srht_l2_kernel<HB>, (int)l2_smem<HB>());
     static const bool discard = [] {  // IHS_SRHT_L2_DISCARD=0: keep the consumed T lines (A/B of the discard)
         const char* e = std::getenv("IHS_SRHT_L2_DISCARD");
         return !(e && e[0] == '0');
     }();
     CUDA_CHECK(cudaMemsetAsync(ctl, 0, srht_l2_ctl_bytes(p), st));
     const uint32_t* bits = reinterpret_cast<const uint32_t*>(tiles + n_tiles);
+    // the CTAs of one launch wait on each other, so two launches must never share the device: launches from
+    // different streams are chained through one event per device
+    static std::mutex mu;
+    static cudaEvent_t last[64] = {};
+    int dev = 0;
+    CUDA_CHECK(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
+    if (last[dev & 63] == nullptr) CUDA_CHECK(cudaEventCreateWithFlags(&last[dev & 63], cudaEventDisableTiming));
+    CUDA_CHECK(cudaStreamWaitEvent(st, last[dev & 63], 0));
     // one CTA per SM; all must be co-resident (the warps wait on each other's progress), which the
     // launch-bounds/smem footprint guarantees for a grid of num_sms
-    LAUNCH_PDL(srht_l2_kernel<HB>, (unsigned)num_sms, kL2Threads, kL2Smem, st, maps, A, p.n, p.lda, signbits, T, nfull,
+    LAUNCH_PDL(srht_l2_kernel<HB>, (unsigned)num_sms, kL2Threads, l2_smem<HB>(), st, maps, A, p.n, p.lda, signbits, T, nfull,
                p.d, p.l2_ns, tiles, n_tiles, bits, entries, p.scale1, p.scale2, SA, p.sa_ld, ctl, discard ? 1 : 0);
+    CUDA_CHECK(cudaEventRecord(last[dev & 63], st));
 }
 using L2Fn = void (*)(const SrhtPlan&, const ChunkMaps&, int64_t, const double*, const uint32_t*, double*, const int4*,
                       int, const int2*, double*, int*, int, cudaStream_t);
-const L2Fn kL2[13] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
-                      launch_l2<8>, launch_l2<9>, launch_l2<10>, launch_l2<11>, launch_l2<12>};
+const L2Fn kL2[13] = {nullptr, nullptr, nullptr,      nullptr,       nullptr,       nullptr,      nullptr,
+                      nullptr, nullptr, launch_l2<9>, launch_l2<10>, launch_l2<11>, launch_l2<12>};
 
 void srht_run_device(const SrhtPlan& p, const double* d_A, const uint32_t* d_signbits, const int2* d_entries,
                      const int4* d_tiles, int n_tiles, double* d_T, double* d_SA, cudaStream_t st,

@@ -46,5 +46,23 @@ __device__ __forceinline__ void load_4d(void* dst, const CUtensorMap* map, int c
         : "memory");
 }
 
+// the same with an L2 cache policy (createpolicy), e.g. evict-first for data read exactly once
+__device__ __forceinline__ void load_4d_hint(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
+                                             uint64_t* bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, "
+        "%3, %4, %5}], [%6], %7;" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+}
+
+// prefetch a 4-D box into L2 (no shared memory, no completion tracking)
+__device__ __forceinline__ void prefetch_4d_l2(const CUtensorMap* map, int c0, int c1, int c2, int c3) {
+    asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global.tile [%0, {%1, %2, %3, %4}];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+                 : "memory");
+}
+
 }  // namespace tma
 }  // namespace ihs_b200

@@ -394,9 +394,9 @@ def test_srht_l2_resident_bit_exact(gpu, O, n, d, m, seed):
 
 
 def test_srht_l2_ring_depths_and_two_kernel_path_agree(gpu):
-    """The opt-in L2-resident launch (IHS_SRHT_L2=1) at ring depths 2 and 3 (every slot reused), with sparse
-    tiles at n_pad = 2^20 (compact T disabled), at 2^22 rows, and the default two-kernel path all give the
-    oracle's bytes."""
+    """The L2-resident launch (default for 10..12 high bits; IHS_SRHT_L2=1 also takes 9) at ring depths 2 and 3
+    (every slot reused), with sparse tiles at n_pad = 2^20 (compact T disabled), at 2^19, 2^21 and 2^22 rows, and
+    the two-kernel path (IHS_SRHT_L2=0) all give the oracle's bytes."""
     import os
     import subprocess
     import sys
@@ -410,13 +410,43 @@ def test_srht_l2_ring_depths_and_two_kernel_path_agree(gpu):
             "B = np.asfortranarray(rng.standard_normal(((1 << 22) - 3, 3)))\n"
             "for m in (9, 131072):\n"
             "    assert np.array_equal(ihs.srht_sketch(B, m, 4 + m), O.srht_sketch(B, m, 4 + m)), m\n"
+            "C = np.asfortranarray(rng.standard_normal(((1 << 19) - 5, 5)))\n"
+            "D = np.asfortranarray(rng.standard_normal(((1 << 21) + 9, 3)))\n"
+            "for X, m in ((C, 300), (C, 60000), (D, 70000)):\n"
+            "    assert np.array_equal(ihs.srht_sketch(X, m, 5 + m), O.srht_sketch(X, m, 5 + m)), m\n"
             "print('ok')\n")
     root = str(__import__("pathlib").Path(__file__).resolve().parents[1])
     for extra in ({"IHS_SRHT_L2": "1", "IHS_SRHT_L2_NS": "2"},
-                  {"IHS_SRHT_L2": "1", "IHS_SRHT_L2_NS": "3", "IHS_SRHT_NO_COMPACT": "1"}, {}):
+                  {"IHS_SRHT_L2": "1", "IHS_SRHT_L2_NS": "3", "IHS_SRHT_NO_COMPACT": "1"}, {"IHS_SRHT_L2": "0"}, {}):
         env = dict(os.environ, **extra)
         r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300, env=env, cwd=root)
         assert r.returncode == 0 and "ok" in r.stdout, (extra, r.stderr[-2000:])
+
+
+def test_srht_l2_concurrent_problems(gpu, O):
+    """Two problems sketching at once from two host threads (two streams): the L2-resident launches, whose CTAs
+    wait on each other, are chained on the device and never share it — no hang, both bit-exact."""
+    import threading
+    rng = np.random.default_rng(12)
+    mats = [np.asfortranarray(rng.standard_normal(((1 << 20) - 3, 6))) for _ in range(2)]
+    probs = [gpu.ProblemInstance(M, np.zeros(M.shape[0]), 1e-2) for M in mats]
+    out, err = [None, None], []
+
+    def work(i):
+        try:
+            out[i] = [gpu.srht_sketch(probs[i], 30000 + 7 * k, 40 + k) for k in range(4)]
+        except Exception as e:  # noqa: BLE001
+            err.append(e)
+
+    th = [threading.Thread(target=work, args=(i,)) for i in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=300)
+    assert not any(t.is_alive() for t in th) and not err, err
+    for i in range(2):
+        for k in range(4):
+            assert np.array_equal(out[i][k], O.srht_sketch(mats[i], 30000 + 7 * k, 40 + k))
 
 
 def test_srht_column_batches_bit_exact(gpu):
