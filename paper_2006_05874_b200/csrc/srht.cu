@@ -797,19 +797,24 @@ __global__ void __launch_bounds__(32 * kCmpU) srht_phase2_compact_kernel(const d
 }
 
 // ------------------------------------------------------------ L2-resident single launch (default)
-// The two-kernel path moves every column three times through HBM (A read, T write, T read: 8.6 GB -> ~26 GB
-// at C3, 69 GB -> ~200 GB at C4). This persistent kernel keeps T on chip in the 126 MB L2 instead:
-//   * T is a ring of NS column slots (NS x n_pad doubles, <= ~64 MB), stored TILE-MAJOR: the emitting tile of
-//     W consecutive low indices x 2^HB high combinations is one contiguous 8192-double block, so the emitting
-//     pass reads it with fully coalesced L2 loads and then drops its lines with discard.global.L2 (no
-//     write-back: T never reaches HBM unless L2 pressure evicts it first);
-//   * work items (8 phase-1 chunks of a column, or one emitting tile of a column) are handed out in
-//     dependency order by one atomic counter: P1(col 0..NS-1), then per column j the emitting tiles of j
-//     followed by the P1 items of column j + NS. An emitting tile waits (one thread spinning on an acquire
-//     load) until all P1 items of its column have stored; a P1 item of column j + NS waits until every tile of
-//     column j has been emitted (its slot is free). Every item is handed out only after all items it waits
-//     for, and all CTAs are co-resident (grid = resident CTA count), so no wait can deadlock;
-//   * A arrives by TMA with an L2 evict-first hint (read once), T is stored with evict-last.
+// The two-kernel path moves every column three times through HBM (A read, T write, T read: 69 GB -> 208 GB per
+// C4 sketch). This persistent kernel (one CTA per SM) keeps T on chip in the 126 MB L2 instead:
+//   * T is a ring of NS column slots (NS x n_pad doubles, ~96 MB), each column stored TILE-MAJOR: the emitting
+//     tile of W consecutive low indices x 2^H high combinations is one contiguous 8192-double block, c-major
+//     inside ((b & 63) 128 + (b >> 6) W + w), so the emitting pass reads it with coalesced L2 loads and then
+//     drops the lines with discard.global.L2 (no write-back unless L2 pressure evicted them first);
+//   * phase-1 warps (8, one chunk each) work on CTA-wide items of 8 chunks q = c + 64 (8 g' + j), whose pieces
+//     of every tile are adjacent, so an item stores whole 128-byte lines (the 16-byte pieces of a lone chunk
+//     made ~4.6 G L2 write requests per C4 sketch; whole lines make 0.55-0.8 G). A is prefetched into L2
+//     (cp.async.bulk.prefetch.tensor) 4 items ahead, then copied chunk by chunk into shared memory by TMA;
+//   * two emitting groups (128 threads x 64 registers each: the two-round pass of srht_phase2_r2_kernel)
+//     take tiles; setmaxnreg moves registers from the phase-1 warps to them;
+//   * items and tiles are claimed in dependency order from two atomic counters: an emitting tile of column j
+//     waits until every phase-1 item of j has stored (per-column counter, released once per run of a CTA's
+//     items in one column), a phase-1 item of column j + NS until every tile of column j is emitted (its slot
+//     is free). Every wait is on work claimed earlier by a running CTA, so no wait can deadlock, whatever the
+//     residency;
+//   * A arrives with an L2 evict-first hint (read once), T is stored with evict-last.
 // Butterfly order, the sign flip and the two scalings are exactly those of the two-kernel path.
 constexpr int kL2P1Warps = 8;        // phase-1 warps: one chunk of every item each (each a 2-slot TMA ring)
 constexpr int kL2EmitThreads = 128;  // emitting group: two-round tiles of 128 threads x 64 registers
@@ -955,6 +960,13 @@ srht_l2_kernel(const __grid_constant__ ChunkMaps maps, const double* __restrict_
         // 16-byte units of a chunk's natural-order copy are XOR-swizzled by its warp so the item store's reads
         // (8 lanes = the 8 chunks' pieces of one tile) hit distinct banks
         auto swz = [](int e, int jj) { return ((((e >> 1) ^ ((jj * SWZ) & 7))) << 1) | (e & 1); };
+        // the sign word of the current item's chunk, loaded one item ahead (its L2 round trip overlaps an item)
+        auto sign_word = [&](int64_t it) -> uint32_t {
+            if (it >= total) return 0u;
+            const int64_t rl = (chunk_of(it, j) << kChunkL) + (lane << 5);
+            return rl < n ? __ldg(signbits + (rl >> 5)) : 0u;
+        };
+        uint32_t sw = sign_word(cur);
         while (cur < total) {
             if (kL2Slots > 1) issue(s_claim[(kq + 1) % kL2Queue], sl ^ 1);
             prefetch(s_claim[(kq + kL2Prefetch) % kL2Queue]);
@@ -973,7 +985,7 @@ srht_l2_kernel(const __grid_constant__ ChunkMaps maps, const double* __restrict_
             const int64_t rl = r0 + (lane << 5);
             uint32_t flip = 0u;
             if (rl < n) {
-                flip = ~__ldg(signbits + (rl >> 5));
+                flip = ~sw;
                 if (rl + 32 > n) flip &= (1u << (n - rl)) - 1u;
             }
             double v[32];
@@ -1051,6 +1063,7 @@ srht_l2_kernel(const __grid_constant__ ChunkMaps maps, const double* __restrict_
             }
             ++kq;
             cur = s_claim[kq % kL2Queue];
+            sw = sign_word(cur);
             if (kL2Slots > 1) sl ^= 1;
         }
         return;
@@ -1847,8 +1860,10 @@ void launch_l2(const SrhtPlan& p, const ChunkMaps& maps, int64_t nfull, const do
     }();
     CUDA_CHECK(cudaMemsetAsync(ctl, 0, srht_l2_ctl_bytes(p), st));
     const uint32_t* bits = reinterpret_cast<const uint32_t*>(tiles + n_tiles);
-    // the CTAs of one launch wait on each other, so two launches must never share the device: launches from
-    // different streams are chained through one event per device
+    // one launch at a time per device: each sizes its T ring to most of L2, so two concurrent launches (problems
+    // on different streams) would evict each other's rings; launches from different streams are chained through
+    // one event per device. (Concurrency would still be deadlock-free: items and tiles are claimed in dependency
+    // order by running CTAs only, so no CTA ever waits on work held by a CTA that is not resident.)
     static std::mutex mu;
     static cudaEvent_t last[64] = {};
     int dev = 0;
@@ -1856,8 +1871,7 @@ void launch_l2(const SrhtPlan& p, const ChunkMaps& maps, int64_t nfull, const do
     std::lock_guard<std::mutex> lk(mu);
     if (last[dev & 63] == nullptr) CUDA_CHECK(cudaEventCreateWithFlags(&last[dev & 63], cudaEventDisableTiming));
     CUDA_CHECK(cudaStreamWaitEvent(st, last[dev & 63], 0));
-    // one CTA per SM; all must be co-resident (the warps wait on each other's progress), which the
-    // launch-bounds/smem footprint guarantees for a grid of num_sms
+    // one CTA per SM (the launch-bounds/smem footprint allows one)
     LAUNCH_PDL(srht_l2_kernel<HB>, (unsigned)num_sms, kL2Threads, l2_smem<HB>(), st, maps, A, p.n, p.lda, signbits, T, nfull,
                p.d, p.l2_ns, tiles, n_tiles, bits, entries, p.scale1, p.scale2, SA, p.sa_ld, ctl, discard ? 1 : 0);
     CUDA_CHECK(cudaEventRecord(last[dev & 63], st));
