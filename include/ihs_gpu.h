@@ -218,6 +218,9 @@ ihs_status ihs_gpu_nccl_unique_id(uint8_t out[128]);
 ihs_status ihs_gpu_nccl_comm_create(const uint8_t id[128], int32_t world_size, int32_t rank, int32_t device,
                                     void** comm);
 void ihs_gpu_nccl_comm_destroy(void* comm);
+/* Self-test of the sharded path's collectives (all-reduce sum, all-gather, all-to-all) on exact fp64 patterns:
+ * *mismatches = wrong elements of this rank's results (0 on success). Any world size, NCCL or emulated. */
+ihs_status ihs_gpu_comm_selftest(void* comm, int32_t device, int64_t count, int64_t* mismatches);
 /* world_size EMULATED ranks of this process (comms[r] for rank r; free each with ihs_gpu_nccl_comm_destroy):
  * the row-sharded code runs unchanged with one host thread per rank, collectives become host barriers plus
  * device copies ordered by events (tests and single-GPU development of the sharded path). */

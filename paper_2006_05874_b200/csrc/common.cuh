@@ -177,6 +177,8 @@ void* nccl_comm_create(const uint8_t id[128], int world, int rank);
 void nccl_comm_destroy(void* comm);
 // world_size emulated ranks of this process (out[r] = rank r's communicator; host threads drive the ranks)
 void emu_comm_create(int world, void** out);
+int comm_world(const void* comm);
+int comm_rank(const void* comm);
 void nccl_allreduce_sum(double* buf, size_t count, void* comm, cudaStream_t st);
 void nccl_allgather(const double* send, double* recv, size_t count_per_rank, void* comm, cudaStream_t st);
 // all-to-all: block p of send (count doubles) goes to rank p, block p of recv comes from rank p

@@ -206,6 +206,9 @@ void emu_comm_create(int world, void** out) {
     }
 }
 
+int comm_world(const void* comm) { return comm ? static_cast<const Comm*>(comm)->world : 1; }
+int comm_rank(const void* comm) { return comm ? static_cast<const Comm*>(comm)->rank : 0; }
+
 void nccl_comm_destroy(void* comm) {
     auto* c = static_cast<Comm*>(comm);
     if (!c) return;

@@ -821,21 +821,22 @@ constexpr int kL2EmitThreads = 128;  // emitting group: two-round tiles of 128 t
 constexpr int kL2EmitGroups = 2;     // independent emitting groups (one warp of each per SM sub-partition)
 constexpr int kL2Slots = 1;          // chunk buffers per phase-1 warp (A comes from L2: see kL2Prefetch)
 constexpr int kL2Threads = kL2P1Warps * 32 + kL2EmitGroups * kL2EmitThreads;
+constexpr int l2_threads(int eg) { return kL2P1Warps * 32 + eg * kL2EmitThreads; }
 constexpr int kL2TileElems = kL2EmitThreads * 64;
 // registers: the launch grants 168 per thread (384 threads); phase-1 warps hand some to the emitting group
 // (64 doubles of tile per thread) with setmaxnreg: 256 x 128 + 128 x 232 <= 384 x 168
 constexpr int kL2Prefetch = 4;  // phase-1 items whose A is prefetched into L2 ahead of the current one
-constexpr int kL2Queue = 8;     // claimed-item queue (> kL2Prefetch + 1)
+constexpr int kL2Queue = 16;    // claimed-item queue (> prefetch distance + 1)
 constexpr int kL2P1Regs = 96;
 constexpr int kL2EmitRegs = 160;
 static_assert(kL2P1Warps * 32 * kL2P1Regs + kL2EmitGroups * kL2EmitThreads * kL2EmitRegs <=
                   kL2Threads * ((65536 / kL2Threads) & ~7),
               "register budget");
 // phase-1 rings (8 warps x 2 x 8 KiB) + padded exchange buffer + mbarriers + 1 KiB alignment slack
-template <int HB>
+template <int HB, int S1 = kL2Slots, int EG = kL2EmitGroups>
 constexpr size_t l2_smem() {
-    return (size_t)(kL2P1Warps * kL2Slots * kChunkDoubles +
-                    kL2EmitGroups * pad_r2<kL2EmitThreads, (kL2TileElems >> HB)>(kL2TileElems) + 2 * kL2P1Warps) *
+    return (size_t)(kL2P1Warps * S1 * kChunkDoubles +
+                    EG * pad_r2<kL2EmitThreads, (kL2TileElems >> HB)>(kL2TileElems) + 2 * kL2P1Warps) *
                sizeof(double) +
            1024 + 64;
 }
@@ -853,6 +854,11 @@ __device__ __forceinline__ int ld_relaxed(const int* p) {
     asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
+__device__ __forceinline__ uint64_t policy_evict_normal() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;\n" : "=l"(pol));
+    return pol;
+}
 __device__ __forceinline__ uint64_t policy_evict_last() {
     uint64_t pol;
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(pol));
@@ -864,13 +870,13 @@ __device__ __forceinline__ void st2_hint(double* p, double a, double b, uint64_t
 __device__ __forceinline__ void discard_l2(const void* p) {
     asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
 }
-template <int HB>
-__global__ void __launch_bounds__(kL2Threads, 1)
-srht_l2_kernel(const __grid_constant__ ChunkMaps maps, const double* __restrict__ A, int64_t n, int64_t lda,
+template <int HB, int P1T, bool TS, int S1, int EG>
+__global__ void __launch_bounds__(l2_threads(EG), 1)
+srht_l2_kernel(const __grid_constant__ ChunkMaps maps, const __grid_constant__ CUtensorMap tmap_T, const double* __restrict__ A, int64_t n, int64_t lda,
                const uint32_t* __restrict__ signbits, double* __restrict__ T, int64_t nfull, int64_t d, int ns,
                const int4* __restrict__ tiles, int n_tiles, const uint32_t* __restrict__ tile_bits,
                const int2* __restrict__ entries, double s1, double s2, double* __restrict__ SA, int64_t m,
-               int* __restrict__ ctl, int discard) {
+               int* __restrict__ ctl, int discard, int dbg, int pf, int tpol) {
     static_assert(HB >= 9 && HB <= 12, "L2-resident tile geometry");
     constexpr int E = 64;                       // registers per emitting thread
     constexpr int R2 = HB - 6;                  // pass bits of round 2
@@ -881,21 +887,24 @@ srht_l2_kernel(const __grid_constant__ ChunkMaps maps, const double* __restrict_
     constexpr int NG = kL2EmitThreads / W;      // round-1 thread groups (= 2^(HB - 6))
     constexpr int64_t NPAD = int64_t{1} << (HB + kChunkL);
     constexpr int CPC = 1 << HB;                // chunks per column
-    constexpr int IPC = CPC / kL2P1Warps;       // phase-1 items per column
-    constexpr int RUN = kL2P1Warps * W;         // contiguous doubles one item stores into each tile
+    constexpr int P1W = kL2P1Warps / P1T;       // warps (= chunks) of a phase-1 item; P1T teams take items independently
+    constexpr int IPC = CPC / P1W;              // phase-1 items per column
+    constexpr int RUN = P1W * W;                // contiguous doubles one item stores into each tile
     constexpr int UPT = RUN / 2;                // ... as 16-byte units
     constexpr int SWZ = (W / 2) * (UPT >= 8 ? 1 : 8 / UPT);  // XOR stride of the chunk copies' 16-byte units
-    static_assert(NG >= kL2P1Warps && RUN % 8 == 0, "an item fills whole 64-byte halves of 128-byte lines");
+    static_assert(NG >= P1W && RUN % 8 == 0, "an item fills whole 64-byte halves of 128-byte lines");
     auto pad = [](int i) { return pad_r2<kL2EmitThreads, W>(i); };
     pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible after this
     extern __shared__ unsigned char l2_raw[];
     double* base = align1024(l2_raw);
     double* rings = base;                                // kL2P1Warps x 2 chunk buffers (1 KiB aligned)
-    double* xs0 = base + kL2P1Warps * kL2Slots * kChunkDoubles;  // emitting-tile exchange buffers (one per group)
-    uint64_t* bars = reinterpret_cast<uint64_t*>(xs0 + kL2EmitGroups * pad(TE));  // 2 per phase-1 warp
-    __shared__ int s_claim[kL2Queue];
+    // rings: slot sl of phase-1 warp w at rings + (sl kL2P1Warps + w) kChunkDoubles, so a team's chunks of one slot
+    // are contiguous (the tensor store's item buffer)
+    double* xs0 = base + kL2P1Warps * S1 * kChunkDoubles;  // emitting-tile exchange buffers (one per group)
+    uint64_t* bars = reinterpret_cast<uint64_t*>(xs0 + EG * pad(TE));  // S1 per phase-1 warp
+    __shared__ int s_claim_all[P1T][kL2Queue];
     __shared__ uint32_t s_bits[16];  // occupancy of the (<= 512) low-index tiles
-    __shared__ int s_p2_all[kL2EmitGroups][2];
+    __shared__ int s_p2_all[EG][2];
     const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
     if (t < 16) s_bits[t] = tile_bits[t];
     __syncthreads();
@@ -905,37 +914,43 @@ srht_l2_kernel(const __grid_constant__ ChunkMaps maps, const double* __restrict_
     int* done2 = ctl + 2 + d;
     if (warp < kL2P1Warps) {
         asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kL2P1Regs));
-        // ---- phase-1 group (warps 0-7, named barrier 2). Item it of column col = it / IPC, r = it % IPC, holds
-        // the 8 chunks q = (r & 63) + 64 (8 (r >> 6) + j), j = warp: their high indices b = q differ only in
-        // b >> 6, so in the c-major tile layout below their W-element pieces of every tile are adjacent — the
-        // item stores RUN contiguous doubles (whole 128-byte lines) per tile instead of 16-byte scraps per chunk.
-        const int j = warp;
-        double* ring = rings + warp * kL2Slots * kChunkDoubles;
-        uint64_t* bar = bars + kL2Slots * warp;
+        // ---- phase-1 teams (P1T teams of P1W warps, named barriers 2 and 5). Item it of column col = it / IPC,
+        // r = it % IPC, holds the P1W chunks q = (r & 63) + 64 (P1W (r >> 6) + j), j = warp in the team: their
+        // high indices b = q differ only in b >> 6, so in the c-major tile layout below their W-element pieces of
+        // every tile are adjacent — the item stores RUN contiguous doubles (whole 128-byte lines for 8-chunk
+        // items, halves for 4) per tile instead of 16-byte scraps per chunk. Two teams overlap one team's chunk
+        // copies with the other's butterflies.
+        const int team = warp / P1W;
+        const int j = warp % P1W;
+        const int tt = t - team * P1W * 32;  // thread index in the team
+        int* s_claim = s_claim_all[team];
+        auto slotbuf = [&](int sl_, int w_) { return rings + ((size_t)sl_ * kL2P1Warps + w_) * kChunkDoubles; };
+        uint64_t* bar = bars + S1 * warp;
         if (lane == 0) {
             tma::mbar_init(&bar[0], 1);
-            if (kL2Slots > 1) tma::mbar_init(&bar[1], 1);
+            if (S1 > 1) tma::mbar_init(&bar[1], 1);
             tma::fence_mbar_init();
         }
         __syncwarp();
-        const GroupBar pbar{2, kL2P1Warps * 32};
+        const GroupBar pbar{team == 0 ? 2 : 5, P1W * 32};
         const int64_t total = d * IPC;
-        const uint64_t pol_first = policy_evict_first(), pol_last = policy_evict_last();
+        const uint64_t pol_first = policy_evict_first();
+        const uint64_t pol_last = tpol == 1 ? policy_evict_normal() : tpol == 2 ? pol_first : policy_evict_last();
         auto chunk_of = [&](int64_t it, int jj) -> int64_t {
             const int r = (int)(it & (IPC - 1));
-            return (r & 63) + 64 * ((r >> 6) * kL2P1Warps + jj);
+            return (r & 63) + 64 * ((r >> 6) * P1W + jj);
         };
         auto issue = [&](int64_t it, int sl) {
             if (it >= total || lane != 0) return;
             const int64_t q = chunk_of(it, j), col = it / IPC;
             if (q >= nfull) return;
-            double* buf = ring + sl * kChunkDoubles;
+            double* buf = slotbuf(sl, warp);
             tma::fence_proxy_async();
             tma::mbar_expect_tx(&bar[sl], kChunkDoubles * sizeof(double));
             tma::load_4d_hint(buf, &maps.even, 0, 0, (int)q, (int)col, &bar[sl], pol_first);
             tma::load_4d_hint(buf + kChunkDoubles / 2, &maps.odd, 0, 0, (int)q, (int)col, &bar[sl], pol_first);
         };
-        // A of item it -> L2 (no shared memory): issued kL2Prefetch items ahead so the shared-memory copy, one
+        // A of item it -> L2 (no shared memory): issued pf items ahead so the shared-memory copy, one
         // item ahead, comes from L2
         auto prefetch = [&](int64_t it) {
             if (it >= total || lane != 0) return;
@@ -945,13 +960,13 @@ srht_l2_kernel(const __grid_constant__ ChunkMaps maps, const double* __restrict_
             tma::prefetch_4d_l2(&maps.odd, 0, 0, (int)q, (int)col);
         };
         // claimed items: queue slot k % kL2Queue holds the k-th item of this CTA; thread 0 claims item k +
-        // kL2Prefetch + 1 during item k (visible to the group after the item's barriers)
-        if (t == 0)
-            for (int k = 0; k <= kL2Prefetch; ++k) s_claim[k] = atomicAdd(p1_counter, 1);
+        // pf + 1 during item k (visible to the group after the item's barriers)
+        if (tt == 0)
+            for (int k = 0; k <= pf; ++k) s_claim[k] = atomicAdd(p1_counter, 1);
         pbar();
         int64_t cur = s_claim[0];
         issue(cur, 0);
-        for (int k = 1; k < kL2Prefetch; ++k) prefetch(s_claim[k]);
+        for (int k = 1; k < pf; ++k) prefetch(s_claim[k]);
         uint32_t phase = 0u;  // bit s: parity of slot s
         int sl = 0;
         int kq = 0;   // queue index of cur
@@ -968,13 +983,13 @@ srht_l2_kernel(const __grid_constant__ ChunkMaps maps, const double* __restrict_
         };
         uint32_t sw = sign_word(cur);
         while (cur < total) {
-            if (kL2Slots > 1) issue(s_claim[(kq + 1) % kL2Queue], sl ^ 1);
-            prefetch(s_claim[(kq + kL2Prefetch) % kL2Queue]);
+            if (S1 > 1) issue(s_claim[(kq + 1) % kL2Queue], sl ^ 1);
+            prefetch(s_claim[(kq + pf) % kL2Queue]);
             int claimed = 0;  // published only after the store loop: the atomic's round trip overlaps the item
-            if (t == 0) claimed = atomicAdd(p1_counter, 1);
+            if (tt == 0) claimed = atomicAdd(p1_counter, 1);
             const int64_t q = chunk_of(cur, j), col = cur / IPC;
             const int64_t r0 = q << kChunkL;
-            double* buf = ring + sl * kChunkDoubles;
+            double* buf = slotbuf(sl, warp);
             if (q < nfull) {
                 tma::mbar_wait(&bar[sl], (phase >> sl) & 1u);
                 phase ^= 1u << sl;
@@ -992,6 +1007,7 @@ srht_l2_kernel(const __grid_constant__ ChunkMaps maps, const double* __restrict_
             double* row0 = buf + (lane << 4);
             double* row1 = buf + ((32 + lane) << 4);
             const int x = lane & 7;
+            if (dbg != 2 && dbg != 4 && dbg != 5 && dbg != 6) {
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
                 const double2 a = *reinterpret_cast<const double2*>(row0 + ((u ^ x) << 1));
@@ -1025,10 +1041,26 @@ srht_l2_kernel(const __grid_constant__ ChunkMaps maps, const double* __restrict_
                 for (int c = 0; c < 32; ++c)
                     if (!(c & (1 << s_))) bfly(v[c], v[c | (1 << s_)]);
             // element e = 32c + lane back into the slot in natural (swizzled) order
+            if constexpr (TS) {
+                // the item's output in the tensor-store box layout [te][chunk j][w] (128-byte swizzle, as the
+                // store map's SWIZZLE_128B expects): it overwrites every slot of the team, so all chunks must
+                // have been read first
+                pbar();
+                char* ib = reinterpret_cast<char*>(slotbuf(sl, team * P1W));
 #pragma unroll
-            for (int c = 0; c < 32; ++c) buf[swz((c << 5) | lane, j)] = v[c];
+                for (int c = 0; c < 32; ++c) {
+                    const int e = (c << 5) | lane;
+                    const int L = (((e >> LOGW) * P1W + j) * W + (e & (W - 1))) * 8;
+                    *reinterpret_cast<double*>(ib + (L ^ (((L >> 7) & 7) << 4))) = v[c];
+                }
+                tma::fence_proxy_async();  // generic writes before the async-proxy (TMA) read of the buffer
+            } else {
+#pragma unroll
+                for (int c = 0; c < 32; ++c) buf[swz((c << 5) | lane, j)] = v[c];
+            }
+            }  // dbg != 2
             // the slot's previous column must be fully emitted before it is overwritten
-            if (t == 0 && col >= ns && col != slot_ok_col) {
+            if (tt == 0 && col >= ns && col != slot_ok_col) {
                 while (ld_relaxed(done2 + (col - ns)) < n_tiles) __nanosleep(64);
                 (void)ld_acquire(done2 + (col - ns));
                 slot_ok_col = col;
@@ -1036,27 +1068,45 @@ srht_l2_kernel(const __grid_constant__ ChunkMaps maps, const double* __restrict_
             pbar();  // every chunk of the item is in its slot; the column's ring slot is free
             // store: tile te gets, at c 128 + 8 (r >> 6) W (c = r & 63), the pieces [chunk j][w] of the 8 chunks
             const int r = (int)(cur & (IPC - 1));
-            double* dst0 = T + (col % ns) * NPAD + (r & 63) * kL2EmitThreads + (r >> 6) * kL2P1Warps * W;
+            if constexpr (TS) {
+                // one thread stores the whole item with (1024 / W) / 256 tensor copies: RUN contiguous doubles
+                // into each tile, evict-last (the emitting side reads them next)
+                constexpr int BOXT = (1024 / W) < 256 ? (1024 / W) : 256;
+                if (tt == 0 && !(dbg >= 3 && dbg <= 5 || dbg == 7)) {
+                    const char* ib = reinterpret_cast<const char*>(slotbuf(sl, team * P1W));
+#pragma unroll
+                    for (int h = 0; h < (1024 / W) / BOXT; ++h)
+                        tma::store_5d_hint(&tmap_T, 0, (r >> 6) * P1W * W / 16, h * BOXT, r & 63, (int)(col % ns),
+                                           ib + (size_t)h * BOXT * P1W * W * 8, pol_last);
+                    tma::bulk_commit();
+                    tma::bulk_wait_read0();  // the slots are refilled by the next item's copies
+                }
+            }
+            double* dst0 = T + (col % ns) * NPAD + (r & 63) * kL2EmitThreads + (r >> 6) * P1W * W;
 #pragma unroll 4
-            for (int i = 0; i < kChunkDoubles / 64; ++i) {
-                const int u = i * (kL2P1Warps * 32) + t;  // 16-byte unit of the item's output
+            for (int i = 0; i < (TS || (dbg >= 3 && dbg <= 5 || dbg == 7) ? 0 : kChunkDoubles / 64); ++i) {
+                const int u = i * (P1W * 32) + tt;  // 16-byte unit of the item's output
                 const int te = u / UPT;
                 const int kk = (u % UPT) << 1;            // double offset inside the run
                 const int jj = kk >> LOGW, w = kk & (W - 1);
                 if (!((s_bits[te >> 5] >> (te & 31)) & 1u)) continue;
-                const double2 val = *reinterpret_cast<const double2*>(rings + (jj * kL2Slots + sl) * kChunkDoubles +
+                const double2 val = *reinterpret_cast<const double2*>(slotbuf(sl, team * P1W + jj) +
                                                                       swz((te << LOGW) + w, jj));
                 st2_hint(dst0 + (int64_t)te * TE + kk, val.x, val.y, pol_last);
             }
-            if (t == 0) s_claim[(kq + kL2Prefetch + 1) % kL2Queue] = claimed;
+            if (tt == 0) s_claim[(kq + pf + 1) % kL2Queue] = claimed;
             pbar();  // the item's stores are issued and every slot sl is read (the next TMA may refill it)
-            if (kL2Slots == 1) issue(s_claim[(kq + 1) % kL2Queue], 0);
+            if (S1 == 1) issue(s_claim[(kq + 1) % kL2Queue], 0);
             // completions are released once per run of this CTA's items in one column (its claims only move to
             // later columns): one release (a memory barrier for thread 0) per column instead of per item
-            if (t == 0) {
+            if (tt == 0) {
                 ++run;
                 const int64_t nx = s_claim[(kq + 1) % kL2Queue];
                 if (nx >= total || nx / IPC != col) {
+                    if constexpr (TS) {  // the tensor stores' global writes are performed and ordered before the
+                        tma::bulk_wait0();  // release that publishes them
+                        tma::fence_proxy_async_global();
+                    }
                     red_release_add(done1 + col, run);
                     run = 0;
                 }
@@ -1064,7 +1114,7 @@ srht_l2_kernel(const __grid_constant__ ChunkMaps maps, const double* __restrict_
             ++kq;
             cur = s_claim[kq % kL2Queue];
             sw = sign_word(cur);
-            if (kL2Slots > 1) sl ^= 1;
+            if (S1 > 1) sl ^= 1;
         }
         return;
     }
@@ -1097,6 +1147,21 @@ srht_l2_kernel(const __grid_constant__ ChunkMaps maps, const double* __restrict_
             ready_col = col;
         }
         gbar();
+        if (dbg == 1 || dbg == 5 || dbg == 6 || dbg == 7) {  // timing probe: the emitting side only hands tiles on
+            if (gt == 0) s_p2[par2] = claimed;
+            gbar();
+            if (gt == 0) {
+                ++run2;
+                const int64_t nx = s_p2[par2];
+                if (nx >= total2 || nx / n_tiles != col) {
+                    red_release_add(done2 + col, run2);
+                    run2 = 0;
+                }
+            }
+            item = s_p2[par2];
+            par2 ^= 1;
+            continue;
+        }
         const double* tptr = T + (col % ns) * NPAD + (int64_t)(tile.x >> LOGW) * TE;
         double v[E];
 #pragma unroll
@@ -1849,14 +1914,65 @@ bool srht_build_mask(const SrhtPlan& p, const std::vector<int4>& tiles, uint32_t
     return true;
 }
 
-template <int HB>
-void launch_l2(const SrhtPlan& p, const ChunkMaps& maps, int64_t nfull, const double* A, const uint32_t* signbits,
+// Tensor-store map of the T ring for the L2-resident launch's phase-1 items (TS), the c-major tile layout: dims
+// (u & 15, u >> 4, tile, b & 63, slot), u = (b >> 6) W + w, strides (8, 128, 8 TE, 8 ET, 8 n_pad) bytes, box
+// (16, P1W W / 16, <= 256 tiles, 1, 1) under SWIZZLE_128B. False when an item's run is narrower than 128 bytes or
+// the driver rejects the map (the item store loop is used then).
+bool srht_l2_store_map(double* T, int HB, int ns, int p1w, CUtensorMap* out) {
+    struct Entry {
+        double* T;
+        int HB, ns, p1w;
+        CUtensorMap map;
+        bool ok;
+    };
+    static std::vector<Entry> cache;
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lock(mu);
+    for (const Entry& e : cache)
+        if (e.T == T && e.HB == HB && e.ns == ns && e.p1w == p1w) {
+            *out = e.map;
+            return e.ok;
+        }
+    const int64_t TE = kL2TileElems, W = TE >> HB, npad = int64_t{1} << (HB + kChunkL);
+    // the 128 doubles u = (b >> 6) W + w of one (tile, b & 63) row are contiguous: split as (u & 15, u >> 4) so
+    // the box's inner dimension is exactly the 128-byte swizzle span (a narrower one is padded to it in shared
+    // memory)
+    if (p1w * W < 16) return false;
+    const cuuint64_t dims[5] = {16, (cuuint64_t)(kL2EmitThreads / 16), (cuuint64_t)(1024 / W), 64, (cuuint64_t)ns};
+    const cuuint64_t strides[4] = {128, (cuuint64_t)(8 * TE), (cuuint64_t)(8 * kL2EmitThreads), (cuuint64_t)(8 * npad)};
+    const cuuint32_t box[5] = {16, (cuuint32_t)(p1w * W / 16), (cuuint32_t)std::min<int64_t>(256, 1024 / W), 1, 1};
+    const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+    CUtensorMap m{};
+    const CUresult r = tma_encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, T, dims, strides, box, estr,
+                                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                       CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (cache.size() >= 32) cache.erase(cache.begin());
+    cache.push_back(Entry{T, HB, ns, p1w, m, r == CUDA_SUCCESS});
+    *out = m;
+    return r == CUDA_SUCCESS;
+}
+
+template <int HB, int P1T, bool TS, int S1 = kL2Slots, int EG = kL2EmitGroups>
+void launch_l2_t(const SrhtPlan& p, const ChunkMaps& maps, int64_t nfull, const double* A, const uint32_t* signbits,
                double* T, const int4* tiles, int n_tiles, const int2* entries, double* SA, int* ctl, int num_sms,
                cudaStream_t st) {
-    IHS_SMEM_ATTR(srht_l2_kernel<HB>, (int)l2_smem<HB>());
+    IHS_SMEM_ATTR((srht_l2_kernel<HB, P1T, TS, S1, EG>), (int)(l2_smem<HB, S1, EG>()));
     static const bool discard = [] {  // IHS_SRHT_L2_DISCARD=0: keep the consumed T lines (A/B of the discard)
         const char* e = std::getenv("IHS_SRHT_L2_DISCARD");
         return !(e && e[0] == '0');
+    }();
+    static const int pf = [] {  // IHS_SRHT_L2_PF: prefetch distance in items (1 .. kL2Queue - 2)
+        const char* e = std::getenv("IHS_SRHT_L2_PF");
+        return e ? std::max(1, std::min(kL2Queue - 2, std::atoi(e))) : kL2Prefetch;
+    }();
+    static const int tpol = [] {  // IHS_SRHT_L2_TPOL: L2 policy of the T stores (0 evict-last, 1 normal, 2 first)
+        const char* e = std::getenv("IHS_SRHT_L2_TPOL");
+        return e ? std::atoi(e) : 0;
+    }();
+    static const int dbg = [] {  // IHS_SRHT_L2_DBG (timing probes, wrong results): 1 emitting side idle, 2 no
+        const char* e = std::getenv("IHS_SRHT_L2_DBG");  // phase-1 transform, 3 no phase-1 store, 4 = 2 + 3,
+                                                         // 5 = 1 + 2 + 3, 6 = 1 + 2, 7 = 1 + 3
+        return e ? std::atoi(e) : 0;
     }();
     CUDA_CHECK(cudaMemsetAsync(ctl, 0, srht_l2_ctl_bytes(p), st));
     const uint32_t* bits = reinterpret_cast<const uint32_t*>(tiles + n_tiles);
@@ -1872,9 +1988,41 @@ void launch_l2(const SrhtPlan& p, const ChunkMaps& maps, int64_t nfull, const do
     if (last[dev & 63] == nullptr) CUDA_CHECK(cudaEventCreateWithFlags(&last[dev & 63], cudaEventDisableTiming));
     CUDA_CHECK(cudaStreamWaitEvent(st, last[dev & 63], 0));
     // one CTA per SM (the launch-bounds/smem footprint allows one)
-    LAUNCH_PDL(srht_l2_kernel<HB>, (unsigned)num_sms, kL2Threads, l2_smem<HB>(), st, maps, A, p.n, p.lda, signbits, T, nfull,
-               p.d, p.l2_ns, tiles, n_tiles, bits, entries, p.scale1, p.scale2, SA, p.sa_ld, ctl, discard ? 1 : 0);
+    CUtensorMap tmap{};
+    if (TS && !srht_l2_store_map(T, HB, p.l2_ns, kL2P1Warps / P1T, &tmap)) fail(IHS_INTERNAL_ERROR, "srht: T store map");
+    LAUNCH_PDL((srht_l2_kernel<HB, P1T, TS, S1, EG>), (unsigned)num_sms, l2_threads(EG), (l2_smem<HB, S1, EG>()), st, maps, tmap, A, p.n, p.lda, signbits, T, nfull,
+               p.d, p.l2_ns, tiles, n_tiles, bits, entries, p.scale1, p.scale2, SA, p.sa_ld, ctl, discard ? 1 : 0, dbg, pf, tpol);
     CUDA_CHECK(cudaEventRecord(last[dev & 63], st));
+}
+template <int HB>
+void launch_l2(const SrhtPlan& p, const ChunkMaps& maps, int64_t nfull, const double* A, const uint32_t* signbits,
+               double* T, const int4* tiles, int n_tiles, const int2* entries, double* SA, int* ctl, int num_sms,
+               cudaStream_t st) {
+    static const int teams = [] {  // IHS_SRHT_L2_TEAMS: phase-1 teams (1: one 8-chunk item at a time, 2: two 4-chunk)
+        const char* e = std::getenv("IHS_SRHT_L2_TEAMS");
+        return e ? std::atoi(e) : 1;
+    }();
+    static const int ts_env = [] {  // IHS_SRHT_L2_TS=0: phase-1 items stored by the thread loop, not by TMA
+        const char* e = std::getenv("IHS_SRHT_L2_TS");
+        return e ? std::atoi(e) : 1;
+    }();
+    CUtensorMap probe{};
+    const bool ts = ts_env != 0 && teams == 1 && srht_l2_store_map(T, HB, p.l2_ns, kL2P1Warps, &probe);
+    static const int shape = [] {  // IHS_SRHT_L2_SHAPE: 0 one chunk slot per phase-1 warp + two emitting groups,
+        const char* e = std::getenv("IHS_SRHT_L2_SHAPE");  // 1 two slots + one emitting group
+        return e ? std::atoi(e) : 0;
+    }();
+    if (shape == 1 && teams == 1) {
+        if (ts) launch_l2_t<HB, 1, true, 2, 1>(p, maps, nfull, A, signbits, T, tiles, n_tiles, entries, SA, ctl, num_sms, st);
+        else launch_l2_t<HB, 1, false, 2, 1>(p, maps, nfull, A, signbits, T, tiles, n_tiles, entries, SA, ctl, num_sms, st);
+        return;
+    }
+    if (teams == 2) {
+        launch_l2_t<HB, 2, false>(p, maps, nfull, A, signbits, T, tiles, n_tiles, entries, SA, ctl, num_sms, st);
+    } else {
+        if (ts) launch_l2_t<HB, 1, true>(p, maps, nfull, A, signbits, T, tiles, n_tiles, entries, SA, ctl, num_sms, st);
+        else launch_l2_t<HB, 1, false>(p, maps, nfull, A, signbits, T, tiles, n_tiles, entries, SA, ctl, num_sms, st);
+    }
 }
 using L2Fn = void (*)(const SrhtPlan&, const ChunkMaps&, int64_t, const double*, const uint32_t*, double*, const int4*,
                       int, const int2*, double*, int*, int, cudaStream_t);

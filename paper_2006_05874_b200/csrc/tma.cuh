@@ -64,5 +64,21 @@ __device__ __forceinline__ void prefetch_4d_l2(const CUtensorMap* map, int c0, i
                  : "memory");
 }
 
+// 5-D tensor store shared -> global (bulk async-group completion) with an L2 cache policy
+__device__ __forceinline__ void store_5d_hint(const CUtensorMap* map, int c0, int c1, int c2, int c3, int c4,
+                                              const void* src, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.tensor.5d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%1, %2, %3, %4, %5}], [%6], %7;" ::
+            "l"(reinterpret_cast<uint64_t>(map)),
+        "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(smem_u32(src)), "l"(pol)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// the committed bulk stores have read their shared-memory source (the buffer may be rewritten)
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+// the committed bulk stores are complete (their global writes performed)
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+
 }  // namespace tma
 }  // namespace ihs_b200

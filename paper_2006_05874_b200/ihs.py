@@ -278,6 +278,14 @@ class NcclComm:
             self.handle = None
 
 
+def comm_selftest(comm, device: int = 0, count: int = 4099) -> int:
+    """Run the sharded path's three collectives (all-reduce sum, all-gather, all-to-all) on exact fp64 patterns
+    through `comm` (NcclComm or EmuComm); returns this rank's wrong elements (0 on success)."""
+    bad = C.c_int64(-1)
+    _check(lib().ihs_gpu_comm_selftest(comm.handle, device, count, C.byref(bad)))
+    return int(bad.value)
+
+
 class EmuComm:
     """One rank's communicator of an EMULATED group (ihs_gpu_emu_comm_create): world_size ranks of this process,
     each driven by its own host thread, run the library's real row-sharded code on one device; collectives are
