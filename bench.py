@@ -113,6 +113,15 @@ def fp64_peak():
         return 37.0, "fallback (B200 fp64 tensor nominal)"
 
 
+def l2_write_peak():
+    """Measured L2-resident write bandwidth (tools/l2_bw.cu -> profiles/l2_bw.json, 96 MiB buffer, whole lines)."""
+    try:
+        j = json.loads((ROOT / "profiles" / "l2_bw.json").read_text())
+        return float(j["96_MiB"]["write_GBps"])
+    except Exception:  # noqa: BLE001
+        return None
+
+
 def ncu_traffic(cfg, which):
     """DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) of the dominant kernel from the
     committed `ncu --set full` summary profiles/traffic.json (written by tools/ncu_traffic.py), or None."""
@@ -538,6 +547,18 @@ def main():
                               "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
                               "algorithmic_bytes_per_launch": t["sketch_bytes"] / t["n_sketch_kernel"],
                               "peak_source": peak_kind}
+            # the two-pass transform writes every element twice into L2 (A's fill from HBM, then the phase-1
+            # result T into the on-chip ring), and L2 absorbs writes at about the HBM rate: the L2-write roofline
+            # (16 n d + 8 m d bytes per sketch against the measured L2 write bandwidth) is the one the launch sits on
+            l2w = l2_write_peak()
+            n_pad = 1 << (int(c["n"]) - 1).bit_length()
+            l2_bytes = t["sketch_bytes"] + t["n_sketch_kernel"] * 8.0 * n_pad * c["d"]
+            if l2w:
+                a2 = l2_bytes / (sk_ms * 1e-3) / 1e9
+                kern["sketch"]["l2_write_roofline"] = {
+                    "bytes_per_launch": l2_bytes / t["n_sketch_kernel"], "achieved": a2, "peak": l2w, "unit": "GB/s",
+                    "frac": a2 / l2w, "peak_source": "measured (tools/l2_bw.cu: L2-resident whole-line stores, "
+                                                     "profiles/l2_bw.json)"}
         else:
             ach = t["sketch_flops"] / (sk_ms * 1e-3) / 1e12
             kern["sketch"] = {"kernel": "dgemm_nn_big_kernel S*A (128x128 cp.async tiles, mma.sync m8n8k4 f64 = "
