@@ -730,7 +730,30 @@ void cholesky_invert(const double* d_L, int64_t n, double* d_W, double* d_tmp, c
             LAUNCH_PDL(tri_inv64_kernel, (unsigned)ceil_div(n, NB), 256, ti_smem, st, d_L, n, d_W);
         }
     }
-    tri_inv_rec(d_L, d_W, n, 0, n, d_tmp, st, base);
+    // n = base * 2^L: the recursion's nodes of one size are independent and equally shaped, so each level is
+    // two strided-batched products (2 L launches instead of 2 (2^L - 1)); otherwise the recursion itself
+    static const bool rec_only = [] {  // IHS_TRI_INV_REC=1: the depth-first recursion (A/B)
+        const char* e = std::getenv("IHS_TRI_INV_REC");
+        return e && e[0] == '1';
+    }();
+    int64_t blocks = n / base;
+    if (!rec_only && n % base == 0 && blocks > 1 && (blocks & (blocks - 1)) == 0) {
+        for (int64_t h = base; h < n; h *= 2) {
+            const int64_t s = 2 * h, nodes = n / s, diag = s * (n + 1);  // node i: rows/cols [i s, i s + s)
+            // tmp_i (h x h) = L21_i W11_i;  W21_i = -W22_i tmp_i
+            if (nodes == 1) {  // the top level: one product, on whichever kernel suits its size
+                dgemm(false, false, h, h, h, 1.0, d_L + h, n, d_W, n, 0.0, d_tmp, h, false, 1, nullptr, st);
+                dgemm(false, false, h, h, h, -1.0, d_W + h + h * n, n, d_tmp, h, 0.0, d_W + h, n, false, 1, nullptr, st);
+                continue;
+            }
+            dgemm_batched(false, false, h, h, h, 1.0, d_L + h, n, diag, d_W, n, diag, 0.0, d_tmp, h, h * h,
+                          (int)nodes, st);
+            dgemm_batched(false, false, h, h, h, -1.0, d_W + h + h * n, n, diag, d_tmp, h, h * h, 0.0, d_W + h, n, diag,
+                          (int)nodes, st);
+        }
+    } else {
+        tri_inv_rec(d_L, d_W, n, 0, n, d_tmp, st, base);
+    }
     dim3 grid((unsigned)ceil_div(n, 32), (unsigned)ceil_div(n, 32));
     LAUNCH_PDL(mirror_upper_kernel, grid, dim3(32, 8), 0, st, d_W, n);
 }

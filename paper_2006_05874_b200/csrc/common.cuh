@@ -189,6 +189,9 @@ void nccl_alltoall(const double* send, double* recv, size_t count_per_rank, void
 // transA: A stored K x M col-major (lda); else M x K col-major. transB: B
 // stored N x K; else K x N. lower_only: skip tiles strictly above diagonal.
 // splitk > 1: deterministic split-K through d_work (splitk*M*N doubles).
+void dgemm_batched(bool transA, bool transB, int64_t M, int64_t N, int64_t K, double alpha, const double* A,
+                   int64_t lda, int64_t sA, const double* B, int64_t ldb, int64_t sB, double beta, double* C, int64_t ldc,
+                   int64_t sC, int batch, cudaStream_t st);
 void dgemm(bool transA, bool transB, int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t lda,
            const double* B, int64_t ldb, double beta, double* C, int64_t ldc, bool lower_only, int splitk,
            double* d_work, cudaStream_t st);

@@ -30,12 +30,20 @@ template <bool TA, bool TB>
 __global__ void __launch_bounds__(THREADS)
 dgemm_kernel(int64_t M, int64_t N, int64_t K, double alpha, const double* __restrict__ A, int64_t lda,
              const double* __restrict__ B, int64_t ldb, double beta, double* __restrict__ C, int64_t ldc,
-             int lower_only, int64_t k_per_split, double* __restrict__ work) {
+             int lower_only, int64_t k_per_split, double* __restrict__ work, int64_t sA = 0, int64_t sB = 0,
+             int64_t sC = 0) {
     pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible after this
     const int64_t m0 = (int64_t)blockIdx.x * BM;
     const int64_t n0 = (int64_t)blockIdx.y * BN;
     if (lower_only && n0 > m0 + BM - 1) return;
-    const int64_t kbeg = (int64_t)blockIdx.z * k_per_split;
+    // strided batch (sC != 0): blockIdx.z is the problem index, no split-K
+    const bool batched = sC != 0;
+    if (batched) {
+        A += (int64_t)blockIdx.z * sA;
+        B += (int64_t)blockIdx.z * sB;
+        C += (int64_t)blockIdx.z * sC;
+    }
+    const int64_t kbeg = batched ? 0 : (int64_t)blockIdx.z * k_per_split;
     const int64_t kend = min(K, kbeg + k_per_split);
 
     __shared__ double As[BK][LDS];
@@ -335,6 +343,24 @@ int dgemm_pick_splitk(int64_t M, int64_t N, int64_t K, int num_sms, bool transA,
     return s;
 }
 
+// C_i = alpha op(A_i) op(B_i) + beta C_i for i < batch, X_i = X + i sX (the 64x64 DMMA kernel, one launch)
+void dgemm_batched(bool transA, bool transB, int64_t M, int64_t N, int64_t K, double alpha, const double* A,
+                   int64_t lda, int64_t sA, const double* B, int64_t ldb, int64_t sB, double beta, double* C, int64_t ldc,
+                   int64_t sC, int batch, cudaStream_t st) {
+    if (M <= 0 || N <= 0 || K <= 0 || batch <= 0) fail(IHS_INTERNAL_ERROR, "dgemm_batched: empty product");
+    if (sC == 0) fail(IHS_INTERNAL_ERROR, "dgemm_batched: output stride must be nonzero");
+    const dim3 grid((unsigned)ceil_div(M, BM), (unsigned)ceil_div(N, BN), (unsigned)batch);
+    const int64_t kps = ceil_div(K, BK) * BK;
+#define IHS_BATCHED(TA_, TB_)                                                                                    \
+    LAUNCH_PDL((dgemm_kernel<TA_, TB_>), grid, THREADS, 0, st, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, 0, kps, \
+               (double*)nullptr, sA, sB, sC)
+    if (!transA && !transB) IHS_BATCHED(false, false);
+    else if (transA && !transB) IHS_BATCHED(true, false);
+    else if (!transA && transB) IHS_BATCHED(false, true);
+    else IHS_BATCHED(true, true);
+#undef IHS_BATCHED
+}
+
 void dgemm(bool transA, bool transB, int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t lda,
            const double* B, int64_t ldb, double beta, double* C, int64_t ldc, bool lower_only, int splitk,
            double* d_work, cudaStream_t st) {
@@ -375,16 +401,16 @@ void dgemm(bool transA, bool transB, int64_t M, int64_t N, int64_t K, double alp
 #undef IHS_BIG
     else if (!transA && !transB)
         LAUNCH_PDL((dgemm_kernel<false, false>), grid, THREADS, 0, st, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc,
-               (int)lower_only, kps, work);
+               (int)lower_only, kps, work, (int64_t)0, (int64_t)0, (int64_t)0);
     else if (transA && !transB)
         LAUNCH_PDL((dgemm_kernel<true, false>), grid, THREADS, 0, st, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc,
-               (int)lower_only, kps, work);
+               (int)lower_only, kps, work, (int64_t)0, (int64_t)0, (int64_t)0);
     else if (!transA && transB)
         LAUNCH_PDL((dgemm_kernel<false, true>), grid, THREADS, 0, st, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc,
-               (int)lower_only, kps, work);
+               (int)lower_only, kps, work, (int64_t)0, (int64_t)0, (int64_t)0);
     else
         LAUNCH_PDL((dgemm_kernel<true, true>), grid, THREADS, 0, st, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc,
-               (int)lower_only, kps, work);
+               (int)lower_only, kps, work, (int64_t)0, (int64_t)0, (int64_t)0);
     if (work) {
         const int64_t total = M * N;
         const int blocks = (int)std::min<int64_t>(ceil_div(total, 256), 148 * 8);

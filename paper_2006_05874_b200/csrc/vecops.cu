@@ -192,6 +192,18 @@ __global__ void __launch_bounds__(32 * SV_W) symv_col_kernel(const double* __res
     if (i < k) {
         const double* col = H + i * k;
         int64_t t = lane;
+        // eight column loads in flight per lane before any is consumed (one L2 round trip per 256 rows instead
+        // of one per 64)
+        for (; t + 224 < k; t += 256) {
+            double a[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) a[u] = __ldcg(col + t + 32 * u);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                acc[0][u & 1] = fma(a[u], xs[t + 32 * u], acc[0][u & 1]);
+                if (nrhs > 1) acc[1][u & 1] = fma(a[u], xs[k + t + 32 * u], acc[1][u & 1]);
+            }
+        }
         for (; t + 32 < k; t += 64) {
             const double a0 = col[t], a1 = col[t + 32];
             acc[0][0] = fma(a0, xs[t], acc[0][0]);
