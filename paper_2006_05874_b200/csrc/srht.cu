@@ -1079,7 +1079,7 @@ srht_l2_kernel(const __grid_constant__ ChunkMaps maps, const __grid_constant__ C
                         tma::store_5d_hint(&tmap_T, 0, (r >> 6) * P1W * W / 16, h * BOXT, r & 63, (int)(col % ns),
                                            ib + (size_t)h * BOXT * P1W * W * 8, pol_last);
                     tma::bulk_commit();
-                    tma::bulk_wait_read0();  // the slots are refilled by the next item's copies
+                    if (dbg != 8) tma::bulk_wait_read0();  // the slots are refilled by the next item's copies
                 }
             }
             double* dst0 = T + (col % ns) * NPAD + (r & 63) * kL2EmitThreads + (r >> 6) * P1W * W;
@@ -1971,7 +1971,8 @@ void launch_l2_t(const SrhtPlan& p, const ChunkMaps& maps, int64_t nfull, const 
     }();
     static const int dbg = [] {  // IHS_SRHT_L2_DBG (timing probes, wrong results): 1 emitting side idle, 2 no
         const char* e = std::getenv("IHS_SRHT_L2_DBG");  // phase-1 transform, 3 no phase-1 store, 4 = 2 + 3,
-                                                         // 5 = 1 + 2 + 3, 6 = 1 + 2, 7 = 1 + 3
+                                                         // 5 = 1 + 2 + 3, 6 = 1 + 2, 7 = 1 + 3,
+                                                         // 8 = no wait for the item store's shared reads
         return e ? std::atoi(e) : 0;
     }();
     CUDA_CHECK(cudaMemsetAsync(ctl, 0, srht_l2_ctl_bytes(p), st));
