@@ -73,6 +73,37 @@ def _worker(rank, world, port, case, q):
         s2 = np.sqrt(float(n_pad) / float(m))
         SA = (comb * s1) * s2
         ok_srht = bool(np.array_equal(SA, O.srht_sketch(A, m, seed)))
+        # ---- owner-reduce exchange (the device path, runtime.cpp device_sketch): row k is owned by rank
+        # k // mq; an all-to-all hands each owner the P partials of its rows, the owner runs the top stages over
+        # the shard index in order, and an all-gather assembles SA on every rank
+        mq = -(-m // world)
+        send = np.zeros((world, mq, d))
+        for k in range(m):
+            send[k // mq, k % mq] = U_r[k]
+        recv = torch.zeros(world * mq * d, dtype=torch.float64)
+        dist.all_to_all_single(recv, torch.from_numpy(send.reshape(-1)))
+        Vq = fwht_unnormalized(recv.numpy().reshape(world, mq, d))  # [source rank p][my rows][d]
+        mine = np.zeros((mq, d))
+        for kk in range(mq):
+            k = rank * mq + kk
+            if k < m:
+                mine[kk] = (Vq[hi[k], kk] * s1) * s2
+        blocks = [torch.zeros(mq * d, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(blocks, torch.from_numpy(mine.reshape(-1)))
+        SA_or = np.concatenate([t.numpy().reshape(mq, d) for t in blocks])[:m]
+        ok_srht = ok_srht and bool(np.array_equal(SA_or, SA))
+        # ---- split SYRK (system_factorize with split_comm): this rank's ceil(m/P) rows of the replicated SA
+        # (Gram), or its ceil(d/P) columns (Woodbury inner), then an all-reduce of the k x k partials
+        r0 = min(m, rank * mq)
+        G = torch.from_numpy(np.ascontiguousarray(SA[r0:r0 + mq].T @ SA[r0:r0 + mq]))
+        dist.all_reduce(G)
+        dq = -(-d // world)
+        c0 = min(d, rank * dq)
+        Ii = torch.from_numpy(np.ascontiguousarray(SA[:, c0:c0 + dq] @ SA[:, c0:c0 + dq].T))
+        dist.all_reduce(Ii)
+        G_ref, I_ref = SA.T @ SA, SA @ SA.T
+        ok_srht = ok_srht and bool(np.linalg.norm(G.numpy() - G_ref) <= 1e-13 * np.linalg.norm(G_ref) * world)
+        ok_srht = ok_srht and bool(np.linalg.norm(Ii.numpy() - I_ref) <= 1e-13 * np.linalg.norm(I_ref) * world)
         # ---- gradient partial + all_reduce (+ nu^2 x once)
         x = np.random.default_rng(7).standard_normal(d)
         Ar, br = A[row0:row0 + rows], b[row0:row0 + rows]
@@ -104,7 +135,7 @@ def test_sharded_srht_and_gradient_gloo(world, case):
         p.join(timeout=60)
         assert p.exitcode == 0
     assert sorted(r[0] for r in results) == list(range(world))
-    assert all(r[1] for r in results), "sharded SRHT differs from the single-process oracle"
+    assert all(r[1] for r in results), "sharded SRHT / owner-reduce / split Gram differs from the single process"
     assert all(r[2] for r in results), "sharded gradient differs from the oracle"
 
 
