@@ -796,131 +796,6 @@ bool cholesky_factor_coop(double* d_H, int64_t n, double* d_Xd, int* d_info, int
     return true;
 }
 
-// ---------------------------------------------------------------- small sketched systems (k <= 64)
-// The whole factorization of a k x k sketched system in ONE launch (one CTA): the product (Woodbury inner
-// SA SA^T or Gram SA^T SA, staged through shared memory in 32-wide slices of the inner dimension) + nu^2 I, the
-// finiteness check of SA, an unblocked right-looking LLT, the triangular inverse W = L^{-1} (a column per
-// thread) with W^T mirrored into the strict upper triangle, and on the Gram path H^{-1} = W^T W. It replaces
-// the check / SYRK / diagonal / LLT / inverse / mirror chain (8-10 launches) of the early doublings, whose k
-// is 1..64. Tolerance-level parity with the chain (its products sum in another order).
-constexpr int SMK = 64;
-__global__ void __launch_bounds__(256) small_system_kernel(const double* __restrict__ SA, int64_t lds, int64_t k,
-                                                           int64_t K, int woodbury, double nu2,
-                                                           double* __restrict__ W, double* __restrict__ Hinv,
-                                                           int* __restrict__ info) {
-    pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible after this
-    extern __shared__ double ss_raw[];
-    double(*a)[SMK + 1] = reinterpret_cast<double(*)[SMK + 1]>(ss_raw);                    // H, then L (lower)
-    double(*x)[SMK + 1] = reinterpret_cast<double(*)[SMK + 1]>(ss_raw + SMK * (SMK + 1));  // SA slice, then W
-    __shared__ double s_pivinv;
-    __shared__ int s_bad, s_fail;
-    const int tid = threadIdx.x;
-    const int kk = (int)k;
-    if (tid == 0) s_bad = 0, s_fail = 0;
-    // this thread's lower-triangle entries e = tid, tid + 256, ... of the packed k (k + 1) / 2 triangle
-    const int ntri = kk * (kk + 1) / 2;
-    double acc[9];
-    int ei[9], ej[9];
-#pragma unroll
-    for (int q = 0; q < 9; ++q) {
-        acc[q] = 0.0;
-        int e = tid + 256 * q, i = 0;
-        while (e >= i + 1) e -= ++i;  // row i holds entries (i, 0..i)
-        ei[q] = i;
-        ej[q] = e;
-    }
-    // vector i, element t: Woodbury SA[i, t] (row i of the m x d sketch); Gram SA[t, i] (column i)
-    for (int64_t t0 = 0; t0 < K; t0 += 32) {
-        __syncthreads();
-        for (int e = tid; e < kk * 32; e += 256) {
-            const int i = woodbury ? e % kk : e / 32, t = woodbury ? e / kk : e % 32;
-            double v = 0.0;
-            if (t0 + t < K) {
-                v = woodbury ? SA[i + (t0 + t) * lds] : SA[(t0 + t) + i * lds];
-                if (!isfinite(v)) s_bad = 1;
-            }
-            x[i][t] = v;
-        }
-        __syncthreads();
-#pragma unroll
-        for (int q = 0; q < 9; ++q)
-            if (tid + 256 * q < ntri) {
-                double sq = acc[q];
-#pragma unroll 8
-                for (int t = 0; t < 32; ++t) sq = fma(x[ei[q]][t], x[ej[q]][t], sq);
-                acc[q] = sq;
-            }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int q = 0; q < 9; ++q)
-        if (tid + 256 * q < ntri) a[ei[q]][ej[q]] = acc[q] + (ei[q] == ej[q] ? nu2 : 0.0);
-    __syncthreads();
-    // unblocked right-looking LLT (a non-positive / non-finite pivot records column + 1, a harmless pivot
-    // is substituted so the kernel completes)
-    for (int j = 0; j < kk; ++j) {
-        if (tid == 0) {
-            double d = a[j][j];
-            if (!(d > 0.0) || !isfinite(d)) {
-                if (!s_fail) s_fail = j + 1;
-                d = 1.0;
-            }
-            const double l = sqrt(d);
-            a[j][j] = l;
-            s_pivinv = 1.0 / l;
-        }
-        __syncthreads();
-        for (int i = j + 1 + tid; i < kk; i += 256) a[i][j] *= s_pivinv;
-        __syncthreads();
-        const int r = kk - j - 1;  // trailing (i, c), j < c <= i < k
-        for (int e = tid; e < r * r; e += 256) {
-            const int i = e % r, c = e / r;  // consecutive threads: consecutive rows (distinct banks)
-            if (c > i) continue;
-            const int ii = j + 1 + i, cc = j + 1 + c;
-            a[ii][cc] = fma(-a[ii][j], a[cc][j], a[ii][cc]);
-        }
-        __syncthreads();
-    }
-    // W = L^{-1}: thread c forms column c by forward substitution
-    if (tid < kk) {
-        const int c = tid;
-        for (int i = 0; i < c; ++i) x[i][c] = 0.0;
-        x[c][c] = 1.0 / a[c][c];
-        for (int i = c + 1; i < kk; ++i) {
-            double sum = 0.0;
-            for (int t = c; t < i; ++t) sum = fma(a[i][t], x[t][c], sum);
-            x[i][c] = -sum / a[i][i];
-        }
-    }
-    __syncthreads();
-    for (int e = tid; e < kk * kk; e += 256) {
-        const int i = e % kk, j = e / kk;
-        W[i + (int64_t)j * kk] = i >= j ? x[i][j] : x[j][i];  // lower: W; strict upper: W^T mirrored
-    }
-    if (Hinv) {  // H^{-1} = W^T W (symmetric, both triangles)
-        for (int e = tid; e < kk * kk; e += 256) {
-            const int i = e % kk, j = e / kk;
-            double sum = 0.0;
-            for (int t = i > j ? i : j; t < kk; ++t) sum = fma(x[t][i], x[t][j], sum);
-            Hinv[i + (int64_t)j * kk] = sum;
-        }
-    }
-    if (tid == 0) {
-        info[0] = s_fail;
-        if (s_bad) info[1] = 1;
-    }
-}
-
-bool small_system_factor(const double* d_SA, int64_t lds, int64_t m, int64_t d, bool woodbury, double nu2,
-                         double* d_W, double* d_Hinv, int* d_info, cudaStream_t st) {
-    const int64_t k = woodbury ? m : d, K = woodbury ? d : m;
-    if (k < 1 || k > SMK) return false;
-    const size_t smem = (size_t)2 * SMK * (SMK + 1) * sizeof(double);
-    IHS_SMEM_ATTR(small_system_kernel, (int)smem);
-    LAUNCH_PDL(small_system_kernel, 1, 256, smem, st, d_SA, lds, k, K, woodbury ? 1 : 0, nu2, d_W, d_Hinv, d_info);
-    return true;
-}
-
 void cholesky_factor(double* d_H, int64_t n, double* d_Xd, int* d_info, int num_sms, cudaStream_t st) {
     (void)num_sms;
     CUDA_CHECK(cudaMemsetAsync(d_info, 0, sizeof(int), st));

@@ -304,9 +304,5 @@ void tril_copy(const double* W, int64_t k, double* Wl, cudaStream_t st);
 void add_diag(double* H, int64_t n, double v, cudaStream_t st);
 void add_scaled(double* y, const double* x, double a, int64_t n, cudaStream_t st);  // y = y + a x
 void check_finite(const double* v, int64_t count, int* d_flag, cudaStream_t st);
-// the whole k x k sketched-system factorization (k <= 64) in one launch: W (with the mirrored upper triangle),
-// H^{-1} when d_Hinv != nullptr (Gram path), info[0] = failing column + 1, info[1] = 1 on a non-finite SA
-bool small_system_factor(const double* d_SA, int64_t lds, int64_t m, int64_t d, bool woodbury, double nu2,
-                         double* d_W, double* d_Hinv, int* d_info, cudaStream_t st);
 
 }  // namespace ihs_b200
