@@ -88,6 +88,30 @@ def test_sharded_sketches_and_gradient(gpu, O, P):
     del probs, comms
 
 
+@pytest.mark.parametrize("P,n", [(2, (1 << 21) - 3), (4, (1 << 22) - 5), (2, (1 << 23) - 7)])
+def test_sharded_srht_l2_resident(gpu, O, P, n):
+    """Shards of 2^20..2^22 padded rows (10..12 high bits) take the L2-resident launch with the owner-block
+    emission: bit-identical to the single-GPU sketch, and to the oracle, with ragged last shards."""
+    d = 2
+    A = np.asfortranarray(np.random.default_rng(n % 97).standard_normal((n, d)))
+    b = np.zeros(n)
+    comms, probs = _shards(gpu, A, b, 1e-2, P)
+    single = gpu.ProblemInstance(A, b, 1e-2)
+    ms = (4097, 70001)
+
+    def work(r):
+        return [gpu.srht_sketch(probs[r], m, 31 + m) for m in ms]
+
+    res = _run_ranks(P, work)
+    for r in range(1, P):
+        for a, b_ in zip(res[0], res[r]):
+            assert np.array_equal(a, b_), f"rank {r} differs from rank 0"
+    for m, SA in zip(ms, res[0]):
+        assert np.array_equal(SA, gpu.srht_sketch(single, m, 31 + m)), f"m={m}: sharded L2 sketch differs"
+    assert np.array_equal(res[0][0], O.srht_sketch(A, ms[0], 31 + ms[0]))
+    del probs, comms
+
+
 @pytest.mark.parametrize("P,kind", [(2, "SRHT"), (4, "SRHT"), (8, "SRHT"), (2, "Gaussian"), (4, "Gaussian")])
 def test_sharded_adaptive_solve(gpu, P, kind):
     n, d = 60000, 48
