@@ -353,7 +353,96 @@ GradPlan grad_plan(int64_t n, int64_t d, int64_t lda, int num_sms) {
     return p;
 }
 
-size_t grad_work_doubles(const GradPlan& p) { return (size_t)p.grid * 2 * p.d; }
+// ---- v6: A too large for a row-major copy and too large for L2 — two streaming passes over column-major A.
+// The fused column-major kernels (v2/v3) stage R-row panels, so each column contributes only an R x 8-byte
+// segment per panel (1.2 TB/s at C4's shape); here every access is a long contiguous column run instead:
+//   pass 1: R = A X - b, one CTA per 1024 rows, the columns streamed 4 at a time (8 KiB runs per column);
+//   pass 2: per-block partials of A^T R, one CTA per 4096 rows (R's block in shared memory), one warp per
+//           column at a time (32 KiB runs), partials reduced in fixed order by grad_reduce_kernel (+ nu^2 X).
+constexpr int GC1_ROWS = 1024, GC2_ROWS = 4096;
+template <int NR>
+__global__ void __launch_bounds__(256) gcol_residual_kernel(const double* __restrict__ A, int64_t d, int64_t lda,
+                                                            const double* __restrict__ b, const double* __restrict__ X,
+                                                            double* __restrict__ R) {
+    pdl_wait();
+    extern __shared__ double gxs[];  // NR x d
+    for (int64_t e = threadIdx.x; e < (int64_t)NR * d; e += 256) gxs[e] = X[e];
+    __syncthreads();
+    const int64_t i0 = (int64_t)blockIdx.x * GC1_ROWS + threadIdx.x;
+    double acc[NR][4];
+#pragma unroll
+    for (int q = 0; q < NR; ++q)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) acc[q][v] = 0.0;
+    for (int64_t j = 0; j < d; j += 4) {
+        double a[4][4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+                const int64_t i = i0 + 256 * v;
+                a[u][v] = (j + u < d && i < lda) ? __ldcs(A + i + (j + u) * lda) : 0.0;
+            }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (j + u < d)
+#pragma unroll
+                for (int q = 0; q < NR; ++q) {
+                    const double xv = gxs[q * d + j + u];
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) acc[q][v] = fma(a[u][v], xv, acc[q][v]);
+                }
+    }
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+        const int64_t i = i0 + 256 * v;
+        if (i < lda)
+#pragma unroll
+            for (int q = 0; q < NR; ++q) R[q * lda + i] = acc[q][v] - b[i];
+    }
+}
+
+template <int NR>
+__global__ void __launch_bounds__(256) gcol_partial_kernel(const double* __restrict__ A, int64_t d, int64_t lda,
+                                                           const double* __restrict__ R, double* __restrict__ part) {
+    pdl_wait();
+    extern __shared__ double grs[];  // NR x GC2_ROWS
+    const int64_t i0 = (int64_t)blockIdx.x * GC2_ROWS;
+    const int rows = (int)(lda - i0 < GC2_ROWS ? lda - i0 : GC2_ROWS);
+    for (int e = threadIdx.x; e < NR * GC2_ROWS; e += 256) {
+        const int q = e / GC2_ROWS, i = e % GC2_ROWS;
+        grs[e] = i < rows ? R[q * lda + i0 + i] : 0.0;
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    double* out = part + (int64_t)blockIdx.x * NR * d;
+    for (int64_t j = w; j < d; j += 8) {
+        const double* col = A + j * lda + i0;
+        double s[NR][2];
+#pragma unroll
+        for (int q = 0; q < NR; ++q) s[q][0] = s[q][1] = 0.0;
+        for (int t = lane; t < rows; t += 256) {
+            double a[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) a[u] = t + 32 * u < rows ? __ldcs(col + t + 32 * u) : 0.0;
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+#pragma unroll
+                for (int q = 0; q < NR; ++q) s[q][u & 1] = fma(a[u], grs[q * GC2_ROWS + t + 32 * u], s[q][u & 1]);
+        }
+#pragma unroll
+        for (int q = 0; q < NR; ++q) {
+            double v = s[q][0] + s[q][1];
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+            if (lane == 0) out[q * d + j] = v;
+        }
+    }
+}
+
+size_t grad_work_doubles(const GradPlan& p) {
+    return (size_t)p.grid * 2 * p.d + (p.version == 6 ? (size_t)2 * p.lda : 0);
+}
 
 bool grad_plan_use_rowmajor(GradPlan& p) {
     static const bool disabled = [] {
@@ -387,6 +476,16 @@ void grad_plan_attach_tma(GradPlan& p, const double* d_A) {
         const char* e = std::getenv("IHS_GRAD_NO_TMA");
         return e && e[0] == '1';
     }();
+    static const bool no_colpass = [] {  // IHS_GRAD_NO_COLPASS=1: keep the fused column-major kernels (A/B)
+        const char* e = std::getenv("IHS_GRAD_NO_COLPASS");
+        return e && e[0] == '1';
+    }();
+    // A beyond L2 by far (> 1 GiB): the two streaming passes (x in shared memory: d <= 8192)
+    if (!no_colpass && 8.0 * (double)p.lda * (double)p.d > (double)(1ll << 30) && p.d <= 8192) {
+        p.version = 6;
+        p.grid = (int)ceil_div(p.lda, (int64_t)GC2_ROWS);
+        return;
+    }
     if (disabled || p.version != 2) return;
     if (grad_tma_smem(p.d, p.R, 2, p.stages) > 225u * 1024) return;
     if (!grad_tma_make_map(d_A, p.lda, p.d, p.R, p.tmap)) return;
@@ -400,6 +499,26 @@ void grad_run(const GradPlan& p, const double* d_A, const double* d_b, double nu
         if (p.version != 5)
             candidates(cs->x, cs->xprev, cs->gt, cs->mu_p, cs->beta_p, cs->mu_gd, p.d, nrhs == 2 ? cs->out : nullptr,
                        nrhs == 2 ? cs->out + p.d : cs->out, st);
+    }
+    if (p.version == 6) {
+        double* R = d_work + (size_t)p.grid * 2 * p.d;
+        const size_t xs = (size_t)nrhs * p.d * sizeof(double), rs = (size_t)nrhs * GC2_ROWS * sizeof(double);
+        const unsigned g1 = (unsigned)ceil_div(p.lda, (int64_t)GC1_ROWS);
+        if (nrhs == 1) {
+            IHS_SMEM_ATTR((gcol_residual_kernel<1>), 64 * 1024);
+            IHS_SMEM_ATTR((gcol_partial_kernel<1>), 64 * 1024);
+            LAUNCH_PDL(gcol_residual_kernel<1>, g1, 256, xs, st, d_A, p.d, p.lda, d_b, d_X, R);
+            LAUNCH_PDL(gcol_partial_kernel<1>, (unsigned)p.grid, 256, rs, st, d_A, p.d, p.lda, (const double*)R, d_work);
+        } else {
+            IHS_SMEM_ATTR((gcol_residual_kernel<2>), 128 * 1024);
+            IHS_SMEM_ATTR((gcol_partial_kernel<2>), 64 * 1024);
+            LAUNCH_PDL(gcol_residual_kernel<2>, g1, 256, xs, st, d_A, p.d, p.lda, d_b, d_X, R);
+            LAUNCH_PDL(gcol_partial_kernel<2>, (unsigned)p.grid, 256, rs, st, d_A, p.d, p.lda, (const double*)R, d_work);
+        }
+        const int64_t total = (int64_t)nrhs * p.d;
+        LAUNCH_PDL(grad_reduce_kernel, dim3((unsigned)ceil_div(total, 16)), dim3(256), 0, st, (const double*)d_work,
+                   p.grid, p.d, nrhs, d_X, nu2, d_G);
+        return;
     }
     if (p.version >= 2) {
         if (p.version == 5) grad_rr_run(p, d_Arm, d_b, d_X, nrhs, d_work, st, cs);

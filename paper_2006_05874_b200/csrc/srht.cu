@@ -1764,8 +1764,8 @@ void srht_unpack_blocks(const double* d_G, int P, int64_t mq, int64_t m, int64_t
 size_t srht_scratch_bytes(const SrhtPlan& p) { return p.H > 0 ? (size_t)p.n_pad * (size_t)p.d * sizeof(double) : 0; }
 
 bool srht_plan_l2(SrhtPlan& p) {
-    // default for single-pass plans with 10..12 high bits (IHS_SRHT_L2=0: the two-kernel path; =1 also allows 9
-    // high bits; IHS_SRHT_L2_NS sets the ring depth). T stays in L2, so HBM sees A and SA only.
+    // default for single-pass plans with 9..12 high bits (IHS_SRHT_L2=0: the two-kernel path; IHS_SRHT_L2_NS sets
+    // the ring depth). T stays in L2, so HBM sees A and SA only.
     // Measured (device sketch, ms, two-kernel -> L2): C4 n_pad 2^22 m 8192 40.4 -> 36.3, m 131072 48.6 -> 44.6
     // (ring depth 3, 96 MB); n_pad 2^20 m 65536: C3 7.02 -> 6.77, C5 27.4 -> 26.9 (depth >= 6). Shallower rings
     // couple the two halves column by column and lose (C4 depth 2: 40.3; n_pad 2^20 depth 3: 10.2).
@@ -1777,7 +1777,9 @@ bool srht_plan_l2(SrhtPlan& p) {
         const char* e = std::getenv("IHS_SRHT_L2_NS");
         return e ? std::atoi(e) : 0;
     }();
-    const int min_h = mode == 1 ? 9 : 10;
+    // 9 high bits (a 2^19-row column: C4 over 8 GPUs, C5 over 2) measured 18.1 vs 20.4 ms for the two-kernel path
+    // (n = 2^19, d = 2048, m = 4096, incl. the SA read-back)
+    const int min_h = 9;
     if (mode == 0 || p.H < min_h || p.H > 12 || p.npass != 1 || p.compact || p.stream) return false;
     p.l2 = 1;
     p.p2t = kL2TileElems / 32;  // tile geometry of the host's tiles: W = 8192 >> H low indices
