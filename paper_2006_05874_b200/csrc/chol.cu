@@ -16,8 +16,6 @@
 
 #include <cstdlib>
 
-#include <cooperative_groups.h>
-namespace cg = cooperative_groups;
 
 namespace ihs_b200 {
 
@@ -116,187 +114,6 @@ __global__ void __launch_bounds__(256) potrf_diag_kernel(double* __restrict__ H,
     }
 }
 
-// ---- diagonal block: LLT and its inverse in one CTA (4 warps)
-// 64 = 32 + 32 blocking: warp 0 factors a 32x32 block in registers (lane i
-// holds row i; column j's pivot and entries are broadcast by shuffles), the
-// four warps form L21 = A21 L11^{-T}, A22 -= L21 L21^T and X21 = -X22 L21 X11
-// as small shared-memory products, so the only sequential parts are the two
-// 32-column warp factorizations and inversions (no CTA barrier per column).
-constexpr int PB = 65;  // padded row stride of the 64x64 shared blocks
-
-// Warp-level LLT of the 32x32 block a[r0.., r0..] in place. Lane i keeps its
-// row in registers; the loop over columns is not unrolled (straight-line code
-// of the whole factorization would be instruction-fetch bound), so the row is
-// shifted left after every column: at step j, r[q] holds a[i][j+q] of the
-// partially reduced block and every register index is static. Column j's
-// entries are broadcast by shuffles; no shared-memory round trip per column.
-__device__ __noinline__ void potrf32_warp(double (*a)[PB], int r0, int* info, int64_t kglob, int nvalid) {
-    const int lane = threadIdx.x & 31;
-    double r[32];
-#pragma unroll
-    for (int q = 0; q < 32; ++q) r[q] = q <= lane ? a[r0 + lane][r0 + q] : 0.0;
-#pragma unroll 1
-    for (int j = 0; j < 32; ++j) {
-        double dj = __shfl_sync(0xffffffffu, r[0], j);
-        if (!(dj > 0.0) || !isfinite(dj)) {
-            if (lane == 0 && r0 + j < nvalid) atomicCAS(info, 0, (int)(kglob + r0 + j + 1));
-            dj = 1.0;  // keep going with a harmless pivot; the result is flagged
-        }
-        const double ljj = sqrt(dj);
-        const double l = lane == j ? ljj : (lane > j ? r[0] / ljj : 0.0);
-        if (lane >= j) a[r0 + lane][r0 + j] = l;
-#pragma unroll
-        for (int q = 1; q < 32; ++q) {
-            const double c = __shfl_sync(0xffffffffu, l, (j + q) & 31);
-            if (j + q < 32 && lane >= j + q) r[q] = fma(-l, c, r[q]);
-        }
-#pragma unroll
-        for (int q = 0; q < 31; ++q) r[q] = r[q + 1];
-        r[31] = 0.0;
-    }
-}
-
-// x[r0.., r0..] = inverse of the lower-triangular 32x32 block a[r0.., r0..];
-// lane = column c, rows i in order: x[i][c] = (delta_ic - sum_{q<i} a[i][q] x[q][c]) / a[i][i]
-// (a[i][q]: same-address broadcasts; x[q][c]: consecutive lanes, conflict-free)
-__device__ __noinline__ void trtri32_warp(const double (*__restrict__ a)[PB], double (*__restrict__ x)[PB], int r0) {
-    const int lane = threadIdx.x & 31;
-#pragma unroll 1
-    for (int i = 0; i < 32; ++i) {
-        double s0 = (i == lane) ? 1.0 : 0.0, s1 = 0.0;
-        const double* ai = &a[r0 + i][r0];
-#pragma unroll
-        for (int q = 0; q < 32; q += 2) {
-            if (q < i) s0 = fma(-ai[q], x[r0 + q][r0 + lane], s0);
-            if (q + 1 < i) s1 = fma(-ai[q + 1], x[r0 + q + 1][r0 + lane], s1);
-        }
-        x[r0 + i][r0 + lane] = i < lane ? 0.0 : (s0 + s1) / ai[i];
-        __syncwarp();
-    }
-}
-
-__global__ void __launch_bounds__(128) potrf_inv_diag_kernel(double* __restrict__ H, int64_t n, int64_t k, int nb,
-                                                             double* __restrict__ Xd, int* __restrict__ info) {
-    pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible after this
-    extern __shared__ double pi_smem[];
-    double(*a)[PB] = reinterpret_cast<double(*)[PB]>(pi_smem);
-    double(*x)[PB] = reinterpret_cast<double(*)[PB]>(pi_smem + 64 * PB);
-    double(*t)[PB] = reinterpret_cast<double(*)[PB]>(pi_smem + 128 * PB);  // 32 x 32 scratch
-    const int tid = threadIdx.x, warp = tid >> 5;
-    for (int e = tid; e < 64 * 64; e += 128) {
-        const int i = e & 63, j = e >> 6;
-        double v = 0.0;
-        if (i < nb && j < nb) v = i >= j ? H[(k + i) + (k + j) * n] : 0.0;
-        else if (i == j) v = 1.0;  // identity padding of a ragged last block
-        a[i][j] = v;
-        x[i][j] = 0.0;
-    }
-    __syncthreads();
-    if (warp == 0) {
-        potrf32_warp(a, 0, info, k, nb);
-        __syncwarp();
-        trtri32_warp(a, x, 0);
-    }
-    __syncthreads();
-    // L21[i][j] = sum_{q <= j} A21[i][q] X11[j][q]   (i, j < 32) -> t
-    for (int e = tid; e < 32 * 32; e += 128) {
-        const int i = e & 31, j = e >> 5;
-        double s = 0.0;
-        for (int q = 0; q <= j; ++q) s = fma(a[32 + i][q], x[j][q], s);
-        t[i][j] = s;
-    }
-    __syncthreads();
-    for (int e = tid; e < 32 * 32; e += 128) {
-        const int i = e & 31, j = e >> 5;
-        a[32 + i][j] = t[i][j];
-    }
-    __syncthreads();
-    // A22 -= L21 L21^T (lower)
-    for (int e = tid; e < 32 * 32; e += 128) {
-        const int i = e & 31, j = e >> 5;
-        if (i >= j) {
-            double s = 0.0;
-            for (int q = 0; q < 32; ++q) s = fma(a[32 + i][q], a[32 + j][q], s);
-            a[32 + i][32 + j] -= s;
-        }
-    }
-    __syncthreads();
-    if (warp == 0) {
-        potrf32_warp(a, 32, info, k, nb);
-        __syncwarp();
-        trtri32_warp(a, x, 32);
-    }
-    __syncthreads();
-    // X21 = -X22 (L21 X11): T = L21 X11 (X11 lower: q >= j), then X21 = -X22 T (X22 lower: q <= i)
-    for (int e = tid; e < 32 * 32; e += 128) {
-        const int i = e & 31, j = e >> 5;
-        double s = 0.0;
-        for (int q = j; q < 32; ++q) s = fma(a[32 + i][q], x[q][j], s);
-        t[i][j] = s;
-    }
-    __syncthreads();
-    for (int e = tid; e < 32 * 32; e += 128) {
-        const int i = e & 31, j = e >> 5;
-        double s = 0.0;
-        for (int q = 0; q <= i; ++q) s = fma(x[32 + i][32 + q], t[q][j], s);
-        x[32 + i][j] = -s;
-    }
-    __syncthreads();
-    double* X = Xd + (k / 64) * 64 * 64;
-    for (int e = tid; e < 64 * 64; e += 128) {
-        const int i = e & 63, j = e >> 6;
-        if (i < nb && j < nb && i >= j) H[(k + i) + (k + j) * n] = a[i][j];
-        X[i + 64 * j] = x[i][j];  // column-major 64x64, zero above the diagonal
-    }
-}
-
-// L21 = A21 L11^{-T} with the block inverse X = L11^{-1} from potrf_inv_diag:
-// one warp per row, lane c produces columns c and c + 32 (no sequential chain).
-__global__ void __launch_bounds__(32 * TRSM_WARPS) trsm_inv_panel_kernel(double* __restrict__ H, int64_t n, int64_t k,
-                                                                         int nb, const double* __restrict__ Xd) {
-    pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible after this
-    __shared__ double xs[64][PB];
-    __shared__ double rowv[TRSM_WARPS][64];
-    const double* X = Xd + (k / 64) * 64 * 64;
-    for (int e = threadIdx.x; e < 64 * 64; e += blockDim.x) xs[e & 63][e >> 6] = X[e];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int64_t row = k + nb + (int64_t)blockIdx.x * TRSM_WARPS + warp;
-    if (row < n) {
-        rowv[warp][lane] = lane < nb ? H[row + (k + lane) * n] : 0.0;
-        rowv[warp][lane + 32] = lane + 32 < nb ? H[row + (k + lane + 32) * n] : 0.0;
-    }
-    __syncthreads();
-    if (row >= n) return;
-    double s0 = 0.0, s1 = 0.0;
-    for (int q = 0; q <= lane; ++q) s0 = fma(rowv[warp][q], xs[lane][q], s0);
-    for (int q = 0; q <= lane + 32; ++q) s1 = fma(rowv[warp][q], xs[lane + 32][q], s1);
-    if (lane < nb) H[row + (k + lane) * n] = s0;
-    if (lane + 32 < nb) H[row + (k + lane + 32) * n] = s1;
-}
-
-// W's diagonal 32-blocks <- the block inverses of the cooperative factorization
-__global__ void place_diag_inv32_kernel(const double* __restrict__ Xd, int64_t n, double* __restrict__ W) {
-    pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible after this
-    const int64_t k = (int64_t)blockIdx.x * 32;
-    const double* X = Xd + (int64_t)blockIdx.x * 32 * 32;
-    for (int e = threadIdx.x; e < 32 * 32; e += blockDim.x) {
-        const int i = e & 31, j = e >> 5;
-        if (k + i < n && k + j < n && i >= j) W[(k + i) + (k + j) * n] = X[e];
-    }
-}
-
-// W's diagonal 64-blocks <- the block inverses computed during the factorization
-__global__ void place_diag_inv_kernel(const double* __restrict__ Xd, int64_t n, double* __restrict__ W) {
-    pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible after this
-    const int64_t k = (int64_t)blockIdx.x * 64;
-    const double* X = Xd + (int64_t)blockIdx.x * 64 * 64;
-    for (int e = threadIdx.x; e < 64 * 64; e += blockDim.x) {
-        const int i = e & 63, j = e >> 6;
-        if (k + i < n && k + j < n && i >= j) W[(k + i) + (k + j) * n] = X[e];
-    }
-}
-
-
 // L21 = A21 * L11^{-T}: one warp per row, lane c holds columns c and c+32 of
 // the row; column c is finished by its owner lane and broadcast by shuffle.
 __global__ void __launch_bounds__(32 * TRSM_WARPS) trsm_panel_kernel(double* __restrict__ H, int64_t n, int64_t k,
@@ -352,37 +169,6 @@ __global__ void mirror_upper_kernel(double* __restrict__ H, int64_t n) {
         if (i < n && j < n && i < j) H[i + j * n] = tile[r][tx];
     }
 }
-
-// Inverse of each 64x64 lower-triangular diagonal block: W_bb = L_bb^{-1}.
-// One CTA per block, one thread per column of the inverse.
-__global__ void __launch_bounds__(64) tri_inv_diag_kernel(const double* __restrict__ L, int64_t n,
-                                                          double* __restrict__ W) {
-    pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible after this
-    extern __shared__ double tri_smem[];
-    double(*l)[NB + 1] = reinterpret_cast<double(*)[NB + 1]>(tri_smem);
-    double(*x)[NB + 1] = reinterpret_cast<double(*)[NB + 1]>(tri_smem + NB * (NB + 1));
-    const int64_t k = (int64_t)blockIdx.x * NB;
-    const int nb = (int)imin64(NB, n - k);
-    for (int e = threadIdx.x; e < NB * NB; e += blockDim.x) {
-        const int i = e % NB, j = e / NB;
-        l[i][j] = (i < nb && j < nb && i >= j) ? L[(k + i) + (k + j) * n] : 0.0;
-    }
-    __syncthreads();
-    const int c = threadIdx.x;  // column of the inverse
-    if (c < nb) {
-        for (int i = 0; i < nb; ++i) {
-            double s = (i == c) ? 1.0 : 0.0;
-            for (int q = c; q < i; ++q) s -= l[i][q] * x[q][c];
-            x[i][c] = (i < c) ? 0.0 : s / l[i][i];
-        }
-    }
-    __syncthreads();
-    for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) {
-        const int i = e % nb, j = e / nb;
-        if (i >= j) W[(k + i) + (k + j) * n] = x[i][j];
-    }
-}
-
 
 // Inverse of each 64x64 lower-triangular diagonal block, latency-shaped for
 // parallelism: eight 8x8 leaves
@@ -539,156 +325,6 @@ void trmv(const double* Wf, int64_t n, bool lower, const double* x, int nrhs, do
            (int)grid.y, (int)lower, y);
 }
 
-// ---------------------------------------------------------------- single-launch blocked LLT
-// The column-serial factorization of each diagonal block is latency-bound and,
-// launched per panel with its TRSM and trailing update, costs ~3 launches of
-// tens of microseconds per 64 columns. Here the whole right-looking LLT
-// (NB = 32) runs in one cooperative launch: per panel, CTA 0's first warp
-// factors the diagonal block in registers (row per lane, shuffles, no shared
-// round trip per column) and inverts it (column per lane), every warp of the
-// grid then forms one row of L21 = A21 X^T from that inverse, and the CTAs
-// share the 32x32 tiles of the trailing update A22 -= L21 L21^T; grid-wide
-// barriers separate the three steps. The 32x32 diagonal-block inverses are
-// kept (Xd) for the triangular inverse that follows.
-constexpr int CB = 32;           // panel width
-constexpr int CTHREADS = 256;    // 8 warps per CTA
-
-// lane i holds row i of the lower block (r[q] = a[i][q], q <= i); on return r holds row i of L.
-// Right-looking with a left shift per column so every register index is static.
-__device__ __forceinline__ void potrf32_regs(double (&r)[CB], int nvalid, int* info, int64_t kglob) {
-    const int lane = threadIdx.x & 31;
-    double out[CB];
-#pragma unroll
-    for (int q = 0; q < CB; ++q) out[q] = 0.0;
-#pragma unroll 1
-    for (int j = 0; j < CB; ++j) {
-        double dj = __shfl_sync(0xffffffffu, r[0], j);
-        if (!(dj > 0.0) || !isfinite(dj)) {
-            if (lane == 0 && j < nvalid) atomicCAS(info, 0, (int)(kglob + j + 1));
-            dj = 1.0;
-        }
-        const double ljj = sqrt(dj);
-        const double l = lane == j ? ljj : (lane > j ? r[0] / ljj : 0.0);
-#pragma unroll
-        for (int q = 1; q < CB; ++q) {
-            const double c = __shfl_sync(0xffffffffu, l, (j + q) & 31);
-            if (j + q < CB && lane >= j + q) r[q] = fma(-l, c, r[q]);
-        }
-        // out[j] = l, with j dynamic: rotate the output row instead (out[0] always receives)
-#pragma unroll
-        for (int q = 0; q < CB - 1; ++q) out[q] = out[q + 1];
-        out[CB - 1] = l;
-#pragma unroll
-        for (int q = 0; q < CB - 1; ++q) r[q] = r[q + 1];
-        r[CB - 1] = 0.0;
-    }
-#pragma unroll
-    for (int q = 0; q < CB; ++q) r[q] = out[q];
-}
-
-__global__ void __launch_bounds__(CTHREADS) chol_coop_kernel(double* __restrict__ H, int64_t k,
-                                                             double* __restrict__ Xd, int* __restrict__ info) {
-    pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible after this
-    cg::grid_group grid = cg::this_grid();
-    __shared__ double xs[CB][CB + 1];     // panel block inverse (or scratch)
-    __shared__ double ta[CB][CB + 1], tb[CB][CB + 1];
-    __shared__ double rowv[CTHREADS / 32][CB];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int nwarps_grid = gridDim.x * (CTHREADS / 32);
-    for (int64_t p = 0; p < k; p += CB) {
-        const int nb = (int)imin64(CB, k - p);
-        // ---- A: diagonal block factor + inverse (CTA 0, warp 0)
-        if (blockIdx.x == 0 && warp == 0) {
-            double r[CB];
-#pragma unroll
-            for (int q = 0; q < CB; ++q) {
-                double v = 0.0;
-                if (lane < nb && q < nb) v = q <= lane ? H[(p + lane) + (p + q) * k] : 0.0;
-                else if (lane == q) v = 1.0;  // identity padding of a ragged last panel
-                r[q] = v;
-            }
-            potrf32_regs(r, nb, info, p);
-#pragma unroll
-            for (int q = 0; q < CB; ++q) {
-                if (lane < nb && q < nb && q <= lane) H[(p + lane) + (p + q) * k] = r[q];
-                xs[lane][q] = q <= lane ? r[q] : 0.0;  // L block, row lane
-            }
-            __syncwarp();
-            // X = L^{-1}: lane = column c, rows in order
-            double xc[CB];
-#pragma unroll
-            for (int i = 0; i < CB; ++i) {
-                double s0 = (i == lane) ? 1.0 : 0.0, s1 = 0.0;
-#pragma unroll
-                for (int q = 0; q < i; q += 2) {
-                    s0 = fma(-xs[i][q], xc[q], s0);
-                    if (q + 1 < i) s1 = fma(-xs[i][q + 1], xc[q + 1], s1);
-                }
-                xc[i] = i < lane ? 0.0 : (s0 + s1) / xs[i][i];
-            }
-            double* X = Xd + (p / CB) * CB * CB;
-#pragma unroll
-            for (int i = 0; i < CB; ++i) X[i + CB * lane] = xc[i];  // column-major, X[i][lane]
-        }
-        grid.sync();
-        const int64_t rest = k - p - nb;
-        if (rest <= 0) break;
-        // ---- B: L21 = A21 X^T, one warp per row
-        {
-            const double* X = Xd + (p / CB) * CB * CB;
-            for (int e = tid; e < CB * CB; e += CTHREADS) xs[e % CB][e / CB] = __ldcg(X + e);  // xs[i][c] = X[i][c]
-            __syncthreads();
-            for (int64_t rr = (int64_t)blockIdx.x * (CTHREADS / 32) + warp; rr < rest; rr += nwarps_grid) {
-                const int64_t row = p + nb + rr;
-                rowv[warp][lane] = lane < nb ? __ldcg(H + row + (p + lane) * k) : 0.0;
-                __syncwarp();
-                // out[c] = sum_{q <= c} a[q] X[c][q]
-                double s = 0.0;
-                for (int q = 0; q <= lane; ++q) s = fma(rowv[warp][q], xs[lane][q], s);
-                if (lane < nb) H[row + (p + lane) * k] = s;
-                __syncwarp();
-            }
-        }
-        grid.sync();
-        // ---- C: trailing update of the lower tiles, A22 -= L21 L21^T
-        {
-            const int64_t nt = (rest + CB - 1) / CB;
-            const int64_t ntiles = nt * (nt + 1) / 2;
-            const int64_t base = p + nb;
-            for (int64_t tix = blockIdx.x; tix < ntiles; tix += gridDim.x) {
-                // tile (ti, tj), ti >= tj, enumerated row by row
-                int64_t ti = (int64_t)((sqrt(8.0 * (double)tix + 1.0) - 1.0) * 0.5);
-                while (ti * (ti + 1) / 2 > tix) --ti;
-                while ((ti + 1) * (ti + 2) / 2 <= tix) ++ti;
-                const int64_t tj = tix - ti * (ti + 1) / 2;
-                const int64_t i0 = base + ti * CB, j0 = base + tj * CB;
-                __syncthreads();
-                for (int e = tid; e < CB * CB; e += CTHREADS) {
-                    const int rr = e % CB, q = e / CB;
-                    ta[rr][q] = (i0 + rr < k && q < nb) ? __ldcg(H + (i0 + rr) + (p + q) * k) : 0.0;
-                    tb[rr][q] = (j0 + rr < k && q < nb) ? __ldcg(H + (j0 + rr) + (p + q) * k) : 0.0;
-                }
-                __syncthreads();
-                // thread -> (row i, 4 columns j = jq, jq+8, jq+16, jq+24)
-                const int i = tid % CB, jq = tid / CB;
-                double acc[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll 8
-                for (int q = 0; q < CB; ++q) {
-                    const double a = ta[i][q];
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) acc[u] = fma(a, tb[jq + 8 * u][q], acc[u]);
-                }
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int64_t gi = i0 + i, gj = j0 + jq + 8 * u;
-                    if (gi < k && gj < k && gi >= gj) H[gi + gj * k] -= acc[u];
-                }
-            }
-        }
-        grid.sync();
-    }
-}
-
 // W[n0:n0+size, n0:n0+size] <- L^{-1} of the same diagonal block (lower), with
 // the diagonal 64-blocks already inverted and the strict upper part zero.
 void tri_inv_rec(const double* L, double* W, int64_t n, int64_t n0, int64_t size, double* tmp, cudaStream_t st,
@@ -707,29 +343,12 @@ void tri_inv_rec(const double* L, double* W, int64_t n, int64_t n0, int64_t size
 }
 }  // namespace
 
-void cholesky_invert(const double* d_L, int64_t n, double* d_W, double* d_tmp, const double* d_Xd, cudaStream_t st,
-                     int xd_block) {
+void cholesky_invert(const double* d_L, int64_t n, double* d_W, double* d_tmp, cudaStream_t st) {
     CUDA_CHECK(cudaMemsetAsync(d_W, 0, (size_t)n * n * sizeof(double), st));
-    int base = NB;
-    if (d_Xd && xd_block == 32) {
-        LAUNCH_PDL(place_diag_inv32_kernel, (unsigned)ceil_div(n, 32), 256, 0, st, d_Xd, n, d_W);
-        base = 32;
-    } else if (d_Xd) {
-        LAUNCH_PDL(place_diag_inv_kernel, (unsigned)ceil_div(n, NB), 256, 0, st, d_Xd, n, d_W);
-    } else {
-        const size_t smem = (size_t)2 * NB * (NB + 1) * sizeof(double);
-        IHS_SMEM_ATTR(tri_inv_diag_kernel, (int)smem);
-        static const bool old_inv = [] {
-            const char* e = std::getenv("IHS_TRI_INV_OLD");
-            return e && e[0] == '1';
-        }();
-        if (old_inv) LAUNCH_PDL(tri_inv_diag_kernel, (unsigned)ceil_div(n, NB), 64, smem, st, d_L, n, d_W);
-        else {
-            const size_t ti_smem = (size_t)3 * TI * TIP * sizeof(double);
-            IHS_SMEM_ATTR(tri_inv64_kernel, (int)ti_smem);
-            LAUNCH_PDL(tri_inv64_kernel, (unsigned)ceil_div(n, NB), 256, ti_smem, st, d_L, n, d_W);
-        }
-    }
+    const int base = NB;
+    const size_t ti_smem = (size_t)3 * TI * TIP * sizeof(double);
+    IHS_SMEM_ATTR(tri_inv64_kernel, (int)ti_smem);
+    LAUNCH_PDL(tri_inv64_kernel, (unsigned)ceil_div(n, NB), 256, ti_smem, st, d_L, n, d_W);
     // n = base * 2^L: the recursion's nodes of one size are independent and equally shaped, so each level is
     // two strided-batched products (2 L launches instead of 2 (2^L - 1)); otherwise the recursion itself
     static const bool rec_only = [] {  // IHS_TRI_INV_REC=1: the depth-first recursion (A/B)
@@ -768,50 +387,14 @@ void cholesky_solve_inv(const double* d_W, int64_t n, const double* d_R, double*
     trmv(d_W, n, false, y, nrhs, d_Z, part, st);   // z = L^{-T} y
 }
 
-size_t cholesky_diag_inv_doubles(int64_t n) {
-    return std::max((size_t)ceil_div(n, NB) * NB * NB, (size_t)ceil_div(n, CB) * CB * CB);
-}
-
-// One cooperative launch for the whole factorization (see chol_coop_kernel); false when the device
-// cannot co-schedule the grid (the caller then uses the per-panel kernels).
-bool cholesky_factor_coop(double* d_H, int64_t n, double* d_Xd, int* d_info, int num_sms, cudaStream_t st) {
-    static std::atomic<int> per_sm_cache{-1};
-    int per_sm = per_sm_cache.load();
-    if (per_sm < 0) {
-        int supported = 0, dev = 0;
-        CUDA_CHECK(cudaGetDevice(&dev));
-        CUDA_CHECK(cudaDeviceGetAttribute(&supported, cudaDevAttrCooperativeLaunch, dev));
-        per_sm = 0;
-        if (supported) CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, chol_coop_kernel, CTHREADS, 0));
-        per_sm_cache.store(per_sm);
-    }
-    if (per_sm < 1) return false;
+void cholesky_factor(double* d_H, int64_t n, int* d_info, cudaStream_t st) {
     CUDA_CHECK(cudaMemsetAsync(d_info, 0, sizeof(int), st));
-    const int64_t nt = std::max<int64_t>(1, ceil_div(n - CB, CB));
-    const int64_t want = std::max<int64_t>(1, std::min<int64_t>(nt * (nt + 1) / 2, (int64_t)num_sms));
-    const int grid = (int)std::min<int64_t>(want, (int64_t)num_sms * per_sm);
-    void* args[] = {&d_H, &n, &d_Xd, &d_info};
-    CUDA_CHECK(cudaLaunchCooperativeKernel((const void*)chol_coop_kernel, dim3(grid), dim3(CTHREADS), args, 0, st));
-    note_launch();
-    return true;
-}
-
-void cholesky_factor(double* d_H, int64_t n, double* d_Xd, int* d_info, int num_sms, cudaStream_t st) {
-    (void)num_sms;
-    CUDA_CHECK(cudaMemsetAsync(d_info, 0, sizeof(int), st));
-    const size_t pi_smem = (size_t)(64 + 64 + 32) * PB * sizeof(double);
-    IHS_SMEM_ATTR(potrf_inv_diag_kernel, (int)pi_smem);
     for (int64_t k = 0; k < n; k += NB) {
         const int nb = (int)std::min<int64_t>(NB, n - k);
-        if (d_Xd) LAUNCH_PDL(potrf_inv_diag_kernel, 1, 128, pi_smem, st, d_H, n, k, nb, d_Xd, d_info);
-        else LAUNCH_PDL(potrf_diag_kernel, 1, 256, 0, st, d_H, n, k, nb, d_info);
+        LAUNCH_PDL(potrf_diag_kernel, 1, 256, 0, st, d_H, n, k, nb, d_info);
         const int64_t rest = n - k - nb;
         if (rest > 0) {
-            if (d_Xd)
-                LAUNCH_PDL(trsm_inv_panel_kernel, (unsigned)ceil_div(rest, TRSM_WARPS), 32 * TRSM_WARPS, 0, st, d_H, n, k,
-                       nb, d_Xd);
-            else
-                LAUNCH_PDL(trsm_panel_kernel, (unsigned)ceil_div(rest, TRSM_WARPS), 32 * TRSM_WARPS, 0, st, d_H, n, k, nb);
+            LAUNCH_PDL(trsm_panel_kernel, (unsigned)ceil_div(rest, TRSM_WARPS), 32 * TRSM_WARPS, 0, st, d_H, n, k, nb);
             // A22 -= L21 L21^T (lower)
             double* L21 = d_H + (k + nb) + k * n;
             double* A22 = d_H + (k + nb) + (k + nb) * n;

@@ -127,7 +127,6 @@ struct SrhtPlan {
     int pass_lo[3], pass_hb[3];
     double scale1, scale2;   // 1/sqrt(n_pad), sqrt(n_pad/m) (host-computed, :47 and :95)
     int p2t;                 // threads per phase-2 tile (128; 256 for the 64 KiB-tile variant)
-    int stream;              // 1: streamed single-launch kernel (srht_plan_stream)
     int compact;             // 1: compact T (only the sampled low indices; srht_plan_compact)
     int l2;                  // 1: L2-resident single launch (srht_plan_l2): T is a ring of l2_ns column slots
     int l2_ns;               // ring depth (column slots)
@@ -135,7 +134,6 @@ struct SrhtPlan {
 SrhtPlan srht_plan(int64_t n, int64_t d, int64_t lda, int64_t m);
 // switch the plan to the streamed single-launch kernel when it applies (sets
 // p2t before the entries are built); false = two-kernel path
-bool srht_plan_stream(SrhtPlan& p, int num_sms);
 // switch a two-kernel plan with 10 high bits (n_pad = 2^20) to compact T when the sample has few distinct
 // low indices (U <= 640): phase 1 stores, per chunk, only the low indices some sampled row has
 // (T[j][h][u]) and the emitting pass runs one warp per (u, column). Set before the entries are built (they then carry U tiles followed by the 1024-entry
@@ -152,10 +150,8 @@ size_t srht_l2_ctl_bytes(const SrhtPlan& p);
 // tile. entries = (row, k) pairs grouped by tile; tiles = (rlo0, begin, end).
 void srht_build_entries(const SrhtPlan& p, const int64_t* rows, std::vector<int2>& entries,
                         std::vector<int4>& tiles);
-// d_ctl != nullptr selects the fused single-launch path (when the high bits
-// fit one pass): T is then a ring of srht_fused_scratch_bytes() and d_ctl a
-// control block of *ctl_bytes.
-size_t srht_fused_scratch_bytes(const SrhtPlan& p, size_t* ctl_bytes, int num_sms = 148);
+// p.l2 (srht_plan_l2) selects the L2-resident single launch: T is then a ring of srht_l2_scratch_bytes() and
+// d_ctl its control block of srht_l2_ctl_bytes().
 // d_mask (8 words, from srht_build_mask): phase 1 stores only the low-index
 // groups the single emitting pass reads.
 void srht_run_device(const SrhtPlan& p, const double* d_A, const uint32_t* d_signbits, const int2* d_entries,
@@ -199,17 +195,9 @@ int dgemm_pick_splitk(int64_t M, int64_t N, int64_t K, int num_sms, bool transA 
                       bool lower_only = false);
 
 // chol.cu — blocked Cholesky (lower, in place). d_info: int (0 ok, j+1 = failed pivot).
-// d_Xd (cholesky_diag_inv_doubles(n), or nullptr for the column-serial kernels)
-// receives the inverses of the 64x64 diagonal blocks of L.
-size_t cholesky_diag_inv_doubles(int64_t n);
-void cholesky_factor(double* d_H, int64_t n, double* d_Xd, int* d_info, int num_sms, cudaStream_t st);
-// single cooperative launch (32-column panels); d_Xd receives the 32x32 diagonal-block inverses
-bool cholesky_factor_coop(double* d_H, int64_t n, double* d_Xd, int* d_info, int num_sms, cudaStream_t st);
-// W = L^{-1} (lower) with W^T mirrored into the strict upper triangle;
-// d_tmp holds ceil(n/2)^2 doubles; d_Xd = the factorization's block inverses (or nullptr).
-// xd_block: 64 (potrf_inv_diag) or 32 (cholesky_factor_coop) when d_Xd is given
-void cholesky_invert(const double* d_L, int64_t n, double* d_W, double* d_tmp, const double* d_Xd, cudaStream_t st,
-                     int xd_block = 64);
+void cholesky_factor(double* d_H, int64_t n, int* d_info, cudaStream_t st);
+// W = L^{-1} (lower) with W^T mirrored into the strict upper triangle; d_tmp holds (ceil(n/2) + 64)^2 doubles
+void cholesky_invert(const double* d_L, int64_t n, double* d_W, double* d_tmp, cudaStream_t st);
 size_t cholesky_solve_work_doubles(int64_t n);
 // Z = L^{-T} L^{-1} R for nrhs columns (ld = n), two parallel triangular mat-vecs
 void cholesky_solve_inv(const double* d_W, int64_t n, const double* d_R, double* d_Z, int nrhs, double* d_work,

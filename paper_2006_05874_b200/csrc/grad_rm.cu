@@ -43,6 +43,14 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
                  "l"(src), "r"(bytes), "r"(smem_u32(bar))
                  : "memory");
 }
+// the same with an L2 cache policy: panels [0, keep) of A are loaded evict-last so they stay in L2 from one pass to
+// the next (A a few times larger than L2: C2), the rest evict-first so they do not displace them
+__device__ __forceinline__ void bulk_load_pol(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], "
+                 "%4;" ::"r"(smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+                 : "memory");
+}
 
 // RR rows per panel, MAXC = ceil(d / 512) columns per thread, NS stages.
 template <int NRHS, int RR, int MAXC, int NS>
@@ -207,7 +215,7 @@ constexpr int RTHREADS = 32 * RW;
 template <int NRHS, int KP, int RR, int NS, int CG>
 __global__ void __launch_bounds__(RTHREADS, 1)
 grad_rr_kernel(const double* __restrict__ Arm, int64_t d, int64_t npanels, const double* __restrict__ b,
-               const double* __restrict__ X, double* __restrict__ work, CandSpec cs) {
+               const double* __restrict__ X, double* __restrict__ work, CandSpec cs, int64_t keep) {
     constexpr int RG = RW / CG;  // row groups (rows in flight)
     extern __shared__ __align__(128) double sm[];
     const int64_t stage = (int64_t)RR * d;
@@ -227,13 +235,19 @@ grad_rr_kernel(const double* __restrict__ Arm, int64_t d, int64_t npanels, const
     }
     __syncthreads();
     const uint32_t stage_bytes = (uint32_t)(stage * sizeof(double));
+    uint64_t pol_last = 0, pol_first = 0;
+    if (keep > 0) {
+        asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_last));
+        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_first));
+    }
     // prologue: the first NS panels (A is constant for the whole solve, so these loads may overlap the
     // tail of the previous kernel under programmatic dependent launch)
     if (t == 0) {
         int64_t p = blockIdx.x;
         for (int k = 0; k < NS && p < npanels; ++k, p += gridDim.x) {
             mbar_expect_tx(&full[k], stage_bytes);
-            bulk_load(panel + k * stage, Arm + p * stage, stage_bytes, &full[k]);
+            if (keep > 0) bulk_load_pol(panel + k * stage, Arm + p * stage, stage_bytes, &full[k], p < keep ? pol_last : pol_first);
+            else bulk_load(panel + k * stage, Arm + p * stage, stage_bytes, &full[k]);
         }
     }
     pdl_wait();  // x / the heavy-ball state and the work buffer belong to the previous kernels
@@ -368,7 +382,11 @@ grad_rr_kernel(const double* __restrict__ Arm, int64_t d, int64_t npanels, const
                 if (pn < npanels) {
                     mbar_wait(&empty[s], ph);
                     mbar_expect_tx(&full[s], stage_bytes);
-                    bulk_load(panel + s * stage, Arm + pn * stage, stage_bytes, &full[s]);
+                    if (keep > 0)
+                        bulk_load_pol(panel + s * stage, Arm + pn * stage, stage_bytes, &full[s],
+                                      pn < keep ? pol_last : pol_first);
+                    else
+                        bulk_load(panel + s * stage, Arm + pn * stage, stage_bytes, &full[s]);
                 }
             }
             if (++s == NS) {
@@ -405,8 +423,18 @@ void launch_rr(const GradPlan& p, const double* Arm, const double* b, const doub
                const CandSpec& cs) {
     const size_t smem = grad_rr_smem(p.d, RR, NS);
     IHS_SMEM_ATTR((grad_rr_kernel<NRHS, KP, RR, NS, CG>), 227 * 1024);
+    // A up to ~4x L2: keep its first ~80 MiB of panels L2-resident across passes (IHS_GRAD_L2_KEEP_MB, 0 = off);
+    // larger A gains nothing from it and its evict-last lines would crowd the SRHT's L2 ring
+    static const int64_t keep_mb = [] {
+        const char* e = std::getenv("IHS_GRAD_L2_KEEP_MB");
+        return e ? (int64_t)std::atoll(e) : (int64_t)80;
+    }();
+    const int64_t a_bytes = p.lda * p.d * (int64_t)sizeof(double);
+    const int64_t stage_b = (int64_t)RR * p.d * (int64_t)sizeof(double);
+    const int64_t keep = (keep_mb > 0 && a_bytes <= (512ll << 20)) ? std::min<int64_t>(p.lda / RR, (keep_mb << 20) / stage_b)
+                                                                   : 0;
     LAUNCH_PDL((grad_rr_kernel<NRHS, KP, RR, NS, CG>), dim3(p.grid), dim3(RTHREADS), smem, st, Arm, p.d,
-               p.lda / RR, b, X, work, cs);
+               p.lda / RR, b, X, work, cs, keep);
 }
 
 template <int NRHS, int RR, int NS>

@@ -130,10 +130,6 @@ grad_partial_kernel(const double* __restrict__ A, int64_t n, int64_t d, int64_t 
 constexpr int T2 = 512;
 constexpr int W2 = T2 / 32;
 
-__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
-    const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(src));
-}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }

@@ -48,29 +48,6 @@ __global__ void __launch_bounds__(mt::THREADS) mt_raw_kernel(uint64_t seed, int6
     }
 }
 
-// Substream raw generator: CTA q starts from the 312-word window in
-// starts[q] (state after q*stride draws), produces draws
-// [q*stride, min((q+1)*stride, count)).
-__global__ void __launch_bounds__(mt::THREADS) mt_substream_kernel(const uint64_t* __restrict__ starts, int64_t stride,
-                                                                   int64_t count, uint64_t* __restrict__ out) {
-    pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible after this
-    __shared__ uint64_t buf[2 * NN];
-    const int64_t q = blockIdx.x;
-    for (int i = threadIdx.x; i < NN; i += blockDim.x) buf[i] = starts[q * NN + i];
-    __syncthreads();
-    mt::Twister tw{buf, 0};
-    const int k = threadIdx.x;
-    const int64_t beg = q * stride;
-    const int64_t end = min(count, beg + stride);
-    for (int64_t base = beg; base < end; base += NN) {
-        uint64_t lo, hi;
-        tw.next(lo, hi);
-        if (tw.worker()) {
-            if (base + k < end) out[base + k] = temper(lo);
-            if (base + mt::MM + k < end) out[base + mt::MM + k] = temper(hi);
-        }
-    }
-}
 
 // Sign bits of draws [beg, end) into a shared bit buffer (bit g - beg).
 __device__ __forceinline__ void or_bits32(uint32_t* accw, int64_t o, uint32_t v) {

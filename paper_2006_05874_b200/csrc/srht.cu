@@ -39,7 +39,6 @@ namespace ihs_b200 {
 namespace {
 constexpr int kSmallL = 10;  // n_pad <= 2^10: single on-chip kernel
 constexpr int kChunkL = 10;  // phase-1 chunk: 1024 rows per warp
-constexpr int kP1Warps = 8;
 
 constexpr int kP2Threads = 256;
 
@@ -1226,180 +1225,6 @@ srht_l2_kernel(const __grid_constant__ ChunkMaps maps, const __grid_constant__ C
     }
 }
 
-// ------------------------------------------------------------ streamed (one pass of high bits)
-// Persistent single-launch SRHT, warp-specialised: phase 1 and the emitting
-// pass run concurrently so T lives in an L2-resident ring of nslot slots x G
-// columns instead of making an HBM round trip. One CTA per SM:
-//   * warps 0-7 (phase 1) stream the 1024-row chunks in global order (warp w
-//     of CTA b takes chunks (k*grid + b)*8 + w), each keeping its next chunk
-//     in flight by cp.async; a warp adds its finished chunks to done1[group]
-//     when it moves to the next group, and before its first write into group
-//     g's slot waits until done2[g - nslot] shows the slot consumed;
-//   * warps 8-15 (emitting group, named barrier 1) take their share of each
-//     group's active tiles once done1[group] is complete and add them to
-//     done2[group].
-// Phase-1 warps wait only for emits of earlier groups, whose chunks precede
-// theirs in every warp's order, and emitting warps never block phase-1 warps
-// of their own CTA, so the pipeline cannot deadlock for any G or nslot.
-__device__ __forceinline__ void spin_until(const int* ctr, int target) {
-    while (ld_acquire(ctr) < target) __nanosleep(100);
-}
-
-
-// Streamed kernel shape: kP1Warps phase-1 warps (TMA-fed two-slot rings) and
-// kEmitGroups emitting groups of kEmitThreads threads, each with its own
-// exchange buffer, so two emitting tiles are in flight per SM.
-constexpr int kEmitGroups = 2;
-constexpr int kEmitThreads = 128;
-constexpr int kEmitXs = 32 * kEmitThreads + kEmitThreads;  // pad32(tile) for hb >= 5
-constexpr int kStreamThreads = 32 * kP1Warps + kEmitGroups * kEmitThreads;
-constexpr int kFlushChunks = 4;  // phase-1 warps publish done1 counts at most every 4 chunks
-constexpr size_t kStreamSmem = ((size_t)kP1Warps * 2 * kChunkDoubles + (size_t)kEmitGroups * kEmitXs) * sizeof(double) +
-                               kP1Warps * 2 * 8 + 1024;
-
-template <int HB>
-__global__ void __launch_bounds__(kStreamThreads, 1)
-srht_stream_kernel(const __grid_constant__ ChunkMaps maps, const double* __restrict__ A, int64_t n, int64_t lda,
-                   int64_t nfull, const uint32_t* __restrict__ signbits, double* __restrict__ T, int64_t n_pad,
-                   int64_t d, int lcpc, int G, int nslot, int ng, const int4* __restrict__ tiles, int n_tiles,
-                   const int2* __restrict__ entries, int lo, double s1, double s2, double* __restrict__ SA, int64_t m,
-                   int* __restrict__ ctl, const uint32_t* __restrict__ mask, int logw, int dbg,
-                   unsigned long long* __restrict__ prof) {
-    pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible after this
-    extern __shared__ unsigned char stream_raw[];
-    const long long t_start = clock64();
-    double* base = align1024(stream_raw);
-    double* xs_all = base + kP1Warps * 2 * kChunkDoubles;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    int* done1 = ctl;
-    int* done2 = ctl + ng;
-    const int64_t cpc = int64_t{1} << lcpc, cmask = cpc - 1;
-    auto group_cols = [&](int g) { return (int)imin64(G, d - (int64_t)g * G); };
-    if (warp >= kP1Warps) {
-        if (dbg & 1) return;
-        // ---------------- emitting groups: worker k of CTA b is worker b*kEmitGroups + k; item i of
-        // group g goes to worker (first(g) + i) mod workers, first(g) = items handed out before g
-        const int k = (threadIdx.x - 32 * kP1Warps) / kEmitThreads;
-        const int t = (threadIdx.x - 32 * kP1Warps) % kEmitThreads;
-        const GroupBar bar{1 + k, kEmitThreads};
-        double* xs = xs_all + k * kEmitXs;
-        const int64_t workers = (int64_t)gridDim.x * kEmitGroups;
-        const int64_t me = (int64_t)blockIdx.x * kEmitGroups + k;
-        int64_t first = 0;
-        long long w_wait = 0, w_busy = 0;
-        for (int g = 0; g < ng; ++g) {
-            const int gc = group_cols(g);
-            const int items = gc * n_tiles;
-            const int i0 = (int)((me - first % workers + workers) % workers);
-            first += items;
-            if (i0 >= items) continue;
-            const long long tw0 = clock64();
-            if (t == 0) spin_until(done1 + g, (int)(gc * cpc));
-            bar();
-            const long long tw1 = clock64();
-            w_wait += tw1 - tw0;
-            int mine = 0;
-            for (int i = i0; i < items; i += (int)workers) {
-                const int jj = i / n_tiles;
-                const int4 tile = tiles[i % n_tiles];
-                p2_tile<HB, true, GroupBar, kEmitThreads>(xs, T + ((int64_t)(g % nslot) * G + jj) * n_pad + tile.x,
-                                                          lo, true, tile, entries, (int64_t)g * G + jj, s1, s2, SA, m,
-                                                          t, bar);
-                bar();  // the exchange buffer is rewritten by the next tile
-                ++mine;
-            }
-            if (t == 0) atomicAdd(done2 + g, mine);
-            w_busy += clock64() - tw1;
-        }
-        if (prof && t == 0) {
-            atomicAdd(prof + 4, (unsigned long long)w_wait);
-            atomicAdd(prof + 5, (unsigned long long)w_busy);
-            atomicAdd(prof + 6, (unsigned long long)(clock64() - t_start));
-            atomicAdd(prof + 8, 1ull);
-        }
-        return;
-    }
-    // ---------------- phase-1 warps (TMA-fed two-slot rings)
-    double* ring = base + warp * (2 * kChunkDoubles);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(xs_all + kEmitGroups * kEmitXs) + 2 * warp;
-    if (lane == 0) {
-        tma::mbar_init(&bars[0], 1);
-        tma::mbar_init(&bars[1], 1);
-        tma::fence_mbar_init();
-    }
-    __syncwarp();
-    const int64_t total = d * cpc;
-    const int64_t SC = (int64_t)gridDim.x * kP1Warps;  // chunks per round of all phase-1 warps
-    const uint32_t store_bits = p1_store_bits(mask, logw);
-    auto issue = [&](int64_t chunk, int slot) {
-        if (lane == 0 && chunk < total && (chunk & cmask) < nfull)
-            p1_tma_issue(ring + slot * kChunkDoubles, &maps, (int)(chunk & cmask), (int)(chunk >> lcpc), &bars[slot],
-                         policy_evict_first());
-    };
-    // finished-chunk counts not yet published: one release fence covers them all
-    int pend_g[kFlushChunks], pend_c[kFlushChunks], npend = 0, since = 0;
-    long long c_spin = 0, c_mbar = 0, c_flush = 0;
-    auto flush = [&]() {
-        if (!npend) return;
-        const long long f0 = clock64();
-        if (!(dbg & 2)) __threadfence();
-        c_flush += clock64() - f0;
-        __syncwarp();
-        if (lane == 0)
-            for (int i = 0; i < npend; ++i) atomicAdd(done1 + pend_g[i], pend_c[i]);
-        npend = 0;
-        since = 0;
-    };
-    uint32_t parity = 0u;
-    int slot = 0, cur_g = -1;
-    int64_t chunk = (int64_t)blockIdx.x * kP1Warps + warp;
-    issue(chunk, 0);
-    for (; chunk < total; chunk += SC) {
-        issue(chunk + SC, slot ^ 1);
-        const int j = (int)(chunk >> lcpc);
-        const int g = j / G;
-        if (g != cur_g) {
-            cur_g = g;
-            if (g >= nslot && !(dbg & 1)) {
-                // about to wait on the emits of group g - nslot: publish first
-                flush();
-                const long long s0 = clock64();
-                if (lane == 0) spin_until(done2 + g - nslot, group_cols(g - nslot) * n_tiles);
-                __syncwarp();
-                c_spin += clock64() - s0;
-            }
-        }
-        const int64_t q = chunk & cmask, r0 = q << kChunkL;
-        double* buf = ring + slot * kChunkDoubles;
-        if (q < nfull) {
-            const long long m0 = clock64();
-            tma::mbar_wait(&bars[slot], (parity >> slot) & 1u);
-            c_mbar += clock64() - m0;
-            parity ^= 1u << slot;
-        } else {
-            p1_sync_load(buf, A + (int64_t)j * lda, n, r0);
-        }
-        p1_transform_store_swz(buf, signbits, n, r0, T + ((int64_t)(g % nslot) * G + (j - g * G)) * n_pad + r0,
-                               store_bits);
-        if (npend && pend_g[npend - 1] == g) {
-            ++pend_c[npend - 1];
-        } else {
-            pend_g[npend] = g;
-            pend_c[npend] = 1;
-            ++npend;
-        }
-        if (++since >= kFlushChunks || npend == kFlushChunks) flush();
-        slot ^= 1;
-    }
-    flush();
-    if (prof && lane == 0) {
-        atomicAdd(prof + 0, (unsigned long long)c_spin);
-        atomicAdd(prof + 1, (unsigned long long)c_mbar);
-        atomicAdd(prof + 2, (unsigned long long)c_flush);
-        atomicAdd(prof + 3, (unsigned long long)(clock64() - t_start));
-        atomicAdd(prof + 7, 1ull);
-    }
-}
 
 // Row-sharded SRHT combine (H_{n_pad} = H_P (x) H_{n_pad/P}, shard index =
 // top log2(P) row bits): U holds every shard's unscaled partial T_p[r_lo(k)]
@@ -1547,67 +1372,6 @@ bool srht_chunk_maps(const double* A, int64_t lda, int64_t nfull, int64_t d, Chu
     return true;
 }
 
-constexpr int64_t kStreamRingBytes = 64ll << 20;  // T ring budget: about half of the 126 MB L2
-
-// Group width G (about half a round of phase-1 chunks, so a column group is
-// finished by all SMs together) and ring depth nslot (2..8 slots within the
-// L2 budget), or false when the streamed kernel does not apply.
-bool srht_stream_geometry(const SrhtPlan& p, int grid, int* G_out, int* nslot_out) {
-    if (p.H == 0 || p.npass != 1) return false;
-    const int64_t cpc = p.n_pad >> kChunkL;
-    const int64_t SC = (int64_t)grid * kP1Warps;
-    const int64_t col_bytes = p.n_pad * (int64_t)sizeof(double);
-    const int64_t G = std::max<int64_t>(1, std::min<int64_t>(p.d, ceil_div(SC, 2 * cpc)));
-    const int64_t nslot = std::min<int64_t>(8, kStreamRingBytes / (G * col_bytes));
-    if (nslot < 2) return false;
-    *G_out = (int)G;
-    *nslot_out = (int)nslot;
-    return true;
-}
-
-// timing experiments only (results are wrong): bit 0 drops the emitting
-// warps and the slot waits, bit 1 the release fences
-int stream_dbg() {
-    static const int v = [] {
-        const char* e = std::getenv("IHS_SRHT_STREAM_DBG");
-        return e ? std::atoi(e) : 0;
-    }();
-    return v;
-}
-
-template <int HB>
-void launch_stream(const SrhtPlan& p, const ChunkMaps& maps, int64_t nfull, const double* A, const uint32_t* signbits,
-                   double* T, int G, int nslot, const int4* tiles, int n_tiles, const int2* entries, double* SA,
-                   int* ctl, int grid, const uint32_t* mask, int logw, cudaStream_t st) {
-    IHS_SMEM_ATTR((srht_stream_kernel<HB>), (int)kStreamSmem);
-    const int ng = (int)ceil_div(p.d, G);
-    CUDA_CHECK(cudaMemsetAsync(ctl, 0, 2 * sizeof(int) * (size_t)ng, st));
-    // IHS_SRHT_STREAM_PROF=1: per-role cycle accounting of the pipeline (debug, prints to stderr)
-    static const bool prof_on = std::getenv("IHS_SRHT_STREAM_PROF") != nullptr;
-    static unsigned long long* prof = nullptr;
-    if (prof_on && !prof) CUDA_CHECK(cudaMalloc(&prof, 16 * sizeof(unsigned long long)));
-    if (prof_on) CUDA_CHECK(cudaMemsetAsync(prof, 0, 16 * sizeof(unsigned long long), st));
-    LAUNCH_PDL(srht_stream_kernel<HB>, (unsigned)grid, kStreamThreads, kStreamSmem, st, maps, A, p.n, p.lda, nfull,
-           signbits, T, p.n_pad, p.d, p.logn - kChunkL, G, nslot, ng, tiles, n_tiles, entries, p.pass_lo[0], p.scale1,
-           p.scale2, SA, p.sa_ld, ctl, mask, logw, stream_dbg(), prof_on ? prof : nullptr);
-    if (prof_on) {
-        unsigned long long h[16];
-        CUDA_CHECK(cudaMemcpyAsync(h, prof, sizeof(h), cudaMemcpyDeviceToHost, st));
-        CUDA_CHECK(cudaStreamSynchronize(st));
-        const double p1n = (double)std::max(1ull, h[7]), p2n = (double)std::max(1ull, h[8]);
-        fprintf(stderr,
-                "[srht stream m=%lld G=%d nslot=%d tiles=%d] P1 warps %llu: total %.0f cyc, slot-wait %.1f%%, tma-wait "
-                "%.1f%%, fence %.1f%% | P2 groups %llu: total %.0f cyc, done1-wait %.1f%%, busy %.1f%%\n",
-                (long long)p.m, G, nslot, n_tiles, h[7], h[3] / p1n, 100.0 * h[0] / std::max(1ull, h[3]),
-                100.0 * h[1] / std::max(1ull, h[3]), 100.0 * h[2] / std::max(1ull, h[3]), h[8], h[6] / p2n,
-                100.0 * h[4] / std::max(1ull, h[6]), 100.0 * h[5] / std::max(1ull, h[6]));
-    }
-}
-using StreamFn = void (*)(const SrhtPlan&, const ChunkMaps&, int64_t, const double*, const uint32_t*, double*, int, int,
-                          const int4*, int, const int2*, double*, int*, int, const uint32_t*, int, cudaStream_t);
-const StreamFn kStream[11] = {nullptr,          launch_stream<1>, launch_stream<2>, launch_stream<3>,
-                              launch_stream<4>, launch_stream<5>, launch_stream<6>, launch_stream<7>,
-                              launch_stream<8>, launch_stream<9>, launch_stream<10>};
 using PassFn = void (*)(const SrhtPlan&, double*, int, const int4*, int, bool, const int2*, double*, cudaStream_t);
 const PassFn kPass[13] = {nullptr,
                           launch_pass<1, 256>,
@@ -1697,7 +1461,6 @@ SrhtPlan srht_plan(int64_t n, int64_t d, int64_t lda, int64_t m) {
             // host tiles match the emitting pass: two-round 128-thread tiles for 12 bits (W = 2 = the 256-thread
             // three-round geometry), 256-thread ones for 11 (W = 8 = the 512-thread geometry)
             p.p2t = r2_plan ? (p.H == 12 ? 256 : 512) : (p2t_env == 256 ? 256 : 512);
-            p.stream = 0;
             p.compact = 0;
             return p;
         }
@@ -1716,7 +1479,6 @@ SrhtPlan srht_plan(int64_t n, int64_t d, int64_t lda, int64_t m) {
     p.scale1 = 1.0 / std::sqrt(static_cast<double>(np));
     p.scale2 = std::sqrt(static_cast<double>(np) / static_cast<double>(m));
     p.p2t = p2_threads_default();
-    p.stream = 0;
     p.compact = 0;
     return p;
 }
@@ -1780,7 +1542,7 @@ bool srht_plan_l2(SrhtPlan& p) {
     // 9 high bits (a 2^19-row column: C4 over 8 GPUs, C5 over 2) measured 18.1 vs 20.4 ms for the two-kernel path
     // (n = 2^19, d = 2048, m = 4096, incl. the SA read-back)
     const int min_h = 9;
-    if (mode == 0 || p.H < min_h || p.H > 12 || p.npass != 1 || p.compact || p.stream) return false;
+    if (mode == 0 || p.H < min_h || p.H > 12 || p.npass != 1 || p.compact) return false;
     p.l2 = 1;
     p.p2t = kL2TileElems / 32;  // tile geometry of the host's tiles: W = 8192 >> H low indices
     const int64_t col_bytes = p.n_pad * (int64_t)sizeof(double);
@@ -1800,7 +1562,7 @@ bool srht_plan_compact(SrhtPlan& p, const int64_t* rows) {
         const char* e = std::getenv("IHS_SRHT_COMPACT_MAX");
         return e ? std::atoi(e) : 640;
     }();
-    if (disabled || p.H != 10 || p.npass != 1 || p.stream) return false;
+    if (disabled || p.H != 10 || p.npass != 1) return false;
     // measured (profiles/r01_srht_compact.txt): compact phase 1 + emitting pass beat the masked T up to
     // ~640 distinct low indices (m ~ 1000 at n_pad = 2^20); beyond that the tiled pass is faster
     std::vector<uint8_t> seen(1024, 0);
@@ -1882,26 +1644,6 @@ void srht_build_entries(const SrhtPlan& p, const int64_t* rows, std::vector<int2
         tiles.resize(b0 + 4);
         std::memcpy(tiles.data() + b0, bits, sizeof(bits));
     }
-}
-
-bool srht_plan_stream(SrhtPlan& p, int num_sms) {
-    static const bool enabled = [] {
-        const char* e = std::getenv("IHS_SRHT_FUSED");
-        return e && e[0] == '1';
-    }();
-    int G = 0, nslot = 0;
-    if (!enabled || (p.n >> kChunkL) == 0 || p.pass_hb[0] > 10 || !srht_stream_geometry(p, num_sms, &G, &nslot))
-        return false;
-    p.p2t = kEmitThreads;
-    p.stream = 1;
-    return true;
-}
-
-size_t srht_fused_scratch_bytes(const SrhtPlan& p, size_t* ctl_bytes, int num_sms) {
-    if (ctl_bytes) *ctl_bytes = 2 * sizeof(int) * (size_t)(p.d + 1) + 64;
-    int G = 0, nslot = 0;
-    if (!srht_stream_geometry(p, num_sms, &G, &nslot)) return srht_scratch_bytes(p);
-    return (size_t)nslot * G * p.n_pad * sizeof(double);
 }
 
 bool srht_build_mask(const SrhtPlan& p, const std::vector<int4>& tiles, uint32_t mask[8]) {
@@ -2050,18 +1792,8 @@ void srht_run_device(const SrhtPlan& p, const double* d_A, const uint32_t* d_sig
         kSmall[p.L](p, d_A, d_signbits, d_entries, d_SA, st);
         return;
     }
-    int G = 0, nslot = 0;
     ChunkMaps maps;
     const int64_t nfull = p.n >> kChunkL;
-    if (p.npass == 1 && p.stream && p.p2t == kEmitThreads && n_tiles > 0 && d_ctl != nullptr &&
-        srht_stream_geometry(p, num_sms, &G, &nslot) &&
-        nfull > 0 && srht_chunk_maps(d_A, p.lda, nfull, p.d, &maps)) {
-        // one launch, T kept in an L2-resident ring of column groups
-        const int logw = pass_logw(p);
-        kStream[p.pass_hb[0]](p, maps, nfull, d_A, d_signbits, d_T, G, nslot, d_tiles, n_tiles, d_entries, d_SA,
-                              reinterpret_cast<int*>(d_ctl), num_sms, d_mask, logw, st);
-        return;
-    }
     const int64_t chunks_per_col = p.n_pad >> kChunkL;
     const int64_t total = chunks_per_col * p.d;
     // compact T: n_tiles distinct low indices, their rank map after the tiles
