@@ -44,6 +44,31 @@ __global__ void __launch_bounds__(512) l2_write_strided(double2* __restrict__ ds
         }
 }
 
+// half the CTAs stream a large buffer from HBM (read once per pass, 16-byte loads), the other half store into an
+// L2-resident buffer: do A's fill and T's store share one L2 write budget (the SRHT's two streams)?
+__global__ void __launch_bounds__(512) mixed(const double2* __restrict__ big, size_t nbig16, double2* __restrict__ l2buf,
+                                             size_t nl2_16, int passes, double* out, unsigned long long* cyc) {
+    const int half = gridDim.x / 2;
+    const bool reader = blockIdx.x < half;
+    const int b = reader ? blockIdx.x : blockIdx.x - half;
+    const size_t stride = (size_t)half * blockDim.x;
+    const long long t0 = clock64();
+    if (reader) {
+        double acc = 0.0;
+        for (size_t i = (size_t)b * blockDim.x + threadIdx.x; i + 3 * stride < nbig16; i += 4 * stride) {
+            const double2 a = __ldcs(big + i), c = __ldcs(big + i + stride), e = __ldcs(big + i + 2 * stride),
+                          f = __ldcs(big + i + 3 * stride);
+            acc += (a.x + c.y) + (e.x + f.y);
+        }
+        if (acc == 1234.5) out[0] = acc;
+    } else {
+        for (int p = 0; p < passes; ++p)
+            for (size_t i = (size_t)b * blockDim.x + threadIdx.x; i < nl2_16; i += stride)
+                __stcg(l2buf + i, make_double2((double)p, (double)i));
+    }
+    if (threadIdx.x == 0) atomicMax(cyc + (reader ? 0 : 1), (unsigned long long)(clock64() - t0));
+}
+
 int main(int argc, char** argv) {
     const int reps = 5, passes = 20;
     int sms = 0;
@@ -82,6 +107,40 @@ int main(int argc, char** argv) {
                gb / (best[0] * 1e-3), gb / (best[1] * 1e-3), gb / (best[2] * 1e-3));
         cudaFree(buf);
         if (argc > 1) break;
+    }
+    {  // mixed: 8 GiB streamed from HBM by half the CTAs while the other half store into a 64 MiB L2 buffer
+        const size_t big_b = 8ull << 30, l2_b = 64ull << 20;
+        double2 *big = nullptr, *l2 = nullptr;
+        unsigned long long* cyc = nullptr;
+        if (cudaMalloc(&big, big_b) == cudaSuccess && cudaMalloc(&l2, l2_b) == cudaSuccess &&
+            cudaMalloc(&cyc, 16) == cudaSuccess) {
+            cudaMemset(big, 0, big_b);
+            cudaMemset(l2, 0, l2_b);
+            int clk_khz = 0;
+            cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, 0);
+            // passes chosen so the store half moves about as many bytes as the read half
+            const int mpasses = (int)(big_b / l2_b);
+            float best = 1e30f;
+            for (int r = 0; r < 3; ++r) {
+                cudaMemset(cyc, 0, 16);
+                cudaEventRecord(e0);
+                mixed<<<sms * 4, 512>>>(big, big_b / 16, l2, l2_b / 16, mpasses, out, cyc);
+                cudaEventRecord(e1);
+                cudaEventSynchronize(e1);
+                float ms = 0.f;
+                cudaEventElapsedTime(&ms, e0, e1);
+                best = ms < best ? ms : best;
+            }
+            unsigned long long hc[2] = {0, 0};
+            cudaMemcpy(hc, cyc, 16, cudaMemcpyDeviceToHost);
+            printf(", \"mixed\": {\"ms\": %.3f, \"hbm_read_GB\": %.2f, \"l2_write_GB\": %.2f, \"aggregate_GBps\": %.0f, "
+                   "\"reader_cycles\": %llu, \"writer_cycles\": %llu}",
+                   best, big_b / 1e9, (double)l2_b * mpasses / 1e9, (big_b + (double)l2_b * mpasses) / 1e9 / (best * 1e-3),
+                   hc[0], hc[1]);
+        }
+        cudaFree(big);
+        cudaFree(l2);
+        cudaFree(cyc);
     }
     const cudaError_t err = cudaGetLastError();
     printf(", \"err\": \"%s\"}\n", cudaGetErrorString(err));
