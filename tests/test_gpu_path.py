@@ -204,3 +204,23 @@ def test_upload_async_matches_sync(gpu, O):
                           gpu.pcg_solve(gpu.ProblemInstance(A, b, 0.1), gpu.SketchKind.SRHT, 1, 0.5, 1e-10, 50).x)
     with pytest.raises(gpu.InvalidInput):
         p.upload_async(np.ascontiguousarray(A), b)  # C-ordered: would need a copy that dies before the transfer
+
+
+def test_upload_async_chunked_matches_sync(gpu):
+    """A large A (>= 256 MB, IHS_UPLOAD_CHUNK_MB) re-uploaded asynchronously goes in column chunks whose row-major
+    copies are built as they land, and the next solve's first SRHT runs chunk by chunk behind the copies: the solve
+    and a gradient must equal those after a synchronous upload bit for bit."""
+    n, d = (1 << 19) + 5, 72  # 302 MB
+    A, b, _ = gpu.synth_generate(n, d, decay=0.97, noise_std=0.05, data_seed=11)
+    A2 = np.asfortranarray(A * 0.75)
+    b2 = np.ascontiguousarray(b * 1.25)
+    ref = gpu.ProblemInstance(A2, b2, 0.05)
+    p = gpu.ProblemInstance(A, b, 0.05)
+    cfg = gpu.SolverConfig(sketch_kind=gpu.SketchKind.SRHT, seed=3, m_initial=2 * d, eps=1e-21)
+    p.upload_async(A2, b2)
+    r1 = gpu.adaptive_solve(p, cfg)
+    r0 = gpu.adaptive_solve(ref, cfg)
+    assert np.array_equal(r1.x, r0.x) and r1.iterations == r0.iterations and r1.final_m == r0.final_m
+    x = RNG(9).standard_normal(d)
+    p.upload_async(A, b)
+    assert np.array_equal(gpu.gradient(p, x), gpu.gradient(gpu.ProblemInstance(A, b, 0.05), x))
