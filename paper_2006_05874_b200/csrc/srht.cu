@@ -1743,31 +1743,16 @@ template <int HB>
 void launch_l2(const SrhtPlan& p, const ChunkMaps& maps, int64_t nfull, const double* A, const uint32_t* signbits,
                double* T, const int4* tiles, int n_tiles, const int2* entries, double* SA, int* ctl, int num_sms,
                cudaStream_t st) {
-    static const int teams = [] {  // IHS_SRHT_L2_TEAMS: phase-1 teams (1: one 8-chunk item at a time, 2: two 4-chunk)
-        const char* e = std::getenv("IHS_SRHT_L2_TEAMS");
-        return e ? std::atoi(e) : 1;
-    }();
+    // (measured and not kept: two 4-chunk phase-1 teams, two chunk slots with one emitting group — DESIGN §7; the
+    // kernel's P1T / S1 / EG template parameters still describe those shapes)
     static const int ts_env = [] {  // IHS_SRHT_L2_TS=0: phase-1 items stored by the thread loop, not by TMA
         const char* e = std::getenv("IHS_SRHT_L2_TS");
         return e ? std::atoi(e) : 1;
     }();
     CUtensorMap probe{};
-    const bool ts = ts_env != 0 && teams == 1 && srht_l2_store_map(T, HB, p.l2_ns, kL2P1Warps, &probe);
-    static const int shape = [] {  // IHS_SRHT_L2_SHAPE: 0 one chunk slot per phase-1 warp + two emitting groups,
-        const char* e = std::getenv("IHS_SRHT_L2_SHAPE");  // 1 two slots + one emitting group
-        return e ? std::atoi(e) : 0;
-    }();
-    if (shape == 1 && teams == 1) {
-        if (ts) launch_l2_t<HB, 1, true, 2, 1>(p, maps, nfull, A, signbits, T, tiles, n_tiles, entries, SA, ctl, num_sms, st);
-        else launch_l2_t<HB, 1, false, 2, 1>(p, maps, nfull, A, signbits, T, tiles, n_tiles, entries, SA, ctl, num_sms, st);
-        return;
-    }
-    if (teams == 2) {
-        launch_l2_t<HB, 2, false>(p, maps, nfull, A, signbits, T, tiles, n_tiles, entries, SA, ctl, num_sms, st);
-    } else {
-        if (ts) launch_l2_t<HB, 1, true>(p, maps, nfull, A, signbits, T, tiles, n_tiles, entries, SA, ctl, num_sms, st);
-        else launch_l2_t<HB, 1, false>(p, maps, nfull, A, signbits, T, tiles, n_tiles, entries, SA, ctl, num_sms, st);
-    }
+    const bool ts = ts_env != 0 && srht_l2_store_map(T, HB, p.l2_ns, kL2P1Warps, &probe);
+    if (ts) launch_l2_t<HB, 1, true>(p, maps, nfull, A, signbits, T, tiles, n_tiles, entries, SA, ctl, num_sms, st);
+    else launch_l2_t<HB, 1, false>(p, maps, nfull, A, signbits, T, tiles, n_tiles, entries, SA, ctl, num_sms, st);
 }
 using L2Fn = void (*)(const SrhtPlan&, const ChunkMaps&, int64_t, const double*, const uint32_t*, double*, const int4*,
                       int, const int2*, double*, int*, int, cudaStream_t);

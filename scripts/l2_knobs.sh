@@ -1,10 +1,9 @@
 #!/bin/bash
 # A/B of the L2-resident SRHT launch's knobs at C4's row count (d = $D, default 512): each argument is one env
-# setting, e.g.  bash scripts/l2_knobs.sh "" "IHS_SRHT_L2_TS=0" "IHS_SRHT_L2_SHAPE=1" "IHS_SRHT_L2_NS=2"
+# setting, e.g.  bash scripts/l2_knobs.sh "" "IHS_SRHT_L2_TS=0" "IHS_SRHT_L2_NS=2"
 # CHECK=1 first verifies bit-exactness of each setting against the oracle (scripts/l2_check.py).
-# Knobs: IHS_SRHT_L2_TS (tensor-store items, default 1), IHS_SRHT_L2_TEAMS (1|2), IHS_SRHT_L2_SHAPE (0: 1 slot +
-# 2 emitting groups, 1: 2 slots + 1 group), IHS_SRHT_L2_NS (ring depth), IHS_SRHT_L2_PF (prefetch distance),
-# IHS_SRHT_L2_TPOL (T store policy), IHS_SRHT_L2_DBG (timing probes: see srht.cu launch_l2_t).
+# Knobs: IHS_SRHT_L2_TS (tensor-store items, default 1), IHS_SRHT_L2_NS (ring depth), IHS_SRHT_L2_PF (prefetch
+# distance), IHS_SRHT_L2_TPOL (T store policy), IHS_SRHT_L2_DBG (timing probes: see srht.cu launch_l2_t).
 for setting in "$@"; do
   echo "== ${setting:-default}"
   if [ "${CHECK:-0}" = 1 ]; then env $setting timeout -s KILL 400 python scripts/l2_check.py 2>&1 | tail -1; fi
