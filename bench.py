@@ -661,6 +661,11 @@ def main():
         print(s, flush=True)
         if args.out:
             pathlib.Path(args.out).write_text(s + "\n")
+    # the NCCL communicator is destroyed explicitly (all work synchronized above), before the process group and
+    # before interpreter shutdown could collect it in any order
+    if comm is not None:
+        torch.cuda.synchronize()
+        comm.close()
     if dist:
         dist.destroy_process_group()
     return 0

@@ -271,11 +271,18 @@ class NcclComm:
         _check(lib().ihs_gpu_nccl_comm_create(buf, world_size, rank, device, C.byref(h)))
         self.handle = h
 
-    def __del__(self):
+    def close(self):
+        """Destroy the communicator now (ncclCommDestroy); also done on garbage collection."""
         h = getattr(self, "handle", None)
         if h:
             lib().ihs_gpu_nccl_comm_destroy(h)
             self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001  (interpreter shutdown: the library wrapper may already be gone)
+            pass
 
 
 def comm_selftest(comm, device: int = 0, count: int = 4099) -> int:

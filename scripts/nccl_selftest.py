@@ -17,5 +17,6 @@ dist.broadcast_object_list(uid, src=0)
 comm = ihs.NcclComm(uid[0], world, rank, local)
 bad = ihs.comm_selftest(comm, local, 1 << 16)
 print(f"rank {rank}/{world}: mismatches {bad}", flush=True)
+comm.close()
 dist.destroy_process_group()
 sys.exit(1 if bad else 0)
