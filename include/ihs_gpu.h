@@ -228,6 +228,9 @@ ihs_status ihs_gpu_emu_comm_create(int32_t world_size, int32_t device, void** co
 /* MT19937-64 draws the calling thread's Gaussian sketches have generated so far (count and emission passes over
  * whole substreams): a row shard's share of the stream's generation work. */
 int64_t ihs_gpu_thread_generated_draws(void);
+/* Doublings (beyond the first sketch) that adaptive solves of the calling thread have sketched chunk by chunk behind
+ * a chunked asynchronous upload of A (the speculative builds of ihs_gpu_problem_upload_async + adaptive_solve). */
+int64_t ihs_gpu_thread_upload_doublings(void);
 /* The sharded SRHT decomposition run back to back on one device (P virtual
  * shards of a single-GPU problem): proves the decomposition bit-exact. */
 ihs_status ihs_gpu_sketch_sharded_emulated(ihs_gpu_problem* p, int32_t kind, int64_t m, uint64_t seed,

@@ -831,6 +831,11 @@ def thread_generated_draws() -> int:
     return int(lib().ihs_gpu_thread_generated_draws())
 
 
+def thread_upload_doublings() -> int:
+    """Doublings this thread's adaptive solves sketched behind a chunked asynchronous upload (diagnostic)."""
+    return int(lib().ihs_gpu_thread_upload_doublings())
+
+
 def kernel_launch_count() -> int:
     return int(lib().ihs_gpu_kernel_launch_count())
 

@@ -224,3 +224,33 @@ def test_upload_async_chunked_matches_sync(gpu):
     x = RNG(9).standard_normal(d)
     p.upload_async(A, b)
     assert np.array_equal(gpu.gradient(p, x), gpu.gradient(gpu.ProblemInstance(A, b, 0.05), x))
+
+
+@pytest.mark.parametrize("m_initial,eps", [(144, 1e-21), (8, 1e-21), (4096, 1e-12)])
+def test_doublings_sketched_behind_chunked_upload(gpu, m_initial, eps):
+    """An adaptive SRHT solve started while a chunked upload is in flight prepares the first sketch and the next
+    doublings (IHS_UPLOAD_SPEC_DEPTH, default 5) up front and runs them chunk by chunk behind the copies, their
+    factorizations on side streams; doublings beyond them are sketched in place, unused ones are only waited for.
+    The solve must equal the one on a resident A bit for bit: x, the m-schedule, iterations and cost counters
+    (few doublings, more doublings than the depth, and none needed)."""
+    n, d = (1 << 19) + 5, 72  # 302 MB: copied in chunks
+    A, b, _ = gpu.synth_generate(n, d, decay=0.97, noise_std=0.05, data_seed=11)
+    A2 = np.asfortranarray(A * 0.75)
+    b2 = np.ascontiguousarray(b * 1.25)
+    ref = gpu.ProblemInstance(A2, b2, 0.05)
+    p = gpu.ProblemInstance(A, b, 0.05)
+    cfg = gpu.SolverConfig(sketch_kind=gpu.SketchKind.SRHT, seed=3, m_initial=m_initial, eps=eps)
+    r0 = gpu.adaptive_solve(ref, cfg)
+    before = gpu.thread_upload_doublings()
+    for _ in range(2):  # the second round reuses the pooled systems and sketch contexts
+        p.upload_async(A2, b2)
+        r1 = gpu.adaptive_solve(p, cfg)
+        assert np.array_equal(r1.x, r0.x)
+        assert (r1.iterations, r1.rejections, r1.final_m) == (r0.iterations, r0.rejections, r0.final_m)
+        assert [(e.t, e.m, e.r, e.branch) for e in r1.log] == [(e.t, e.m, e.r, e.branch) for e in r0.log]
+        assert r1.counters == r0.counters
+    assert gpu.thread_upload_doublings() - before == 2 * 5
+    # and a solve of the now resident problem takes the plain path with the same result
+    r2 = gpu.adaptive_solve(p, cfg)
+    assert np.array_equal(r2.x, r0.x) and r2.counters == r0.counters
+    assert gpu.thread_upload_doublings() - before == 2 * 5
