@@ -360,7 +360,7 @@ class ProblemInstance:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h:
+        if h and lib is not None:  # (module globals are already cleared at interpreter shutdown)
             lib().ihs_gpu_problem_destroy(h)
             self._h = None
 
