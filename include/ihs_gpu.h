@@ -231,6 +231,9 @@ int64_t ihs_gpu_thread_generated_draws(void);
 /* Doublings (beyond the first sketch) that adaptive solves of the calling thread have sketched chunk by chunk behind
  * a chunked asynchronous upload of A (the speculative builds of ihs_gpu_problem_upload_async + adaptive_solve). */
 int64_t ihs_gpu_thread_upload_doublings(void);
+/* Rows of sketched Gram matrices SA^T SA that those solves enqueued block row by block row behind the upload
+ * (the factorization then only reduces the split-K partials). */
+int64_t ihs_gpu_thread_upload_gram_rows(void);
 /* The sharded SRHT decomposition run back to back on one device (P virtual
  * shards of a single-GPU problem): proves the decomposition bit-exact. */
 ihs_status ihs_gpu_sketch_sharded_emulated(ihs_gpu_problem* p, int32_t kind, int64_t m, uint64_t seed,

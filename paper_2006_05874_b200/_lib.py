@@ -80,6 +80,7 @@ def lib():
         "ihs_gpu_comm_selftest": (C.c_int, [vp, i32, i64, P(i64)]),
         "ihs_gpu_thread_generated_draws": (i64, []),
         "ihs_gpu_thread_upload_doublings": (i64, []),
+        "ihs_gpu_thread_upload_gram_rows": (i64, []),
         "ihs_gpu_sketch_sharded_emulated": (C.c_int, [vp, i32, i64, u64, i32, d]),
         "ihs_pcg_sketch_size": (C.c_int, [i64, i64, i32, C.c_double, P(i64), P(i32)]),
         "ihs_gpu_problem_set_nu": (C.c_int, [vp, C.c_double]),
@@ -107,7 +108,7 @@ EXPORTED_SYMBOLS = (
     "ihs_gpu_system_m", "ihs_gpu_system_d", "ihs_gpu_system_factor_flops", "ihs_gpu_system_flops_per_solve",
     "ihs_gpu_system_solve", "ihs_newton_decrement", "ihs_gpu_adaptive_solve", "ihs_gpu_solve_underdetermined", "ihs_gpu_prediction_error", "ihs_gpu_fixed_sketch_ihs",
     "ihs_synth_generate", "ihs_gpu_shard_rows", "ihs_gpu_nccl_unique_id", "ihs_gpu_nccl_comm_create",
-    "ihs_gpu_nccl_comm_destroy", "ihs_gpu_emu_comm_create", "ihs_gpu_comm_selftest", "ihs_gpu_thread_generated_draws", "ihs_gpu_thread_upload_doublings", "ihs_gpu_sketch_sharded_emulated", "ihs_pcg_sketch_size", "ihs_gpu_cg_solve",
+    "ihs_gpu_nccl_comm_destroy", "ihs_gpu_emu_comm_create", "ihs_gpu_comm_selftest", "ihs_gpu_thread_generated_draws", "ihs_gpu_thread_upload_doublings", "ihs_gpu_thread_upload_gram_rows", "ihs_gpu_sketch_sharded_emulated", "ihs_pcg_sketch_size", "ihs_gpu_cg_solve",
     "ihs_gpu_pcg_solve_with", "ihs_gpu_pcg_solve", "ihs_gpu_problem_set_nu", "ihs_gpu_direct_solve",
     "ihs_gpu_problem_upload_async", "ihs_gpu_fill_gaussian_window",
 )

@@ -171,12 +171,13 @@ template <bool TA, bool TB>
 __global__ void __launch_bounds__(GTHREADS, 1)
 dgemm_big_kernel(int64_t M, int64_t N, int64_t K, double alpha, const double* __restrict__ A, int64_t lda,
                  const double* __restrict__ B, int64_t ldb, double beta, double* __restrict__ C, int64_t ldc,
-                 int64_t k_per_split, double* __restrict__ work, int lower_only) {
+                 int64_t k_per_split, double* __restrict__ work, int lower_only, int bx0) {
     constexpr bool KA = !TA;  // A staged k-major ([k][m])
     constexpr bool KB = TB;   // B staged k-major ([k][n])
     constexpr int SA_D = KA ? GBK * GLA : GBM * GLB;
     constexpr int SB_D = KB ? GBK * GLA : GBN * GLB;
-    const int64_t m0 = (int64_t)blockIdx.x * GBM, n0 = (int64_t)blockIdx.y * GBN;
+    // bx0: first block row of this launch (a product launched in block-row pieces, dgemm_rows)
+    const int64_t m0 = ((int64_t)blockIdx.x + bx0) * GBM, n0 = (int64_t)blockIdx.y * GBN;
     if (lower_only && n0 > m0 + GBM - 1) return;
     pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible after this
     extern __shared__ double gsm[];
@@ -392,7 +393,7 @@ void dgemm(bool transA, bool transB, int64_t M, int64_t N, int64_t K, double alp
     do {                                                                                                        \
         IHS_SMEM_ATTR((dgemm_big_kernel<TA_, TB_>), (int)(big_smem<TA_, TB_>()));                               \
         LAUNCH_PDL((dgemm_big_kernel<TA_, TB_>), grid, GTHREADS, (big_smem<TA_, TB_>()), st, M, N, K, alpha, A, lda, B,\
-                   ldb, beta, C, ldc, kps, work, (int)lower_only);                                              \
+                   ldb, beta, C, ldc, kps, work, (int)lower_only, 0);                                           \
     } while (0)
     if (big && !transA && !transB) IHS_BIG(false, false);
     else if (big && transA && !transB) IHS_BIG(true, false);
@@ -416,6 +417,51 @@ void dgemm(bool transA, bool transB, int64_t M, int64_t N, int64_t K, double alp
         const int blocks = (int)std::min<int64_t>(ceil_div(total, 256), 148 * 8);
         LAUNCH_PDL(splitk_reduce_kernel, blocks, 256, 0, st, M, N, splits, work, alpha, beta, C, ldc, (int)lower_only);
     }
+}
+
+// The same product as dgemm(...) on the 128x128 kernel, launched in pieces: phase 0 runs the output block rows
+// covering rows [row0, row1) (row0 a multiple of dgemm_row_block()) without the split-K reduction, phase 1 runs only
+// the reduction. Every tile is computed by the same CTA code over the same K partition whatever the pieces, so
+// pieces + reduction give the bytes of the single call (the sketched Gram accumulated block row by block row as
+// SA's columns arrive). Returns false, doing nothing, when dgemm would not take the 128x128 kernel.
+int64_t dgemm_row_block() { return GBM; }
+bool dgemm_rows(bool transA, bool transB, int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t lda,
+                const double* B, int64_t ldb, double beta, double* C, int64_t ldc, bool lower_only, int splitk,
+                double* d_work, cudaStream_t st, int64_t row0, int64_t row1, int phase) {
+    if (M <= 0 || N <= 0 || K <= 0) return false;
+    if (splitk < 1) splitk = 1;
+    const bool big = dgemm_use_big(transA, transB, M, N, K, lda, ldb, lower_only) && aligned16(A) && aligned16(B) &&
+                     ceil_div(M, GBM) * ceil_div(N, GBN) * std::max(splitk, 1) >= 96;
+    if (!big) return false;
+    int64_t kps = ceil_div(K, splitk);
+    kps = ceil_div(kps, BK) * BK;
+    const int splits = (int)std::max<int64_t>(1, ceil_div(K, kps));
+    double* work = splits > 1 ? d_work : nullptr;
+    if (splits > 1 && !d_work) fail(IHS_INTERNAL_ERROR, "dgemm_rows: split-K without workspace");
+    if (phase == 1) {
+        if (work) {
+            const int64_t total = M * N;
+            const int blocks = (int)std::min<int64_t>(ceil_div(total, 256), 148 * 8);
+            LAUNCH_PDL(splitk_reduce_kernel, blocks, 256, 0, st, M, N, splits, work, alpha, beta, C, ldc,
+                       (int)lower_only);
+        }
+        return true;
+    }
+    if (row0 % GBM != 0 || row1 <= row0 || row1 > M) fail(IHS_INTERNAL_ERROR, "dgemm_rows: bad row window");
+    const int bx0 = (int)(row0 / GBM);
+    dim3 grid((unsigned)(ceil_div(row1, GBM) - bx0), (unsigned)ceil_div(N, GBN), (unsigned)splits);
+#define IHS_BIGW(TA_, TB_)                                                                                      \
+    do {                                                                                                        \
+        IHS_SMEM_ATTR((dgemm_big_kernel<TA_, TB_>), (int)(big_smem<TA_, TB_>()));                               \
+        LAUNCH_PDL((dgemm_big_kernel<TA_, TB_>), grid, GTHREADS, (big_smem<TA_, TB_>()), st, M, N, K, alpha, A, lda, B,\
+                   ldb, beta, C, ldc, kps, work, (int)lower_only, bx0);                                         \
+    } while (0)
+    if (!transA && !transB) IHS_BIGW(false, false);
+    else if (transA && !transB) IHS_BIGW(true, false);
+    else if (!transA && transB) IHS_BIGW(false, true);
+    else IHS_BIGW(true, true);
+#undef IHS_BIGW
+    return true;
 }
 
 }  // namespace ihs_b200

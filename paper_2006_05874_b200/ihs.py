@@ -836,6 +836,11 @@ def thread_upload_doublings() -> int:
     return int(lib().ihs_gpu_thread_upload_doublings())
 
 
+def thread_upload_gram_rows() -> int:
+    """Rows of sketched Gram matrices this thread's solves enqueued behind a chunked upload (diagnostic)."""
+    return int(lib().ihs_gpu_thread_upload_gram_rows())
+
+
 def kernel_launch_count() -> int:
     return int(lib().ihs_gpu_kernel_launch_count())
 

@@ -254,3 +254,26 @@ def test_doublings_sketched_behind_chunked_upload(gpu, m_initial, eps):
     r2 = gpu.adaptive_solve(p, cfg)
     assert np.array_equal(r2.x, r0.x) and r2.counters == r0.counters
     assert gpu.thread_upload_doublings() - before == 2 * 5
+
+
+def test_gram_accumulated_behind_chunked_upload(gpu):
+    """With d >= 256 the sketched Gram SA^T SA of each doubling prepared behind the upload is launched block row by
+    block row (128 rows) as the columns are sketched, on the same tiles and K partition as the single product, and
+    the factorization only reduces it: the solve must still equal the resident one bit for bit. (m = 1024..4096
+    fall back to the whole product - too few tiles for the 128 x 128 kernel - the larger doublings take the pieces.)"""
+    n, d = 1 << 19, 512  # 2 GiB: 8 chunks of 64 columns
+    A, b, _ = gpu.synth_generate(n, d, decay=0.99, noise_std=0.05, data_seed=5)
+    p = gpu.ProblemInstance(A, b, 0.02)
+    cfg = gpu.SolverConfig(sketch_kind=gpu.SketchKind.SRHT, seed=7, m_initial=1024, eps=1e-21)
+    r0 = gpu.adaptive_solve(p, cfg)
+    rows0, dbl0 = gpu.thread_upload_gram_rows(), gpu.thread_upload_doublings()
+    for _ in range(2):
+        p.upload_async(A, b)
+        r1 = gpu.adaptive_solve(p, cfg)
+        assert np.array_equal(r1.x, r0.x)
+        assert (r1.iterations, r1.rejections, r1.final_m) == (r0.iterations, r0.rejections, r0.final_m)
+        assert [(e.t, e.m, e.r, e.branch) for e in r1.log] == [(e.t, e.m, e.r, e.branch) for e in r0.log]
+        assert r1.counters == r0.counters
+    assert gpu.thread_upload_doublings() - dbl0 == 10
+    rows = gpu.thread_upload_gram_rows() - rows0
+    assert rows > 0 and rows % (2 * d) == 0  # whole Gram matrices of some doublings, both rounds
