@@ -256,12 +256,13 @@ def test_doublings_sketched_behind_chunked_upload(gpu, m_initial, eps):
     assert gpu.thread_upload_doublings() - before == 2 * 5
 
 
-def test_gram_accumulated_behind_chunked_upload(gpu):
+@pytest.mark.parametrize("d", [512, 300])
+def test_gram_accumulated_behind_chunked_upload(gpu, d):
     """With d >= 256 the sketched Gram SA^T SA of each doubling prepared behind the upload is launched block row by
     block row (128 rows) as the columns are sketched, on the same tiles and K partition as the single product, and
     the factorization only reduces it: the solve must still equal the resident one bit for bit. (m = 1024..4096
     fall back to the whole product - too few tiles for the 128 x 128 kernel - the larger doublings take the pieces.)"""
-    n, d = 1 << 19, 512  # 2 GiB: 8 chunks of 64 columns
+    n = 1 << 19  # d = 512: 2 GiB in 8 chunks of 64 columns; d = 300: chunks of 38 columns, a ragged last block row
     A, b, _ = gpu.synth_generate(n, d, decay=0.99, noise_std=0.05, data_seed=5)
     p = gpu.ProblemInstance(A, b, 0.02)
     cfg = gpu.SolverConfig(sketch_kind=gpu.SketchKind.SRHT, seed=7, m_initial=1024, eps=1e-21)
