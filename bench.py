@@ -505,8 +505,9 @@ def main():
         # the end-to-end solve must return what the device-timed one did (same data re-uploaded, same trail)
         same_x = bool(args.solver != "ihs" or np.array_equal(np.asarray(rep_e.x), np.asarray(reps[-1].x)))
         e2e = {"value": v, "unit": "s", "h2d_bytes_per_step": 8 * rows * d + 8 * rows, "d2h_bytes_per_step": 8 * d,
-               "timer": "host wall clock around upload_async+solve (includes the H2D copies; the sketches of the "
-                        "first system and the next doublings, and their Gram products, run chunk by chunk behind them)", "x_matches_timed_solve": same_x}
+               "timer": "host wall clock around upload_async+solve (includes the H2D copies; work that does not "
+                        "depend on the iterates runs chunk by chunk behind them: the SRHT sketches of the first "
+                        "system and the next doublings with their Gram products, or the Gaussian S*A)", "x_matches_timed_solve": same_x}
 
     # ---- roofline of the dominant kernel (live, from CUDA-event phase timers on the library's stream: the
     # sketch kernels (SRHT transform / S*A GEMM) and the fused gradient kernels are bracketed by events) of an

@@ -197,6 +197,10 @@ int64_t dgemm_row_block();
 bool dgemm_rows(bool transA, bool transB, int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t lda,
                 const double* B, int64_t ldb, double beta, double* C, int64_t ldc, bool lower_only, int splitk,
                 double* d_work, cudaStream_t st, int64_t row0, int64_t row1, int phase);
+int64_t dgemm_col_block();
+bool dgemm_cols(bool transA, bool transB, int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t lda,
+                const double* B, int64_t ldb, double beta, double* C, int64_t ldc, int splitk, double* d_work,
+                cudaStream_t st, int64_t col0, int64_t col1, int phase);
 int dgemm_pick_splitk(int64_t M, int64_t N, int64_t K, int num_sms, bool transA = false, bool transB = false,
                       bool lower_only = false);
 

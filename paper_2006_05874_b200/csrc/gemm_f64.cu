@@ -171,13 +171,13 @@ template <bool TA, bool TB>
 __global__ void __launch_bounds__(GTHREADS, 1)
 dgemm_big_kernel(int64_t M, int64_t N, int64_t K, double alpha, const double* __restrict__ A, int64_t lda,
                  const double* __restrict__ B, int64_t ldb, double beta, double* __restrict__ C, int64_t ldc,
-                 int64_t k_per_split, double* __restrict__ work, int lower_only, int bx0) {
+                 int64_t k_per_split, double* __restrict__ work, int lower_only, int bx0, int by0) {
     constexpr bool KA = !TA;  // A staged k-major ([k][m])
     constexpr bool KB = TB;   // B staged k-major ([k][n])
     constexpr int SA_D = KA ? GBK * GLA : GBM * GLB;
     constexpr int SB_D = KB ? GBK * GLA : GBN * GLB;
     // bx0: first block row of this launch (a product launched in block-row pieces, dgemm_rows)
-    const int64_t m0 = ((int64_t)blockIdx.x + bx0) * GBM, n0 = (int64_t)blockIdx.y * GBN;
+    const int64_t m0 = ((int64_t)blockIdx.x + bx0) * GBM, n0 = ((int64_t)blockIdx.y + by0) * GBN;
     if (lower_only && n0 > m0 + GBM - 1) return;
     pdl_wait();  // programmatic dependent launch: the previous kernel's results are visible after this
     extern __shared__ double gsm[];
@@ -393,7 +393,7 @@ void dgemm(bool transA, bool transB, int64_t M, int64_t N, int64_t K, double alp
     do {                                                                                                        \
         IHS_SMEM_ATTR((dgemm_big_kernel<TA_, TB_>), (int)(big_smem<TA_, TB_>()));                               \
         LAUNCH_PDL((dgemm_big_kernel<TA_, TB_>), grid, GTHREADS, (big_smem<TA_, TB_>()), st, M, N, K, alpha, A, lda, B,\
-                   ldb, beta, C, ldc, kps, work, (int)lower_only, 0);                                           \
+                   ldb, beta, C, ldc, kps, work, (int)lower_only, 0, 0);                                        \
     } while (0)
     if (big && !transA && !transB) IHS_BIG(false, false);
     else if (big && transA && !transB) IHS_BIG(true, false);
@@ -425,9 +425,10 @@ void dgemm(bool transA, bool transB, int64_t M, int64_t N, int64_t K, double alp
 // pieces + reduction give the bytes of the single call (the sketched Gram accumulated block row by block row as
 // SA's columns arrive). Returns false, doing nothing, when dgemm would not take the 128x128 kernel.
 int64_t dgemm_row_block() { return GBM; }
-bool dgemm_rows(bool transA, bool transB, int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t lda,
-                const double* B, int64_t ldb, double beta, double* C, int64_t ldc, bool lower_only, int splitk,
-                double* d_work, cudaStream_t st, int64_t row0, int64_t row1, int phase) {
+static bool dgemm_window(bool transA, bool transB, int64_t M, int64_t N, int64_t K, double alpha, const double* A,
+                         int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc, bool lower_only,
+                         int splitk, double* d_work, cudaStream_t st, int64_t row0, int64_t row1, int64_t col0,
+                         int64_t col1, int phase) {
     if (M <= 0 || N <= 0 || K <= 0) return false;
     if (splitk < 1) splitk = 1;
     const bool big = dgemm_use_big(transA, transB, M, N, K, lda, ldb, lower_only) && aligned16(A) && aligned16(B) &&
@@ -447,14 +448,15 @@ bool dgemm_rows(bool transA, bool transB, int64_t M, int64_t N, int64_t K, doubl
         }
         return true;
     }
-    if (row0 % GBM != 0 || row1 <= row0 || row1 > M) fail(IHS_INTERNAL_ERROR, "dgemm_rows: bad row window");
-    const int bx0 = (int)(row0 / GBM);
-    dim3 grid((unsigned)(ceil_div(row1, GBM) - bx0), (unsigned)ceil_div(N, GBN), (unsigned)splits);
+    if (row0 % GBM != 0 || row1 <= row0 || row1 > M || col0 % GBN != 0 || col1 <= col0 || col1 > N)
+        fail(IHS_INTERNAL_ERROR, "dgemm window: bad tile window");
+    const int bx0 = (int)(row0 / GBM), by0 = (int)(col0 / GBN);
+    dim3 grid((unsigned)(ceil_div(row1, GBM) - bx0), (unsigned)(ceil_div(col1, GBN) - by0), (unsigned)splits);
 #define IHS_BIGW(TA_, TB_)                                                                                      \
     do {                                                                                                        \
         IHS_SMEM_ATTR((dgemm_big_kernel<TA_, TB_>), (int)(big_smem<TA_, TB_>()));                               \
         LAUNCH_PDL((dgemm_big_kernel<TA_, TB_>), grid, GTHREADS, (big_smem<TA_, TB_>()), st, M, N, K, alpha, A, lda, B,\
-                   ldb, beta, C, ldc, kps, work, (int)lower_only, bx0);                                         \
+                   ldb, beta, C, ldc, kps, work, (int)lower_only, bx0, by0);                                    \
     } while (0)
     if (!transA && !transB) IHS_BIGW(false, false);
     else if (transA && !transB) IHS_BIGW(true, false);
@@ -462,6 +464,22 @@ bool dgemm_rows(bool transA, bool transB, int64_t M, int64_t N, int64_t K, doubl
     else IHS_BIGW(true, true);
 #undef IHS_BIGW
     return true;
+}
+
+bool dgemm_rows(bool transA, bool transB, int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t lda,
+                const double* B, int64_t ldb, double beta, double* C, int64_t ldc, bool lower_only, int splitk,
+                double* d_work, cudaStream_t st, int64_t row0, int64_t row1, int phase) {
+    return dgemm_window(transA, transB, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, lower_only, splitk, d_work, st,
+                        row0, row1, 0, N, phase);
+}
+// ... and in block-column pieces (columns [col0, col1), col0 a multiple of dgemm_col_block()): S*A over the columns
+// of an A that is still arriving
+int64_t dgemm_col_block() { return GBN; }
+bool dgemm_cols(bool transA, bool transB, int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t lda,
+                const double* B, int64_t ldb, double beta, double* C, int64_t ldc, int splitk, double* d_work,
+                cudaStream_t st, int64_t col0, int64_t col1, int phase) {
+    return dgemm_window(transA, transB, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, false, splitk, d_work, st, 0, M,
+                        col0, col1, phase);
 }
 
 }  // namespace ihs_b200

@@ -278,3 +278,22 @@ def test_gram_accumulated_behind_chunked_upload(gpu, d):
     assert gpu.thread_upload_doublings() - dbl0 == 10
     rows = gpu.thread_upload_gram_rows() - rows0
     assert rows > 0 and rows % (2 * d) == 0  # whole Gram matrices of some doublings, both rounds
+
+
+@pytest.mark.parametrize("d", [640, 200])
+def test_gaussian_product_behind_chunked_upload(gpu, d):
+    """A Gaussian-sketch solve started behind a chunked upload launches S*A in block-column pieces (128 columns,
+    the tiles and K partition of the single call) as A's chunks land and reduces them at the end: bit-identical to
+    the solve on a resident A (d = 640: pieces every 128 columns over chunks of 80; d = 200: chunks of 25)."""
+    n = (1 << 16) + 3 if d == 640 else (1 << 18) + 1  # 335 MB / 419 MB
+    A, b, _ = gpu.synth_generate(n, d, decay=0.98, noise_std=0.01, data_seed=2)
+    p = gpu.ProblemInstance(A, b, 1e-3)
+    cfg = gpu.SolverConfig(sketch_kind=gpu.SketchKind.Gaussian, seed=1, rho=0.35, m_initial=1024, max_sketch=1024,
+                           enforce_validity=False, eps=1e-18)
+    r0 = gpu.adaptive_solve(p, cfg)
+    for _ in range(2):
+        p.upload_async(A, b)
+        r1 = gpu.adaptive_solve(p, cfg)
+        assert np.array_equal(r1.x, r0.x)
+        assert (r1.iterations, r1.rejections, r1.final_m) == (r0.iterations, r0.rejections, r0.final_m)
+        assert r1.counters == r0.counters
